@@ -1,0 +1,650 @@
+/*
+ * mnmt_oracle.c — plain, slow, obviously-correct CPU oracle for batched greedy
+ * decoding of a distilled Transformer / AAN student with int8 products
+ * (arXiv 1805.12096, "Marian: Cost-effective High-Quality Neural Machine
+ * Translation in C++", WNMT 2018).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.  The
+ * product path (paper_1805_12096_b200/, libmnmt) never links, imports or calls
+ * it, and it shares no code, header, table or constant generator with it.
+ *
+ * Citations: P:L<n> = /root/reference/PAPER.md line n; "R<k>" = the reading
+ * numbered k in DESIGN.md section "Readings of the paper".
+ *
+ * Numeric contract (R1-R6, R20):
+ *   - activations are stored in fp32 (Marian tensors);
+ *   - every product with a parameter is int8 x int8 -> exact int32 (P:L94,
+ *     P:L100; R3), dequantized as fmaf((float)acc, s, b) (R5);
+ *   - LayerNorm / attention / softmax / sigmoid accumulate in fp64 and round
+ *     once to fp32 (R20);
+ *   - elementwise adds/multiplies/divides are single fp32 operations
+ *     (compile with -ffp-contract=off so nothing is fused).
+ *
+ * Parity pins: tests/test_oracle_pins.py.  Functions with no independent pin
+ * would be marked "parity unpinned" here; see the per-function notes.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORC_MAX_LAYERS 16
+
+/* ---------------------------------------------------------------- config */
+typedef struct {
+    int32_t d_model, d_ffn, n_heads, enc_layers, dec_layers, vocab;
+    int32_t decoder;        /* 0 = self-attention + KV cache, 1 = AAN */
+    int32_t aan_ffn_depth;  /* 0 (= "-ffn"), 1, 2 (R9) */
+    int32_t aan_gate;       /* 1 or 0 (= "-gate") */
+    int32_t out_bias;       /* 1 or 0 (R14) */
+    int32_t eos_id;         /* R16 */
+    float clip;             /* c = 2 */
+    float ln_eps;           /* R10 */
+} orc_cfg;
+
+typedef struct { float *W, *b; int8_t *qW; int out, in; } orc_lin;
+typedef struct { float *g, *b; } orc_ln;
+typedef struct { orc_lin q, k, v, o, f1, f2; orc_ln ln1, ln2; } orc_enc_layer;
+typedef struct {
+    orc_lin a1, a2, gi, gf;          /* AAN FFN and gates (R8, R9) */
+    orc_lin q, k, v, o;              /* decoder self-attention */
+    orc_lin sq, sk, sv, so;          /* source attention */
+    orc_lin f1, f2;                  /* FFN */
+    orc_ln ln1, ln2, ln3;
+} orc_dec_layer;
+
+typedef struct {
+    orc_cfg c;
+    float *E, *out_b;                /* tied embedding [V x d] */
+    int8_t *qE;
+    orc_enc_layer enc[ORC_MAX_LAYERS];
+    orc_dec_layer dec[ORC_MAX_LAYERS];
+    int quantized;
+} orc_model;
+
+/* ------------------------------------------------------------- scalars */
+/* sigma = 127/c, s = c^2/127^2 ("scaled linearly to [-127,127]"; R2). */
+float orc_sigma(float clip) { return 127.0f / clip; }
+float orc_dequant_scale(float clip) {
+    return (float)(((double)clip * (double)clip) / (127.0 * 127.0));
+}
+
+/* Q(x) = RNE(clip(x, +-c) * sigma) ("clipped to a range ... scaled
+ * linearly to [-127,127] and rounded to integers"; rounding mode R1). */
+int8_t orc_q(float x, float clip) {
+    float v = x;
+    if (v > clip) v = clip;
+    if (v < -clip) v = -clip;
+    float y = v * orc_sigma(clip);
+    return (int8_t)nearbyintf(y);   /* FE_TONEAREST: ties to even */
+}
+
+void orc_quantize(const float *x, int64_t n, float clip, int8_t *out) {
+    for (int64_t i = 0; i < n; ++i) out[i] = orc_q(x[i], clip);
+}
+
+/* dotint(quant(A), quant(B^T)) = A . B^T with int32 accumulation (
+ * exact s32 accumulation R3).  acc[i][j] = sum_k a[i][k] * w[j][k]. */
+void orc_gemm_acc(const int8_t *a, const int8_t *w, int M, int N, int K, int32_t *acc) {
+    for (int i = 0; i < M; ++i)
+        for (int j = 0; j < N; ++j) {
+            int32_t s = 0;
+            const int8_t *ar = a + (int64_t)i * K, *wr = w + (int64_t)j * K;
+            for (int k = 0; k < K; ++k) s += (int32_t)ar[k] * (int32_t)wr[k];
+            acc[(int64_t)i * N + j] = s;
+        }
+}
+
+/* lin(qa; W, b)[j] = fmaf((float)acc_j, s, b_j)  (R5). b may be NULL (= 0). */
+static void lin1(const orc_lin *L, const int8_t *qa, float s, float *out) {
+    for (int j = 0; j < L->out; ++j) {
+        int32_t acc = 0;
+        const int8_t *wr = L->qW + (int64_t)j * L->in;
+        for (int k = 0; k < L->in; ++k) acc += (int32_t)qa[k] * (int32_t)wr[k];
+        out[j] = fmaf((float)acc, s, L->b ? L->b[j] : 0.0f);
+    }
+}
+
+/* LayerNorm, post-norm (P:L65 Vaswani recipe; R10), fp64 accumulation (R20):
+ * mu = sum r / d; var = sum (r-mu)^2 / d; out = (r-mu)/sqrt(var+eps)*g + b. */
+void orc_layernorm(const float *r, int d, const float *g, const float *b, float eps, float *out) {
+    double mu = 0.0, var = 0.0;
+    for (int k = 0; k < d; ++k) mu += (double)r[k];
+    mu /= (double)d;
+    for (int k = 0; k < d; ++k) { double t = (double)r[k] - mu; var += t * t; }
+    var /= (double)d;
+    double inv = 1.0 / sqrt(var + (double)eps);
+    for (int k = 0; k < d; ++k)
+        out[k] = (float)((((double)r[k] - mu) * inv) * (double)g[k] + (double)b[k]);
+}
+
+/* Scaled dot-product attention of one query row over n key/value rows
+ * (Vaswani et al.).  Head h uses columns [h*dh, (h+1)*dh) (R11).
+ * fp64 accumulation, one rounding to fp32 per context element (R20).
+ * k, v: row j at k + j*ld. */
+void orc_attention(const float *q, const float *k, const float *v, int64_t ld, int n,
+                   int d, int H, float *ctx) {
+    int dh = d / H;
+    double inv_sqrt = 1.0 / sqrt((double)dh);
+    double *sc = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    for (int h = 0; h < H; ++h) {
+        double mx = -INFINITY;
+        for (int j = 0; j < n; ++j) {
+            double dot = 0.0;
+            for (int c = 0; c < dh; ++c)
+                dot += (double)q[h * dh + c] * (double)k[(int64_t)j * ld + h * dh + c];
+            sc[j] = dot * inv_sqrt;
+            if (sc[j] > mx) mx = sc[j];
+        }
+        double Z = 0.0;
+        for (int j = 0; j < n; ++j) { sc[j] = exp(sc[j] - mx); Z += sc[j]; }
+        for (int c = 0; c < dh; ++c) {
+            double acc = 0.0;
+            for (int j = 0; j < n; ++j) acc += sc[j] * (double)v[(int64_t)j * ld + h * dh + c];
+            ctx[h * dh + c] = (float)(acc / Z);
+        }
+    }
+    free(sc);
+}
+
+/* AAN cumulative average, incremental form ("cumulative uniform
+ * averaging ... computed based on the single last step"): the state is the
+ * running sum C (R6); C <- fl(C + y); g = fl(C / t), t = 1, 2, ... (R7). */
+void orc_aan_step(float *C, const float *y, int t, int d, float *g) {
+    for (int k = 0; k < d; ++k) {
+        C[k] = C[k] + y[k];
+        g[k] = C[k] / (float)t;
+    }
+}
+
+/* sigma(x) = 1/(1+exp(-x)), fp64 then rounded (R20). */
+float orc_sigmoid(float x) { return (float)(1.0 / (1.0 + exp(-(double)x))); }
+
+/* Sinusoidal position encoding (P:L65 Vaswani recipe; R12):
+ * PE[pos][2i] = sin(pos / 10000^(2i/d)), PE[pos][2i+1] = cos(same). */
+void orc_pe(int pos, int d, float *out) {
+    for (int i = 0; 2 * i < d; ++i) {
+        double ang = (double)pos / pow(10000.0, (double)(2 * i) / (double)d);
+        out[2 * i] = (float)sin(ang);
+        if (2 * i + 1 < d) out[2 * i + 1] = (float)cos(ang);
+    }
+}
+
+/* emb(id, pos) = fl(fl(E[id] * fl32(sqrt d)) + PE[pos]); id < 0 = zero vector
+ * (the start symbol, R13).  Tied embedding E. */
+static void embed(const orc_model *m, int id, int pos, float *out, float *pe_tmp) {
+    int d = m->c.d_model;
+    float r = (float)sqrt((double)d);
+    orc_pe(pos, d, pe_tmp);
+    for (int k = 0; k < d; ++k) {
+        float e = id >= 0 ? m->E[(int64_t)id * d + k] * r : 0.0f;
+        out[k] = e + pe_tmp[k];
+    }
+}
+
+/* ----------------------------------------------------- model assembly */
+static int cfg_ok(const orc_cfg *c) {
+    if (c->d_model <= 0 || c->d_ffn <= 0 || c->n_heads <= 0 || c->vocab <= 0) return 0;
+    if (c->d_model % c->n_heads) return 0;
+    if (c->enc_layers < 0 || c->dec_layers < 1) return 0;
+    if (c->enc_layers > ORC_MAX_LAYERS || c->dec_layers > ORC_MAX_LAYERS) return 0;
+    if (c->decoder != 0 && c->decoder != 1) return 0;
+    if (c->aan_ffn_depth < 0 || c->aan_ffn_depth > 2) return 0;
+    if (!(c->clip > 0.0f)) return 0;
+    if (c->eos_id < 0 || c->eos_id >= c->vocab) return 0;
+    return 1;
+}
+
+orc_model *orc_model_new(const orc_cfg *c) {
+    if (!cfg_ok(c)) return NULL;
+    orc_model *m = (orc_model *)calloc(1, sizeof(orc_model));
+    m->c = *c;
+    return m;
+}
+
+static void free_lin(orc_lin *l) { free(l->W); free(l->b); free(l->qW); }
+static void free_ln(orc_ln *l) { free(l->g); free(l->b); }
+
+void orc_model_free(orc_model *m) {
+    if (!m) return;
+    free(m->E); free(m->out_b); free(m->qE);
+    for (int l = 0; l < ORC_MAX_LAYERS; ++l) {
+        orc_enc_layer *e = &m->enc[l];
+        free_lin(&e->q); free_lin(&e->k); free_lin(&e->v); free_lin(&e->o);
+        free_lin(&e->f1); free_lin(&e->f2); free_ln(&e->ln1); free_ln(&e->ln2);
+        orc_dec_layer *D = &m->dec[l];
+        free_lin(&D->a1); free_lin(&D->a2); free_lin(&D->gi); free_lin(&D->gf);
+        free_lin(&D->q); free_lin(&D->k); free_lin(&D->v); free_lin(&D->o);
+        free_lin(&D->sq); free_lin(&D->sk); free_lin(&D->sv); free_lin(&D->so);
+        free_lin(&D->f1); free_lin(&D->f2);
+        free_ln(&D->ln1); free_ln(&D->ln2); free_ln(&D->ln3);
+    }
+    free(m);
+}
+
+static float *dup(const float *p, int64_t n) {
+    float *q = (float *)malloc(sizeof(float) * (size_t)n);
+    memcpy(q, p, sizeof(float) * (size_t)n);
+    return q;
+}
+
+/* Resolve a manifest name to its slot.  Returns element count expected, or -1. */
+static int64_t slot(orc_model *m, const char *name, float ***dst, orc_lin **lin_out) {
+    const orc_cfg *c = &m->c;
+    int d = c->d_model, F = c->d_ffn;
+    *lin_out = NULL;
+    if (!strcmp(name, "emb.E")) { *dst = &m->E; return (int64_t)c->vocab * d; }
+    if (!strcmp(name, "out.b")) { if (!c->out_bias) return -1; *dst = &m->out_b; return c->vocab; }
+    int l = -1, n = 0;
+    char rest[64];
+    if (sscanf(name, "enc.%d.%63s%n", &l, rest, &n) == 2 && l >= 0 && l < c->enc_layers) {
+        orc_enc_layer *e = &m->enc[l];
+        struct { const char *nm; orc_lin *L; int out, in; } lt[] = {
+            {"self.q", &e->q, d, d}, {"self.k", &e->k, d, d}, {"self.v", &e->v, d, d},
+            {"self.o", &e->o, d, d}, {"ffn.1", &e->f1, F, d}, {"ffn.2", &e->f2, d, F}};
+        for (size_t i = 0; i < sizeof(lt) / sizeof(lt[0]); ++i) {
+            size_t ln = strlen(lt[i].nm);
+            if (!strncmp(rest, lt[i].nm, ln) && rest[ln] == '.') {
+                lt[i].L->out = lt[i].out; lt[i].L->in = lt[i].in; *lin_out = lt[i].L;
+                if (!strcmp(rest + ln, ".W")) { *dst = &lt[i].L->W; return (int64_t)lt[i].out * lt[i].in; }
+                if (!strcmp(rest + ln, ".b")) { *dst = &lt[i].L->b; return lt[i].out; }
+                return -1;
+            }
+        }
+        if (!strcmp(rest, "ln1.g")) { *dst = &e->ln1.g; return d; }
+        if (!strcmp(rest, "ln1.b")) { *dst = &e->ln1.b; return d; }
+        if (!strcmp(rest, "ln2.g")) { *dst = &e->ln2.g; return d; }
+        if (!strcmp(rest, "ln2.b")) { *dst = &e->ln2.b; return d; }
+        return -1;
+    }
+    if (sscanf(name, "dec.%d.%63s%n", &l, rest, &n) == 2 && l >= 0 && l < c->dec_layers) {
+        orc_dec_layer *D = &m->dec[l];
+        int aan = c->decoder == 1;
+        struct { const char *nm; orc_lin *L; int out, in; int present; } lt[] = {
+            {"aan.ffn.1", &D->a1, d, d, aan && c->aan_ffn_depth >= 1},
+            {"aan.ffn.2", &D->a2, d, d, aan && c->aan_ffn_depth >= 2},
+            {"aan.gate.i", &D->gi, d, d, aan && c->aan_gate},
+            {"aan.gate.f", &D->gf, d, d, aan && c->aan_gate},
+            {"self.q", &D->q, d, d, !aan}, {"self.k", &D->k, d, d, !aan},
+            {"self.v", &D->v, d, d, !aan}, {"self.o", &D->o, d, d, !aan},
+            {"src.q", &D->sq, d, d, 1}, {"src.k", &D->sk, d, d, 1},
+            {"src.v", &D->sv, d, d, 1}, {"src.o", &D->so, d, d, 1},
+            {"ffn.1", &D->f1, F, d, 1}, {"ffn.2", &D->f2, d, F, 1}};
+        for (size_t i = 0; i < sizeof(lt) / sizeof(lt[0]); ++i) {
+            size_t ln = strlen(lt[i].nm);
+            if (!strncmp(rest, lt[i].nm, ln) && rest[ln] == '.' &&
+                (!strcmp(rest + ln, ".W") || !strcmp(rest + ln, ".b"))) {
+                if (!lt[i].present) return -1;
+                lt[i].L->out = lt[i].out; lt[i].L->in = lt[i].in; *lin_out = lt[i].L;
+                if (rest[ln + 1] == 'W') { *dst = &lt[i].L->W; return (int64_t)lt[i].out * lt[i].in; }
+                *dst = &lt[i].L->b; return lt[i].out;
+            }
+        }
+        orc_ln *lns[3] = {&D->ln1, &D->ln2, &D->ln3};
+        for (int i = 0; i < 3; ++i) {
+            char nm[16];
+            snprintf(nm, sizeof nm, "ln%d.g", i + 1);
+            if (!strcmp(rest, nm)) { *dst = &lns[i]->g; return d; }
+            snprintf(nm, sizeof nm, "ln%d.b", i + 1);
+            if (!strcmp(rest, nm)) { *dst = &lns[i]->b; return d; }
+        }
+    }
+    return -1;
+}
+
+/* 0 ok, 2 = unknown name or wrong numel, 4 = after quantize. */
+int orc_model_set(orc_model *m, const char *name, const float *data, int64_t numel) {
+    if (m->quantized) return 4;
+    float **dst = NULL; orc_lin *L = NULL;
+    int64_t want = slot(m, name, &dst, &L);
+    if (want < 0 || want != numel) return 2;
+    free(*dst);
+    *dst = dup(data, numel);
+    return 0;
+}
+
+static int lin_ready(const orc_lin *l) { return l->W && l->b; }
+
+/* One-time quantization of every parameter matrix: the memoized
+ * quant(B^T) of P:L100-105.  Returns 0, or 4 if any parameter is missing. */
+int orc_model_quantize(orc_model *m) {
+    const orc_cfg *c = &m->c;
+    float clip = c->clip;
+    if (!m->E || (c->out_bias && !m->out_b)) return 4;
+    for (int l = 0; l < c->enc_layers; ++l) {
+        orc_enc_layer *e = &m->enc[l];
+        orc_lin *ls[6] = {&e->q, &e->k, &e->v, &e->o, &e->f1, &e->f2};
+        for (int i = 0; i < 6; ++i) if (!lin_ready(ls[i])) return 4;
+        if (!e->ln1.g || !e->ln1.b || !e->ln2.g || !e->ln2.b) return 4;
+    }
+    for (int l = 0; l < c->dec_layers; ++l) {
+        orc_dec_layer *D = &m->dec[l];
+        if (c->decoder == 1) {
+            if (c->aan_ffn_depth >= 1 && !lin_ready(&D->a1)) return 4;
+            if (c->aan_ffn_depth >= 2 && !lin_ready(&D->a2)) return 4;
+            if (c->aan_gate && (!lin_ready(&D->gi) || !lin_ready(&D->gf))) return 4;
+        } else {
+            if (!lin_ready(&D->q) || !lin_ready(&D->k) || !lin_ready(&D->v) || !lin_ready(&D->o)) return 4;
+        }
+        orc_lin *ls[6] = {&D->sq, &D->sk, &D->sv, &D->so, &D->f1, &D->f2};
+        for (int i = 0; i < 6; ++i) if (!lin_ready(ls[i])) return 4;
+        if (!D->ln1.g || !D->ln1.b || !D->ln2.g || !D->ln2.b || !D->ln3.g || !D->ln3.b) return 4;
+    }
+    int64_t nE = (int64_t)c->vocab * c->d_model;
+    m->qE = (int8_t *)malloc((size_t)nE);
+    orc_quantize(m->E, nE, clip, m->qE);
+#define QL(L) do { if ((L).W) { int64_t n_ = (int64_t)(L).out * (L).in; \
+        (L).qW = (int8_t *)malloc((size_t)n_); orc_quantize((L).W, n_, clip, (L).qW); } } while (0)
+    for (int l = 0; l < c->enc_layers; ++l) {
+        orc_enc_layer *e = &m->enc[l];
+        QL(e->q); QL(e->k); QL(e->v); QL(e->o); QL(e->f1); QL(e->f2);
+    }
+    for (int l = 0; l < c->dec_layers; ++l) {
+        orc_dec_layer *D = &m->dec[l];
+        QL(D->a1); QL(D->a2); QL(D->gi); QL(D->gf);
+        QL(D->q); QL(D->k); QL(D->v); QL(D->o);
+        QL(D->sq); QL(D->sk); QL(D->sv); QL(D->so); QL(D->f1); QL(D->f2);
+    }
+#undef QL
+    m->quantized = 1;
+    return 0;
+}
+
+/* ------------------------------------------------------------ encoder */
+/* Encoder: x = emb(src, 0..S-1); per layer
+ *   qkv = lin(Q(x)); ctx = attn; x = LN1(fl(x + lin(Q(ctx))));
+ *   h = Q(ReLU(lin(Q(x)))); x = LN2(fl(x + lin(h))).
+ * Then the source keys/values of every decoder layer: K_l = lin(Q(x); Wk_l),
+ * V_l = lin(Q(x); Wv_l).  enc_out [S x d] and kv [L][2][S][d] may be NULL. */
+int orc_encode(const orc_model *m, const int32_t *src, int S, float *enc_out, float *kv) {
+    const orc_cfg *c = &m->c;
+    int d = c->d_model, F = c->d_ffn, H = c->n_heads;
+    float clip = c->clip, s = orc_dequant_scale(clip);
+    if (!m->quantized) return 4;
+    for (int i = 0; i < S; ++i) if (src[i] < 0 || src[i] >= c->vocab) return 3;
+    float *x = (float *)malloc(sizeof(float) * (size_t)S * d);
+    float *Q = (float *)malloc(sizeof(float) * (size_t)S * d);
+    float *Kt = (float *)malloc(sizeof(float) * (size_t)S * d);
+    float *Vt = (float *)malloc(sizeof(float) * (size_t)S * d);
+    float *ctx = (float *)malloc(sizeof(float) * d);
+    float *o = (float *)malloc(sizeof(float) * d);
+    float *r = (float *)malloc(sizeof(float) * d);
+    float *h = (float *)malloc(sizeof(float) * F);
+    int8_t *qa = (int8_t *)malloc((size_t)(F > d ? F : d));
+    float *pe = (float *)malloc(sizeof(float) * d);
+    for (int i = 0; i < S; ++i) embed(m, src[i], i, x + (int64_t)i * d, pe);
+    for (int l = 0; l < c->enc_layers; ++l) {
+        const orc_enc_layer *e = &m->enc[l];
+        for (int i = 0; i < S; ++i) {
+            orc_quantize(x + (int64_t)i * d, d, clip, qa);
+            lin1(&e->q, qa, s, Q + (int64_t)i * d);
+            lin1(&e->k, qa, s, Kt + (int64_t)i * d);
+            lin1(&e->v, qa, s, Vt + (int64_t)i * d);
+        }
+        for (int i = 0; i < S; ++i) {
+            float *xi = x + (int64_t)i * d;
+            orc_attention(Q + (int64_t)i * d, Kt, Vt, d, S, d, H, ctx);
+            orc_quantize(ctx, d, clip, qa);
+            lin1(&e->o, qa, s, o);
+            for (int k = 0; k < d; ++k) r[k] = xi[k] + o[k];
+            orc_layernorm(r, d, e->ln1.g, e->ln1.b, c->ln_eps, xi);
+            orc_quantize(xi, d, clip, qa);
+            lin1(&e->f1, qa, s, h);
+            for (int k = 0; k < F; ++k) qa[k] = orc_q(h[k] > 0.0f ? h[k] : 0.0f, clip);
+            lin1(&e->f2, qa, s, o);
+            for (int k = 0; k < d; ++k) r[k] = xi[k] + o[k];
+            orc_layernorm(r, d, e->ln2.g, e->ln2.b, c->ln_eps, xi);
+        }
+    }
+    if (enc_out) memcpy(enc_out, x, sizeof(float) * (size_t)S * d);
+    if (kv) {
+        for (int l = 0; l < c->dec_layers; ++l) {
+            const orc_dec_layer *D = &m->dec[l];
+            for (int i = 0; i < S; ++i) {
+                orc_quantize(x + (int64_t)i * d, d, clip, qa);
+                lin1(&D->sk, qa, s, kv + (((int64_t)l * 2 + 0) * S + i) * d);
+                lin1(&D->sv, qa, s, kv + (((int64_t)l * 2 + 1) * S + i) * d);
+            }
+        }
+    }
+    free(x); free(Q); free(Kt); free(Vt); free(ctx); free(o); free(r); free(h); free(qa); free(pe);
+    return 0;
+}
+
+/* ------------------------------------------------------------ decoder */
+typedef struct {
+    int32_t *ids;        /* [T] model argmax at each step */
+    int32_t *second;     /* [T] runner-up id */
+    float *margin;       /* [T] top-1 minus top-2 logit (fp32 difference in double) */
+    float *dec_out;      /* [T][d] decoder output of the last layer */
+    float *layer_out;    /* [T][L][3][d] x1, x2, x3 of every layer */
+    int8_t *out_codes;   /* [T][d] Q(dec_out): the output-layer A operand */
+} orc_trace;
+
+/* Greedy decode of ONE sentence (beam 1, softmax skipped, "select the
+ * output word with highest activation").
+ * forced == NULL: free-running; stop at EOS (not emitted) or t == max_len (R16).
+ * forced != NULL: teacher forcing for max_len steps; the input at step t >= 2
+ * is forced[t-2]; every step's argmax is recorded in trace/out_ids.
+ * Returns the number of ids written to out_ids, or <0 on error. */
+int orc_decode_one(const orc_model *m, const int32_t *src, int S, int max_len,
+                   const int32_t *forced, int32_t *out_ids, orc_trace *tr) {
+    const orc_cfg *c = &m->c;
+    int d = c->d_model, F = c->d_ffn, H = c->n_heads, L = c->dec_layers, V = c->vocab;
+    float clip = c->clip, s = orc_dequant_scale(clip);
+    if (!m->quantized) return -4;
+    if (max_len < 0) return -1;
+    for (int i = 0; i < S; ++i) if (src[i] < 0 || src[i] >= V) return -3;
+    if (forced) for (int i = 0; i + 1 < max_len; ++i) if (forced[i] < 0 || forced[i] >= V) return -3;
+    float *kv = (float *)malloc(sizeof(float) * (size_t)L * 2 * (S > 0 ? S : 1) * d);
+    if (S > 0) orc_encode(m, src, S, NULL, kv);
+    float *C = (float *)calloc((size_t)L * d, sizeof(float));       /* AAN state (R6) */
+    int Tcap = max_len > 0 ? max_len : 1;
+    float *Ks = NULL, *Vs = NULL;
+    if (c->decoder == 0) {
+        Ks = (float *)malloc(sizeof(float) * (size_t)L * Tcap * d);
+        Vs = (float *)malloc(sizeof(float) * (size_t)L * Tcap * d);
+    }
+    float *y = (float *)malloc(sizeof(float) * d), *g = (float *)malloc(sizeof(float) * d);
+    float *a = (float *)malloc(sizeof(float) * d), *t1 = (float *)malloc(sizeof(float) * d);
+    float *gi = (float *)malloc(sizeof(float) * d), *gf = (float *)malloc(sizeof(float) * d);
+    float *r = (float *)malloc(sizeof(float) * d), *x1 = (float *)malloc(sizeof(float) * d);
+    float *x2 = (float *)malloc(sizeof(float) * d), *ctx = (float *)malloc(sizeof(float) * d);
+    float *h = (float *)malloc(sizeof(float) * F), *pe = (float *)malloc(sizeof(float) * d);
+    float *qs = (float *)malloc(sizeof(float) * d);
+    int8_t *qa = (int8_t *)malloc((size_t)(F > d ? F : d)), *qy = (int8_t *)malloc((size_t)d);
+    int n_out = 0, prev = -1;
+    for (int t = 1; t <= max_len; ++t) {
+        /* A5: decoder input y = emb(id_{t-1}, t-1); zero embedding at t=1 (R13). */
+        int in_id = t == 1 ? -1 : (forced ? forced[t - 2] : prev);
+        embed(m, in_id, t - 1, y, pe);
+        for (int l = 0; l < L; ++l) {
+            const orc_dec_layer *D = &m->dec[l];
+            if (c->decoder == 1) {
+                /* A6: AAN.  C <- fl(C + y); g = fl(C / t) (R6, R7). */
+                orc_aan_step(C + (int64_t)l * d, y, t, d, g);
+                if (c->aan_ffn_depth == 0) {
+                    memcpy(a, g, sizeof(float) * d);
+                } else {
+                    orc_quantize(g, d, clip, qa);
+                    lin1(&D->a1, qa, s, t1);
+                    if (c->aan_ffn_depth == 1) {
+                        for (int k = 0; k < d; ++k) a[k] = t1[k] > 0.0f ? t1[k] : 0.0f;
+                    } else {
+                        for (int k = 0; k < d; ++k) qa[k] = orc_q(t1[k] > 0.0f ? t1[k] : 0.0f, clip);
+                        lin1(&D->a2, qa, s, a);
+                    }
+                }
+                if (c->aan_gate) {
+                    /* Gate (R8): i = sig(W_i y + b_i), f = sig(W_f a + b_f), z = i*y + f*a. */
+                    orc_quantize(y, d, clip, qy);
+                    lin1(&D->gi, qy, s, gi);
+                    orc_quantize(a, d, clip, qa);
+                    lin1(&D->gf, qa, s, gf);
+                    for (int k = 0; k < d; ++k) {
+                        float iy = orc_sigmoid(gi[k]) * y[k];
+                        float fa = orc_sigmoid(gf[k]) * a[k];
+                        float z = iy + fa;
+                        r[k] = y[k] + z;
+                    }
+                } else {
+                    for (int k = 0; k < d; ++k) r[k] = y[k] + a[k];
+                }
+                orc_layernorm(r, d, D->ln1.g, D->ln1.b, c->ln_eps, x1);
+            } else {
+                /* A6': self-attention over positions 1..t with a KV cache. */
+                float *Kl = Ks + (int64_t)l * Tcap * d, *Vl = Vs + (int64_t)l * Tcap * d;
+                orc_quantize(y, d, clip, qy);
+                lin1(&D->q, qy, s, qs);
+                lin1(&D->k, qy, s, Kl + (int64_t)(t - 1) * d);
+                lin1(&D->v, qy, s, Vl + (int64_t)(t - 1) * d);
+                orc_attention(qs, Kl, Vl, d, t, d, H, ctx);
+                orc_quantize(ctx, d, clip, qa);
+                lin1(&D->o, qa, s, a);
+                for (int k = 0; k < d; ++k) r[k] = y[k] + a[k];
+                orc_layernorm(r, d, D->ln1.g, D->ln1.b, c->ln_eps, x1);
+            }
+            /* A7: source attention. */
+            orc_quantize(x1, d, clip, qa);
+            lin1(&D->sq, qa, s, qs);
+            if (S > 0) {
+                orc_attention(qs, kv + ((int64_t)l * 2 + 0) * S * d, kv + ((int64_t)l * 2 + 1) * S * d,
+                              d, S, d, H, ctx);
+            } else {
+                memset(ctx, 0, sizeof(float) * d);
+            }
+            orc_quantize(ctx, d, clip, qa);
+            lin1(&D->so, qa, s, a);
+            for (int k = 0; k < d; ++k) r[k] = x1[k] + a[k];
+            orc_layernorm(r, d, D->ln2.g, D->ln2.b, c->ln_eps, x2);
+            /* A8: FFN; ReLU output goes straight to int8 codes. */
+            orc_quantize(x2, d, clip, qa);
+            lin1(&D->f1, qa, s, h);
+            for (int k = 0; k < F; ++k) qa[k] = orc_q(h[k] > 0.0f ? h[k] : 0.0f, clip);
+            lin1(&D->f2, qa, s, a);
+            for (int k = 0; k < d; ++k) r[k] = x2[k] + a[k];
+            orc_layernorm(r, d, D->ln3.g, D->ln3.b, c->ln_eps, y);
+            if (tr && tr->layer_out) {
+                float *dst = tr->layer_out + (((int64_t)(t - 1) * L + l) * 3) * d;
+                memcpy(dst, x1, sizeof(float) * d);
+                memcpy(dst + d, x2, sizeof(float) * d);
+                memcpy(dst + 2 * d, y, sizeof(float) * d);
+            }
+        }
+        /* A9: tied output projection + argmax, softmax skipped.
+         * logit_j = fmaf((float)acc_j, s, b_j); lowest j wins ties (R15). */
+        orc_quantize(y, d, clip, qy);
+        int best = -1, second = -1;
+        float bv = 0.0f, sv = 0.0f;
+        for (int j = 0; j < V; ++j) {
+            int32_t acc = 0;
+            const int8_t *er = m->qE + (int64_t)j * d;
+            for (int k = 0; k < d; ++k) acc += (int32_t)qy[k] * (int32_t)er[k];
+            float lg = fmaf((float)acc, s, c->out_bias ? m->out_b[j] : 0.0f);
+            if (best < 0 || lg > bv) { second = best; sv = bv; best = j; bv = lg; }
+            else if (second < 0 || lg > sv) { second = j; sv = lg; }
+        }
+        if (tr) {
+            int i = t - 1;
+            if (tr->ids) tr->ids[i] = best;
+            if (tr->second) tr->second[i] = second;
+            if (tr->margin) tr->margin[i] = second >= 0 ? (float)((double)bv - (double)sv) : INFINITY;
+            if (tr->dec_out) memcpy(tr->dec_out + (int64_t)i * d, y, sizeof(float) * d);
+            if (tr->out_codes) memcpy(tr->out_codes + (int64_t)i * d, qy, (size_t)d);
+        }
+        if (forced) {
+            out_ids[n_out++] = best;
+        } else {
+            /* A10: EOS is not emitted and ends the sentence (R16). */
+            if (best == c->eos_id) break;
+            out_ids[n_out++] = best;
+            prev = best;
+        }
+    }
+    free(kv); free(C); free(Ks); free(Vs); free(y); free(g); free(a); free(t1); free(gi); free(gf);
+    free(r); free(x1); free(x2); free(ctx); free(h); free(pe); free(qs); free(qa); free(qy);
+    return n_out;
+}
+
+/* Decode n independent sentences (rows are independent: static scales,
+ * P:L94), parallel over sentences with OpenMP for timing only.  Sentence i's
+ * ids go to out_ids[out_off[i] ...], out_off = exclusive prefix sum of max_len.
+ * nthreads <= 0: library default.  Returns 0 or a status code. */
+int orc_decode_many(const orc_model *m, const int32_t *src_ids, const int64_t *src_off, int n,
+                    const int32_t *max_len, int32_t *out_ids, int32_t *out_len, int nthreads) {
+    int64_t *oo = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+    oo[0] = 0;
+    for (int i = 0; i < n; ++i) oo[i + 1] = oo[i] + max_len[i];
+    int err = 0;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1)
+#endif
+    for (int i = 0; i < n; ++i) {
+        int r = orc_decode_one(m, src_ids + src_off[i], (int)(src_off[i + 1] - src_off[i]),
+                               max_len[i], NULL, out_ids + oo[i], NULL);
+        if (r < 0) err = -r; else out_len[i] = r;
+    }
+    free(oo);
+    return err;
+}
+
+int orc_max_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+/* ------------------------------------------------------------ batcher */
+/* Length-sorted word-budget batching ("sorted by source length ...
+ * batch based on number of words ... at least 384 words"; R17).
+ * Stable sort ascending by (S_i, i); append sentences while the batch holds
+ * fewer than `budget` words; close it once it holds >= budget words.
+ * Returns 0, or 1 for budget < 1 / n < 0. */
+int orc_batch_by_words(const int32_t *len, int n, int budget, int32_t *order, int32_t *off,
+                       int32_t *n_batches) {
+    if (budget < 1 || n < 0) return 1;
+    for (int i = 0; i < n; ++i) order[i] = i;
+    /* insertion sort: obviously stable */
+    for (int i = 1; i < n; ++i) {
+        int32_t v = order[i];
+        int j = i - 1;
+        while (j >= 0 && len[order[j]] > len[v]) { order[j + 1] = order[j]; --j; }
+        order[j + 1] = v;
+    }
+    int nb = 0;
+    int64_t words = 0;
+    off[0] = 0;
+    for (int i = 0; i < n; ++i) {
+        words += len[order[i]];
+        if (words >= budget) { off[++nb] = i + 1; words = 0; }
+    }
+    if (n > 0 && off[nb] != n) off[++nb] = n;
+    *n_batches = nb;
+    return 0;
+}
+
+/* ---------------------------------------------------- size arithmetic */
+/* Parameter count of a Table-1 student: tied embedding V*d
+ * (P:L31), 6+6 layers, biases, LayerNorm gain/bias, output bias. */
+int64_t orc_param_count(const orc_cfg *c) {
+    int64_t d = c->d_model, F = c->d_ffn, V = c->vocab;
+    int64_t lin_dd = d * d + d;
+    int64_t ffn = (F * d + F) + (d * F + d);
+    int64_t enc = 4 * lin_dd + ffn + 2 * 2 * d;
+    int64_t self_blk;
+    if (c->decoder == 1)
+        self_blk = (c->aan_ffn_depth >= 1 ? lin_dd : 0) + (c->aan_ffn_depth >= 2 ? lin_dd : 0) +
+                   (c->aan_gate ? 2 * lin_dd : 0);
+    else
+        self_blk = 4 * lin_dd;
+    int64_t dec = self_blk + 4 * lin_dd + ffn + 3 * 2 * d;
+    return V * d + c->enc_layers * enc + c->dec_layers * dec + (c->out_bias ? V : 0);
+}

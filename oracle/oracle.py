@@ -1,0 +1,261 @@
+"""ctypes wrapper of liboracle.so (TEST INFRASTRUCTURE ONLY — see __init__.py).
+
+Argument marshalling only; every computation is in mnmt_oracle.c.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from typing import Dict, Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "mnmt_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared", "-std=c11"]
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (plain gcc; no CUDA)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class Cfg(C.Structure):
+    _fields_ = [("d_model", C.c_int32), ("d_ffn", C.c_int32), ("n_heads", C.c_int32),
+                ("enc_layers", C.c_int32), ("dec_layers", C.c_int32), ("vocab", C.c_int32),
+                ("decoder", C.c_int32), ("aan_ffn_depth", C.c_int32), ("aan_gate", C.c_int32),
+                ("out_bias", C.c_int32), ("eos_id", C.c_int32), ("clip", C.c_float),
+                ("ln_eps", C.c_float)]
+
+
+class Trace(C.Structure):
+    _fields_ = [("ids", C.c_void_p), ("second", C.c_void_p), ("margin", C.c_void_p),
+                ("dec_out", C.c_void_p), ("layer_out", C.c_void_p), ("out_codes", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        L = _lib
+        P = C.c_void_p
+        L.orc_sigma.restype = C.c_float; L.orc_sigma.argtypes = [C.c_float]
+        L.orc_dequant_scale.restype = C.c_float; L.orc_dequant_scale.argtypes = [C.c_float]
+        L.orc_q.restype = C.c_int8; L.orc_q.argtypes = [C.c_float, C.c_float]
+        L.orc_quantize.argtypes = [P, C.c_int64, C.c_float, P]
+        L.orc_gemm_acc.argtypes = [P, P, C.c_int, C.c_int, C.c_int, P]
+        L.orc_layernorm.argtypes = [P, C.c_int, P, P, C.c_float, P]
+        L.orc_attention.argtypes = [P, P, P, C.c_int64, C.c_int, C.c_int, C.c_int, P]
+        L.orc_sigmoid.restype = C.c_float; L.orc_sigmoid.argtypes = [C.c_float]
+        L.orc_pe.argtypes = [C.c_int, C.c_int, P]
+        L.orc_aan_step.argtypes = [P, P, C.c_int, C.c_int, P]
+        L.orc_model_new.restype = P; L.orc_model_new.argtypes = [C.POINTER(Cfg)]
+        L.orc_model_free.argtypes = [P]
+        L.orc_model_set.restype = C.c_int; L.orc_model_set.argtypes = [P, C.c_char_p, P, C.c_int64]
+        L.orc_model_quantize.restype = C.c_int; L.orc_model_quantize.argtypes = [P]
+        L.orc_encode.restype = C.c_int; L.orc_encode.argtypes = [P, P, C.c_int, P, P]
+        L.orc_decode_one.restype = C.c_int
+        L.orc_decode_one.argtypes = [P, P, C.c_int, C.c_int, P, P, C.POINTER(Trace)]
+        L.orc_decode_many.restype = C.c_int
+        L.orc_decode_many.argtypes = [P, P, P, C.c_int, P, P, P, C.c_int]
+        L.orc_max_threads.restype = C.c_int
+        L.orc_batch_by_words.restype = C.c_int
+        L.orc_batch_by_words.argtypes = [P, C.c_int, C.c_int, P, P, P]
+        L.orc_param_count.restype = C.c_int64; L.orc_param_count.argtypes = [C.POINTER(Cfg)]
+    return _lib
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def cfg_from_dims(m) -> Cfg:
+    return Cfg(m.d_model, m.d_ffn, m.n_heads, m.enc_layers, m.dec_layers, m.vocab, m.decoder,
+               m.aan_ffn_depth, m.aan_gate, m.out_bias, m.eos_id, m.clip, m.ln_eps)
+
+
+# ------------------------------------------------------------------ scalars / kernels
+def sigma(clip: float = 2.0) -> float:
+    return lib().orc_sigma(clip)
+
+
+def dequant_scale(clip: float = 2.0) -> float:
+    return lib().orc_dequant_scale(clip)
+
+
+def quantize(x: np.ndarray, clip: float = 2.0) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.empty(x.shape, dtype=np.int8)
+    lib().orc_quantize(_p(x), x.size, clip, _p(out))
+    return out
+
+
+def gemm_acc(a: np.ndarray, w: np.ndarray) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.int8); w = np.ascontiguousarray(w, dtype=np.int8)
+    M, K = a.shape; N, K2 = w.shape
+    assert K == K2
+    out = np.empty((M, N), dtype=np.int32)
+    lib().orc_gemm_acc(_p(a), _p(w), M, N, K, _p(out))
+    return out
+
+
+def layernorm(r: np.ndarray, g: np.ndarray, b: np.ndarray, eps: float = 1e-6) -> np.ndarray:
+    r = np.ascontiguousarray(r, dtype=np.float32)
+    g = np.ascontiguousarray(g, dtype=np.float32); b = np.ascontiguousarray(b, dtype=np.float32)
+    out = np.empty_like(r)
+    d = r.shape[-1]
+    rr = r.reshape(-1, d); oo = out.reshape(-1, d)
+    for i in range(rr.shape[0]):
+        lib().orc_layernorm(_p(rr[i]), d, _p(g), _p(b), eps, _p(oo[i]))
+    return out
+
+
+def attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, H: int) -> np.ndarray:
+    """One query row q [d] over key/value rows k, v [n x d]."""
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    k = np.ascontiguousarray(k, dtype=np.float32); v = np.ascontiguousarray(v, dtype=np.float32)
+    d = q.shape[0]; n = k.shape[0]
+    ctx = np.empty(d, dtype=np.float32)
+    lib().orc_attention(_p(q), _p(k), _p(v), d, n, d, H, _p(ctx))
+    return ctx
+
+
+def sigmoid(x: float) -> float:
+    return lib().orc_sigmoid(float(x))
+
+
+def pe(pos: int, d: int) -> np.ndarray:
+    out = np.empty(d, dtype=np.float32)
+    lib().orc_pe(pos, d, _p(out))
+    return out
+
+
+def aan_average(Y: np.ndarray) -> np.ndarray:
+    """Run the incremental AAN recurrence over rows of Y [T x d]; returns G [T x d]."""
+    Y = np.ascontiguousarray(Y, dtype=np.float32)
+    T, d = Y.shape
+    Cst = np.zeros(d, np.float32); G = np.empty_like(Y)
+    for t in range(T):
+        lib().orc_aan_step(_p(Cst), _p(Y[t]), t + 1, d, _p(G[t]))
+    return G
+
+
+def batch_by_words(lengths: np.ndarray, budget: int):
+    lengths = np.ascontiguousarray(lengths, dtype=np.int32)
+    n = lengths.shape[0]
+    order = np.empty(max(n, 1), dtype=np.int32); off = np.empty(n + 2, dtype=np.int32)
+    nb = np.zeros(1, dtype=np.int32)
+    st = lib().orc_batch_by_words(_p(lengths), n, budget, _p(order), _p(off), _p(nb))
+    if st:
+        raise ValueError("batch_by_words: bad argument")
+    return order[:n].copy(), off[:nb[0] + 1].copy()
+
+
+def param_count(m) -> int:
+    c = cfg_from_dims(m)
+    return int(lib().orc_param_count(C.byref(c)))
+
+
+# ------------------------------------------------------------------ model
+class OracleModel:
+    """The oracle's model: set every parameter, quantize once."""
+
+    def __init__(self, dims, weights: Optional[Dict[str, np.ndarray]] = None):
+        self.dims = dims
+        self._cfg = cfg_from_dims(dims)
+        self.h = lib().orc_model_new(C.byref(self._cfg))
+        if not self.h:
+            raise ValueError("oracle: bad config")
+        if weights is not None:
+            for k, v in weights.items():
+                self.set(k, v)
+            self.quantize()
+
+    def set(self, name: str, arr: np.ndarray) -> None:
+        a = np.ascontiguousarray(arr, dtype=np.float32)
+        st = lib().orc_model_set(self.h, name.encode(), _p(a), a.size)
+        if st:
+            raise ValueError(f"oracle: set {name}: status {st}")
+
+    def quantize(self) -> None:
+        st = lib().orc_model_quantize(self.h)
+        if st:
+            raise ValueError(f"oracle: quantize status {st}")
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().orc_model_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def encode(self, src: np.ndarray):
+        """Returns (enc_out [S x d], kv [L][2][S][d])."""
+        src = np.ascontiguousarray(src, dtype=np.int32)
+        S = src.shape[0]; d = self.dims.d_model; L = self.dims.dec_layers
+        enc = np.empty((S, d), np.float32); kv = np.empty((L, 2, S, d), np.float32)
+        st = lib().orc_encode(self.h, _p(src), S, _p(enc), _p(kv))
+        if st:
+            raise ValueError(f"oracle: encode status {st}")
+        return enc, kv
+
+    def decode_one(self, src: np.ndarray, max_len: int, forced: Optional[np.ndarray] = None,
+                   trace: bool = False, layers: bool = False):
+        src = np.ascontiguousarray(src, dtype=np.int32)
+        d = self.dims.d_model; L = self.dims.dec_layers
+        T = max(max_len, 0)
+        out = np.zeros(max(T, 1), np.int32)
+        tr = None; res = {}
+        if trace:
+            res = dict(ids=np.zeros(T, np.int32), second=np.zeros(T, np.int32),
+                       margin=np.zeros(T, np.float32), dec_out=np.zeros((T, d), np.float32),
+                       out_codes=np.zeros((T, d), np.int8))
+            if layers:
+                res["layer_out"] = np.zeros((T, L, 3, d), np.float32)
+            tr = Trace(_p(res["ids"]), _p(res["second"]), _p(res["margin"]), _p(res["dec_out"]),
+                       _p(res.get("layer_out")), _p(res["out_codes"]))
+        f = None
+        if forced is not None:
+            f = np.ascontiguousarray(forced, dtype=np.int32)
+            if f.size == 0:
+                f = np.zeros(1, np.int32)
+        n = lib().orc_decode_one(self.h, _p(src), src.shape[0], T, _p(f), _p(out),
+                                 C.byref(tr) if tr is not None else None)
+        if n < 0:
+            raise ValueError(f"oracle: decode status {-n}")
+        ids = out[:n].copy()
+        return (ids, res) if trace else ids
+
+    def decode_many(self, sset, nthreads: int = 0):
+        """Free-running greedy decode of a SentenceSet; returns list of id arrays."""
+        n = sset.n
+        ml = np.ascontiguousarray(sset.max_len, dtype=np.int32)
+        out = np.zeros(max(int(ml.sum()), 1), np.int32)
+        out_len = np.zeros(max(n, 1), np.int32)
+        ids = np.ascontiguousarray(sset.ids, dtype=np.int32)
+        offs = np.ascontiguousarray(sset.offsets, dtype=np.int64)
+        st = lib().orc_decode_many(self.h, _p(ids), _p(offs), n, _p(ml), _p(out), _p(out_len),
+                                   nthreads)
+        if st:
+            raise ValueError(f"oracle: decode_many status {st}")
+        res = []
+        o = 0
+        for i in range(n):
+            res.append(out[o:o + out_len[i]].copy())
+            o += int(ml[i])
+        return res
+
+
+def max_threads() -> int:
+    return int(lib().orc_max_threads())
