@@ -1,0 +1,163 @@
+/*
+ * mnmt.h — C ABI of libmnmt: batched greedy (beam-1) decoding of a distilled
+ * Transformer / AAN student with int8 matrix products on one B200 (sm_100a).
+ *
+ * The calls follow the paper's statement of the problem (arXiv 1805.12096,
+ * /root/reference/PAPER.md, cited P:L<n>): load a student of Table 1's
+ * dimensions with tied source/target/output embeddings over a
+ * 36,000-entry joint vocabulary; quantize every parameter matrix once
+ * (memoization of quant(B^T); int8 clip [-2,2] -> [-127,127],
+ * P:L94); sort sentences by source length and cut word-budget batches
+ * (P:L42); decode with beam 1, softmax skipped, "select the output word with
+ * highest activation".  Readings of points the paper leaves open are
+ * numbered R<k> in DESIGN.md.
+ *
+ * Conventions shared by every call:
+ *   - Every call returns an mnmt_status; nothing throws or aborts across the ABI.
+ *     mnmt_last_error() describes the last failure of the calling thread.
+ *   - Pointers named *_host are host memory owned by the caller, read or written
+ *     only during the call.  Pointers named *_dev are device memory on the
+ *     model's GPU, owned by the caller.
+ *   - One host thread per model handle at a time; handles are independent.
+ *   - A CUDA failure returns MNMT_ERR_CUDA once and makes the handle fail-stop:
+ *     every later call on it returns MNMT_ERR_STATE.
+ */
+#ifndef MNMT_H_
+#define MNMT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MNMT_ABI_VERSION 1
+
+typedef enum {
+  MNMT_OK = 0,
+  MNMT_ERR_ARG = 1,       /* bad argument: budget < 1, n < 0, bad config field, NULL pointer */
+  MNMT_ERR_DIM = 2,       /* unknown parameter name or wrong element count */
+  MNMT_ERR_VOCAB = 3,     /* token id < 0 or >= vocab */
+  MNMT_ERR_STATE = 4,     /* call-order violation, missing parameters, or fail-stopped handle */
+  MNMT_ERR_CAPACITY = 5,  /* output capacity too small, or a span > MNMT_MAX_SPAN */
+  MNMT_ERR_CUDA = 6,      /* CUDA runtime/driver failure (handle becomes fail-stop) */
+  MNMT_ERR_OOM = 7        /* device allocation failed */
+} mnmt_status;
+
+/* Longest source sentence / number of decoder steps per sentence. */
+#define MNMT_MAX_SPAN 512
+
+/* Student configuration (Table 1; AAN block P:L70-72). */
+typedef struct {
+  int32_t abi_version;    /* = MNMT_ABI_VERSION */
+  int32_t d_model;        /* embedding / model width d; d % 16 == 0, d % n_heads == 0, d <= 1024 */
+  int32_t d_ffn;          /* FFN width F; F % 16 == 0 */
+  int32_t n_heads;        /* H; d / H <= 64 and (d / H) % 4 == 0 (R11) */
+  int32_t enc_layers;     /* 6 in the paper */
+  int32_t dec_layers;     /* 6 in the paper */
+  int32_t vocab;          /* V = 36000 */
+  int32_t decoder;        /* 1 = AAN; 0 = self-attention with a KV cache */
+  int32_t aan_ffn_depth;  /* AAN FFN, hidden width = d (R9): 0 = "-ffn", 1, 2 (default) */
+  int32_t aan_gate;       /* 1 = gated AAN (default; R8), 0 = "-gate" */
+  int32_t out_bias;       /* 1 = output bias present (default; R14) */
+  int32_t eos_id;         /* end-of-sentence id, default 0 (R16) */
+  float clip;             /* quantization clip c = 2.0 */
+  float ln_eps;           /* LayerNorm epsilon, default 1e-6 (R10) */
+} mnmt_config;
+
+typedef struct mnmt_model mnmt_model;   /* opaque; owns all of its device memory */
+
+/* Fills *cfg with the defaults above and the given Table-1 widths. */
+void mnmt_config_default(mnmt_config* cfg, int32_t d_model, int32_t d_ffn, int32_t n_heads);
+
+/* Creates a model on CUDA device `cuda_device` (the caller's current device is
+ * restored).  Errors: MNMT_ERR_ARG (bad config), MNMT_ERR_CUDA, MNMT_ERR_OOM. */
+mnmt_status mnmt_model_create(const mnmt_config* cfg, int32_t cuda_device, mnmt_model** out);
+
+/* Copies one fp32 parameter.  `name` is a manifest name (DESIGN.md "Parameter
+ * manifest"), e.g. "emb.E" [V x d], "dec.3.src.q.W" [d x d]; every W is row-major
+ * [out x in], i.e. already the B^T operand of dotint(A, B).
+ * Errors: MNMT_ERR_DIM (unknown name / wrong numel), MNMT_ERR_STATE (after quantize). */
+mnmt_status mnmt_model_set_param(mnmt_model* m, const char* name, const float* host,
+                                 int64_t numel);
+
+/* One-time weight preparation: quantizes every parameter matrix to int8 codes on
+ * the device and builds its TMA descriptors — the memoized quant(B^T) of
+ * P:L100-105.  Errors: MNMT_ERR_STATE (missing parameters; names listed in
+ * mnmt_last_error()), MNMT_ERR_CUDA, MNMT_ERR_OOM. */
+mnmt_status mnmt_model_quantize(mnmt_model* m);
+
+/* Length-sorted word-budget batching (R17).  Stable sort of sentence
+ * indices by (src_len, index); a batch closes as soon as it holds >= budget
+ * words; the last batch may be short.  order[n], batch_off[n+1] (only the first
+ * *n_batches + 1 entries are written).  Host-only.  Errors: MNMT_ERR_ARG. */
+mnmt_status mnmt_batch_by_words(const int32_t* src_len_host, int32_t n, int32_t word_budget,
+                                int32_t* order_host, int32_t* batch_off_host,
+                                int32_t* n_batches);
+
+/* Greedy decode of n sentences as ONE batch (rows are independent: static
+ * scales).  Source sentence i is src_ids[src_off[i] .. src_off[i+1]);
+ * it decodes at most max_len[i] steps, stopping at EOS (not emitted) (R16).
+ * Its ids are written to out_ids[O_i ...] with O_i = sum_{k<i} max_len[k];
+ * out_len[i] = number written.  Work is enqueued on `cuda_stream` (NULL =
+ * legacy default stream) and the stream is synchronized before returning.
+ * Errors: MNMT_ERR_ARG, MNMT_ERR_VOCAB, MNMT_ERR_CAPACITY (out_cap < sum max_len,
+ * or a span > MNMT_MAX_SPAN), MNMT_ERR_STATE (before quantize), MNMT_ERR_CUDA. */
+mnmt_status mnmt_decode(mnmt_model* m, const int32_t* src_ids_host, const int64_t* src_off_host,
+                        int32_t n, const int32_t* max_len_host, int32_t* out_ids_host,
+                        int64_t out_cap, int32_t* out_len_host, void* cuda_stream);
+
+/* The whole translation job: batch_by_words(word_budget), then every batch is
+ * decoded back to back on one stream (one synchronization at the end); outputs
+ * are in INPUT order with the layout of mnmt_decode.
+ * flags & MNMT_DEVICE_IO: src_ids and out_ids/out_len are device pointers (the
+ * ids are already resident in HBM; offsets and max_len stay host arrays).
+ * Errors as mnmt_decode. */
+#define MNMT_DEVICE_IO 1u
+mnmt_status mnmt_translate(mnmt_model* m, const int32_t* src_ids, const int64_t* src_off_host,
+                           int32_t n, const int32_t* max_len_host, int32_t word_budget,
+                           int32_t* out_ids, int64_t out_cap, int32_t* out_len, uint32_t flags,
+                           void* cuda_stream);
+
+/* Teacher-forced decode (test hook for the parity protocol):
+ * sentence i runs T_i = forced_off[i+1] - forced_off[i] steps; the input at step
+ * t >= 2 is forced_ids[forced_off[i] + t - 2]; argmax_ids[forced_off[i] + t - 1]
+ * receives the model's argmax at step t.  No EOS stop.
+ * dump_mask selects intermediates copied to dump_host (sections in bit order):
+ *   MNMT_DUMP_ENC_OUT   fp32 [sum S_i][d]         encoder output
+ *   MNMT_DUMP_SRC_KV    fp32 [L][sum S_i][2][d]   source keys | values per layer
+ *   MNMT_DUMP_DEC_OUT   fp32 [sum T_i][d]         last decoder layer output per step
+ *   MNMT_DUMP_OUT_CODES int8 [sum T_i][d]         Q(dec_out): the output-layer operand
+ *   MNMT_DUMP_LAYERS    fp32 [sum T_i][L][3][d]   x1, x2, x3 of every decoder layer
+ * Errors as mnmt_decode; MNMT_ERR_CAPACITY if dump_cap is too small. */
+#define MNMT_DUMP_ENC_OUT 1u
+#define MNMT_DUMP_SRC_KV 2u
+#define MNMT_DUMP_DEC_OUT 4u
+#define MNMT_DUMP_OUT_CODES 8u
+#define MNMT_DUMP_LAYERS 16u
+mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids_host,
+                               const int64_t* src_off_host, int32_t n,
+                               const int32_t* forced_ids_host, const int64_t* forced_off_host,
+                               int32_t* argmax_ids_host, uint32_t dump_mask, void* dump_host,
+                               int64_t dump_cap, void* cuda_stream);
+
+/* Statistics of the last mnmt_translate / mnmt_decode call. */
+typedef struct {
+  int64_t gpu_launches;     /* kernels launched (graph nodes counted per replay) */
+  int64_t decode_steps;     /* decoder steps summed over batches */
+  int64_t batches;
+  int64_t target_words;     /* ids emitted (EOS excluded) */
+  int64_t h2d_bytes, d2h_bytes;
+} mnmt_stats;
+mnmt_status mnmt_get_stats(const mnmt_model* m, mnmt_stats* out);
+
+/* Thread-local description of the last failure; valid until the next call. */
+const char* mnmt_last_error(void);
+
+/* Frees every device allocation of the handle.  NULL is a no-op. */
+void mnmt_model_destroy(mnmt_model* m);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MNMT_H_ */

@@ -1,0 +1,81 @@
+/*
+ * mnmt_ops.h — op-level C ABI of libmnmt: each step of the decode path
+ * as one call on caller-owned DEVICE memory.
+ * Used by the kernel-level parity tests (P-1 of the parity protocol: inject the
+ * oracle's exact operands) and by the benchmark's per-kernel timing.  The
+ * model-level path (mnmt.h) runs the very same kernels.
+ *
+ * Conventions: every *_dev pointer is device memory on the current CUDA device,
+ * row-major, 16-byte aligned; work is enqueued on `stream` and NOT synchronized.
+ * Errors: MNMT_ERR_ARG for bad sizes/NULL pointers, MNMT_ERR_CUDA for launch
+ * failures (no handle is involved, so nothing becomes fail-stop).
+ * Quantization everywhere: Q(x) = RNE(clip(x, +-c) * 127/c) (R1, R2);
+ * dequantization: fmaf((float)acc, s, b), s = fl32(c^2/127^2) (R5).
+ */
+#ifndef MNMT_OPS_H_
+#define MNMT_OPS_H_
+
+#include <stdint.h>
+
+#include "mnmt.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* A1 / activation quantization: out[i] = Q(x[i]), n elements. */
+mnmt_status mnmt_op_quantize(const float* x_dev, int64_t n, float clip, int8_t* out_dev,
+                             void* stream);
+
+/* Epilogues of mnmt_op_gemm_i8 (v = fmaf((float)acc, s, bias)). */
+#define MNMT_EPI_F32 0        /* out fp32 [M x N] = v                              */
+#define MNMT_EPI_F32_Q 1      /* out fp32 = v and out2 int8 = Q(v)                 */
+#define MNMT_EPI_RELU_Q 2     /* out int8 = Q(ReLU(v))                             */
+#define MNMT_EPI_RELU_F32_Q 3 /* out fp32 = ReLU(v), out2 int8 = Q(ReLU(v))        */
+#define MNMT_EPI_SIGMOID 4    /* out fp32 = sigmoid(v) (fp64 exp, R20)             */
+#define MNMT_EPI_ARGMAX 5     /* out u64 [M] = max over columns of packed (v, col); caller zeroes it */
+#define MNMT_EPI_ACC 6        /* out int32 [M x N] = exact s32 accumulator         */
+
+/* dotint(quant(A), quant(B^T)) = A . W^T on the int8 tensor cores (R3):
+ * A [M x K] codes, W [N x K] codes (K % 16 == 0), bias [N] fp32 or NULL.
+ * For EPI_F32* / SIGMOID / ACC, N % 16 == 0; out row stride = N.
+ * n_tile = 0 (auto), 64, 128 or 256. */
+mnmt_status mnmt_op_gemm_i8(const int8_t* A_dev, const int8_t* W_dev, int32_t M, int32_t N,
+                            int32_t K, const float* bias_dev, float clip, int32_t epilogue,
+                            void* out_dev, void* out2_dev, int32_t n_tile, void* stream);
+
+/* Argmax key -> id (the packed key of MNMT_EPI_ARGMAX; lowest id wins ties, R15). */
+mnmt_status mnmt_op_argmax_ids(const uint64_t* keys_dev, int32_t n, int32_t* ids_dev,
+                               void* stream);
+
+/* A3/A6-A8: out = LN(fl(x + delta)) (post-norm, fp64 statistics; R10, R20) and
+ * out_q = Q(out).  Gate form (gi_dev != NULL, R8): out = LN(fl(x + fl(fl(gi*x) + fl(gf*delta)))). */
+mnmt_status mnmt_op_layernorm(const float* x_dev, const float* delta_dev, const float* gi_dev,
+                              const float* gf_dev, const float* gamma_dev, const float* beta_dev,
+                              int32_t n, int32_t d, float eps, float clip, float* out_dev,
+                              int8_t* out_q_dev, void* stream);
+
+/* A6 (AAN): one step t of the running sum for n rows: C <- fl(C + y),
+ * g = fl(C / t); writes g (fp32, may be NULL) and Q(g) (may be NULL). */
+mnmt_status mnmt_op_aan_step(float* C_dev, const float* y_dev, int32_t n, int32_t d, int32_t t,
+                             float clip, float* g_dev, int8_t* g_q_dev, void* stream);
+
+/* A2/A5: x = fl(fl(E[id] * fl32(sqrt d)) + PE[pos]) (id < 0: zero vector, R13) and Q(x). */
+mnmt_status mnmt_op_embed(const float* E_dev, int32_t d, const int32_t* ids_dev,
+                          const int32_t* pos_dev, int32_t n, float clip, float* x_dev,
+                          int8_t* x_q_dev, void* stream);
+
+/* A3/A7: attention of n query rows over per-row key/value spans (fp64, R20):
+ * row r attends over kv rows kv_start[r] .. kv_start[r] + kv_len[r] - 1;
+ * query at q + r*ldq, key j at kv + j*ldkv + k_off, value at kv + j*ldkv + v_off.
+ * Head h uses columns [h*d/H, (h+1)*d/H) (R11).  out_q = Q(ctx) [n x d];
+ * out_f (may be NULL) = ctx fp32.  kv_len[r] <= MNMT_MAX_SPAN. */
+mnmt_status mnmt_op_attention(const float* q_dev, int64_t ldq, const float* kv_dev, int64_t ldkv,
+                              int32_t k_off, int32_t v_off, const int32_t* kv_start_dev,
+                              const int32_t* kv_len_dev, int32_t n, int32_t d, int32_t H,
+                              float clip, int8_t* out_q_dev, float* out_f_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MNMT_OPS_H_ */

@@ -110,6 +110,16 @@ static void lin1(const orc_lin *L, const int8_t *qa, float s, float *out) {
     }
 }
 
+/* lin over M rows: out[i][j] = fmaf((float)sum_k qa[i][k] qw[j][k], s, b[j]) (R5). */
+void orc_linear(const int8_t *qa, const int8_t *qw, int M, int N, int K, const float *b,
+                float clip, float *out) {
+    orc_lin L = {NULL, (float *)b, (int8_t *)qw, N, K};
+    float s = orc_dequant_scale(clip);
+    for (int i = 0; i < M; ++i) lin1(&L, qa + (int64_t)i * K, s, out + (int64_t)i * N);
+}
+
+void orc_sigmoid_array(const float *x, int64_t n, float *out);
+
 /* LayerNorm, post-norm (P:L65 Vaswani recipe; R10), fp64 accumulation (R20):
  * mu = sum r / d; var = sum (r-mu)^2 / d; out = (r-mu)/sqrt(var+eps)*g + b. */
 void orc_layernorm(const float *r, int d, const float *g, const float *b, float eps, float *out) {
@@ -164,6 +174,28 @@ void orc_aan_step(float *C, const float *y, int t, int d, float *g) {
 
 /* sigma(x) = 1/(1+exp(-x)), fp64 then rounded (R20). */
 float orc_sigmoid(float x) { return (float)(1.0 / (1.0 + exp(-(double)x))); }
+void orc_sigmoid_array(const float *x, int64_t n, float *out) {
+    for (int64_t i = 0; i < n; ++i) out[i] = orc_sigmoid(x[i]);
+}
+
+/* Residual + LayerNorm of one row: out = LN(fl(x + z)) with z = delta, or, in the gate
+ * form (gi != NULL; R8), z = fl(fl(sig_i * x) + fl(sig_f * delta)) where gi/gf are the
+ * gate activations after the sigmoid. */
+void orc_residual_ln(const float *x, const float *delta, const float *gi, const float *gf, int d,
+                     const float *g, const float *b, float eps, float *out) {
+    float *r = (float *)malloc(sizeof(float) * (size_t)d);
+    for (int k = 0; k < d; ++k) {
+        float z = delta[k];
+        if (gi) {
+            float iy = gi[k] * x[k];
+            float fa = gf[k] * delta[k];
+            z = iy + fa;
+        }
+        r[k] = x[k] + z;
+    }
+    orc_layernorm(r, d, g, b, eps, out);
+    free(r);
+}
 
 /* Sinusoidal position encoding (P:L65 Vaswani recipe; R12):
  * PE[pos][2i] = sin(pos / 10000^(2i/d)), PE[pos][2i+1] = cos(same). */
@@ -177,14 +209,20 @@ void orc_pe(int pos, int d, float *out) {
 
 /* emb(id, pos) = fl(fl(E[id] * fl32(sqrt d)) + PE[pos]); id < 0 = zero vector
  * (the start symbol, R13).  Tied embedding E. */
-static void embed(const orc_model *m, int id, int pos, float *out, float *pe_tmp) {
-    int d = m->c.d_model;
+void orc_embed_row(const float *E, int d, int id, int pos, float *out) {
     float r = (float)sqrt((double)d);
-    orc_pe(pos, d, pe_tmp);
+    float *pe = (float *)malloc(sizeof(float) * (size_t)d);
+    orc_pe(pos, d, pe);
     for (int k = 0; k < d; ++k) {
-        float e = id >= 0 ? m->E[(int64_t)id * d + k] * r : 0.0f;
-        out[k] = e + pe_tmp[k];
+        float e = id >= 0 ? E[(int64_t)id * d + k] * r : 0.0f;
+        out[k] = e + pe[k];
     }
+    free(pe);
+}
+
+static void embed(const orc_model *m, int id, int pos, float *out, float *pe_tmp) {
+    (void)pe_tmp;
+    orc_embed_row(m->E, m->c.d_model, id, pos, out);
 }
 
 /* ----------------------------------------------------- model assembly */
@@ -391,14 +429,14 @@ int orc_encode(const orc_model *m, const int32_t *src, int S, float *enc_out, fl
             orc_attention(Q + (int64_t)i * d, Kt, Vt, d, S, d, H, ctx);
             orc_quantize(ctx, d, clip, qa);
             lin1(&e->o, qa, s, o);
-            for (int k = 0; k < d; ++k) r[k] = xi[k] + o[k];
-            orc_layernorm(r, d, e->ln1.g, e->ln1.b, c->ln_eps, xi);
+            orc_residual_ln(xi, o, NULL, NULL, d, e->ln1.g, e->ln1.b, c->ln_eps, r);
+            memcpy(xi, r, sizeof(float) * d);
             orc_quantize(xi, d, clip, qa);
             lin1(&e->f1, qa, s, h);
             for (int k = 0; k < F; ++k) qa[k] = orc_q(h[k] > 0.0f ? h[k] : 0.0f, clip);
             lin1(&e->f2, qa, s, o);
-            for (int k = 0; k < d; ++k) r[k] = xi[k] + o[k];
-            orc_layernorm(r, d, e->ln2.g, e->ln2.b, c->ln_eps, xi);
+            orc_residual_ln(xi, o, NULL, NULL, d, e->ln2.g, e->ln2.b, c->ln_eps, r);
+            memcpy(xi, r, sizeof(float) * d);
         }
     }
     if (enc_out) memcpy(enc_out, x, sizeof(float) * (size_t)S * d);
@@ -486,16 +524,12 @@ int orc_decode_one(const orc_model *m, const int32_t *src, int S, int max_len,
                     lin1(&D->gi, qy, s, gi);
                     orc_quantize(a, d, clip, qa);
                     lin1(&D->gf, qa, s, gf);
-                    for (int k = 0; k < d; ++k) {
-                        float iy = orc_sigmoid(gi[k]) * y[k];
-                        float fa = orc_sigmoid(gf[k]) * a[k];
-                        float z = iy + fa;
-                        r[k] = y[k] + z;
-                    }
+                    orc_sigmoid_array(gi, d, gi);
+                    orc_sigmoid_array(gf, d, gf);
+                    orc_residual_ln(y, a, gi, gf, d, D->ln1.g, D->ln1.b, c->ln_eps, x1);
                 } else {
-                    for (int k = 0; k < d; ++k) r[k] = y[k] + a[k];
+                    orc_residual_ln(y, a, NULL, NULL, d, D->ln1.g, D->ln1.b, c->ln_eps, x1);
                 }
-                orc_layernorm(r, d, D->ln1.g, D->ln1.b, c->ln_eps, x1);
             } else {
                 /* A6': self-attention over positions 1..t with a KV cache. */
                 float *Kl = Ks + (int64_t)l * Tcap * d, *Vl = Vs + (int64_t)l * Tcap * d;
@@ -506,8 +540,7 @@ int orc_decode_one(const orc_model *m, const int32_t *src, int S, int max_len,
                 orc_attention(qs, Kl, Vl, d, t, d, H, ctx);
                 orc_quantize(ctx, d, clip, qa);
                 lin1(&D->o, qa, s, a);
-                for (int k = 0; k < d; ++k) r[k] = y[k] + a[k];
-                orc_layernorm(r, d, D->ln1.g, D->ln1.b, c->ln_eps, x1);
+                orc_residual_ln(y, a, NULL, NULL, d, D->ln1.g, D->ln1.b, c->ln_eps, x1);
             }
             /* A7: source attention. */
             orc_quantize(x1, d, clip, qa);
@@ -520,15 +553,13 @@ int orc_decode_one(const orc_model *m, const int32_t *src, int S, int max_len,
             }
             orc_quantize(ctx, d, clip, qa);
             lin1(&D->so, qa, s, a);
-            for (int k = 0; k < d; ++k) r[k] = x1[k] + a[k];
-            orc_layernorm(r, d, D->ln2.g, D->ln2.b, c->ln_eps, x2);
+            orc_residual_ln(x1, a, NULL, NULL, d, D->ln2.g, D->ln2.b, c->ln_eps, x2);
             /* A8: FFN; ReLU output goes straight to int8 codes. */
             orc_quantize(x2, d, clip, qa);
             lin1(&D->f1, qa, s, h);
             for (int k = 0; k < F; ++k) qa[k] = orc_q(h[k] > 0.0f ? h[k] : 0.0f, clip);
             lin1(&D->f2, qa, s, a);
-            for (int k = 0; k < d; ++k) r[k] = x2[k] + a[k];
-            orc_layernorm(r, d, D->ln3.g, D->ln3.b, c->ln_eps, y);
+            orc_residual_ln(x2, a, NULL, NULL, d, D->ln3.g, D->ln3.b, c->ln_eps, y);
             if (tr && tr->layer_out) {
                 float *dst = tr->layer_out + (((int64_t)(t - 1) * L + l) * 3) * d;
                 memcpy(dst, x1, sizeof(float) * d);

@@ -59,6 +59,10 @@ def lib():
         L.orc_sigmoid.restype = C.c_float; L.orc_sigmoid.argtypes = [C.c_float]
         L.orc_pe.argtypes = [C.c_int, C.c_int, P]
         L.orc_aan_step.argtypes = [P, P, C.c_int, C.c_int, P]
+        L.orc_linear.argtypes = [P, P, C.c_int, C.c_int, C.c_int, P, C.c_float, P]
+        L.orc_sigmoid_array.argtypes = [P, C.c_int64, P]
+        L.orc_residual_ln.argtypes = [P, P, P, P, C.c_int, P, P, C.c_float, P]
+        L.orc_embed_row.argtypes = [P, C.c_int, C.c_int, C.c_int, P]
         L.orc_model_new.restype = P; L.orc_model_new.argtypes = [C.POINTER(Cfg)]
         L.orc_model_free.argtypes = [P]
         L.orc_model_set.restype = C.c_int; L.orc_model_set.argtypes = [P, C.c_char_p, P, C.c_int64]
@@ -106,6 +110,46 @@ def gemm_acc(a: np.ndarray, w: np.ndarray) -> np.ndarray:
     assert K == K2
     out = np.empty((M, N), dtype=np.int32)
     lib().orc_gemm_acc(_p(a), _p(w), M, N, K, _p(out))
+    return out
+
+
+def linear(qa: np.ndarray, qw: np.ndarray, bias: Optional[np.ndarray], clip: float = 2.0) -> np.ndarray:
+    """lin(qa; W, b) = fmaf((float)acc, s, b) over rows of qa [M x K], qw [N x K]."""
+    qa = np.ascontiguousarray(qa, dtype=np.int8); qw = np.ascontiguousarray(qw, dtype=np.int8)
+    M, K = qa.shape; N = qw.shape[0]
+    b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float32)
+    out = np.empty((M, N), np.float32)
+    lib().orc_linear(_p(qa), _p(qw), M, N, K, _p(b), clip, _p(out))
+    return out
+
+
+def sigmoid_array(x: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.empty_like(x)
+    lib().orc_sigmoid_array(_p(x), x.size, _p(out))
+    return out
+
+
+def residual_ln(x, delta, g, b, eps=1e-6, gi=None, gf=None) -> np.ndarray:
+    """Rows: LN(fl(x + delta)) or the gate form LN(fl(x + fl(fl(gi*x) + fl(gf*delta))))."""
+    x = np.ascontiguousarray(x, np.float32); delta = np.ascontiguousarray(delta, np.float32)
+    g = np.ascontiguousarray(g, np.float32); b = np.ascontiguousarray(b, np.float32)
+    if gi is not None:
+        gi = np.ascontiguousarray(gi, np.float32); gf = np.ascontiguousarray(gf, np.float32)
+    d = x.shape[-1]
+    out = np.empty_like(x)
+    for i in range(x.shape[0]):
+        lib().orc_residual_ln(_p(x[i]), _p(delta[i]), _p(None if gi is None else gi[i]),
+                              _p(None if gf is None else gf[i]), d, _p(g), _p(b), eps, _p(out[i]))
+    return out
+
+
+def embed_rows(E: np.ndarray, ids, pos) -> np.ndarray:
+    E = np.ascontiguousarray(E, np.float32)
+    d = E.shape[1]
+    out = np.empty((len(ids), d), np.float32)
+    for i, (t, p) in enumerate(zip(ids, pos)):
+        lib().orc_embed_row(_p(E), d, int(t), int(p), _p(out[i]))
     return out
 
 

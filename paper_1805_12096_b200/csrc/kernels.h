@@ -1,0 +1,50 @@
+// kernels.h — host-side launch interface of the sm_100a kernels (internal to libmnmt).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace mnmt {
+
+// Epilogues of the int8 GEMM (acc = exact s32; v = fmaf((float)acc, s, bias)).
+enum Epi : int {
+  EPI_F32 = 0,        // out_f = v                       (projections, residual deltas)
+  EPI_F32_Q = 1,      // out_f = v, out_q = Q(v)         (AAN FFN output a, needed as both)
+  EPI_RELU_Q = 2,     // out_q = Q(ReLU(v))              (FFN1: ReLU straight to codes)
+  EPI_RELU_F32_Q = 3, // out_f = ReLU(v), out_q = Q(.)   (AAN FFN depth 1)
+  EPI_SIGMOID = 4,    // out_f = sigmoid(v)              (AAN gates)
+  EPI_ARGMAX = 5,     // keys[row] = max packed(v, col)  (output layer, A9)
+  EPI_ACC = 6,        // out_i = acc                     (test hook: raw accumulators)
+};
+
+struct GemmArgs {
+  int M;                       // rows covered by the grid (static upper bound)
+  const int32_t* M_dyn;        // optional device row count (live rows), <= M
+  int N, K;
+  float scale;                 // s = fl32(c^2 / 127^2)
+  const float* bias;           // [N] or nullptr
+  float clip, sigma;
+  float* out_f;
+  int8_t* out_q;
+  int32_t* out_i;
+  int64_t ldo;                 // output row stride (elements)
+  int col_block;               // scatter: out + (n / col_block) * block_stride + m * ldo + n % col_block
+  int64_t block_stride;
+  unsigned long long* keys;    // [rows] for EPI_ARGMAX
+};
+
+// Tensor map over a row-major int8 matrix [rows x K] (K contiguous, K % 16 == 0):
+// box {128 bytes, 64 rows}, 128-byte swizzle (the UMMA K-major SW128 atom).
+bool make_tmap_i8(CUtensorMap* map, const void* base, int64_t rows, int64_t K);
+
+// A is [>= M x K] activation codes, B is [N x K] weight codes (both via make_tmap_i8).
+// bn = 0 picks the N tile.
+cudaError_t launch_gemm_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
+                           int epi, int bn, cudaStream_t st);
+
+int gemm_pick_bn(int M, int N);   // 64, 128 or 256
+
+// Sets the dynamic-smem attribute of every GEMM instantiation on the current device.
+cudaError_t gemm_init();
+
+}  // namespace mnmt

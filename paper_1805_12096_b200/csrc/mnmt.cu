@@ -1,0 +1,1258 @@
+// mnmt.cu — libmnmt runtime: the C ABI of include/mnmt.h on top of the sm_100a kernels.
+//
+// Host side only schedules; every step of the decode path runs in kernels
+// (gemm_i8.cu, rowops.cu).  Per batch (PAPER.md:L42 length-sorted word batches):
+//   encoder: embed -> L x [QKV GEMM -> attn -> O GEMM -> LN -> FFN1(ReLU->codes) -> FFN2 -> LN]
+//            -> one GEMM for every decoder layer's source K|V (N = 2 d L), scattered per layer;
+//   decoder step (one CUDA graph, replayed max_len times; live-row count and t live on device):
+//            embed(+AAN step of layer 0) -> L x [AAN FFN / gates | self-attn] -> LN1
+//            -> src-q GEMM -> src attention -> src-o GEMM -> LN2 -> FFN1 -> FFN2
+//            -> LN3 (+AAN step of the next layer) -> output GEMM fused with argmax -> finish.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/mnmt.h"
+#include "../../include/mnmt_ops.h"
+#include "kernels.h"
+#include "rowops.h"
+
+using namespace mnmt;
+
+static thread_local std::string g_err;
+
+static void set_err(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+extern "C" const char* mnmt_last_error(void) { return g_err.c_str(); }
+void mnmt_set_error_str(const char* s) { g_err = s; }
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+struct Lin {
+  int8_t* q = nullptr;
+  float* b = nullptr;
+  int out = 0, in = 0;
+  CUtensorMap tm;
+};
+
+struct EncLayer {
+  Lin qkv, o, f1, f2;
+  float *ln1g = nullptr, *ln1b = nullptr, *ln2g = nullptr, *ln2b = nullptr;
+};
+struct DecLayer {
+  Lin a1, a2, gi, gf, qkv, o, sq, so, f1, f2;
+  float* ln[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+};
+
+struct Workspace {
+  int64_t M_cap = 0, B_cap = 0, T_cap = 0, O_cap = 0, N_cap = 0, tok_cap = 0;
+  std::vector<void*> allocs;
+  // encoder (token rows)
+  float *x = nullptr, *qkv = nullptr, *o = nullptr, *kv = nullptr;
+  int8_t *cx = nullptr, *cctx = nullptr, *ch = nullptr;
+  CUtensorMap tm_cx, tm_cctx, tm_ch;
+  // decoder (compact live rows)
+  int32_t *ctrl = nullptr, *live = nullptr, *prev_id = nullptr;
+  int32_t *row_start = nullptr, *row_len = nullptr, *max_len = nullptr, *len_idx = nullptr;
+  int64_t *out_off = nullptr, *forced_off = nullptr;
+  int32_t* forced = nullptr;
+  unsigned long long* keys = nullptr;
+  float *C = nullptr, *y = nullptr, *g = nullptr, *a = nullptr, *gi = nullptr, *gf = nullptr;
+  float *x1 = nullptr, *qs = nullptr, *od = nullptr, *x2 = nullptr, *f = nullptr, *qkvd = nullptr;
+  float* selfkv = nullptr;
+  int8_t *cy = nullptr, *cg = nullptr, *ch1 = nullptr, *ca = nullptr, *cx1 = nullptr;
+  int8_t *cctxd = nullptr, *cx2 = nullptr, *chd = nullptr;
+  CUtensorMap tm_cy, tm_cg, tm_ch1, tm_ca, tm_cx1, tm_cctxd, tm_cx2, tm_chd;
+  // job-level
+  int32_t* out_ids = nullptr;
+  int32_t* out_len = nullptr;
+  int32_t* src_ids = nullptr;
+  int32_t* meta = nullptr;   // token metadata of all batches of a job
+  int64_t meta_cap = 0;
+  int32_t* rmeta32 = nullptr;  // row metadata of all batches: [start|len|max_len|len_idx] x B_b
+  int64_t* rmeta64 = nullptr;  // [out_off|forced_off] x B_b
+  int64_t rows_cap = 0;
+};
+
+}  // namespace
+
+struct mnmt_model {
+  mnmt_config c;
+  int dev = 0;
+  bool quantized = false, failed = false;
+  std::map<std::string, int64_t> manifest;               // name -> numel
+  std::map<std::string, std::vector<float>> host;        // set parameters (until quantize)
+  std::vector<void*> allocs;
+  float *E = nullptr, *out_b = nullptr, *PE = nullptr;
+  int8_t* qE = nullptr;
+  CUtensorMap tmE;
+  std::vector<EncLayer> enc;
+  std::vector<DecLayer> dec;
+  Lin kv_all;
+  Workspace ws;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  std::map<int64_t, cudaGraphExec_t> graphs;             // key: padded live-row bound
+  int64_t launches_per_step = 0;
+  mnmt_stats stats{};
+  int max_pos = MNMT_MAX_SPAN + 1;
+};
+
+namespace {
+
+#define CK(call)                                                                    \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      set_err("CUDA error %s at %s:%d: %s", cudaGetErrorName(e_), __FILE__, __LINE__, \
+              cudaGetErrorString(e_));                                              \
+      return MNMT_ERR_CUDA;                                                         \
+    }                                                                               \
+  } while (0)
+
+#define CKS(call)                    \
+  do {                               \
+    mnmt_status s_ = (call);         \
+    if (s_ != MNMT_OK) return s_;    \
+  } while (0)
+
+// CUDA failure -> fail-stop handle.
+static mnmt_status fail(mnmt_model* m, mnmt_status s) {
+  if (s == MNMT_ERR_CUDA) m->failed = true;
+  return s;
+}
+
+static float sigma_of(const mnmt_model* m) { return 127.0f / m->c.clip; }
+static float scale_of(const mnmt_model* m) {
+  return (float)(((double)m->c.clip * (double)m->c.clip) / (127.0 * 127.0));
+}
+
+static mnmt_status dmalloc(std::vector<void*>& list, void** p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_err("cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    return MNMT_ERR_OOM;
+  }
+  list.push_back(*p);
+  return MNMT_OK;
+}
+template <typename T>
+static mnmt_status dalloc(std::vector<void*>& list, T** p, int64_t n) {
+  return dmalloc(list, reinterpret_cast<void**>(p), (size_t)std::max<int64_t>(n, 1) * sizeof(T));
+}
+
+static void build_manifest(mnmt_model* m) {
+  const auto& c = m->c;
+  const int64_t d = c.d_model, F = c.d_ffn, V = c.vocab;
+  auto& mf = m->manifest;
+  mf["emb.E"] = V * d;
+  if (c.out_bias) mf["out.b"] = V;
+  auto lin = [&](const std::string& p, int64_t out, int64_t in) {
+    mf[p + ".W"] = out * in;
+    mf[p + ".b"] = out;
+  };
+  auto ln = [&](const std::string& p) {
+    mf[p + ".g"] = d;
+    mf[p + ".b"] = d;
+  };
+  for (int l = 0; l < c.enc_layers; ++l) {
+    const std::string p = "enc." + std::to_string(l) + ".";
+    for (const char* s : {"q", "k", "v", "o"}) lin(p + "self." + s, d, d);
+    lin(p + "ffn.1", F, d);
+    lin(p + "ffn.2", d, F);
+    ln(p + "ln1");
+    ln(p + "ln2");
+  }
+  for (int l = 0; l < c.dec_layers; ++l) {
+    const std::string p = "dec." + std::to_string(l) + ".";
+    if (c.decoder == 1) {
+      if (c.aan_ffn_depth >= 1) lin(p + "aan.ffn.1", d, d);
+      if (c.aan_ffn_depth >= 2) lin(p + "aan.ffn.2", d, d);
+      if (c.aan_gate) {
+        lin(p + "aan.gate.i", d, d);
+        lin(p + "aan.gate.f", d, d);
+      }
+    } else {
+      for (const char* s : {"q", "k", "v", "o"}) lin(p + "self." + s, d, d);
+    }
+    for (const char* s : {"q", "k", "v", "o"}) lin(p + "src." + s, d, d);
+    lin(p + "ffn.1", F, d);
+    lin(p + "ffn.2", d, F);
+    ln(p + "ln1");
+    ln(p + "ln2");
+    ln(p + "ln3");
+  }
+}
+
+static const char* cfg_problem(const mnmt_config* c) {
+  if (!c) return "config is NULL";
+  if (c->abi_version != MNMT_ABI_VERSION) return "abi_version mismatch";
+  if (c->d_model < 16 || c->d_model > 1024 || c->d_model % 16) return "d_model must be 16..1024, multiple of 16";
+  if (c->d_ffn < 16 || c->d_ffn % 16) return "d_ffn must be a positive multiple of 16";
+  if (c->n_heads < 1 || c->d_model % c->n_heads) return "d_model must be divisible by n_heads";
+  const int dh = c->d_model / c->n_heads;
+  if (dh % 4 || dh > 64) return "head width d/H must be a multiple of 4 and <= 64";
+  if (c->enc_layers < 0 || c->enc_layers > 64 || c->dec_layers < 1 || c->dec_layers > 64) return "layer count out of range";
+  if (c->vocab < 1) return "vocab must be >= 1";
+  if (c->decoder != 0 && c->decoder != 1) return "decoder must be 0 or 1";
+  if (c->aan_ffn_depth < 0 || c->aan_ffn_depth > 2) return "aan_ffn_depth must be 0, 1 or 2";
+  if (c->aan_gate != 0 && c->aan_gate != 1) return "aan_gate must be 0 or 1";
+  if (c->out_bias != 0 && c->out_bias != 1) return "out_bias must be 0 or 1";
+  if (c->eos_id < 0 || c->eos_id >= c->vocab) return "eos_id out of range";
+  if (!(c->clip > 0.0f) || !std::isfinite(c->clip)) return "clip must be > 0";
+  if (!(c->ln_eps >= 0.0f)) return "ln_eps must be >= 0";
+  return nullptr;
+}
+
+// Upload and quantize a (possibly concatenated) weight: rows from `names` stacked in order.
+static mnmt_status prep_lin(mnmt_model* m, Lin& L, const std::vector<std::string>& names,
+                            int rows_each, int in, float* tmp) {
+  const int out = rows_each * (int)names.size();
+  L.out = out;
+  L.in = in;
+  CKS(dalloc(m->allocs, &L.q, (int64_t)out * in));
+  CKS(dalloc(m->allocs, &L.b, out));
+  for (size_t i = 0; i < names.size(); ++i) {
+    const auto& W = m->host[names[i] + ".W"];
+    const auto& b = m->host[names[i] + ".b"];
+    CK(cudaMemcpyAsync(tmp, W.data(), W.size() * sizeof(float), cudaMemcpyHostToDevice, m->st));
+    CK(launch_quantize(tmp, (int64_t)W.size(), m->c.clip, L.q + (int64_t)i * rows_each * in, m->st));
+    CK(cudaMemcpyAsync(L.b + (int64_t)i * rows_each, b.data(), b.size() * sizeof(float),
+                       cudaMemcpyHostToDevice, m->st));
+    CK(cudaStreamSynchronize(m->st));  // tmp is reused
+  }
+  if (!make_tmap_i8(&L.tm, L.q, out, in)) {
+    set_err("cuTensorMapEncodeTiled failed for %s", names[0].c_str());
+    return MNMT_ERR_CUDA;
+  }
+  return MNMT_OK;
+}
+
+static mnmt_status upload_vec(mnmt_model* m, float** dst, const std::string& name) {
+  const auto& v = m->host[name];
+  CKS(dalloc(m->allocs, dst, (int64_t)v.size()));
+  CK(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(float), cudaMemcpyHostToDevice, m->st));
+  return MNMT_OK;
+}
+
+// ------------------------------------------------------------------ workspace
+static void ws_free(mnmt_model* m) {
+  for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
+  m->graphs.clear();
+  for (void* p : m->ws.allocs) cudaFree(p);
+  m->ws = Workspace();
+}
+
+static mnmt_status ws_tmap(CUtensorMap* tm, const void* p, int64_t rows, int64_t K) {
+  if (!make_tmap_i8(tm, p, rows, K)) {
+    set_err("cuTensorMapEncodeTiled failed (workspace)");
+    return MNMT_ERR_CUDA;
+  }
+  return MNMT_OK;
+}
+
+// Grows the workspace to hold M tokens, B rows, T steps, O output ids, N sentences.
+static mnmt_status ws_ensure(mnmt_model* m, int64_t M, int64_t B, int64_t T, int64_t O, int64_t N,
+                             int64_t tok, int64_t meta, int64_t rows) {
+  Workspace& w = m->ws;
+  if (M <= w.M_cap && B <= w.B_cap && T <= w.T_cap && O <= w.O_cap && N <= w.N_cap &&
+      tok <= w.tok_cap && meta <= w.meta_cap && rows <= w.rows_cap)
+    return MNMT_OK;
+  CK(cudaStreamSynchronize(m->st));
+  auto grow = [](int64_t need, int64_t have) { return std::max(need, have); };
+  auto rnd = [](int64_t v, int64_t a) { return (std::max<int64_t>(v, 1) + a - 1) / a * a; };
+  const int64_t Mc = rnd(grow(M, w.M_cap), 128), Bc = rnd(grow(B, w.B_cap), 128);
+  const int64_t Tc = grow(T, w.T_cap), Oc = grow(O, w.O_cap), Nc = grow(N, w.N_cap);
+  const int64_t tokc = grow(tok, w.tok_cap), metac = grow(meta, w.meta_cap);
+  const int64_t rowsc = grow(rows, w.rows_cap);
+  ws_free(m);
+  Workspace& z = m->ws;
+  z.M_cap = Mc; z.B_cap = Bc; z.T_cap = Tc; z.O_cap = Oc; z.N_cap = Nc; z.tok_cap = tokc; z.meta_cap = metac;
+  z.rows_cap = rowsc;
+  const auto& c = m->c;
+  const int64_t d = c.d_model, F = c.d_ffn, L = c.dec_layers;
+  auto& A = z.allocs;
+  CKS(dalloc(A, &z.x, Mc * d));
+  CKS(dalloc(A, &z.qkv, Mc * 3 * d));
+  CKS(dalloc(A, &z.o, Mc * d));
+  CKS(dalloc(A, &z.kv, L * Mc * 2 * d));
+  CKS(dalloc(A, &z.cx, Mc * d));
+  CKS(dalloc(A, &z.cctx, Mc * d));
+  CKS(dalloc(A, &z.ch, Mc * F));
+  CKS(dalloc(A, &z.ctrl, 64));
+  CKS(dalloc(A, &z.live, Bc));
+  CKS(dalloc(A, &z.prev_id, Bc));
+  CKS(dalloc(A, &z.row_start, Bc));
+  CKS(dalloc(A, &z.row_len, Bc));
+  CKS(dalloc(A, &z.max_len, Bc));
+  CKS(dalloc(A, &z.len_idx, Bc));
+  CKS(dalloc(A, &z.out_off, Bc));
+  CKS(dalloc(A, &z.forced_off, Bc));
+  CKS(dalloc(A, &z.forced, Oc));
+  CKS(dalloc(A, &z.keys, Bc));
+  CKS(dalloc(A, &z.C, L * Bc * d));
+  for (float** p : {&z.y, &z.g, &z.a, &z.gi, &z.gf, &z.x1, &z.qs, &z.od, &z.x2, &z.f})
+    CKS(dalloc(A, p, Bc * d));
+  CKS(dalloc(A, &z.qkvd, Bc * 3 * d));
+  if (c.decoder == 0) CKS(dalloc(A, &z.selfkv, L * Bc * Tc * 2 * d));
+  for (int8_t** p : {&z.cy, &z.cg, &z.ch1, &z.ca, &z.cx1, &z.cctxd, &z.cx2})
+    CKS(dalloc(A, p, Bc * d));
+  CKS(dalloc(A, &z.chd, Bc * F));
+  CKS(dalloc(A, &z.out_ids, Oc));
+  CKS(dalloc(A, &z.out_len, Nc));
+  CKS(dalloc(A, &z.src_ids, tokc));
+  CKS(dalloc(A, &z.meta, metac));
+  CKS(dalloc(A, &z.rmeta32, 4 * rowsc));
+  CKS(dalloc(A, &z.rmeta64, 2 * rowsc));
+  CKS(ws_tmap(&z.tm_cx, z.cx, Mc, d));
+  CKS(ws_tmap(&z.tm_cctx, z.cctx, Mc, d));
+  CKS(ws_tmap(&z.tm_ch, z.ch, Mc, F));
+  CKS(ws_tmap(&z.tm_cy, z.cy, Bc, d));
+  CKS(ws_tmap(&z.tm_cg, z.cg, Bc, d));
+  CKS(ws_tmap(&z.tm_ch1, z.ch1, Bc, d));
+  CKS(ws_tmap(&z.tm_ca, z.ca, Bc, d));
+  CKS(ws_tmap(&z.tm_cx1, z.cx1, Bc, d));
+  CKS(ws_tmap(&z.tm_cctxd, z.cctxd, Bc, d));
+  CKS(ws_tmap(&z.tm_cx2, z.cx2, Bc, d));
+  CKS(ws_tmap(&z.tm_chd, z.chd, Bc, F));
+  return MNMT_OK;
+}
+
+// ------------------------------------------------------------------ launch helpers
+static cudaError_t gemm(mnmt_model* m, const CUtensorMap& tmA, const Lin& W, int M,
+                        const int32_t* M_dyn, int epi, float* out_f, int8_t* out_q, int64_t ldo,
+                        unsigned long long* keys = nullptr, int col_block = 0,
+                        int64_t block_stride = 0) {
+  GemmArgs a{};
+  a.M = M;
+  a.M_dyn = M_dyn;
+  a.N = W.out;
+  a.K = W.in;
+  a.scale = scale_of(m);
+  a.bias = W.b;
+  a.clip = m->c.clip;
+  a.sigma = sigma_of(m);
+  a.out_f = out_f;
+  a.out_q = out_q;
+  a.ldo = ldo;
+  a.col_block = col_block > 0 ? col_block : W.out;
+  a.block_stride = block_stride;
+  a.keys = keys;
+  return launch_gemm_i8(tmA, W.tm, a, epi, 0, m->st);
+}
+
+static LnArgs ln_args(mnmt_model* m, int n, const int32_t* n_dyn, const float* x,
+                      const float* delta, const float* gamma, const float* beta, float* out,
+                      int8_t* out_q) {
+  LnArgs a{};
+  a.n = n;
+  a.n_dyn = n_dyn;
+  a.ctrl = m->ws.ctrl;
+  a.live = m->ws.live;
+  a.d = m->c.d_model;
+  a.eps = m->c.ln_eps;
+  a.x = x;
+  a.delta = delta;
+  a.gamma = gamma;
+  a.beta = beta;
+  a.out = out;
+  a.out_q = out_q;
+  a.clip = m->c.clip;
+  a.sigma = sigma_of(m);
+  a.aan.clip = m->c.clip;
+  a.aan.sigma = sigma_of(m);
+  return a;
+}
+
+// AAN step of decoder layer l fused into the producer of that layer's input.
+static AanOut aan_for_layer(mnmt_model* m, int l) {
+  AanOut o{};
+  o.clip = m->c.clip;
+  o.sigma = sigma_of(m);
+  if (m->c.decoder != 1 || l >= m->c.dec_layers) return o;
+  const int64_t d = m->c.d_model;
+  o.C = m->ws.C + (int64_t)l * m->ws.B_cap * d;
+  if (m->c.aan_ffn_depth == 0) {
+    o.g_f = m->ws.g;                       // a = g (fp32) for the residual / gate
+    if (m->c.aan_gate) o.g_q = m->ws.cg;   // Q(a) = Q(g) feeds the f-gate
+  } else {
+    o.g_q = m->ws.cg;                      // Q(g) feeds the AAN FFN
+  }
+  return o;
+}
+
+// Encoder over M tokens (A2-A4).  meta: [idx M][pos M][start M][len M].
+static cudaError_t launch_encoder(mnmt_model* m, int M, const int32_t* tok_idx,
+                                  const int32_t* tok_pos, const int32_t* tok_start,
+                                  const int32_t* tok_len, int64_t* nlaunch) {
+  auto& w = m->ws;
+  const auto& c = m->c;
+  const int d = c.d_model;
+  cudaError_t e;
+  if ((e = launch_embed_src(w.src_ids, tok_idx, tok_pos, M, m->E, m->PE, d, c.clip, w.x, w.cx,
+                            m->st)) != cudaSuccess)
+    return e;
+  ++*nlaunch;
+  for (int l = 0; l < c.enc_layers; ++l) {
+    const EncLayer& E = m->enc[l];
+    if ((e = gemm(m, w.tm_cx, E.qkv, M, nullptr, EPI_F32, w.qkv, nullptr, 3 * d)) != cudaSuccess) return e;
+    AttnArgs at{};
+    at.mode = ATTN_ENC;
+    at.n = M;
+    at.H = c.n_heads;
+    at.dh = d / c.n_heads;
+    at.d = d;
+    at.q = w.qkv;
+    at.ldq = 3 * d;
+    at.kv = w.qkv;
+    at.ldkv = 3 * d;
+    at.k_off = d;
+    at.v_off = 2 * d;
+    at.kv_start = tok_start;
+    at.kv_len = tok_len;
+    at.clip = c.clip;
+    at.sigma = sigma_of(m);
+    at.out_q = w.cctx;
+    if ((e = launch_attn(at, m->st)) != cudaSuccess) return e;
+    if ((e = gemm(m, w.tm_cctx, E.o, M, nullptr, EPI_F32, w.o, nullptr, d)) != cudaSuccess) return e;
+    LnArgs la = ln_args(m, M, nullptr, w.x, w.o, E.ln1g, E.ln1b, w.x, w.cx);
+    if ((e = launch_ln(la, m->st)) != cudaSuccess) return e;
+    if ((e = gemm(m, w.tm_cx, E.f1, M, nullptr, EPI_RELU_Q, nullptr, w.ch, c.d_ffn)) != cudaSuccess) return e;
+    if ((e = gemm(m, w.tm_ch, E.f2, M, nullptr, EPI_F32, w.o, nullptr, d)) != cudaSuccess) return e;
+    LnArgs lb = ln_args(m, M, nullptr, w.x, w.o, E.ln2g, E.ln2b, w.x, w.cx);
+    if ((e = launch_ln(lb, m->st)) != cudaSuccess) return e;
+    *nlaunch += 7;
+  }
+  // Source keys/values of all decoder layers in one GEMM, scattered to [L][M_cap][2d].
+  if ((e = gemm(m, w.tm_cx, m->kv_all, M, nullptr, EPI_F32, w.kv, nullptr, 2 * d, nullptr, 2 * d,
+                w.M_cap * 2 * d)) != cudaSuccess)
+    return e;
+  ++*nlaunch;
+  return cudaSuccess;
+}
+
+// Dump hook for teacher-forced runs (called between kernels; never inside a graph).
+struct StepHook {
+  virtual ~StepHook() = default;
+  virtual cudaError_t layer(mnmt_model* m, int l) = 0;   // after LN3 of layer l
+  virtual cudaError_t x1(mnmt_model* m, int l) = 0;
+  virtual cudaError_t x2(mnmt_model* m, int l) = 0;
+};
+
+// One decoder step for up to `n` live rows (A5-A10).  Returns kernels launched via *nlaunch.
+static cudaError_t launch_step(mnmt_model* m, int n, bool forced, StepHook* hook,
+                               int64_t* nlaunch) {
+  auto& w = m->ws;
+  const auto& c = m->c;
+  const int d = c.d_model, L = c.dec_layers, H = c.n_heads;
+  const int32_t* nd = w.ctrl;  // ctrl[0] = live rows
+  cudaError_t e;
+  int64_t k = 0;
+  EmbedTgtArgs ea{};
+  ea.ctrl = w.ctrl;
+  ea.live = w.live;
+  ea.prev_id = w.prev_id;
+  ea.E = m->E;
+  ea.PE = m->PE;
+  ea.d = d;
+  ea.rsd = (float)std::sqrt((double)d);
+  ea.y = w.y;
+  ea.yq = w.cy;
+  ea.aan = aan_for_layer(m, 0);
+  if ((e = launch_embed_tgt(ea, n, m->st)) != cudaSuccess) return e;
+  ++k;
+  for (int l = 0; l < L; ++l) {
+    const DecLayer& D = m->dec[l];
+    LnArgs l1;
+    if (c.decoder == 1) {
+      // A6: AAN block. g (or its codes) was produced with this layer's input.
+      const float* a_f = w.g;
+      if (c.aan_ffn_depth == 2) {
+        if ((e = gemm(m, w.tm_cg, D.a1, n, nd, EPI_RELU_Q, nullptr, w.ch1, d)) != cudaSuccess) return e;
+        if ((e = gemm(m, w.tm_ch1, D.a2, n, nd, EPI_F32_Q, w.a, w.ca, d)) != cudaSuccess) return e;
+        a_f = w.a;
+        k += 2;
+      } else if (c.aan_ffn_depth == 1) {
+        if ((e = gemm(m, w.tm_cg, D.a1, n, nd, EPI_RELU_F32_Q, w.a, w.ca, d)) != cudaSuccess) return e;
+        a_f = w.a;
+        k += 1;
+      }
+      if (c.aan_gate) {
+        // gate (R8): i = sigmoid(W_i Q(y)), f = sigmoid(W_f Q(a)); for -ffn, Q(a) = Q(g)
+        const CUtensorMap& tm_a = c.aan_ffn_depth == 0 ? w.tm_cg : w.tm_ca;
+        if ((e = gemm(m, w.tm_cy, D.gi, n, nd, EPI_SIGMOID, w.gi, nullptr, d)) != cudaSuccess) return e;
+        if ((e = gemm(m, tm_a, D.gf, n, nd, EPI_SIGMOID, w.gf, nullptr, d)) != cudaSuccess) return e;
+        k += 2;
+        l1 = ln_args(m, n, nd, w.y, a_f, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
+        l1.gi = w.gi;
+        l1.gf = w.gf;
+      } else {
+        l1 = ln_args(m, n, nd, w.y, a_f, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
+      }
+    } else {
+      // A6': self-attention with a KV cache
+      if ((e = gemm(m, w.tm_cy, D.qkv, n, nd, EPI_F32, w.qkvd, nullptr, 3 * d)) != cudaSuccess) return e;
+      AttnArgs at{};
+      at.mode = ATTN_SELF;
+      at.n = n;
+      at.n_dyn = nd;
+      at.ctrl = w.ctrl;
+      at.live = w.live;
+      at.H = H;
+      at.dh = d / H;
+      at.d = d;
+      at.q = w.qkvd;
+      at.ldq = 3 * d;
+      at.kv = w.selfkv + (int64_t)l * w.B_cap * w.T_cap * 2 * d;
+      at.kv_w = const_cast<float*>(at.kv);
+      at.ldkv = 2 * d;
+      at.k_off = 0;
+      at.v_off = d;
+      at.t_cap = (int)w.T_cap;
+      at.clip = c.clip;
+      at.sigma = sigma_of(m);
+      at.out_q = w.cctxd;
+      if ((e = launch_attn(at, m->st)) != cudaSuccess) return e;
+      if ((e = gemm(m, w.tm_cctxd, D.o, n, nd, EPI_F32, w.od, nullptr, d)) != cudaSuccess) return e;
+      k += 3;
+      l1 = ln_args(m, n, nd, w.y, w.od, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
+    }
+    if ((e = launch_ln(l1, m->st)) != cudaSuccess) return e;
+    ++k;
+    if (hook && (e = hook->x1(m, l)) != cudaSuccess) return e;
+    // A7: source attention
+    if ((e = gemm(m, w.tm_cx1, D.sq, n, nd, EPI_F32, w.qs, nullptr, d)) != cudaSuccess) return e;
+    AttnArgs as{};
+    as.mode = ATTN_SRC;
+    as.n = n;
+    as.n_dyn = nd;
+    as.ctrl = w.ctrl;
+    as.live = w.live;
+    as.H = H;
+    as.dh = d / H;
+    as.d = d;
+    as.q = w.qs;
+    as.ldq = d;
+    as.kv = w.kv + (int64_t)l * w.M_cap * 2 * d;
+    as.ldkv = 2 * d;
+    as.k_off = 0;
+    as.v_off = d;
+    as.kv_start = w.row_start;
+    as.kv_len = w.row_len;
+    as.clip = c.clip;
+    as.sigma = sigma_of(m);
+    as.out_q = w.cctxd;
+    if ((e = launch_attn(as, m->st)) != cudaSuccess) return e;
+    if ((e = gemm(m, w.tm_cctxd, D.so, n, nd, EPI_F32, w.od, nullptr, d)) != cudaSuccess) return e;
+    LnArgs l2 = ln_args(m, n, nd, w.x1, w.od, D.ln[1][0], D.ln[1][1], w.x2, w.cx2);
+    if ((e = launch_ln(l2, m->st)) != cudaSuccess) return e;
+    k += 4;
+    if (hook && (e = hook->x2(m, l)) != cudaSuccess) return e;
+    // A8: FFN
+    if ((e = gemm(m, w.tm_cx2, D.f1, n, nd, EPI_RELU_Q, nullptr, w.chd, c.d_ffn)) != cudaSuccess) return e;
+    if ((e = gemm(m, w.tm_chd, D.f2, n, nd, EPI_F32, w.f, nullptr, d)) != cudaSuccess) return e;
+    LnArgs l3 = ln_args(m, n, nd, w.x2, w.f, D.ln[2][0], D.ln[2][1], w.y, w.cy);
+    l3.aan = aan_for_layer(m, l + 1);
+    if ((e = launch_ln(l3, m->st)) != cudaSuccess) return e;
+    k += 3;
+    if (hook && (e = hook->layer(m, l)) != cudaSuccess) return e;
+  }
+  // A9: tied output projection fused with the argmax (softmax skipped)
+  {
+    GemmArgs a{};
+    a.M = n;
+    a.M_dyn = nd;
+    a.N = c.vocab;
+    a.K = d;
+    a.scale = scale_of(m);
+    a.bias = c.out_bias ? m->out_b : nullptr;
+    a.clip = c.clip;
+    a.sigma = sigma_of(m);
+    a.col_block = c.vocab;
+    a.keys = w.keys;
+    if ((e = launch_gemm_i8(w.tm_cy, m->tmE, a, EPI_ARGMAX, 0, m->st)) != cudaSuccess) return e;
+  }
+  // A10: finish + compaction
+  FinishArgs fa{};
+  fa.ctrl = w.ctrl;
+  fa.live = w.live;
+  fa.keys = w.keys;
+  fa.prev_id = w.prev_id;
+  fa.max_len = w.max_len;
+  fa.out_off = w.out_off;
+  fa.out_ids = w.out_ids;
+  fa.out_len = w.out_len;
+  fa.len_idx = w.len_idx;
+  fa.eos = c.eos_id;
+  fa.forced = forced ? w.forced : nullptr;
+  fa.forced_off = forced ? w.forced_off : nullptr;
+  if ((e = launch_finish(fa, m->st)) != cudaSuccess) return e;
+  k += 2;
+  *nlaunch += k;
+  return cudaSuccess;
+}
+
+// ------------------------------------------------------------------ job planning
+struct Batch {
+  std::vector<int32_t> rows;  // sentence indices in row order
+  int64_t tok0 = 0;           // first token of this batch in the job's token metadata
+  int64_t M = 0;
+  int T = 0;                  // max steps
+};
+
+struct Job {
+  std::vector<Batch> batches;
+  std::vector<int32_t> meta;  // per batch: tok_idx, tok_pos, tok_start, tok_len (4 x M)
+  std::vector<int64_t> out_off;  // per sentence: output offset (prefix sum of max_len)
+  std::vector<int32_t> rmeta32;  // per batch: [row_start|row_len|max_len|len_idx] x B
+  std::vector<int64_t> rmeta64;  // per batch: [out_off|forced_off] x B
+  std::vector<int64_t> r0;       // per batch: first row in rmeta
+  int64_t out_total = 0, tok_total = 0, rows_total = 0;
+  int64_t maxM = 0, maxB = 0;
+  int maxT = 0;
+};
+
+static mnmt_status check_inputs(mnmt_model* m, const int64_t* src_off, int32_t n,
+                                const int32_t* max_len) {
+  if (n < 0) { set_err("n < 0"); return MNMT_ERR_ARG; }
+  if (n > 0 && (!src_off || !max_len)) { set_err("NULL src_off / max_len"); return MNMT_ERR_ARG; }
+  if (n > 0 && src_off[0] != 0) { set_err("src_off[0] must be 0"); return MNMT_ERR_ARG; }
+  for (int i = 0; i < n; ++i) {
+    const int64_t S = src_off[i + 1] - src_off[i];
+    if (S < 0) { set_err("src_off not monotone at %d", i); return MNMT_ERR_ARG; }
+    if (S > MNMT_MAX_SPAN) { set_err("sentence %d longer than MNMT_MAX_SPAN", i); return MNMT_ERR_CAPACITY; }
+    if (max_len[i] < 0) { set_err("max_len[%d] < 0", i); return MNMT_ERR_ARG; }
+    if (max_len[i] > MNMT_MAX_SPAN) { set_err("max_len[%d] > MNMT_MAX_SPAN", i); return MNMT_ERR_CAPACITY; }
+  }
+  return MNMT_OK;
+}
+
+static void plan_job(const int64_t* src_off, int32_t n, const int32_t* max_len,
+                     const std::vector<std::vector<int32_t>>& batch_rows, Job& job) {
+  job.out_off.assign(n + 1, 0);
+  for (int i = 0; i < n; ++i) job.out_off[i + 1] = job.out_off[i] + max_len[i];
+  job.out_total = job.out_off[n];
+  job.tok_total = n > 0 ? src_off[n] : 0;
+  for (const auto& rows_all : batch_rows) {
+    Batch b;
+    for (int32_t s : rows_all)
+      if (max_len[s] > 0) b.rows.push_back(s);   // max_len 0: nothing to decode
+    if (b.rows.empty()) continue;
+    b.tok0 = (int64_t)job.meta.size();
+    int64_t M = 0;
+    for (int32_t s : b.rows) {
+      M += src_off[s + 1] - src_off[s];
+      b.T = std::max(b.T, max_len[s]);
+    }
+    b.M = M;
+    job.meta.resize(job.meta.size() + 4 * M);
+    int32_t* idx = job.meta.data() + b.tok0;
+    int32_t *pos = idx + M, *st = idx + 2 * M, *ln = idx + 3 * M;
+    int64_t t = 0;
+    for (int32_t s : b.rows) {
+      const int64_t S = src_off[s + 1] - src_off[s];
+      for (int64_t j = 0; j < S; ++j) {
+        idx[t + j] = (int32_t)(src_off[s] + j);
+        pos[t + j] = (int32_t)j;
+        st[t + j] = (int32_t)t;
+        ln[t + j] = (int32_t)S;
+      }
+      t += S;
+    }
+    job.maxM = std::max(job.maxM, M);
+    job.maxB = std::max<int64_t>(job.maxB, (int64_t)b.rows.size());
+    job.maxT = std::max(job.maxT, b.T);
+    job.batches.push_back(std::move(b));
+  }
+}
+
+// Row metadata of every batch, staged host-side once per job (uploaded in one copy).
+static void plan_rows(Job& job, const int64_t* src_off, const int32_t* max_len, bool forced,
+                      const int64_t* forced_off) {
+  job.rmeta32.clear();
+  job.rmeta64.clear();
+  job.r0.clear();
+  int64_t r0 = 0;
+  for (const Batch& b : job.batches) {
+    const int B = (int)b.rows.size();
+    job.r0.push_back(r0);
+    job.rmeta32.resize((size_t)4 * (r0 + B));
+    job.rmeta64.resize((size_t)2 * (r0 + B));
+    int32_t* rs = job.rmeta32.data() + 4 * r0;
+    int32_t *rl = rs + B, *ml = rs + 2 * B, *li = rs + 3 * B;
+    int64_t* oo = job.rmeta64.data() + 2 * r0;
+    int64_t* fo = oo + B;
+    int64_t t = 0;
+    for (int r = 0; r < B; ++r) {
+      const int s = b.rows[r];
+      const int64_t S = src_off[s + 1] - src_off[s];
+      rs[r] = (int32_t)t;
+      rl[r] = (int32_t)S;
+      ml[r] = max_len[s];
+      li[r] = s;
+      oo[r] = job.out_off[s];
+      fo[r] = forced ? forced_off[s] : 0;
+      t += S;
+    }
+    r0 += B;
+  }
+  job.rows_total = r0;
+}
+
+// Runs every batch of a job on m->st.  Source ids must already be in ws.src_ids and
+// the metadata in ws.meta / ws.rmeta* (upload_job).
+static mnmt_status upload_job(mnmt_model* m, const Job& job) {
+  auto& w = m->ws;
+  if (!job.meta.empty())
+    CK(cudaMemcpyAsync(w.meta, job.meta.data(), job.meta.size() * 4, cudaMemcpyHostToDevice, m->st));
+  if (!job.rmeta32.empty()) {
+    CK(cudaMemcpyAsync(w.rmeta32, job.rmeta32.data(), job.rmeta32.size() * 4, cudaMemcpyHostToDevice, m->st));
+    CK(cudaMemcpyAsync(w.rmeta64, job.rmeta64.data(), job.rmeta64.size() * 8, cudaMemcpyHostToDevice, m->st));
+  }
+  m->stats.h2d_bytes += (int64_t)job.meta.size() * 4 + (int64_t)job.rmeta32.size() * 4 +
+                        (int64_t)job.rmeta64.size() * 8;
+  // pageable host memory: the copies above are staged before cudaMemcpyAsync returns
+  return MNMT_OK;
+}
+
+static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook* hook,
+                           bool use_graphs) {
+  auto& w = m->ws;
+  const auto& c = m->c;
+  const int64_t d = c.d_model;
+  int64_t launches = 0, steps = 0;
+  for (size_t bi = 0; bi < job.batches.size(); ++bi) {
+    const Batch& b = job.batches[bi];
+    const int B = (int)b.rows.size();
+    const int32_t* r32 = w.rmeta32 + 4 * job.r0[bi];
+    const int64_t* r64 = w.rmeta64 + 2 * job.r0[bi];
+    CK(cudaMemcpyAsync(w.row_start, r32, B * 4, cudaMemcpyDeviceToDevice, m->st));
+    CK(cudaMemcpyAsync(w.row_len, r32 + B, B * 4, cudaMemcpyDeviceToDevice, m->st));
+    CK(cudaMemcpyAsync(w.max_len, r32 + 2 * B, B * 4, cudaMemcpyDeviceToDevice, m->st));
+    CK(cudaMemcpyAsync(w.len_idx, r32 + 3 * B, B * 4, cudaMemcpyDeviceToDevice, m->st));
+    CK(cudaMemcpyAsync(w.out_off, r64, B * 8, cudaMemcpyDeviceToDevice, m->st));
+    if (forced) CK(cudaMemcpyAsync(w.forced_off, r64 + B, B * 8, cudaMemcpyDeviceToDevice, m->st));
+    const int32_t* base = w.meta + b.tok0;
+    const int M = (int)b.M;
+    CK(launch_encoder(m, M, base, base + M, base + 2 * M, base + 3 * M, &launches));
+    if (c.decoder == 1)
+      CK(cudaMemsetAsync(w.C, 0, (size_t)c.dec_layers * w.B_cap * d * sizeof(float), m->st));
+    CK(launch_decode_init(w.ctrl, w.live, B, w.keys, m->st));
+    launches += 1;
+    const int npad = (B + 127) / 128 * 128;
+    if (use_graphs && !hook) {
+      auto it = m->graphs.find(npad);
+      if (it == m->graphs.end()) {
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
+        int64_t per_step = 0;
+        cudaError_t e = launch_step(m, npad, forced, nullptr, &per_step);
+        cudaError_t e2 = cudaStreamEndCapture(m->st, &g);
+        CK(e);
+        CK(e2);
+        cudaGraphExec_t ge;
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        cudaGraphDestroy(g);
+        it = m->graphs.emplace(npad, ge).first;
+        m->launches_per_step = per_step;
+      }
+      for (int t = 0; t < b.T; ++t) CK(cudaGraphLaunch(it->second, m->st));
+      launches += (int64_t)b.T * m->launches_per_step;
+    } else {
+      for (int t = 0; t < b.T; ++t) CK(launch_step(m, npad, forced, hook, &launches));
+    }
+    steps += b.T;
+  }
+  m->stats.gpu_launches += launches;
+  m->stats.decode_steps += steps;
+  m->stats.batches += (int64_t)job.batches.size();
+  return MNMT_OK;
+}
+
+static mnmt_status begin_call(mnmt_model* m, void* cuda_stream) {
+  if (m->failed) { set_err("handle is fail-stopped after an earlier CUDA error"); return MNMT_ERR_STATE; }
+  if (!m->quantized) { set_err("decode before mnmt_model_quantize"); return MNMT_ERR_STATE; }
+  m->stats = mnmt_stats{};
+  CK(cudaEventRecord(m->ev_in, (cudaStream_t)cuda_stream));
+  CK(cudaStreamWaitEvent(m->st, m->ev_in, 0));
+  return MNMT_OK;
+}
+
+static mnmt_status end_call(mnmt_model* m, void* cuda_stream) {
+  CK(cudaEventRecord(m->ev_out, m->st));
+  CK(cudaStreamWaitEvent((cudaStream_t)cuda_stream, m->ev_out, 0));
+  CK(cudaStreamSynchronize(m->st));
+  return MNMT_OK;
+}
+
+static mnmt_status check_ids_host(const mnmt_model* m, const int32_t* ids, int64_t n) {
+  for (int64_t i = 0; i < n; ++i)
+    if (ids[i] < 0 || ids[i] >= m->c.vocab) {
+      set_err("token id %d at %lld out of range [0, %d)", ids[i], (long long)i, m->c.vocab);
+      return MNMT_ERR_VOCAB;
+    }
+  return MNMT_OK;
+}
+
+// Device-side id validation (DEVICE_IO mode): counts out-of-range ids.
+__global__ void k_count_bad_ids(const int32_t* ids, int64_t n, int V, int32_t* bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (ids[i] < 0 || ids[i] >= V) atomicAdd(bad, 1);
+}
+
+}  // namespace
+
+// ======================================================================== C ABI
+extern "C" {
+
+void mnmt_config_default(mnmt_config* c, int32_t d_model, int32_t d_ffn, int32_t n_heads) {
+  if (!c) return;
+  c->abi_version = MNMT_ABI_VERSION;
+  c->d_model = d_model;
+  c->d_ffn = d_ffn;
+  c->n_heads = n_heads;
+  c->enc_layers = 6;
+  c->dec_layers = 6;
+  c->vocab = 36000;
+  c->decoder = 1;
+  c->aan_ffn_depth = 2;
+  c->aan_gate = 1;
+  c->out_bias = 1;
+  c->eos_id = 0;
+  c->clip = 2.0f;
+  c->ln_eps = 1e-6f;
+}
+
+mnmt_status mnmt_model_create(const mnmt_config* cfg, int32_t cuda_device, mnmt_model** out) {
+  if (!out) { set_err("out is NULL"); return MNMT_ERR_ARG; }
+  *out = nullptr;
+  if (const char* p = cfg_problem(cfg)) { set_err("bad config: %s", p); return MNMT_ERR_ARG; }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev) {
+    cudaGetLastError();
+    set_err("CUDA device %d not available", cuda_device);
+    return MNMT_ERR_CUDA;
+  }
+  DeviceGuard g(cuda_device);
+  if (cudaError_t e = gemm_init(); e != cudaSuccess) {
+    set_err("GEMM init failed: %s", cudaGetErrorString(e));
+    return MNMT_ERR_CUDA;
+  }
+  mnmt_model* m = new mnmt_model();
+  m->c = *cfg;
+  m->dev = cuda_device;
+  build_manifest(m);
+  if (cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&m->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&m->ev_out, cudaEventDisableTiming) != cudaSuccess) {
+    set_err("stream/event creation failed");
+    delete m;
+    return MNMT_ERR_CUDA;
+  }
+  *out = m;
+  return MNMT_OK;
+}
+
+mnmt_status mnmt_model_set_param(mnmt_model* m, const char* name, const float* host,
+                                 int64_t numel) {
+  if (!m || !name || (!host && numel > 0)) { set_err("NULL argument"); return MNMT_ERR_ARG; }
+  if (m->failed) { set_err("handle is fail-stopped"); return MNMT_ERR_STATE; }
+  if (m->quantized) { set_err("set_param after quantize (weights are immutable)"); return MNMT_ERR_STATE; }
+  auto it = m->manifest.find(name);
+  if (it == m->manifest.end()) { set_err("unknown parameter '%s' for this config", name); return MNMT_ERR_DIM; }
+  if (it->second != numel) {
+    set_err("parameter '%s': numel %lld, expected %lld", name, (long long)numel, (long long)it->second);
+    return MNMT_ERR_DIM;
+  }
+  m->host[name].assign(host, host + numel);
+  return MNMT_OK;
+}
+
+mnmt_status mnmt_model_quantize(mnmt_model* m) {
+  if (!m) { set_err("NULL model"); return MNMT_ERR_ARG; }
+  if (m->failed) { set_err("handle is fail-stopped"); return MNMT_ERR_STATE; }
+  if (m->quantized) { set_err("already quantized"); return MNMT_ERR_STATE; }
+  std::string missing;
+  for (const auto& kv : m->manifest)
+    if (!m->host.count(kv.first)) missing += (missing.empty() ? "" : ", ") + kv.first;
+  if (!missing.empty()) {
+    if (missing.size() > 900) missing = missing.substr(0, 900) + "...";
+    set_err("missing parameters: %s", missing.c_str());
+    return MNMT_ERR_STATE;
+  }
+  DeviceGuard g(m->dev);
+  const auto& c = m->c;
+  const int d = c.d_model, F = c.d_ffn, L = c.dec_layers;
+  mnmt_status s;
+  float* tmp = nullptr;
+  int64_t tmp_n = std::max<int64_t>((int64_t)c.vocab * d, (int64_t)F * d);
+  if ((s = dmalloc(m->allocs, reinterpret_cast<void**>(&tmp), tmp_n * 4)) != MNMT_OK) return s;
+  auto done = [&](mnmt_status st) { return fail(m, st); };
+  // tied embedding: fp32 for gathers (A2/A5), int8 codes for the output layer (A9)
+  if ((s = upload_vec(m, &m->E, "emb.E")) != MNMT_OK) return done(s);
+  if ((s = dalloc(m->allocs, &m->qE, (int64_t)c.vocab * d)) != MNMT_OK) return done(s);
+  if (launch_quantize(m->E, (int64_t)c.vocab * d, c.clip, m->qE, m->st) != cudaSuccess) {
+    set_err("quantize launch failed");
+    return done(MNMT_ERR_CUDA);
+  }
+  if (!make_tmap_i8(&m->tmE, m->qE, c.vocab, d)) { set_err("tensor map (E) failed"); return done(MNMT_ERR_CUDA); }
+  if (c.out_bias && (s = upload_vec(m, &m->out_b, "out.b")) != MNMT_OK) return done(s);
+  if ((s = dalloc(m->allocs, &m->PE, (int64_t)m->max_pos * d)) != MNMT_OK) return done(s);
+  if (launch_pe_table(m->PE, m->max_pos, d, m->st) != cudaSuccess) { set_err("PE launch failed"); return done(MNMT_ERR_CUDA); }
+  m->enc.resize(c.enc_layers);
+  m->dec.resize(L);
+  for (int l = 0; l < c.enc_layers; ++l) {
+    const std::string p = "enc." + std::to_string(l) + ".";
+    EncLayer& E = m->enc[l];
+    if ((s = prep_lin(m, E.qkv, {p + "self.q", p + "self.k", p + "self.v"}, d, d, tmp)) != MNMT_OK) return done(s);
+    if ((s = prep_lin(m, E.o, {p + "self.o"}, d, d, tmp)) != MNMT_OK) return done(s);
+    if ((s = prep_lin(m, E.f1, {p + "ffn.1"}, F, d, tmp)) != MNMT_OK) return done(s);
+    if ((s = prep_lin(m, E.f2, {p + "ffn.2"}, d, F, tmp)) != MNMT_OK) return done(s);
+    if ((s = upload_vec(m, &E.ln1g, p + "ln1.g")) != MNMT_OK) return done(s);
+    if ((s = upload_vec(m, &E.ln1b, p + "ln1.b")) != MNMT_OK) return done(s);
+    if ((s = upload_vec(m, &E.ln2g, p + "ln2.g")) != MNMT_OK) return done(s);
+    if ((s = upload_vec(m, &E.ln2b, p + "ln2.b")) != MNMT_OK) return done(s);
+  }
+  std::vector<std::string> kv_names;
+  for (int l = 0; l < L; ++l) {
+    const std::string p = "dec." + std::to_string(l) + ".";
+    DecLayer& D = m->dec[l];
+    if (c.decoder == 1) {
+      if (c.aan_ffn_depth >= 1 && (s = prep_lin(m, D.a1, {p + "aan.ffn.1"}, d, d, tmp)) != MNMT_OK) return done(s);
+      if (c.aan_ffn_depth >= 2 && (s = prep_lin(m, D.a2, {p + "aan.ffn.2"}, d, d, tmp)) != MNMT_OK) return done(s);
+      if (c.aan_gate) {
+        if ((s = prep_lin(m, D.gi, {p + "aan.gate.i"}, d, d, tmp)) != MNMT_OK) return done(s);
+        if ((s = prep_lin(m, D.gf, {p + "aan.gate.f"}, d, d, tmp)) != MNMT_OK) return done(s);
+      }
+    } else {
+      if ((s = prep_lin(m, D.qkv, {p + "self.q", p + "self.k", p + "self.v"}, d, d, tmp)) != MNMT_OK) return done(s);
+      if ((s = prep_lin(m, D.o, {p + "self.o"}, d, d, tmp)) != MNMT_OK) return done(s);
+    }
+    if ((s = prep_lin(m, D.sq, {p + "src.q"}, d, d, tmp)) != MNMT_OK) return done(s);
+    if ((s = prep_lin(m, D.so, {p + "src.o"}, d, d, tmp)) != MNMT_OK) return done(s);
+    if ((s = prep_lin(m, D.f1, {p + "ffn.1"}, F, d, tmp)) != MNMT_OK) return done(s);
+    if ((s = prep_lin(m, D.f2, {p + "ffn.2"}, d, F, tmp)) != MNMT_OK) return done(s);
+    for (int i = 0; i < 3; ++i) {
+      const std::string ln = p + "ln" + std::to_string(i + 1);
+      if ((s = upload_vec(m, &D.ln[i][0], ln + ".g")) != MNMT_OK) return done(s);
+      if ((s = upload_vec(m, &D.ln[i][1], ln + ".b")) != MNMT_OK) return done(s);
+    }
+    kv_names.push_back(p + "src.k");
+    kv_names.push_back(p + "src.v");
+  }
+  if ((s = prep_lin(m, m->kv_all, kv_names, d, d, tmp)) != MNMT_OK) return done(s);
+  if (cudaStreamSynchronize(m->st) != cudaSuccess) {
+    set_err("weight preparation failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return done(MNMT_ERR_CUDA);
+  }
+  cudaFree(tmp);
+  m->allocs.erase(std::remove(m->allocs.begin(), m->allocs.end(), (void*)tmp), m->allocs.end());
+  m->host.clear();
+  m->quantized = true;
+  return MNMT_OK;
+}
+
+mnmt_status mnmt_batch_by_words(const int32_t* len, int32_t n, int32_t budget, int32_t* order,
+                                int32_t* off, int32_t* n_batches) {
+  if (budget < 1) { set_err("word_budget < 1"); return MNMT_ERR_ARG; }
+  if (n < 0) { set_err("n < 0"); return MNMT_ERR_ARG; }
+  if (!off || !n_batches || (n > 0 && (!len || !order))) { set_err("NULL argument"); return MNMT_ERR_ARG; }
+  std::vector<int32_t> idx(n);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) { return len[a] < len[b]; });
+  int nb = 0;
+  int64_t words = 0;
+  off[0] = 0;
+  for (int i = 0; i < n; ++i) {
+    order[i] = idx[i];
+    words += len[idx[i]];
+    if (words >= budget) {
+      off[++nb] = i + 1;
+      words = 0;
+    }
+  }
+  if (n > 0 && off[nb] != n) off[++nb] = n;
+  *n_batches = nb;
+  return MNMT_OK;
+}
+
+static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const int64_t* src_off,
+                                  int32_t n, const int32_t* max_len, int32_t budget,
+                                  bool sorted_batches, int32_t* out_ids, int64_t out_cap,
+                                  int32_t* out_len, uint32_t flags, void* cuda_stream) {
+  if (!m) { set_err("NULL model"); return MNMT_ERR_ARG; }
+  mnmt_status s;
+  if ((s = check_inputs(m, src_off, n, max_len)) != MNMT_OK) return s;
+  const bool dev_io = (flags & MNMT_DEVICE_IO) != 0;
+  int64_t O = 0, ntok = n > 0 ? src_off[n] : 0;
+  for (int i = 0; i < n; ++i) O += max_len[i];
+  if (out_cap < O) { set_err("out_cap %lld < sum(max_len) %lld", (long long)out_cap, (long long)O); return MNMT_ERR_CAPACITY; }
+  if (n > 0 && (!src_ids && ntok > 0)) { set_err("NULL src_ids"); return MNMT_ERR_ARG; }
+  if (n > 0 && (!out_len || (!out_ids && O > 0))) { set_err("NULL outputs"); return MNMT_ERR_ARG; }
+  if (!dev_io && (s = check_ids_host(m, src_ids, ntok)) != MNMT_OK) return s;
+  DeviceGuard g(m->dev);
+  if ((s = begin_call(m, cuda_stream)) != MNMT_OK) return fail(m, s);
+  std::vector<std::vector<int32_t>> rows;
+  if (sorted_batches) {
+    if (budget < 1) { set_err("word_budget < 1"); return MNMT_ERR_ARG; }
+    std::vector<int32_t> L(n), order(std::max(n, 1)), off(n + 2);
+    for (int i = 0; i < n; ++i) L[i] = (int32_t)(src_off[i + 1] - src_off[i]);
+    int32_t nb = 0;
+    mnmt_batch_by_words(L.data(), n, budget, order.data(), off.data(), &nb);
+    for (int b = 0; b < nb; ++b) rows.emplace_back(order.begin() + off[b], order.begin() + off[b + 1]);
+  } else {
+    rows.emplace_back(n);
+    std::iota(rows[0].begin(), rows[0].end(), 0);
+  }
+  Job job;
+  plan_job(src_off, n, max_len, rows, job);
+  plan_rows(job, src_off, max_len, false, nullptr);
+  if ((s = ws_ensure(m, job.maxM, job.maxB, job.maxT, std::max<int64_t>(O, 1), std::max(n, 1),
+                     std::max<int64_t>(ntok, 1), (int64_t)job.meta.size(), job.rows_total)) != MNMT_OK)
+    return fail(m, s);
+  auto& w = m->ws;
+  if ((s = upload_job(m, job)) != MNMT_OK) return fail(m, s);
+  if (ntok > 0) {
+    CK(cudaMemcpyAsync(w.src_ids, src_ids, ntok * 4,
+                       dev_io ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, m->st));
+    if (!dev_io) m->stats.h2d_bytes += ntok * 4;
+  }
+  if (dev_io && ntok > 0) {
+    int32_t* bad = w.ctrl + 32;
+    CK(cudaMemsetAsync(bad, 0, 4, m->st));
+    k_count_bad_ids<<<148, 256, 0, m->st>>>(w.src_ids, ntok, m->c.vocab, bad);
+    int32_t hbad = 0;
+    CK(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, m->st));
+    CK(cudaStreamSynchronize(m->st));
+    if (hbad) { set_err("%d source ids out of range", hbad); return MNMT_ERR_VOCAB; }
+  }
+  CK(cudaMemsetAsync(w.out_len, 0, (size_t)n * 4, m->st));
+  if ((s = run_job(m, job, false, nullptr, true)) != MNMT_OK) return fail(m, s);
+  if (O > 0)
+    CK(cudaMemcpyAsync(out_ids, w.out_ids, O * 4, dev_io ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, m->st));
+  if (n > 0)
+    CK(cudaMemcpyAsync(out_len, w.out_len, (size_t)n * 4, dev_io ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, m->st));
+  if (!dev_io) m->stats.d2h_bytes += O * 4 + (int64_t)n * 4;
+  if ((s = end_call(m, cuda_stream)) != MNMT_OK) return fail(m, s);
+  if (!dev_io) {
+    int64_t words = 0;
+    for (int i = 0; i < n; ++i) words += out_len[i];
+    m->stats.target_words = words;
+  }
+  return MNMT_OK;
+}
+
+mnmt_status mnmt_decode(mnmt_model* m, const int32_t* src_ids, const int64_t* src_off, int32_t n,
+                        const int32_t* max_len, int32_t* out_ids, int64_t out_cap,
+                        int32_t* out_len, void* cuda_stream) {
+  return translate_impl(m, src_ids, src_off, n, max_len, 1, false, out_ids, out_cap, out_len, 0,
+                        cuda_stream);
+}
+
+mnmt_status mnmt_translate(mnmt_model* m, const int32_t* src_ids, const int64_t* src_off, int32_t n,
+                           const int32_t* max_len, int32_t budget, int32_t* out_ids,
+                           int64_t out_cap, int32_t* out_len, uint32_t flags, void* cuda_stream) {
+  if (budget < 1) { set_err("word_budget < 1"); return MNMT_ERR_ARG; }
+  return translate_impl(m, src_ids, src_off, n, max_len, budget, true, out_ids, out_cap, out_len,
+                        flags, cuda_stream);
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ teacher-forced dumps
+namespace {
+struct DumpHook : StepHook {
+  uint32_t mask = 0;
+  int n = 0;
+  const int64_t* foff = nullptr;   // forced offsets per sentence (host)
+  char* dec_out = nullptr;         // sections inside dump_host
+  char* out_codes = nullptr;
+  char* layers = nullptr;
+  std::vector<int32_t> live;
+  std::vector<float> buf;
+  std::vector<int8_t> cbuf;
+  int t = 0;                       // current step (1-based), tracked on host
+
+  cudaError_t fetch_live(mnmt_model* m, int* n_live) {
+    int32_t ctrl[2];
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(ctrl, m->ws.ctrl, 8, cudaMemcpyDeviceToHost, m->st)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(m->st)) != cudaSuccess) return e;
+    *n_live = ctrl[0];
+    t = ctrl[1];
+    live.resize(std::max(1, ctrl[0]));
+    if ((e = cudaMemcpyAsync(live.data(), m->ws.live, (size_t)ctrl[0] * 4, cudaMemcpyDeviceToHost, m->st)) != cudaSuccess) return e;
+    return cudaStreamSynchronize(m->st);
+  }
+  cudaError_t grab(mnmt_model* m, const float* src, char* base, int64_t row_elems, int64_t slot,
+                   int64_t slots) {
+    const int d = m->c.d_model;
+    int nl = 0;
+    cudaError_t e;
+    if ((e = fetch_live(m, &nl)) != cudaSuccess) return e;
+    buf.resize((size_t)std::max(1, nl) * d);
+    if ((e = cudaMemcpyAsync(buf.data(), src, (size_t)nl * d * 4, cudaMemcpyDeviceToHost, m->st)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(m->st)) != cudaSuccess) return e;
+    for (int r = 0; r < nl; ++r) {
+      const int64_t row = foff[live[r]] + t - 1;
+      std::memcpy(base + ((row * slots + slot) * row_elems) * 4, buf.data() + (size_t)r * d, (size_t)d * 4);
+    }
+    return cudaSuccess;
+  }
+  cudaError_t x1(mnmt_model* m, int l) override {
+    if (!(mask & MNMT_DUMP_LAYERS)) return cudaSuccess;
+    return grab(m, m->ws.x1, layers, m->c.d_model, (int64_t)l * 3 + 0, (int64_t)m->c.dec_layers * 3);
+  }
+  cudaError_t x2(mnmt_model* m, int l) override {
+    if (!(mask & MNMT_DUMP_LAYERS)) return cudaSuccess;
+    return grab(m, m->ws.x2, layers, m->c.d_model, (int64_t)l * 3 + 1, (int64_t)m->c.dec_layers * 3);
+  }
+  cudaError_t layer(mnmt_model* m, int l) override {
+    cudaError_t e;
+    const int d = m->c.d_model;
+    if (mask & MNMT_DUMP_LAYERS)
+      if ((e = grab(m, m->ws.y, layers, d, (int64_t)l * 3 + 2, (int64_t)m->c.dec_layers * 3)) != cudaSuccess) return e;
+    if (l != m->c.dec_layers - 1) return cudaSuccess;
+    if (mask & MNMT_DUMP_DEC_OUT)
+      if ((e = grab(m, m->ws.y, dec_out, d, 0, 1)) != cudaSuccess) return e;
+    if (mask & MNMT_DUMP_OUT_CODES) {
+      int nl = 0;
+      if ((e = fetch_live(m, &nl)) != cudaSuccess) return e;
+      cbuf.resize((size_t)std::max(1, nl) * d);
+      if ((e = cudaMemcpyAsync(cbuf.data(), m->ws.cy, (size_t)nl * d, cudaMemcpyDeviceToHost, m->st)) != cudaSuccess) return e;
+      if ((e = cudaStreamSynchronize(m->st)) != cudaSuccess) return e;
+      for (int r = 0; r < nl; ++r)
+        std::memcpy(out_codes + (foff[live[r]] + t - 1) * d, cbuf.data() + (size_t)r * d, d);
+    }
+    return cudaSuccess;
+  }
+};
+}  // namespace
+
+extern "C" mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids,
+                                          const int64_t* src_off, int32_t n,
+                                          const int32_t* forced_ids, const int64_t* forced_off,
+                                          int32_t* argmax_ids, uint32_t dump_mask,
+                                          void* dump_host, int64_t dump_cap, void* cuda_stream) {
+  if (!m) { set_err("NULL model"); return MNMT_ERR_ARG; }
+  if (n < 0 || (n > 0 && (!src_off || !forced_off))) { set_err("bad arguments"); return MNMT_ERR_ARG; }
+  std::vector<int32_t> ml(std::max(n, 1));
+  for (int i = 0; i < n; ++i) {
+    const int64_t T = forced_off[i + 1] - forced_off[i];
+    if (T < 0) { set_err("forced_off not monotone"); return MNMT_ERR_ARG; }
+    ml[i] = (int32_t)std::min<int64_t>(T, MNMT_MAX_SPAN + 1);
+  }
+  mnmt_status s;
+  if ((s = check_inputs(m, src_off, n, ml.data())) != MNMT_OK) return s;
+  const int64_t ntok = n > 0 ? src_off[n] : 0, O = n > 0 ? forced_off[n] : 0;
+  if (n > 0 && forced_off[0] != 0) { set_err("forced_off[0] must be 0"); return MNMT_ERR_ARG; }
+  if ((ntok > 0 && !src_ids) || (O > 0 && (!forced_ids || !argmax_ids))) { set_err("NULL arrays"); return MNMT_ERR_ARG; }
+  if ((s = check_ids_host(m, src_ids, ntok)) != MNMT_OK) return s;
+  if ((s = check_ids_host(m, forced_ids, O)) != MNMT_OK) return s;
+  const int64_t d = m->c.d_model, L = m->c.dec_layers;
+  int64_t need = 0;
+  if (dump_mask & MNMT_DUMP_ENC_OUT) need += ntok * d * 4;
+  if (dump_mask & MNMT_DUMP_SRC_KV) need += L * ntok * 2 * d * 4;
+  if (dump_mask & MNMT_DUMP_DEC_OUT) need += O * d * 4;
+  if (dump_mask & MNMT_DUMP_OUT_CODES) need += O * d;
+  if (dump_mask & MNMT_DUMP_LAYERS) need += O * L * 3 * d * 4;
+  if (need > 0 && (!dump_host || dump_cap < need)) { set_err("dump_cap %lld < %lld", (long long)dump_cap, (long long)need); return MNMT_ERR_CAPACITY; }
+  DeviceGuard g(m->dev);
+  if ((s = begin_call(m, cuda_stream)) != MNMT_OK) return fail(m, s);
+  std::vector<std::vector<int32_t>> rows(1, std::vector<int32_t>(n));
+  std::iota(rows[0].begin(), rows[0].end(), 0);
+  Job job;
+  plan_job(src_off, n, ml.data(), rows, job);
+  // forced_off doubles as the output offset in forced mode (out layout == forced layout)
+  job.out_off.assign(forced_off, forced_off + n + 1);
+  plan_rows(job, src_off, ml.data(), true, forced_off);
+  if ((s = ws_ensure(m, job.maxM, job.maxB, job.maxT, std::max<int64_t>(O, 1), std::max(n, 1),
+                     std::max<int64_t>(ntok, 1), (int64_t)job.meta.size(), job.rows_total)) != MNMT_OK)
+    return fail(m, s);
+  auto& w = m->ws;
+  if ((s = upload_job(m, job)) != MNMT_OK) return fail(m, s);
+  if (ntok > 0) CK(cudaMemcpyAsync(w.src_ids, src_ids, ntok * 4, cudaMemcpyHostToDevice, m->st));
+  if (O > 0) CK(cudaMemcpyAsync(w.forced, forced_ids, O * 4, cudaMemcpyHostToDevice, m->st));
+  CK(cudaMemsetAsync(w.out_len, 0, (size_t)std::max(n, 1) * 4, m->st));
+  char* p = static_cast<char*>(dump_host);
+  char* enc_out = nullptr;
+  char* src_kv = nullptr;
+  DumpHook hook;
+  hook.mask = dump_mask;
+  hook.n = n;
+  hook.foff = forced_off;
+  if (dump_mask & MNMT_DUMP_ENC_OUT) { enc_out = p; p += ntok * d * 4; }
+  if (dump_mask & MNMT_DUMP_SRC_KV) { src_kv = p; p += L * ntok * 2 * d * 4; }
+  if (dump_mask & MNMT_DUMP_DEC_OUT) { hook.dec_out = p; p += O * d * 4; }
+  if (dump_mask & MNMT_DUMP_OUT_CODES) { hook.out_codes = p; p += O * d; }
+  if (dump_mask & MNMT_DUMP_LAYERS) { hook.layers = p; p += O * L * 3 * d * 4; }
+  if ((s = run_job(m, job, true, &hook, false)) != MNMT_OK) return fail(m, s);
+  if (ntok > 0 && (enc_out || src_kv)) {
+    // the encoder buffers still hold the (single) batch: tokens are in sentence order
+    // only when every sentence has T_i > 0; otherwise rebuild per-sentence placement
+    int64_t t = 0;
+    for (int i = 0; i < n; ++i) {
+      const int64_t S = src_off[i + 1] - src_off[i];
+      if (ml[i] == 0 || S == 0) continue;
+      if (enc_out) CK(cudaMemcpyAsync(enc_out + src_off[i] * d * 4, w.x + t * d, S * d * 4, cudaMemcpyDeviceToHost, m->st));
+      if (src_kv)
+        for (int64_t l = 0; l < L; ++l)
+          CK(cudaMemcpyAsync(src_kv + ((l * ntok + src_off[i]) * 2 * d) * 4,
+                             w.kv + (l * w.M_cap + t) * 2 * d, S * 2 * d * 4, cudaMemcpyDeviceToHost, m->st));
+      t += S;
+    }
+  }
+  if (O > 0) CK(cudaMemcpyAsync(argmax_ids, w.out_ids, O * 4, cudaMemcpyDeviceToHost, m->st));
+  if ((s = end_call(m, cuda_stream)) != MNMT_OK) return fail(m, s);
+  return MNMT_OK;
+}
+
+extern "C" mnmt_status mnmt_get_stats(const mnmt_model* m, mnmt_stats* out) {
+  if (!m || !out) { set_err("NULL argument"); return MNMT_ERR_ARG; }
+  *out = m->stats;
+  return MNMT_OK;
+}
+
+extern "C" void mnmt_model_destroy(mnmt_model* m) {
+  if (!m) return;
+  {
+    DeviceGuard g(m->dev);
+    cudaStreamSynchronize(m->st);
+    ws_free(m);
+    for (void* p : m->allocs) cudaFree(p);
+    if (m->st) cudaStreamDestroy(m->st);
+    if (m->ev_in) cudaEventDestroy(m->ev_in);
+    if (m->ev_out) cudaEventDestroy(m->ev_out);
+    cudaGetLastError();
+  }
+  delete m;
+}

@@ -1,0 +1,165 @@
+// ops_api.cu — op-level C ABI (include/mnmt_ops.h): each decode-path kernel on caller memory.
+#include <cstdio>
+#include <string>
+
+#include "../../include/mnmt_ops.h"
+#include "kernels.h"
+#include "rowops.h"
+
+using namespace mnmt;
+
+// defined in mnmt.cu
+extern "C" const char* mnmt_last_error(void);
+void mnmt_set_error_str(const char* s);
+
+namespace {
+mnmt_status cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return MNMT_OK;
+  char buf[512];
+  snprintf(buf, sizeof buf, "%s: %s", what, cudaGetErrorString(e));
+  mnmt_set_error_str(buf);
+  return MNMT_ERR_CUDA;
+}
+mnmt_status arg_error(const char* what) {
+  mnmt_set_error_str(what);
+  return MNMT_ERR_ARG;
+}
+float sigma_of(float clip) { return 127.0f / clip; }
+}  // namespace
+
+extern "C" {
+
+mnmt_status mnmt_op_quantize(const float* x, int64_t n, float clip, int8_t* out, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !out)) || !(clip > 0.0f)) return arg_error("mnmt_op_quantize: bad arguments");
+  return cuda_status(launch_quantize(x, n, clip, out, (cudaStream_t)stream), "quantize");
+}
+
+mnmt_status mnmt_op_gemm_i8(const int8_t* A, const int8_t* W, int32_t M, int32_t N, int32_t K,
+                            const float* bias, float clip, int32_t epi, void* out, void* out2,
+                            int32_t n_tile, void* stream) {
+  if (!A || !W || !out || M < 1 || N < 1 || K < 16 || K % 16 || !(clip > 0.0f))
+    return arg_error("mnmt_op_gemm_i8: bad arguments (K must be a positive multiple of 16)");
+  if (epi < MNMT_EPI_F32 || epi > MNMT_EPI_ACC) return arg_error("mnmt_op_gemm_i8: bad epilogue");
+  if (epi != MNMT_EPI_ARGMAX && N % 16) return arg_error("mnmt_op_gemm_i8: N % 16 != 0");
+  if ((epi == MNMT_EPI_F32_Q || epi == MNMT_EPI_RELU_F32_Q) && !out2)
+    return arg_error("mnmt_op_gemm_i8: epilogue needs out2");
+  if (n_tile != 0 && n_tile != 64 && n_tile != 128 && n_tile != 256)
+    return arg_error("mnmt_op_gemm_i8: n_tile must be 0, 64, 128 or 256");
+  if (cudaError_t e = gemm_init(); e != cudaSuccess) return cuda_status(e, "gemm init");
+  CUtensorMap ta, tb;
+  if (!make_tmap_i8(&ta, A, M, K) || !make_tmap_i8(&tb, W, N, K))
+    return cuda_status(cudaErrorInvalidValue, "tensor map encode");
+  GemmArgs a{};
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.scale = (float)(((double)clip * (double)clip) / (127.0 * 127.0));
+  a.bias = bias;
+  a.clip = clip;
+  a.sigma = sigma_of(clip);
+  a.ldo = N;
+  a.col_block = N;
+  a.block_stride = 0;
+  switch (epi) {
+    case MNMT_EPI_F32:
+    case MNMT_EPI_SIGMOID: a.out_f = (float*)out; break;
+    case MNMT_EPI_F32_Q:
+    case MNMT_EPI_RELU_F32_Q: a.out_f = (float*)out; a.out_q = (int8_t*)out2; break;
+    case MNMT_EPI_RELU_Q: a.out_q = (int8_t*)out; break;
+    case MNMT_EPI_ARGMAX: a.keys = (unsigned long long*)out; break;
+    case MNMT_EPI_ACC: a.out_i = (int32_t*)out; break;
+  }
+  return cuda_status(launch_gemm_i8(ta, tb, a, epi, n_tile, (cudaStream_t)stream), "gemm_i8");
+}
+
+mnmt_status mnmt_op_argmax_ids(const uint64_t* keys, int32_t n, int32_t* ids, void* stream) {
+  if (n < 0 || (n > 0 && (!keys || !ids))) return arg_error("mnmt_op_argmax_ids: bad arguments");
+  return cuda_status(launch_argmax_ids((const unsigned long long*)keys, n, ids, (cudaStream_t)stream),
+                     "argmax_ids");
+}
+
+mnmt_status mnmt_op_layernorm(const float* x, const float* delta, const float* gi, const float* gf,
+                              const float* gamma, const float* beta, int32_t n, int32_t d,
+                              float eps, float clip, float* out, int8_t* out_q, void* stream) {
+  if (n < 0 || d < 4 || d % 4 || d > 1024 || !x || !delta || !gamma || !beta || (!out && !out_q) ||
+      ((gi == nullptr) != (gf == nullptr)) || !(clip > 0.0f))
+    return arg_error("mnmt_op_layernorm: bad arguments");
+  LnArgs a{};
+  a.n = n;
+  a.d = d;
+  a.eps = eps;
+  a.x = x;
+  a.delta = delta;
+  a.gi = gi;
+  a.gf = gf;
+  a.gamma = gamma;
+  a.beta = beta;
+  a.out = out;
+  a.out_q = out_q;
+  a.clip = clip;
+  a.sigma = sigma_of(clip);
+  return cuda_status(launch_ln(a, (cudaStream_t)stream), "layernorm");
+}
+
+mnmt_status mnmt_op_aan_step(float* C, const float* y, int32_t n, int32_t d, int32_t t, float clip,
+                             float* g, int8_t* g_q, void* stream) {
+  if (n < 0 || d < 4 || d % 4 || t < 1 || !C || !y || !(clip > 0.0f))
+    return arg_error("mnmt_op_aan_step: bad arguments");
+  AanOut o{};
+  o.C = C;
+  o.g_f = g;
+  o.g_q = g_q;
+  o.clip = clip;
+  o.sigma = sigma_of(clip);
+  return cuda_status(launch_aan_step_rows(C, y, n, d, t, o, (cudaStream_t)stream), "aan_step");
+}
+
+mnmt_status mnmt_op_embed(const float* E, int32_t d, const int32_t* ids, const int32_t* pos,
+                          int32_t n, float clip, float* x, int8_t* x_q, void* stream) {
+  if (n < 0 || d < 4 || d % 4 || d > 1024 || !E || !ids || !pos || !x || !x_q || !(clip > 0.0f))
+    return arg_error("mnmt_op_embed: bad arguments");
+  // positions come from a table of MNMT_MAX_SPAN + 1 rows built on the device
+  static thread_local float* pe = nullptr;
+  static thread_local int pe_d = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (pe_d != d) {
+    if (pe) cudaFree(pe);
+    pe = nullptr;
+    if (cudaMalloc(&pe, sizeof(float) * (size_t)(MNMT_MAX_SPAN + 1) * d) != cudaSuccess)
+      return cuda_status(cudaGetLastError(), "embed: PE table");
+    pe_d = d;
+    cudaError_t e = launch_pe_table(pe, MNMT_MAX_SPAN + 1, d, st);
+    if (e != cudaSuccess) return cuda_status(e, "embed: PE table");
+  }
+  return cuda_status(launch_embed_src(ids, nullptr, pos, n, E, pe, d, clip, x, x_q, st), "embed");
+}
+
+mnmt_status mnmt_op_attention(const float* q, int64_t ldq, const float* kv, int64_t ldkv,
+                              int32_t k_off, int32_t v_off, const int32_t* kv_start,
+                              const int32_t* kv_len, int32_t n, int32_t d, int32_t H, float clip,
+                              int8_t* out_q, float* out_f, void* stream) {
+  if (n < 0 || H < 1 || d % H || (d / H) % 4 || d / H > 64 || !q || !kv || !kv_start || !kv_len ||
+      !out_q || ldq % 4 || ldkv % 4 || k_off % 4 || v_off % 4 || !(clip > 0.0f))
+    return arg_error("mnmt_op_attention: bad arguments");
+  AttnArgs a{};
+  a.mode = ATTN_ENC;
+  a.n = n;
+  a.H = H;
+  a.dh = d / H;
+  a.d = d;
+  a.q = q;
+  a.ldq = ldq;
+  a.kv = kv;
+  a.ldkv = ldkv;
+  a.k_off = k_off;
+  a.v_off = v_off;
+  a.kv_start = kv_start;
+  a.kv_len = kv_len;
+  a.clip = clip;
+  a.sigma = sigma_of(clip);
+  a.out_q = out_q;
+  a.out_f = out_f;
+  return cuda_status(launch_attn(a, (cudaStream_t)stream), "attention");
+}
+
+}  // extern "C"

@@ -1,0 +1,105 @@
+// rowops.h — launch interface of the HBM-bound kernels (internal to libmnmt).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define MNMT_MAX_KV 512   // longest attended span (source length or decoder steps)
+
+namespace mnmt {
+
+// Optional "next layer AAN step" fused into a row kernel (R6/R7):
+// C[orig] <- fl(C + y); g = fl(C / t); writes g (fp32, for -ffn) and/or Q(g).
+struct AanOut {
+  float* C;          // [rows_cap x d] state of the layer being entered, indexed by orig row; null = off
+  float* g_f;        // compact [n x d] or null
+  int8_t* g_q;       // compact [n x d] or null
+  float clip, sigma;
+};
+
+struct EmbedTgtArgs {
+  const int32_t* ctrl;      // [0] = live rows, [1] = t
+  const int32_t* live;      // compact -> original row
+  const int32_t* prev_id;   // [orig] previous output id
+  const float* E;
+  const float* PE;
+  int d;
+  float rsd;                // fl32(sqrt d)
+  float* y;                 // compact [n x d]
+  int8_t* yq;
+  AanOut aan;
+};
+
+struct LnArgs {
+  int n;                    // static row bound
+  const int32_t* n_dyn;     // live rows (device) or null
+  const int32_t* ctrl;      // for t when aan.C is set
+  const int32_t* live;      // for orig when aan.C is set
+  int d;
+  float eps;
+  const float* x;           // residual input (for the gate form: y)
+  const float* delta;       // added to x (for the gate form: a)
+  const float* gi;          // gate form when non-null: r = x + (gi*x + gf*delta)
+  const float* gf;
+  const float* gamma;
+  const float* beta;
+  float* out;               // fp32 output or null
+  int8_t* out_q;            // Q(out) or null
+  float clip, sigma;
+  AanOut aan;
+};
+
+enum AttnMode : int { ATTN_ENC = 0, ATTN_SRC = 1, ATTN_SELF = 2 };
+
+struct AttnArgs {
+  int mode;
+  int n;                    // static row bound
+  const int32_t* n_dyn;
+  const int32_t* ctrl;      // t (self mode)
+  const int32_t* live;      // compact -> orig (src / self)
+  int H, dh, d;
+  const float* q;           // query rows, row stride ldq (self mode: the qkv rows)
+  int64_t ldq;
+  const float* kv;          // key/value rows, row stride ldkv; K at +k_off, V at +v_off
+  float* kv_w;              // self mode: writable cache (same as kv)
+  int64_t ldkv;
+  int k_off, v_off;
+  const int32_t* kv_start;  // enc: [row]; src: [orig]
+  const int32_t* kv_len;
+  int t_cap;                // self mode: cache rows per sentence
+  float clip, sigma;
+  int8_t* out_q;            // Q(ctx) [n x d]
+  float* out_f;             // optional fp32 ctx (tests)
+};
+
+struct FinishArgs {
+  int32_t* ctrl;
+  int32_t* live;
+  unsigned long long* keys;
+  int32_t* prev_id;
+  const int32_t* max_len;   // [orig]
+  const int64_t* out_off;   // [orig]
+  int32_t* out_ids;
+  int32_t* out_len;         // [len_idx[orig]] (len_idx null: [orig])
+  const int32_t* len_idx;   // batch row -> sentence index in the job
+  int eos;
+  const int32_t* forced;    // teacher forcing ids (flat) or null
+  const int64_t* forced_off;
+};
+
+cudaError_t launch_quantize(const float* x, int64_t n, float clip, int8_t* out, cudaStream_t st);
+cudaError_t launch_pe_table(float* pe, int max_pos, int d, cudaStream_t st);
+// x[i] = emb(ids[idx[i]], pos[i]) (idx may be null; id < 0 = zero vector) and Q(x).
+cudaError_t launch_embed_src(const int32_t* ids, const int32_t* idx, const int32_t* pos, int M,
+                             const float* E, const float* PE, int d, float clip, float* x,
+                             int8_t* xq, cudaStream_t st);
+cudaError_t launch_embed_tgt(const EmbedTgtArgs& a, int rows, cudaStream_t st);
+cudaError_t launch_ln(const LnArgs& a, cudaStream_t st);
+cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st);
+cudaError_t launch_finish(const FinishArgs& a, cudaStream_t st);
+cudaError_t launch_decode_init(int32_t* ctrl, int32_t* live, int B, unsigned long long* keys,
+                               cudaStream_t st);
+cudaError_t launch_aan_step_rows(float* C, const float* y, int n, int d, int t, const AanOut& o,
+                                 cudaStream_t st);
+cudaError_t launch_argmax_ids(const unsigned long long* keys, int n, int32_t* ids, cudaStream_t st);
+
+}  // namespace mnmt

@@ -1,0 +1,203 @@
+"""P-1: kernel parity with injected operands.  Every CUDA kernel gets the
+oracle's exact inputs through the op-level C-ABI (include/mnmt_ops.h) and is compared with
+the oracle: s32 accumulators, fmaf epilogues, codes and argmax bit-exactly; fp64-reduced
+floats (LN, attention) exactly up to rare last-bit double-rounding events."""
+import numpy as np
+import pytest
+
+import oracle.oracle as O
+import synth
+from tests.gpu_util import boundary_explained, empty, ptr, sync, to_dev, zeros
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1805_12096_b200 import mnmt as M  # noqa: E402
+
+CLIP = 2.0
+
+
+def rand_codes(shape, seed):
+    return np.random.default_rng(seed).integers(-127, 128, size=shape).astype(np.int8)
+
+
+# ------------------------------------------------------------------ quantizer (A1)
+def test_quantize_bitexact():
+    x = synth.uniform_activations((1 << 20,), seed=1, scale=3.0)
+    # add every exact half case k + 1/2 (R1) and the clip boundaries
+    halves = []
+    for k in range(-127, 127):
+        x0 = np.float32((k + 0.5) / 63.5)
+        for _ in range(3):
+            if np.float32(x0) * np.float32(63.5) == np.float32(k + 0.5):
+                halves.append(x0)
+            x0 = np.nextafter(x0, np.float32(np.inf), dtype=np.float32)
+    x = np.concatenate([x, np.array(halves, np.float32), np.array([2.0, -2.0, 0.0, -0.0, 1e9, -1e9], np.float32)])
+    xd = to_dev(x)
+    out = empty((x.size,), torch.int8)
+    M.op_quantize(ptr(xd), x.size, CLIP, ptr(out))
+    sync()
+    assert np.array_equal(out.cpu().numpy(), O.quantize(x, CLIP))
+
+
+# ------------------------------------------------------------------ int8 GEMM (A3, A4, A6-A9)
+GEMM_SHAPES = [
+    (1, 64, 64, 0), (4, 192, 192, 64), (130, 256, 192, 64), (300, 2048, 256, 128),
+    (257, 1536, 2048, 256), (383, 512, 1024, 0), (128, 6144, 512, 256), (77, 36000, 256, 256),
+    (520, 256, 2048, 128), (1000, 1024, 4096, 0),
+]
+
+
+@pytest.mark.parametrize("Mr,N,K,bn", GEMM_SHAPES)
+def test_gemm_acc_bitexact(Mr, N, K, bn):
+    a = rand_codes((Mr, K), Mr + K)
+    w = rand_codes((N, K), N + 7)
+    out = empty((Mr, N), torch.int32)
+    M.op_gemm_i8(ptr(to_dev(a)), ptr(to_dev(w)), Mr, N, K, None, CLIP, M.EPI_ACC, ptr(out), None, bn)
+    sync()
+    assert np.array_equal(out.cpu().numpy(), O.gemm_acc(a, w))
+
+
+@pytest.mark.parametrize("epi", [M.EPI_F32, M.EPI_F32_Q, M.EPI_RELU_Q, M.EPI_RELU_F32_Q, M.EPI_SIGMOID])
+@pytest.mark.parametrize("Mr,N,K", [(5, 256, 256), (260, 2048, 512), (131, 512, 2048)])
+def test_gemm_epilogues_bitexact(epi, Mr, N, K):
+    rng = np.random.default_rng(epi * 100 + Mr)
+    x = rng.normal(0, 1.0, size=(Mr, K)).astype(np.float32)
+    W = rng.uniform(-0.08, 0.08, size=(N, K)).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, size=N).astype(np.float32)
+    qa, qw = O.quantize(x), O.quantize(W)
+    v = O.linear(qa, qw, b, CLIP)                                   # oracle: fmaf((float)acc, s, b)
+    A, Wd, bd = to_dev(qa), to_dev(qw), to_dev(b)
+    of = empty((Mr, N), torch.float32)
+    oq = empty((Mr, N), torch.int8)
+    if epi == M.EPI_RELU_Q:
+        M.op_gemm_i8(ptr(A), ptr(Wd), Mr, N, K, ptr(bd), CLIP, epi, ptr(oq))
+    else:
+        M.op_gemm_i8(ptr(A), ptr(Wd), Mr, N, K, ptr(bd), CLIP, epi, ptr(of), ptr(oq))
+    sync()
+    if epi == M.EPI_F32:
+        assert np.array_equal(of.cpu().numpy(), v)
+    elif epi == M.EPI_F32_Q:
+        assert np.array_equal(of.cpu().numpy(), v)
+        assert np.array_equal(oq.cpu().numpy(), O.quantize(v))
+    elif epi == M.EPI_RELU_Q:
+        assert np.array_equal(oq.cpu().numpy(), O.quantize(np.maximum(v, np.float32(0))))
+    elif epi == M.EPI_RELU_F32_Q:
+        r = np.maximum(v, np.float32(0))
+        assert np.array_equal(of.cpu().numpy(), r)
+        assert np.array_equal(oq.cpu().numpy(), O.quantize(r))
+    else:
+        assert np.array_equal(of.cpu().numpy(), O.sigmoid_array(v))
+
+
+@pytest.mark.parametrize("Mr,N,K,bias", [(3, 50, 32, True), (200, 36000, 256, True),
+                                         (129, 36000, 192, False), (390, 36000, 512, True)])
+def test_gemm_argmax_bitexact_with_ties(Mr, N, K, bias):
+    rng = np.random.default_rng(Mr + N)
+    x = rng.normal(0, 1.0, size=(Mr, K)).astype(np.float32)
+    E = rng.uniform(-0.5, 0.5, size=(N, K)).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, size=N).astype(np.float32) if bias else None
+    qa, qE = O.quantize(x), O.quantize(E)
+    logits = O.linear(qa, qE, b, CLIP)
+    best = np.argmax(logits, axis=1)
+    # exact ties: copy each row's winner (code row and bias) to a LOWER and a HIGHER column
+    for i in range(0, Mr, 3):
+        j = int(best[i])
+        for j2 in ((j * 7 + 11) % N, (j + N // 2) % N):
+            if j2 != j:
+                qE[j2] = qE[j]
+                if b is not None:
+                    b[j2] = b[j]
+    logits = O.linear(qa, qE, b, CLIP)
+    ref = np.argmax(logits, axis=1)                   # first maximum = lowest id (R15)
+    keys = zeros((Mr,), torch.int64)
+    M.op_gemm_i8(ptr(to_dev(qa)), ptr(to_dev(qE)), Mr, N, K, ptr(to_dev(b)) if b is not None else None,
+                 CLIP, M.EPI_ARGMAX, ptr(keys))
+    ids = empty((Mr,), torch.int32)
+    M.op_argmax_ids(ptr(keys), Mr, ptr(ids))
+    sync()
+    assert np.array_equal(ids.cpu().numpy(), ref)
+
+
+# ------------------------------------------------------------------ LayerNorm (+gate) (A6-A8)
+@pytest.mark.parametrize("d", [192, 256, 512, 1024])
+@pytest.mark.parametrize("gate", [False, True])
+def test_layernorm(d, gate):
+    n = 333
+    x, dl = synth.uniform_activations((n, d), 1, 2.0), synth.uniform_activations((n, d), 2, 2.0)
+    g = synth.uniform_activations((d,), 3, 0.1) + np.float32(1)
+    b = synth.uniform_activations((d,), 4, 0.1)
+    gi = O.sigmoid_array(synth.uniform_activations((n, d), 5, 3.0)) if gate else None
+    gf = O.sigmoid_array(synth.uniform_activations((n, d), 6, 3.0)) if gate else None
+    ref = O.residual_ln(x, dl, g, b, 1e-6, gi, gf)
+    out = empty((n, d), torch.float32)
+    oq = empty((n, d), torch.int8)
+    M.op_layernorm(ptr(to_dev(x)), ptr(to_dev(dl)), ptr(to_dev(gi)) if gate else None,
+                   ptr(to_dev(gf)) if gate else None, ptr(to_dev(g)), ptr(to_dev(b)), n, d, 1e-6,
+                   CLIP, ptr(out), ptr(oq))
+    sync()
+    got = out.cpu().numpy()
+    assert np.mean(got == ref) > 0.9999
+    np.testing.assert_allclose(got, ref, rtol=1e-6, atol=1e-6)
+    assert not boundary_explained(ref, O.quantize(ref), oq.cpu().numpy()).any()
+
+
+# ------------------------------------------------------------------ AAN running sum (A6)
+def test_aan_step_bitexact():
+    n, d, T = 70, 256, 9
+    Y = synth.uniform_activations((T, n, d), 8, 3.0)
+    Cd = zeros((n, d), torch.float32)
+    g = empty((n, d), torch.float32)
+    gq = empty((n, d), torch.int8)
+    ref_G = np.stack([O.aan_average(Y[:, i, :]) for i in range(n)], axis=1)   # [T, n, d]
+    for t in range(T):
+        M.op_aan_step(ptr(Cd), ptr(to_dev(Y[t])), n, d, t + 1, CLIP, ptr(g), ptr(gq))
+        sync()
+        assert np.array_equal(g.cpu().numpy(), ref_G[t])
+        assert np.array_equal(gq.cpu().numpy(), O.quantize(ref_G[t]))
+
+
+# ------------------------------------------------------------------ embedding (A2, A5)
+@pytest.mark.parametrize("d", [192, 512])
+def test_embed_bitexact(d):
+    V = 1000
+    E = synth.uniform_activations((V, d), 9, 0.5)
+    rng = np.random.default_rng(d)
+    ids = rng.integers(-1, V, size=300).astype(np.int32)
+    pos = rng.integers(0, 512, size=300).astype(np.int32)
+    x = empty((300, d), torch.float32)
+    xq = empty((300, d), torch.int8)
+    M.op_embed(ptr(to_dev(E)), d, ptr(to_dev(ids)), ptr(to_dev(pos)), 300, CLIP, ptr(x), ptr(xq))
+    sync()
+    ref = O.embed_rows(E, ids, pos)
+    assert np.array_equal(x.cpu().numpy(), ref)
+    assert np.array_equal(xq.cpu().numpy(), O.quantize(ref))
+
+
+# ------------------------------------------------------------------ attention (A3, A7)
+@pytest.mark.parametrize("d,H", [(192, 8), (256, 8), (512, 8), (1024, 16)])
+def test_attention(d, H):
+    rng = np.random.default_rng(d + H)
+    lens = rng.integers(0, 101, size=40).astype(np.int32)
+    lens[0], lens[1] = 1, 100
+    starts = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int32)
+    S = int(lens.sum())
+    kv = rng.normal(0, 1, size=(S, 2 * d)).astype(np.float32)        # K | V per row
+    q = rng.normal(0, 1, size=(40, d)).astype(np.float32)
+    oq = empty((40, d), torch.int8)
+    of = empty((40, d), torch.float32)
+    M.op_attention(ptr(to_dev(q)), d, ptr(to_dev(kv)), 2 * d, 0, d, ptr(to_dev(starts)),
+                   ptr(to_dev(lens)), 40, d, H, CLIP, ptr(oq), ptr(of))
+    sync()
+    ref = np.zeros((40, d), np.float32)
+    for r in range(40):
+        if lens[r] > 0:
+            blk = kv[starts[r]:starts[r] + lens[r]]
+            ref[r] = O.attention(q[r], blk[:, :d], blk[:, d:], H)
+    got = of.cpu().numpy()
+    assert np.mean(got == ref) > 0.9999
+    np.testing.assert_allclose(got, ref, rtol=1e-6, atol=1e-7)
+    assert not boundary_explained(ref, O.quantize(ref), oq.cpu().numpy()).any()

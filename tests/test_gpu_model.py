@@ -1,0 +1,190 @@
+"""P-2/P-3/P-4: whole-pipeline parity of libmnmt against the CPU oracle.
+
+  * teacher-forced: per-step argmax ids bit-exact (near-ties flagged only when explained by
+    final-layer code flips), encoder output / source K,V / every decoder layer's x1,x2,x3
+    equal to the oracle's up to last-bit double-rounding events;
+  * free-running: whole-sequence agreement (required 100% on these sizes);
+  * invariance: ids identical across word budgets, batch composition and order.
+"""
+import numpy as np
+import pytest
+
+import oracle.oracle as O
+import synth
+from synth import ModelDims
+from tests.gpu_util import check_forced_steps
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1805_12096_b200 import mnmt as M  # noqa: E402
+
+TINY_VARIANTS = [
+    ModelDims("t-aan", 32, 64, 4, vocab=64, enc_layers=2, dec_layers=2),
+    ModelDims("t-ffn1", 32, 64, 4, vocab=64, enc_layers=2, dec_layers=2, aan_ffn_depth=1),
+    ModelDims("t-noffn-gate", 32, 64, 4, vocab=64, enc_layers=2, dec_layers=2, aan_ffn_depth=0),
+    ModelDims("t-noffn-nogate", 32, 64, 4, vocab=64, enc_layers=2, dec_layers=2,
+              aan_ffn_depth=0, aan_gate=0),
+    ModelDims("t-self", 32, 64, 4, vocab=64, enc_layers=2, dec_layers=2, decoder=0),
+    ModelDims("t-nobias-ragged-vocab", 48, 96, 4, vocab=50, enc_layers=1, dec_layers=3, out_bias=0),
+]
+
+
+def pair(dims, seed):
+    w = synth.make_weights(dims, seed=seed)
+    return w, O.OracleModel(dims, w), M.Model(dims, w)
+
+
+def forced_case(dims, n, lo, hi, T_lo, T_hi, seed):
+    ss = synth.random_set(n, lo, hi, seed=seed, vocab=dims.vocab)
+    rng = np.random.default_rng(seed + 1)
+    T = rng.integers(T_lo, T_hi + 1, size=n)
+    foff = np.zeros(n + 1, np.int64)
+    foff[1:] = np.cumsum(T)
+    forced = synth.forced_targets(T.tolist(), seed=seed + 2, vocab=dims.vocab)
+    return ss, forced, foff
+
+
+def run_forced_parity(dims, w, om, gm, ss, forced, foff, layers=True):
+    mask = M.DUMP_ENC_OUT | M.DUMP_SRC_KV | M.DUMP_DEC_OUT | M.DUMP_OUT_CODES
+    if layers:
+        mask |= M.DUMP_LAYERS
+    ids, dumps = gm.decode_forced(ss, forced, foff, mask)
+    qE = O.quantize(w["emb.E"])
+    s = O.dequant_scale(dims.clip)
+    tot = ex = fl = 0
+    for i in range(ss.n):
+        src = ss.ids[ss.offsets[i]:ss.offsets[i + 1]]
+        T = int(foff[i + 1] - foff[i])
+        f = forced[foff[i]:foff[i + 1]]
+        oids, tr = om.decode_one(src, T, forced=f, trace=True, layers=layers)
+        sl = slice(int(foff[i]), int(foff[i + 1]))
+        if len(src):
+            enc, kv = om.encode(src)
+            a, b = int(ss.offsets[i]), int(ss.offsets[i + 1])
+            np.testing.assert_allclose(dumps["enc_out"][a:b], enc, rtol=1e-6, atol=1e-6)
+            np.testing.assert_allclose(dumps["src_kv"][:, a:b].transpose(0, 2, 1, 3), kv, rtol=1e-6, atol=1e-6)
+        if T == 0:
+            continue
+        np.testing.assert_allclose(dumps["dec_out"][sl], tr["dec_out"], rtol=1e-5, atol=1e-5)
+        if layers:
+            np.testing.assert_allclose(dumps["layers"][sl], tr["layer_out"], rtol=1e-5, atol=1e-5)
+        n_, e_, f_ = check_forced_steps(ids[sl], dumps["out_codes"][sl], tr, qE, s)
+        tot += n_; ex += e_; fl += f_
+    return tot, ex, fl
+
+
+@pytest.mark.parametrize("dims", TINY_VARIANTS, ids=lambda d: d.name)
+def test_tiny_teacher_forced(dims):
+    w, om, gm = pair(dims, 11)
+    ss, forced, foff = forced_case(dims, 9, 0, 13, 0, 17, seed=3)
+    tot, ex, fl = run_forced_parity(dims, w, om, gm, ss, forced, foff)
+    assert ex == tot, f"{tot - ex} flagged near-ties"
+
+
+@pytest.mark.parametrize("dims", TINY_VARIANTS, ids=lambda d: d.name)
+def test_tiny_free_running(dims):
+    w, om, gm = pair(dims, 12)
+    ss = synth.random_set(17, 1, 15, seed=5, vocab=dims.vocab)
+    ref = om.decode_many(ss, 4)
+    got = gm.decode(ss)
+    assert all(np.array_equal(a, b) for a, b in zip(got, ref))
+
+
+def test_config0_tiny192_aan():
+    """BASELINE configs[0]: tiny-192 AAN, 36k vocab, 4 sentences of length 20."""
+    dims = synth.PRESETS["tiny192-aan"]
+    w, om, gm = pair(dims, 1)
+    ss = synth.uniform_set(4, 20, seed=7)
+    ref = om.decode_many(ss, 4)
+    got = gm.translate(ss, 8192)
+    assert all(np.array_equal(a, b) for a, b in zip(got, ref))
+    T = np.full(4, 20)
+    foff = np.concatenate([[0], np.cumsum(T)]).astype(np.int64)
+    forced = synth.forced_targets(T.tolist(), seed=9)
+    tot, ex, fl = run_forced_parity(dims, w, om, gm, ss, forced, foff, layers=True)
+    assert ex == tot
+
+
+def test_tiny192_noffn_nogate_eos_and_edges():
+    dims = synth.PRESETS["tiny192-aan-noffn-nogate"]
+    w = synth.make_weights(dims, seed=4)
+    w["out.b"] = w["out.b"].copy()
+    w["out.b"][dims.eos_id] = 0.35     # EOS wins sometimes: exercises stop + compaction
+    om, gm = O.OracleModel(dims, w), M.Model(dims, w)
+    ss = synth.random_set(40, 0, 30, seed=8)
+    ss.max_len[:] = np.random.default_rng(2).integers(0, 40, size=40)
+    ref = om.decode_many(ss, 4)
+    got = gm.translate(ss, 100)
+    assert all(np.array_equal(a, b) for a, b in zip(got, ref))
+    assert any(len(r) < m for r, m in zip(ref, ss.max_len)), "no sentence stopped at EOS"
+
+
+def test_batch_and_order_invariance():
+    dims = synth.PRESETS["tiny192-aan"]
+    w = synth.make_weights(dims, seed=2)
+    gm = M.Model(dims, w)
+    ss = synth.random_set(120, 1, 40, seed=21)
+    base = gm.translate(ss, 1 << 20)
+    for budget in (1, 64, 333, 4096):
+        assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, budget), base))
+    perm = np.random.default_rng(3).permutation(ss.n)
+    sub = gm.decode(ss.subset(perm))
+    assert all(np.array_equal(sub[k], base[perm[k]]) for k in range(ss.n))
+
+
+def test_errors_and_fail_fast():
+    dims = ModelDims("t", 32, 64, 4, vocab=64, enc_layers=1, dec_layers=1)
+    with pytest.raises(M.MnmtError) as e:
+        M.Model(ModelDims("bad", 30, 64, 4))
+    assert e.value.status == 1
+    gm = M.Model(dims)
+    with pytest.raises(M.MnmtError) as e:
+        gm.set_param("enc.0.self.q.W", np.zeros(7, np.float32))
+    assert e.value.status == 2
+    with pytest.raises(M.MnmtError) as e:
+        gm.decode(synth.uniform_set(1, 3, vocab=64))
+    assert e.value.status == 4                      # before quantize
+    with pytest.raises(M.MnmtError) as e:
+        gm.quantize()                               # missing parameters
+    assert e.value.status == 4
+    gm = M.Model(dims, synth.make_weights(dims, 1))
+    bad = synth.uniform_set(1, 3, vocab=64)
+    bad.ids[1] = 64
+    with pytest.raises(M.MnmtError) as e:
+        gm.decode(bad)
+    assert e.value.status == 3
+    with pytest.raises(M.MnmtError) as e:
+        gm.translate(synth.uniform_set(1, 3, vocab=64), 0)
+    assert e.value.status == 1
+
+
+# ------------------------------------------------------------------ full-size sampled parity
+def _sampled(dims, n_sample, seed, budget=8192):
+    w = synth.make_weights(dims, seed=1)
+    gm = M.Model(dims, w)
+    ss = synth.newstest_set()
+    got = gm.translate(ss, budget)                  # the launch configuration bench.py times
+    om = O.OracleModel(dims, w)
+    L = ss.lengths
+    rng = np.random.default_rng(seed)
+    idx = list(rng.choice(ss.n, size=n_sample - 2, replace=False)) + [int(np.argmax(L)), int(np.argmin(L))]
+    ref = om.decode_many(ss.subset(idx), 0)
+    agree = sum(np.array_equal(got[i], r) for i, r in zip(idx, ref))
+    words = sum(len(g) for g in got)
+    return agree, len(idx), words, ss
+
+
+def test_config1_small_aan_newstest_sampled():
+    agree, n, words, ss = _sampled(synth.PRESETS["small-aan"], 16, 5)
+    assert agree == n
+    assert words <= int(ss.max_len.sum())
+
+
+@pytest.mark.slow
+def test_config2_base_selfattn_sampled():
+    agree, n, _, _ = _sampled(synth.PRESETS["base"], 6, 6)
+    assert agree == n

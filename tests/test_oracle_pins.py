@@ -314,3 +314,38 @@ def test_batcher_invariants(orc):
         for i in range(len(order) - 1):
             if Ls[i] == Ls[i + 1]:
                 assert order[i] < order[i + 1]
+
+
+# --------------------------------------------------------------- exported primitives used by P-1
+def test_linear_matches_exact_fma(orc):
+    """fmaf((float)acc, s, b): acc*s is exact in float64 (<= 48 significant bits), so one
+    float64 add followed by rounding to fp32 equals the fused result (R5)."""
+    rng = np.random.default_rng(77)
+    qa = rng.integers(-127, 128, size=(9, 96)).astype(np.int8)
+    qw = rng.integers(-127, 128, size=(40, 96)).astype(np.int8)
+    b = rng.uniform(-0.1, 0.1, 40).astype(np.float32)
+    acc = qa.astype(np.int64) @ qw.astype(np.int64).T
+    ref = (acc.astype(np.float64) * np.float64(orc.dequant_scale()) + b.astype(np.float64)).astype(np.float32)
+    assert np.array_equal(orc.linear(qa, qw, b), ref)
+    assert np.array_equal(orc.linear(qa, qw, None),
+                          (acc.astype(np.float64) * np.float64(orc.dequant_scale())).astype(np.float32))
+
+
+def test_residual_ln_gate_form(orc):
+    d = 48
+    x, dl, gi, gf = (synth.uniform_activations((5, d), s, 2.0) for s in (1, 2, 3, 4))
+    gi, gf = orc.sigmoid_array(gi), orc.sigmoid_array(gf)
+    g = synth.uniform_activations((d,), 5, 0.1) + np.float32(1)
+    b = synth.uniform_activations((d,), 6, 0.1)
+    z = gi * x + gf * dl                                  # numpy fp32: one rounding per op
+    assert np.allclose(orc.residual_ln(x, dl, g, b, 1e-6, gi, gf), RP.layernorm(x + z, g, b, 1e-6),
+                       rtol=1e-6, atol=1e-7)
+    assert np.allclose(orc.residual_ln(x, dl, g, b), RP.layernorm(x + dl, g, b, 1e-6), rtol=1e-6, atol=1e-7)
+
+
+def test_embed_rows(orc):
+    E = synth.uniform_activations((20, 16), 8, 0.5)
+    out = orc.embed_rows(E, [-1, 3, 19], [0, 5, 7])
+    assert np.array_equal(out[0], orc.pe(0, 16))           # start symbol: PE(0) only (R13)
+    assert np.array_equal(out[1], RP.embed(E, [3], 5, 16)[0])
+    assert np.array_equal(out[2], RP.embed(E, [19], 7, 16)[0])
