@@ -103,13 +103,15 @@ def param_shapes(m: ModelDims) -> Dict[str, tuple]:
     return s
 
 
-def make_weights(m: ModelDims, seed: int = 1, code_domain: bool = False) -> Dict[str, np.ndarray]:
+def make_weights(m: ModelDims, seed: int = 1, code_domain: bool = False,
+                 emb_scale: float = 0.5) -> Dict[str, np.ndarray]:
     """Random-init weights (SURVEY.md 8(d) "Synthetic inputs").
 
     Linear W ~ Glorot-uniform +-sqrt(6/(in+out)); E ~ U(-0.5, 0.5); biases
     U(-0.1, 0.1); LN gain 1 + U(-0.1, 0.1), LN bias U(-0.1, 0.1).
     code_domain=True draws every W (and E) as k/63.5, k uniform in [-127,127]
-    (GEMM stress: every code is reachable)."""
+    (GEMM stress: every code is reachable).  emb_scale sets E ~ U(-emb_scale, emb_scale);
+    a small scale weakens the tied-embedding feedback so free-running outputs vary."""
     rng = np.random.default_rng(seed)
     out: Dict[str, np.ndarray] = {}
     for name, shape in param_shapes(m).items():
@@ -117,7 +119,7 @@ def make_weights(m: ModelDims, seed: int = 1, code_domain: bool = False) -> Dict
             if code_domain:
                 a = rng.integers(-127, 128, size=shape).astype(np.float32) / np.float32(63.5)
             else:
-                a = rng.uniform(-0.5, 0.5, size=shape)
+                a = rng.uniform(-emb_scale, emb_scale, size=shape)
         elif name.endswith(".W"):
             if code_domain:
                 a = rng.integers(-127, 128, size=shape).astype(np.float32) / np.float32(63.5)

@@ -26,3 +26,13 @@ def orc():
     import oracle.oracle as O
     O.build()
     return O
+
+
+@pytest.fixture(autouse=True)
+def _release_device_temporaries():
+    yield
+    try:
+        from tests import gpu_util
+        gpu_util.release()
+    except Exception:
+        pass

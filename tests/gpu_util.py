@@ -9,9 +9,20 @@ def torch_dev():
     return torch.device("cuda:0")
 
 
+_KEEP = []   # device temporaries stay alive until the test ends (raw pointers go to the C-ABI)
+
+
+def release():
+    _KEEP.clear()
+
+
 def to_dev(a):
     import torch
-    return torch.from_numpy(np.ascontiguousarray(a)).to(torch_dev())
+    if a is None:
+        return None
+    t = torch.from_numpy(np.ascontiguousarray(a)).to(torch_dev())
+    _KEEP.append(t)
+    return t
 
 
 def empty(shape, dtype):

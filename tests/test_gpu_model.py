@@ -110,17 +110,24 @@ def test_config0_tiny192_aan():
 
 
 def test_tiny192_noffn_nogate_eos_and_edges():
+    """EOS handling + compaction: with the EOS bias raised to 16 (the top logits of this
+    random student are ~17-18) about half of the sentences emit EOS at step 1 (nothing is
+    written, R16) and the rest run to their own max_len (0..39), so live rows drop out at
+    many different steps.  Random-init students repeat one token per sentence, so EOS
+    cannot be made to win mid-sentence; teacher-forced tests carry the id diversity."""
     dims = synth.PRESETS["tiny192-aan-noffn-nogate"]
     w = synth.make_weights(dims, seed=4)
     w["out.b"] = w["out.b"].copy()
-    w["out.b"][dims.eos_id] = 0.35     # EOS wins sometimes: exercises stop + compaction
-    om, gm = O.OracleModel(dims, w), M.Model(dims, w)
+    w["out.b"][dims.eos_id] = 16.0
     ss = synth.random_set(40, 0, 30, seed=8)
     ss.max_len[:] = np.random.default_rng(2).integers(0, 40, size=40)
+    om, gm = O.OracleModel(dims, w), M.Model(dims, w)
     ref = om.decode_many(ss, 4)
     got = gm.translate(ss, 100)
     assert all(np.array_equal(a, b) for a, b in zip(got, ref))
-    assert any(len(r) < m for r, m in zip(ref, ss.max_len)), "no sentence stopped at EOS"
+    n_eos = sum(len(r) == 0 and m > 0 for r, m in zip(ref, ss.max_len))
+    n_full = sum(len(r) == m > 0 for r, m in zip(ref, ss.max_len))
+    assert n_eos >= 5 and n_full >= 5, (n_eos, n_full)
 
 
 def test_batch_and_order_invariance():
