@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""Benchmark: batched greedy int8 decoding of a distilled AAN student (arXiv 1805.12096).
+
+One "step" = one pass of the whole hot path over one batch of synthetic input: the
+newstest2014-shaped set (3003 sentences, 62,954 source tokens), sorted by
+length and cut into >= 8192-word batches, encoded and greedily decoded
+(max_len = source length) with every product in int8 on the tensor cores.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mnmt|reference]
+
+N > 1 is launched by torchrun (one process per GPU, NCCL); each rank decodes its own
+newstest-shaped set (weak scaling) and the output ids are gathered to rank 0.
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "target words/sec greedy decode at 1/2/4/8 B200; int8 tensor-pipe % of peak"
+UNIT = "target words/s"
+WORKLOADS = {
+    # name: (preset, word budget, BASELINE.json config)
+    "small-aan-newstest-8192w": ("small-aan", 8192, "configs[1]"),
+    "tiny192-aan-newstest-8192w": ("tiny192-aan", 8192, "configs[0] model"),
+    "base-newstest-8192w": ("base", 8192, "configs[2] self-attention"),
+    "base-aan-newstest-8192w": ("base-aan", 8192, "configs[2] AAN"),
+    "big-newstest-8192w": ("big", 8192, "configs[3]"),
+}
+DEFAULT_WORKLOAD = "small-aan-newstest-8192w"
+L2_FLUSH_BYTES = 512 << 20   # > 126 MB L2
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "source": "fallback (B200_PROFILING.md)"}
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- oracle legs
+def oracle_sample(sset, dims, weights, seconds: float, seed: int = 99):
+    """Decode a seeded random sample of the workload with the oracle, sized to ~`seconds`.
+    Returns (target words/s, threads, description)."""
+    import oracle.oracle as O
+    om = O.OracleModel(dims, weights)
+    threads = O.max_threads()
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(sset.n)
+    probe = sset.subset(perm[:max(threads, 8)])
+    t0 = time.perf_counter()
+    out = om.decode_many(probe, 0)
+    dt = time.perf_counter() - t0
+    w_probe = sum(len(o) for o in out)
+    rate = w_probe / max(dt, 1e-9)
+    mean_len = float(np.mean(probe.max_len))
+    n = int(min(sset.n, max(len(probe.max_len), rate * seconds / max(mean_len, 1.0))))
+    samp = sset.subset(perm[:n])
+    t0 = time.perf_counter()
+    out = om.decode_many(samp, 0)
+    dt = time.perf_counter() - t0
+    words = sum(len(o) for o in out)
+    desc = (f"oracle greedy decode of {n} of {sset.n} sentences (seeded random sample, "
+            f"{int(samp.lengths.sum())} source / {words} target words, one batch per sentence, "
+            f"OpenMP over sentences) in {dt:.1f} s")
+    return words / dt, threads, desc, dt
+
+
+def run_reference(args, dims, weights, sset, workload_cfg):
+    """`--impl reference`: the CPU oracle as it stands, timed on the host cores."""
+    import oracle.oracle as O
+    O.build()
+    om = O.OracleModel(dims, weights)
+    threads = O.max_threads()
+    rng = np.random.default_rng(123)
+    perm = rng.permutation(sset.n)
+    # size one step to ~8 s of CPU work
+    probe = sset.subset(perm[:max(threads, 8)])
+    t0 = time.perf_counter()
+    out = om.decode_many(probe, 0)
+    rate = sum(len(o) for o in out) / max(time.perf_counter() - t0, 1e-9)
+    n = int(min(sset.n, max(len(probe.max_len), rate * 8.0 / max(float(np.mean(probe.max_len)), 1.0))))
+    samp = sset.subset(perm[:n])
+    for _ in range(args.warmup):
+        om.decode_many(samp, 0)
+    t0 = time.perf_counter()
+    words = 0
+    for _ in range(args.steps):
+        words += sum(len(o) for o in om.decode_many(samp, 0))
+    dt = time.perf_counter() - t0
+    value = words / dt
+    desc = (f"oracle greedy decode of the same {n}-sentence seeded sample of the workload per step "
+            f"({int(samp.lengths.sum())} source words)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8/f32/f64",
+        "data": "synthetic (seeded random-init weights, newstest2014-shaped ids)",
+        "config": workload_cfg,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------- roofline legs
+def time_kernel(fn, iters: int, stream):
+    import torch
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(iters):
+        fn()
+    e.record(stream)
+    e.synchronize()
+    return s.elapsed_time(e) / iters    # ms per launch
+
+
+def live_rows_profile(sset, budget):
+    """Live decode rows at every step of every batch (max_len = S_i, no EOS) -> list."""
+    from paper_1805_12096_b200 import mnmt as M
+    order, off = M.batch_by_words(sset.lengths, budget)
+    rows = []
+    for b in range(len(off) - 1):
+        ml = sset.max_len[order[off[b]:off[b + 1]]]
+        for t in range(1, int(ml.max()) + 1):
+            rows.append(int(np.sum(ml >= t)))
+    return rows
+
+
+def roofline_out_gemm(dims, weights, sset, budget, peaks, stream):
+    """A9: output projection fused with argmax, at the workload's mean live-row count."""
+    import torch
+    from paper_1805_12096_b200 import mnmt as M
+    rows = live_rows_profile(sset, budget)
+    Mr = int(round(np.mean(rows)))
+    d, V = dims.d_model, dims.vocab
+    dev = torch.device("cuda", torch.cuda.current_device())
+    E = torch.from_numpy(weights["emb.E"]).to(dev)
+    qE = torch.empty((V, d), dtype=torch.int8, device=dev)
+    M.op_quantize(E.data_ptr(), V * d, dims.clip, qE.data_ptr(), stream)
+    x = torch.randn((Mr, d), device=dev)
+    qa = torch.empty((Mr, d), dtype=torch.int8, device=dev)
+    M.op_quantize(x.data_ptr(), Mr * d, dims.clip, qa.data_ptr(), stream)
+    b = torch.from_numpy(weights["out.b"]).to(dev)
+    keys = torch.zeros(Mr, dtype=torch.int64, device=dev)
+
+    def fn():
+        M.op_gemm_i8(qa.data_ptr(), qE.data_ptr(), Mr, V, d, b.data_ptr(), dims.clip,
+                     M.EPI_ARGMAX, keys.data_ptr(), None, 0, stream)
+    ms = time_kernel(fn, 200, stream)
+    ops = 2.0 * Mr * V * d
+    peak = 2.0 * peaks["bf16_tflops"]          # int8 dense = 2x bf16 (nominal 4.5 / 2.25)
+    ach = ops / (ms * 1e-3) / 1e12
+    return {"kernel": "k_gemm_i8<EPI_ARGMAX> (A9 output GEMM + argmax)", "bound": "tensor",
+            "achieved": ach, "peak": peak, "unit": "TOP/s (int8)", "frac": ach / peak,
+            "traffic": None, "shape": f"M={Mr} (mean live rows/step) N={V} K={d}",
+            "ms_per_launch": ms, "launches_per_step": len(rows),
+            "ms_per_step_est": ms * len(rows) * 1.0,
+            "peak_source": f"{peaks['source']} bf16 burst x2"}
+
+
+def roofline_src_attn(dims, sset, budget, peaks, stream):
+    """A7: source attention over the fp32 K/V cache at the workload's mean live rows."""
+    import torch
+    from paper_1805_12096_b200 import mnmt as M
+    order, off = M.batch_by_words(sset.lengths, budget)
+    # representative batch: the one holding the median sentence
+    b = int(np.searchsorted(off, sset.n // 2, side="right") - 1)
+    idx = order[off[b]:off[b + 1]]
+    L = sset.lengths[idx].astype(np.int32)
+    starts = np.concatenate([[0], np.cumsum(L)[:-1]]).astype(np.int32)
+    d, H = dims.d_model, dims.n_heads
+    n = len(idx)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    kv = torch.randn((int(L.sum()), 2 * d), device=dev)
+    q = torch.randn((n, d), device=dev)
+    st, ln = torch.from_numpy(starts).to(dev), torch.from_numpy(L).to(dev)
+    oq = torch.empty((n, d), dtype=torch.int8, device=dev)
+
+    def fn():
+        M.op_attention(q.data_ptr(), d, kv.data_ptr(), 2 * d, 0, d, st.data_ptr(), ln.data_ptr(),
+                       n, d, H, dims.clip, oq.data_ptr(), None, stream)
+    ms = time_kernel(fn, 200, stream)
+    bytes_ = float(8 * d * L.sum() + n * (4 * d + d))   # K,V fp32 + q fp32 + codes
+    ach = bytes_ / (ms * 1e-3) / 1e9
+    peak = peaks["hbm_gbs"]
+    return {"kernel": "k_attn (A7 source attention, fp64 accumulate)", "bound": "hbm",
+            "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
+            "shape": f"rows={n} S_mean={L.mean():.1f} d={d} H={H} (one layer)",
+            "ms_per_launch": ms, "peak_source": peaks["source"]}
+
+
+# ---------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mnmt", choices=["mnmt", "reference"])
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-roofline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    preset, budget, cfg_ref = WORKLOADS[args.workload]
+    dims = synth.PRESETS[preset]
+    workload_cfg = {"workload": args.workload, "baseline_config": cfg_ref,
+                    "student": f"{preset}: d={dims.d_model} F={dims.d_ffn} H={dims.n_heads} "
+                               f"L={dims.enc_layers}+{dims.dec_layers} V={dims.vocab} "
+                               f"decoder={'AAN' if dims.decoder else 'self-attn'}",
+                    "sentences_per_gpu": synth.NEWSTEST_SENTENCES,
+                    "source_words_per_gpu": synth.NEWSTEST_TOKENS, "word_budget": budget,
+                    "beam": 1, "max_len": "source length", "parallelism": f"dp{args.gpus}",
+                    "l2": "flushed between timed steps (512 MiB write)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        weights = synth.make_weights(dims, seed=1)
+        run_reference(args, dims, weights, synth.newstest_set(seed=2014), workload_cfg)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dist_on = world > 1
+    if dist_on:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1805_12096_b200 import dist as D
+    from paper_1805_12096_b200 import mnmt as M
+
+    weights = synth.make_weights(dims, seed=1)
+    model = M.Model(dims, weights, device=local)
+    sset = synth.newstest_set(seed=2014 + rank)          # weak scaling: one set per GPU
+    stream = torch.cuda.current_stream()
+    dev = torch.device("cuda", local)
+    ids_dev = torch.from_numpy(sset.ids).to(dev)
+    cap = int(sset.max_len.sum())
+    out_dev = torch.zeros(cap, dtype=torch.int32, device=dev)
+    len_dev = torch.zeros(sset.n, dtype=torch.int32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        model.translate_device(ids_dev.data_ptr(), sset.offsets, sset.max_len, budget,
+                               out_dev.data_ptr(), cap, len_dev.data_ptr(), stream)
+        if dist_on:
+            D.gather_ids(out_dev, len_dev)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = model.stats()["gpu_launches"]
+    words_rank = int(len_dev.sum().item())
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if dist_on:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    for k in range(args.steps):
+        flush.zero_()                       # untimed: L2 flush between timed steps
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    if dist_on:
+        dist.barrier()
+    clk = clocks.stop()
+    ms_total = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([ms_total, float(words_rank)], dtype=torch.float64, device=dev)
+    if dist_on:
+        tmax = t.clone()
+        dist.all_reduce(tmax[0:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tmax[1:2], op=dist.ReduceOp.SUM)
+        t = tmax
+    ms_max, words_total = float(t[0]), float(t[1])
+    value = words_total * args.steps / (ms_max / 1000.0)
+
+    # ---- e2e: the public host-buffer call (H2D of ids, D2H of ids inside the timed region)
+    model.translate(sset, budget, stream)
+    torch.cuda.synchronize()
+    st = model.stats()
+    e_ms = []
+    for _ in range(args.e2e_steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        outs = model.translate(sset, budget, stream)
+        if dist_on:
+            flat, lens = D.pack_ids(outs, sset.max_len)
+            D.gather_ids(torch.from_numpy(flat).to(dev), torch.from_numpy(lens).to(dev))
+        torch.cuda.synchronize()
+        e_ms.append(1000 * (time.perf_counter() - t0))
+    e = torch.tensor([sum(e_ms)], dtype=torch.float64, device=dev)
+    if dist_on:
+        dist.all_reduce(e, op=dist.ReduceOp.MAX)
+    e2e_value = words_total * args.e2e_steps / (float(e[0]) / 1000.0)
+
+    roof = None
+    cpu = None
+    if rank == 0 and not args.no_roofline:
+        peaks = load_peaks()
+        cands = [roofline_out_gemm(dims, weights, sset, budget, peaks, stream),
+                 roofline_src_attn(dims, sset, budget, peaks, stream)]
+        cands[1]["launches_per_step"] = len(live_rows_profile(sset, budget)) * dims.dec_layers
+        cands[1]["ms_per_step_est"] = cands[1]["ms_per_launch"] * cands[1]["launches_per_step"]
+        roof = max(cands, key=lambda c: c["ms_per_step_est"])
+        roof["share_of_step_est"] = roof["ms_per_step_est"] / (ms_max / args.steps)
+        roof["other"] = {c["kernel"]: {"frac": c["frac"], "ms_per_step_est": c["ms_per_step_est"]}
+                         for c in cands if c is not roof}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, desc, _ = oracle_sample(sset, dims, weights, args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int8 products (s32 acc), f32 activations, f64 reductions",
+            "data": "synthetic (seeded random-init weights, newstest2014-shaped length-sorted ids)",
+            "config": workload_cfg,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": st["h2d_bytes"],
+                    "d2h_bytes_per_step": st["d2h_bytes"]},
+            "gpu_launches": launches_per_step * args.steps,
+            "target_words_per_step": words_total,
+            "decode_steps_per_gpu": st["decode_steps"], "batches_per_gpu": st["batches"],
+            "clocks": clk, "roofline": roof, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if dist_on:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
