@@ -169,14 +169,22 @@ def run_reference(args, dims, weights, sset, workload_cfg):
 
 # ---------------------------------------------------------------------------- roofline legs
 def time_kernel(fn, iters: int, stream):
+    """Average device time of one launch: `iters` launches captured in a CUDA graph (so host
+    overhead of the op-level call is excluded), replayed, timed with CUDA events."""
     import torch
     for _ in range(3):
-        fn()
+        fn(torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        cs = torch.cuda.current_stream()
+        for _ in range(iters):
+            fn(cs)
+    g.replay()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record(stream)
-    for _ in range(iters):
-        fn()
+    g.replay()
     e.record(stream)
     e.synchronize()
     return s.elapsed_time(e) / iters    # ms per launch
@@ -211,9 +219,9 @@ def roofline_out_gemm(dims, weights, sset, budget, peaks, stream):
     b = torch.from_numpy(weights["out.b"]).to(dev)
     keys = torch.zeros(Mr, dtype=torch.int64, device=dev)
 
-    def fn():
+    def fn(st):
         M.op_gemm_i8(qa.data_ptr(), qE.data_ptr(), Mr, V, d, b.data_ptr(), dims.clip,
-                     M.EPI_ARGMAX, keys.data_ptr(), None, 0, stream)
+                     M.EPI_ARGMAX, keys.data_ptr(), None, 0, st)
     ms = time_kernel(fn, 200, stream)
     ops = 2.0 * Mr * V * d
     peak = 2.0 * peaks["bf16_tflops"]          # int8 dense = 2x bf16 (nominal 4.5 / 2.25)
@@ -244,9 +252,9 @@ def roofline_src_attn(dims, sset, budget, peaks, stream):
     st, ln = torch.from_numpy(starts).to(dev), torch.from_numpy(L).to(dev)
     oq = torch.empty((n, d), dtype=torch.int8, device=dev)
 
-    def fn():
+    def fn(s_):
         M.op_attention(q.data_ptr(), d, kv.data_ptr(), 2 * d, 0, d, st.data_ptr(), ln.data_ptr(),
-                       n, d, H, dims.clip, oq.data_ptr(), None, stream)
+                       n, d, H, dims.clip, oq.data_ptr(), None, s_)
     ms = time_kernel(fn, 200, stream)
     bytes_ = float(8 * d * L.sum() + n * (4 * d + d))   # K,V fp32 + q fp32 + codes
     ach = bytes_ / (ms * 1e-3) / 1e9
@@ -269,6 +277,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--max-concurrent-rows", type=int, default=4096,
+                    help="co-schedule consecutive >=budget-word batches in one decode wave "
+                         "(scheduling only; 0 = one batch at a time)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -284,7 +295,8 @@ def main():
                     "sentences_per_gpu": synth.NEWSTEST_SENTENCES,
                     "source_words_per_gpu": synth.NEWSTEST_TOKENS, "word_budget": budget,
                     "beam": 1, "max_len": "source length", "parallelism": f"dp{args.gpus}",
-                    "l2": "flushed between timed steps (512 MiB write)"}
+                    "l2": "flushed between timed steps (512 MiB write)",
+                    "max_concurrent_rows": args.max_concurrent_rows}
 
     if args.impl == "reference":
         if rank != 0:
@@ -304,6 +316,7 @@ def main():
 
     weights = synth.make_weights(dims, seed=1)
     model = M.Model(dims, weights, device=local)
+    model.set_option("max_concurrent_rows", args.max_concurrent_rows)
     sset = synth.newstest_set(seed=2014 + rank)          # weak scaling: one set per GPU
     stream = torch.cuda.current_stream()
     dev = torch.device("cuda", local)

@@ -141,6 +141,15 @@ mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids_host,
                                int32_t* argmax_ids_host, uint32_t dump_mask, void* dump_host,
                                int64_t dump_cap, void* cuda_stream);
 
+/* Runtime options (not part of the method; they change scheduling only, never results —
+ * rows are independent, so ids are identical for every setting):
+ *   "max_concurrent_rows"  mnmt_translate co-schedules consecutive word-budget batches in
+ *                          one decode wave while the wave holds at most this many sentences
+ *                          (0 = default = one batch at a time).  A single >=8192-word batch
+ *                          (~375 sentences) cannot fill 148 SMs.
+ * Errors: MNMT_ERR_ARG (unknown name or negative value). */
+mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, int64_t value);
+
 /* Statistics of the last mnmt_translate / mnmt_decode call. */
 typedef struct {
   int64_t gpu_launches;     /* kernels launched (graph nodes counted per replay) */

@@ -49,7 +49,8 @@ mnmt_status mnmt_op_argmax_ids(const uint64_t* keys_dev, int32_t n, int32_t* ids
                                void* stream);
 
 /* A3/A6-A8: out = LN(fl(x + delta)) (post-norm, fp64 statistics; R10, R20) and
- * out_q = Q(out).  Gate form (gi_dev != NULL, R8): out = LN(fl(x + fl(fl(gi*x) + fl(gf*delta)))). */
+ * out_q = Q(out).  Gate form (gi_dev != NULL, R8): gi/gf are the gate LOGITS of the two gate
+ * products; out = LN(fl(x + fl(fl(s(gi)*x) + fl(s(gf)*delta)))), s = fp64 sigmoid (R20). */
 mnmt_status mnmt_op_layernorm(const float* x_dev, const float* delta_dev, const float* gi_dev,
                               const float* gf_dev, const float* gamma_dev, const float* beta_dev,
                               int32_t n, int32_t d, float eps, float clip, float* out_dev,

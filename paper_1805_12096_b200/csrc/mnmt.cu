@@ -122,6 +122,7 @@ struct mnmt_model {
   int64_t launches_per_step = 0;
   mnmt_stats stats{};
   int max_pos = MNMT_MAX_SPAN + 1;
+  int64_t max_concurrent_rows = 0;   // option: co-schedule batches in waves of <= this many rows
 };
 
 namespace {
@@ -506,10 +507,11 @@ static cudaError_t launch_step(mnmt_model* m, int n, bool forced, StepHook* hook
         k += 1;
       }
       if (c.aan_gate) {
-        // gate (R8): i = sigmoid(W_i Q(y)), f = sigmoid(W_f Q(a)); for -ffn, Q(a) = Q(g)
+        // gate (R8): logits W_i Q(y) + b_i and W_f Q(a) + b_f (for -ffn, Q(a) = Q(g));
+        // the sigmoids are applied in the gate-LayerNorm kernel
         const CUtensorMap& tm_a = c.aan_ffn_depth == 0 ? w.tm_cg : w.tm_ca;
-        if ((e = gemm(m, w.tm_cy, D.gi, n, nd, EPI_SIGMOID, w.gi, nullptr, d)) != cudaSuccess) return e;
-        if ((e = gemm(m, tm_a, D.gf, n, nd, EPI_SIGMOID, w.gf, nullptr, d)) != cudaSuccess) return e;
+        if ((e = gemm(m, w.tm_cy, D.gi, n, nd, EPI_F32, w.gi, nullptr, d)) != cudaSuccess) return e;
+        if ((e = gemm(m, tm_a, D.gf, n, nd, EPI_F32, w.gf, nullptr, d)) != cudaSuccess) return e;
         k += 2;
         l1 = ln_args(m, n, nd, w.y, a_f, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
         l1.gi = w.gi;
@@ -863,9 +865,14 @@ mnmt_status mnmt_model_create(const mnmt_config* cfg, int32_t cuda_device, mnmt_
     return MNMT_ERR_CUDA;
   }
   DeviceGuard g(cuda_device);
-  if (cudaError_t e = gemm_init(); e != cudaSuccess) {
-    set_err("GEMM init failed: %s", cudaGetErrorString(e));
-    return MNMT_ERR_CUDA;
+  {
+    DeviceGuard g0(cuda_device);
+    cudaError_t e = gemm_init();
+    if (e == cudaSuccess) e = attn_init();
+    if (e != cudaSuccess) {
+      set_err("kernel init failed: %s", cudaGetErrorString(e));
+      return MNMT_ERR_CUDA;
+    }
   }
   mnmt_model* m = new mnmt_model();
   m->c = *cfg;
@@ -1028,7 +1035,15 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
     for (int i = 0; i < n; ++i) L[i] = (int32_t)(src_off[i + 1] - src_off[i]);
     int32_t nb = 0;
     mnmt_batch_by_words(L.data(), n, budget, order.data(), off.data(), &nb);
-    for (int b = 0; b < nb; ++b) rows.emplace_back(order.begin() + off[b], order.begin() + off[b + 1]);
+    // Waves: consecutive batches decoded together while the wave holds at most
+    // max_concurrent_rows sentences (scheduling only; results are row-independent).
+    for (int b = 0; b < nb;) {
+      int e = b + 1;
+      if (m->max_concurrent_rows > 0)
+        while (e < nb && off[e + 1] - off[b] <= m->max_concurrent_rows) ++e;
+      rows.emplace_back(order.begin() + off[b], order.begin() + off[e]);
+      b = e;
+    }
   } else {
     rows.emplace_back(n);
     std::iota(rows[0].begin(), rows[0].end(), 0);
@@ -1234,6 +1249,17 @@ extern "C" mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids,
   if (O > 0) CK(cudaMemcpyAsync(argmax_ids, w.out_ids, O * 4, cudaMemcpyDeviceToHost, m->st));
   if ((s = end_call(m, cuda_stream)) != MNMT_OK) return fail(m, s);
   return MNMT_OK;
+}
+
+extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, int64_t value) {
+  if (!m || !name) { set_err("NULL argument"); return MNMT_ERR_ARG; }
+  if (std::string(name) == "max_concurrent_rows") {
+    if (value < 0) { set_err("max_concurrent_rows < 0"); return MNMT_ERR_ARG; }
+    m->max_concurrent_rows = value;
+    return MNMT_OK;
+  }
+  set_err("unknown option '%s'", name);
+  return MNMT_ERR_ARG;
 }
 
 extern "C" mnmt_status mnmt_get_stats(const mnmt_model* m, mnmt_stats* out) {

@@ -141,6 +141,7 @@ mnmt_status mnmt_op_attention(const float* q, int64_t ldq, const float* kv, int6
   if (n < 0 || H < 1 || d % H || (d / H) % 4 || d / H > 64 || !q || !kv || !kv_start || !kv_len ||
       !out_q || ldq % 4 || ldkv % 4 || k_off % 4 || v_off % 4 || !(clip > 0.0f))
     return arg_error("mnmt_op_attention: bad arguments");
+  if (cudaError_t e = attn_init(); e != cudaSuccess) return cuda_status(e, "attention init");
   AttnArgs a{};
   a.mode = ATTN_ENC;
   a.n = n;

@@ -160,9 +160,13 @@ __global__ void k_ln(LnArgs a) {
       float4 x = ld4(a.x + off + 4 * c4);
       float4 z;
       if (a.gi) {
-        // AAN gate (R8): z = fl(fl(i*y) + fl(f*a)), residual r = fl(y + z)
-        float4 iy = mul4(ld4(a.gi + off + 4 * c4), x);
-        float4 fa = mul4(ld4(a.gf + off + 4 * c4), ld4(a.delta + off + 4 * c4));
+        // AAN gate (R8): i = sigmoid(gi), f = sigmoid(gf) from the gate GEMMs' logits;
+        // z = fl(fl(i*y) + fl(f*a)), residual r = fl(y + z)
+        float4 li = ld4(a.gi + off + 4 * c4), lf = ld4(a.gf + off + 4 * c4);
+        float4 si = make_float4(sigmoid_f64(li.x), sigmoid_f64(li.y), sigmoid_f64(li.z), sigmoid_f64(li.w));
+        float4 sf = make_float4(sigmoid_f64(lf.x), sigmoid_f64(lf.y), sigmoid_f64(lf.z), sigmoid_f64(lf.w));
+        float4 iy = mul4(si, x);
+        float4 fa = mul4(sf, ld4(a.delta + off + 4 * c4));
         z = add4(iy, fa);
       } else {
         z = ld4(a.delta + off + 4 * c4);
@@ -210,23 +214,34 @@ __global__ void k_ln(LnArgs a) {
 }
 
 // ------------------------------------------------------------------ attention
-// One warp per (row, head).  Scores and context in fp64; the per-position dot
-// products and the context sums run in the oracle's order (sequential over the
-// head dimension / over positions), the normaliser Z is summed sequentially.
-constexpr int ATTN_WARPS = 4;
+// One CTA per query row, all heads.  K and V rows stream through shared memory in chunks
+// of ATTN_CH positions with coalesced float4 loads (rows padded by 4 floats: conflict-free
+// float4 reads).  Scores / softmax / context in fp64 (R20): each dot product runs over the
+// head dimension in order and each context sum over positions in order (the plain definition);
+// the per-head normaliser Z is summed sequentially.
+constexpr int ATTN_THREADS = 256;
+constexpr int ATTN_CH = 32;
 
-__global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn(AttnArgs a) {
-  __shared__ double sc_all[ATTN_WARPS][MNMT_MAX_KV];
+__host__ __device__ inline size_t attn_smem_bytes(int d, int H) {
+  return (size_t)H * MNMT_MAX_KV * sizeof(double) + (size_t)ATTN_CH * (d + 4) * sizeof(float) +
+         (size_t)d * sizeof(float) + (size_t)H * sizeof(double);
+}
+
+__global__ void __launch_bounds__(ATTN_THREADS) k_attn(AttnArgs a) {
+  extern __shared__ __align__(16) uint8_t attn_smem[];
+  const int H = a.H, dh = a.dh, d = a.d;
+  double* sc = reinterpret_cast<double*>(attn_smem);                 // [H][MAX_KV]
+  float* buf = reinterpret_cast<float*>(sc + (size_t)H * MNMT_MAX_KV);  // [CH][d + 4]
+  float* qs = buf + (size_t)ATTN_CH * (d + 4);                       // [d]
+  double* Zs = reinterpret_cast<double*>(qs + d);                    // [H]
+  const int ld = d + 4;
   pdl_wait();
-  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * ATTN_WARPS + wi;
-  const int H = a.H, dh = a.dh;
-  const int r = gw / H, h = gw - r * H;
+  const int r = blockIdx.x;
   const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
   if (r >= n_live) return;
-  double* sc = sc_all[wi];
+  const int tid = threadIdx.x, nth = blockDim.x;
   int start, len;
-  const float* q = a.q + (int64_t)r * a.ldq + h * dh;
+  const float* qrow = a.q + (int64_t)r * a.ldq;
   if (a.mode == ATTN_ENC) {
     start = a.kv_start[r];
     len = a.kv_len[r];
@@ -234,55 +249,98 @@ __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn(AttnArgs a) {
     const int orig = a.live[r];
     start = a.kv_start[orig];
     len = a.kv_len[orig];
-  } else {  // ATTN_SELF: append this step's k, v (head slice) to the cache, attend over 1..t
+  } else {  // ATTN_SELF: append this step's k, v to the cache, attend over positions 1..t
     const int orig = a.live[r];
     const int t = a.ctrl[1];
     start = orig * a.t_cap;
     len = t;
-    float* dst = a.kv_w + (int64_t)(start + t - 1) * a.ldkv + h * dh;
-    const float* src = a.q + (int64_t)r * a.ldq + h * dh;
-    for (int c = lane; c < dh; c += 32) {
-      dst[a.k_off + c] = src[a.d + c];        // k at qkv columns [d, 2d)
-      dst[a.v_off + c] = src[2 * a.d + c];    // v at qkv columns [2d, 3d)
+    float* dst = a.kv_w + (int64_t)(start + t - 1) * a.ldkv;
+    for (int c = tid; c < d; c += nth) {
+      dst[a.k_off + c] = qrow[d + c];        // k at qkv columns [d, 2d)
+      dst[a.v_off + c] = qrow[2 * d + c];    // v at qkv columns [2d, 3d)
     }
-    __syncwarp();
     __threadfence_block();
   }
-  const float* K = a.kv + (int64_t)start * a.ldkv + a.k_off + h * dh;
-  const float* V = a.kv + (int64_t)start * a.ldkv + a.v_off + h * dh;
+  for (int c = tid; c < d; c += nth) qs[c] = qrow[c];
   const double inv_sqrt = 1.0 / sqrt((double)dh);
-  // pass 1: scores (lane j takes positions j, j+32, ...)
-  double mx = -INFINITY;
-  for (int j = lane; j < len; j += 32) {
-    const float* kr = K + (int64_t)j * a.ldkv;
-    double dot = 0.0;
-    for (int c = 0; c < dh; c += 4) {
-      const float4 k4 = ld4(kr + c);
-      const float4 q4 = ld4(q + c);
-      dot = __dadd_rn(dot, __dmul_rn((double)q4.x, (double)k4.x));
-      dot = __dadd_rn(dot, __dmul_rn((double)q4.y, (double)k4.y));
-      dot = __dadd_rn(dot, __dmul_rn((double)q4.z, (double)k4.z));
-      dot = __dadd_rn(dot, __dmul_rn((double)q4.w, (double)k4.w));
+  const float* K = a.kv + (int64_t)start * a.ldkv + a.k_off;
+  const float* V = a.kv + (int64_t)start * a.ldkv + a.v_off;
+  const int d4 = d >> 2;
+  // ---- pass 1: scores, chunk by chunk
+  for (int j0 = 0; j0 < len; j0 += ATTN_CH) {
+    const int cn = min(ATTN_CH, len - j0);
+    __syncthreads();
+    for (int i = tid; i < cn * d4; i += nth) {
+      const int jj = i / d4, c4 = i - jj * d4;
+      *reinterpret_cast<float4*>(buf + jj * ld + 4 * c4) =
+          *reinterpret_cast<const float4*>(K + (int64_t)(j0 + jj) * a.ldkv + 4 * c4);
     }
-    const double s = __dmul_rn(dot, inv_sqrt);
-    sc[j] = s;
-    mx = fmax(mx, s);
+    __syncthreads();
+    for (int p = tid; p < cn * H; p += nth) {
+      const int h = p / cn, jj = p - h * cn;        // consecutive threads: consecutive positions
+      const float* kr = buf + jj * ld + h * dh;
+      const float* qh = qs + h * dh;
+      double dot = 0.0;
+      for (int c = 0; c < dh; c += 4) {
+        const float4 k4 = *reinterpret_cast<const float4*>(kr + c);
+        const float4 q4 = *reinterpret_cast<const float4*>(qh + c);
+        dot = __dadd_rn(dot, __dmul_rn((double)q4.x, (double)k4.x));
+        dot = __dadd_rn(dot, __dmul_rn((double)q4.y, (double)k4.y));
+        dot = __dadd_rn(dot, __dmul_rn((double)q4.z, (double)k4.z));
+        dot = __dadd_rn(dot, __dmul_rn((double)q4.w, (double)k4.w));
+      }
+      sc[h * MNMT_MAX_KV + j0 + jj] = __dmul_rn(dot, inv_sqrt);
+    }
   }
-  mx = warp_max_f64(mx);
-  for (int j = lane; j < len; j += 32) sc[j] = exp(__dsub_rn(sc[j], mx));
-  __syncwarp();
-  double Z = 0.0;
-  if (lane == 0)
-    for (int j = 0; j < len; ++j) Z = __dadd_rn(Z, sc[j]);
-  Z = __shfl_sync(0xffffffffu, Z, 0);
-  // pass 3: context, lane = head dimension
-  for (int c = lane; c < dh; c += 32) {
-    double acc = 0.0;
-    for (int j = 0; j < len; ++j)
-      acc = __dadd_rn(acc, __dmul_rn(sc[j], (double)V[(int64_t)j * a.ldkv + c]));
-    const float ctx = len > 0 ? (float)__ddiv_rn(acc, Z) : 0.0f;
-    a.out_q[(int64_t)r * a.d + h * dh + c] = (int8_t)q8(ctx, a.clip, a.sigma);
-    if (a.out_f) a.out_f[(int64_t)r * a.d + h * dh + c] = ctx;
+  __syncthreads();
+  // ---- softmax: max per head (one warp per head), exp in parallel, Z sequential per head
+  const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
+  for (int h = warp; h < H; h += nwarps) {
+    double m = -INFINITY;
+    for (int j = lane; j < len; j += 32) m = fmax(m, sc[h * MNMT_MAX_KV + j]);
+    m = warp_max_f64(m);
+    for (int j = lane; j < len; j += 32) sc[h * MNMT_MAX_KV + j] = exp(__dsub_rn(sc[h * MNMT_MAX_KV + j], m));
+  }
+  __syncthreads();
+  for (int h = tid; h < H; h += nth) {
+    double Z = 0.0;
+    for (int j = 0; j < len; ++j) Z = __dadd_rn(Z, sc[h * MNMT_MAX_KV + j]);
+    Zs[h] = Z;
+  }
+  // ---- pass 3: context, thread = column, positions in order
+  constexpr int MAXC = 4;   // d <= MAXC * ATTN_THREADS
+  double acc[MAXC];
+#pragma unroll
+  for (int k = 0; k < MAXC; ++k) acc[k] = 0.0;
+  for (int j0 = 0; j0 < len; j0 += ATTN_CH) {
+    const int cn = min(ATTN_CH, len - j0);
+    __syncthreads();
+    for (int i = tid; i < cn * d4; i += nth) {
+      const int jj = i / d4, c4 = i - jj * d4;
+      *reinterpret_cast<float4*>(buf + jj * ld + 4 * c4) =
+          *reinterpret_cast<const float4*>(V + (int64_t)(j0 + jj) * a.ldkv + 4 * c4);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < MAXC; ++k) {
+      const int c = tid + k * nth;
+      if (c < d) {
+        const double* ph = sc + (c / dh) * MNMT_MAX_KV + j0;
+        double s = acc[k];
+        for (int jj = 0; jj < cn; ++jj) s = __dadd_rn(s, __dmul_rn(ph[jj], (double)buf[jj * ld + c]));
+        acc[k] = s;
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < MAXC; ++k) {
+    const int c = tid + k * nth;
+    if (c < d) {
+      const float ctx = len > 0 ? (float)__ddiv_rn(acc[k], Zs[c / dh]) : 0.0f;
+      a.out_q[(int64_t)r * d + c] = (int8_t)q8(ctx, a.clip, a.sigma);
+      if (a.out_f) a.out_f[(int64_t)r * d + c] = ctx;
+    }
   }
 }
 
@@ -424,11 +482,21 @@ cudaError_t launch_ln(const LnArgs& a, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
+cudaError_t attn_init() {   // once per device
+  static bool done[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 0 && dev < 64 && done[dev]) return cudaSuccess;
+  e = cudaFuncSetAttribute(k_attn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)attn_smem_bytes(1024, 16));
+  if (e == cudaSuccess && dev >= 0 && dev < 64) done[dev] = true;
+  return e;
+}
+
 cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
   if (a.n <= 0) return cudaSuccess;
-  const int64_t warps = (int64_t)a.n * a.H;
-  dim3 grid((unsigned)((warps + ATTN_WARPS - 1) / ATTN_WARPS)), block(32 * ATTN_WARPS);
-  return launch_pdl(k_attn, grid, block, 0, st, a);
+  return launch_pdl(k_attn, dim3(a.n), dim3(ATTN_THREADS), attn_smem_bytes(a.d, a.H), st, a);
 }
 
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t st) {

@@ -38,7 +38,7 @@ struct LnArgs {
   float eps;
   const float* x;           // residual input (for the gate form: y)
   const float* delta;       // added to x (for the gate form: a)
-  const float* gi;          // gate form when non-null: r = x + (gi*x + gf*delta)
+  const float* gi;          // gate form when non-null: gate LOGITS; r = x + (s(gi)*x + s(gf)*delta)
   const float* gf;
   const float* gamma;
   const float* beta;
@@ -95,6 +95,7 @@ cudaError_t launch_embed_src(const int32_t* ids, const int32_t* idx, const int32
 cudaError_t launch_embed_tgt(const EmbedTgtArgs& a, int rows, cudaStream_t st);
 cudaError_t launch_ln(const LnArgs& a, cudaStream_t st);
 cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st);
+cudaError_t attn_init();   // dynamic-smem attribute (call once per device, outside capture)
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t st);
 cudaError_t launch_decode_init(int32_t* ctrl, int32_t* live, int B, unsigned long long* keys,
                                cudaStream_t st);

@@ -48,7 +48,7 @@ class Stats(C.Structure):
 EXPORTS = [
     "mnmt_config_default", "mnmt_model_create", "mnmt_model_set_param", "mnmt_model_quantize",
     "mnmt_batch_by_words", "mnmt_decode", "mnmt_translate", "mnmt_decode_forced",
-    "mnmt_get_stats", "mnmt_last_error", "mnmt_model_destroy",
+    "mnmt_get_stats", "mnmt_last_error", "mnmt_model_destroy", "mnmt_model_set_option",
     "mnmt_op_quantize", "mnmt_op_gemm_i8", "mnmt_op_argmax_ids", "mnmt_op_layernorm",
     "mnmt_op_aan_step", "mnmt_op_embed", "mnmt_op_attention",
 ]
@@ -76,6 +76,7 @@ def lib():
     L.mnmt_translate.argtypes = [P, P, P, I32, P, I32, P, I64, P, C.c_uint32, P]
     L.mnmt_decode_forced.argtypes = [P, P, P, I32, P, P, P, C.c_uint32, P, I64, P]
     L.mnmt_get_stats.argtypes = [P, C.POINTER(Stats)]
+    L.mnmt_model_set_option.argtypes = [P, C.c_char_p, I64]
     L.mnmt_last_error.argtypes = []
     L.mnmt_last_error.restype = C.c_char_p
     L.mnmt_model_destroy.argtypes = [P]
@@ -164,6 +165,10 @@ class Model:
             self.close()
         except Exception:
             pass
+
+    def set_option(self, name: str, value: int) -> None:
+        """Scheduling options (include/mnmt.h); never change results."""
+        _check(lib().mnmt_model_set_option(self.h, name.encode(), int(value)))
 
     def stats(self) -> Dict[str, int]:
         s = Stats()

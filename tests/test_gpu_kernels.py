@@ -130,9 +130,10 @@ def test_layernorm(d, gate):
     x, dl = synth.uniform_activations((n, d), 1, 2.0), synth.uniform_activations((n, d), 2, 2.0)
     g = synth.uniform_activations((d,), 3, 0.1) + np.float32(1)
     b = synth.uniform_activations((d,), 4, 0.1)
-    gi = O.sigmoid_array(synth.uniform_activations((n, d), 5, 3.0)) if gate else None
-    gf = O.sigmoid_array(synth.uniform_activations((n, d), 6, 3.0)) if gate else None
-    ref = O.residual_ln(x, dl, g, b, 1e-6, gi, gf)
+    gi = synth.uniform_activations((n, d), 5, 3.0) if gate else None     # gate logits
+    gf = synth.uniform_activations((n, d), 6, 3.0) if gate else None
+    ref = O.residual_ln(x, dl, g, b, 1e-6, O.sigmoid_array(gi) if gate else None,
+                        O.sigmoid_array(gf) if gate else None)
     out = empty((n, d), torch.float32)
     oq = empty((n, d), torch.int8)
     M.op_layernorm(ptr(to_dev(x)), ptr(to_dev(dl)), ptr(to_dev(gi)) if gate else None,

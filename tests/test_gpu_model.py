@@ -138,6 +138,10 @@ def test_batch_and_order_invariance():
     base = gm.translate(ss, 1 << 20)
     for budget in (1, 64, 333, 4096):
         assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, budget), base))
+    for rows in (7, 50, 1 << 20):          # co-scheduled batch waves: identical ids
+        gm.set_option("max_concurrent_rows", rows)
+        assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, 64), base))
+    gm.set_option("max_concurrent_rows", 0)
     perm = np.random.default_rng(3).permutation(ss.n)
     sub = gm.decode(ss.subset(perm))
     assert all(np.array_equal(sub[k], base[perm[k]]) for k in range(ss.n))
