@@ -411,9 +411,11 @@ static AanOut aan_for_layer(mnmt_model* m, int l) {
 }
 
 // Encoder over M tokens (A2-A4).  meta: [idx M][pos M][start M][len M].
-static cudaError_t launch_encoder(mnmt_model* m, int M, const int32_t* tok_idx,
+static cudaError_t launch_encoder(mnmt_model* m, int M, int n_sent, const int32_t* tok_idx,
                                   const int32_t* tok_pos, const int32_t* tok_start,
                                   const int32_t* tok_len, int64_t* nlaunch) {
+  (void)tok_start;
+  (void)tok_len;   // sentence spans come from the row metadata (row_start / row_len)
   auto& w = m->ws;
   const auto& c = m->c;
   const int d = c.d_model;
@@ -425,24 +427,18 @@ static cudaError_t launch_encoder(mnmt_model* m, int M, const int32_t* tok_idx,
   for (int l = 0; l < c.enc_layers; ++l) {
     const EncLayer& E = m->enc[l];
     if ((e = gemm(m, w.tm_cx, E.qkv, M, nullptr, EPI_F32, w.qkv, nullptr, 3 * d)) != cudaSuccess) return e;
-    AttnArgs at{};
-    at.mode = ATTN_ENC;
-    at.n = M;
+    EncAttnArgs at{};
+    at.qkv = w.qkv;
+    at.sent_start = w.row_start;
+    at.sent_len = w.row_len;
+    at.n_sent = n_sent;
     at.H = c.n_heads;
     at.dh = d / c.n_heads;
     at.d = d;
-    at.q = w.qkv;
-    at.ldq = 3 * d;
-    at.kv = w.qkv;
-    at.ldkv = 3 * d;
-    at.k_off = d;
-    at.v_off = 2 * d;
-    at.kv_start = tok_start;
-    at.kv_len = tok_len;
     at.clip = c.clip;
     at.sigma = sigma_of(m);
     at.out_q = w.cctx;
-    if ((e = launch_attn(at, m->st)) != cudaSuccess) return e;
+    if ((e = launch_attn_enc(at, m->st)) != cudaSuccess) return e;
     if ((e = gemm(m, w.tm_cctx, E.o, M, nullptr, EPI_F32, w.o, nullptr, d)) != cudaSuccess) return e;
     LnArgs la = ln_args(m, M, nullptr, w.x, w.o, E.ln1g, E.ln1b, w.x, w.cx);
     if ((e = launch_ln(la, m->st)) != cudaSuccess) return e;
@@ -764,7 +760,7 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
     if (forced) CK(cudaMemcpyAsync(w.forced_off, r64 + B, B * 8, cudaMemcpyDeviceToDevice, m->st));
     const int32_t* base = w.meta + b.tok0;
     const int M = (int)b.M;
-    CK(launch_encoder(m, M, base, base + M, base + 2 * M, base + 3 * M, &launches));
+    CK(launch_encoder(m, M, B, base, base + M, base + 2 * M, base + 3 * M, &launches));
     if (c.decoder == 1)
       CK(cudaMemsetAsync(w.C, 0, (size_t)c.dec_layers * w.B_cap * d * sizeof(float), m->st));
     CK(launch_decode_init(w.ctrl, w.live, B, w.keys, m->st));

@@ -214,34 +214,77 @@ __global__ void k_ln(LnArgs a) {
 }
 
 // ------------------------------------------------------------------ attention
-// One CTA per query row, all heads.  K and V rows stream through shared memory in chunks
-// of ATTN_CH positions with coalesced float4 loads (rows padded by 4 floats: conflict-free
-// float4 reads).  Scores / softmax / context in fp64 (R20): each dot product runs over the
-// head dimension in order and each context sum over positions in order (the plain definition);
-// the per-head normaliser Z is summed sequentially.
-constexpr int ATTN_THREADS = 256;
-constexpr int ATTN_CH = 32;
-
-__host__ __device__ inline size_t attn_smem_bytes(int d, int H) {
-  return (size_t)H * MNMT_MAX_KV * sizeof(double) + (size_t)ATTN_CH * (d + 4) * sizeof(float) +
-         (size_t)d * sizeof(float) + (size_t)H * sizeof(double);
+// fp64 scores / softmax / context (R20).  Dot products run over the head dimension in
+// order and context sums over positions in order (the plain definition); the max and the
+// normaliser Z use warp tree reductions.
+//
+// warp_attend: one warp computes one (query row, head): lane j scores positions j, j+32,
+// ...; probabilities go to a per-warp scratch in shared memory; lane c then sums column c
+// over the positions in order (V loads issued 4 ahead).
+__device__ __forceinline__ void warp_attend(const float* __restrict__ q, const float* k,
+                                            const float* v, int64_t ld, int len, int dh,
+                                            double* sc, float clip, float sigma,
+                                            int8_t* out_q, float* out_f) {
+  const int lane = threadIdx.x & 31;
+  const double inv_sqrt = 1.0 / sqrt((double)dh);
+  double mx = -INFINITY;
+  for (int j = lane; j < len; j += 32) {
+    const float* kr = k + (int64_t)j * ld;
+    double dot = 0.0;
+    for (int c = 0; c < dh; c += 4) {
+      const float4 k4 = *reinterpret_cast<const float4*>(kr + c);
+      const float4 q4 = *reinterpret_cast<const float4*>(q + c);
+      dot = __dadd_rn(dot, __dmul_rn((double)q4.x, (double)k4.x));
+      dot = __dadd_rn(dot, __dmul_rn((double)q4.y, (double)k4.y));
+      dot = __dadd_rn(dot, __dmul_rn((double)q4.z, (double)k4.z));
+      dot = __dadd_rn(dot, __dmul_rn((double)q4.w, (double)k4.w));
+    }
+    const double s = __dmul_rn(dot, inv_sqrt);
+    sc[j] = s;
+    mx = fmax(mx, s);
+  }
+  mx = warp_max_f64(mx);
+  double z = 0.0;
+  for (int j = lane; j < len; j += 32) {
+    const double p = exp(__dsub_rn(sc[j], mx));
+    sc[j] = p;
+    z = __dadd_rn(z, p);
+  }
+  z = warp_sum_f64(z);
+  __syncwarp();
+  for (int c = lane; c < dh; c += 32) {
+    double acc = 0.0;
+    int j = 0;
+    for (; j + 4 <= len; j += 4) {
+      const float v0 = v[(int64_t)(j + 0) * ld + c], v1 = v[(int64_t)(j + 1) * ld + c];
+      const float v2 = v[(int64_t)(j + 2) * ld + c], v3 = v[(int64_t)(j + 3) * ld + c];
+      acc = __dadd_rn(acc, __dmul_rn(sc[j + 0], (double)v0));
+      acc = __dadd_rn(acc, __dmul_rn(sc[j + 1], (double)v1));
+      acc = __dadd_rn(acc, __dmul_rn(sc[j + 2], (double)v2));
+      acc = __dadd_rn(acc, __dmul_rn(sc[j + 3], (double)v3));
+    }
+    for (; j < len; ++j) acc = __dadd_rn(acc, __dmul_rn(sc[j], (double)v[(int64_t)j * ld + c]));
+    const float ctx = len > 0 ? (float)__ddiv_rn(acc, z) : 0.0f;
+    out_q[c] = (int8_t)q8(ctx, clip, sigma);
+    if (out_f) out_f[c] = ctx;
+  }
+  __syncwarp();
 }
 
-__global__ void __launch_bounds__(ATTN_THREADS) k_attn(AttnArgs a) {
-  extern __shared__ __align__(16) uint8_t attn_smem[];
-  const int H = a.H, dh = a.dh, d = a.d;
-  double* sc = reinterpret_cast<double*>(attn_smem);                 // [H][MAX_KV]
-  float* buf = reinterpret_cast<float*>(sc + (size_t)H * MNMT_MAX_KV);  // [CH][d + 4]
-  float* qs = buf + (size_t)ATTN_CH * (d + 4);                       // [d]
-  double* Zs = reinterpret_cast<double*>(qs + d);                    // [H]
-  const int ld = d + 4;
+constexpr int ATTN_WARPS = 8;
+
+// Decoder (SRC, SELF) and op-level (ENC) attention: one warp per (row, head).
+__global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn(AttnArgs a) {
+  __shared__ double sc_all[ATTN_WARPS][MNMT_MAX_KV];
   pdl_wait();
-  const int r = blockIdx.x;
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * ATTN_WARPS + wi;
+  const int H = a.H, dh = a.dh;
+  const int r = (int)(gw / H), h = (int)(gw - (int64_t)r * H);
   const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
   if (r >= n_live) return;
-  const int tid = threadIdx.x, nth = blockDim.x;
   int start, len;
-  const float* qrow = a.q + (int64_t)r * a.ldq;
+  const float* q = a.q + (int64_t)r * a.ldq + h * dh;
   if (a.mode == ATTN_ENC) {
     start = a.kv_start[r];
     len = a.kv_len[r];
@@ -249,98 +292,68 @@ __global__ void __launch_bounds__(ATTN_THREADS) k_attn(AttnArgs a) {
     const int orig = a.live[r];
     start = a.kv_start[orig];
     len = a.kv_len[orig];
-  } else {  // ATTN_SELF: append this step's k, v to the cache, attend over positions 1..t
+  } else {  // ATTN_SELF: append this step's k, v (head slice), attend over positions 1..t
     const int orig = a.live[r];
     const int t = a.ctrl[1];
     start = orig * a.t_cap;
     len = t;
-    float* dst = a.kv_w + (int64_t)(start + t - 1) * a.ldkv;
-    for (int c = tid; c < d; c += nth) {
-      dst[a.k_off + c] = qrow[d + c];        // k at qkv columns [d, 2d)
-      dst[a.v_off + c] = qrow[2 * d + c];    // v at qkv columns [2d, 3d)
+    float* dst = a.kv_w + (int64_t)(start + t - 1) * a.ldkv + h * dh;
+    for (int c = lane; c < dh; c += 32) {
+      dst[a.k_off + c] = q[a.d + c];        // k at qkv columns [d, 2d)
+      dst[a.v_off + c] = q[2 * a.d + c];    // v at qkv columns [2d, 3d)
     }
-    __threadfence_block();
+    __syncwarp();
   }
-  for (int c = tid; c < d; c += nth) qs[c] = qrow[c];
-  const double inv_sqrt = 1.0 / sqrt((double)dh);
-  const float* K = a.kv + (int64_t)start * a.ldkv + a.k_off;
-  const float* V = a.kv + (int64_t)start * a.ldkv + a.v_off;
-  const int d4 = d >> 2;
-  // ---- pass 1: scores, chunk by chunk
-  for (int j0 = 0; j0 < len; j0 += ATTN_CH) {
-    const int cn = min(ATTN_CH, len - j0);
-    __syncthreads();
-    for (int i = tid; i < cn * d4; i += nth) {
-      const int jj = i / d4, c4 = i - jj * d4;
-      *reinterpret_cast<float4*>(buf + jj * ld + 4 * c4) =
-          *reinterpret_cast<const float4*>(K + (int64_t)(j0 + jj) * a.ldkv + 4 * c4);
-    }
-    __syncthreads();
-    for (int p = tid; p < cn * H; p += nth) {
-      const int h = p / cn, jj = p - h * cn;        // consecutive threads: consecutive positions
-      const float* kr = buf + jj * ld + h * dh;
-      const float* qh = qs + h * dh;
-      double dot = 0.0;
-      for (int c = 0; c < dh; c += 4) {
-        const float4 k4 = *reinterpret_cast<const float4*>(kr + c);
-        const float4 q4 = *reinterpret_cast<const float4*>(qh + c);
-        dot = __dadd_rn(dot, __dmul_rn((double)q4.x, (double)k4.x));
-        dot = __dadd_rn(dot, __dmul_rn((double)q4.y, (double)k4.y));
-        dot = __dadd_rn(dot, __dmul_rn((double)q4.z, (double)k4.z));
-        dot = __dadd_rn(dot, __dmul_rn((double)q4.w, (double)k4.w));
-      }
-      sc[h * MNMT_MAX_KV + j0 + jj] = __dmul_rn(dot, inv_sqrt);
-    }
-  }
-  __syncthreads();
-  // ---- softmax: max per head (one warp per head), exp in parallel, Z sequential per head
-  const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
-  for (int h = warp; h < H; h += nwarps) {
-    double m = -INFINITY;
-    for (int j = lane; j < len; j += 32) m = fmax(m, sc[h * MNMT_MAX_KV + j]);
-    m = warp_max_f64(m);
-    for (int j = lane; j < len; j += 32) sc[h * MNMT_MAX_KV + j] = exp(__dsub_rn(sc[h * MNMT_MAX_KV + j], m));
-  }
-  __syncthreads();
-  for (int h = tid; h < H; h += nth) {
-    double Z = 0.0;
-    for (int j = 0; j < len; ++j) Z = __dadd_rn(Z, sc[h * MNMT_MAX_KV + j]);
-    Zs[h] = Z;
-  }
-  // ---- pass 3: context, thread = column, positions in order
-  constexpr int MAXC = 4;   // d <= MAXC * ATTN_THREADS
-  double acc[MAXC];
-#pragma unroll
-  for (int k = 0; k < MAXC; ++k) acc[k] = 0.0;
-  for (int j0 = 0; j0 < len; j0 += ATTN_CH) {
-    const int cn = min(ATTN_CH, len - j0);
-    __syncthreads();
-    for (int i = tid; i < cn * d4; i += nth) {
-      const int jj = i / d4, c4 = i - jj * d4;
-      *reinterpret_cast<float4*>(buf + jj * ld + 4 * c4) =
-          *reinterpret_cast<const float4*>(V + (int64_t)(j0 + jj) * a.ldkv + 4 * c4);
+  const float* K = a.kv + (int64_t)start * a.ldkv + a.k_off + h * dh;
+  const float* V = a.kv + (int64_t)start * a.ldkv + a.v_off + h * dh;
+  warp_attend(q, K, V, a.ldkv, len, dh, sc_all[wi], a.clip, a.sigma,
+              a.out_q + (int64_t)r * a.d + h * dh, a.out_f ? a.out_f + (int64_t)r * a.d + h * dh : nullptr);
+}
+
+// Encoder self-attention: one CTA per (sentence, head).  The sentence's K and V head
+// slices are staged in shared memory once (rows padded by 4 floats) and reused by all of
+// its query rows (warp per query).  Sentences longer than ENC_STAGE_MAX read from L2/HBM.
+constexpr int ENC_STAGE_MAX = 160;
+
+__host__ __device__ inline size_t enc_attn_smem(int dh) {
+  return (size_t)ATTN_WARPS * MNMT_MAX_KV * sizeof(double) +
+         2 * (size_t)ENC_STAGE_MAX * (dh + 4) * sizeof(float);
+}
+
+__global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn_enc(EncAttnArgs a) {
+  extern __shared__ __align__(16) uint8_t enc_smem[];
+  double* sc = reinterpret_cast<double*>(enc_smem);                       // [warps][MAX_KV]
+  float* ks = reinterpret_cast<float*>(sc + (size_t)ATTN_WARPS * MNMT_MAX_KV);
+  pdl_wait();
+  const int s = blockIdx.x, h = blockIdx.y;
+  const int dh = a.dh, d = a.d, ld3 = 3 * d, lds = dh + 4;
+  const int start = a.sent_start[s], len = a.sent_len[s];
+  const float* base = a.qkv + (int64_t)start * ld3 + h * dh;
+  const float *K, *V;
+  int64_t ldk;
+  if (len <= ENC_STAGE_MAX) {
+    float* vs = ks + (size_t)ENC_STAGE_MAX * lds;
+    const int d4 = dh >> 2;
+    for (int i = threadIdx.x; i < len * d4; i += blockDim.x) {
+      const int j = i / d4, c4 = i - j * d4;
+      *reinterpret_cast<float4*>(ks + j * lds + 4 * c4) =
+          *reinterpret_cast<const float4*>(base + (int64_t)j * ld3 + d + 4 * c4);
+      *reinterpret_cast<float4*>(vs + j * lds + 4 * c4) =
+          *reinterpret_cast<const float4*>(base + (int64_t)j * ld3 + 2 * d + 4 * c4);
     }
     __syncthreads();
-#pragma unroll
-    for (int k = 0; k < MAXC; ++k) {
-      const int c = tid + k * nth;
-      if (c < d) {
-        const double* ph = sc + (c / dh) * MNMT_MAX_KV + j0;
-        double s = acc[k];
-        for (int jj = 0; jj < cn; ++jj) s = __dadd_rn(s, __dmul_rn(ph[jj], (double)buf[jj * ld + c]));
-        acc[k] = s;
-      }
-    }
+    K = ks;
+    V = vs;
+    ldk = lds;
+  } else {
+    K = base + d;
+    V = base + 2 * d;
+    ldk = ld3;
   }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < MAXC; ++k) {
-    const int c = tid + k * nth;
-    if (c < d) {
-      const float ctx = len > 0 ? (float)__ddiv_rn(acc[k], Zs[c / dh]) : 0.0f;
-      a.out_q[(int64_t)r * d + c] = (int8_t)q8(ctx, a.clip, a.sigma);
-      if (a.out_f) a.out_f[(int64_t)r * d + c] = ctx;
-    }
+  const int wi = threadIdx.x >> 5;
+  for (int i = wi; i < len; i += ATTN_WARPS) {
+    warp_attend(base + (int64_t)i * ld3, K, V, ldk, len, dh, sc + (size_t)wi * MNMT_MAX_KV,
+                a.clip, a.sigma, a.out_q + (int64_t)(start + i) * d + h * dh, nullptr);
   }
 }
 
@@ -488,15 +501,23 @@ cudaError_t attn_init() {   // once per device
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev >= 0 && dev < 64 && done[dev]) return cudaSuccess;
-  e = cudaFuncSetAttribute(k_attn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)attn_smem_bytes(1024, 16));
+  e = cudaFuncSetAttribute(k_attn_enc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)enc_attn_smem(64));
   if (e == cudaSuccess && dev >= 0 && dev < 64) done[dev] = true;
   return e;
 }
 
 cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
   if (a.n <= 0) return cudaSuccess;
-  return launch_pdl(k_attn, dim3(a.n), dim3(ATTN_THREADS), attn_smem_bytes(a.d, a.H), st, a);
+  const int64_t warps = (int64_t)a.n * a.H;
+  return launch_pdl(k_attn, dim3((unsigned)((warps + ATTN_WARPS - 1) / ATTN_WARPS)),
+                    dim3(ATTN_WARPS * 32), 0, st, a);
+}
+
+cudaError_t launch_attn_enc(const EncAttnArgs& a, cudaStream_t st) {
+  if (a.n_sent <= 0) return cudaSuccess;
+  return launch_pdl(k_attn_enc, dim3(a.n_sent, a.H), dim3(ATTN_WARPS * 32), enc_attn_smem(a.dh),
+                    st, a);
 }
 
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t st) {

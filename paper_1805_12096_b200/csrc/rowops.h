@@ -71,6 +71,16 @@ struct AttnArgs {
   float* out_f;             // optional fp32 ctx (tests)
 };
 
+// Encoder self-attention over Q|K|V rows [M x 3d] (A3), one CTA per (sentence, head).
+struct EncAttnArgs {
+  const float* qkv;
+  const int32_t* sent_start;   // [n_sent] first token row of each sentence
+  const int32_t* sent_len;     // [n_sent]
+  int n_sent, H, dh, d;
+  float clip, sigma;
+  int8_t* out_q;               // Q(ctx) [M x d]
+};
+
 struct FinishArgs {
   int32_t* ctrl;
   int32_t* live;
@@ -95,6 +105,7 @@ cudaError_t launch_embed_src(const int32_t* ids, const int32_t* idx, const int32
 cudaError_t launch_embed_tgt(const EmbedTgtArgs& a, int rows, cudaStream_t st);
 cudaError_t launch_ln(const LnArgs& a, cudaStream_t st);
 cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st);
+cudaError_t launch_attn_enc(const EncAttnArgs& a, cudaStream_t st);
 cudaError_t attn_init();   // dynamic-smem attribute (call once per device, outside capture)
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t st);
 cudaError_t launch_decode_init(int32_t* ctrl, int32_t* live, int B, unsigned long long* keys,
