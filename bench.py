@@ -277,6 +277,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--megakernel", type=int, default=1,
+                    help="1: persistent step kernel per batch; 0: one kernel per op (CUDA graph)")
+    ap.add_argument("--lanes", type=int, default=1,
+                    help="independent decoder lanes (streams) per GPU (scheduling only)")
     ap.add_argument("--max-concurrent-rows", type=int, default=4096,
                     help="co-schedule consecutive >=budget-word batches in one decode wave "
                          "(scheduling only; 0 = one batch at a time)")
@@ -296,7 +300,8 @@ def main():
                     "source_words_per_gpu": synth.NEWSTEST_TOKENS, "word_budget": budget,
                     "beam": 1, "max_len": "source length", "parallelism": f"dp{args.gpus}",
                     "l2": "flushed between timed steps (512 MiB write)",
-                    "max_concurrent_rows": args.max_concurrent_rows}
+                    "max_concurrent_rows": args.max_concurrent_rows, "lanes": args.lanes,
+                    "step_engine": "persistent cooperative kernel" if args.megakernel else "kernel-per-op CUDA graph"}
 
     if args.impl == "reference":
         if rank != 0:
@@ -317,6 +322,8 @@ def main():
     weights = synth.make_weights(dims, seed=1)
     model = M.Model(dims, weights, device=local)
     model.set_option("max_concurrent_rows", args.max_concurrent_rows)
+    model.set_option("lanes", args.lanes)
+    model.set_option("megakernel", args.megakernel)
     sset = synth.newstest_set(seed=2014 + rank)          # weak scaling: one set per GPU
     stream = torch.cuda.current_stream()
     dev = torch.device("cuda", local)

@@ -16,6 +16,7 @@
 // Rows beyond the live-row count (M_dyn, read on device) are computed but never stored,
 // and whole M-tiles beyond it exit before allocating TMEM.
 #include <cstdio>
+#include <cstdlib>
 #include <cudaTypedefs.h>
 
 #include "kernels.h"
@@ -261,6 +262,14 @@ bool make_tmap_i8(CUtensorMap* map, const void* base, int64_t rows, int64_t K) {
   return r == CUDA_SUCCESS;
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MNMT_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 int gemm_pick_bn(int M, int N) {
   const int mt = (M + BM - 1) / BM;
   if (((N + 255) / 256) * mt >= 148) return 256;
@@ -281,7 +290,7 @@ static cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k_gemm_i8<BN, EPI>, tmA, tmB, a);

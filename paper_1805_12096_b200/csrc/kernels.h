@@ -44,6 +44,9 @@ cudaError_t launch_gemm_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const
 
 int gemm_pick_bn(int M, int N);   // 64, 128 or 256
 
+// Programmatic dependent launch on every kernel (env MNMT_NO_PDL=1 disables; A/B testing).
+bool pdl_enabled();
+
 // Sets the dynamic-smem attribute of every GEMM instantiation on the current device.
 cudaError_t gemm_init();
 

@@ -9,6 +9,7 @@
 //            -> src-q GEMM -> src attention -> src-o GEMM -> LN2 -> FFN1 -> FFN2
 //            -> LN3 (+AAN step of the next layer) -> output GEMM fused with argmax -> finish.
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -22,6 +23,7 @@
 #include "../../include/mnmt_ops.h"
 #include "kernels.h"
 #include "rowops.h"
+#include "stepkernel.h"
 
 using namespace mnmt;
 
@@ -71,7 +73,7 @@ struct DecLayer {
 };
 
 struct Workspace {
-  int64_t M_cap = 0, B_cap = 0, T_cap = 0, O_cap = 0, N_cap = 0, tok_cap = 0;
+  int64_t M_cap = 0, B_cap = 0, T_cap = 0, O_cap = 0;
   std::vector<void*> allocs;
   // encoder (token rows)
   float *x = nullptr, *qkv = nullptr, *o = nullptr, *kv = nullptr;
@@ -89,15 +91,35 @@ struct Workspace {
   int8_t *cy = nullptr, *cg = nullptr, *ch1 = nullptr, *ca = nullptr, *cx1 = nullptr;
   int8_t *cctxd = nullptr, *cx2 = nullptr, *chd = nullptr;
   CUtensorMap tm_cy, tm_cg, tm_ch1, tm_ca, tm_cx1, tm_cctxd, tm_cx2, tm_chd;
-  // job-level
-  int32_t* out_ids = nullptr;
-  int32_t* out_len = nullptr;
-  int32_t* src_ids = nullptr;
-  int32_t* meta = nullptr;   // token metadata of all batches of a job
-  int64_t meta_cap = 0;
-  int32_t* rmeta32 = nullptr;  // row metadata of all batches: [start|len|max_len|len_idx] x B_b
-  int64_t* rmeta64 = nullptr;  // [out_off|forced_off] x B_b
-  int64_t rows_cap = 0;
+};
+
+// Job-level device buffers shared by all lanes.
+struct JobBuf {
+  int64_t O_cap = 0, N_cap = 0, tok_cap = 0, meta_cap = 0, rows_cap = 0;
+  std::vector<void*> allocs;
+  int32_t* out_ids = nullptr;   // [sum max_len] output ids, input-order layout
+  int32_t* out_len = nullptr;   // [n]
+  int32_t* src_ids = nullptr;   // [sum S_i]
+  int32_t* meta = nullptr;      // token metadata of all batches: idx|pos|start|len per batch
+  int32_t* rmeta32 = nullptr;   // row metadata of all batches: [start|len|max_len|len_idx] x B_b
+  int64_t* rmeta64 = nullptr;   // [out_off|forced_off] x B_b
+};
+
+// A lane = one independent decoder (workspace + stream + step graphs).  Rows are
+// independent, so lanes run concurrently and their kernel chains overlap on the GPU.
+struct Lane {
+  Workspace ws;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev = nullptr;
+  std::map<int64_t, cudaGraphExec_t> graphs;   // key: padded live-row bound
+  int64_t launches_per_step = 0;
+  // persistent step kernel program (built for this lane's workspace)
+  Phase* d_phases = nullptr;
+  int n_phases = 0;
+  bool prog_forced = false;
+  const int32_t* prog_out = nullptr;   // job output buffer the program writes to
+  CUtensorMap* d_tmaps = nullptr;
+  unsigned* d_bar = nullptr;
 };
 
 }  // namespace
@@ -115,14 +137,15 @@ struct mnmt_model {
   std::vector<EncLayer> enc;
   std::vector<DecLayer> dec;
   Lin kv_all;
-  Workspace ws;
-  cudaStream_t st = nullptr;
-  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-  std::map<int64_t, cudaGraphExec_t> graphs;             // key: padded live-row bound
-  int64_t launches_per_step = 0;
+  std::vector<Lane> lanes;      // lanes[0] always exists after create
+  int n_lanes = 1;               // option "lanes"
+  JobBuf jb;
+  cudaStream_t st = nullptr;     // main stream: uploads, joins, output copies
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_job = nullptr;
   mnmt_stats stats{};
   int max_pos = MNMT_MAX_SPAN + 1;
   int64_t max_concurrent_rows = 0;   // option: co-schedule batches in waves of <= this many rows
+  int megakernel = 1;                  // option: persistent step kernel (1) or one kernel per op (0)
 };
 
 namespace {
@@ -265,11 +288,35 @@ static mnmt_status upload_vec(mnmt_model* m, float** dst, const std::string& nam
 }
 
 // ------------------------------------------------------------------ workspace
-static void ws_free(mnmt_model* m) {
-  for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
-  m->graphs.clear();
-  for (void* p : m->ws.allocs) cudaFree(p);
-  m->ws = Workspace();
+static void lane_free(Lane& L) {
+  for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
+  L.graphs.clear();
+  for (void* p : L.ws.allocs) cudaFree(p);
+  L.ws = Workspace();
+  if (L.d_phases) cudaFree(L.d_phases);
+  if (L.d_tmaps) cudaFree(L.d_tmaps);
+  if (L.d_bar) cudaFree(L.d_bar);
+  L.d_phases = nullptr;
+  L.d_tmaps = nullptr;
+  L.d_bar = nullptr;
+  L.n_phases = 0;
+}
+
+static void jb_free(mnmt_model* m) {
+  for (void* p : m->jb.allocs) cudaFree(p);
+  m->jb = JobBuf();
+}
+
+static mnmt_status lane_init(mnmt_model* m, Lane& L) {
+  if (L.st) return MNMT_OK;
+  if (cudaStreamCreateWithFlags(&L.st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&L.ev, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    set_err("lane stream/event creation failed");
+    return MNMT_ERR_CUDA;
+  }
+  (void)m;
+  return MNMT_OK;
 }
 
 static mnmt_status ws_tmap(CUtensorMap* tm, const void* p, int64_t rows, int64_t K) {
@@ -280,24 +327,43 @@ static mnmt_status ws_tmap(CUtensorMap* tm, const void* p, int64_t rows, int64_t
   return MNMT_OK;
 }
 
-// Grows the workspace to hold M tokens, B rows, T steps, O output ids, N sentences.
-static mnmt_status ws_ensure(mnmt_model* m, int64_t M, int64_t B, int64_t T, int64_t O, int64_t N,
-                             int64_t tok, int64_t meta, int64_t rows) {
-  Workspace& w = m->ws;
-  if (M <= w.M_cap && B <= w.B_cap && T <= w.T_cap && O <= w.O_cap && N <= w.N_cap &&
-      tok <= w.tok_cap && meta <= w.meta_cap && rows <= w.rows_cap)
+// Job buffers for O output ids, N sentences, tok source tokens, token/row metadata.
+static mnmt_status jb_ensure(mnmt_model* m, int64_t O, int64_t N, int64_t tok, int64_t meta,
+                             int64_t rows) {
+  JobBuf& j = m->jb;
+  if (O <= j.O_cap && N <= j.N_cap && tok <= j.tok_cap && meta <= j.meta_cap && rows <= j.rows_cap)
     return MNMT_OK;
-  CK(cudaStreamSynchronize(m->st));
-  auto grow = [](int64_t need, int64_t have) { return std::max(need, have); };
+  CK(cudaDeviceSynchronize());
+  const int64_t Oc = std::max(O, j.O_cap), Nc = std::max(N, j.N_cap), tc = std::max(tok, j.tok_cap);
+  const int64_t mc = std::max(meta, j.meta_cap), rc = std::max(rows, j.rows_cap);
+  jb_free(m);
+  for (Lane& L : m->lanes) {   // captured graphs / step programs point at the job buffers
+    for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
+    L.graphs.clear();
+    L.prog_out = nullptr;
+  }
+  JobBuf& z = m->jb;
+  z.O_cap = Oc; z.N_cap = Nc; z.tok_cap = tc; z.meta_cap = mc; z.rows_cap = rc;
+  CKS(dalloc(z.allocs, &z.out_ids, Oc));
+  CKS(dalloc(z.allocs, &z.out_len, Nc));
+  CKS(dalloc(z.allocs, &z.src_ids, tc));
+  CKS(dalloc(z.allocs, &z.meta, mc));
+  CKS(dalloc(z.allocs, &z.rmeta32, 4 * rc));
+  CKS(dalloc(z.allocs, &z.rmeta64, 2 * rc));
+  return MNMT_OK;
+}
+
+// Grows a lane's workspace to hold M tokens, B rows, T steps, O forced ids.
+static mnmt_status lane_ensure(mnmt_model* m, Lane& Ln, int64_t M, int64_t B, int64_t T, int64_t O) {
+  Workspace& w = Ln.ws;
+  if (M <= w.M_cap && B <= w.B_cap && T <= w.T_cap && O <= w.O_cap) return MNMT_OK;
+  CK(cudaDeviceSynchronize());
   auto rnd = [](int64_t v, int64_t a) { return (std::max<int64_t>(v, 1) + a - 1) / a * a; };
-  const int64_t Mc = rnd(grow(M, w.M_cap), 128), Bc = rnd(grow(B, w.B_cap), 128);
-  const int64_t Tc = grow(T, w.T_cap), Oc = grow(O, w.O_cap), Nc = grow(N, w.N_cap);
-  const int64_t tokc = grow(tok, w.tok_cap), metac = grow(meta, w.meta_cap);
-  const int64_t rowsc = grow(rows, w.rows_cap);
-  ws_free(m);
-  Workspace& z = m->ws;
-  z.M_cap = Mc; z.B_cap = Bc; z.T_cap = Tc; z.O_cap = Oc; z.N_cap = Nc; z.tok_cap = tokc; z.meta_cap = metac;
-  z.rows_cap = rowsc;
+  const int64_t Mc = rnd(std::max(M, w.M_cap), 128), Bc = rnd(std::max(B, w.B_cap), 128);
+  const int64_t Tc = std::max(T, w.T_cap), Oc = std::max<int64_t>(std::max(O, w.O_cap), 1);
+  lane_free(Ln);
+  Workspace& z = Ln.ws;
+  z.M_cap = Mc; z.B_cap = Bc; z.T_cap = Tc; z.O_cap = Oc;
   const auto& c = m->c;
   const int64_t d = c.d_model, F = c.d_ffn, L = c.dec_layers;
   auto& A = z.allocs;
@@ -327,12 +393,6 @@ static mnmt_status ws_ensure(mnmt_model* m, int64_t M, int64_t B, int64_t T, int
   for (int8_t** p : {&z.cy, &z.cg, &z.ch1, &z.ca, &z.cx1, &z.cctxd, &z.cx2})
     CKS(dalloc(A, p, Bc * d));
   CKS(dalloc(A, &z.chd, Bc * F));
-  CKS(dalloc(A, &z.out_ids, Oc));
-  CKS(dalloc(A, &z.out_len, Nc));
-  CKS(dalloc(A, &z.src_ids, tokc));
-  CKS(dalloc(A, &z.meta, metac));
-  CKS(dalloc(A, &z.rmeta32, 4 * rowsc));
-  CKS(dalloc(A, &z.rmeta64, 2 * rowsc));
   CKS(ws_tmap(&z.tm_cx, z.cx, Mc, d));
   CKS(ws_tmap(&z.tm_cctx, z.cctx, Mc, d));
   CKS(ws_tmap(&z.tm_ch, z.ch, Mc, F));
@@ -348,7 +408,7 @@ static mnmt_status ws_ensure(mnmt_model* m, int64_t M, int64_t B, int64_t T, int
 }
 
 // ------------------------------------------------------------------ launch helpers
-static cudaError_t gemm(mnmt_model* m, const CUtensorMap& tmA, const Lin& W, int M,
+static cudaError_t gemm(mnmt_model* m, cudaStream_t st, const CUtensorMap& tmA, const Lin& W, int M,
                         const int32_t* M_dyn, int epi, float* out_f, int8_t* out_q, int64_t ldo,
                         unsigned long long* keys = nullptr, int col_block = 0,
                         int64_t block_stride = 0) {
@@ -367,17 +427,17 @@ static cudaError_t gemm(mnmt_model* m, const CUtensorMap& tmA, const Lin& W, int
   a.col_block = col_block > 0 ? col_block : W.out;
   a.block_stride = block_stride;
   a.keys = keys;
-  return launch_gemm_i8(tmA, W.tm, a, epi, 0, m->st);
+  return launch_gemm_i8(tmA, W.tm, a, epi, 0, st);
 }
 
-static LnArgs ln_args(mnmt_model* m, int n, const int32_t* n_dyn, const float* x,
+static LnArgs ln_args(mnmt_model* m, const Workspace& w, int n, const int32_t* n_dyn, const float* x,
                       const float* delta, const float* gamma, const float* beta, float* out,
                       int8_t* out_q) {
   LnArgs a{};
   a.n = n;
   a.n_dyn = n_dyn;
-  a.ctrl = m->ws.ctrl;
-  a.live = m->ws.live;
+  a.ctrl = w.ctrl;
+  a.live = w.live;
   a.d = m->c.d_model;
   a.eps = m->c.ln_eps;
   a.x = x;
@@ -394,39 +454,40 @@ static LnArgs ln_args(mnmt_model* m, int n, const int32_t* n_dyn, const float* x
 }
 
 // AAN step of decoder layer l fused into the producer of that layer's input.
-static AanOut aan_for_layer(mnmt_model* m, int l) {
+static AanOut aan_for_layer(mnmt_model* m, const Workspace& w, int l) {
   AanOut o{};
   o.clip = m->c.clip;
   o.sigma = sigma_of(m);
   if (m->c.decoder != 1 || l >= m->c.dec_layers) return o;
   const int64_t d = m->c.d_model;
-  o.C = m->ws.C + (int64_t)l * m->ws.B_cap * d;
+  o.C = w.C + (int64_t)l * w.B_cap * d;
   if (m->c.aan_ffn_depth == 0) {
-    o.g_f = m->ws.g;                       // a = g (fp32) for the residual / gate
-    if (m->c.aan_gate) o.g_q = m->ws.cg;   // Q(a) = Q(g) feeds the f-gate
+    o.g_f = w.g;                       // a = g (fp32) for the residual / gate
+    if (m->c.aan_gate) o.g_q = w.cg;   // Q(a) = Q(g) feeds the f-gate
   } else {
-    o.g_q = m->ws.cg;                      // Q(g) feeds the AAN FFN
+    o.g_q = w.cg;                      // Q(g) feeds the AAN FFN
   }
   return o;
 }
 
 // Encoder over M tokens (A2-A4).  meta: [idx M][pos M][start M][len M].
-static cudaError_t launch_encoder(mnmt_model* m, int M, int n_sent, const int32_t* tok_idx,
+static cudaError_t launch_encoder(mnmt_model* m, Lane& Ln, int M, int n_sent, const int32_t* tok_idx,
                                   const int32_t* tok_pos, const int32_t* tok_start,
                                   const int32_t* tok_len, int64_t* nlaunch) {
   (void)tok_start;
   (void)tok_len;   // sentence spans come from the row metadata (row_start / row_len)
-  auto& w = m->ws;
+  auto& w = Ln.ws;
+  cudaStream_t st = Ln.st;
   const auto& c = m->c;
   const int d = c.d_model;
   cudaError_t e;
-  if ((e = launch_embed_src(w.src_ids, tok_idx, tok_pos, M, m->E, m->PE, d, c.clip, w.x, w.cx,
-                            m->st)) != cudaSuccess)
+  if ((e = launch_embed_src(m->jb.src_ids, tok_idx, tok_pos, M, m->E, m->PE, d, c.clip, w.x, w.cx,
+                            st)) != cudaSuccess)
     return e;
   ++*nlaunch;
   for (int l = 0; l < c.enc_layers; ++l) {
     const EncLayer& E = m->enc[l];
-    if ((e = gemm(m, w.tm_cx, E.qkv, M, nullptr, EPI_F32, w.qkv, nullptr, 3 * d)) != cudaSuccess) return e;
+    if ((e = gemm(m, st, w.tm_cx, E.qkv, M, nullptr, EPI_F32, w.qkv, nullptr, 3 * d)) != cudaSuccess) return e;
     EncAttnArgs at{};
     at.qkv = w.qkv;
     at.sent_start = w.row_start;
@@ -438,18 +499,18 @@ static cudaError_t launch_encoder(mnmt_model* m, int M, int n_sent, const int32_
     at.clip = c.clip;
     at.sigma = sigma_of(m);
     at.out_q = w.cctx;
-    if ((e = launch_attn_enc(at, m->st)) != cudaSuccess) return e;
-    if ((e = gemm(m, w.tm_cctx, E.o, M, nullptr, EPI_F32, w.o, nullptr, d)) != cudaSuccess) return e;
-    LnArgs la = ln_args(m, M, nullptr, w.x, w.o, E.ln1g, E.ln1b, w.x, w.cx);
-    if ((e = launch_ln(la, m->st)) != cudaSuccess) return e;
-    if ((e = gemm(m, w.tm_cx, E.f1, M, nullptr, EPI_RELU_Q, nullptr, w.ch, c.d_ffn)) != cudaSuccess) return e;
-    if ((e = gemm(m, w.tm_ch, E.f2, M, nullptr, EPI_F32, w.o, nullptr, d)) != cudaSuccess) return e;
-    LnArgs lb = ln_args(m, M, nullptr, w.x, w.o, E.ln2g, E.ln2b, w.x, w.cx);
-    if ((e = launch_ln(lb, m->st)) != cudaSuccess) return e;
+    if ((e = launch_attn_enc(at, st)) != cudaSuccess) return e;
+    if ((e = gemm(m, st, w.tm_cctx, E.o, M, nullptr, EPI_F32, w.o, nullptr, d)) != cudaSuccess) return e;
+    LnArgs la = ln_args(m, w, M, nullptr, w.x, w.o, E.ln1g, E.ln1b, w.x, w.cx);
+    if ((e = launch_ln(la, st)) != cudaSuccess) return e;
+    if ((e = gemm(m, st, w.tm_cx, E.f1, M, nullptr, EPI_RELU_Q, nullptr, w.ch, c.d_ffn)) != cudaSuccess) return e;
+    if ((e = gemm(m, st, w.tm_ch, E.f2, M, nullptr, EPI_F32, w.o, nullptr, d)) != cudaSuccess) return e;
+    LnArgs lb = ln_args(m, w, M, nullptr, w.x, w.o, E.ln2g, E.ln2b, w.x, w.cx);
+    if ((e = launch_ln(lb, st)) != cudaSuccess) return e;
     *nlaunch += 7;
   }
   // Source keys/values of all decoder layers in one GEMM, scattered to [L][M_cap][2d].
-  if ((e = gemm(m, w.tm_cx, m->kv_all, M, nullptr, EPI_F32, w.kv, nullptr, 2 * d, nullptr, 2 * d,
+  if ((e = gemm(m, st, w.tm_cx, m->kv_all, M, nullptr, EPI_F32, w.kv, nullptr, 2 * d, nullptr, 2 * d,
                 w.M_cap * 2 * d)) != cudaSuccess)
     return e;
   ++*nlaunch;
@@ -462,12 +523,14 @@ struct StepHook {
   virtual cudaError_t layer(mnmt_model* m, int l) = 0;   // after LN3 of layer l
   virtual cudaError_t x1(mnmt_model* m, int l) = 0;
   virtual cudaError_t x2(mnmt_model* m, int l) = 0;
+  virtual bool megakernel_ok() const { return false; }   // no per-layer dumps needed
 };
 
 // One decoder step for up to `n` live rows (A5-A10).  Returns kernels launched via *nlaunch.
-static cudaError_t launch_step(mnmt_model* m, int n, bool forced, StepHook* hook,
+static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, StepHook* hook,
                                int64_t* nlaunch) {
-  auto& w = m->ws;
+  auto& w = Ln.ws;
+  cudaStream_t st = Ln.st;
   const auto& c = m->c;
   const int d = c.d_model, L = c.dec_layers, H = c.n_heads;
   const int32_t* nd = w.ctrl;  // ctrl[0] = live rows
@@ -483,8 +546,8 @@ static cudaError_t launch_step(mnmt_model* m, int n, bool forced, StepHook* hook
   ea.rsd = (float)std::sqrt((double)d);
   ea.y = w.y;
   ea.yq = w.cy;
-  ea.aan = aan_for_layer(m, 0);
-  if ((e = launch_embed_tgt(ea, n, m->st)) != cudaSuccess) return e;
+  ea.aan = aan_for_layer(m, w, 0);
+  if ((e = launch_embed_tgt(ea, n, st)) != cudaSuccess) return e;
   ++k;
   for (int l = 0; l < L; ++l) {
     const DecLayer& D = m->dec[l];
@@ -493,12 +556,12 @@ static cudaError_t launch_step(mnmt_model* m, int n, bool forced, StepHook* hook
       // A6: AAN block. g (or its codes) was produced with this layer's input.
       const float* a_f = w.g;
       if (c.aan_ffn_depth == 2) {
-        if ((e = gemm(m, w.tm_cg, D.a1, n, nd, EPI_RELU_Q, nullptr, w.ch1, d)) != cudaSuccess) return e;
-        if ((e = gemm(m, w.tm_ch1, D.a2, n, nd, EPI_F32_Q, w.a, w.ca, d)) != cudaSuccess) return e;
+        if ((e = gemm(m, st, w.tm_cg, D.a1, n, nd, EPI_RELU_Q, nullptr, w.ch1, d)) != cudaSuccess) return e;
+        if ((e = gemm(m, st, w.tm_ch1, D.a2, n, nd, EPI_F32_Q, w.a, w.ca, d)) != cudaSuccess) return e;
         a_f = w.a;
         k += 2;
       } else if (c.aan_ffn_depth == 1) {
-        if ((e = gemm(m, w.tm_cg, D.a1, n, nd, EPI_RELU_F32_Q, w.a, w.ca, d)) != cudaSuccess) return e;
+        if ((e = gemm(m, st, w.tm_cg, D.a1, n, nd, EPI_RELU_F32_Q, w.a, w.ca, d)) != cudaSuccess) return e;
         a_f = w.a;
         k += 1;
       }
@@ -506,18 +569,18 @@ static cudaError_t launch_step(mnmt_model* m, int n, bool forced, StepHook* hook
         // gate (R8): logits W_i Q(y) + b_i and W_f Q(a) + b_f (for -ffn, Q(a) = Q(g));
         // the sigmoids are applied in the gate-LayerNorm kernel
         const CUtensorMap& tm_a = c.aan_ffn_depth == 0 ? w.tm_cg : w.tm_ca;
-        if ((e = gemm(m, w.tm_cy, D.gi, n, nd, EPI_F32, w.gi, nullptr, d)) != cudaSuccess) return e;
-        if ((e = gemm(m, tm_a, D.gf, n, nd, EPI_F32, w.gf, nullptr, d)) != cudaSuccess) return e;
+        if ((e = gemm(m, st, w.tm_cy, D.gi, n, nd, EPI_F32, w.gi, nullptr, d)) != cudaSuccess) return e;
+        if ((e = gemm(m, st, tm_a, D.gf, n, nd, EPI_F32, w.gf, nullptr, d)) != cudaSuccess) return e;
         k += 2;
-        l1 = ln_args(m, n, nd, w.y, a_f, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
+        l1 = ln_args(m, w, n, nd, w.y, a_f, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
         l1.gi = w.gi;
         l1.gf = w.gf;
       } else {
-        l1 = ln_args(m, n, nd, w.y, a_f, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
+        l1 = ln_args(m, w, n, nd, w.y, a_f, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
       }
     } else {
       // A6': self-attention with a KV cache
-      if ((e = gemm(m, w.tm_cy, D.qkv, n, nd, EPI_F32, w.qkvd, nullptr, 3 * d)) != cudaSuccess) return e;
+      if ((e = gemm(m, st, w.tm_cy, D.qkv, n, nd, EPI_F32, w.qkvd, nullptr, 3 * d)) != cudaSuccess) return e;
       AttnArgs at{};
       at.mode = ATTN_SELF;
       at.n = n;
@@ -538,16 +601,16 @@ static cudaError_t launch_step(mnmt_model* m, int n, bool forced, StepHook* hook
       at.clip = c.clip;
       at.sigma = sigma_of(m);
       at.out_q = w.cctxd;
-      if ((e = launch_attn(at, m->st)) != cudaSuccess) return e;
-      if ((e = gemm(m, w.tm_cctxd, D.o, n, nd, EPI_F32, w.od, nullptr, d)) != cudaSuccess) return e;
+      if ((e = launch_attn(at, st)) != cudaSuccess) return e;
+      if ((e = gemm(m, st, w.tm_cctxd, D.o, n, nd, EPI_F32, w.od, nullptr, d)) != cudaSuccess) return e;
       k += 3;
-      l1 = ln_args(m, n, nd, w.y, w.od, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
+      l1 = ln_args(m, w, n, nd, w.y, w.od, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
     }
-    if ((e = launch_ln(l1, m->st)) != cudaSuccess) return e;
+    if ((e = launch_ln(l1, st)) != cudaSuccess) return e;
     ++k;
     if (hook && (e = hook->x1(m, l)) != cudaSuccess) return e;
     // A7: source attention
-    if ((e = gemm(m, w.tm_cx1, D.sq, n, nd, EPI_F32, w.qs, nullptr, d)) != cudaSuccess) return e;
+    if ((e = gemm(m, st, w.tm_cx1, D.sq, n, nd, EPI_F32, w.qs, nullptr, d)) != cudaSuccess) return e;
     AttnArgs as{};
     as.mode = ATTN_SRC;
     as.n = n;
@@ -568,18 +631,18 @@ static cudaError_t launch_step(mnmt_model* m, int n, bool forced, StepHook* hook
     as.clip = c.clip;
     as.sigma = sigma_of(m);
     as.out_q = w.cctxd;
-    if ((e = launch_attn(as, m->st)) != cudaSuccess) return e;
-    if ((e = gemm(m, w.tm_cctxd, D.so, n, nd, EPI_F32, w.od, nullptr, d)) != cudaSuccess) return e;
-    LnArgs l2 = ln_args(m, n, nd, w.x1, w.od, D.ln[1][0], D.ln[1][1], w.x2, w.cx2);
-    if ((e = launch_ln(l2, m->st)) != cudaSuccess) return e;
+    if ((e = launch_attn(as, st)) != cudaSuccess) return e;
+    if ((e = gemm(m, st, w.tm_cctxd, D.so, n, nd, EPI_F32, w.od, nullptr, d)) != cudaSuccess) return e;
+    LnArgs l2 = ln_args(m, w, n, nd, w.x1, w.od, D.ln[1][0], D.ln[1][1], w.x2, w.cx2);
+    if ((e = launch_ln(l2, st)) != cudaSuccess) return e;
     k += 4;
     if (hook && (e = hook->x2(m, l)) != cudaSuccess) return e;
     // A8: FFN
-    if ((e = gemm(m, w.tm_cx2, D.f1, n, nd, EPI_RELU_Q, nullptr, w.chd, c.d_ffn)) != cudaSuccess) return e;
-    if ((e = gemm(m, w.tm_chd, D.f2, n, nd, EPI_F32, w.f, nullptr, d)) != cudaSuccess) return e;
-    LnArgs l3 = ln_args(m, n, nd, w.x2, w.f, D.ln[2][0], D.ln[2][1], w.y, w.cy);
-    l3.aan = aan_for_layer(m, l + 1);
-    if ((e = launch_ln(l3, m->st)) != cudaSuccess) return e;
+    if ((e = gemm(m, st, w.tm_cx2, D.f1, n, nd, EPI_RELU_Q, nullptr, w.chd, c.d_ffn)) != cudaSuccess) return e;
+    if ((e = gemm(m, st, w.tm_chd, D.f2, n, nd, EPI_F32, w.f, nullptr, d)) != cudaSuccess) return e;
+    LnArgs l3 = ln_args(m, w, n, nd, w.x2, w.f, D.ln[2][0], D.ln[2][1], w.y, w.cy);
+    l3.aan = aan_for_layer(m, w, l + 1);
+    if ((e = launch_ln(l3, st)) != cudaSuccess) return e;
     k += 3;
     if (hook && (e = hook->layer(m, l)) != cudaSuccess) return e;
   }
@@ -596,7 +659,7 @@ static cudaError_t launch_step(mnmt_model* m, int n, bool forced, StepHook* hook
     a.sigma = sigma_of(m);
     a.col_block = c.vocab;
     a.keys = w.keys;
-    if ((e = launch_gemm_i8(w.tm_cy, m->tmE, a, EPI_ARGMAX, 0, m->st)) != cudaSuccess) return e;
+    if ((e = launch_gemm_i8(w.tm_cy, m->tmE, a, EPI_ARGMAX, 0, st)) != cudaSuccess) return e;
   }
   // A10: finish + compaction
   FinishArgs fa{};
@@ -606,16 +669,243 @@ static cudaError_t launch_step(mnmt_model* m, int n, bool forced, StepHook* hook
   fa.prev_id = w.prev_id;
   fa.max_len = w.max_len;
   fa.out_off = w.out_off;
-  fa.out_ids = w.out_ids;
-  fa.out_len = w.out_len;
+  fa.out_ids = m->jb.out_ids;
+  fa.out_len = m->jb.out_len;
   fa.len_idx = w.len_idx;
   fa.eos = c.eos_id;
   fa.forced = forced ? w.forced : nullptr;
   fa.forced_off = forced ? w.forced_off : nullptr;
-  if ((e = launch_finish(fa, m->st)) != cudaSuccess) return e;
+  if ((e = launch_finish(fa, st)) != cudaSuccess) return e;
   k += 2;
   *nlaunch += k;
   return cudaSuccess;
+}
+
+// ------------------------------------------------------------------ step program
+// The phase list of one decoder step (A5-A10) for the persistent step kernel.  It issues
+// exactly the operations of launch_step, in the same order, with the same arguments.
+struct ProgBuilder {
+  std::vector<Phase> ph;
+  std::vector<CUtensorMap> maps;
+  std::vector<std::array<int, 4>> fix;   // {phase, prob, mapA, mapB}
+  int map(const CUtensorMap& t) {
+    maps.push_back(t);
+    return (int)maps.size() - 1;
+  }
+};
+
+static GemmProb gprob(mnmt_model* m, ProgBuilder& pb, int phase, int prob,
+                      const CUtensorMap& tmA, const CUtensorMap& tmB, int N, int K,
+                      const float* bias, int M, const int32_t* M_dyn, int epi, float* out_f,
+                      int8_t* out_q, int64_t ldo, unsigned long long* keys = nullptr) {
+  GemmProb g{};
+  g.a.M = M;
+  g.a.M_dyn = M_dyn;
+  g.a.N = N;
+  g.a.K = K;
+  g.a.scale = scale_of(m);
+  g.a.bias = bias;
+  g.a.clip = m->c.clip;
+  g.a.sigma = sigma_of(m);
+  g.a.out_f = out_f;
+  g.a.out_q = out_q;
+  g.a.ldo = ldo;
+  g.a.col_block = N;
+  g.a.block_stride = 0;
+  g.a.keys = keys;
+  g.epi = epi;
+  g.bn = N >= 8192 ? 256 : (N >= 2048 ? 128 : 64);
+  g.n_tiles = (N + g.bn - 1) / g.bn;
+  pb.fix.push_back({phase, prob, pb.map(tmA), pb.map(tmB)});
+  return g;
+}
+
+static mnmt_status build_program(mnmt_model* m, Lane& Ln, bool forced) {
+  const auto& c = m->c;
+  auto& w = Ln.ws;
+  const int d = c.d_model, L = c.dec_layers, H = c.n_heads;
+  const int n = (int)w.B_cap;
+  const int32_t* nd = w.ctrl;
+  ProgBuilder pb;
+  auto gemm1 = [&](const CUtensorMap& tmA, const Lin& W, int epi, float* of, int8_t* oq, int64_t ldo) {
+    Phase P{};
+    P.type = PH_GEMM;
+    P.nprob = 1;
+    const int idx = (int)pb.ph.size();
+    P.g[0] = gprob(m, pb, idx, 0, tmA, W.tm, W.out, W.in, W.b, n, nd, epi, of, oq, ldo);
+    pb.ph.push_back(P);
+  };
+  auto gemm2 = [&](const CUtensorMap& tA0, const Lin& W0, int e0, float* f0, int8_t* q0,
+                   const CUtensorMap& tA1, const Lin& W1, int e1, float* f1, int8_t* q1) {
+    Phase P{};
+    P.type = PH_GEMM;
+    P.nprob = 2;
+    const int idx = (int)pb.ph.size();
+    P.g[0] = gprob(m, pb, idx, 0, tA0, W0.tm, W0.out, W0.in, W0.b, n, nd, e0, f0, q0, W0.out);
+    P.g[1] = gprob(m, pb, idx, 1, tA1, W1.tm, W1.out, W1.in, W1.b, n, nd, e1, f1, q1, W1.out);
+    pb.ph.push_back(P);
+  };
+  auto ln = [&](const LnArgs& a) {
+    Phase P{};
+    P.type = PH_LN;
+    P.ln = a;
+    pb.ph.push_back(P);
+  };
+  {
+    Phase P{};
+    P.type = PH_EMBED;
+    P.em.ctrl = w.ctrl;
+    P.em.live = w.live;
+    P.em.prev_id = w.prev_id;
+    P.em.E = m->E;
+    P.em.PE = m->PE;
+    P.em.d = d;
+    P.em.rsd = (float)std::sqrt((double)d);
+    P.em.y = w.y;
+    P.em.yq = w.cy;
+    P.em.aan = aan_for_layer(m, w, 0);
+    pb.ph.push_back(P);
+  }
+  for (int l = 0; l < L; ++l) {
+    const DecLayer& D = m->dec[l];
+    LnArgs l1;
+    if (c.decoder == 1) {
+      const float* a_f = w.g;
+      const CUtensorMap& tm_a = c.aan_ffn_depth == 0 ? w.tm_cg : w.tm_ca;
+      if (c.aan_ffn_depth == 2) {
+        if (c.aan_gate)
+          gemm2(w.tm_cg, D.a1, EPI_RELU_Q, nullptr, w.ch1, w.tm_cy, D.gi, EPI_F32, w.gi, nullptr);
+        else
+          gemm1(w.tm_cg, D.a1, EPI_RELU_Q, nullptr, w.ch1, d);
+        gemm1(w.tm_ch1, D.a2, EPI_F32_Q, w.a, w.ca, d);
+        a_f = w.a;
+        if (c.aan_gate) gemm1(tm_a, D.gf, EPI_F32, w.gf, nullptr, d);
+      } else if (c.aan_ffn_depth == 1) {
+        if (c.aan_gate)
+          gemm2(w.tm_cg, D.a1, EPI_RELU_F32_Q, w.a, w.ca, w.tm_cy, D.gi, EPI_F32, w.gi, nullptr);
+        else
+          gemm1(w.tm_cg, D.a1, EPI_RELU_F32_Q, w.a, w.ca, d);
+        a_f = w.a;
+        if (c.aan_gate) gemm1(tm_a, D.gf, EPI_F32, w.gf, nullptr, d);
+      } else if (c.aan_gate) {
+        gemm2(w.tm_cy, D.gi, EPI_F32, w.gi, nullptr, tm_a, D.gf, EPI_F32, w.gf, nullptr);
+      }
+      l1 = ln_args(m, w, n, nd, w.y, a_f, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
+      if (c.aan_gate) {
+        l1.gi = w.gi;
+        l1.gf = w.gf;
+      }
+    } else {
+      gemm1(w.tm_cy, D.qkv, EPI_F32, w.qkvd, nullptr, 3 * d);
+      Phase P{};
+      P.type = PH_ATTN;
+      AttnArgs& at = P.at;
+      at.mode = ATTN_SELF;
+      at.n = n;
+      at.n_dyn = nd;
+      at.ctrl = w.ctrl;
+      at.live = w.live;
+      at.H = H;
+      at.dh = d / H;
+      at.d = d;
+      at.q = w.qkvd;
+      at.ldq = 3 * d;
+      at.kv = w.selfkv + (int64_t)l * w.B_cap * w.T_cap * 2 * d;
+      at.kv_w = const_cast<float*>(at.kv);
+      at.ldkv = 2 * d;
+      at.k_off = 0;
+      at.v_off = d;
+      at.t_cap = (int)w.T_cap;
+      at.clip = c.clip;
+      at.sigma = sigma_of(m);
+      at.out_q = w.cctxd;
+      pb.ph.push_back(P);
+      gemm1(w.tm_cctxd, D.o, EPI_F32, w.od, nullptr, d);
+      l1 = ln_args(m, w, n, nd, w.y, w.od, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
+    }
+    ln(l1);
+    gemm1(w.tm_cx1, D.sq, EPI_F32, w.qs, nullptr, d);
+    {
+      Phase P{};
+      P.type = PH_ATTN;
+      AttnArgs& as = P.at;
+      as.mode = ATTN_SRC;
+      as.n = n;
+      as.n_dyn = nd;
+      as.ctrl = w.ctrl;
+      as.live = w.live;
+      as.H = H;
+      as.dh = d / H;
+      as.d = d;
+      as.q = w.qs;
+      as.ldq = d;
+      as.kv = w.kv + (int64_t)l * w.M_cap * 2 * d;
+      as.ldkv = 2 * d;
+      as.k_off = 0;
+      as.v_off = d;
+      as.kv_start = w.row_start;
+      as.kv_len = w.row_len;
+      as.clip = c.clip;
+      as.sigma = sigma_of(m);
+      as.out_q = w.cctxd;
+      pb.ph.push_back(P);
+    }
+    gemm1(w.tm_cctxd, D.so, EPI_F32, w.od, nullptr, d);
+    ln(ln_args(m, w, n, nd, w.x1, w.od, D.ln[1][0], D.ln[1][1], w.x2, w.cx2));
+    gemm1(w.tm_cx2, D.f1, EPI_RELU_Q, nullptr, w.chd, c.d_ffn);
+    gemm1(w.tm_chd, D.f2, EPI_F32, w.f, nullptr, d);
+    LnArgs l3 = ln_args(m, w, n, nd, w.x2, w.f, D.ln[2][0], D.ln[2][1], w.y, w.cy);
+    l3.aan = aan_for_layer(m, w, l + 1);
+    ln(l3);
+  }
+  {
+    Phase P{};
+    P.type = PH_GEMM;
+    P.nprob = 1;
+    const int idx = (int)pb.ph.size();
+    P.g[0] = gprob(m, pb, idx, 0, w.tm_cy, m->tmE, c.vocab, d, c.out_bias ? m->out_b : nullptr, n,
+                   nd, EPI_ARGMAX, nullptr, nullptr, 0, w.keys);
+    pb.ph.push_back(P);
+  }
+  {
+    Phase P{};
+    P.type = PH_FINISH;
+    FinishArgs& fa = P.fi;
+    fa.ctrl = w.ctrl;
+    fa.live = w.live;
+    fa.keys = w.keys;
+    fa.prev_id = w.prev_id;
+    fa.max_len = w.max_len;
+    fa.out_off = w.out_off;
+    fa.out_ids = m->jb.out_ids;
+    fa.out_len = m->jb.out_len;
+    fa.len_idx = w.len_idx;
+    fa.eos = c.eos_id;
+    fa.forced = forced ? w.forced : nullptr;
+    fa.forced_off = forced ? w.forced_off : nullptr;
+    pb.ph.push_back(P);
+  }
+  // upload: tensor maps first, then phases with their device addresses patched in
+  if (Ln.d_phases) cudaFree(Ln.d_phases);
+  if (Ln.d_tmaps) cudaFree(Ln.d_tmaps);
+  Ln.d_phases = nullptr;
+  Ln.d_tmaps = nullptr;
+  CK(cudaMalloc(&Ln.d_tmaps, pb.maps.size() * sizeof(CUtensorMap)));
+  CK(cudaMemcpy(Ln.d_tmaps, pb.maps.data(), pb.maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+  for (const auto& f : pb.fix) {
+    pb.ph[f[0]].g[f[1]].tmA = Ln.d_tmaps + f[2];
+    pb.ph[f[0]].g[f[1]].tmB = Ln.d_tmaps + f[3];
+  }
+  CK(cudaMalloc(&Ln.d_phases, pb.ph.size() * sizeof(Phase)));
+  CK(cudaMemcpy(Ln.d_phases, pb.ph.data(), pb.ph.size() * sizeof(Phase), cudaMemcpyHostToDevice));
+  if (!Ln.d_bar) {
+    CK(cudaMalloc(&Ln.d_bar, 64 * sizeof(unsigned)));
+    CK(cudaMemset(Ln.d_bar, 0, 64 * sizeof(unsigned)));
+  }
+  Ln.n_phases = (int)pb.ph.size();
+  Ln.prog_forced = forced;
+  Ln.prog_out = m->jb.out_ids;
+  return MNMT_OK;
 }
 
 // ------------------------------------------------------------------ job planning
@@ -624,6 +914,7 @@ struct Batch {
   int64_t tok0 = 0;           // first token of this batch in the job's token metadata
   int64_t M = 0;
   int T = 0;                  // max steps
+  int lane = 0;               // decoder lane (stream) that runs this batch
 };
 
 struct Job {
@@ -636,6 +927,7 @@ struct Job {
   int64_t out_total = 0, tok_total = 0, rows_total = 0;
   int64_t maxM = 0, maxB = 0;
   int maxT = 0;
+  std::vector<int64_t> lane_M, lane_B, lane_T;   // per-lane maxima (workspace sizing)
 };
 
 static mnmt_status check_inputs(mnmt_model* m, const int64_t* src_off, int32_t n,
@@ -654,13 +946,20 @@ static mnmt_status check_inputs(mnmt_model* m, const int64_t* src_off, int32_t n
 }
 
 static void plan_job(const int64_t* src_off, int32_t n, const int32_t* max_len,
-                     const std::vector<std::vector<int32_t>>& batch_rows, Job& job) {
+                     const std::vector<std::vector<int32_t>>& batch_rows,
+                     const std::vector<int>& batch_lane, int n_lanes, Job& job) {
+  job.lane_M.assign(n_lanes, 0);
+  job.lane_B.assign(n_lanes, 0);
+  job.lane_T.assign(n_lanes, 0);
+  size_t bi_in = 0;
   job.out_off.assign(n + 1, 0);
   for (int i = 0; i < n; ++i) job.out_off[i + 1] = job.out_off[i] + max_len[i];
   job.out_total = job.out_off[n];
   job.tok_total = n > 0 ? src_off[n] : 0;
   for (const auto& rows_all : batch_rows) {
     Batch b;
+    b.lane = batch_lane.empty() ? 0 : batch_lane[bi_in];
+    ++bi_in;
     for (int32_t s : rows_all)
       if (max_len[s] > 0) b.rows.push_back(s);   // max_len 0: nothing to decode
     if (b.rows.empty()) continue;
@@ -688,6 +987,9 @@ static void plan_job(const int64_t* src_off, int32_t n, const int32_t* max_len,
     job.maxM = std::max(job.maxM, M);
     job.maxB = std::max<int64_t>(job.maxB, (int64_t)b.rows.size());
     job.maxT = std::max(job.maxT, b.T);
+    job.lane_M[b.lane] = std::max(job.lane_M[b.lane], M);
+    job.lane_B[b.lane] = std::max<int64_t>(job.lane_B[b.lane], (int64_t)b.rows.size());
+    job.lane_T[b.lane] = std::max<int64_t>(job.lane_T[b.lane], b.T);
     job.batches.push_back(std::move(b));
   }
 }
@@ -728,7 +1030,7 @@ static void plan_rows(Job& job, const int64_t* src_off, const int32_t* max_len, 
 // Runs every batch of a job on m->st.  Source ids must already be in ws.src_ids and
 // the metadata in ws.meta / ws.rmeta* (upload_job).
 static mnmt_status upload_job(mnmt_model* m, const Job& job) {
-  auto& w = m->ws;
+  auto& w = m->jb;
   if (!job.meta.empty())
     CK(cudaMemcpyAsync(w.meta, job.meta.data(), job.meta.size() * 4, cudaMemcpyHostToDevice, m->st));
   if (!job.rmeta32.empty()) {
@@ -743,55 +1045,98 @@ static mnmt_status upload_job(mnmt_model* m, const Job& job) {
 
 static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook* hook,
                            bool use_graphs) {
-  auto& w = m->ws;
   const auto& c = m->c;
   const int64_t d = c.d_model;
   int64_t launches = 0, steps = 0;
+  // fan out: every lane waits for the uploads on the main stream
+  CK(cudaEventRecord(m->ev_job, m->st));
+  std::vector<char> used(m->lanes.size(), 0);
+  for (const Batch& b : job.batches) used[b.lane] = 1;
+  for (size_t li = 0; li < m->lanes.size(); ++li)
+    if (used[li]) CK(cudaStreamWaitEvent(m->lanes[li].st, m->ev_job, 0));
   for (size_t bi = 0; bi < job.batches.size(); ++bi) {
     const Batch& b = job.batches[bi];
+    Lane& Ln = m->lanes[b.lane];
+    auto& w = Ln.ws;
+    cudaStream_t st = Ln.st;
     const int B = (int)b.rows.size();
-    const int32_t* r32 = w.rmeta32 + 4 * job.r0[bi];
-    const int64_t* r64 = w.rmeta64 + 2 * job.r0[bi];
-    CK(cudaMemcpyAsync(w.row_start, r32, B * 4, cudaMemcpyDeviceToDevice, m->st));
-    CK(cudaMemcpyAsync(w.row_len, r32 + B, B * 4, cudaMemcpyDeviceToDevice, m->st));
-    CK(cudaMemcpyAsync(w.max_len, r32 + 2 * B, B * 4, cudaMemcpyDeviceToDevice, m->st));
-    CK(cudaMemcpyAsync(w.len_idx, r32 + 3 * B, B * 4, cudaMemcpyDeviceToDevice, m->st));
-    CK(cudaMemcpyAsync(w.out_off, r64, B * 8, cudaMemcpyDeviceToDevice, m->st));
-    if (forced) CK(cudaMemcpyAsync(w.forced_off, r64 + B, B * 8, cudaMemcpyDeviceToDevice, m->st));
-    const int32_t* base = w.meta + b.tok0;
+    const int32_t* r32 = m->jb.rmeta32 + 4 * job.r0[bi];
+    const int64_t* r64 = m->jb.rmeta64 + 2 * job.r0[bi];
+    CK(cudaMemcpyAsync(w.row_start, r32, B * 4, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(w.row_len, r32 + B, B * 4, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(w.max_len, r32 + 2 * B, B * 4, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(w.len_idx, r32 + 3 * B, B * 4, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(w.out_off, r64, B * 8, cudaMemcpyDeviceToDevice, st));
+    if (forced) CK(cudaMemcpyAsync(w.forced_off, r64 + B, B * 8, cudaMemcpyDeviceToDevice, st));
+    const int32_t* base = m->jb.meta + b.tok0;
     const int M = (int)b.M;
-    CK(launch_encoder(m, M, B, base, base + M, base + 2 * M, base + 3 * M, &launches));
+    CK(launch_encoder(m, Ln, M, B, base, base + M, base + 2 * M, base + 3 * M, &launches));
     if (c.decoder == 1)
-      CK(cudaMemsetAsync(w.C, 0, (size_t)c.dec_layers * w.B_cap * d * sizeof(float), m->st));
-    CK(launch_decode_init(w.ctrl, w.live, B, w.keys, m->st));
+      CK(cudaMemsetAsync(w.C, 0, (size_t)c.dec_layers * w.B_cap * d * sizeof(float), st));
+    CK(launch_decode_init(w.ctrl, w.live, B, w.keys, st));
     launches += 1;
     const int npad = (B + 127) / 128 * 128;
-    if (use_graphs && !hook) {
-      auto it = m->graphs.find(npad);
-      if (it == m->graphs.end()) {
+    if (m->megakernel && (!hook || hook->megakernel_ok())) {
+      if (!Ln.d_phases || Ln.prog_forced != forced || Ln.prog_out != m->jb.out_ids)
+        CKS(build_program(m, Ln, forced));
+      StepArgs sa{};
+      sa.phases = Ln.d_phases;
+      sa.n_phases = Ln.n_phases;
+      sa.ctrl = w.ctrl;
+      sa.bar = Ln.d_bar;
+      if (!hook) {
+        sa.max_steps = b.T;
+        CK(launch_step_kernel(sa, (int)d, st));
+        launches += 1;
+      } else {
+        sa.max_steps = 1;
+        for (int t = 0; t < b.T; ++t) {
+          CK(launch_step_kernel(sa, (int)d, st));
+          launches += 1;
+        }
+      }
+    } else if (use_graphs && !hook) {
+      auto it = Ln.graphs.find(npad);
+      if (it == Ln.graphs.end()) {
         cudaGraph_t g;
-        CK(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         int64_t per_step = 0;
-        cudaError_t e = launch_step(m, npad, forced, nullptr, &per_step);
-        cudaError_t e2 = cudaStreamEndCapture(m->st, &g);
+        cudaError_t e = launch_step(m, Ln, npad, forced, nullptr, &per_step);
+        cudaError_t e2 = cudaStreamEndCapture(st, &g);
         CK(e);
         CK(e2);
         cudaGraphExec_t ge;
         CK(cudaGraphInstantiate(&ge, g, 0));
         cudaGraphDestroy(g);
-        it = m->graphs.emplace(npad, ge).first;
-        m->launches_per_step = per_step;
+        it = Ln.graphs.emplace(npad, ge).first;
+        Ln.launches_per_step = per_step;
       }
-      for (int t = 0; t < b.T; ++t) CK(cudaGraphLaunch(it->second, m->st));
-      launches += (int64_t)b.T * m->launches_per_step;
+      for (int t = 0; t < b.T; ++t) CK(cudaGraphLaunch(it->second, st));
+      launches += (int64_t)b.T * Ln.launches_per_step;
     } else {
-      for (int t = 0; t < b.T; ++t) CK(launch_step(m, npad, forced, hook, &launches));
+      for (int t = 0; t < b.T; ++t) CK(launch_step(m, Ln, npad, forced, hook, &launches));
     }
     steps += b.T;
   }
+  // join: the main stream waits for every lane
+  for (size_t li = 0; li < m->lanes.size(); ++li)
+    if (used[li]) {
+      CK(cudaEventRecord(m->lanes[li].ev, m->lanes[li].st));
+      CK(cudaStreamWaitEvent(m->st, m->lanes[li].ev, 0));
+    }
   m->stats.gpu_launches += launches;
   m->stats.decode_steps += steps;
   m->stats.batches += (int64_t)job.batches.size();
+  return MNMT_OK;
+}
+
+// Sizes every lane a job uses.
+static mnmt_status ensure_lanes(mnmt_model* m, const Job& job, int64_t forced_O) {
+  for (size_t li = 0; li < job.lane_M.size(); ++li) {
+    if (job.lane_B[li] == 0) continue;
+    CKS(lane_init(m, m->lanes[li]));
+    CKS(lane_ensure(m, m->lanes[li], job.lane_M[li], job.lane_B[li], job.lane_T[li], forced_O));
+  }
   return MNMT_OK;
 }
 
@@ -865,6 +1210,7 @@ mnmt_status mnmt_model_create(const mnmt_config* cfg, int32_t cuda_device, mnmt_
     DeviceGuard g0(cuda_device);
     cudaError_t e = gemm_init();
     if (e == cudaSuccess) e = attn_init();
+    if (e == cudaSuccess && step_kernel_grid() <= 0) e = cudaErrorInvalidConfiguration;
     if (e != cudaSuccess) {
       set_err("kernel init failed: %s", cudaGetErrorString(e));
       return MNMT_ERR_CUDA;
@@ -874,9 +1220,12 @@ mnmt_status mnmt_model_create(const mnmt_config* cfg, int32_t cuda_device, mnmt_
   m->c = *cfg;
   m->dev = cuda_device;
   build_manifest(m);
+  m->lanes.resize(1);
   if (cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&m->ev_in, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&m->ev_out, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&m->ev_out, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&m->ev_job, cudaEventDisableTiming) != cudaSuccess ||
+      lane_init(m, m->lanes[0]) != MNMT_OK) {
     set_err("stream/event creation failed");
     delete m;
     return MNMT_ERR_CUDA;
@@ -1025,6 +1374,7 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
   DeviceGuard g(m->dev);
   if ((s = begin_call(m, cuda_stream)) != MNMT_OK) return fail(m, s);
   std::vector<std::vector<int32_t>> rows;
+  std::vector<int> lanes_of;
   if (sorted_batches) {
     if (budget < 1) { set_err("word_budget < 1"); return MNMT_ERR_ARG; }
     std::vector<int32_t> L(n), order(std::max(n, 1)), off(n + 2);
@@ -1032,25 +1382,37 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
     int32_t nb = 0;
     mnmt_batch_by_words(L.data(), n, budget, order.data(), off.data(), &nb);
     // Waves: consecutive batches decoded together while the wave holds at most
-    // max_concurrent_rows sentences (scheduling only; results are row-independent).
+    // max_concurrent_rows sentences; each wave's sentences are dealt round-robin (in
+    // length order) to the decoder lanes, which run concurrently.  Scheduling only:
+    // rows are independent, so the ids do not depend on it.
+    const int P = std::max(1, m->n_lanes);
     for (int b = 0; b < nb;) {
       int e = b + 1;
       if (m->max_concurrent_rows > 0)
         while (e < nb && off[e + 1] - off[b] <= m->max_concurrent_rows) ++e;
-      rows.emplace_back(order.begin() + off[b], order.begin() + off[e]);
+      for (int li = 0; li < P; ++li) {
+        std::vector<int32_t> part;
+        for (int i = off[b] + li; i < off[e]; i += P) part.push_back(order[i]);
+        if (!part.empty()) {
+          rows.push_back(std::move(part));
+          lanes_of.push_back(li);
+        }
+      }
       b = e;
     }
   } else {
     rows.emplace_back(n);
     std::iota(rows[0].begin(), rows[0].end(), 0);
+    lanes_of.push_back(0);
   }
   Job job;
-  plan_job(src_off, n, max_len, rows, job);
+  plan_job(src_off, n, max_len, rows, lanes_of, (int)m->lanes.size(), job);
   plan_rows(job, src_off, max_len, false, nullptr);
-  if ((s = ws_ensure(m, job.maxM, job.maxB, job.maxT, std::max<int64_t>(O, 1), std::max(n, 1),
-                     std::max<int64_t>(ntok, 1), (int64_t)job.meta.size(), job.rows_total)) != MNMT_OK)
+  if ((s = jb_ensure(m, std::max<int64_t>(O, 1), std::max(n, 1), std::max<int64_t>(ntok, 1),
+                     (int64_t)job.meta.size(), job.rows_total)) != MNMT_OK)
     return fail(m, s);
-  auto& w = m->ws;
+  if ((s = ensure_lanes(m, job, 1)) != MNMT_OK) return fail(m, s);
+  auto& w = m->jb;
   if ((s = upload_job(m, job)) != MNMT_OK) return fail(m, s);
   if (ntok > 0) {
     CK(cudaMemcpyAsync(w.src_ids, src_ids, ntok * 4,
@@ -1058,7 +1420,7 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
     if (!dev_io) m->stats.h2d_bytes += ntok * 4;
   }
   if (dev_io && ntok > 0) {
-    int32_t* bad = w.ctrl + 32;
+    int32_t* bad = m->lanes[0].ws.ctrl + 32;
     CK(cudaMemsetAsync(bad, 0, 4, m->st));
     k_count_bad_ids<<<148, 256, 0, m->st>>>(w.src_ids, ntok, m->c.vocab, bad);
     int32_t hbad = 0;
@@ -1112,17 +1474,18 @@ struct DumpHook : StepHook {
   std::vector<float> buf;
   std::vector<int8_t> cbuf;
   int t = 0;                       // current step (1-based), tracked on host
+  bool megakernel_ok() const override { return mask == 0; }
 
   cudaError_t fetch_live(mnmt_model* m, int* n_live) {
     int32_t ctrl[2];
     cudaError_t e;
-    if ((e = cudaMemcpyAsync(ctrl, m->ws.ctrl, 8, cudaMemcpyDeviceToHost, m->st)) != cudaSuccess) return e;
-    if ((e = cudaStreamSynchronize(m->st)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(ctrl, m->lanes[0].ws.ctrl, 8, cudaMemcpyDeviceToHost, m->lanes[0].st)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(m->lanes[0].st)) != cudaSuccess) return e;
     *n_live = ctrl[0];
     t = ctrl[1];
     live.resize(std::max(1, ctrl[0]));
-    if ((e = cudaMemcpyAsync(live.data(), m->ws.live, (size_t)ctrl[0] * 4, cudaMemcpyDeviceToHost, m->st)) != cudaSuccess) return e;
-    return cudaStreamSynchronize(m->st);
+    if ((e = cudaMemcpyAsync(live.data(), m->lanes[0].ws.live, (size_t)ctrl[0] * 4, cudaMemcpyDeviceToHost, m->lanes[0].st)) != cudaSuccess) return e;
+    return cudaStreamSynchronize(m->lanes[0].st);
   }
   cudaError_t grab(mnmt_model* m, const float* src, char* base, int64_t row_elems, int64_t slot,
                    int64_t slots) {
@@ -1131,8 +1494,8 @@ struct DumpHook : StepHook {
     cudaError_t e;
     if ((e = fetch_live(m, &nl)) != cudaSuccess) return e;
     buf.resize((size_t)std::max(1, nl) * d);
-    if ((e = cudaMemcpyAsync(buf.data(), src, (size_t)nl * d * 4, cudaMemcpyDeviceToHost, m->st)) != cudaSuccess) return e;
-    if ((e = cudaStreamSynchronize(m->st)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(buf.data(), src, (size_t)nl * d * 4, cudaMemcpyDeviceToHost, m->lanes[0].st)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(m->lanes[0].st)) != cudaSuccess) return e;
     for (int r = 0; r < nl; ++r) {
       const int64_t row = foff[live[r]] + t - 1;
       std::memcpy(base + ((row * slots + slot) * row_elems) * 4, buf.data() + (size_t)r * d, (size_t)d * 4);
@@ -1141,26 +1504,26 @@ struct DumpHook : StepHook {
   }
   cudaError_t x1(mnmt_model* m, int l) override {
     if (!(mask & MNMT_DUMP_LAYERS)) return cudaSuccess;
-    return grab(m, m->ws.x1, layers, m->c.d_model, (int64_t)l * 3 + 0, (int64_t)m->c.dec_layers * 3);
+    return grab(m, m->lanes[0].ws.x1, layers, m->c.d_model, (int64_t)l * 3 + 0, (int64_t)m->c.dec_layers * 3);
   }
   cudaError_t x2(mnmt_model* m, int l) override {
     if (!(mask & MNMT_DUMP_LAYERS)) return cudaSuccess;
-    return grab(m, m->ws.x2, layers, m->c.d_model, (int64_t)l * 3 + 1, (int64_t)m->c.dec_layers * 3);
+    return grab(m, m->lanes[0].ws.x2, layers, m->c.d_model, (int64_t)l * 3 + 1, (int64_t)m->c.dec_layers * 3);
   }
   cudaError_t layer(mnmt_model* m, int l) override {
     cudaError_t e;
     const int d = m->c.d_model;
     if (mask & MNMT_DUMP_LAYERS)
-      if ((e = grab(m, m->ws.y, layers, d, (int64_t)l * 3 + 2, (int64_t)m->c.dec_layers * 3)) != cudaSuccess) return e;
+      if ((e = grab(m, m->lanes[0].ws.y, layers, d, (int64_t)l * 3 + 2, (int64_t)m->c.dec_layers * 3)) != cudaSuccess) return e;
     if (l != m->c.dec_layers - 1) return cudaSuccess;
     if (mask & MNMT_DUMP_DEC_OUT)
-      if ((e = grab(m, m->ws.y, dec_out, d, 0, 1)) != cudaSuccess) return e;
+      if ((e = grab(m, m->lanes[0].ws.y, dec_out, d, 0, 1)) != cudaSuccess) return e;
     if (mask & MNMT_DUMP_OUT_CODES) {
       int nl = 0;
       if ((e = fetch_live(m, &nl)) != cudaSuccess) return e;
       cbuf.resize((size_t)std::max(1, nl) * d);
-      if ((e = cudaMemcpyAsync(cbuf.data(), m->ws.cy, (size_t)nl * d, cudaMemcpyDeviceToHost, m->st)) != cudaSuccess) return e;
-      if ((e = cudaStreamSynchronize(m->st)) != cudaSuccess) return e;
+      if ((e = cudaMemcpyAsync(cbuf.data(), m->lanes[0].ws.cy, (size_t)nl * d, cudaMemcpyDeviceToHost, m->lanes[0].st)) != cudaSuccess) return e;
+      if ((e = cudaStreamSynchronize(m->lanes[0].st)) != cudaSuccess) return e;
       for (int r = 0; r < nl; ++r)
         std::memcpy(out_codes + (foff[live[r]] + t - 1) * d, cbuf.data() + (size_t)r * d, d);
     }
@@ -1202,17 +1565,19 @@ extern "C" mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids,
   std::vector<std::vector<int32_t>> rows(1, std::vector<int32_t>(n));
   std::iota(rows[0].begin(), rows[0].end(), 0);
   Job job;
-  plan_job(src_off, n, ml.data(), rows, job);
+  plan_job(src_off, n, ml.data(), rows, std::vector<int>(1, 0), (int)m->lanes.size(), job);
   // forced_off doubles as the output offset in forced mode (out layout == forced layout)
   job.out_off.assign(forced_off, forced_off + n + 1);
   plan_rows(job, src_off, ml.data(), true, forced_off);
-  if ((s = ws_ensure(m, job.maxM, job.maxB, job.maxT, std::max<int64_t>(O, 1), std::max(n, 1),
-                     std::max<int64_t>(ntok, 1), (int64_t)job.meta.size(), job.rows_total)) != MNMT_OK)
+  if ((s = jb_ensure(m, std::max<int64_t>(O, 1), std::max(n, 1), std::max<int64_t>(ntok, 1),
+                     (int64_t)job.meta.size(), job.rows_total)) != MNMT_OK)
     return fail(m, s);
-  auto& w = m->ws;
+  if ((s = ensure_lanes(m, job, std::max<int64_t>(O, 1))) != MNMT_OK) return fail(m, s);
+  auto& w = m->jb;
+  Workspace& w0 = m->lanes[0].ws;
   if ((s = upload_job(m, job)) != MNMT_OK) return fail(m, s);
   if (ntok > 0) CK(cudaMemcpyAsync(w.src_ids, src_ids, ntok * 4, cudaMemcpyHostToDevice, m->st));
-  if (O > 0) CK(cudaMemcpyAsync(w.forced, forced_ids, O * 4, cudaMemcpyHostToDevice, m->st));
+  if (O > 0) CK(cudaMemcpyAsync(w0.forced, forced_ids, O * 4, cudaMemcpyHostToDevice, m->st));
   CK(cudaMemsetAsync(w.out_len, 0, (size_t)std::max(n, 1) * 4, m->st));
   char* p = static_cast<char*>(dump_host);
   char* enc_out = nullptr;
@@ -1234,11 +1599,11 @@ extern "C" mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids,
     for (int i = 0; i < n; ++i) {
       const int64_t S = src_off[i + 1] - src_off[i];
       if (ml[i] == 0 || S == 0) continue;
-      if (enc_out) CK(cudaMemcpyAsync(enc_out + src_off[i] * d * 4, w.x + t * d, S * d * 4, cudaMemcpyDeviceToHost, m->st));
+      if (enc_out) CK(cudaMemcpyAsync(enc_out + src_off[i] * d * 4, w0.x + t * d, S * d * 4, cudaMemcpyDeviceToHost, m->st));
       if (src_kv)
         for (int64_t l = 0; l < L; ++l)
           CK(cudaMemcpyAsync(src_kv + ((l * ntok + src_off[i]) * 2 * d) * 4,
-                             w.kv + (l * w.M_cap + t) * 2 * d, S * 2 * d * 4, cudaMemcpyDeviceToHost, m->st));
+                             w0.kv + (l * w0.M_cap + t) * 2 * d, S * 2 * d * 4, cudaMemcpyDeviceToHost, m->st));
       t += S;
     }
   }
@@ -1252,6 +1617,19 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
   if (std::string(name) == "max_concurrent_rows") {
     if (value < 0) { set_err("max_concurrent_rows < 0"); return MNMT_ERR_ARG; }
     m->max_concurrent_rows = value;
+    return MNMT_OK;
+  }
+  if (std::string(name) == "megakernel") {
+    if (value != 0 && value != 1) { set_err("megakernel must be 0 or 1"); return MNMT_ERR_ARG; }
+    m->megakernel = (int)value;
+    return MNMT_OK;
+  }
+  if (std::string(name) == "lanes") {
+    if (value < 1 || value > 16) { set_err("lanes must be 1..16"); return MNMT_ERR_ARG; }
+    DeviceGuard g(m->dev);
+    cudaDeviceSynchronize();
+    if ((int64_t)m->lanes.size() < value) m->lanes.resize(value);
+    m->n_lanes = (int)value;
     return MNMT_OK;
   }
   set_err("unknown option '%s'", name);
@@ -1268,12 +1646,18 @@ extern "C" void mnmt_model_destroy(mnmt_model* m) {
   if (!m) return;
   {
     DeviceGuard g(m->dev);
-    cudaStreamSynchronize(m->st);
-    ws_free(m);
+    cudaDeviceSynchronize();
+    for (Lane& L : m->lanes) {
+      lane_free(L);
+      if (L.st) cudaStreamDestroy(L.st);
+      if (L.ev) cudaEventDestroy(L.ev);
+    }
+    jb_free(m);
     for (void* p : m->allocs) cudaFree(p);
     if (m->st) cudaStreamDestroy(m->st);
     if (m->ev_in) cudaEventDestroy(m->ev_in);
     if (m->ev_out) cudaEventDestroy(m->ev_out);
+    if (m->ev_job) cudaEventDestroy(m->ev_job);
     cudaGetLastError();
   }
   delete m;

@@ -86,12 +86,29 @@ def test_tiny_teacher_forced(dims):
 
 
 @pytest.mark.parametrize("dims", TINY_VARIANTS, ids=lambda d: d.name)
+def test_tiny_teacher_forced_persistent_kernel(dims):
+    """Teacher forcing through the persistent step kernel (no dumps): per-step ids bit-exact."""
+    w, om, gm = pair(dims, 13)
+    ss, forced, foff = forced_case(dims, 11, 0, 13, 0, 17, seed=4)
+    for mk in (1, 0):
+        gm.set_option("megakernel", mk)
+        ids, _ = gm.decode_forced(ss, forced, foff, 0)
+        for i in range(ss.n):
+            T = int(foff[i + 1] - foff[i])
+            f = forced[foff[i]:foff[i + 1]]
+            oids = om.decode_one(ss.ids[ss.offsets[i]:ss.offsets[i + 1]], T, forced=f)
+            assert np.array_equal(ids[foff[i]:foff[i + 1]], oids), (dims.name, mk, i)
+
+
+@pytest.mark.parametrize("dims", TINY_VARIANTS, ids=lambda d: d.name)
 def test_tiny_free_running(dims):
     w, om, gm = pair(dims, 12)
     ss = synth.random_set(17, 1, 15, seed=5, vocab=dims.vocab)
     ref = om.decode_many(ss, 4)
-    got = gm.decode(ss)
-    assert all(np.array_equal(a, b) for a, b in zip(got, ref))
+    for mk in (1, 0):          # persistent step kernel / one kernel per op (graph)
+        gm.set_option("megakernel", mk)
+        got = gm.decode(ss)
+        assert all(np.array_equal(a, b) for a, b in zip(got, ref)), mk
 
 
 def test_config0_tiny192_aan():
@@ -138,10 +155,13 @@ def test_batch_and_order_invariance():
     base = gm.translate(ss, 1 << 20)
     for budget in (1, 64, 333, 4096):
         assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, budget), base))
-    for rows in (7, 50, 1 << 20):          # co-scheduled batch waves: identical ids
-        gm.set_option("max_concurrent_rows", rows)
-        assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, 64), base))
+    for lanes in (1, 2, 3):                # concurrent decoder lanes: identical ids
+        gm.set_option("lanes", lanes)
+        for rows in (7, 50, 1 << 20):      # co-scheduled batch waves: identical ids
+            gm.set_option("max_concurrent_rows", rows)
+            assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, 64), base))
     gm.set_option("max_concurrent_rows", 0)
+    gm.set_option("lanes", 1)
     perm = np.random.default_rng(3).permutation(ss.n)
     sub = gm.decode(ss.subset(perm))
     assert all(np.array_equal(sub[k], base[perm[k]]) for k in range(ss.n))
