@@ -277,7 +277,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--megakernel", type=int, default=1,
+    ap.add_argument("--megakernel", type=int, default=0,
                     help="1: persistent step kernel per batch; 0: one kernel per op (CUDA graph)")
     ap.add_argument("--lanes", type=int, default=1,
                     help="independent decoder lanes (streams) per GPU (scheduling only)")

@@ -150,9 +150,9 @@ mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids_host,
  *   "lanes"                1..16 independent decoders (workspace + stream + step graph);
  *                          each wave's sentences are dealt round-robin to the lanes in
  *                          length order and the lanes' kernel chains overlap (default 1).
- *   "megakernel"           1 (default): each batch's decoder steps run in ONE persistent
+ *   "megakernel"           1: each batch's decoder steps run in ONE persistent
  *                          cooperative kernel (phases separated by grid barriers);
- *                          0: one kernel per operation, replayed as a CUDA graph per step.
+ *                          0 (default): one kernel per operation, replayed as a CUDA graph per step.
  * Errors: MNMT_ERR_ARG (unknown name or negative value). */
 mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, int64_t value);
 

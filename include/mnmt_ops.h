@@ -76,6 +76,13 @@ mnmt_status mnmt_op_attention(const float* q_dev, int64_t ldq, const float* kv_d
                               const int32_t* kv_len_dev, int32_t n, int32_t d, int32_t H,
                               float clip, int8_t* out_q_dev, float* out_f_dev, void* stream);
 
+/* Profiling hook: with model option "profile_phases" = 1, the persistent step kernel of
+ * lane 0 stamps %globaltimer after every grid barrier.  out_ns_by_type[k] receives the
+ * nanoseconds spent in phases of type k (0 GEMM, 1 embed, 2 LayerNorm, 3 attention,
+ * 4 finish) summed over the *steps_out steps of the last batch.  n_types >= 5. */
+mnmt_status mnmt_debug_phase_profile(mnmt_model* m, int64_t* out_ns_by_type, int32_t n_types,
+                                     int32_t* steps_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -120,6 +120,9 @@ struct Lane {
   const int32_t* prog_out = nullptr;   // job output buffer the program writes to
   CUtensorMap* d_tmaps = nullptr;
   unsigned* d_bar = nullptr;
+  std::vector<int> phase_types;             // host copy, for profiling
+  unsigned long long* d_timing = nullptr;   // phase timestamps of the last launch (option)
+  int64_t timing_steps = 0;
 };
 
 }  // namespace
@@ -145,7 +148,8 @@ struct mnmt_model {
   mnmt_stats stats{};
   int max_pos = MNMT_MAX_SPAN + 1;
   int64_t max_concurrent_rows = 0;   // option: co-schedule batches in waves of <= this many rows
-  int megakernel = 1;                  // option: persistent step kernel (1) or one kernel per op (0)
+  int megakernel = 0;                  // option: persistent step kernel (1) or one kernel per op (0)
+  int profile_phases = 0;              // option: record per-phase timestamps (lane 0)
 };
 
 namespace {
@@ -296,6 +300,9 @@ static void lane_free(Lane& L) {
   if (L.d_phases) cudaFree(L.d_phases);
   if (L.d_tmaps) cudaFree(L.d_tmaps);
   if (L.d_bar) cudaFree(L.d_bar);
+  if (L.d_timing) cudaFree(L.d_timing);
+  L.d_timing = nullptr;
+  L.timing_steps = 0;
   L.d_phases = nullptr;
   L.d_tmaps = nullptr;
   L.d_bar = nullptr;
@@ -903,6 +910,8 @@ static mnmt_status build_program(mnmt_model* m, Lane& Ln, bool forced) {
     CK(cudaMemset(Ln.d_bar, 0, 64 * sizeof(unsigned)));
   }
   Ln.n_phases = (int)pb.ph.size();
+  Ln.phase_types.clear();
+  for (const Phase& P : pb.ph) Ln.phase_types.push_back(P.type);
   Ln.prog_forced = forced;
   Ln.prog_out = m->jb.out_ids;
   return MNMT_OK;
@@ -1084,6 +1093,16 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
       sa.n_phases = Ln.n_phases;
       sa.ctrl = w.ctrl;
       sa.bar = Ln.d_bar;
+      if (m->profile_phases && b.lane == 0 && !hook) {
+        const int64_t need = (int64_t)b.T * (Ln.n_phases + 1);
+        if (Ln.timing_steps < b.T) {
+          if (Ln.d_timing) cudaFree(Ln.d_timing);
+          CK(cudaMalloc(&Ln.d_timing, need * sizeof(unsigned long long)));
+          Ln.timing_steps = b.T;
+        }
+        CK(cudaMemsetAsync(Ln.d_timing, 0, need * sizeof(unsigned long long), st));
+        sa.timing = Ln.d_timing;
+      }
       if (!hook) {
         sa.max_steps = b.T;
         CK(launch_step_kernel(sa, (int)d, st));
@@ -1619,6 +1638,10 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
     m->max_concurrent_rows = value;
     return MNMT_OK;
   }
+  if (std::string(name) == "profile_phases") {
+    m->profile_phases = value ? 1 : 0;
+    return MNMT_OK;
+  }
   if (std::string(name) == "megakernel") {
     if (value != 0 && value != 1) { set_err("megakernel must be 0 or 1"); return MNMT_ERR_ARG; }
     m->megakernel = (int)value;
@@ -1634,6 +1657,57 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
   }
   set_err("unknown option '%s'", name);
   return MNMT_ERR_ARG;
+}
+
+// Per-phase-type time of the last persistent-kernel launch of lane 0 (option
+// "profile_phases"): out[type] += ns spent in phases of that type; returns #steps recorded.
+extern "C" mnmt_status mnmt_debug_phase_profile(mnmt_model* m, int64_t* out_ns_by_type,
+                                                int32_t n_types, int32_t* steps_out) {
+  if (!m || !out_ns_by_type || !steps_out || n_types < 5) { set_err("bad arguments"); return MNMT_ERR_ARG; }
+  Lane& L = m->lanes[0];
+  for (int i = 0; i < n_types; ++i) out_ns_by_type[i] = 0;
+  *steps_out = 0;
+  if (!L.d_timing || L.timing_steps == 0) return MNMT_OK;
+  DeviceGuard g(m->dev);
+  std::vector<unsigned long long> t((size_t)L.timing_steps * (L.n_phases + 1));
+  CK(cudaMemcpy(t.data(), L.d_timing, t.size() * 8, cudaMemcpyDeviceToHost));
+  int steps = 0;
+  for (int64_t s = 0; s < L.timing_steps; ++s) {
+    const unsigned long long* r = t.data() + s * (L.n_phases + 1);
+    if (r[0] == 0 || r[L.n_phases] == 0) break;
+    for (int p = 0; p < L.n_phases; ++p) out_ns_by_type[L.phase_types[p]] += (int64_t)(r[p + 1] - r[p]);
+    ++steps;
+  }
+  *steps_out = steps;
+  return MNMT_OK;
+}
+
+// Average ns of every phase of the last persistent-kernel batch of lane 0; types[i] gets
+// the phase type.  Returns the number of phases written (<= cap) in *n_out.
+extern "C" mnmt_status mnmt_debug_phase_times(mnmt_model* m, int64_t* avg_ns, int32_t* types,
+                                              int32_t cap, int32_t* n_out) {
+  if (!m || !avg_ns || !types || !n_out) { set_err("bad arguments"); return MNMT_ERR_ARG; }
+  Lane& L = m->lanes[0];
+  *n_out = 0;
+  if (!L.d_timing || L.timing_steps == 0) return MNMT_OK;
+  DeviceGuard g(m->dev);
+  std::vector<unsigned long long> t((size_t)L.timing_steps * (L.n_phases + 1));
+  CK(cudaMemcpy(t.data(), L.d_timing, t.size() * 8, cudaMemcpyDeviceToHost));
+  const int np = std::min(cap, L.n_phases);
+  std::vector<int64_t> acc(np, 0);
+  int steps = 0;
+  for (int64_t s = 0; s < L.timing_steps; ++s) {
+    const unsigned long long* r = t.data() + s * (L.n_phases + 1);
+    if (r[0] == 0 || r[L.n_phases] == 0) break;
+    for (int p = 0; p < np; ++p) acc[p] += (int64_t)(r[p + 1] - r[p]);
+    ++steps;
+  }
+  for (int p = 0; p < np; ++p) {
+    avg_ns[p] = steps ? acc[p] / steps : 0;
+    types[p] = L.phase_types[p];
+  }
+  *n_out = np;
+  return MNMT_OK;
 }
 
 extern "C" mnmt_status mnmt_get_stats(const mnmt_model* m, mnmt_stats* out) {

@@ -49,7 +49,7 @@ __device__ __forceinline__ void aan4(float* C, float4 y, float tf, const AanOut&
 
 // ------------------------------------------------------------------ target embedding (A5)
 template <int NV>
-__device__ __forceinline__ void embed_tgt_row(const EmbedTgtArgs& a, int r) {
+__device__ __forceinline__ void embed_tgt_row(const EmbedTgtArgs a, int r) {
   const int lane = threadIdx.x & 31, d = a.d, d4 = d >> 2;
   const int t = a.ctrl[1];
   const int orig = a.live[r];
@@ -72,7 +72,7 @@ __device__ __forceinline__ void embed_tgt_row(const EmbedTgtArgs& a, int r) {
 
 // ------------------------------------------------------------------ residual + LayerNorm (+AAN)
 template <int NV>
-__device__ __forceinline__ void ln_row(const LnArgs& a, int r) {
+__device__ __forceinline__ void ln_row(const LnArgs a, int r) {
   const int lane = threadIdx.x & 31, d = a.d, d4 = d >> 2;
   const int64_t off = (int64_t)r * d;
   float4 v[NV];
@@ -196,7 +196,7 @@ __device__ __forceinline__ void warp_attend(const float* __restrict__ q, const f
 }
 
 // Attention of one (row, head) by one warp (SRC, SELF and ENC modes); sc = per-warp scratch.
-__device__ __forceinline__ void attn_row_head(const AttnArgs& a, int r, int h, double* sc) {
+__device__ __forceinline__ void attn_row_head(const AttnArgs a, int r, int h, double* sc) {
   const int lane = threadIdx.x & 31;
   const int dh = a.dh;
   int start, len;
@@ -231,7 +231,7 @@ __device__ __forceinline__ void attn_row_head(const AttnArgs& a, int r, int h, d
 // unless it is EOS; row is done at EOS or t == max_len (R16).  Then the live
 // list is compacted stably in place (new index <= old index, chunk by chunk).
 // Block-wide (any blockDim multiple of 32, <= 1024).  warp_cnt: smem [32], base_s: smem.
-__device__ __forceinline__ void finish_block(const FinishArgs& a, int32_t* warp_cnt,
+__device__ __forceinline__ void finish_block(const FinishArgs a, int32_t* warp_cnt,
                                              int32_t& base_s) {
   const int n_live = a.ctrl[0];
   const int t = a.ctrl[1];

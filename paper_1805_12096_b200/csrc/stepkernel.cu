@@ -43,6 +43,11 @@ constexpr int SK_TMEM_COLS = 512;
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async;" ::: "memory");
 }
@@ -100,7 +105,7 @@ __device__ __forceinline__ void tile_of(const Phase& P, const int* mt_live, int 
 }
 
 // Epilogue of one 32-column chunk of one row (same arithmetic as k_gemm_i8).
-__device__ __forceinline__ void epi_chunk(int epi, const GemmArgs& a, int row, bool row_ok, int n,
+__device__ __forceinline__ void epi_chunk(int epi, const GemmArgs a, int row, bool row_ok, int n,
                                           const int32_t* acc, float& best_v, int& best_j) {
   if (n >= a.N) return;
   if (epi == EPI_ARGMAX) {
@@ -162,6 +167,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1) k_step(const StepArgs s) {
   __shared__ int32_t fin_warp_cnt[32];
   __shared__ int32_t fin_base;
   __shared__ int mt_live_s[2];
+  __shared__ __align__(16) Phase sP;   // current phase descriptor (copied from global once)
 
   const uint32_t warp = warp_id(), lane = lane_id();
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sk_smem_raw) + 1023) &
@@ -193,8 +199,16 @@ __global__ void __launch_bounds__(SK_THREADS, 1) k_step(const StepArgs s) {
 
   for (int step = 0; step < s.max_steps; ++step) {
     if (*reinterpret_cast<const volatile int32_t*>(s.ctrl) <= 0) break;   // uniform
+    if (s.timing && blockIdx.x == 0 && threadIdx.x == 0)
+      s.timing[(size_t)step * (s.n_phases + 1)] = globaltimer_ns();
     for (int ph = 0; ph < s.n_phases; ++ph) {
-      const Phase& P = s.phases[ph];
+      {
+        const int4* src = reinterpret_cast<const int4*>(s.phases + ph);
+        int4* dst = reinterpret_cast<int4*>(&sP);
+        for (int i = threadIdx.x; i < (int)(sizeof(Phase) / 16); i += blockDim.x) dst[i] = src[i];
+      }
+      __syncthreads();
+      const Phase& P = sP;
       switch (P.type) {
         case PH_GEMM: {
           if (threadIdx.x == 0) {
@@ -216,18 +230,20 @@ __global__ void __launch_bounds__(SK_THREADS, 1) k_step(const StepArgs s) {
               for (int i = blockIdx.x; i < T; i += gridDim.x) {
                 int p, m0, n0;
                 tile_of(P, mt_live_s, i, p, m0, n0);
-                const GemmProb& G = P.g[p];
-                const int nkb = (G.a.K + SK_BK - 1) / SK_BK;
-                const uint32_t bytes = SK_A_BYTES + G.bn * SK_BK;
+                const CUtensorMap* tmA = P.g[p].tmA;
+                const CUtensorMap* tmB = P.g[p].tmB;
+                const int bn = P.g[p].bn;
+                const int nkb = (P.g[p].a.K + SK_BK - 1) / SK_BK;
+                const uint32_t bytes = SK_A_BYTES + bn * SK_BK;
                 for (int kb = 0; kb < nkb; ++kb) {
                   mbar_wait(&empty_bar[pp.ps], pp.pph ^ 1);
                   uint8_t* sa = ring + pp.ps * SK_STAGE;
                   uint8_t* sb = sa + SK_A_BYTES;
                   mbar_arrive_expect_tx(&full_bar[pp.ps], bytes);
-                  tma_load_2d(sa, G.tmA, &full_bar[pp.ps], kb * SK_BK, m0);
-                  tma_load_2d(sa + 64 * SK_BK, G.tmA, &full_bar[pp.ps], kb * SK_BK, m0 + 64);
-                  for (int j = 0; j < G.bn / 64; ++j)
-                    tma_load_2d(sb + j * 64 * SK_BK, G.tmB, &full_bar[pp.ps], kb * SK_BK, n0 + j * 64);
+                  tma_load_2d(sa, tmA, &full_bar[pp.ps], kb * SK_BK, m0);
+                  tma_load_2d(sa + 64 * SK_BK, tmA, &full_bar[pp.ps], kb * SK_BK, m0 + 64);
+                  for (int j = 0; j < bn / 64; ++j)
+                    tma_load_2d(sb + j * 64 * SK_BK, tmB, &full_bar[pp.ps], kb * SK_BK, n0 + j * 64);
                   if (++pp.ps == SK_STAGES) { pp.ps = 0; pp.pph ^= 1; }
                 }
               }
@@ -237,9 +253,8 @@ __global__ void __launch_bounds__(SK_THREADS, 1) k_step(const StepArgs s) {
               for (int i = blockIdx.x; i < T; i += gridDim.x) {
                 int p, m0, n0;
                 tile_of(P, mt_live_s, i, p, m0, n0);
-                const GemmProb& G = P.g[p];
-                const int nkb = (G.a.K + SK_BK - 1) / SK_BK;
-                const uint32_t idesc = idesc_rt(G.bn);
+                const int nkb = (P.g[p].a.K + SK_BK - 1) / SK_BK;
+                const uint32_t idesc = idesc_rt(P.g[p].bn);
                 mbar_wait(&tempty_bar[pp.ab], pp.aph ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + pp.ab * 256;
@@ -267,14 +282,15 @@ __global__ void __launch_bounds__(SK_THREADS, 1) k_step(const StepArgs s) {
             for (int i = blockIdx.x; i < T; i += gridDim.x) {
               int p, m0, n0;
               tile_of(P, mt_live_s, i, p, m0, n0);
-              const GemmProb& G = P.g[p];
-              const GemmArgs& a = G.a;
+              const GemmArgs a = P.g[p].a;     // registers: no reloads around global stores
+              const int epi = P.g[p].epi;
+              const int bn = P.g[p].bn;
               const int ml = a.M_dyn ? min(a.M, *a.M_dyn) : a.M;
               const int row = m0 + q * 32 + (int)lane;
               const bool row_ok = row < ml;
               mbar_wait(&tfull_bar[pp.ab], pp.aph);
               tc_fence_after();
-              const int HALF = G.bn >> 1;
+              const int HALF = bn >> 1;
               const uint32_t t_row = tmem_base + pp.ab * 256 + ((uint32_t)(q * 32) << 16) + half * HALF;
               float best_v = -INFINITY;
               int best_j = -1;
@@ -283,9 +299,9 @@ __global__ void __launch_bounds__(SK_THREADS, 1) k_step(const StepArgs s) {
                 tmem_ld16(t_row + c, *reinterpret_cast<int32_t(*)[16]>(acc));
                 tmem_ld16(t_row + c + 16, *reinterpret_cast<int32_t(*)[16]>(acc + 16));
                 tmem_ld_wait();
-                epi_chunk(G.epi, a, row, row_ok, n0 + half * HALF + c, acc, best_v, best_j);
+                epi_chunk(epi, a, row, row_ok, n0 + half * HALF + c, acc, best_v, best_j);
               }
-              if (G.epi == EPI_ARGMAX && row_ok && best_j >= 0)
+              if (epi == EPI_ARGMAX && row_ok && best_j >= 0)
                 atomicMax(a.keys + row, argmax_key(best_v, (uint32_t)best_j));
               tc_fence_before();
               __syncwarp();
@@ -299,20 +315,21 @@ __global__ void __launch_bounds__(SK_THREADS, 1) k_step(const StepArgs s) {
           break;
         }
         case PH_EMBED: {
-          const int n_live = P.em.ctrl[0];
-          for (int r = gwarp; r < n_live; r += nwarps_all) embed_tgt_row<NV>(P.em, r);
+          const EmbedTgtArgs a = P.em;
+          const int n_live = a.ctrl[0];
+          for (int r = gwarp; r < n_live; r += nwarps_all) embed_tgt_row<NV>(a, r);
           fence_proxy_async();
           break;
         }
         case PH_LN: {
-          const LnArgs& a = P.ln;
+          const LnArgs a = P.ln;
           const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
           for (int r = gwarp; r < n_live; r += nwarps_all) ln_row<NV>(a, r);
           fence_proxy_async();
           break;
         }
         case PH_ATTN: {
-          const AttnArgs& a = P.at;
+          const AttnArgs a = P.at;
           const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
           const int total = n_live * a.H;
           for (int i = gwarp; i < total; i += nwarps_all) {
@@ -324,16 +341,73 @@ __global__ void __launch_bounds__(SK_THREADS, 1) k_step(const StepArgs s) {
         }
         case PH_FINISH: {
           if (blockIdx.x == 0) finish_block(P.fi, fin_warp_cnt, fin_base);
+          __syncthreads();
           break;
         }
       }
       grid_sync(s.bar, gen);
+      if (s.timing && blockIdx.x == 0 && threadIdx.x == 0)
+        s.timing[(size_t)step * (s.n_phases + 1) + ph + 1] = globaltimer_ns();
     }
   }
 
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<SK_TMEM_COLS>(tmem_base);
+}
+
+// ------------------------------------------------------------------ barrier microbenchmark
+// mode 0: atomic counter + generation (as used);  mode 1: same without nanosleep;
+// mode 2: per-CTA arrival flags (no contended atomic) gathered by CTA 0, generation release.
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void grid_sync_flags(unsigned* flags, unsigned* genp, unsigned& gen) {
+  __syncthreads();
+  const unsigned g = gen + 1;
+  if (threadIdx.x == 0) st_release_gpu(flags + blockIdx.x * 32, g);   // one line per CTA
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += 32)
+      while (ld_acquire_gpu(flags + i * 32) < g) __nanosleep(0);
+    __syncwarp();
+    if (threadIdx.x == 0) st_release_gpu(genp, g);
+  }
+  if (threadIdx.x == 0)
+    while (ld_acquire_gpu(genp) < g) {}
+  gen = g;
+  __syncthreads();
+}
+
+__global__ void k_barrier_bench(unsigned* bar, int mode, int iters, unsigned long long* out) {
+  unsigned gen = ld_acquire_gpu(mode == 2 ? bar + 16384 : bar + 32);
+  __syncthreads();
+  grid_sync(bar, gen);
+  if (mode == 2) gen = ld_acquire_gpu(bar + 16384);
+  unsigned long long t0 = globaltimer_ns();
+  for (int i = 0; i < iters; ++i) {
+    if (mode == 2) {
+      grid_sync_flags(bar + 4096, bar + 16384, gen);
+    } else if (mode == 1) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const unsigned g = gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+          atomicExch(bar, 0u);
+          __threadfence();
+          atomicExch(bar + 32, g + 1);
+        } else {
+          while (ld_acquire_gpu(bar + 32) == g) {}
+        }
+        gen = g + 1;
+      }
+      __syncthreads();
+    } else {
+      grid_sync(bar, gen);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *out = (globaltimer_ns() - t0) / iters;
 }
 
 // ------------------------------------------------------------------ host side
@@ -378,6 +452,31 @@ cudaError_t launch_step_kernel(const StepArgs& a, int d, cudaStream_t st) {
     case 8: return cudaLaunchKernelEx(&cfg, k_step<8>, a);
   }
   return cudaErrorInvalidValue;
+}
+
+
+extern "C" long long mnmt_debug_barrier_ns(int mode, int iters) {
+  unsigned* bar = nullptr;
+  unsigned long long* out = nullptr;
+  if (cudaMalloc(&bar, 65536 * 4) != cudaSuccess) return -1;
+  cudaMemset(bar, 0, 65536 * 4);
+  cudaMalloc(&out, 8);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sms);
+  cfg.blockDim = dim3(SK_THREADS);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_barrier_bench, bar, mode, iters, out);
+  unsigned long long ns = 0;
+  if (e == cudaSuccess) e = cudaMemcpy(&ns, out, 8, cudaMemcpyDeviceToHost);
+  cudaFree(bar);
+  cudaFree(out);
+  return e == cudaSuccess ? (long long)ns : -1;
 }
 
 }  // namespace mnmt

@@ -25,7 +25,7 @@ struct GemmProb {
   int n_tiles;
 };
 
-struct Phase {
+struct alignas(16) Phase {
   int type;
   int nprob;                // PH_GEMM: 1 or 2 independent problems
   GemmProb g[2];
@@ -41,6 +41,7 @@ struct StepArgs {
   const int32_t* ctrl;      // [0] live rows, [1] t
   int max_steps;            // steps this launch may run (stops early when no row is live)
   unsigned int* bar;        // grid barrier state {count, pad..., generation}
+  unsigned long long* timing;   // optional: [max_steps][n_phases + 1] %globaltimer stamps
 };
 
 // Launch (cooperative, one CTA per SM) on `st`; d selects the row-kernel width.

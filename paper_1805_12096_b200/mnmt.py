@@ -50,7 +50,7 @@ EXPORTS = [
     "mnmt_batch_by_words", "mnmt_decode", "mnmt_translate", "mnmt_decode_forced",
     "mnmt_get_stats", "mnmt_last_error", "mnmt_model_destroy", "mnmt_model_set_option",
     "mnmt_op_quantize", "mnmt_op_gemm_i8", "mnmt_op_argmax_ids", "mnmt_op_layernorm",
-    "mnmt_op_aan_step", "mnmt_op_embed", "mnmt_op_attention",
+    "mnmt_op_aan_step", "mnmt_op_embed", "mnmt_op_attention", "mnmt_debug_phase_profile",
 ]
 
 _lib = None
@@ -88,6 +88,7 @@ def lib():
     L.mnmt_op_aan_step.argtypes = [P, P, I32, I32, I32, F, P, P, P]
     L.mnmt_op_embed.argtypes = [P, I32, P, P, I32, F, P, P, P]
     L.mnmt_op_attention.argtypes = [P, I64, P, I64, I32, I32, P, P, I32, I32, I32, F, P, P, P]
+    L.mnmt_debug_phase_profile.argtypes = [P, P, I32, P]
     for name in EXPORTS:
         fn = getattr(L, name)
         if name not in ("mnmt_config_default", "mnmt_last_error", "mnmt_model_destroy"):
@@ -169,6 +170,15 @@ class Model:
     def set_option(self, name: str, value: int) -> None:
         """Scheduling options (include/mnmt.h); never change results."""
         _check(lib().mnmt_model_set_option(self.h, name.encode(), int(value)))
+
+    def phase_profile(self):
+        """ns per phase type over the last persistent-kernel batch of lane 0 (option
+        "profile_phases"): ({"gemm":..,"embed":..,"ln":..,"attn":..,"finish":..}, steps)."""
+        out = np.zeros(8, np.int64)
+        steps = np.zeros(1, np.int32)
+        _check(lib().mnmt_debug_phase_profile(self.h, _p(out), 8, _p(steps)))
+        names = ["gemm", "embed", "ln", "attn", "finish"]
+        return {k: int(out[i]) for i, k in enumerate(names)}, int(steps[0])
 
     def stats(self) -> Dict[str, int]:
         s = Stats()

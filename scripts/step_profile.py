@@ -32,3 +32,16 @@ for lanes in [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "1,4").spli
         e.record(st); e.synchronize()
         stt = m.stats()
         print(f"lanes={lanes} steps<={cap_steps:4d}: {s.elapsed_time(e)/3:8.2f} ms  decode_steps={stt['decode_steps']} launches={stt['gpu_launches']}", flush=True)
+
+# per-phase-type breakdown of the persistent step kernel (lane 0, one wave)
+m.set_option("lanes", 1)
+m.set_option("megakernel", 1)
+m.set_option("profile_phases", 1)
+for cap_steps in (1, 200):
+    ml = np.minimum(ss.max_len, cap_steps).astype(np.int32)
+    m.translate_device(ids.data_ptr(), ss.offsets, ml, 8192, out.data_ptr(), cap, ln.data_ptr(), st)
+    torch.cuda.synchronize()
+    prof, steps = m.phase_profile()
+    tot = sum(prof.values())
+    print(f"steps={steps} total={tot/1e6:.2f} ms per-step={tot/max(steps,1)/1e3:.1f} us",
+          {k: f"{v/max(steps,1)/1e3:.1f}us" for k, v in prof.items()})
