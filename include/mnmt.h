@@ -153,6 +153,9 @@ mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids_host,
  *   "megakernel"           1: each batch's decoder steps run in ONE persistent
  *                          cooperative kernel (phases separated by grid barriers);
  *                          0 (default): one kernel per operation, replayed as a CUDA graph per step.
+ *   "fuse_ln"              1: residual / gate + LayerNorm + Q fused into the epilogue
+ *                          of the producing GEMM when one CTA can own whole rows (d = 192, 256);
+ *                          0 (default, measured faster): separate LayerNorm kernels.
  * Errors: MNMT_ERR_ARG (unknown name or negative value). */
 mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, int64_t value);
 

@@ -25,20 +25,255 @@
 
 namespace mnmt {
 
+static int num_sms();
+bool gemm_persistent(int M, int N, int bn);
+
 constexpr int BM = 128;           // MMA M (rows of A per tile)
 constexpr int BK = 128;           // K bytes per stage = one 128B swizzle atom row
 constexpr int EPI_WARPS = 8;      // two warps per TMEM lane quarter, splitting the columns
 constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
+constexpr int EPI_STAGE_LD = 33;                       // padded row stride (floats)
+constexpr int EPI_STAGE_FLOATS = 32 * EPI_STAGE_LD;    // per epilogue warp
+constexpr int EPI_STAGE_BYTES = EPI_WARPS * EPI_STAGE_FLOATS * 4;
 
 template <int BN>
 struct GemmCfg {
   static constexpr int A_BYTES = BM * BK;
   static constexpr int B_BYTES = BN * BK;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (196 * 1024 / STAGE_BYTES) > 8 ? 8 : (196 * 1024 / STAGE_BYTES);
-  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
-  static constexpr int smem_for(int stages) { return stages * STAGE_BYTES + 1024; }
+  static constexpr int STAGES = (190 * 1024 / STAGE_BYTES) > 8 ? 8 : (190 * 1024 / STAGE_BYTES);
+  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static constexpr int smem_for(int stages) { return stages * STAGE_BYTES + 1024 + EPI_STAGE_BYTES; }
 };
+
+// Exact (float)acc for |acc| < 2^22 without the quarter-rate I2F: place acc in the
+// mantissa of 1.5 * 2^23 and subtract.  Used when K <= 256 (|acc| <= 127^2 * 256 < 2^22).
+__device__ __forceinline__ float acc_to_float(int32_t acc, bool small) {
+  return small ? __fsub_rn(__int_as_float(0x4B400000 + acc), 12582912.0f) : __int2float_rn(acc);
+}
+
+
+// One 32-column chunk of the 32 rows of this warp (lane = row): dequant + fused op +
+// store, or running argmax.  fp32 outputs go through a padded per-warp smem tile so each
+// store instruction writes four full 128-byte lines.
+template <int EPI>
+__device__ __forceinline__ void epi_store_chunk(const GemmArgs& args, int row, bool row_ok, int n,
+                                                const int32_t (&acc)[32], float& best_v,
+                                                int& best_j, float* stage) {
+  const bool small = args.K <= 256;
+  const bool full = n + 32 <= args.N;
+  float bias[32];
+  if (args.bias && full) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      const float4 b4 = __ldg(reinterpret_cast<const float4*>(args.bias + n + j));
+      bias[j] = b4.x; bias[j + 1] = b4.y; bias[j + 2] = b4.z; bias[j + 3] = b4.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) bias[j] = (args.bias && n + j < args.N) ? __ldg(args.bias + n + j) : 0.0f;
+  }
+  if constexpr (EPI == EPI_ARGMAX) {
+    // Branch-free chunk maximum; the lowest column holding it is searched only when the
+    // chunk beats the running best, and a strictly greater value is required, so among
+    // equal logits the lowest column wins (R15).
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      v[j] = __fmaf_rn(acc_to_float(acc[j], small), args.scale, bias[j]);
+      if (!full && n + j >= args.N) v[j] = -INFINITY;
+    }
+    float m[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) m[j] = fmaxf(v[j], v[j + 16]);
+#pragma unroll
+    for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+      for (int j = 0; j < w; ++j) m[j] = fmaxf(m[j], m[j + w]);
+    if (m[0] > best_v) {
+      int jj = 31;
+#pragma unroll
+      for (int j = 31; j >= 0; --j) jj = (v[j] == m[0]) ? j : jj;
+      best_v = m[0];
+      best_j = n + jj;
+    }
+  } else if constexpr (EPI == EPI_ACC) {
+    if (row_ok) {
+      int4* dst = reinterpret_cast<int4*>(args.out_i + (int64_t)row * args.ldo + n);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (n + 4 * j < args.N)
+          dst[j] = make_int4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+    }
+  } else {
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      v[j] = __fmaf_rn(acc_to_float(acc[j], small), args.scale, bias[j]);
+      if constexpr (EPI == EPI_RELU_Q || EPI == EPI_RELU_F32_Q) v[j] = relu(v[j]);
+      if constexpr (EPI == EPI_SIGMOID) v[j] = sigmoid_f64(v[j]);
+    }
+    if constexpr (EPI == EPI_F32 || EPI == EPI_F32_Q || EPI == EPI_RELU_F32_Q || EPI == EPI_SIGMOID) {
+      // stage [32 rows][32 cols] then write rows cooperatively (8 lanes x float4 per row)
+      const int lane = threadIdx.x & 31;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) stage[lane * EPI_STAGE_LD + j] = v[j];
+      __syncwarp();
+      const int row0 = row - lane;
+      const int blk = n / args.col_block;   // 32-column chunks never straddle a block (16 | col_block)
+      float* base = args.out_f + (int64_t)blk * args.block_stride + (n - blk * args.col_block);
+      const int sub = lane >> 3, c4 = (lane & 7) * 4;
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int r = it * 4 + sub;
+        const bool ok = __shfl_sync(0xffffffffu, row_ok ? 1 : 0, r) != 0;
+        if (ok && n + c4 < args.N) {
+          const float* sr = stage + r * EPI_STAGE_LD + c4;
+          *reinterpret_cast<float4*>(base + (int64_t)(row0 + r) * args.ldo + c4) =
+              make_float4(sr[0], sr[1], sr[2], sr[3]);
+        }
+      }
+      __syncwarp();
+    }
+    if constexpr (EPI == EPI_F32_Q || EPI == EPI_RELU_Q || EPI == EPI_RELU_F32_Q) {
+      if (row_ok) {
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {          // two 16-column groups (N % 16 == 0)
+          const int ng = n + 16 * g;
+          if (ng >= args.N) break;
+          const float* vg = v + 16 * g;
+          uint32_t w[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint32_t b0 = (uint32_t)(q8(vg[4 * j + 0], args.clip, args.sigma) & 0xff);
+            uint32_t b1 = (uint32_t)(q8(vg[4 * j + 1], args.clip, args.sigma) & 0xff);
+            uint32_t b2 = (uint32_t)(q8(vg[4 * j + 2], args.clip, args.sigma) & 0xff);
+            uint32_t b3 = (uint32_t)(q8(vg[4 * j + 3], args.clip, args.sigma) & 0xff);
+            w[j] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
+          }
+          *reinterpret_cast<uint4*>(args.out_q + (int64_t)row * args.ldo + ng) =
+              make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// Full-row LayerNorm epilogue (EPI_LN, BN = d): the 8 epilogue warps hold the tile's 128
+// rows as two column halves per row.  Pass 1 forms the residual r (written to the output
+// row as scratch), passes 2-3 form the fp64 statistics (R20) with the two halves combined
+// through shared memory, pass 3 writes LN(r), Q(LN(r)) and the next layer's AAN step --
+// the arithmetic of ln_row / k_ln, with the row sums split into two ordered halves.
+template <int BN>
+__device__ __forceinline__ void ln_epilogue(const GemmArgs& a, uint32_t t_row, int row,
+                                            bool row_ok, int half, int rl, double* part) {
+  constexpr int HALF = BN / 2;
+  const LnArgs& L = a.ln;
+  const bool small = a.K <= 256;
+  const int c0 = half * HALF;
+  const int64_t off = (int64_t)row * BN;
+  const bool gate = L.gi != nullptr;
+  // ---- pass 1: residual (+ gate), sum
+  double s = 0.0;
+#pragma unroll 1
+  for (int c = 0; c < HALF; c += 32) {
+    int32_t acc[32];
+    tmem_ld16(t_row + c, *reinterpret_cast<int32_t(*)[16]>(acc));
+    tmem_ld16(t_row + c + 16, *reinterpret_cast<int32_t(*)[16]>(acc + 16));
+    tmem_ld_wait();
+    if (row_ok) {
+#pragma unroll 4
+      for (int j = 0; j < 32; ++j) {
+        const int col = c0 + c + j;
+        const float v = __fmaf_rn(acc_to_float(acc[j], small), a.scale, a.bias ? __ldg(a.bias + col) : 0.0f);
+        const float x = L.x[off + col];
+        float r;
+        if (gate) {
+          // AAN gate (R8): i = sigmoid(gi logit), f = sigmoid(v); z = fl(fl(i*y) + fl(f*a))
+          const float iy = __fmul_rn(sigmoid_f64(L.gi[off + col]), x);
+          const float fa = __fmul_rn(sigmoid_f64(v), L.delta[off + col]);
+          r = __fadd_rn(x, __fadd_rn(iy, fa));
+        } else {
+          r = __fadd_rn(x, v);
+        }
+        L.out[off + col] = r;
+        s = __dadd_rn(s, (double)r);
+      }
+    }
+  }
+  part[half * 128 + rl] = s;
+  epi_bar();
+  const double mu = __ddiv_rn(__dadd_rn(part[rl], part[128 + rl]), (double)BN);
+  epi_bar();
+  // ---- pass 2: variance
+  double qv = 0.0;
+  if (row_ok) {
+#pragma unroll 4
+    for (int j = 0; j < HALF; ++j) {
+      const double t = __dsub_rn((double)L.out[off + c0 + j], mu);
+      qv = __dadd_rn(qv, __dmul_rn(t, t));
+    }
+  }
+  part[half * 128 + rl] = qv;
+  epi_bar();
+  const double var = __ddiv_rn(__dadd_rn(part[rl], part[128 + rl]), (double)BN);
+  epi_bar();
+  const double inv = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(var, (double)L.eps)));
+  if (!row_ok) return;
+  // ---- pass 3: output, codes, AAN step of the next layer
+  const int orig = L.aan.C ? L.live[row] : 0;
+  const float tf = L.aan.C ? (float)L.ctrl[1] : 1.0f;
+#pragma unroll 1
+  for (int c = 0; c < HALF; c += 16) {
+    float o[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int col = c0 + c + j;
+      const double r = (double)L.out[off + col];
+      o[j] = (float)__dadd_rn(__dmul_rn(__dmul_rn(__dsub_rn(r, mu), inv), (double)L.gamma[col]),
+                              (double)L.beta[col]);
+    }
+#pragma unroll
+    for (int j = 0; j < 16; j += 4)
+      *reinterpret_cast<float4*>(L.out + off + c0 + c + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+    if (L.out_q) {
+      uint32_t w[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        w[j] = (uint32_t)(q8(o[4 * j], L.clip, L.sigma) & 0xff) |
+               ((uint32_t)(q8(o[4 * j + 1], L.clip, L.sigma) & 0xff) << 8) |
+               ((uint32_t)(q8(o[4 * j + 2], L.clip, L.sigma) & 0xff) << 16) |
+               ((uint32_t)(q8(o[4 * j + 3], L.clip, L.sigma) & 0xff) << 24);
+      *reinterpret_cast<uint4*>(L.out_q + off + c0 + c) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    if (L.aan.C) {
+      // AAN step (R6, R7): C <- fl(C + y); g = fl(C / t)
+      float* Cr = L.aan.C + (int64_t)orig * BN + c0 + c;
+      float g[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float cv = __fadd_rn(Cr[j], o[j]);
+        Cr[j] = cv;
+        g[j] = __fdiv_rn(cv, tf);
+      }
+      if (L.aan.g_f)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) L.aan.g_f[off + c0 + c + j] = g[j];
+      if (L.aan.g_q) {
+        uint32_t w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          w[j] = (uint32_t)(q8(g[4 * j], L.aan.clip, L.aan.sigma) & 0xff) |
+                 ((uint32_t)(q8(g[4 * j + 1], L.aan.clip, L.aan.sigma) & 0xff) << 8) |
+                 ((uint32_t)(q8(g[4 * j + 2], L.aan.clip, L.aan.sigma) & 0xff) << 16) |
+                 ((uint32_t)(q8(g[4 * j + 3], L.aan.clip, L.aan.sigma) & 0xff) << 24);
+        *reinterpret_cast<uint4*>(L.aan.g_q + off + c0 + c) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+  }
+}
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -50,6 +285,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __shared__ __align__(8) uint64_t empty_bar[Cfg::STAGES];
   __shared__ __align__(8) uint64_t tmem_full_bar;
   __shared__ uint32_t tmem_slot;
+  __shared__ double ln_part[EPI == EPI_LN ? 256 : 1];
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -155,8 +391,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tc_fence_after();
     if (warp == 2 && lane == 0) pdl_launch_dependents();
     const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + half * HALF;
+    float* stage = reinterpret_cast<float*>(smem + stages * Cfg::STAGE_BYTES) +
+                   (warp - 2) * EPI_STAGE_FLOATS;
     float best_v = -INFINITY;
     int best_j = -1;
+    if constexpr (EPI == EPI_LN) {
+      ln_epilogue<BN>(args, t_row, row, row_ok, half, q * 32 + lane, ln_part);
+    } else
 #pragma unroll 1
     for (int c = 0; c < HALF; c += 32) {
       int32_t acc[32];
@@ -165,71 +406,159 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tmem_ld_wait();
       const int n = n0 + half * HALF + c;
       if (n >= args.N) break;  // warp-uniform
-      if constexpr (EPI == EPI_ARGMAX) {
-        // strict '>' over increasing columns keeps the lowest column among equal logits (R15)
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          if (n + j < args.N) {
-            const float b = args.bias ? __ldg(args.bias + n + j) : 0.0f;
-            const float v = dequant(acc[j], args.scale, b);
-            if (v > best_v) { best_v = v; best_j = n + j; }
-          }
-        }
-      } else if constexpr (EPI == EPI_ACC) {
-        if (row_ok) {
-          int4* dst = reinterpret_cast<int4*>(args.out_i + (int64_t)row * args.ldo + n);
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (n + 4 * j < args.N)
-              dst[j] = make_int4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
-        }
-      } else {
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float b = (args.bias && n + j < args.N) ? __ldg(args.bias + n + j) : 0.0f;
-          v[j] = dequant(acc[j], args.scale, b);
-          if constexpr (EPI == EPI_RELU_Q || EPI == EPI_RELU_F32_Q) v[j] = relu(v[j]);
-          if constexpr (EPI == EPI_SIGMOID) v[j] = sigmoid_f64(v[j]);
-        }
-        if (row_ok) {
-#pragma unroll
-          for (int g = 0; g < 2; ++g) {          // two 16-column groups (N % 16 == 0)
-            const int ng = n + 16 * g;
-            if (ng >= args.N) break;
-            const float* vg = v + 16 * g;
-            if constexpr (EPI == EPI_F32 || EPI == EPI_F32_Q || EPI == EPI_RELU_F32_Q ||
-                          EPI == EPI_SIGMOID) {
-              const int blk = ng / args.col_block;
-              float* dst = args.out_f + (int64_t)blk * args.block_stride +
-                           (int64_t)row * args.ldo + (ng - blk * args.col_block);
-              float4* d4 = reinterpret_cast<float4*>(dst);
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                d4[j] = make_float4(vg[4 * j], vg[4 * j + 1], vg[4 * j + 2], vg[4 * j + 3]);
-            }
-            if constexpr (EPI == EPI_F32_Q || EPI == EPI_RELU_Q || EPI == EPI_RELU_F32_Q) {
-              uint32_t w[4];
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                uint32_t b0 = (uint32_t)(q8(vg[4 * j + 0], args.clip, args.sigma) & 0xff);
-                uint32_t b1 = (uint32_t)(q8(vg[4 * j + 1], args.clip, args.sigma) & 0xff);
-                uint32_t b2 = (uint32_t)(q8(vg[4 * j + 2], args.clip, args.sigma) & 0xff);
-                uint32_t b3 = (uint32_t)(q8(vg[4 * j + 3], args.clip, args.sigma) & 0xff);
-                w[j] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
-              }
-              *reinterpret_cast<uint4*>(args.out_q + (int64_t)row * args.ldo + ng) =
-                  make_uint4(w[0], w[1], w[2], w[3]);
-            }
-          }
-        }
-      }
+      epi_store_chunk<EPI>(args, row, row_ok, n, acc, best_v, best_j, stage);
     }
     if constexpr (EPI == EPI_ARGMAX) {
       if (row_ok && best_j >= 0) atomicMax(args.keys + row, argmax_key(best_v, (uint32_t)best_j));
     }
   }
 
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+}
+
+// ------------------------------------------------------------------ persistent variant
+// For large problems (encoder GEMMs at tens of thousands of rows, the output layer at
+// thousands of rows): one CTA per SM loops over 128 x BN tiles (n fastest, so consecutive
+// tiles share the A tile in L2).  Two TMEM accumulators (2 x BN columns) let the
+// epilogue of tile i overlap the MMAs of tile i+1; the TMA ring keeps streaming across
+// tile boundaries.  Same numerics and epilogues as k_gemm_i8.
+template <int BN>
+struct PersCfg {
+  static constexpr int A_BYTES = BM * BK;
+  static constexpr int STAGE_BYTES = A_BYTES + BN * BK;
+  static constexpr int STAGES = (190 * 1024 / STAGE_BYTES) > 8 ? 8 : (190 * 1024 / STAGE_BYTES);
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + EPI_STAGE_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN;
+};
+
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    k_gemm_pers(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const GemmArgs args) {
+  using Cfg = PersCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[STAGES];
+  __shared__ __align__(8) uint64_t tfull_bar[2];
+  __shared__ __align__(8) uint64_t tempty_bar[2];
+  __shared__ uint32_t tmem_slot;
+  const uint32_t warp = warp_id(), lane = lane_id();
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tempty_bar[i], EPI_WARPS);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(&tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_slot;
+  pdl_wait();
+  const int M_live = args.M_dyn ? min(args.M, *args.M_dyn) : args.M;
+  const int m_tiles = (M_live + BM - 1) / BM;
+  const int n_tiles = (args.N + BN - 1) / BN;
+  const int T = m_tiles * n_tiles;
+  const int num_kb = (args.K + BK - 1) / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t ps = 0, pph = 0;
+      for (int t = blockIdx.x; t < T; t += gridDim.x) {
+        const int m0 = (t / n_tiles) * BM, n0 = (t % n_tiles) * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[ps], pph ^ 1);
+          uint8_t* sa = smem + ps * Cfg::STAGE_BYTES;
+          uint8_t* sb = sa + Cfg::A_BYTES;
+          mbar_arrive_expect_tx(&full_bar[ps], Cfg::STAGE_BYTES);
+          tma_load_2d(sa, &tmA, &full_bar[ps], kb * BK, m0);
+          tma_load_2d(sa + 64 * BK, &tmA, &full_bar[ps], kb * BK, m0 + 64);
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j)
+            tma_load_2d(sb + j * 64 * BK, &tmB, &full_bar[ps], kb * BK, n0 + j * 64);
+          if (++ps == STAGES) { ps = 0; pph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_i8<BM, BN>();
+      uint32_t cs = 0, cph = 0, ab = 0, aph = 0;
+      for (int t = blockIdx.x; t < T; t += gridDim.x) {
+        mbar_wait(&tempty_bar[ab], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + ab * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[cs], cph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + cs * Cfg::STAGE_BYTES);
+          const uint64_t adesc = umma_desc_sw128(sa);
+          const uint64_t bdesc = umma_desc_sw128(sa + Cfg::A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 32; ++k)
+            mma_i8(d_tmem, adesc + (uint64_t)(2 * k), bdesc + (uint64_t)(2 * k), idesc, (kb | k) != 0);
+          mma_commit(&empty_bar[cs]);
+          if (++cs == STAGES) { cs = 0; cph ^= 1; }
+        }
+        mma_commit(&tfull_bar[ab]);
+        ab ^= 1;
+        if (ab == 0) aph ^= 1;
+      }
+    }
+  } else {
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    constexpr int HALF = BN / 2;
+    uint32_t ab = 0, aph = 0;
+    bool first = true;
+    for (int t = blockIdx.x; t < T; t += gridDim.x) {
+      const int m0 = (t / n_tiles) * BM, n0 = (t % n_tiles) * BN;
+      const int row = m0 + q * 32 + lane;
+      const bool row_ok = row < M_live;
+      mbar_wait(&tfull_bar[ab], aph);
+      tc_fence_after();
+      if (first && warp == 2 && lane == 0) pdl_launch_dependents();
+      first = false;
+      const uint32_t t_row = tmem_base + ab * BN + ((uint32_t)(q * 32) << 16) + half * HALF;
+      float* stage = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES) +
+                     (warp - 2) * EPI_STAGE_FLOATS;
+      float best_v = -INFINITY;
+      int best_j = -1;
+#pragma unroll 1
+      for (int c = 0; c < HALF; c += 32) {
+        int32_t acc[32];
+        tmem_ld16(t_row + c, *reinterpret_cast<int32_t(*)[16]>(acc));
+        tmem_ld16(t_row + c + 16, *reinterpret_cast<int32_t(*)[16]>(acc + 16));
+        tmem_ld_wait();
+        const int n = n0 + half * HALF + c;
+        if (n >= args.N) break;
+        epi_store_chunk<EPI>(args, row, row_ok, n, acc, best_v, best_j, stage);
+      }
+      if constexpr (EPI == EPI_ARGMAX) {
+        if (row_ok && best_j >= 0) atomicMax(args.keys + row, argmax_key(best_v, (uint32_t)best_j));
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(&tempty_bar[ab]);
+      ab ^= 1;
+      if (ab == 0) aph ^= 1;
+    }
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
@@ -270,16 +599,57 @@ bool pdl_enabled() {
   return on;
 }
 
+// Persistent tile loop once the grid would exceed two waves of one CTA per SM
+// (env MNMT_GEMM_PERSISTENT=0/1 forces it off/on for A/B tests).
+bool gemm_persistent(int M, int N, int bn) {
+  static const int force = [] {
+    const char* e = getenv("MNMT_GEMM_PERSISTENT");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  if (force >= 0) return force == 1;
+  const long tiles = (long)((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+  return tiles > 2L * num_sms();
+}
+
 int gemm_pick_bn(int M, int N) {
   const int mt = (M + BM - 1) / BM;
+  if ((long)mt * ((N + 255) / 256) > 2L * num_sms()) return 256;   // persistent, widest tile
   if (((N + 255) / 256) * mt >= 148) return 256;
   if (((N + 127) / 128) * mt >= 74) return 128;
   return 64;
 }
 
+static int num_sms() {
+  static int n[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!n[dev]) cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
+  return n[dev] > 0 ? n[dev] : 148;
+}
+
+// Persistent launch: grid = min(tiles, SMs), one CTA per SM.
+template <int BN, int EPI>
+static cudaError_t launch_pers_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
+                                 cudaStream_t st) {
+  const int tiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tiles < num_sms() ? tiles : num_sms());
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = PersCfg<BN>::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_gemm_pers<BN, EPI>, tmA, tmB, a);
+}
+
 template <int BN, int EPI>
 static cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                             cudaStream_t st) {
+  if (gemm_persistent(a.M, a.N, BN)) return launch_pers_t<BN, EPI>(tmA, tmB, a, st);
   using Cfg = GemmCfg<BN>;
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM);
   const int num_kb = (a.K + BK - 1) / BK;
@@ -298,8 +668,11 @@ static cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
 
 template <int BN, int EPI>
 static cudaError_t set_attr() {
-  return cudaFuncSetAttribute(k_gemm_i8<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              GemmCfg<BN>::smem_for(GemmCfg<BN>::STAGES));
+  cudaError_t e = cudaFuncSetAttribute(k_gemm_i8<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       GemmCfg<BN>::smem_for(GemmCfg<BN>::STAGES));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_gemm_pers<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              PersCfg<BN>::SMEM);
 }
 template <int BN>
 static cudaError_t set_attr_bn() {
@@ -317,6 +690,14 @@ static cudaError_t gemm_init_all();
 
 // Opt every GEMM instantiation into its dynamic shared memory size on the current
 // device (once per device).  Must run before any launch (never inside a stream capture).
+static cudaError_t set_attr_ln() {
+  cudaError_t e = cudaFuncSetAttribute(k_gemm_i8<192, EPI_LN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       GemmCfg<192>::smem_for(GemmCfg<192>::STAGES));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_gemm_i8<256, EPI_LN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              GemmCfg<256>::smem_for(GemmCfg<256>::STAGES));
+}
+
 cudaError_t gemm_init() {
   static bool done[64] = {};
   int dev = 0;
@@ -332,6 +713,7 @@ static cudaError_t gemm_init_all() {
   cudaError_t e;
   if ((e = set_attr_bn<64>()) != cudaSuccess) return e;
   if ((e = set_attr_bn<128>()) != cudaSuccess) return e;
+  if ((e = set_attr_ln()) != cudaSuccess) return e;
   return set_attr_bn<256>();
 }
 
@@ -350,9 +732,33 @@ static cudaError_t launch_bn(const CUtensorMap& tmA, const CUtensorMap& tmB, con
   return cudaErrorInvalidValue;
 }
 
+// non-persistent launch of one instantiation
+template <int BN, int EPI>
+static cudaError_t launch_np(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
+                             cudaStream_t st) {
+  using Cfg = GemmCfg<BN>;
+  const int num_kb = (a.K + BK - 1) / BK;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((a.N + BN - 1) / BN, (a.M + BM - 1) / BM);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = Cfg::smem_for(num_kb < Cfg::STAGES ? num_kb : Cfg::STAGES);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_gemm_i8<BN, EPI>, tmA, tmB, a);
+}
+
 cudaError_t launch_gemm_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                            int epi, int bn, cudaStream_t st) {
   if (a.M <= 0 || a.N <= 0) return cudaSuccess;
+  if (epi == EPI_LN) {   // one CTA owns whole rows: BN = N = d
+    if (a.N == 192) return launch_np<192, EPI_LN>(tmA, tmB, a, st);
+    if (a.N == 256) return launch_np<256, EPI_LN>(tmA, tmB, a, st);
+    return cudaErrorInvalidValue;
+  }
   if (bn == 0) bn = gemm_pick_bn(a.M, a.N);
   switch (bn) {
     case 64: return launch_bn<64>(tmA, tmB, a, epi, st);

@@ -4,6 +4,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include "rowops.h"
+
 namespace mnmt {
 
 // Epilogues of the int8 GEMM (acc = exact s32; v = fmaf((float)acc, s, bias)).
@@ -15,6 +17,8 @@ enum Epi : int {
   EPI_SIGMOID = 4,    // out_f = sigmoid(v)              (AAN gates)
   EPI_ARGMAX = 5,     // keys[row] = max packed(v, col)  (output layer, A9)
   EPI_ACC = 6,        // out_i = acc                     (test hook: raw accumulators)
+  EPI_LN = 7,         // full rows (BN = N = d): v = GEMM output; r = x + v (or the AAN gate
+                      // form with v = f-gate logit); out = LN(r), Q(out), next-layer AAN step
 };
 
 struct GemmArgs {
@@ -31,6 +35,7 @@ struct GemmArgs {
   int col_block;               // scatter: out + (n / col_block) * block_stride + m * ldo + n % col_block
   int64_t block_stride;
   unsigned long long* keys;    // [rows] for EPI_ARGMAX
+  LnArgs ln;                   // EPI_LN: residual / gate inputs, gamma, beta, outputs, AAN
 };
 
 // Tensor map over a row-major int8 matrix [rows x K] (K contiguous, K % 16 == 0):

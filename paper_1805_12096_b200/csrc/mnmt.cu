@@ -111,6 +111,8 @@ struct Lane {
   Workspace ws;
   cudaStream_t st = nullptr;
   cudaEvent_t ev = nullptr;
+  cudaStream_t side = nullptr;                 // fork stream for independent GEMMs (graph branch)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::map<int64_t, cudaGraphExec_t> graphs;   // key: padded live-row bound
   int64_t launches_per_step = 0;
   // persistent step kernel program (built for this lane's workspace)
@@ -150,6 +152,7 @@ struct mnmt_model {
   int64_t max_concurrent_rows = 0;   // option: co-schedule batches in waves of <= this many rows
   int megakernel = 0;                  // option: persistent step kernel (1) or one kernel per op (0)
   int profile_phases = 0;              // option: record per-phase timestamps (lane 0)
+  int fuse_ln = 0;                     // option: LayerNorm fused into full-row GEMM epilogues
 };
 
 namespace {
@@ -317,6 +320,9 @@ static void jb_free(mnmt_model* m) {
 static mnmt_status lane_init(mnmt_model* m, Lane& L) {
   if (L.st) return MNMT_OK;
   if (cudaStreamCreateWithFlags(&L.st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&L.side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&L.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&L.ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&L.ev, cudaEventDisableTiming) != cudaSuccess) {
     cudaGetLastError();
     set_err("lane stream/event creation failed");
@@ -437,6 +443,29 @@ static cudaError_t gemm(mnmt_model* m, cudaStream_t st, const CUtensorMap& tmA, 
   return launch_gemm_i8(tmA, W.tm, a, epi, 0, st);
 }
 
+// Fused GEMM + residual (+gate) + LayerNorm + Q (+ next-layer AAN) when one CTA can own
+// whole rows (d in {192, 256}); otherwise false (the caller runs GEMM then k_ln).
+static bool fuse_ln(const mnmt_model* m) {
+  return (m->c.d_model == 192 || m->c.d_model == 256) && m->fuse_ln;
+}
+
+static cudaError_t gemm_ln(mnmt_model* m, cudaStream_t st, const CUtensorMap& tmA, const Lin& W,
+                           int M, const int32_t* M_dyn, const LnArgs& ln) {
+  GemmArgs a{};
+  a.M = M;
+  a.M_dyn = M_dyn;
+  a.N = W.out;
+  a.K = W.in;
+  a.scale = scale_of(m);
+  a.bias = W.b;
+  a.clip = m->c.clip;
+  a.sigma = sigma_of(m);
+  a.ldo = W.out;
+  a.col_block = W.out;
+  a.ln = ln;
+  return launch_gemm_i8(tmA, W.tm, a, EPI_LN, 0, st);
+}
+
 static LnArgs ln_args(mnmt_model* m, const Workspace& w, int n, const int32_t* n_dyn, const float* x,
                       const float* delta, const float* gamma, const float* beta, float* out,
                       int8_t* out_q) {
@@ -507,14 +536,21 @@ static cudaError_t launch_encoder(mnmt_model* m, Lane& Ln, int M, int n_sent, co
     at.sigma = sigma_of(m);
     at.out_q = w.cctx;
     if ((e = launch_attn_enc(at, st)) != cudaSuccess) return e;
-    if ((e = gemm(m, st, w.tm_cctx, E.o, M, nullptr, EPI_F32, w.o, nullptr, d)) != cudaSuccess) return e;
     LnArgs la = ln_args(m, w, M, nullptr, w.x, w.o, E.ln1g, E.ln1b, w.x, w.cx);
-    if ((e = launch_ln(la, st)) != cudaSuccess) return e;
-    if ((e = gemm(m, st, w.tm_cx, E.f1, M, nullptr, EPI_RELU_Q, nullptr, w.ch, c.d_ffn)) != cudaSuccess) return e;
-    if ((e = gemm(m, st, w.tm_ch, E.f2, M, nullptr, EPI_F32, w.o, nullptr, d)) != cudaSuccess) return e;
     LnArgs lb = ln_args(m, w, M, nullptr, w.x, w.o, E.ln2g, E.ln2b, w.x, w.cx);
-    if ((e = launch_ln(lb, st)) != cudaSuccess) return e;
-    *nlaunch += 7;
+    if (fuse_ln(m)) {
+      if ((e = gemm_ln(m, st, w.tm_cctx, E.o, M, nullptr, la)) != cudaSuccess) return e;
+      if ((e = gemm(m, st, w.tm_cx, E.f1, M, nullptr, EPI_RELU_Q, nullptr, w.ch, c.d_ffn)) != cudaSuccess) return e;
+      if ((e = gemm_ln(m, st, w.tm_ch, E.f2, M, nullptr, lb)) != cudaSuccess) return e;
+      *nlaunch += 5;
+    } else {
+      if ((e = gemm(m, st, w.tm_cctx, E.o, M, nullptr, EPI_F32, w.o, nullptr, d)) != cudaSuccess) return e;
+      if ((e = launch_ln(la, st)) != cudaSuccess) return e;
+      if ((e = gemm(m, st, w.tm_cx, E.f1, M, nullptr, EPI_RELU_Q, nullptr, w.ch, c.d_ffn)) != cudaSuccess) return e;
+      if ((e = gemm(m, st, w.tm_ch, E.f2, M, nullptr, EPI_F32, w.o, nullptr, d)) != cudaSuccess) return e;
+      if ((e = launch_ln(lb, st)) != cudaSuccess) return e;
+      *nlaunch += 7;
+    }
   }
   // Source keys/values of all decoder layers in one GEMM, scattered to [L][M_cap][2d].
   if ((e = gemm(m, st, w.tm_cx, m->kv_all, M, nullptr, EPI_F32, w.kv, nullptr, 2 * d, nullptr, 2 * d,
@@ -559,9 +595,18 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
   for (int l = 0; l < L; ++l) {
     const DecLayer& D = m->dec[l];
     LnArgs l1;
+    bool l1_done = false;
     if (c.decoder == 1) {
       // A6: AAN block. g (or its codes) was produced with this layer's input.
       const float* a_f = w.g;
+      // The i-gate GEMM needs only Q(y): it runs on a forked branch beside the AAN FFN.
+      const bool fork = c.aan_gate && c.aan_ffn_depth > 0 && !hook;
+      if (fork) {
+        if ((e = cudaEventRecord(Ln.ev_fork, st)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(Ln.side, Ln.ev_fork, 0)) != cudaSuccess) return e;
+        if ((e = gemm(m, Ln.side, w.tm_cy, D.gi, n, nd, EPI_F32, w.gi, nullptr, d)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(Ln.ev_join, Ln.side)) != cudaSuccess) return e;
+      }
       if (c.aan_ffn_depth == 2) {
         if ((e = gemm(m, st, w.tm_cg, D.a1, n, nd, EPI_RELU_Q, nullptr, w.ch1, d)) != cudaSuccess) return e;
         if ((e = gemm(m, st, w.tm_ch1, D.a2, n, nd, EPI_F32_Q, w.a, w.ca, d)) != cudaSuccess) return e;
@@ -576,12 +621,23 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
         // gate (R8): logits W_i Q(y) + b_i and W_f Q(a) + b_f (for -ffn, Q(a) = Q(g));
         // the sigmoids are applied in the gate-LayerNorm kernel
         const CUtensorMap& tm_a = c.aan_ffn_depth == 0 ? w.tm_cg : w.tm_ca;
-        if ((e = gemm(m, st, w.tm_cy, D.gi, n, nd, EPI_F32, w.gi, nullptr, d)) != cudaSuccess) return e;
-        if ((e = gemm(m, st, tm_a, D.gf, n, nd, EPI_F32, w.gf, nullptr, d)) != cudaSuccess) return e;
-        k += 2;
+        if (!fork) {
+          if ((e = gemm(m, st, w.tm_cy, D.gi, n, nd, EPI_F32, w.gi, nullptr, d)) != cudaSuccess) return e;
+        }
         l1 = ln_args(m, w, n, nd, w.y, a_f, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
         l1.gi = w.gi;
         l1.gf = w.gf;
+        if (fuse_ln(m)) {
+          // f-gate GEMM with the gate combine + LayerNorm in its epilogue (reads gi: join first)
+          if (fork && (e = cudaStreamWaitEvent(st, Ln.ev_join, 0)) != cudaSuccess) return e;
+          if ((e = gemm_ln(m, st, tm_a, D.gf, n, nd, l1)) != cudaSuccess) return e;
+          l1_done = true;
+        } else {
+          if ((e = gemm(m, st, tm_a, D.gf, n, nd, EPI_F32, w.gf, nullptr, d)) != cudaSuccess) return e;
+        }
+        if (fork && !fuse_ln(m) && (e = cudaStreamWaitEvent(st, Ln.ev_join, 0)) != cudaSuccess)
+          return e;   // join before the gate LayerNorm reads gi
+        k += 2;
       } else {
         l1 = ln_args(m, w, n, nd, w.y, a_f, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
       }
@@ -613,8 +669,10 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
       k += 3;
       l1 = ln_args(m, w, n, nd, w.y, w.od, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
     }
-    if ((e = launch_ln(l1, st)) != cudaSuccess) return e;
-    ++k;
+    if (!l1_done) {
+      if ((e = launch_ln(l1, st)) != cudaSuccess) return e;
+      ++k;
+    }
     if (hook && (e = hook->x1(m, l)) != cudaSuccess) return e;
     // A7: source attention
     if ((e = gemm(m, st, w.tm_cx1, D.sq, n, nd, EPI_F32, w.qs, nullptr, d)) != cudaSuccess) return e;
@@ -639,18 +697,28 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
     as.sigma = sigma_of(m);
     as.out_q = w.cctxd;
     if ((e = launch_attn(as, st)) != cudaSuccess) return e;
-    if ((e = gemm(m, st, w.tm_cctxd, D.so, n, nd, EPI_F32, w.od, nullptr, d)) != cudaSuccess) return e;
     LnArgs l2 = ln_args(m, w, n, nd, w.x1, w.od, D.ln[1][0], D.ln[1][1], w.x2, w.cx2);
-    if ((e = launch_ln(l2, st)) != cudaSuccess) return e;
-    k += 4;
+    if (fuse_ln(m)) {
+      if ((e = gemm_ln(m, st, w.tm_cctxd, D.so, n, nd, l2)) != cudaSuccess) return e;
+      k += 3;
+    } else {
+      if ((e = gemm(m, st, w.tm_cctxd, D.so, n, nd, EPI_F32, w.od, nullptr, d)) != cudaSuccess) return e;
+      if ((e = launch_ln(l2, st)) != cudaSuccess) return e;
+      k += 4;
+    }
     if (hook && (e = hook->x2(m, l)) != cudaSuccess) return e;
     // A8: FFN
     if ((e = gemm(m, st, w.tm_cx2, D.f1, n, nd, EPI_RELU_Q, nullptr, w.chd, c.d_ffn)) != cudaSuccess) return e;
-    if ((e = gemm(m, st, w.tm_chd, D.f2, n, nd, EPI_F32, w.f, nullptr, d)) != cudaSuccess) return e;
     LnArgs l3 = ln_args(m, w, n, nd, w.x2, w.f, D.ln[2][0], D.ln[2][1], w.y, w.cy);
     l3.aan = aan_for_layer(m, w, l + 1);
-    if ((e = launch_ln(l3, st)) != cudaSuccess) return e;
-    k += 3;
+    if (fuse_ln(m)) {
+      if ((e = gemm_ln(m, st, w.tm_chd, D.f2, n, nd, l3)) != cudaSuccess) return e;
+      k += 2;
+    } else {
+      if ((e = gemm(m, st, w.tm_chd, D.f2, n, nd, EPI_F32, w.f, nullptr, d)) != cudaSuccess) return e;
+      if ((e = launch_ln(l3, st)) != cudaSuccess) return e;
+      k += 3;
+    }
     if (hook && (e = hook->layer(m, l)) != cudaSuccess) return e;
   }
   // A9: tied output projection fused with the argmax (softmax skipped)
@@ -924,6 +992,7 @@ struct Batch {
   int64_t M = 0;
   int T = 0;                  // max steps
   int lane = 0;               // decoder lane (stream) that runs this batch
+  std::vector<int32_t> alive; // alive[t-1] = rows with max_len >= t (upper bound of live rows)
 };
 
 struct Job {
@@ -979,6 +1048,9 @@ static void plan_job(const int64_t* src_off, int32_t n, const int32_t* max_len,
       b.T = std::max(b.T, max_len[s]);
     }
     b.M = M;
+    b.alive.assign(b.T, 0);
+    for (int32_t s : b.rows)
+      for (int t = 0; t < max_len[s]; ++t) ++b.alive[t];
     job.meta.resize(job.meta.size() + 4 * M);
     int32_t* idx = job.meta.data() + b.tok0;
     int32_t *pos = idx + M, *st = idx + 2 * M, *ln = idx + 3 * M;
@@ -1085,6 +1157,9 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
     CK(launch_decode_init(w.ctrl, w.live, B, w.keys, st));
     launches += 1;
     const int npad = (B + 127) / 128 * 128;
+    // per-step row bound: rows are compacted to the front and a row never outlives its
+    // max_len, so step t needs at most alive[t-1] rows -> the smallest cached graph that fits
+    auto pad_at = [&](int t) { return (b.alive[t] + 127) / 128 * 128; };
     if (m->megakernel && (!hook || hook->megakernel_ok())) {
       if (!Ln.d_phases || Ln.prog_forced != forced || Ln.prog_out != m->jb.out_ids)
         CKS(build_program(m, Ln, forced));
@@ -1115,22 +1190,25 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
         }
       }
     } else if (use_graphs && !hook) {
-      auto it = Ln.graphs.find(npad);
-      if (it == Ln.graphs.end()) {
-        cudaGraph_t g;
-        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-        int64_t per_step = 0;
-        cudaError_t e = launch_step(m, Ln, npad, forced, nullptr, &per_step);
-        cudaError_t e2 = cudaStreamEndCapture(st, &g);
-        CK(e);
-        CK(e2);
-        cudaGraphExec_t ge;
-        CK(cudaGraphInstantiate(&ge, g, 0));
-        cudaGraphDestroy(g);
-        it = Ln.graphs.emplace(npad, ge).first;
-        Ln.launches_per_step = per_step;
+      for (int t = 0; t < b.T; ++t) {
+        const int np = pad_at(t);
+        auto it = Ln.graphs.find(np);
+        if (it == Ln.graphs.end()) {
+          cudaGraph_t g;
+          CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+          int64_t per_step = 0;
+          cudaError_t e = launch_step(m, Ln, np, forced, nullptr, &per_step);
+          cudaError_t e2 = cudaStreamEndCapture(st, &g);
+          CK(e);
+          CK(e2);
+          cudaGraphExec_t ge;
+          CK(cudaGraphInstantiate(&ge, g, 0));
+          cudaGraphDestroy(g);
+          it = Ln.graphs.emplace(np, ge).first;
+          Ln.launches_per_step = per_step;
+        }
+        CK(cudaGraphLaunch(it->second, st));
       }
-      for (int t = 0; t < b.T; ++t) CK(cudaGraphLaunch(it->second, st));
       launches += (int64_t)b.T * Ln.launches_per_step;
     } else {
       for (int t = 0; t < b.T; ++t) CK(launch_step(m, Ln, npad, forced, hook, &launches));
@@ -1642,6 +1720,14 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
     m->profile_phases = value ? 1 : 0;
     return MNMT_OK;
   }
+  if (std::string(name) == "fuse_ln") {
+    m->fuse_ln = value ? 1 : 0;
+    for (Lane& L : m->lanes) {   // captured graphs encode the old kernel sequence
+      for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
+      L.graphs.clear();
+    }
+    return MNMT_OK;
+  }
   if (std::string(name) == "megakernel") {
     if (value != 0 && value != 1) { set_err("megakernel must be 0 or 1"); return MNMT_ERR_ARG; }
     m->megakernel = (int)value;
@@ -1724,7 +1810,10 @@ extern "C" void mnmt_model_destroy(mnmt_model* m) {
     for (Lane& L : m->lanes) {
       lane_free(L);
       if (L.st) cudaStreamDestroy(L.st);
+      if (L.side) cudaStreamDestroy(L.side);
       if (L.ev) cudaEventDestroy(L.ev);
+      if (L.ev_fork) cudaEventDestroy(L.ev_fork);
+      if (L.ev_join) cudaEventDestroy(L.ev_join);
     }
     jb_free(m);
     for (void* p : m->allocs) cudaFree(p);

@@ -10,6 +10,7 @@
 //   k_attn         attention, one warp per (row, head), fp64      (A3, A6', A7)
 //   k_finish       argmax decode + EOS/max_len + stable live-row compaction (A9, A10)
 #include <cstdio>
+#include <cstdlib>
 #include <utility>
 
 #include "numerics.cuh"
@@ -19,11 +20,21 @@
 #include "kernels.h"
 
 namespace mnmt {
+__constant__ int c_pdl_early = 1;
+// Let the next kernel of the chain launch (and run its prologue) right away; its
+// griddepcontrol.wait still waits for this grid to complete (env MNMT_PDL_EARLY=0 disables).
+__device__ __forceinline__ void pdl_trigger_early() {
+  if (c_pdl_early) pdl_launch_dependents();
+}
+}  // namespace mnmt
+
+namespace mnmt {
 
 // ------------------------------------------------------------------ quantize
 __global__ void k_quantize(const float* __restrict__ x, int64_t n, float clip, float sigma,
                            int8_t* __restrict__ out) {
   pdl_wait();
+  pdl_trigger_early();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
     out[i] = (int8_t)q8(x[i], clip, sigma);
@@ -59,6 +70,7 @@ __global__ void k_embed_src(const int32_t* __restrict__ ids, const int32_t* __re
                             const float* __restrict__ PE, int d, float rsd, float clip,
                             float sigma, float* __restrict__ x, int8_t* __restrict__ xq) {
   pdl_wait();
+  pdl_trigger_early();
   const int warps = blockDim.x >> 5;
   const int row = blockIdx.x * warps + (threadIdx.x >> 5);
   if (row >= M) return;
@@ -81,6 +93,7 @@ __global__ void k_embed_src(const int32_t* __restrict__ ids, const int32_t* __re
 template <int NV>
 __global__ void k_embed_tgt(EmbedTgtArgs a) {
   pdl_wait();
+  pdl_trigger_early();
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= a.ctrl[0]) return;
   embed_tgt_row<NV>(a, r);
@@ -89,6 +102,7 @@ __global__ void k_embed_tgt(EmbedTgtArgs a) {
 template <int NV>
 __global__ void k_ln(LnArgs a) {
   pdl_wait();
+  pdl_trigger_early();
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
   if (r >= n_live) return;
@@ -101,6 +115,7 @@ constexpr int ATTN_WARPS = 8;
 __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn(AttnArgs a) {
   __shared__ double sc_all[ATTN_WARPS][MNMT_MAX_KV];
   pdl_wait();
+  pdl_trigger_early();
   const int wi = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * ATTN_WARPS + wi;
   const int r = (int)(gw / a.H), h = (int)(gw - (int64_t)r * a.H);
@@ -115,6 +130,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finish(FinishArgs a) {
   __shared__ int32_t warp_cnt[32];
   __shared__ int32_t base_s;
   pdl_wait();
+  pdl_trigger_early();
   finish_block(a, warp_cnt, base_s);
 }
 
@@ -133,6 +149,7 @@ __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn_enc(EncAttnArgs a) {
   double* sc = reinterpret_cast<double*>(enc_smem);                       // [warps][MAX_KV]
   float* ks = reinterpret_cast<float*>(sc + (size_t)ATTN_WARPS * MNMT_MAX_KV);
   pdl_wait();
+  pdl_trigger_early();
   const int s = blockIdx.x, h = blockIdx.y;
   const int dh = a.dh, d = a.d, ld3 = 3 * d, lds = dh + 4;
   const int start = a.sent_start[s], len = a.sent_len[s];
@@ -168,6 +185,7 @@ __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn_enc(EncAttnArgs a) {
 // ------------------------------------------------------------------ decode init
 __global__ void k_decode_init(int32_t* ctrl, int32_t* live, int B, unsigned long long* keys) {
   pdl_wait();
+  pdl_trigger_early();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B; i += gridDim.x * blockDim.x) {
     live[i] = i;
     keys[i] = 0ull;
@@ -238,6 +256,26 @@ cudaError_t launch_ln(const LnArgs& a, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
+// Optional (env MNMT_CARVEOUT=1): every row kernel prefers the maximum shared-memory
+// carveout, the same L1/shared split as the GEMM kernels, so consecutive kernels of a
+// decoder step never need an SM reconfiguration.
+static cudaError_t set_carveouts() {
+  const char* e = getenv("MNMT_CARVEOUT");
+  if (!(e && e[0] == '1')) return cudaSuccess;
+  const void* fns[] = {(const void*)k_quantize, (const void*)k_embed_src<1>, (const void*)k_embed_src<2>,
+                       (const void*)k_embed_src<4>, (const void*)k_embed_src<8>,
+                       (const void*)k_embed_tgt<1>, (const void*)k_embed_tgt<2>,
+                       (const void*)k_embed_tgt<4>, (const void*)k_embed_tgt<8>,
+                       (const void*)k_ln<1>, (const void*)k_ln<2>, (const void*)k_ln<4>, (const void*)k_ln<8>,
+                       (const void*)k_attn, (const void*)k_attn_enc, (const void*)k_finish,
+                       (const void*)k_decode_init};
+  for (const void* f : fns) {
+    cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (r != cudaSuccess) return r;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t attn_init() {   // once per device
   static bool done[64] = {};
   int dev = 0;
@@ -246,6 +284,12 @@ cudaError_t attn_init() {   // once per device
   if (dev >= 0 && dev < 64 && done[dev]) return cudaSuccess;
   e = cudaFuncSetAttribute(k_attn_enc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)enc_attn_smem(64));
+  if (e == cudaSuccess) e = set_carveouts();
+  if (e == cudaSuccess) {
+    const char* pe = getenv("MNMT_PDL_EARLY");
+    const int v = (pe && pe[0] == '0') ? 0 : 1;
+    e = cudaMemcpyToSymbol(c_pdl_early, &v, sizeof v);
+  }
   if (e == cudaSuccess && dev >= 0 && dev < 64) done[dev] = true;
   return e;
 }
@@ -278,6 +322,7 @@ cudaError_t launch_decode_init(int32_t* ctrl, int32_t* live, int B, unsigned lon
 // ------------------------------------------------------------------ op-level helpers (tests)
 __global__ void k_aan_step_rows(float* C, const float* y, int n, int d, int t, AanOut o) {
   pdl_wait();
+  pdl_trigger_early();
   const int64_t total = (int64_t)n * (d / 4);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {

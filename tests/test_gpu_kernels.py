@@ -48,6 +48,7 @@ GEMM_SHAPES = [
     (1, 64, 64, 0), (4, 192, 192, 64), (130, 256, 192, 64), (300, 2048, 256, 128),
     (257, 1536, 2048, 256), (383, 512, 1024, 0), (128, 6144, 512, 256), (77, 36000, 256, 256),
     (520, 256, 2048, 128), (1000, 1024, 4096, 0),
+    (5000, 2048, 256, 0), (4999, 768, 512, 256),      # > 2 waves of tiles: persistent kernel
 ]
 
 
@@ -62,7 +63,8 @@ def test_gemm_acc_bitexact(Mr, N, K, bn):
 
 
 @pytest.mark.parametrize("epi", [M.EPI_F32, M.EPI_F32_Q, M.EPI_RELU_Q, M.EPI_RELU_F32_Q, M.EPI_SIGMOID])
-@pytest.mark.parametrize("Mr,N,K", [(5, 256, 256), (260, 2048, 512), (131, 512, 2048)])
+@pytest.mark.parametrize("Mr,N,K", [(5, 256, 256), (260, 2048, 512), (131, 512, 2048),
+                                    (4700, 2048, 256)])   # last: persistent kernel
 def test_gemm_epilogues_bitexact(epi, Mr, N, K):
     rng = np.random.default_rng(epi * 100 + Mr)
     x = rng.normal(0, 1.0, size=(Mr, K)).astype(np.float32)
@@ -94,7 +96,8 @@ def test_gemm_epilogues_bitexact(epi, Mr, N, K):
 
 
 @pytest.mark.parametrize("Mr,N,K,bias", [(3, 50, 32, True), (200, 36000, 256, True),
-                                         (129, 36000, 192, False), (390, 36000, 512, True)])
+                                         (129, 36000, 192, False), (390, 36000, 512, True),
+                                         (650, 36000, 256, True)])   # persistent kernel
 def test_gemm_argmax_bitexact_with_ties(Mr, N, K, bias):
     rng = np.random.default_rng(Mr + N)
     x = rng.normal(0, 1.0, size=(Mr, K)).astype(np.float32)

@@ -30,6 +30,11 @@ TINY_VARIANTS = [
               aan_ffn_depth=0, aan_gate=0),
     ModelDims("t-self", 32, 64, 4, vocab=64, enc_layers=2, dec_layers=2, decoder=0),
     ModelDims("t-nobias-ragged-vocab", 48, 96, 4, vocab=50, enc_layers=1, dec_layers=3, out_bias=0),
+    # d in {192, 256}: LayerNorm fused into full-row GEMM epilogues
+    ModelDims("t192-aan", 192, 384, 8, vocab=1000, enc_layers=2, dec_layers=2),
+    ModelDims("t192-ffn1", 192, 384, 8, vocab=1000, enc_layers=2, dec_layers=2, aan_ffn_depth=1),
+    ModelDims("t256-noffn-gate", 256, 512, 8, vocab=1000, enc_layers=2, dec_layers=2, aan_ffn_depth=0),
+    ModelDims("t256-self", 256, 512, 8, vocab=1000, enc_layers=2, dec_layers=2, decoder=0),
 ]
 
 
@@ -155,6 +160,9 @@ def test_batch_and_order_invariance():
     base = gm.translate(ss, 1 << 20)
     for budget in (1, 64, 333, 4096):
         assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, budget), base))
+    for fuse in (0, 1):                    # LayerNorm fused into GEMM epilogues or not
+        gm.set_option("fuse_ln", fuse)
+        assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, 333), base))
     for lanes in (1, 2, 3):                # concurrent decoder lanes: identical ids
         gm.set_option("lanes", lanes)
         for rows in (7, 50, 1 << 20):      # co-scheduled batch waves: identical ids
