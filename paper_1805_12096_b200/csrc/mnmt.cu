@@ -507,7 +507,7 @@ static AanOut aan_for_layer(mnmt_model* m, const Workspace& w, int l) {
 }
 
 // Encoder over M tokens (A2-A4).  meta: [idx M][pos M][start M][len M].
-static cudaError_t launch_encoder(mnmt_model* m, Lane& Ln, int M, int n_sent, const int32_t* tok_idx,
+static cudaError_t launch_encoder(mnmt_model* m, Lane& Ln, int M, int n_sent, int s_max, const int32_t* tok_idx,
                                   const int32_t* tok_pos, const int32_t* tok_start,
                                   const int32_t* tok_len, int64_t* nlaunch) {
   (void)tok_start;
@@ -529,6 +529,7 @@ static cudaError_t launch_encoder(mnmt_model* m, Lane& Ln, int M, int n_sent, co
     at.sent_start = w.row_start;
     at.sent_len = w.row_len;
     at.n_sent = n_sent;
+    at.s_max = s_max;
     at.H = c.n_heads;
     at.dh = d / c.n_heads;
     at.d = d;
@@ -992,6 +993,7 @@ struct Batch {
   int64_t M = 0;
   int T = 0;                  // max steps
   int lane = 0;               // decoder lane (stream) that runs this batch
+  int S_max = 1;              // longest source sentence
   std::vector<int32_t> alive; // alive[t-1] = rows with max_len >= t (upper bound of live rows)
 };
 
@@ -1046,6 +1048,7 @@ static void plan_job(const int64_t* src_off, int32_t n, const int32_t* max_len,
     for (int32_t s : b.rows) {
       M += src_off[s + 1] - src_off[s];
       b.T = std::max(b.T, max_len[s]);
+      b.S_max = std::max<int>(b.S_max, (int)(src_off[s + 1] - src_off[s]));
     }
     b.M = M;
     b.alive.assign(b.T, 0);
@@ -1151,7 +1154,7 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
     if (forced) CK(cudaMemcpyAsync(w.forced_off, r64 + B, B * 8, cudaMemcpyDeviceToDevice, st));
     const int32_t* base = m->jb.meta + b.tok0;
     const int M = (int)b.M;
-    CK(launch_encoder(m, Ln, M, B, base, base + M, base + 2 * M, base + 3 * M, &launches));
+    CK(launch_encoder(m, Ln, M, B, b.S_max, base, base + M, base + 2 * M, base + 3 * M, &launches));
     if (c.decoder == 1)
       CK(cudaMemsetAsync(w.C, 0, (size_t)c.dec_layers * w.B_cap * d * sizeof(float), st));
     CK(launch_decode_init(w.ctrl, w.live, B, w.keys, st));

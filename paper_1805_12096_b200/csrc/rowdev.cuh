@@ -145,23 +145,43 @@ __device__ __forceinline__ void ln_row(const LnArgs a, int r) {
 // warp_attend: one warp computes one (query row, head): lane j scores positions j, j+32,
 // ...; probabilities go to a per-warp scratch in shared memory; lane c then sums column c
 // over the positions in order (V loads issued 4 ahead).
-__device__ __forceinline__ void warp_attend(const float* __restrict__ q, const float* k,
-                                            const float* v, int64_t ld, int len, int dh,
-                                            double* sc, float clip, float sigma,
-                                            int8_t* out_q, float* out_f) {
+__device__ __forceinline__ double to_f64(float x) { return (double)x; }
+__device__ __forceinline__ double to_f64(double x) { return x; }
+
+// KT = float: K/V rows in global memory (each element converted once, when used);
+// KT = double: K/V already converted (staged in shared memory by the caller).
+// qd: per-warp scratch of dh doubles (the query converted once).
+template <typename KT>
+__device__ __forceinline__ void warp_attend(const float* __restrict__ q, const KT* k, const KT* v,
+                                            int64_t ld, int len, int dh, double* sc, double* qd,
+                                            float clip, float sigma, int8_t* out_q, float* out_f) {
   const int lane = threadIdx.x & 31;
+  if constexpr (sizeof(KT) == 8) {   // reused K/V: convert the query once as well
+    for (int c = lane; c < dh; c += 32) qd[c] = (double)q[c];
+    __syncwarp();
+  }
   const double inv_sqrt = 1.0 / sqrt((double)dh);
   double mx = -INFINITY;
   for (int j = lane; j < len; j += 32) {
-    const float* kr = k + (int64_t)j * ld;
+    const KT* kr = k + (int64_t)j * ld;
     double dot = 0.0;
     for (int c = 0; c < dh; c += 4) {
-      const float4 k4 = *reinterpret_cast<const float4*>(kr + c);
-      const float4 q4 = *reinterpret_cast<const float4*>(q + c);
-      dot = __dadd_rn(dot, __dmul_rn((double)q4.x, (double)k4.x));
-      dot = __dadd_rn(dot, __dmul_rn((double)q4.y, (double)k4.y));
-      dot = __dadd_rn(dot, __dmul_rn((double)q4.z, (double)k4.z));
-      dot = __dadd_rn(dot, __dmul_rn((double)q4.w, (double)k4.w));
+      double kk[4], qq[4];
+      if constexpr (sizeof(KT) == 4) {
+        const float4 k4 = *reinterpret_cast<const float4*>(kr + c);
+        const float4 q4 = *reinterpret_cast<const float4*>(q + c);   // same address in all lanes
+        kk[0] = k4.x; kk[1] = k4.y; kk[2] = k4.z; kk[3] = k4.w;
+        qq[0] = q4.x; qq[1] = q4.y; qq[2] = q4.z; qq[3] = q4.w;
+      } else {
+        const double2 a = *reinterpret_cast<const double2*>(kr + c);
+        const double2 b = *reinterpret_cast<const double2*>(kr + c + 2);
+        kk[0] = a.x; kk[1] = a.y; kk[2] = b.x; kk[3] = b.y;
+        qq[0] = qd[c]; qq[1] = qd[c + 1]; qq[2] = qd[c + 2]; qq[3] = qd[c + 3];
+      }
+      dot = __dadd_rn(dot, __dmul_rn(qq[0], kk[0]));
+      dot = __dadd_rn(dot, __dmul_rn(qq[1], kk[1]));
+      dot = __dadd_rn(dot, __dmul_rn(qq[2], kk[2]));
+      dot = __dadd_rn(dot, __dmul_rn(qq[3], kk[3]));
     }
     const double s = __dmul_rn(dot, inv_sqrt);
     sc[j] = s;
@@ -180,14 +200,14 @@ __device__ __forceinline__ void warp_attend(const float* __restrict__ q, const f
     double acc = 0.0;
     int j = 0;
     for (; j + 4 <= len; j += 4) {
-      const float v0 = v[(int64_t)(j + 0) * ld + c], v1 = v[(int64_t)(j + 1) * ld + c];
-      const float v2 = v[(int64_t)(j + 2) * ld + c], v3 = v[(int64_t)(j + 3) * ld + c];
-      acc = __dadd_rn(acc, __dmul_rn(sc[j + 0], (double)v0));
-      acc = __dadd_rn(acc, __dmul_rn(sc[j + 1], (double)v1));
-      acc = __dadd_rn(acc, __dmul_rn(sc[j + 2], (double)v2));
-      acc = __dadd_rn(acc, __dmul_rn(sc[j + 3], (double)v3));
+      const double v0 = to_f64(v[(int64_t)(j + 0) * ld + c]), v1 = to_f64(v[(int64_t)(j + 1) * ld + c]);
+      const double v2 = to_f64(v[(int64_t)(j + 2) * ld + c]), v3 = to_f64(v[(int64_t)(j + 3) * ld + c]);
+      acc = __dadd_rn(acc, __dmul_rn(sc[j + 0], v0));
+      acc = __dadd_rn(acc, __dmul_rn(sc[j + 1], v1));
+      acc = __dadd_rn(acc, __dmul_rn(sc[j + 2], v2));
+      acc = __dadd_rn(acc, __dmul_rn(sc[j + 3], v3));
     }
-    for (; j < len; ++j) acc = __dadd_rn(acc, __dmul_rn(sc[j], (double)v[(int64_t)j * ld + c]));
+    for (; j < len; ++j) acc = __dadd_rn(acc, __dmul_rn(sc[j], to_f64(v[(int64_t)j * ld + c])));
     const float ctx = len > 0 ? (float)__ddiv_rn(acc, z) : 0.0f;
     out_q[c] = (int8_t)q8(ctx, clip, sigma);
     if (out_f) out_f[c] = ctx;
@@ -195,8 +215,9 @@ __device__ __forceinline__ void warp_attend(const float* __restrict__ q, const f
   __syncwarp();
 }
 
-// Attention of one (row, head) by one warp (SRC, SELF and ENC modes); sc = per-warp scratch.
-__device__ __forceinline__ void attn_row_head(const AttnArgs a, int r, int h, double* sc) {
+// Attention of one (row, head) by one warp (SRC, SELF and ENC modes); sc = per-warp scratch
+// of span + 64 doubles (scores, then the converted query).
+__device__ __forceinline__ void attn_row_head(const AttnArgs a, int r, int h, double* sc, int span) {
   const int lane = threadIdx.x & 31;
   const int dh = a.dh;
   int start, len;
@@ -222,7 +243,7 @@ __device__ __forceinline__ void attn_row_head(const AttnArgs a, int r, int h, do
   }
   const float* K = a.kv + (int64_t)start * a.ldkv + a.k_off + h * dh;
   const float* V = a.kv + (int64_t)start * a.ldkv + a.v_off + h * dh;
-  warp_attend(q, K, V, a.ldkv, len, dh, sc, a.clip, a.sigma,
+  warp_attend<float>(q, K, V, a.ldkv, len, dh, sc, sc + span, a.clip, a.sigma,
               a.out_q + (int64_t)r * a.d + h * dh, a.out_f ? a.out_f + (int64_t)r * a.d + h * dh : nullptr);
 }
 

@@ -113,7 +113,7 @@ constexpr int ATTN_WARPS = 8;
 
 // Decoder (SRC, SELF) and op-level (ENC) attention: one warp per (row, head).
 __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn(AttnArgs a) {
-  __shared__ double sc_all[ATTN_WARPS][MNMT_MAX_KV];
+  extern __shared__ double sc_dyn[];   // [ATTN_WARPS][span]
   pdl_wait();
   pdl_trigger_early();
   const int wi = threadIdx.x >> 5;
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn(AttnArgs a) {
   const int r = (int)(gw / a.H), h = (int)(gw - (int64_t)r * a.H);
   const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
   if (r >= n_live) return;
-  attn_row_head(a, r, h, sc_all[wi]);
+  attn_row_head(a, r, h, sc_dyn + (size_t)wi * (a.span + 64), a.span);
 }
 
 constexpr int FIN_THREADS = 1024;
@@ -139,46 +139,47 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finish(FinishArgs a) {
 // its query rows (warp per query).  Sentences longer than ENC_STAGE_MAX read from L2/HBM.
 constexpr int ENC_STAGE_MAX = 160;
 
-__host__ __device__ inline size_t enc_attn_smem(int dh) {
-  return (size_t)ATTN_WARPS * MNMT_MAX_KV * sizeof(double) +
-         2 * (size_t)ENC_STAGE_MAX * (dh + 4) * sizeof(float);
+__host__ __device__ inline size_t enc_attn_smem(int dh, int s_max) {
+  const int staged = s_max < ENC_STAGE_MAX ? s_max : ENC_STAGE_MAX;
+  return (size_t)ATTN_WARPS * (s_max + 64) * sizeof(double) +
+         2 * (size_t)staged * (dh + 2) * sizeof(double);
 }
 
 __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn_enc(EncAttnArgs a) {
   extern __shared__ __align__(16) uint8_t enc_smem[];
-  double* sc = reinterpret_cast<double*>(enc_smem);                       // [warps][MAX_KV]
-  float* ks = reinterpret_cast<float*>(sc + (size_t)ATTN_WARPS * MNMT_MAX_KV);
+  double* sc = reinterpret_cast<double*>(enc_smem);                       // [warps][s_max + 64]
+  double* ks = sc + (size_t)ATTN_WARPS * (a.s_max + 64);
   pdl_wait();
   pdl_trigger_early();
   const int s = blockIdx.x, h = blockIdx.y;
-  const int dh = a.dh, d = a.d, ld3 = 3 * d, lds = dh + 4;
+  const int dh = a.dh, d = a.d, ld3 = 3 * d, lds = dh + 2;
   const int start = a.sent_start[s], len = a.sent_len[s];
+  const int staged = a.s_max < ENC_STAGE_MAX ? a.s_max : ENC_STAGE_MAX;
   const float* base = a.qkv + (int64_t)start * ld3 + h * dh;
-  const float *K, *V;
-  int64_t ldk;
-  if (len <= ENC_STAGE_MAX) {
-    float* vs = ks + (size_t)ENC_STAGE_MAX * lds;
+  const int wi = threadIdx.x >> 5;
+  double* scw = sc + (size_t)wi * (a.s_max + 64);
+  if (len <= staged) {
+    // K and V head slices converted to fp64 once, reused by all of the sentence's queries
+    double* vs = ks + (size_t)staged * lds;
     const int d4 = dh >> 2;
     for (int i = threadIdx.x; i < len * d4; i += blockDim.x) {
       const int j = i / d4, c4 = i - j * d4;
-      *reinterpret_cast<float4*>(ks + j * lds + 4 * c4) =
-          *reinterpret_cast<const float4*>(base + (int64_t)j * ld3 + d + 4 * c4);
-      *reinterpret_cast<float4*>(vs + j * lds + 4 * c4) =
-          *reinterpret_cast<const float4*>(base + (int64_t)j * ld3 + 2 * d + 4 * c4);
+      const float4 k4 = *reinterpret_cast<const float4*>(base + (int64_t)j * ld3 + d + 4 * c4);
+      const float4 v4 = *reinterpret_cast<const float4*>(base + (int64_t)j * ld3 + 2 * d + 4 * c4);
+      double* kd = ks + j * lds + 4 * c4;
+      double* vd = vs + j * lds + 4 * c4;
+      kd[0] = k4.x; kd[1] = k4.y; kd[2] = k4.z; kd[3] = k4.w;
+      vd[0] = v4.x; vd[1] = v4.y; vd[2] = v4.z; vd[3] = v4.w;
     }
     __syncthreads();
-    K = ks;
-    V = vs;
-    ldk = lds;
+    for (int i = wi; i < len; i += ATTN_WARPS)
+      warp_attend<double>(base + (int64_t)i * ld3, ks, vs, lds, len, dh, scw, scw + a.s_max, a.clip,
+                          a.sigma, a.out_q + (int64_t)(start + i) * d + h * dh, nullptr);
   } else {
-    K = base + d;
-    V = base + 2 * d;
-    ldk = ld3;
-  }
-  const int wi = threadIdx.x >> 5;
-  for (int i = wi; i < len; i += ATTN_WARPS) {
-    warp_attend(base + (int64_t)i * ld3, K, V, ldk, len, dh, sc + (size_t)wi * MNMT_MAX_KV,
-                a.clip, a.sigma, a.out_q + (int64_t)(start + i) * d + h * dh, nullptr);
+    for (int i = wi; i < len; i += ATTN_WARPS)
+      warp_attend<float>(base + (int64_t)i * ld3, base + d, base + 2 * d, ld3, len, dh, scw,
+                         scw + a.s_max, a.clip, a.sigma, a.out_q + (int64_t)(start + i) * d + h * dh,
+                         nullptr);
   }
 }
 
@@ -283,7 +284,10 @@ cudaError_t attn_init() {   // once per device
   if (e != cudaSuccess) return e;
   if (dev >= 0 && dev < 64 && done[dev]) return cudaSuccess;
   e = cudaFuncSetAttribute(k_attn_enc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)enc_attn_smem(64));
+                           (int)enc_attn_smem(64, MNMT_MAX_KV));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             ATTN_WARPS * (MNMT_MAX_KV + 64) * (int)sizeof(double));
   if (e == cudaSuccess) e = set_carveouts();
   if (e == cudaSuccess) {
     const char* pe = getenv("MNMT_PDL_EARLY");
@@ -297,13 +301,16 @@ cudaError_t attn_init() {   // once per device
 cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
   if (a.n <= 0) return cudaSuccess;
   const int64_t warps = (int64_t)a.n * a.H;
+  AttnArgs b = a;
+  if (b.span <= 0 || b.span > MNMT_MAX_KV) b.span = MNMT_MAX_KV;
   return launch_pdl(k_attn, dim3((unsigned)((warps + ATTN_WARPS - 1) / ATTN_WARPS)),
-                    dim3(ATTN_WARPS * 32), 0, st, a);
+                    dim3(ATTN_WARPS * 32), (size_t)ATTN_WARPS * (b.span + 64) * sizeof(double), st, b);
 }
 
 cudaError_t launch_attn_enc(const EncAttnArgs& a, cudaStream_t st) {
   if (a.n_sent <= 0) return cudaSuccess;
-  return launch_pdl(k_attn_enc, dim3(a.n_sent, a.H), dim3(ATTN_WARPS * 32), enc_attn_smem(a.dh),
+  if (a.s_max < 1 || a.s_max > MNMT_MAX_KV) return cudaErrorInvalidValue;
+  return launch_pdl(k_attn_enc, dim3(a.n_sent, a.H), dim3(ATTN_WARPS * 32), enc_attn_smem(a.dh, a.s_max),
                     st, a);
 }
 

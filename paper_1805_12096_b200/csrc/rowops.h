@@ -52,6 +52,7 @@ enum AttnMode : int { ATTN_ENC = 0, ATTN_SRC = 1, ATTN_SELF = 2 };
 
 struct AttnArgs {
   int mode;
+  int span;                 // longest attended span of the launch (<= MNMT_MAX_KV; sizes smem)
   int n;                    // static row bound
   const int32_t* n_dyn;
   const int32_t* ctrl;      // t (self mode)
@@ -77,6 +78,7 @@ struct EncAttnArgs {
   const int32_t* sent_start;   // [n_sent] first token row of each sentence
   const int32_t* sent_len;     // [n_sent]
   int n_sent, H, dh, d;
+  int s_max;                   // longest sentence of the launch (sizes shared memory)
   float clip, sigma;
   int8_t* out_q;               // Q(ctx) [M x d]
 };

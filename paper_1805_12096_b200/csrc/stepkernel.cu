@@ -36,7 +36,7 @@ constexpr int SK_B_MAX = 256 * SK_BK;         // 32 KB (bn <= 256)
 constexpr int SK_STAGE = SK_A_BYTES + SK_B_MAX;
 constexpr int SK_STAGES = 3;
 constexpr int SK_RING = SK_STAGES * SK_STAGE;                       // 144 KB
-constexpr int SK_SCRATCH = SK_WARPS * MNMT_MAX_KV * 8;              // 48 KB attention scratch
+constexpr int SK_SCRATCH = SK_WARPS * (MNMT_MAX_KV + 64) * 8;       // 54 KB attention scratch
 constexpr int SK_SMEM = SK_RING + SK_SCRATCH + 1024;
 constexpr int SK_TMEM_COLS = 512;
 
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1) k_step(const StepArgs s) {
           const int total = n_live * a.H;
           for (int i = gwarp; i < total; i += nwarps_all) {
             const int r = i / a.H, h = i - r * a.H;
-            attn_row_head(a, r, h, scratch + (size_t)warp * MNMT_MAX_KV);
+            attn_row_head(a, r, h, scratch + (size_t)warp * (MNMT_MAX_KV + 64), MNMT_MAX_KV);
           }
           fence_proxy_async();
           break;
