@@ -190,23 +190,31 @@ def time_kernel(fn, iters: int, stream):
     return s.elapsed_time(e) / iters    # ms per launch
 
 
-def live_rows_profile(sset, budget):
-    """Live decode rows at every step of every batch (max_len = S_i, no EOS) -> list."""
+def live_rows_profile(sset, budget, max_concurrent_rows=0):
+    """Live decode rows at every sequential step (max_len = S_i, no EOS), following the
+    library's schedule: word-budget batches, co-scheduled in waves of <= max_concurrent_rows."""
     from paper_1805_12096_b200 import mnmt as M
     order, off = M.batch_by_words(sset.lengths, budget)
+    nb = len(off) - 1
     rows = []
-    for b in range(len(off) - 1):
-        ml = sset.max_len[order[off[b]:off[b + 1]]]
+    b = 0
+    while b < nb:
+        e = b + 1
+        if max_concurrent_rows > 0:
+            while e < nb and off[e + 1] - off[b] <= max_concurrent_rows:
+                e += 1
+        ml = sset.max_len[order[off[b]:off[e]]]
         for t in range(1, int(ml.max()) + 1):
             rows.append(int(np.sum(ml >= t)))
+        b = e
     return rows
 
 
-def roofline_out_gemm(dims, weights, sset, budget, peaks, stream):
+def roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr):
     """A9: output projection fused with argmax, at the workload's mean live-row count."""
     import torch
     from paper_1805_12096_b200 import mnmt as M
-    rows = live_rows_profile(sset, budget)
+    rows = live_rows_profile(sset, budget, mcr)
     Mr = int(round(np.mean(rows)))
     d, V = dims.d_model, dims.vocab
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -234,14 +242,44 @@ def roofline_out_gemm(dims, weights, sset, budget, peaks, stream):
             "peak_source": f"{peaks['source']} bf16 burst x2"}
 
 
-def roofline_src_attn(dims, sset, budget, peaks, stream):
-    """A7: source attention over the fp32 K/V cache at the workload's mean live rows."""
+def roofline_dxd_gemm(dims, sset, budget, peaks, stream, mcr):
+    """A6-A7: the decoder's d x d projections (AAN FFN, gates, source q/o): 6 per layer per step,
+    at the workload's mean live-row count."""
     import torch
     from paper_1805_12096_b200 import mnmt as M
-    order, off = M.batch_by_words(sset.lengths, budget)
-    # representative batch: the one holding the median sentence
-    b = int(np.searchsorted(off, sset.n // 2, side="right") - 1)
-    idx = order[off[b]:off[b + 1]]
+    rows = live_rows_profile(sset, budget, mcr)
+    Mr = max(1, int(round(np.mean(rows))))
+    d = dims.d_model
+    dev = torch.device("cuda", torch.cuda.current_device())
+    A = torch.randint(-127, 128, (Mr, d), dtype=torch.int8, device=dev)
+    W = torch.randint(-127, 128, (d, d), dtype=torch.int8, device=dev)
+    b = torch.zeros(d, device=dev)
+    out = torch.empty((Mr, d), device=dev)
+
+    def fn(st):
+        M.op_gemm_i8(A.data_ptr(), W.data_ptr(), Mr, d, d, b.data_ptr(), dims.clip, M.EPI_F32,
+                     out.data_ptr(), None, 0, st)
+    ms = time_kernel(fn, 200, stream)
+    ops = 2.0 * Mr * d * d
+    peak = 2.0 * peaks["bf16_tflops"]
+    ach = ops / (ms * 1e-3) / 1e12
+    per_step = 6 * dims.dec_layers if dims.decoder == 1 else 5 * dims.dec_layers
+    return {"kernel": "k_gemm_i8<64, EPI_F32> (decoder d x d projections)", "bound": "tensor",
+            "achieved": ach, "peak": peak, "unit": "TOP/s (int8)", "frac": ach / peak,
+            "traffic": None, "shape": f"M={Mr} (mean live rows/step) N={d} K={d}",
+            "ms_per_launch": ms, "launches_per_step": len(rows) * per_step,
+            "ms_per_step_est": ms * len(rows) * per_step,
+            "peak_source": f"{peaks['source']} bf16 burst x2"}
+
+
+def roofline_src_attn(dims, sset, budget, peaks, stream, mcr):
+    """A7: source attention over the fp32 K/V cache, rows = the workload's mean live rows per
+    step, drawn (seeded) from the set so the source-length mix matches."""
+    import torch
+    from paper_1805_12096_b200 import mnmt as M
+    rows = live_rows_profile(sset, budget, mcr)
+    n_rows = max(1, int(round(np.mean(rows))))
+    idx = np.random.default_rng(3).choice(sset.n, size=min(n_rows, sset.n), replace=False)
     L = sset.lengths[idx].astype(np.int32)
     starts = np.concatenate([[0], np.cumsum(L)[:-1]]).astype(np.int32)
     d, H = dims.d_model, dims.n_heads
@@ -396,9 +434,11 @@ def main():
     cpu = None
     if rank == 0 and not args.no_roofline:
         peaks = load_peaks()
-        cands = [roofline_out_gemm(dims, weights, sset, budget, peaks, stream),
-                 roofline_src_attn(dims, sset, budget, peaks, stream)]
-        cands[1]["launches_per_step"] = len(live_rows_profile(sset, budget)) * dims.dec_layers
+        mcr = args.max_concurrent_rows
+        cands = [roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr),
+                 roofline_src_attn(dims, sset, budget, peaks, stream, mcr),
+                 roofline_dxd_gemm(dims, sset, budget, peaks, stream, mcr)]
+        cands[1]["launches_per_step"] = len(live_rows_profile(sset, budget, mcr)) * dims.dec_layers
         cands[1]["ms_per_step_est"] = cands[1]["ms_per_launch"] * cands[1]["launches_per_step"]
         roof = max(cands, key=lambda c: c["ms_per_step_est"])
         roof["share_of_step_est"] = roof["ms_per_step_est"] / (ms_max / args.steps)

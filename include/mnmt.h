@@ -156,6 +156,10 @@ mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids_host,
  *   "fuse_ln"              1: residual / gate + LayerNorm + Q fused into the epilogue
  *                          of the producing GEMM when one CTA can own whole rows (d = 192, 256);
  *                          0 (default, measured faster): separate LayerNorm kernels.
+ *   "rowlocal"             persistent kernel only: 1 = GEMM/LayerNorm/embedding phases split by
+ *                          128-row tile (CTA barriers between them), 0 (default) = split over the
+ *                          grid with grid barriers.
+ *   "profile_phases"       1 = the persistent kernel stamps every phase (mnmt_debug_phase_*).
  * Errors: MNMT_ERR_ARG (unknown name or negative value). */
 mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, int64_t value);
 

@@ -153,6 +153,7 @@ struct mnmt_model {
   int megakernel = 0;                  // option: persistent step kernel (1) or one kernel per op (0)
   int profile_phases = 0;              // option: record per-phase timestamps (lane 0)
   int fuse_ln = 0;                     // option: LayerNorm fused into full-row GEMM epilogues
+  int rowlocal = 0;                    // option: row-local phases in the persistent step kernel (measured slower)
 };
 
 namespace {
@@ -961,6 +962,20 @@ static mnmt_status build_program(mnmt_model* m, Lane& Ln, bool forced) {
     fa.forced_off = forced ? w.forced_off : nullptr;
     pb.ph.push_back(P);
   }
+  // Row-local chain: GEMMs (except the output layer), LayerNorms and the embedding run on
+  // the CTA that owns the 128-row tile; only attention, the output layer and the finish are
+  // spread over the grid.  A grid barrier is needed after a phase iff it or its successor
+  // is grid-wide (or the option is off).
+  for (size_t i = 0; i < pb.ph.size(); ++i) {
+    Phase& P = pb.ph[i];
+    const bool vocab_gemm = P.type == PH_GEMM && P.g[0].epi == EPI_ARGMAX;
+    P.rowlocal = m->rowlocal && (P.type == PH_EMBED || P.type == PH_LN ||
+                                 (P.type == PH_GEMM && !vocab_gemm)) ? 1 : 0;
+  }
+  for (size_t i = 0; i < pb.ph.size(); ++i) {
+    const bool next_local = i + 1 < pb.ph.size() && pb.ph[i + 1].rowlocal;
+    pb.ph[i].sync_grid = (pb.ph[i].rowlocal && next_local) ? 0 : 1;
+  }
   // upload: tensor maps first, then phases with their device addresses patched in
   if (Ln.d_phases) cudaFree(Ln.d_phases);
   if (Ln.d_tmaps) cudaFree(Ln.d_tmaps);
@@ -1721,6 +1736,11 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
   }
   if (std::string(name) == "profile_phases") {
     m->profile_phases = value ? 1 : 0;
+    return MNMT_OK;
+  }
+  if (std::string(name) == "rowlocal") {
+    m->rowlocal = value ? 1 : 0;
+    for (Lane& L : m->lanes) L.prog_out = nullptr;   // rebuild the step program
     return MNMT_OK;
   }
   if (std::string(name) == "fuse_ln") {

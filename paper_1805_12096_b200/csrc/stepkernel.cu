@@ -93,15 +93,34 @@ struct Pipe {
   uint32_t ab = 0, aph = 0;   // accumulator buffer / phase (MMA and epilogue keep own copies)
 };
 
-// Tile i of the phase's live tiles -> (problem, m0, n0).
-__device__ __forceinline__ void tile_of(const Phase& P, const int* mt_live, int i, int& p, int& m0,
-                                        int& n0) {
+// The k-th tile of this CTA in the phase -> (problem, m0, n0); false when exhausted.
+//   grid-wide: tiles i = blockIdx.x + k * gridDim.x of all live tiles (problem 0 first);
+//   row-local: the CTA owns 128-row tiles mt = blockIdx.x + j * gridDim.x and runs every
+//              column tile of every problem of those rows.
+__device__ __forceinline__ bool tile_k(const Phase& P, const int* mt_live, int k, int& p, int& m0,
+                                       int& n0) {
+  if (P.rowlocal) {
+    const int tpm = P.g[0].n_tiles + (P.nprob > 1 ? P.g[1].n_tiles : 0);
+    const int j = k / tpm;
+    int r = k - j * tpm;
+    const int mt = blockIdx.x + j * gridDim.x;
+    if (mt >= mt_live[0]) return false;
+    p = 0;
+    if (r >= P.g[0].n_tiles) { p = 1; r -= P.g[0].n_tiles; }
+    m0 = mt * SK_BM;
+    n0 = r * P.g[p].bn;
+    return true;
+  }
+  int i = blockIdx.x + k * gridDim.x;
+  const int T = mt_live[0] * P.g[0].n_tiles + (P.nprob > 1 ? mt_live[1] * P.g[1].n_tiles : 0);
+  if (i >= T) return false;
   p = 0;
-  int t0 = mt_live[0] * P.g[0].n_tiles;
+  const int t0 = mt_live[0] * P.g[0].n_tiles;
   if (i >= t0) { p = 1; i -= t0; }
   const int nt = P.g[p].n_tiles;
   m0 = (i / nt) * SK_BM;
   n0 = (i % nt) * P.g[p].bn;
+  return true;
 }
 
 // Epilogue of one 32-column chunk of one row (same arithmetic as k_gemm_i8).
@@ -223,13 +242,11 @@ __global__ void __launch_bounds__(SK_THREADS, 1) k_step(const StepArgs s) {
             }
           }
           __syncthreads();
-          const int T = mt_live_s[0] * P.g[0].n_tiles + (P.nprob > 1 ? mt_live_s[1] * P.g[1].n_tiles : 0);
+          int p, m0, n0;
           if (warp == 0) {
             if (lane == 0) {
               fence_proxy_async();   // activations written by the previous phase -> TMA reads
-              for (int i = blockIdx.x; i < T; i += gridDim.x) {
-                int p, m0, n0;
-                tile_of(P, mt_live_s, i, p, m0, n0);
+              for (int k = 0; tile_k(P, mt_live_s, k, p, m0, n0); ++k) {
                 const CUtensorMap* tmA = P.g[p].tmA;
                 const CUtensorMap* tmB = P.g[p].tmB;
                 const int bn = P.g[p].bn;
@@ -250,9 +267,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1) k_step(const StepArgs s) {
             }
           } else if (warp == 1) {
             if (lane == 0) {
-              for (int i = blockIdx.x; i < T; i += gridDim.x) {
-                int p, m0, n0;
-                tile_of(P, mt_live_s, i, p, m0, n0);
+              for (int k = 0; tile_k(P, mt_live_s, k, p, m0, n0); ++k) {
                 const int nkb = (P.g[p].a.K + SK_BK - 1) / SK_BK;
                 const uint32_t idesc = idesc_rt(P.g[p].bn);
                 mbar_wait(&tempty_bar[pp.ab], pp.aph ^ 1);
@@ -279,9 +294,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1) k_step(const StepArgs s) {
           } else if (warp >= 4) {
             const int q = warp & 3, half = (warp - 4) >> 2;
             bool wrote = false;
-            for (int i = blockIdx.x; i < T; i += gridDim.x) {
-              int p, m0, n0;
-              tile_of(P, mt_live_s, i, p, m0, n0);
+            for (int k = 0; tile_k(P, mt_live_s, k, p, m0, n0); ++k) {
               const GemmArgs a = P.g[p].a;     // registers: no reloads around global stores
               const int epi = P.g[p].epi;
               const int bn = P.g[p].bn;
@@ -317,14 +330,24 @@ __global__ void __launch_bounds__(SK_THREADS, 1) k_step(const StepArgs s) {
         case PH_EMBED: {
           const EmbedTgtArgs a = P.em;
           const int n_live = a.ctrl[0];
-          for (int r = gwarp; r < n_live; r += nwarps_all) embed_tgt_row<NV>(a, r);
+          if (P.rowlocal) {
+            for (int t0 = blockIdx.x * SK_BM; t0 < n_live; t0 += gridDim.x * SK_BM)
+              for (int r = t0 + (int)warp; r < min(n_live, t0 + SK_BM); r += SK_WARPS) embed_tgt_row<NV>(a, r);
+          } else {
+            for (int r = gwarp; r < n_live; r += nwarps_all) embed_tgt_row<NV>(a, r);
+          }
           fence_proxy_async();
           break;
         }
         case PH_LN: {
           const LnArgs a = P.ln;
           const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
-          for (int r = gwarp; r < n_live; r += nwarps_all) ln_row<NV>(a, r);
+          if (P.rowlocal) {
+            for (int t0 = blockIdx.x * SK_BM; t0 < n_live; t0 += gridDim.x * SK_BM)
+              for (int r = t0 + (int)warp; r < min(n_live, t0 + SK_BM); r += SK_WARPS) ln_row<NV>(a, r);
+          } else {
+            for (int r = gwarp; r < n_live; r += nwarps_all) ln_row<NV>(a, r);
+          }
           fence_proxy_async();
           break;
         }
@@ -345,7 +368,12 @@ __global__ void __launch_bounds__(SK_THREADS, 1) k_step(const StepArgs s) {
           break;
         }
       }
-      grid_sync(s.bar, gen);
+      if (P.sync_grid) {
+        grid_sync(s.bar, gen);
+      } else {
+        fence_proxy_async();   // this CTA's global writes -> its own TMA reads in the next phase
+        __syncthreads();
+      }
       if (s.timing && blockIdx.x == 0 && threadIdx.x == 0)
         s.timing[(size_t)step * (s.n_phases + 1) + ph + 1] = globaltimer_ns();
     }

@@ -27,6 +27,9 @@ struct GemmProb {
 
 struct alignas(16) Phase {
   int type;
+  int rowlocal;             // 1: work split by 128-row tile, tile i -> CTA i % grid (GEMM, LN,
+                            //    embed); 0: split over the whole grid (attention, output, finish)
+  int sync_grid;            // 1: grid barrier after this phase; 0: CTA barrier (row-local chain)
   int nprob;                // PH_GEMM: 1 or 2 independent problems
   GemmProb g[2];
   EmbedTgtArgs em;

@@ -10,7 +10,8 @@ L.mnmt_debug_phase_times.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int
 dims = synth.PRESETS[sys.argv[1] if len(sys.argv) > 1 else "small-aan"]
 m = M.Model(dims, synth.make_weights(dims, 1))
 ss = synth.newstest_set()
-m.set_option("max_concurrent_rows", 4096); m.set_option("profile_phases", 1)
+m.set_option("max_concurrent_rows", 4096); m.set_option("profile_phases", 1); m.set_option("megakernel", 1)
+if len(sys.argv) > 2: m.set_option("rowlocal", int(sys.argv[2]))
 names = ["GEMM", "EMBED", "LN", "ATTN", "FINISH"]
 for cap in (1, 200):
     s2 = synth.SentenceSet(ss.ids, ss.offsets, np.minimum(ss.max_len, cap).astype(np.int32))
