@@ -56,32 +56,71 @@ __device__ __forceinline__ float acc_to_float(int32_t acc, bool small) {
 // One 32-column chunk of the 32 rows of this warp (lane = row): dequant + fused op +
 // store, or running argmax.  fp32 outputs go through a padded per-warp smem tile so each
 // store instruction writes four full 128-byte lines.
+// Packed fp32 pairs (sm_100a FFMA2 / FADD2): each half is one IEEE round-to-nearest op.
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(unsigned long long r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+
+// v[j] = fmaf((float)acc[j], s, bias[j]) for one 32-column chunk.
+// Fast path (K <= 256, whole chunk in range): exact magic-number conversion + packed ops.
+__device__ __forceinline__ void dequant32(const GemmArgs& args, int n, bool fast,
+                                          const int32_t (&acc)[32], float (&v)[32]) {
+  if (fast) {
+    float bias[32];
+    if (args.bias) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        const float4 b4 = __ldg(reinterpret_cast<const float4*>(args.bias + n + j));
+        bias[j] = b4.x; bias[j + 1] = b4.y; bias[j + 2] = b4.z; bias[j + 3] = b4.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) bias[j] = 0.0f;
+    }
+    const unsigned long long negc = pk2(-12582912.0f, -12582912.0f);
+    const unsigned long long s2 = pk2(args.scale, args.scale);
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      unsigned long long t = pk2(__int_as_float(0x4B400000 + acc[j]), __int_as_float(0x4B400000 + acc[j + 1]));
+      asm("add.rn.f32x2 %0, %0, %1;" : "+l"(t) : "l"(negc));
+      unsigned long long r;
+      asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(t), "l"(s2), "l"(pk2(bias[j], bias[j + 1])));
+      upk2(r, v[j], v[j + 1]);
+    }
+  } else {
+    const bool small = args.K <= 256;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float b = (args.bias && n + j < args.N) ? __ldg(args.bias + n + j) : 0.0f;
+      v[j] = __fmaf_rn(acc_to_float(acc[j], small), args.scale, b);
+    }
+  }
+}
+
+// One 32-column chunk of the 32 rows of this warp (lane = row): dequant + fused op +
+// store, or running argmax.  fp32 outputs go through a padded per-warp smem tile so each
+// store instruction writes four full 128-byte lines.
 template <int EPI>
 __device__ __forceinline__ void epi_store_chunk(const GemmArgs& args, int row, bool row_ok, int n,
                                                 const int32_t (&acc)[32], float& best_v,
                                                 int& best_j, float* stage) {
-  const bool small = args.K <= 256;
   const bool full = n + 32 <= args.N;
-  float bias[32];
-  if (args.bias && full) {
-#pragma unroll
-    for (int j = 0; j < 32; j += 4) {
-      const float4 b4 = __ldg(reinterpret_cast<const float4*>(args.bias + n + j));
-      bias[j] = b4.x; bias[j + 1] = b4.y; bias[j + 2] = b4.z; bias[j + 3] = b4.w;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) bias[j] = (args.bias && n + j < args.N) ? __ldg(args.bias + n + j) : 0.0f;
-  }
+  const bool fast = full && args.K <= 256;
   if constexpr (EPI == EPI_ARGMAX) {
     // Branch-free chunk maximum; the lowest column holding it is searched only when the
     // chunk beats the running best, and a strictly greater value is required, so among
     // equal logits the lowest column wins (R15).
     float v[32];
+    dequant32(args, n, fast, acc, v);
+    if (!full) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      v[j] = __fmaf_rn(acc_to_float(acc[j], small), args.scale, bias[j]);
-      if (!full && n + j >= args.N) v[j] = -INFINITY;
+      for (int j = 0; j < 32; ++j)
+        if (n + j >= args.N) v[j] = -INFINITY;
     }
     float m[16];
 #pragma unroll
@@ -107,9 +146,9 @@ __device__ __forceinline__ void epi_store_chunk(const GemmArgs& args, int row, b
     }
   } else {
     float v[32];
+    dequant32(args, n, fast, acc, v);
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      v[j] = __fmaf_rn(acc_to_float(acc[j], small), args.scale, bias[j]);
       if constexpr (EPI == EPI_RELU_Q || EPI == EPI_RELU_F32_Q) v[j] = relu(v[j]);
       if constexpr (EPI == EPI_SIGMOID) v[j] = sigmoid_f64(v[j]);
     }
