@@ -1,0 +1,28 @@
+"""One launch (after warm-up) of a decoder kernel at the bench shape, for ncu.
+usage: KERNEL=dxd|out|attn M=630 python scripts/kernel_once.py"""
+import os, sys
+import numpy as np
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1805_12096_b200 import mnmt as M
+k = os.environ.get("KERNEL", "dxd")
+Mr = int(os.environ.get("M", 630))
+d, V, H = 256, 36000, 8
+dev = torch.device("cuda:0")
+if k in ("dxd", "out"):
+    N = d if k == "dxd" else V
+    A = torch.randint(-127, 128, (Mr, d), dtype=torch.int8, device=dev)
+    W = torch.randint(-127, 128, (N, d), dtype=torch.int8, device=dev)
+    b = torch.zeros(N, device=dev)
+    out = torch.empty((Mr, N) if k == "dxd" else (Mr,), dtype=torch.float32 if k == "dxd" else torch.int64, device=dev)
+    epi = M.EPI_F32 if k == "dxd" else M.EPI_ARGMAX
+    for _ in range(4):
+        M.op_gemm_i8(A.data_ptr(), W.data_ptr(), Mr, N, d, b.data_ptr(), 2.0, epi, out.data_ptr(), None, 0, None)
+else:
+    L = np.full(Mr, 21, np.int32); st = (np.arange(Mr) * 21).astype(np.int32)
+    kv = torch.randn(Mr * 21, 2 * d, device=dev); q = torch.randn(Mr, d, device=dev)
+    S, Ln = torch.from_numpy(st).to(dev), torch.from_numpy(L).to(dev)
+    oq = torch.empty(Mr, d, dtype=torch.int8, device=dev)
+    for _ in range(4):
+        M.op_attention(q.data_ptr(), d, kv.data_ptr(), 2 * d, 0, d, S.data_ptr(), Ln.data_ptr(), Mr, d, H, 2.0, oq.data_ptr(), None, None)
+torch.cuda.synchronize()
