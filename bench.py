@@ -15,6 +15,7 @@ Rank 0 prints ONE JSON line.
 from __future__ import annotations
 
 import argparse
+import re
 import json
 import os
 import statistics
@@ -303,6 +304,23 @@ def roofline_src_attn(dims, sset, budget, peaks, stream, mcr):
             "ms_per_launch": ms, "peak_source": peaks["source"]}
 
 
+def ncu_traffic(key, shape):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of this kernel from the committed
+    `ncu --set full` capture (profiles/r1_ncu_full_kernels.json, scripts/kernel_once.py), used
+    only when the captured shape has the same row count as the one timed here."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                        "r1_ncu_full_kernels.json")
+    try:
+        with open(path) as f:
+            rec = json.load(f)[key]
+    except (OSError, KeyError, ValueError):
+        return None, "no ncu capture"
+    rows = lambda t: (re.search(r"(?:M|rows)=(\d+)", t) or [None, None])[1]
+    if rows(rec["shape"]) != rows(shape):
+        return None, f"ncu capture shape {rec['shape']} differs"
+    return rec["traffic_bytes"], f"ncu --set full (cold L2), {rec['shape']}"
+
+
 # ---------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -440,6 +458,8 @@ def main():
                  roofline_dxd_gemm(dims, sset, budget, peaks, stream, mcr)]
         cands[1]["launches_per_step"] = len(live_rows_profile(sset, budget, mcr)) * dims.dec_layers
         cands[1]["ms_per_step_est"] = cands[1]["ms_per_launch"] * cands[1]["launches_per_step"]
+        for key, c in zip(("out", "attn", "dxd"), cands):
+            c["traffic"], c["traffic_source"] = ncu_traffic(key, c["shape"])
         roof = max(cands, key=lambda c: c["ms_per_step_est"])
         roof["share_of_step_est"] = roof["ms_per_step_est"] / (ms_max / args.steps)
         roof["other"] = {c["kernel"]: {"frac": c["frac"], "ms_per_step_est": c["ms_per_step_est"]}
