@@ -337,6 +337,14 @@ def main():
                     help="1: persistent step kernel per batch; 0: one kernel per op (CUDA graph)")
     ap.add_argument("--lanes", type=int, default=1,
                     help="independent decoder lanes (streams) per GPU (scheduling only)")
+    ap.add_argument("--lane-tiers", type=int, default=0,
+                    help="0: deal sentences round-robin to lanes; 10*p: contiguous length tiers "
+                         "of equal sum S^p (scheduling only)")
+    ap.add_argument("--steps-per-graph", type=int, default=1,
+                    help="decoder steps captured per CUDA graph (scheduling only)")
+    ap.add_argument("--fuse-ln", type=int, default=0,
+                    help="LayerNorm in the producing GEMM's epilogue: 0 separate kernels, "
+                         "1 one CTA per row block (d <= 256), 2 a CTA cluster per row block")
     ap.add_argument("--max-concurrent-rows", type=int, default=4096,
                     help="co-schedule consecutive >=budget-word batches in one decode wave "
                          "(scheduling only; 0 = one batch at a time)")
@@ -357,6 +365,8 @@ def main():
                     "beam": 1, "max_len": "source length", "parallelism": f"dp{args.gpus}",
                     "l2": "flushed between timed steps (512 MiB write)",
                     "max_concurrent_rows": args.max_concurrent_rows, "lanes": args.lanes,
+                    "fuse_ln": args.fuse_ln, "steps_per_graph": args.steps_per_graph,
+                    "lane_tiers": args.lane_tiers,
                     "step_engine": "persistent cooperative kernel" if args.megakernel else "kernel-per-op CUDA graph"}
 
     if args.impl == "reference":
@@ -380,6 +390,9 @@ def main():
     model.set_option("max_concurrent_rows", args.max_concurrent_rows)
     model.set_option("lanes", args.lanes)
     model.set_option("megakernel", args.megakernel)
+    model.set_option("fuse_ln", args.fuse_ln)
+    model.set_option("steps_per_graph", args.steps_per_graph)
+    model.set_option("lane_tiers", args.lane_tiers)
     sset = synth.newstest_set(seed=2014 + rank)          # weak scaling: one set per GPU
     stream = torch.cuda.current_stream()
     dev = torch.device("cuda", local)

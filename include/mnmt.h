@@ -153,12 +153,15 @@ mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids_host,
  *   "megakernel"           1: each batch's decoder steps run in ONE persistent
  *                          cooperative kernel (phases separated by grid barriers);
  *                          0 (default): one kernel per operation, replayed as a CUDA graph per step.
- *   "fuse_ln"              1: residual / gate + LayerNorm + Q fused into the epilogue
- *                          of the producing GEMM when one CTA can own whole rows (d = 192, 256);
+ *   "fuse_ln"              residual / gate + LayerNorm + Q fused into the epilogue of the
+ *                          producing GEMM: 1 = one CTA owns whole rows (d = 192, 256);
+ *                          2 = the d / BN N-tiles of a row block form a thread-block cluster
+ *                          and exchange row statistics through distributed shared memory;
  *                          0 (default, measured faster): separate LayerNorm kernels.
  *   "rowlocal"             persistent kernel only: 1 = GEMM/LayerNorm/embedding phases split by
  *                          128-row tile (CTA barriers between them), 0 (default) = split over the
  *                          grid with grid barriers.
+ *   "steps_per_graph"      1..63 consecutive decoder steps captured in one CUDA graph (default 1).
  *   "profile_phases"       1 = the persistent kernel stamps every phase (mnmt_debug_phase_*).
  * Errors: MNMT_ERR_ARG (unknown name or negative value). */
 mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, int64_t value);

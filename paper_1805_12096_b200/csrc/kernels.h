@@ -19,6 +19,7 @@ enum Epi : int {
   EPI_ACC = 6,        // out_i = acc                     (test hook: raw accumulators)
   EPI_LN = 7,         // full rows (BN = N = d): v = GEMM output; r = x + v (or the AAN gate
                       // form with v = f-gate logit); out = LN(r), Q(out), next-layer AAN step
+  EPI_LNC = 8,        // as EPI_LN, rows owned by a cluster of N / BN CTAs (gemm_lnc_bn)
 };
 
 struct GemmArgs {
@@ -48,6 +49,7 @@ cudaError_t launch_gemm_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const
                            int epi, int bn, cudaStream_t st);
 
 int gemm_pick_bn(int M, int N);   // 64, 128 or 256
+int gemm_lnc_bn(int d);           // EPI_LNC tile width for N = d (0: not supported)
 
 // Programmatic dependent launch on every kernel (env MNMT_NO_PDL=1 disables; A/B testing).
 bool pdl_enabled();

@@ -81,6 +81,7 @@ struct Workspace {
   CUtensorMap tm_cx, tm_cctx, tm_ch;
   // decoder (compact live rows)
   int32_t *ctrl = nullptr, *live = nullptr, *prev_id = nullptr;
+  int32_t *prev_live = nullptr, *live_start = nullptr, *live_len = nullptr;   // compact order
   int32_t *row_start = nullptr, *row_len = nullptr, *max_len = nullptr, *len_idx = nullptr;
   int64_t *out_off = nullptr, *forced_off = nullptr;
   int32_t* forced = nullptr;
@@ -101,7 +102,7 @@ struct JobBuf {
   int32_t* out_len = nullptr;   // [n]
   int32_t* src_ids = nullptr;   // [sum S_i]
   int32_t* meta = nullptr;      // token metadata of all batches: idx|pos|start|len per batch
-  int32_t* rmeta32 = nullptr;   // row metadata of all batches: [start|len|max_len|len_idx] x B_b
+  int32_t* rmeta32 = nullptr;   // row metadata of all batches: [start|len|max_len|len_idx|order] x B_b
   int64_t* rmeta64 = nullptr;   // [out_off|forced_off] x B_b
 };
 
@@ -115,6 +116,7 @@ struct Lane {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::map<int64_t, cudaGraphExec_t> graphs;   // key: padded live-row bound
   int64_t launches_per_step = 0;
+  int span_cap = 0;                            // attention span the step kernels are sized for
   // persistent step kernel program (built for this lane's workspace)
   Phase* d_phases = nullptr;
   int n_phases = 0;
@@ -154,6 +156,9 @@ struct mnmt_model {
   int profile_phases = 0;              // option: record per-phase timestamps (lane 0)
   int fuse_ln = 0;                     // option: LayerNorm fused into full-row GEMM epilogues
   int rowlocal = 0;                    // option: row-local phases in the persistent step kernel (measured slower)
+  int steps_per_graph = 1;             // option: decoder steps captured per CUDA graph
+  int lane_tiers = 0;                  // option: 0 = deal sentences round-robin to lanes;
+                                       // p*10 = contiguous length tiers of equal sum S^p
 };
 
 namespace {
@@ -362,7 +367,7 @@ static mnmt_status jb_ensure(mnmt_model* m, int64_t O, int64_t N, int64_t tok, i
   CKS(dalloc(z.allocs, &z.out_len, Nc));
   CKS(dalloc(z.allocs, &z.src_ids, tc));
   CKS(dalloc(z.allocs, &z.meta, mc));
-  CKS(dalloc(z.allocs, &z.rmeta32, 4 * rc));
+  CKS(dalloc(z.allocs, &z.rmeta32, 5 * rc));
   CKS(dalloc(z.allocs, &z.rmeta64, 2 * rc));
   return MNMT_OK;
 }
@@ -391,6 +396,9 @@ static mnmt_status lane_ensure(mnmt_model* m, Lane& Ln, int64_t M, int64_t B, in
   CKS(dalloc(A, &z.ctrl, 64));
   CKS(dalloc(A, &z.live, Bc));
   CKS(dalloc(A, &z.prev_id, Bc));
+  CKS(dalloc(A, &z.prev_live, Bc));
+  CKS(dalloc(A, &z.live_start, Bc));
+  CKS(dalloc(A, &z.live_len, Bc));
   CKS(dalloc(A, &z.row_start, Bc));
   CKS(dalloc(A, &z.row_len, Bc));
   CKS(dalloc(A, &z.max_len, Bc));
@@ -446,8 +454,10 @@ static cudaError_t gemm(mnmt_model* m, cudaStream_t st, const CUtensorMap& tmA, 
 
 // Fused GEMM + residual (+gate) + LayerNorm + Q (+ next-layer AAN) when one CTA can own
 // whole rows (d in {192, 256}); otherwise false (the caller runs GEMM then k_ln).
+// fuse_ln 1: one CTA owns whole rows (d in {192, 256}); 2: a cluster of d / BN CTAs owns them.
 static bool fuse_ln(const mnmt_model* m) {
-  return (m->c.d_model == 192 || m->c.d_model == 256) && m->fuse_ln;
+  if (m->fuse_ln == 2) return gemm_lnc_bn(m->c.d_model) != 0;
+  return (m->c.d_model == 192 || m->c.d_model == 256) && m->fuse_ln == 1;
 }
 
 static cudaError_t gemm_ln(mnmt_model* m, cudaStream_t st, const CUtensorMap& tmA, const Lin& W,
@@ -464,7 +474,7 @@ static cudaError_t gemm_ln(mnmt_model* m, cudaStream_t st, const CUtensorMap& tm
   a.ldo = W.out;
   a.col_block = W.out;
   a.ln = ln;
-  return launch_gemm_i8(tmA, W.tm, a, EPI_LN, 0, st);
+  return launch_gemm_i8(tmA, W.tm, a, m->fuse_ln == 2 ? EPI_LNC : EPI_LN, 0, st);
 }
 
 static LnArgs ln_args(mnmt_model* m, const Workspace& w, int n, const int32_t* n_dyn, const float* x,
@@ -508,9 +518,12 @@ static AanOut aan_for_layer(mnmt_model* m, const Workspace& w, int l) {
 }
 
 // Encoder over M tokens (A2-A4).  meta: [idx M][pos M][start M][len M].
-static cudaError_t launch_encoder(mnmt_model* m, Lane& Ln, int M, int n_sent, int s_max, const int32_t* tok_idx,
-                                  const int32_t* tok_pos, const int32_t* tok_start,
-                                  const int32_t* tok_len, int64_t* nlaunch) {
+// order: the batch's rows in (length, row) order (device); buckets: {first, count, longest} ranges
+// of it, one encoder-attention launch each.
+static cudaError_t launch_encoder(mnmt_model* m, Lane& Ln, int M, const int32_t* order,
+                                  const std::vector<std::array<int, 3>>& buckets,
+                                  const int32_t* tok_idx, const int32_t* tok_pos,
+                                  const int32_t* tok_start, const int32_t* tok_len, int64_t* nlaunch) {
   (void)tok_start;
   (void)tok_len;   // sentence spans come from the row metadata (row_start / row_len)
   auto& w = Ln.ws;
@@ -529,15 +542,20 @@ static cudaError_t launch_encoder(mnmt_model* m, Lane& Ln, int M, int n_sent, in
     at.qkv = w.qkv;
     at.sent_start = w.row_start;
     at.sent_len = w.row_len;
-    at.n_sent = n_sent;
-    at.s_max = s_max;
     at.H = c.n_heads;
     at.dh = d / c.n_heads;
     at.d = d;
     at.clip = c.clip;
     at.sigma = sigma_of(m);
     at.out_q = w.cctx;
-    if ((e = launch_attn_enc(at, st)) != cudaSuccess) return e;
+    for (const auto& bk : buckets) {
+      at.sent_order = order + bk[0];
+      at.n_sent = bk[1];
+      at.s_max = bk[2];
+      if ((e = launch_attn_enc(at, st)) != cudaSuccess) return e;
+      ++*nlaunch;
+    }
+    --*nlaunch;   // counted below with the layer's other kernels
     LnArgs la = ln_args(m, w, M, nullptr, w.x, w.o, E.ln1g, E.ln1b, w.x, w.cx);
     LnArgs lb = ln_args(m, w, M, nullptr, w.x, w.o, E.ln2g, E.ln2b, w.x, w.cx);
     if (fuse_ln(m)) {
@@ -585,6 +603,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
   ea.ctrl = w.ctrl;
   ea.live = w.live;
   ea.prev_id = w.prev_id;
+  ea.prev_live = w.prev_live;
   ea.E = m->E;
   ea.PE = m->PE;
   ea.d = d;
@@ -648,6 +667,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
       if ((e = gemm(m, st, w.tm_cy, D.qkv, n, nd, EPI_F32, w.qkvd, nullptr, 3 * d)) != cudaSuccess) return e;
       AttnArgs at{};
       at.mode = ATTN_SELF;
+      at.span = Ln.span_cap;
       at.n = n;
       at.n_dyn = nd;
       at.ctrl = w.ctrl;
@@ -680,6 +700,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
     if ((e = gemm(m, st, w.tm_cx1, D.sq, n, nd, EPI_F32, w.qs, nullptr, d)) != cudaSuccess) return e;
     AttnArgs as{};
     as.mode = ATTN_SRC;
+    as.span = Ln.span_cap;
     as.n = n;
     as.n_dyn = nd;
     as.ctrl = w.ctrl;
@@ -695,6 +716,8 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
     as.v_off = d;
     as.kv_start = w.row_start;
     as.kv_len = w.row_len;
+    as.live_start = w.live_start;
+    as.live_len = w.live_len;
     as.clip = c.clip;
     as.sigma = sigma_of(m);
     as.out_q = w.cctxd;
@@ -752,6 +775,11 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
   fa.eos = c.eos_id;
   fa.forced = forced ? w.forced : nullptr;
   fa.forced_off = forced ? w.forced_off : nullptr;
+  fa.prev_live = w.prev_live;
+  fa.row_start = w.row_start;
+  fa.row_len = w.row_len;
+  fa.live_start = w.live_start;
+  fa.live_len = w.live_len;
   if ((e = launch_finish(fa, st)) != cudaSuccess) return e;
   k += 2;
   *nlaunch += k;
@@ -878,6 +906,7 @@ static mnmt_status build_program(mnmt_model* m, Lane& Ln, bool forced) {
       P.type = PH_ATTN;
       AttnArgs& at = P.at;
       at.mode = ATTN_SELF;
+      at.span = Ln.span_cap;
       at.n = n;
       at.n_dyn = nd;
       at.ctrl = w.ctrl;
@@ -1010,13 +1039,15 @@ struct Batch {
   int lane = 0;               // decoder lane (stream) that runs this batch
   int S_max = 1;              // longest source sentence
   std::vector<int32_t> alive; // alive[t-1] = rows with max_len >= t (upper bound of live rows)
+  // encoder attention launches: {first index into the length-sorted row order, rows, longest}
+  std::vector<std::array<int, 3>> enc_buckets;
 };
 
 struct Job {
   std::vector<Batch> batches;
   std::vector<int32_t> meta;  // per batch: tok_idx, tok_pos, tok_start, tok_len (4 x M)
   std::vector<int64_t> out_off;  // per sentence: output offset (prefix sum of max_len)
-  std::vector<int32_t> rmeta32;  // per batch: [row_start|row_len|max_len|len_idx] x B
+  std::vector<int32_t> rmeta32;  // per batch: [row_start|row_len|max_len|len_idx|len_order] x B
   std::vector<int64_t> rmeta64;  // per batch: [out_off|forced_off] x B
   std::vector<int64_t> r0;       // per batch: first row in rmeta
   int64_t out_total = 0, tok_total = 0, rows_total = 0;
@@ -1100,13 +1131,13 @@ static void plan_rows(Job& job, const int64_t* src_off, const int32_t* max_len, 
   job.rmeta64.clear();
   job.r0.clear();
   int64_t r0 = 0;
-  for (const Batch& b : job.batches) {
+  for (Batch& b : job.batches) {
     const int B = (int)b.rows.size();
     job.r0.push_back(r0);
-    job.rmeta32.resize((size_t)4 * (r0 + B));
+    job.rmeta32.resize((size_t)5 * (r0 + B));
+    int32_t* rs = job.rmeta32.data() + 5 * r0;
+    int32_t *rl = rs + B, *ml = rs + 2 * B, *li = rs + 3 * B, *ord = rs + 4 * B;
     job.rmeta64.resize((size_t)2 * (r0 + B));
-    int32_t* rs = job.rmeta32.data() + 4 * r0;
-    int32_t *rl = rs + B, *ml = rs + 2 * B, *li = rs + 3 * B;
     int64_t* oo = job.rmeta64.data() + 2 * r0;
     int64_t* fo = oo + B;
     int64_t t = 0;
@@ -1120,6 +1151,18 @@ static void plan_rows(Job& job, const int64_t* src_off, const int32_t* max_len, 
       oo[r] = job.out_off[s];
       fo[r] = forced ? forced_off[s] : 0;
       t += S;
+    }
+    // rows in (length, row) order, cut into length buckets for the encoder attention
+    for (int r = 0; r < B; ++r) ord[r] = r;
+    std::stable_sort(ord, ord + B, [&](int32_t x, int32_t y) { return rl[x] < rl[y]; });
+    static const int kEdges[] = {8, 16, 32, 64, 96, 128, 160, MNMT_MAX_SPAN};
+    b.enc_buckets.clear();
+    for (int i = 0, e = 0; i < B;) {
+      while (rl[ord[i]] > kEdges[e]) ++e;
+      int j = i;
+      while (j < B && rl[ord[j]] <= kEdges[e]) ++j;
+      b.enc_buckets.push_back({i, j - i, rl[ord[j - 1]]});
+      i = j;
     }
     r0 += B;
   }
@@ -1159,7 +1202,7 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
     auto& w = Ln.ws;
     cudaStream_t st = Ln.st;
     const int B = (int)b.rows.size();
-    const int32_t* r32 = m->jb.rmeta32 + 4 * job.r0[bi];
+    const int32_t* r32 = m->jb.rmeta32 + 5 * job.r0[bi];
     const int64_t* r64 = m->jb.rmeta64 + 2 * job.r0[bi];
     CK(cudaMemcpyAsync(w.row_start, r32, B * 4, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(w.row_len, r32 + B, B * 4, cudaMemcpyDeviceToDevice, st));
@@ -1169,12 +1212,25 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
     if (forced) CK(cudaMemcpyAsync(w.forced_off, r64 + B, B * 8, cudaMemcpyDeviceToDevice, st));
     const int32_t* base = m->jb.meta + b.tok0;
     const int M = (int)b.M;
-    CK(launch_encoder(m, Ln, M, B, b.S_max, base, base + M, base + 2 * M, base + 3 * M, &launches));
+    CK(launch_encoder(m, Ln, M, r32 + 4 * B, b.enc_buckets, base, base + M, base + 2 * M, base + 3 * M,
+                      &launches));
     if (c.decoder == 1)
       CK(cudaMemsetAsync(w.C, 0, (size_t)c.dec_layers * w.B_cap * d * sizeof(float), st));
-    CK(launch_decode_init(w.ctrl, w.live, B, w.keys, st));
+    CK(launch_decode_init(w.ctrl, w.live, B, w.keys, w.row_start, w.row_len, w.live_start,
+                          w.live_len, st));
     launches += 1;
     const int npad = (B + 127) / 128 * 128;
+    // attention scratch is sized by the longest span a step can attend (source length, or the
+    // step count for the self-attention decoder); it only grows, and captured graphs are
+    // rebuilt when it does
+    {
+      const int need = std::max(b.S_max, c.decoder == 0 ? b.T : 0);
+      if (need > Ln.span_cap) {
+        for (auto& kv : Ln.graphs) cudaGraphExecDestroy(kv.second);
+        Ln.graphs.clear();
+        Ln.span_cap = std::min(MNMT_MAX_KV, (need + 31) / 32 * 32);
+      }
+    }
     // per-step row bound: rows are compacted to the front and a row never outlives its
     // max_len, so step t needs at most alive[t-1] rows -> the smallest cached graph that fits
     auto pad_at = [&](int t) { return (b.alive[t] + 127) / 128 * 128; };
@@ -1208,26 +1264,35 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
         }
       }
     } else if (use_graphs && !hook) {
-      for (int t = 0; t < b.T; ++t) {
-        const int np = pad_at(t);
-        auto it = Ln.graphs.find(np);
+      // k consecutive steps per graph (PDL chains the kernels inside a graph, not across
+      // graph launches), sized for the first step's row bound (rows only decrease)
+      const int K = std::max(1, m->steps_per_graph);
+      for (int t = 0; t < b.T;) {
+        const int np = pad_at(t), k = std::min(K, b.T - t);
+        const int64_t key = (int64_t)np * 64 + k;
+        auto it = Ln.graphs.find(key);
         if (it == Ln.graphs.end()) {
           cudaGraph_t g;
           CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
           int64_t per_step = 0;
-          cudaError_t e = launch_step(m, Ln, np, forced, nullptr, &per_step);
+          cudaError_t e = cudaSuccess;
+          for (int u = 0; u < k && e == cudaSuccess; ++u) {
+            per_step = 0;
+            e = launch_step(m, Ln, np, forced, nullptr, &per_step);
+          }
           cudaError_t e2 = cudaStreamEndCapture(st, &g);
           CK(e);
           CK(e2);
           cudaGraphExec_t ge;
           CK(cudaGraphInstantiate(&ge, g, 0));
           cudaGraphDestroy(g);
-          it = Ln.graphs.emplace(np, ge).first;
+          it = Ln.graphs.emplace(key, ge).first;
           Ln.launches_per_step = per_step;
         }
         CK(cudaGraphLaunch(it->second, st));
+        launches += (int64_t)k * Ln.launches_per_step;
+        t += k;
       }
-      launches += (int64_t)b.T * Ln.launches_per_step;
     } else {
       for (int t = 0; t < b.T; ++t) CK(launch_step(m, Ln, npad, forced, hook, &launches));
     }
@@ -1505,12 +1570,37 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
       int e = b + 1;
       if (m->max_concurrent_rows > 0)
         while (e < nb && off[e + 1] - off[b] <= m->max_concurrent_rows) ++e;
-      for (int li = 0; li < P; ++li) {
+      if (m->lane_tiers > 0 && P > 1) {
+        // contiguous length tiers: lane li takes the li-th of P equal shares of
+        // sum_i S_i^p (p = lane_tiers / 10) in length order, so the long-sentence tail runs on
+        // its own lane beside the bulk instead of stretching every lane's step count
+        const double pw = m->lane_tiers / 10.0;
+        double tot = 0.0;
+        for (int i = off[b]; i < off[e]; ++i) tot += std::pow((double)L[order[i]], pw);
+        double acc = 0.0;
+        int li = 0;
         std::vector<int32_t> part;
-        for (int i = off[b] + li; i < off[e]; i += P) part.push_back(order[i]);
+        for (int i = off[b]; i < off[e]; ++i) {
+          part.push_back(order[i]);
+          acc += std::pow((double)L[order[i]], pw);
+          if (li < P - 1 && acc >= tot * (li + 1) / P) {
+            rows.push_back(std::move(part));
+            lanes_of.push_back(li++);
+            part.clear();
+          }
+        }
         if (!part.empty()) {
           rows.push_back(std::move(part));
           lanes_of.push_back(li);
+        }
+      } else {
+        for (int li = 0; li < P; ++li) {
+          std::vector<int32_t> part;
+          for (int i = off[b] + li; i < off[e]; i += P) part.push_back(order[i]);
+          if (!part.empty()) {
+            rows.push_back(std::move(part));
+            lanes_of.push_back(li);
+          }
         }
       }
       b = e;
@@ -1744,11 +1834,22 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
     return MNMT_OK;
   }
   if (std::string(name) == "fuse_ln") {
-    m->fuse_ln = value ? 1 : 0;
+    if (value > 2) { set_err("fuse_ln must be 0, 1 or 2"); return MNMT_ERR_ARG; }
+    m->fuse_ln = (int)value;
     for (Lane& L : m->lanes) {   // captured graphs encode the old kernel sequence
       for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
       L.graphs.clear();
     }
+    return MNMT_OK;
+  }
+  if (std::string(name) == "lane_tiers") {
+    if (value < 0 || value > 100) { set_err("lane_tiers must be in [0, 100]"); return MNMT_ERR_ARG; }
+    m->lane_tiers = (int)value;
+    return MNMT_OK;
+  }
+  if (std::string(name) == "steps_per_graph") {
+    if (value < 1 || value > 63) { set_err("steps_per_graph must be in [1, 63]"); return MNMT_ERR_ARG; }
+    m->steps_per_graph = (int)value;
     return MNMT_OK;
   }
   if (std::string(name) == "megakernel") {

@@ -95,8 +95,8 @@ __global__ void k_embed_tgt(EmbedTgtArgs a) {
   pdl_wait();
   pdl_trigger_early();
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (r >= a.ctrl[0]) return;
-  embed_tgt_row<NV>(a, r);
+  if (r >= a.n) return;
+  embed_tgt_row<NV>(a, r);   // checks the live-row count itself
 }
 
 template <int NV>
@@ -104,24 +104,32 @@ __global__ void k_ln(LnArgs a) {
   pdl_wait();
   pdl_trigger_early();
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
-  if (r >= n_live) return;
-  ln_row<NV>(a, r);
+  if (r >= a.n) return;
+  ln_row<NV>(a, r);   // checks the live-row count itself, after issuing its loads
 }
 
 constexpr int ATTN_WARPS = 8;
 
-// Decoder (SRC, SELF) and op-level (ENC) attention: one warp per (row, head).
+// Decoder (SRC, SELF) and op-level (ENC) attention: one warp per (row, head), staged body.
+// Dynamic smem: ATTN_WARPS x attn_staged_warp_bytes(span, dh).
+template <int D4MAX>
 __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn(AttnArgs a) {
-  extern __shared__ double sc_dyn[];   // [ATTN_WARPS][span]
+  extern __shared__ __align__(16) uint8_t attn_smem[];
   pdl_wait();
   pdl_trigger_early();
   const int wi = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * ATTN_WARPS + wi;
   const int r = (int)(gw / a.H), h = (int)(gw - (int64_t)r * a.H);
+  if (r >= a.n) return;
+  // independent loads first: live-row count and (src mode) the row's span in compact order
   const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
+  const int pst = a.live_start ? a.live_start[r] : 0, pln = a.live_start ? a.live_len[r] : 0;
   if (r >= n_live) return;
-  attn_row_head(a, r, h, sc_dyn + (size_t)wi * (a.span + 64), a.span);
+  uint8_t* mine = attn_smem + (size_t)wi * attn_staged_warp_bytes(a.span, a.dh);
+  double* sc = reinterpret_cast<double*>(mine);
+  double* qd = sc + ((a.span + 1) & ~1);
+  float* vt = reinterpret_cast<float*>(qd + 64);
+  attn_row_head_staged<D4MAX>(a, r, h, sc, qd, vt, pst, pln);
 }
 
 constexpr int FIN_THREADS = 1024;
@@ -139,19 +147,23 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finish(FinishArgs a) {
 // its query rows (warp per query).  Sentences longer than ENC_STAGE_MAX read from L2/HBM.
 constexpr int ENC_STAGE_MAX = 160;
 
-__host__ __device__ inline size_t enc_attn_smem(int dh, int s_max) {
+// Launches are bucketed by sentence length (sent_order + s_max per bucket) so that shared
+// memory, and with it the number of resident CTAs, follows the bucket's longest sentence.
+__host__ __device__ inline size_t enc_attn_smem(int dh, int s_max, int warps) {
   const int staged = s_max < ENC_STAGE_MAX ? s_max : ENC_STAGE_MAX;
-  return (size_t)ATTN_WARPS * (s_max + 64) * sizeof(double) +
+  return (size_t)warps * (s_max + 64) * sizeof(double) +
          2 * (size_t)staged * (dh + 2) * sizeof(double);
 }
+inline int enc_attn_warps(int s_max) { return s_max <= 8 ? 4 : ATTN_WARPS; }
 
 __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn_enc(EncAttnArgs a) {
   extern __shared__ __align__(16) uint8_t enc_smem[];
+  const int nw = blockDim.x >> 5;
   double* sc = reinterpret_cast<double*>(enc_smem);                       // [warps][s_max + 64]
-  double* ks = sc + (size_t)ATTN_WARPS * (a.s_max + 64);
+  double* ks = sc + (size_t)nw * (a.s_max + 64);
   pdl_wait();
   pdl_trigger_early();
-  const int s = blockIdx.x, h = blockIdx.y;
+  const int s = a.sent_order ? a.sent_order[blockIdx.x] : (int)blockIdx.x, h = blockIdx.y;
   const int dh = a.dh, d = a.d, ld3 = 3 * d, lds = dh + 2;
   const int start = a.sent_start[s], len = a.sent_len[s];
   const int staged = a.s_max < ENC_STAGE_MAX ? a.s_max : ENC_STAGE_MAX;
@@ -172,24 +184,142 @@ __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn_enc(EncAttnArgs a) {
       vd[0] = v4.x; vd[1] = v4.y; vd[2] = v4.z; vd[3] = v4.w;
     }
     __syncthreads();
-    for (int i = wi; i < len; i += ATTN_WARPS)
+    for (int i = wi; i < len; i += nw)
       warp_attend<double>(base + (int64_t)i * ld3, ks, vs, lds, len, dh, scw, scw + a.s_max, a.clip,
                           a.sigma, a.out_q + (int64_t)(start + i) * d + h * dh, nullptr);
   } else {
-    for (int i = wi; i < len; i += ATTN_WARPS)
+    for (int i = wi; i < len; i += nw)
       warp_attend<float>(base + (int64_t)i * ld3, base + d, base + 2 * d, ld3, len, dh, scw,
                          scw + a.s_max, a.clip, a.sigma, a.out_q + (int64_t)(start + i) * d + h * dh,
                          nullptr);
   }
 }
 
+// Encoder self-attention, lane = query row (A3): one CTA per (sentence, head) with
+// ceil(S_max / 32) warps.  K and V head slices are staged once as fp64 in shared memory and read
+// as warp-wide broadcasts (one wavefront feeds 32 lanes x 2 FMAs); each lane keeps its query in
+// registers (32-column chunks); scores live in shared memory [S][nq] (column = query lane).
+// The arithmetic and its order are the plain definition (R20): dot over c in order, scale,
+// max, p_j = exp(s_j - max), Z = sum_j p_j in order, ctx_c = (sum_j p_j v_jc in order) / Z.
+// NCH = 32-column chunks of dh (1: dh <= 32, 2: dh <= 64).
+__host__ __device__ inline int enc_q_max(int dh) { return dh <= 32 ? 128 : 96; }
+__host__ __device__ inline size_t enc_q_smem(int dh, int s_max) {
+  const int nq = (s_max + 31) / 32 * 32;
+  return (size_t)(2 * dh + nq) * s_max * sizeof(double);
+}
+
+template <int NCH>
+__global__ void __launch_bounds__(128) k_attn_enc_q(EncAttnArgs a) {
+  extern __shared__ __align__(16) double es[];
+  const int nq = blockDim.x, S = a.s_max, dh = a.dh, d = a.d, ld3 = 3 * d;
+  double* Ks = es;                 // [S][dh]
+  double* Vs = Ks + S * dh;        // [S][dh]
+  double* sc = Vs + S * dh;        // [S][nq]
+  pdl_wait();
+  pdl_trigger_early();
+  const int s = a.sent_order ? a.sent_order[blockIdx.x] : (int)blockIdx.x, h = blockIdx.y;
+  const int start = a.sent_start[s], len = a.sent_len[s];
+  const float* base = a.qkv + (int64_t)start * ld3 + h * dh;
+  const int d4 = dh >> 2;
+  for (int idx = threadIdx.x; idx < len * d4; idx += nq) {
+    const int j = idx / d4, c4 = idx - j * d4;
+    const float4 k4 = *reinterpret_cast<const float4*>(base + (int64_t)j * ld3 + d + 4 * c4);
+    const float4 v4 = *reinterpret_cast<const float4*>(base + (int64_t)j * ld3 + 2 * d + 4 * c4);
+    double* kd = Ks + j * dh + 4 * c4;
+    double* vd = Vs + j * dh + 4 * c4;
+    kd[0] = k4.x; kd[1] = k4.y; kd[2] = k4.z; kd[3] = k4.w;
+    vd[0] = v4.x; vd[1] = v4.y; vd[2] = v4.z; vd[3] = v4.w;
+  }
+  __syncthreads();
+  const int i = threadIdx.x;
+  if (i >= len) return;            // no further block-wide barriers
+  const float* qrow = base + (int64_t)i * ld3;
+  // ---- scores: dot over c in order, in 32-column chunks (partial dots parked in sc)
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) {
+    double qr[32];
+#pragma unroll
+    for (int c = 0; c < 32; c += 4) {
+      const int cc = ch * 32 + c;
+      float4 q4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (cc < dh) q4 = *reinterpret_cast<const float4*>(qrow + cc);
+      qr[c] = q4.x; qr[c + 1] = q4.y; qr[c + 2] = q4.z; qr[c + 3] = q4.w;
+    }
+#pragma unroll 4
+    for (int j = 0; j < len; ++j) {
+      double dot = ch ? sc[j * nq + i] : 0.0;
+      const double* kr = Ks + j * dh + ch * 32;
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        if (ch * 32 + c < dh) {
+          const double2 k2 = *reinterpret_cast<const double2*>(kr + c);   // broadcast
+          dot = __dadd_rn(dot, __dmul_rn(qr[c], k2.x));
+          dot = __dadd_rn(dot, __dmul_rn(qr[c + 1], k2.y));
+        }
+      }
+      sc[j * nq + i] = dot;
+    }
+  }
+  // ---- softmax over the sentence (sequential in j)
+  const double inv_sqrt = 1.0 / sqrt((double)dh);
+  double mx = -INFINITY;
+  for (int j = 0; j < len; ++j) {
+    const double sj = __dmul_rn(sc[j * nq + i], inv_sqrt);
+    sc[j * nq + i] = sj;
+    mx = fmax(mx, sj);
+  }
+  double z = 0.0;
+  for (int j = 0; j < len; ++j) {
+    const double p = exp(__dsub_rn(sc[j * nq + i], mx));
+    sc[j * nq + i] = p;
+    z = __dadd_rn(z, p);
+  }
+  // ---- context, 32 columns at a time: acc_c = sum_j p_j v_jc in order; ctx = acc / Z
+  int8_t* orow = a.out_q + (int64_t)(start + i) * d + h * dh;
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) {
+    double acc[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) acc[c] = 0.0;
+    for (int j = 0; j < len; ++j) {
+      const double p = sc[j * nq + i];
+      const double* vr = Vs + j * dh + ch * 32;
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        if (ch * 32 + c < dh) {
+          const double2 v2 = *reinterpret_cast<const double2*>(vr + c);   // broadcast
+          acc[c] = __dadd_rn(acc[c], __dmul_rn(p, v2.x));
+          acc[c + 1] = __dadd_rn(acc[c + 1], __dmul_rn(p, v2.y));
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 32; c += 4) {
+      const int cc = ch * 32 + c;
+      if (cc < dh) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          w |= (uint32_t)(q8((float)__ddiv_rn(acc[c + u], z), a.clip, a.sigma) & 0xff) << (8 * u);
+        *reinterpret_cast<uint32_t*>(orow + cc) = w;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ decode init
-__global__ void k_decode_init(int32_t* ctrl, int32_t* live, int B, unsigned long long* keys) {
+__global__ void k_decode_init(int32_t* ctrl, int32_t* live, int B, unsigned long long* keys,
+                              const int32_t* row_start, const int32_t* row_len,
+                              int32_t* live_start, int32_t* live_len) {
   pdl_wait();
   pdl_trigger_early();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B; i += gridDim.x * blockDim.x) {
     live[i] = i;
     keys[i] = 0ull;
+    if (live_start) {
+      live_start[i] = row_start[i];
+      live_len[i] = row_len[i];
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     ctrl[0] = B;
@@ -233,8 +363,10 @@ cudaError_t launch_embed_src(const int32_t* ids, const int32_t* idx, const int32
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_embed_tgt(const EmbedTgtArgs& a, int rows, cudaStream_t st) {
+cudaError_t launch_embed_tgt(const EmbedTgtArgs& a_in, int rows, cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
+  EmbedTgtArgs a = a_in;
+  a.n = rows;
   dim3 grid((rows + ROW_WARPS - 1) / ROW_WARPS), block(32 * ROW_WARPS);
   switch (nv_for(a.d)) {
     case 1: return launch_pdl(k_embed_tgt<1>, grid, block, 0, st, a);
@@ -268,7 +400,7 @@ static cudaError_t set_carveouts() {
                        (const void*)k_embed_tgt<1>, (const void*)k_embed_tgt<2>,
                        (const void*)k_embed_tgt<4>, (const void*)k_embed_tgt<8>,
                        (const void*)k_ln<1>, (const void*)k_ln<2>, (const void*)k_ln<4>, (const void*)k_ln<8>,
-                       (const void*)k_attn, (const void*)k_attn_enc, (const void*)k_finish,
+                       (const void*)k_attn<8>, (const void*)k_attn<16>, (const void*)k_attn_enc, (const void*)k_finish,
                        (const void*)k_decode_init};
   for (const void* f : fns) {
     cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -284,10 +416,19 @@ cudaError_t attn_init() {   // once per device
   if (e != cudaSuccess) return e;
   if (dev >= 0 && dev < 64 && done[dev]) return cudaSuccess;
   e = cudaFuncSetAttribute(k_attn_enc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)enc_attn_smem(64, MNMT_MAX_KV));
+                           (int)enc_attn_smem(64, MNMT_MAX_KV, ATTN_WARPS));
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_attn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             ATTN_WARPS * (MNMT_MAX_KV + 64) * (int)sizeof(double));
+    e = cudaFuncSetAttribute(k_attn_enc_q<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)enc_q_smem(32, enc_q_max(32)));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn_enc_q<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)enc_q_smem(64, enc_q_max(64)));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             ATTN_WARPS * (int)attn_staged_warp_bytes(MNMT_MAX_KV, 32));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             ATTN_WARPS * (int)attn_staged_warp_bytes(MNMT_MAX_KV, 64));
   if (e == cudaSuccess) e = set_carveouts();
   if (e == cudaSuccess) {
     const char* pe = getenv("MNMT_PDL_EARLY");
@@ -303,14 +444,24 @@ cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
   const int64_t warps = (int64_t)a.n * a.H;
   AttnArgs b = a;
   if (b.span <= 0 || b.span > MNMT_MAX_KV) b.span = MNMT_MAX_KV;
-  return launch_pdl(k_attn, dim3((unsigned)((warps + ATTN_WARPS - 1) / ATTN_WARPS)),
-                    dim3(ATTN_WARPS * 32), (size_t)ATTN_WARPS * (b.span + 64) * sizeof(double), st, b);
+  if (b.dh > 64 || (b.dh & 3)) return cudaErrorInvalidValue;
+  const dim3 grid((unsigned)((warps + ATTN_WARPS - 1) / ATTN_WARPS)), block(ATTN_WARPS * 32);
+  const size_t smem = (size_t)ATTN_WARPS * attn_staged_warp_bytes(b.span, b.dh);
+  return b.dh <= 32 ? launch_pdl(k_attn<8>, grid, block, smem, st, b)
+                    : launch_pdl(k_attn<16>, grid, block, smem, st, b);
 }
 
 cudaError_t launch_attn_enc(const EncAttnArgs& a, cudaStream_t st) {
   if (a.n_sent <= 0) return cudaSuccess;
   if (a.s_max < 1 || a.s_max > MNMT_MAX_KV) return cudaErrorInvalidValue;
-  return launch_pdl(k_attn_enc, dim3(a.n_sent, a.H), dim3(ATTN_WARPS * 32), enc_attn_smem(a.dh, a.s_max),
+  if (a.s_max <= enc_q_max(a.dh) && a.dh <= 64 && (a.dh & 3) == 0) {
+    const dim3 grid(a.n_sent, a.H), block((a.s_max + 31) / 32 * 32);
+    const size_t smem = enc_q_smem(a.dh, a.s_max);
+    return a.dh <= 32 ? launch_pdl(k_attn_enc_q<1>, grid, block, smem, st, a)
+                      : launch_pdl(k_attn_enc_q<2>, grid, block, smem, st, a);
+  }
+  const int nw = enc_attn_warps(a.s_max);
+  return launch_pdl(k_attn_enc, dim3(a.n_sent, a.H), dim3(nw * 32), enc_attn_smem(a.dh, a.s_max, nw),
                     st, a);
 }
 
@@ -319,11 +470,13 @@ cudaError_t launch_finish(const FinishArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_decode_init(int32_t* ctrl, int32_t* live, int B, unsigned long long* keys,
-                               cudaStream_t st) {
+                               const int32_t* row_start, const int32_t* row_len,
+                               int32_t* live_start, int32_t* live_len, cudaStream_t st) {
   int blocks = (B + 255) / 256;
   if (blocks < 1) blocks = 1;
   if (blocks > 148) blocks = 148;
-  return launch_pdl(k_decode_init, dim3(blocks), dim3(256), 0, st, ctrl, live, B, keys);
+  return launch_pdl(k_decode_init, dim3(blocks), dim3(256), 0, st, ctrl, live, B, keys, row_start,
+                    row_len, live_start, live_len);
 }
 
 // ------------------------------------------------------------------ op-level helpers (tests)

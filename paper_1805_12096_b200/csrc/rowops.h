@@ -17,9 +17,11 @@ struct AanOut {
 };
 
 struct EmbedTgtArgs {
+  int n;                    // static row bound (grid)
   const int32_t* ctrl;      // [0] = live rows, [1] = t
   const int32_t* live;      // compact -> original row
   const int32_t* prev_id;   // [orig] previous output id
+  const int32_t* prev_live; // optional: [compact] previous output id (written by k_finish)
   const float* E;
   const float* PE;
   int d;
@@ -66,6 +68,8 @@ struct AttnArgs {
   int k_off, v_off;
   const int32_t* kv_start;  // enc: [row]; src: [orig]
   const int32_t* kv_len;
+  const int32_t* live_start;   // optional (src): kv_start / kv_len in compact row order
+  const int32_t* live_len;
   int t_cap;                // self mode: cache rows per sentence
   float clip, sigma;
   int8_t* out_q;            // Q(ctx) [n x d]
@@ -77,7 +81,8 @@ struct EncAttnArgs {
   const float* qkv;
   const int32_t* sent_start;   // [n_sent] first token row of each sentence
   const int32_t* sent_len;     // [n_sent]
-  int n_sent, H, dh, d;
+  const int32_t* sent_order;   // optional: CTA x -> sentence sent_order[x] (a length bucket)
+  int n_sent, H, dh, d;        // n_sent: CTAs in x (sentences of this launch)
   int s_max;                   // longest sentence of the launch (sizes shared memory)
   float clip, sigma;
   int8_t* out_q;               // Q(ctx) [M x d]
@@ -96,6 +101,12 @@ struct FinishArgs {
   int eos;
   const int32_t* forced;    // teacher forcing ids (flat) or null
   const int64_t* forced_off;
+  // optional compact-order copies for the next step (written at each kept row's new index)
+  int32_t* prev_live;       // next input id
+  const int32_t* row_start; // [orig] source span
+  const int32_t* row_len;
+  int32_t* live_start;
+  int32_t* live_len;
 };
 
 cudaError_t launch_quantize(const float* x, int64_t n, float clip, int8_t* out, cudaStream_t st);
@@ -110,8 +121,10 @@ cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st);
 cudaError_t launch_attn_enc(const EncAttnArgs& a, cudaStream_t st);
 cudaError_t attn_init();   // dynamic-smem attribute (call once per device, outside capture)
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t st);
+// live[r] = r, keys = 0, ctrl = {B, 1}; live_start/live_len (optional) = row_start/row_len.
 cudaError_t launch_decode_init(int32_t* ctrl, int32_t* live, int B, unsigned long long* keys,
-                               cudaStream_t st);
+                               const int32_t* row_start, const int32_t* row_len,
+                               int32_t* live_start, int32_t* live_len, cudaStream_t st);
 cudaError_t launch_aan_step_rows(float* C, const float* y, int n, int d, int t, const AanOut& o,
                                  cudaStream_t st);
 cudaError_t launch_argmax_ids(const unsigned long long* keys, int n, int32_t* ids, cudaStream_t st);

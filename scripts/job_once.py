@@ -1,0 +1,19 @@
+"""One full translation job (after 2 warm-up jobs) inside an NVTX range "job", for an ncu
+launch list of exactly one job:  ncu --nvtx --nvtx-include "job/" ... python scripts/job_once.py"""
+import os, sys
+import numpy as np, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth
+from paper_1805_12096_b200 import mnmt as M
+dims = synth.PRESETS[os.environ.get("PRESET", "small-aan")]
+m = M.Model(dims, synth.make_weights(dims, 1))
+m.set_option("max_concurrent_rows", int(os.environ.get("MCR", 4096)))
+ss = synth.newstest_set(seed=2014)
+dev = torch.device("cuda:0"); st = torch.cuda.current_stream()
+ids = torch.from_numpy(ss.ids).to(dev)
+cap = int(ss.max_len.sum())
+out = torch.zeros(cap, dtype=torch.int32, device=dev); ln = torch.zeros(ss.n, dtype=torch.int32, device=dev)
+f = lambda: m.translate_device(ids.data_ptr(), ss.offsets, ss.max_len, 8192, out.data_ptr(), cap, ln.data_ptr(), st)
+f(); f(); torch.cuda.synchronize()
+torch.cuda.nvtx.range_push("job"); f(); torch.cuda.nvtx.range_pop(); torch.cuda.synchronize()
+s = m.stats(); print("launches", s["gpu_launches"], "steps", s["decode_steps"], "words", int(ln.sum()))

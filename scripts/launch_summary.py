@@ -16,9 +16,10 @@ def summarise(path):
     h = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     hdr = rows[h]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    mi = hdr.index("Metric Name")
     tot, cnt = collections.Counter(), collections.Counter()
     for r in rows[h + 1:]:
-        if len(r) <= vi:
+        if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
             continue
         name = re.sub(r"\(.*", "", r[ki]).strip()
         us = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1.0)

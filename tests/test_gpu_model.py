@@ -160,7 +160,7 @@ def test_batch_and_order_invariance():
     base = gm.translate(ss, 1 << 20)
     for budget in (1, 64, 333, 4096):
         assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, budget), base))
-    for fuse in (0, 1):                    # LayerNorm fused into GEMM epilogues or not
+    for fuse in (0, 1, 2):                 # LayerNorm unfused, fused per CTA, fused per cluster
         gm.set_option("fuse_ln", fuse)
         assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, 333), base))
     for lanes in (1, 2, 3):                # concurrent decoder lanes: identical ids
