@@ -1155,7 +1155,8 @@ static void plan_rows(Job& job, const int64_t* src_off, const int32_t* max_len, 
     // rows in (length, row) order, cut into length buckets for the encoder attention
     for (int r = 0; r < B; ++r) ord[r] = r;
     std::stable_sort(ord, ord + B, [&](int32_t x, int32_t y) { return rl[x] < rl[y]; });
-    static const int kEdges[] = {8, 16, 32, 64, 96, 128, 160, MNMT_MAX_SPAN};
+    // (one launch per bucket: shared memory and warps per CTA follow the bucket's longest)
+    static const int kEdges[] = {32, 64, 128, MNMT_MAX_SPAN};
     b.enc_buckets.clear();
     for (int i = 0, e = 0; i < B;) {
       while (rl[ord[i]] > kEdges[e]) ++e;

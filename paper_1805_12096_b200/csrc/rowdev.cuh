@@ -270,10 +270,10 @@ __device__ __forceinline__ void warp_attend_staged(const float* __restrict__ q, 
       if (i < d4) {
         const double2 q01 = *reinterpret_cast<const double2*>(qd + 4 * i);   // broadcast
         const double2 q23 = *reinterpret_cast<const double2*>(qd + 4 * i + 2);
-        dot = __dadd_rn(dot, __dmul_rn(q01.x, (double)kv[i].x));
-        dot = __dadd_rn(dot, __dmul_rn(q01.y, (double)kv[i].y));
-        dot = __dadd_rn(dot, __dmul_rn(q23.x, (double)kv[i].z));
-        dot = __dadd_rn(dot, __dmul_rn(q23.y, (double)kv[i].w));
+        dot = __fma_rn(q01.x, (double)kv[i].x, dot);   // fused product-accumulate (R24)
+        dot = __fma_rn(q01.y, (double)kv[i].y, dot);
+        dot = __fma_rn(q23.x, (double)kv[i].z, dot);
+        dot = __fma_rn(q23.y, (double)kv[i].w, dot);
       }
     const double s = __dmul_rn(dot, inv_sqrt);
     sc[j] = s;
@@ -298,11 +298,11 @@ __device__ __forceinline__ void warp_attend_staged(const float* __restrict__ q, 
     const int cnt = min(32, len - j0);
     if (lane < dh) {
       for (int jj = 0; jj < cnt; ++jj)
-        acc0 = __dadd_rn(acc0, __dmul_rn(sc[j0 + jj], (double)vt[jj * vld + lane]));
+        acc0 = __fma_rn(sc[j0 + jj], (double)vt[jj * vld + lane], acc0);
     }
     if (D4MAX > 8 && lane + 32 < dh) {
       for (int jj = 0; jj < cnt; ++jj)
-        acc1 = __dadd_rn(acc1, __dmul_rn(sc[j0 + jj], (double)vt[jj * vld + lane + 32]));
+        acc1 = __fma_rn(sc[j0 + jj], (double)vt[jj * vld + lane + 32], acc1);
     }
   }
 #pragma unroll

@@ -195,38 +195,47 @@ __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn_enc(EncAttnArgs a) {
   }
 }
 
-// Encoder self-attention, lane = query row (A3): one CTA per (sentence, head) with
-// ceil(S_max / 32) warps.  K and V head slices are staged once as fp64 in shared memory and read
-// as warp-wide broadcasts (one wavefront feeds 32 lanes x 2 FMAs); each lane keeps its query in
-// registers (32-column chunks); scores live in shared memory [S][nq] (column = query lane).
-// The arithmetic and its order are the plain definition (R20): dot over c in order, scale,
-// max, p_j = exp(s_j - max), Z = sum_j p_j in order, ctx_c = (sum_j p_j v_jc in order) / Z.
-// NCH = 32-column chunks of dh (1: dh <= 32, 2: dh <= 64).
-__host__ __device__ inline int enc_q_max(int dh) { return dh <= 32 ? 128 : 96; }
-__host__ __device__ inline size_t enc_q_smem(int dh, int s_max) {
-  const int nq = (s_max + 31) / 32 * 32;
-  return (size_t)(2 * dh + nq) * s_max * sizeof(double);
+// Encoder self-attention, lane = query row (A3), dh <= 32: one CTA per (sentence, head) with
+// ceil(len / 32) warps.  K and V head slices are staged once as fp64 in shared memory and read as
+// warp-wide broadcasts (one wavefront feeds 32 lanes x 2 FMAs); each lane keeps its query in
+// registers.  No score matrix is stored: pass A forms each row's max, pass B recomputes every
+// dot (same order, same value) and accumulates p, Z and the context in one sweep.  The
+// arithmetic and its order are the plain definition (R20): dot over c in order, scale, max,
+// p_j = exp(s_j - max), Z = sum_j p_j in order, ctx_c = (sum_j p_j v_jc in order) / Z, with
+// the product-accumulate steps fused (fp64 FMA, R24).
+constexpr int ENC_R_MAX = 128;   // longest sentence this kernel stages (4 warps)
+__host__ __device__ inline size_t enc_r_smem(int s_max) { return (size_t)2 * 32 * s_max * sizeof(double); }
+
+__device__ __forceinline__ double dot32(const double (&q)[32], const double* kr, int dh) {
+  double dot = 0.0;
+#pragma unroll
+  for (int c = 0; c < 32; c += 2) {
+    if (c < dh) {
+      const double2 k2 = *reinterpret_cast<const double2*>(kr + c);   // broadcast
+      dot = __fma_rn(q[c], k2.x, dot);
+      dot = __fma_rn(q[c + 1], k2.y, dot);
+    }
+  }
+  return dot;
 }
 
-template <int NCH>
-__global__ void __launch_bounds__(128) k_attn_enc_q(EncAttnArgs a) {
+__global__ void __launch_bounds__(ENC_R_MAX) k_attn_enc_r(EncAttnArgs a) {
   extern __shared__ __align__(16) double es[];
-  const int nq = blockDim.x, S = a.s_max, dh = a.dh, d = a.d, ld3 = 3 * d;
-  double* Ks = es;                 // [S][dh]
-  double* Vs = Ks + S * dh;        // [S][dh]
-  double* sc = Vs + S * dh;        // [S][nq]
+  const int S = a.s_max, dh = a.dh, d = a.d, ld3 = 3 * d;
+  double* Ks = es;                 // [S][32]
+  double* Vs = Ks + S * 32;        // [S][32]
   pdl_wait();
   pdl_trigger_early();
   const int s = a.sent_order ? a.sent_order[blockIdx.x] : (int)blockIdx.x, h = blockIdx.y;
   const int start = a.sent_start[s], len = a.sent_len[s];
   const float* base = a.qkv + (int64_t)start * ld3 + h * dh;
   const int d4 = dh >> 2;
-  for (int idx = threadIdx.x; idx < len * d4; idx += nq) {
+  for (int idx = threadIdx.x; idx < len * d4; idx += blockDim.x) {
     const int j = idx / d4, c4 = idx - j * d4;
     const float4 k4 = *reinterpret_cast<const float4*>(base + (int64_t)j * ld3 + d + 4 * c4);
     const float4 v4 = *reinterpret_cast<const float4*>(base + (int64_t)j * ld3 + 2 * d + 4 * c4);
-    double* kd = Ks + j * dh + 4 * c4;
-    double* vd = Vs + j * dh + 4 * c4;
+    double* kd = Ks + j * 32 + 4 * c4;
+    double* vd = Vs + j * 32 + 4 * c4;
     kd[0] = k4.x; kd[1] = k4.y; kd[2] = k4.z; kd[3] = k4.w;
     vd[0] = v4.x; vd[1] = v4.y; vd[2] = v4.z; vd[3] = v4.w;
   }
@@ -234,75 +243,45 @@ __global__ void __launch_bounds__(128) k_attn_enc_q(EncAttnArgs a) {
   const int i = threadIdx.x;
   if (i >= len) return;            // no further block-wide barriers
   const float* qrow = base + (int64_t)i * ld3;
-  // ---- scores: dot over c in order, in 32-column chunks (partial dots parked in sc)
+  double q[32];
 #pragma unroll
-  for (int ch = 0; ch < NCH; ++ch) {
-    double qr[32];
-#pragma unroll
-    for (int c = 0; c < 32; c += 4) {
-      const int cc = ch * 32 + c;
-      float4 q4 = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (cc < dh) q4 = *reinterpret_cast<const float4*>(qrow + cc);
-      qr[c] = q4.x; qr[c + 1] = q4.y; qr[c + 2] = q4.z; qr[c + 3] = q4.w;
-    }
-#pragma unroll 4
-    for (int j = 0; j < len; ++j) {
-      double dot = ch ? sc[j * nq + i] : 0.0;
-      const double* kr = Ks + j * dh + ch * 32;
-#pragma unroll
-      for (int c = 0; c < 32; c += 2) {
-        if (ch * 32 + c < dh) {
-          const double2 k2 = *reinterpret_cast<const double2*>(kr + c);   // broadcast
-          dot = __dadd_rn(dot, __dmul_rn(qr[c], k2.x));
-          dot = __dadd_rn(dot, __dmul_rn(qr[c + 1], k2.y));
-        }
-      }
-      sc[j * nq + i] = dot;
-    }
+  for (int c = 0; c < 32; c += 4) {
+    float4 q4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (c < dh) q4 = *reinterpret_cast<const float4*>(qrow + c);
+    q[c] = q4.x; q[c + 1] = q4.y; q[c + 2] = q4.z; q[c + 3] = q4.w;
   }
-  // ---- softmax over the sentence (sequential in j)
   const double inv_sqrt = 1.0 / sqrt((double)dh);
+  // ---- pass A: row max of the scaled scores
   double mx = -INFINITY;
+#pragma unroll 4
+  for (int j = 0; j < len; ++j) mx = fmax(mx, __dmul_rn(dot32(q, Ks + j * 32, dh), inv_sqrt));
+  // ---- pass B: p_j, Z and the context, in order of j
+  double z = 0.0, acc[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) acc[c] = 0.0;
+#pragma unroll 2
   for (int j = 0; j < len; ++j) {
-    const double sj = __dmul_rn(sc[j * nq + i], inv_sqrt);
-    sc[j * nq + i] = sj;
-    mx = fmax(mx, sj);
-  }
-  double z = 0.0;
-  for (int j = 0; j < len; ++j) {
-    const double p = exp(__dsub_rn(sc[j * nq + i], mx));
-    sc[j * nq + i] = p;
+    const double p = exp(__dsub_rn(__dmul_rn(dot32(q, Ks + j * 32, dh), inv_sqrt), mx));
     z = __dadd_rn(z, p);
+    const double* vr = Vs + j * 32;
+#pragma unroll
+    for (int c = 0; c < 32; c += 2) {
+      if (c < dh) {
+        const double2 v2 = *reinterpret_cast<const double2*>(vr + c);   // broadcast
+        acc[c] = __fma_rn(p, v2.x, acc[c]);
+        acc[c + 1] = __fma_rn(p, v2.y, acc[c + 1]);
+      }
+    }
   }
-  // ---- context, 32 columns at a time: acc_c = sum_j p_j v_jc in order; ctx = acc / Z
   int8_t* orow = a.out_q + (int64_t)(start + i) * d + h * dh;
 #pragma unroll
-  for (int ch = 0; ch < NCH; ++ch) {
-    double acc[32];
+  for (int c = 0; c < 32; c += 4) {
+    if (c < dh) {
+      uint32_t w = 0;
 #pragma unroll
-    for (int c = 0; c < 32; ++c) acc[c] = 0.0;
-    for (int j = 0; j < len; ++j) {
-      const double p = sc[j * nq + i];
-      const double* vr = Vs + j * dh + ch * 32;
-#pragma unroll
-      for (int c = 0; c < 32; c += 2) {
-        if (ch * 32 + c < dh) {
-          const double2 v2 = *reinterpret_cast<const double2*>(vr + c);   // broadcast
-          acc[c] = __dadd_rn(acc[c], __dmul_rn(p, v2.x));
-          acc[c + 1] = __dadd_rn(acc[c + 1], __dmul_rn(p, v2.y));
-        }
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < 32; c += 4) {
-      const int cc = ch * 32 + c;
-      if (cc < dh) {
-        uint32_t w = 0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          w |= (uint32_t)(q8((float)__ddiv_rn(acc[c + u], z), a.clip, a.sigma) & 0xff) << (8 * u);
-        *reinterpret_cast<uint32_t*>(orow + cc) = w;
-      }
+      for (int u = 0; u < 4; ++u)
+        w |= (uint32_t)(q8((float)__ddiv_rn(acc[c + u], z), a.clip, a.sigma) & 0xff) << (8 * u);
+      *reinterpret_cast<uint32_t*>(orow + c) = w;
     }
   }
 }
@@ -418,11 +397,8 @@ cudaError_t attn_init() {   // once per device
   e = cudaFuncSetAttribute(k_attn_enc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)enc_attn_smem(64, MNMT_MAX_KV, ATTN_WARPS));
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_attn_enc_q<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)enc_q_smem(32, enc_q_max(32)));
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_attn_enc_q<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)enc_q_smem(64, enc_q_max(64)));
+    e = cudaFuncSetAttribute(k_attn_enc_r, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)enc_r_smem(ENC_R_MAX));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              ATTN_WARPS * (int)attn_staged_warp_bytes(MNMT_MAX_KV, 32));
@@ -454,11 +430,9 @@ cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
 cudaError_t launch_attn_enc(const EncAttnArgs& a, cudaStream_t st) {
   if (a.n_sent <= 0) return cudaSuccess;
   if (a.s_max < 1 || a.s_max > MNMT_MAX_KV) return cudaErrorInvalidValue;
-  if (a.s_max <= enc_q_max(a.dh) && a.dh <= 64 && (a.dh & 3) == 0) {
+  if (a.dh <= 32 && (a.dh & 3) == 0 && a.s_max <= ENC_R_MAX) {
     const dim3 grid(a.n_sent, a.H), block((a.s_max + 31) / 32 * 32);
-    const size_t smem = enc_q_smem(a.dh, a.s_max);
-    return a.dh <= 32 ? launch_pdl(k_attn_enc_q<1>, grid, block, smem, st, a)
-                      : launch_pdl(k_attn_enc_q<2>, grid, block, smem, st, a);
+    return launch_pdl(k_attn_enc_r, grid, block, enc_r_smem(a.s_max), st, a);
   }
   const int nw = enc_attn_warps(a.s_max);
   return launch_pdl(k_attn_enc, dim3(a.n_sent, a.H), dim3(nw * 32), enc_attn_smem(a.dh, a.s_max, nw),
