@@ -335,9 +335,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--megakernel", type=int, default=0,
                     help="1: persistent step kernel per batch; 0: one kernel per op (CUDA graph)")
-    ap.add_argument("--lanes", type=int, default=1,
+    ap.add_argument("--lanes", type=int, default=3,
                     help="independent decoder lanes (streams) per GPU (scheduling only)")
-    ap.add_argument("--lane-tiers", type=int, default=0,
+    ap.add_argument("--lane-tiers", type=int, default=30,
                     help="0: deal sentences round-robin to lanes; 10*p: contiguous length tiers "
                          "of equal sum S^p (scheduling only)")
     ap.add_argument("--steps-per-graph", type=int, default=1,

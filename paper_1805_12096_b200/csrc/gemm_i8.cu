@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     constexpr int HALF = BN / 2;
     mbar_wait(&tmem_full_bar, 0);
     tc_fence_after();
-    if (warp == 2 && lane == 0) pdl_launch_dependents();
+    if (warp == 2 && lane == 0) pdl_launch_dependents();   // (measured: earlier is slower)
     const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + half * HALF;
     float* stage = reinterpret_cast<float*>(smem + stages * Cfg::STAGE_BYTES) +
                    (warp - 2) * EPI_STAGE_FLOATS;

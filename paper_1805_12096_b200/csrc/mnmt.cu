@@ -157,6 +157,7 @@ struct mnmt_model {
   int fuse_ln = 0;                     // option: LayerNorm fused into full-row GEMM epilogues
   int rowlocal = 0;                    // option: row-local phases in the persistent step kernel (measured slower)
   int steps_per_graph = 1;             // option: decoder steps captured per CUDA graph
+  int mk_ctas = 0;                     // option: persistent step kernel grid cap (0 = one per SM)
   int lane_tiers = 0;                  // option: 0 = deal sentences round-robin to lanes;
                                        // p*10 = contiguous length tiers of equal sum S^p
 };
@@ -323,10 +324,15 @@ static void jb_free(mnmt_model* m) {
   m->jb = JobBuf();
 }
 
-static mnmt_status lane_init(mnmt_model* m, Lane& L) {
+// Lane li's streams get priority li steps above the lowest (clamped): with length tiers the
+// last lane holds the longest sentences, i.e. the job's critical path.
+static mnmt_status lane_init(mnmt_model* m, Lane& L, int li) {
   if (L.st) return MNMT_OK;
-  if (cudaStreamCreateWithFlags(&L.st, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&L.side, cudaStreamNonBlocking) != cudaSuccess ||
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  const int prio = std::max(greatest, least - li);
+  if (cudaStreamCreateWithPriority(&L.st, cudaStreamNonBlocking, prio) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&L.side, cudaStreamNonBlocking, prio) != cudaSuccess ||
       cudaEventCreateWithFlags(&L.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&L.ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&L.ev, cudaEventDisableTiming) != cudaSuccess) {
@@ -621,6 +627,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
       // A6: AAN block. g (or its codes) was produced with this layer's input.
       const float* a_f = w.g;
       // The i-gate GEMM needs only Q(y): it runs on a forked branch beside the AAN FFN.
+      // (measured: in-line is slower; the branch runs beside the AAN FFN)
       const bool fork = c.aan_gate && c.aan_ffn_depth > 0 && !hook;
       if (fork) {
         if ((e = cudaEventRecord(Ln.ev_fork, st)) != cudaSuccess) return e;
@@ -1255,12 +1262,12 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
       }
       if (!hook) {
         sa.max_steps = b.T;
-        CK(launch_step_kernel(sa, (int)d, st));
+        CK(launch_step_kernel(sa, (int)d, st, m->mk_ctas));
         launches += 1;
       } else {
         sa.max_steps = 1;
         for (int t = 0; t < b.T; ++t) {
-          CK(launch_step_kernel(sa, (int)d, st));
+          CK(launch_step_kernel(sa, (int)d, st, m->mk_ctas));
           launches += 1;
         }
       }
@@ -1315,7 +1322,7 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
 static mnmt_status ensure_lanes(mnmt_model* m, const Job& job, int64_t forced_O) {
   for (size_t li = 0; li < job.lane_M.size(); ++li) {
     if (job.lane_B[li] == 0) continue;
-    CKS(lane_init(m, m->lanes[li]));
+    CKS(lane_init(m, m->lanes[li], (int)li));
     CKS(lane_ensure(m, m->lanes[li], job.lane_M[li], job.lane_B[li], job.lane_T[li], forced_O));
   }
   return MNMT_OK;
@@ -1406,7 +1413,7 @@ mnmt_status mnmt_model_create(const mnmt_config* cfg, int32_t cuda_device, mnmt_
       cudaEventCreateWithFlags(&m->ev_in, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&m->ev_out, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&m->ev_job, cudaEventDisableTiming) != cudaSuccess ||
-      lane_init(m, m->lanes[0]) != MNMT_OK) {
+      lane_init(m, m->lanes[0], 0) != MNMT_OK) {
     set_err("stream/event creation failed");
     delete m;
     return MNMT_ERR_CUDA;
@@ -1841,6 +1848,11 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
       for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
       L.graphs.clear();
     }
+    return MNMT_OK;
+  }
+  if (std::string(name) == "mk_ctas") {
+    if (value < 0 || value > 4096) { set_err("mk_ctas must be in [0, 4096]"); return MNMT_ERR_ARG; }
+    m->mk_ctas = (int)value;
     return MNMT_OK;
   }
   if (std::string(name) == "lane_tiers") {

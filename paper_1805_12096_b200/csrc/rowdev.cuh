@@ -187,10 +187,10 @@ __device__ __forceinline__ void warp_attend(const float* __restrict__ q, const K
         kk[0] = a.x; kk[1] = a.y; kk[2] = b.x; kk[3] = b.y;
         qq[0] = qd[c]; qq[1] = qd[c + 1]; qq[2] = qd[c + 2]; qq[3] = qd[c + 3];
       }
-      dot = __dadd_rn(dot, __dmul_rn(qq[0], kk[0]));
-      dot = __dadd_rn(dot, __dmul_rn(qq[1], kk[1]));
-      dot = __dadd_rn(dot, __dmul_rn(qq[2], kk[2]));
-      dot = __dadd_rn(dot, __dmul_rn(qq[3], kk[3]));
+      dot = __fma_rn(qq[0], kk[0], dot);   // fused product-accumulate (R24)
+      dot = __fma_rn(qq[1], kk[1], dot);
+      dot = __fma_rn(qq[2], kk[2], dot);
+      dot = __fma_rn(qq[3], kk[3], dot);
     }
     const double s = __dmul_rn(dot, inv_sqrt);
     sc[j] = s;
@@ -211,12 +211,12 @@ __device__ __forceinline__ void warp_attend(const float* __restrict__ q, const K
     for (; j + 4 <= len; j += 4) {
       const double v0 = to_f64(v[(int64_t)(j + 0) * ld + c]), v1 = to_f64(v[(int64_t)(j + 1) * ld + c]);
       const double v2 = to_f64(v[(int64_t)(j + 2) * ld + c]), v3 = to_f64(v[(int64_t)(j + 3) * ld + c]);
-      acc = __dadd_rn(acc, __dmul_rn(sc[j + 0], v0));
-      acc = __dadd_rn(acc, __dmul_rn(sc[j + 1], v1));
-      acc = __dadd_rn(acc, __dmul_rn(sc[j + 2], v2));
-      acc = __dadd_rn(acc, __dmul_rn(sc[j + 3], v3));
+      acc = __fma_rn(sc[j + 0], v0, acc);
+      acc = __fma_rn(sc[j + 1], v1, acc);
+      acc = __fma_rn(sc[j + 2], v2, acc);
+      acc = __fma_rn(sc[j + 3], v3, acc);
     }
-    for (; j < len; ++j) acc = __dadd_rn(acc, __dmul_rn(sc[j], to_f64(v[(int64_t)j * ld + c])));
+    for (; j < len; ++j) acc = __fma_rn(sc[j], to_f64(v[(int64_t)j * ld + c]), acc);
     const float ctx = len > 0 ? (float)__ddiv_rn(acc, z) : 0.0f;
     out_q[c] = (int8_t)q8(ctx, clip, sigma);
     if (out_f) out_f[c] = ctx;
@@ -224,112 +224,12 @@ __device__ __forceinline__ void warp_attend(const float* __restrict__ q, const K
   __syncwarp();
 }
 
-// ------------------------------------------------------------------ staged attention
-// warp_attend_staged: the same arithmetic, in the same order, as warp_attend<float>, with one
-// memory round trip per 32 positions instead of one per K column group and per 4 V rows:
-// lane j issues all loads of its K row at once (predicated, fully unrolled) and copies its V row
-// into the warp's shared tile vt with cp.async in the same round trip; the context sum then reads
-// V from shared memory.  D4MAX = max dh / 4 (8: dh <= 32, 16: dh <= 64).
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-constexpr int VT_PAD = 4;   // vt row stride dh + 4 floats: conflict-free row writes and column reads
-
-template <int D4MAX>
-__device__ __forceinline__ void warp_attend_staged(const float* __restrict__ q, const float* K,
-                                                   const float* V, int64_t ld, int len, int dh,
-                                                   double* sc, double* qd, float* vt, float clip,
-                                                   float sigma, int8_t* out_q, float* out_f) {
-  const int lane = threadIdx.x & 31;
-  const int d4 = dh >> 2, vld = dh + VT_PAD;
-  auto stage_v = [&](int j0) {
-    const int j = j0 + lane;
-    if (j < len) {
-      const float* vr = V + (int64_t)j * ld;
-#pragma unroll
-      for (int i = 0; i < D4MAX; ++i)
-        if (i < d4) cp_async16(vt + lane * vld + 4 * i, vr + 4 * i);
-    }
-  };
-  stage_v(0);
-  for (int c = lane; c < dh; c += 32) qd[c] = (double)q[c];   // the query, converted once
-  __syncwarp();
-  const double inv_sqrt = 1.0 / sqrt((double)dh);
-  double mx = -INFINITY;
-  for (int j = lane; j < len; j += 32) {
-    const float* kr = K + (int64_t)j * ld;
-    float4 kv[D4MAX];
-#pragma unroll
-    for (int i = 0; i < D4MAX; ++i)
-      if (i < d4) kv[i] = *reinterpret_cast<const float4*>(kr + 4 * i);
-    double dot = 0.0;
-#pragma unroll
-    for (int i = 0; i < D4MAX; ++i)
-      if (i < d4) {
-        const double2 q01 = *reinterpret_cast<const double2*>(qd + 4 * i);   // broadcast
-        const double2 q23 = *reinterpret_cast<const double2*>(qd + 4 * i + 2);
-        dot = __fma_rn(q01.x, (double)kv[i].x, dot);   // fused product-accumulate (R24)
-        dot = __fma_rn(q01.y, (double)kv[i].y, dot);
-        dot = __fma_rn(q23.x, (double)kv[i].z, dot);
-        dot = __fma_rn(q23.y, (double)kv[i].w, dot);
-      }
-    const double s = __dmul_rn(dot, inv_sqrt);
-    sc[j] = s;
-    mx = fmax(mx, s);
-  }
-  mx = warp_max_f64(mx);
-  double z = 0.0;
-  for (int j = lane; j < len; j += 32) {
-    const double p = exp(__dsub_rn(sc[j], mx));
-    sc[j] = p;
-    z = __dadd_rn(z, p);
-  }
-  z = warp_sum_f64(z);
-  double acc0 = 0.0, acc1 = 0.0;   // columns lane and lane + 32
-  for (int j0 = 0; j0 < len; j0 += 32) {
-    if (j0 > 0) {
-      __syncwarp();                  // everyone is done reading the previous chunk
-      stage_v(j0);
-    }
-    cp_async_wait_all();
-    __syncwarp();                    // (also orders the sc[] writes above)
-    const int cnt = min(32, len - j0);
-    if (lane < dh) {
-      for (int jj = 0; jj < cnt; ++jj)
-        acc0 = __fma_rn(sc[j0 + jj], (double)vt[jj * vld + lane], acc0);
-    }
-    if (D4MAX > 8 && lane + 32 < dh) {
-      for (int jj = 0; jj < cnt; ++jj)
-        acc1 = __fma_rn(sc[j0 + jj], (double)vt[jj * vld + lane + 32], acc1);
-    }
-  }
-#pragma unroll
-  for (int hh = 0; hh < 2; ++hh) {
-    const int c = lane + 32 * hh;
-    if (c < dh) {
-      const float ctx = len > 0 ? (float)__ddiv_rn(hh ? acc1 : acc0, z) : 0.0f;
-      out_q[c] = (int8_t)q8(ctx, clip, sigma);
-      if (out_f) out_f[c] = ctx;
-    }
-  }
-  __syncwarp();
-}
-
-// Per-warp scratch of the staged attention: span doubles (scores), 64 doubles (query), then a
-// 32 x (dh + 4) float V tile (16-byte aligned).
-__host__ __device__ inline size_t attn_staged_warp_bytes(int span, int dh) {
-  return (size_t)((span + 1) & ~1) * 8 + 64 * 8 + (size_t)32 * (dh + VT_PAD) * 4;
-}
-
-// One (row, head) in SRC / SELF / ENC mode with the staged body.
-// pre_start / pre_len: the row's source span when a.live_start is set (loaded by the caller
-// together with the live-row count).
-template <int D4MAX>
-__device__ __forceinline__ void attn_row_head_staged(const AttnArgs& a, int r, int h, double* sc,
-                                                     double* qd, float* vt, int pre_start,
-                                                     int pre_len) {
+// Attention of one (row, head) by one warp (SRC, SELF and ENC modes); sc = per-warp scratch
+// of span + 64 doubles (scores, then the converted query).
+// pre_start / pre_len: the row's source span when a.live_start is set (src mode; loaded by the
+// caller together with the live-row count).
+__device__ __forceinline__ void attn_row_head(const AttnArgs a, int r, int h, double* sc, int span,
+                                              int pre_start = 0, int pre_len = 0) {
   const int lane = threadIdx.x & 31;
   const int dh = a.dh;
   int start, len;
@@ -346,40 +246,6 @@ __device__ __forceinline__ void attn_row_head_staged(const AttnArgs& a, int r, i
       start = a.kv_start[orig];
       len = a.kv_len[orig];
     }
-  } else {  // ATTN_SELF: append this step's k, v (head slice), attend over positions 1..t
-    const int orig = a.live[r];
-    const int t = a.ctrl[1];
-    start = orig * a.t_cap;
-    len = t;
-    float* dst = a.kv_w + (int64_t)(start + t - 1) * a.ldkv + h * dh;
-    for (int c = lane; c < dh; c += 32) {
-      dst[a.k_off + c] = q[a.d + c];        // k at qkv columns [d, 2d)
-      dst[a.v_off + c] = q[2 * a.d + c];    // v at qkv columns [2d, 3d)
-    }
-    __threadfence();   // the appended row is read back through L2 (cp.async.cg) by other lanes
-    __syncwarp();
-  }
-  const float* K = a.kv + (int64_t)start * a.ldkv + a.k_off + h * dh;
-  const float* V = a.kv + (int64_t)start * a.ldkv + a.v_off + h * dh;
-  warp_attend_staged<D4MAX>(q, K, V, a.ldkv, len, dh, sc, qd, vt, a.clip, a.sigma,
-                            a.out_q + (int64_t)r * a.d + h * dh,
-                            a.out_f ? a.out_f + (int64_t)r * a.d + h * dh : nullptr);
-}
-
-// Attention of one (row, head) by one warp (SRC, SELF and ENC modes); sc = per-warp scratch
-// of span + 64 doubles (scores, then the converted query).
-__device__ __forceinline__ void attn_row_head(const AttnArgs a, int r, int h, double* sc, int span) {
-  const int lane = threadIdx.x & 31;
-  const int dh = a.dh;
-  int start, len;
-  const float* q = a.q + (int64_t)r * a.ldq + h * dh;
-  if (a.mode == ATTN_ENC) {
-    start = a.kv_start[r];
-    len = a.kv_len[r];
-  } else if (a.mode == ATTN_SRC) {
-    const int orig = a.live[r];
-    start = a.kv_start[orig];
-    len = a.kv_len[orig];
   } else {  // ATTN_SELF: append this step's k, v (head slice), attend over positions 1..t
     const int orig = a.live[r];
     const int t = a.ctrl[1];

@@ -7,7 +7,9 @@
 //   k_embed_src    x = E[id]*sqrt(d) + PE[pos], Q(x)              (A2)
 //   k_embed_tgt    decoder input + first AAN step                 (A5, A6)
 //   k_ln           residual/gate combine + LayerNorm + Q + next-layer AAN step (A6-A8)
-//   k_attn         attention, one warp per (row, head), fp64      (A3, A6', A7)
+//   k_attn         decoder attention, one warp per (row, head), fp64 (A6', A7; op-level A3)
+//   k_attn_enc_r   encoder self-attention, lane per query row, dh <= 32, <= 128 positions (A3)
+//   k_attn_enc     encoder self-attention, warp per query row (other shapes)          (A3)
 //   k_finish       argmax decode + EOS/max_len + stable live-row compaction (A9, A10)
 #include <cstdio>
 #include <cstdlib>
@@ -110,11 +112,11 @@ __global__ void k_ln(LnArgs a) {
 
 constexpr int ATTN_WARPS = 8;
 
-// Decoder (SRC, SELF) and op-level (ENC) attention: one warp per (row, head), staged body.
-// Dynamic smem: ATTN_WARPS x attn_staged_warp_bytes(span, dh).
-template <int D4MAX>
+// Decoder (SRC, SELF) and op-level (ENC) attention: one warp per (row, head) (warp_attend).
+// Dynamic smem: ATTN_WARPS x (span + 64) doubles.  (A variant that staged 32-position V tiles
+// with cp.async measured no faster in the decode: its V tile halved the resident CTAs.)
 __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn(AttnArgs a) {
-  extern __shared__ __align__(16) uint8_t attn_smem[];
+  extern __shared__ double sc_dyn[];
   pdl_wait();
   pdl_trigger_early();
   const int wi = threadIdx.x >> 5;
@@ -125,11 +127,7 @@ __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn(AttnArgs a) {
   const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
   const int pst = a.live_start ? a.live_start[r] : 0, pln = a.live_start ? a.live_len[r] : 0;
   if (r >= n_live) return;
-  uint8_t* mine = attn_smem + (size_t)wi * attn_staged_warp_bytes(a.span, a.dh);
-  double* sc = reinterpret_cast<double*>(mine);
-  double* qd = sc + ((a.span + 1) & ~1);
-  float* vt = reinterpret_cast<float*>(qd + 64);
-  attn_row_head_staged<D4MAX>(a, r, h, sc, qd, vt, pst, pln);
+  attn_row_head(a, r, h, sc_dyn + (size_t)wi * (a.span + 64), a.span, pst, pln);
 }
 
 constexpr int FIN_THREADS = 1024;
@@ -379,7 +377,7 @@ static cudaError_t set_carveouts() {
                        (const void*)k_embed_tgt<1>, (const void*)k_embed_tgt<2>,
                        (const void*)k_embed_tgt<4>, (const void*)k_embed_tgt<8>,
                        (const void*)k_ln<1>, (const void*)k_ln<2>, (const void*)k_ln<4>, (const void*)k_ln<8>,
-                       (const void*)k_attn<8>, (const void*)k_attn<16>, (const void*)k_attn_enc, (const void*)k_finish,
+                       (const void*)k_attn, (const void*)k_attn_enc, (const void*)k_finish,
                        (const void*)k_decode_init};
   for (const void* f : fns) {
     cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -400,11 +398,8 @@ cudaError_t attn_init() {   // once per device
     e = cudaFuncSetAttribute(k_attn_enc_r, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)enc_r_smem(ENC_R_MAX));
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_attn<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             ATTN_WARPS * (int)attn_staged_warp_bytes(MNMT_MAX_KV, 32));
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_attn<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             ATTN_WARPS * (int)attn_staged_warp_bytes(MNMT_MAX_KV, 64));
+    e = cudaFuncSetAttribute(k_attn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             ATTN_WARPS * (MNMT_MAX_KV + 64) * (int)sizeof(double));
   if (e == cudaSuccess) e = set_carveouts();
   if (e == cudaSuccess) {
     const char* pe = getenv("MNMT_PDL_EARLY");
@@ -422,9 +417,7 @@ cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
   if (b.span <= 0 || b.span > MNMT_MAX_KV) b.span = MNMT_MAX_KV;
   if (b.dh > 64 || (b.dh & 3)) return cudaErrorInvalidValue;
   const dim3 grid((unsigned)((warps + ATTN_WARPS - 1) / ATTN_WARPS)), block(ATTN_WARPS * 32);
-  const size_t smem = (size_t)ATTN_WARPS * attn_staged_warp_bytes(b.span, b.dh);
-  return b.dh <= 32 ? launch_pdl(k_attn<8>, grid, block, smem, st, b)
-                    : launch_pdl(k_attn<16>, grid, block, smem, st, b);
+  return launch_pdl(k_attn, grid, block, (size_t)ATTN_WARPS * (b.span + 64) * 8, st, b);
 }
 
 cudaError_t launch_attn_enc(const EncAttnArgs& a, cudaStream_t st) {

@@ -459,9 +459,10 @@ int step_kernel_grid() {
   return grid[dev];
 }
 
-cudaError_t launch_step_kernel(const StepArgs& a, int d, cudaStream_t st) {
-  const int grid = step_kernel_grid();
+cudaError_t launch_step_kernel(const StepArgs& a, int d, cudaStream_t st, int grid_cap) {
+  int grid = step_kernel_grid();
   if (grid <= 0) return cudaErrorInvalidConfiguration;
+  if (grid_cap > 0 && grid_cap < grid) grid = grid_cap;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(SK_THREADS);

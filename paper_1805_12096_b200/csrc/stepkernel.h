@@ -48,7 +48,8 @@ struct StepArgs {
 };
 
 // Launch (cooperative, one CTA per SM) on `st`; d selects the row-kernel width.
-cudaError_t launch_step_kernel(const StepArgs& a, int d, cudaStream_t st);
+// grid_cap > 0 limits the grid (CTAs) below one per SM.
+cudaError_t launch_step_kernel(const StepArgs& a, int d, cudaStream_t st, int grid_cap = 0);
 // Sets the smem attribute once per device; returns the grid size (CTAs) or -1.
 int step_kernel_grid();
 

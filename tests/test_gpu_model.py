@@ -110,10 +110,14 @@ def test_tiny_free_running(dims):
     w, om, gm = pair(dims, 12)
     ss = synth.random_set(17, 1, 15, seed=5, vocab=dims.vocab)
     ref = om.decode_many(ss, 4)
-    for mk in (1, 0):          # persistent step kernel / one kernel per op (graph)
+    # persistent step kernel (grid-wide phases; row-local phases on a capped grid) and one
+    # kernel per op (graph)
+    for mk, rl, ctas in ((1, 0, 0), (1, 1, 8), (0, 0, 0)):
         gm.set_option("megakernel", mk)
+        gm.set_option("rowlocal", rl)
+        gm.set_option("mk_ctas", ctas)
         got = gm.decode(ss)
-        assert all(np.array_equal(a, b) for a, b in zip(got, ref)), mk
+        assert all(np.array_equal(a, b) for a, b in zip(got, ref)), (mk, rl, ctas)
 
 
 def test_config0_tiny192_aan():
@@ -168,6 +172,14 @@ def test_batch_and_order_invariance():
         for rows in (7, 50, 1 << 20):      # co-scheduled batch waves: identical ids
             gm.set_option("max_concurrent_rows", rows)
             assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, 64), base))
+        for tiers in (10, 30):             # length-tiered lanes (prioritised streams)
+            gm.set_option("lane_tiers", tiers)
+            assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, 64), base))
+        gm.set_option("lane_tiers", 0)
+    for k in (3, 8):                       # several decoder steps per CUDA graph
+        gm.set_option("steps_per_graph", k)
+        assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, 333), base))
+    gm.set_option("steps_per_graph", 1)
     gm.set_option("max_concurrent_rows", 0)
     gm.set_option("lanes", 1)
     perm = np.random.default_rng(3).permutation(ss.n)
