@@ -340,6 +340,8 @@ def main():
     ap.add_argument("--lane-tiers", type=int, default=30,
                     help="0: deal sentences round-robin to lanes; 10*p: contiguous length tiers "
                          "of equal sum S^p (scheduling only)")
+    ap.add_argument("--pers-reserve", type=int, default=16,
+                    help="SMs the persistent GEMMs of non-critical lanes leave free")
     ap.add_argument("--steps-per-graph", type=int, default=1,
                     help="decoder steps captured per CUDA graph (scheduling only)")
     ap.add_argument("--fuse-ln", type=int, default=0,
@@ -366,7 +368,7 @@ def main():
                     "l2": "flushed between timed steps (512 MiB write)",
                     "max_concurrent_rows": args.max_concurrent_rows, "lanes": args.lanes,
                     "fuse_ln": args.fuse_ln, "steps_per_graph": args.steps_per_graph,
-                    "lane_tiers": args.lane_tiers,
+                    "lane_tiers": args.lane_tiers, "pers_reserve": args.pers_reserve,
                     "step_engine": "persistent cooperative kernel" if args.megakernel else "kernel-per-op CUDA graph"}
 
     if args.impl == "reference":
@@ -393,6 +395,7 @@ def main():
     model.set_option("fuse_ln", args.fuse_ln)
     model.set_option("steps_per_graph", args.steps_per_graph)
     model.set_option("lane_tiers", args.lane_tiers)
+    model.set_option("pers_reserve", args.pers_reserve)
     sset = synth.newstest_set(seed=2014 + rank)          # weak scaling: one set per GPU
     stream = torch.cuda.current_stream()
     dev = torch.device("cuda", local)

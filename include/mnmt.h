@@ -162,6 +162,11 @@ mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids_host,
  *                          128-row tile (CTA barriers between them), 0 (default) = split over the
  *                          grid with grid barriers.
  *   "steps_per_graph"      1..63 consecutive decoder steps captured in one CUDA graph (default 1).
+ *   "lane_tiers"           0 (default): a wave's sentences are dealt round-robin to the lanes;
+ *                          10*p: contiguous length tiers of equal sum S_i^p, the last lane (the
+ *                          longest sentences, the job's critical path) on the highest-priority stream.
+ *   "pers_reserve"         SMs the persistent GEMMs of the other lanes leave free (default 0).
+ *   "mk_ctas"              grid cap of the persistent step kernel (0 = one CTA per SM).
  *   "profile_phases"       1 = the persistent kernel stamps every phase (mnmt_debug_phase_*).
  * Errors: MNMT_ERR_ARG (unknown name or negative value). */
 mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, int64_t value);

@@ -943,7 +943,9 @@ static cudaError_t launch_pers_t(const CUtensorMap& tmA, const CUtensorMap& tmB,
                                  cudaStream_t st) {
   const int tiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(tiles < num_sms() ? tiles : num_sms());
+  int cap = num_sms();
+  if (a.pers_grid > 0 && a.pers_grid < cap) cap = a.pers_grid;
+  cfg.gridDim = dim3(tiles < cap ? tiles : cap);
   cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = PersCfg<BN>::SMEM;
   cfg.stream = st;

@@ -36,6 +36,7 @@ struct GemmArgs {
   int col_block;               // scatter: out + (n / col_block) * block_stride + m * ldo + n % col_block
   int64_t block_stride;
   unsigned long long* keys;    // [rows] for EPI_ARGMAX
+  int pers_grid;               // persistent variant: CTA cap (0 = one per SM)
   LnArgs ln;                   // EPI_LN: residual / gate inputs, gamma, beta, outputs, AAN
 };
 

@@ -158,6 +158,8 @@ struct mnmt_model {
   int rowlocal = 0;                    // option: row-local phases in the persistent step kernel (measured slower)
   int steps_per_graph = 1;             // option: decoder steps captured per CUDA graph
   int mk_ctas = 0;                     // option: persistent step kernel grid cap (0 = one per SM)
+  int pers_reserve = 0;                // option: SMs the persistent GEMMs of non-critical lanes leave free
+  int cur_pers_grid = 0;               // (launch state) persistent-GEMM CTA cap of the lane being issued
   int lane_tiers = 0;                  // option: 0 = deal sentences round-robin to lanes;
                                        // p*10 = contiguous length tiers of equal sum S^p
 };
@@ -455,6 +457,7 @@ static cudaError_t gemm(mnmt_model* m, cudaStream_t st, const CUtensorMap& tmA, 
   a.col_block = col_block > 0 ? col_block : W.out;
   a.block_stride = block_stride;
   a.keys = keys;
+  a.pers_grid = m->cur_pers_grid;
   return launch_gemm_i8(tmA, W.tm, a, epi, 0, st);
 }
 
@@ -766,6 +769,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
     a.sigma = sigma_of(m);
     a.col_block = c.vocab;
     a.keys = w.keys;
+    a.pers_grid = m->cur_pers_grid;
     if ((e = launch_gemm_i8(w.tm_cy, m->tmE, a, EPI_ARGMAX, 0, st)) != cudaSuccess) return e;
   }
   // A10: finish + compaction
@@ -1218,6 +1222,14 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
     CK(cudaMemcpyAsync(w.len_idx, r32 + 3 * B, B * 4, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(w.out_off, r64, B * 8, cudaMemcpyDeviceToDevice, st));
     if (forced) CK(cudaMemcpyAsync(w.forced_off, r64 + B, B * 8, cudaMemcpyDeviceToDevice, st));
+    // tiered lanes: the last lane (longest sentences) is the critical path; the persistent
+    // GEMMs of the other lanes leave pers_reserve SMs free for it
+    {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->dev);
+      const bool critical = b.lane == m->n_lanes - 1 || m->n_lanes <= 1 || m->lane_tiers == 0;
+      m->cur_pers_grid = (!critical && m->pers_reserve > 0) ? std::max(1, sms - m->pers_reserve) : 0;
+    }
     const int32_t* base = m->jb.meta + b.tok0;
     const int M = (int)b.M;
     CK(launch_encoder(m, Ln, M, r32 + 4 * B, b.enc_buckets, base, base + M, base + 2 * M, base + 3 * M,
@@ -1845,6 +1857,15 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
     if (value > 2) { set_err("fuse_ln must be 0, 1 or 2"); return MNMT_ERR_ARG; }
     m->fuse_ln = (int)value;
     for (Lane& L : m->lanes) {   // captured graphs encode the old kernel sequence
+      for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
+      L.graphs.clear();
+    }
+    return MNMT_OK;
+  }
+  if (std::string(name) == "pers_reserve") {
+    if (value < 0 || value > 128) { set_err("pers_reserve must be in [0, 128]"); return MNMT_ERR_ARG; }
+    m->pers_reserve = (int)value;
+    for (Lane& L : m->lanes) {   // captured graphs encode the old grid sizes
       for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
       L.graphs.clear();
     }
