@@ -337,9 +337,11 @@ def main():
                     help="1: persistent step kernel per batch; 0: one kernel per op (CUDA graph)")
     ap.add_argument("--lanes", type=int, default=3,
                     help="independent decoder lanes (streams) per GPU (scheduling only)")
-    ap.add_argument("--lane-tiers", type=int, default=30,
+    ap.add_argument("--lane-tiers", type=int, default=40,
                     help="0: deal sentences round-robin to lanes; 10*p: contiguous length tiers "
                          "of equal sum S^p (scheduling only)")
+    ap.add_argument("--green-sms", type=int, default=56,
+                    help="SM partition (green context) of the critical lane; 0 = shared SMs")
     ap.add_argument("--pers-reserve", type=int, default=16,
                     help="SMs the persistent GEMMs of non-critical lanes leave free")
     ap.add_argument("--steps-per-graph", type=int, default=1,
@@ -369,6 +371,7 @@ def main():
                     "max_concurrent_rows": args.max_concurrent_rows, "lanes": args.lanes,
                     "fuse_ln": args.fuse_ln, "steps_per_graph": args.steps_per_graph,
                     "lane_tiers": args.lane_tiers, "pers_reserve": args.pers_reserve,
+                    "green_sms": args.green_sms,
                     "step_engine": "persistent cooperative kernel" if args.megakernel else "kernel-per-op CUDA graph"}
 
     if args.impl == "reference":
@@ -396,6 +399,7 @@ def main():
     model.set_option("steps_per_graph", args.steps_per_graph)
     model.set_option("lane_tiers", args.lane_tiers)
     model.set_option("pers_reserve", args.pers_reserve)
+    model.set_option("green_sms", args.green_sms)
     sset = synth.newstest_set(seed=2014 + rank)          # weak scaling: one set per GPU
     stream = torch.cuda.current_stream()
     dev = torch.device("cuda", local)

@@ -166,6 +166,11 @@ mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids_host,
  *                          10*p: contiguous length tiers of equal sum S_i^p, the last lane (the
  *                          longest sentences, the job's critical path) on the highest-priority stream.
  *   "pers_reserve"         SMs the persistent GEMMs of the other lanes leave free (default 0).
+ *   "green_sms"            0 (default) or a multiple of 8: with tiered lanes, the critical lane's
+ *                          streams live in a green context (SM partition) of this many SMs and the
+ *                          other lanes' in one holding the rest.
+ *   "mk_cluster"           1: the persistent step kernel's grid (mk_ctas <= 16) is one thread-block
+ *                          cluster and its phases synchronise with cluster barriers.
  *   "mk_ctas"              grid cap of the persistent step kernel (0 = one CTA per SM).
  *   "profile_phases"       1 = the persistent kernel stamps every phase (mnmt_debug_phase_*).
  * Errors: MNMT_ERR_ARG (unknown name or negative value). */

@@ -9,6 +9,7 @@
 //            -> src-q GEMM -> src attention -> src-o GEMM -> LN2 -> FFN1 -> FFN2
 //            -> LN3 (+AAN step of the next layer) -> output GEMM fused with argmax -> finish.
 #include <algorithm>
+#include <cuda.h>
 #include <array>
 #include <cmath>
 #include <cstdarg>
@@ -117,6 +118,7 @@ struct Lane {
   std::map<int64_t, cudaGraphExec_t> graphs;   // key: padded live-row bound
   int64_t launches_per_step = 0;
   int span_cap = 0;                            // attention span the step kernels are sized for
+  int kind = -1;                               // streams from: 0 runtime, 1 critical / 2 bulk green context
   // persistent step kernel program (built for this lane's workspace)
   Phase* d_phases = nullptr;
   int n_phases = 0;
@@ -158,6 +160,10 @@ struct mnmt_model {
   int rowlocal = 0;                    // option: row-local phases in the persistent step kernel (measured slower)
   int steps_per_graph = 1;             // option: decoder steps captured per CUDA graph
   int mk_ctas = 0;                     // option: persistent step kernel grid cap (0 = one per SM)
+  int mk_cluster = 0;                  // option: persistent step kernel grid = one cluster (mk_ctas <= 16)
+  int green_sms = 0;                   // option: SMs of the critical lane's green context (0 = off)
+  CUgreenCtx green[2] = {nullptr, nullptr};   // [0] critical lane, [1] the other lanes
+  int green_count[2] = {0, 0};                // SMs of each partition
   int pers_reserve = 0;                // option: SMs the persistent GEMMs of non-critical lanes leave free
   int cur_pers_grid = 0;               // (launch state) persistent-GEMM CTA cap of the lane being issued
   int lane_tiers = 0;                  // option: 0 = deal sentences round-robin to lanes;
@@ -326,23 +332,110 @@ static void jb_free(mnmt_model* m) {
   m->jb = JobBuf();
 }
 
+// ------------------------------------------------------------------ green contexts
+// SM partitions (driver API, resolved through cudaGetDriverEntryPoint like the tensor-map
+// encoder, so the library needs no -lcuda): with tiered lanes and option green_sms = N, the
+// critical lane's streams live in a green context of N SMs and the other lanes' in one holding
+// the rest, so the bulk can never occupy the SMs the critical path waits for.
+struct GreenApi {
+  CUresult (*dev_get)(CUdevice*, int) = nullptr;
+  CUresult (*get_res)(CUdevice, CUdevResource*, CUdevResourceType) = nullptr;
+  CUresult (*split)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned,
+                    unsigned) = nullptr;
+  CUresult (*gen_desc)(CUdevResourceDesc*, CUdevResource*, unsigned) = nullptr;
+  CUresult (*create)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned) = nullptr;
+  CUresult (*destroy)(CUgreenCtx) = nullptr;
+  CUresult (*stream_create)(CUstream*, CUgreenCtx, unsigned, int) = nullptr;
+  bool ok = false;
+};
+static const GreenApi& green_api() {
+  static GreenApi g;
+  static bool tried = false;
+  if (tried) return g;
+  tried = true;
+  auto get = [](const char* name, void** fn) {
+    cudaDriverEntryPointQueryResult q;
+    return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+           q == cudaDriverEntryPointSuccess;
+  };
+  g.ok = get("cuDeviceGet", (void**)&g.dev_get) && get("cuDeviceGetDevResource", (void**)&g.get_res) &&
+         get("cuDevSmResourceSplitByCount", (void**)&g.split) &&
+         get("cuDevResourceGenerateDesc", (void**)&g.gen_desc) &&
+         get("cuGreenCtxCreate", (void**)&g.create) && get("cuGreenCtxDestroy", (void**)&g.destroy) &&
+         get("cuGreenCtxStreamCreate", (void**)&g.stream_create);
+  return g;
+}
+
+static mnmt_status green_ensure(mnmt_model* m) {
+  if (m->green[0] || m->green_sms <= 0) return MNMT_OK;
+  const GreenApi& g = green_api();
+  if (!g.ok) { set_err("green contexts unavailable in this driver"); return MNMT_ERR_CUDA; }
+  CUdevice dev;
+  CUdevResource all, part[1], rest;
+  CUdevResourceDesc d0, d1;
+  unsigned n = 1;
+  if (g.dev_get(&dev, m->dev) != CUDA_SUCCESS || g.get_res(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS ||
+      g.split(part, &n, &all, &rest, 0, (unsigned)m->green_sms) != CUDA_SUCCESS || n != 1 ||
+      g.gen_desc(&d0, part, 1) != CUDA_SUCCESS || g.gen_desc(&d1, &rest, 1) != CUDA_SUCCESS ||
+      g.create(&m->green[0], d0, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+      g.create(&m->green[1], d1, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) {
+    set_err("green context creation failed (green_sms %d)", m->green_sms);
+    return MNMT_ERR_CUDA;
+  }
+  m->green_count[0] = (int)part[0].sm.smCount;
+  m->green_count[1] = (int)rest.sm.smCount;
+  return MNMT_OK;
+}
+
+static void lane_streams_free(Lane& L) {
+  for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
+  L.graphs.clear();
+  if (L.st) cudaStreamDestroy(L.st);
+  if (L.side) cudaStreamDestroy(L.side);
+  if (L.ev) cudaEventDestroy(L.ev);
+  if (L.ev_fork) cudaEventDestroy(L.ev_fork);
+  if (L.ev_join) cudaEventDestroy(L.ev_join);
+  L.st = L.side = nullptr;
+  L.ev = L.ev_fork = L.ev_join = nullptr;
+  L.kind = -1;
+}
+
 // Lane li's streams get priority li steps above the lowest (clamped): with length tiers the
-// last lane holds the longest sentences, i.e. the job's critical path.
+// last lane holds the longest sentences, i.e. the job's critical path.  With green_sms the
+// streams come from the lane's SM partition.
 static mnmt_status lane_init(mnmt_model* m, Lane& L, int li) {
-  if (L.st) return MNMT_OK;
+  const bool tiered = m->n_lanes > 1 && m->lane_tiers > 0;
+  const int kind = (m->green_sms > 0 && tiered) ? (li == m->n_lanes - 1 ? 1 : 2) : 0;
+  if (L.st && L.kind == kind) return MNMT_OK;
+  if (L.st) {
+    cudaDeviceSynchronize();
+    lane_streams_free(L);
+  }
   int least = 0, greatest = 0;
   cudaDeviceGetStreamPriorityRange(&least, &greatest);
   const int prio = std::max(greatest, least - li);
-  if (cudaStreamCreateWithPriority(&L.st, cudaStreamNonBlocking, prio) != cudaSuccess ||
-      cudaStreamCreateWithPriority(&L.side, cudaStreamNonBlocking, prio) != cudaSuccess ||
-      cudaEventCreateWithFlags(&L.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+  bool ok;
+  if (kind) {
+    mnmt_status gs = green_ensure(m);
+    if (gs != MNMT_OK) return gs;
+    const GreenApi& g = green_api();
+    CUstream a = nullptr, b = nullptr;
+    ok = g.stream_create(&a, m->green[kind - 1], CU_STREAM_NON_BLOCKING, prio) == CUDA_SUCCESS &&
+         g.stream_create(&b, m->green[kind - 1], CU_STREAM_NON_BLOCKING, prio) == CUDA_SUCCESS;
+    L.st = (cudaStream_t)a;
+    L.side = (cudaStream_t)b;
+  } else {
+    ok = cudaStreamCreateWithPriority(&L.st, cudaStreamNonBlocking, prio) == cudaSuccess &&
+         cudaStreamCreateWithPriority(&L.side, cudaStreamNonBlocking, prio) == cudaSuccess;
+  }
+  if (!ok || cudaEventCreateWithFlags(&L.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&L.ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&L.ev, cudaEventDisableTiming) != cudaSuccess) {
     cudaGetLastError();
     set_err("lane stream/event creation failed");
     return MNMT_ERR_CUDA;
   }
-  (void)m;
+  L.kind = kind;
   return MNMT_OK;
 }
 
@@ -1229,6 +1322,7 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->dev);
       const bool critical = b.lane == m->n_lanes - 1 || m->n_lanes <= 1 || m->lane_tiers == 0;
       m->cur_pers_grid = (!critical && m->pers_reserve > 0) ? std::max(1, sms - m->pers_reserve) : 0;
+      if (Ln.kind > 0) m->cur_pers_grid = m->green_count[Ln.kind - 1];   // the lane's SM partition
     }
     const int32_t* base = m->jb.meta + b.tok0;
     const int M = (int)b.M;
@@ -1258,6 +1352,7 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
       if (!Ln.d_phases || Ln.prog_forced != forced || Ln.prog_out != m->jb.out_ids)
         CKS(build_program(m, Ln, forced));
       StepArgs sa{};
+      sa.cluster = (m->mk_cluster && m->mk_ctas > 0 && m->mk_ctas <= 16) ? 1 : 0;
       sa.phases = Ln.d_phases;
       sa.n_phases = Ln.n_phases;
       sa.ctrl = w.ctrl;
@@ -1871,6 +1966,24 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
     }
     return MNMT_OK;
   }
+  if (std::string(name) == "green_sms") {
+    if (value < 0 || value > 136 || value % 8) { set_err("green_sms must be 0 or a multiple of 8 up to 136"); return MNMT_ERR_ARG; }
+    if (value != m->green_sms) {
+      DeviceGuard g(m->dev);
+      cudaDeviceSynchronize();
+      for (Lane& L : m->lanes) lane_streams_free(L);   // recreated (in the new partitions) on use
+      const GreenApi& ga = green_api();
+      for (auto& gc : m->green)
+        if (gc) { ga.destroy(gc); gc = nullptr; }
+      m->green_sms = (int)value;
+    }
+    return MNMT_OK;
+  }
+  if (std::string(name) == "mk_cluster") {
+    if (value != 0 && value != 1) { set_err("mk_cluster must be 0 or 1"); return MNMT_ERR_ARG; }
+    m->mk_cluster = (int)value;
+    return MNMT_OK;
+  }
   if (std::string(name) == "mk_ctas") {
     if (value < 0 || value > 4096) { set_err("mk_ctas must be in [0, 4096]"); return MNMT_ERR_ARG; }
     m->mk_ctas = (int)value;
@@ -1967,14 +2080,12 @@ extern "C" void mnmt_model_destroy(mnmt_model* m) {
     cudaDeviceSynchronize();
     for (Lane& L : m->lanes) {
       lane_free(L);
-      if (L.st) cudaStreamDestroy(L.st);
-      if (L.side) cudaStreamDestroy(L.side);
-      if (L.ev) cudaEventDestroy(L.ev);
-      if (L.ev_fork) cudaEventDestroy(L.ev_fork);
-      if (L.ev_join) cudaEventDestroy(L.ev_join);
+      lane_streams_free(L);
     }
     jb_free(m);
     for (void* p : m->allocs) cudaFree(p);
+    for (auto& gc : m->green)
+      if (gc) green_api().destroy(gc);
     if (m->st) cudaStreamDestroy(m->st);
     if (m->ev_in) cudaEventDestroy(m->ev_in);
     if (m->ev_out) cudaEventDestroy(m->ev_out);

@@ -209,8 +209,13 @@ __global__ void __launch_bounds__(SK_THREADS, 1) k_step(const StepArgs s) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_slot;
-  unsigned gen = ld_acquire_gpu(s.bar + 32);
-  grid_sync(s.bar, gen);   // everybody has read the generation before anyone moves on
+  unsigned gen = 0;
+  if (s.cluster) {
+    cluster_sync();
+  } else {
+    gen = ld_acquire_gpu(s.bar + 32);
+    grid_sync(s.bar, gen);   // everybody has read the generation before anyone moves on
+  }
 
   Pipe pp;   // each role only touches its own fields
   const int gwarp = blockIdx.x * SK_WARPS + warp;
@@ -369,7 +374,12 @@ __global__ void __launch_bounds__(SK_THREADS, 1) k_step(const StepArgs s) {
         }
       }
       if (P.sync_grid) {
-        grid_sync(s.bar, gen);
+        if (s.cluster) {
+          __syncwarp();
+          cluster_sync();   // release/acquire at cluster scope orders the global writes too
+        } else {
+          grid_sync(s.bar, gen);
+        }
       } else {
         fence_proxy_async();   // this CTA's global writes -> its own TMA reads in the next phase
         __syncthreads();
@@ -446,9 +456,12 @@ int step_kernel_grid() {
   if (grid[dev]) return grid[dev];
   const void* fns[4] = {(const void*)k_step<1>, (const void*)k_step<2>, (const void*)k_step<4>,
                         (const void*)k_step<8>};
-  for (const void* f : fns)
+  for (const void* f : fns) {
     if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SK_SMEM) != cudaSuccess)
       return -1;
+    cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaGetLastError();
+  }
   int sms = 0, per_sm = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step<2>, SK_THREADS, SK_SMEM) !=
@@ -469,8 +482,16 @@ cudaError_t launch_step_kernel(const StepArgs& a, int d, cudaStream_t st, int gr
   cfg.dynamicSmemBytes = SK_SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
+  if (a.cluster) {
+    if (grid > 16) return cudaErrorInvalidConfiguration;
+    attr[0].id = cudaLaunchAttributeClusterDimension;   // one cluster: co-scheduled by construction
+    attr[0].val.clusterDim.x = grid;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+  } else {
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+  }
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const int nv = (d / 4 + 31) / 32;

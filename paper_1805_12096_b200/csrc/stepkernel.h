@@ -45,10 +45,13 @@ struct StepArgs {
   int max_steps;            // steps this launch may run (stops early when no row is live)
   unsigned int* bar;        // grid barrier state {count, pad..., generation}
   unsigned long long* timing;   // optional: [max_steps][n_phases + 1] %globaltimer stamps
+  int cluster;              // 1: the grid is ONE thread-block cluster; phases sync with
+                            //    barrier.cluster (release/acquire) instead of the global barrier
 };
 
 // Launch (cooperative, one CTA per SM) on `st`; d selects the row-kernel width.
-// grid_cap > 0 limits the grid (CTAs) below one per SM.
+// grid_cap > 0 limits the grid (CTAs) below one per SM.  a.cluster = 1 launches the grid as one
+// cluster of grid_cap (<= 16) CTAs.
 cudaError_t launch_step_kernel(const StepArgs& a, int d, cudaStream_t st, int grid_cap = 0);
 // Sets the smem attribute once per device; returns the grid size (CTAs) or -1.
 int step_kernel_grid();

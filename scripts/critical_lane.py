@@ -33,3 +33,7 @@ for k in (100, 206, 400):
     print(f"longest {k} sentences alone (1 lane): {t_job(sub, 1, 0):.2f} ms")
 sub = ss.subset(order[:-206])
 print(f"all but the longest 206 (2 lanes tiers 30): {t_job(sub, 2, 30):.2f} ms")
+for k in (206,):
+    sub = ss.subset(order[-k:])
+    cap1 = synth.SentenceSet(sub.ids, sub.offsets, np.minimum(sub.max_len, 1).astype(np.int32))
+    print(f"longest {k} sentences, 1 decoder step (encoder + 1 step): {t_job(cap1, 1, 0):.2f} ms")

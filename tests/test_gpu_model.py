@@ -112,12 +112,13 @@ def test_tiny_free_running(dims):
     ref = om.decode_many(ss, 4)
     # persistent step kernel (grid-wide phases; row-local phases on a capped grid) and one
     # kernel per op (graph)
-    for mk, rl, ctas in ((1, 0, 0), (1, 1, 8), (0, 0, 0)):
+    for mk, rl, ctas, cl in ((1, 0, 0, 0), (1, 1, 8, 0), (1, 0, 16, 1), (0, 0, 0, 0)):
         gm.set_option("megakernel", mk)
         gm.set_option("rowlocal", rl)
         gm.set_option("mk_ctas", ctas)
+        gm.set_option("mk_cluster", cl)   # grid = one 16-CTA cluster, cluster barriers
         got = gm.decode(ss)
-        assert all(np.array_equal(a, b) for a, b in zip(got, ref)), (mk, rl, ctas)
+        assert all(np.array_equal(a, b) for a, b in zip(got, ref)), (mk, rl, ctas, cl)
 
 
 def test_config0_tiny192_aan():
@@ -175,6 +176,10 @@ def test_batch_and_order_invariance():
         for tiers in (10, 30):             # length-tiered lanes (prioritised streams)
             gm.set_option("lane_tiers", tiers)
             assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, 64), base))
+            if lanes > 1:                  # critical lane in its own SM partition (green context)
+                gm.set_option("green_sms", 48)
+                assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, 64), base))
+                gm.set_option("green_sms", 0)
         gm.set_option("lane_tiers", 0)
     for k in (3, 8):                       # several decoder steps per CUDA graph
         gm.set_option("steps_per_graph", k)
