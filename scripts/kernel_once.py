@@ -19,8 +19,9 @@ if k in ("dxd", "out"):
     for _ in range(4):
         M.op_gemm_i8(A.data_ptr(), W.data_ptr(), Mr, N, d, b.data_ptr(), 2.0, epi, out.data_ptr(), None, 0, None)
 else:
-    L = np.full(Mr, 21, np.int32); st = (np.arange(Mr) * 21).astype(np.int32)
-    kv = torch.randn(Mr * 21, 2 * d, device=dev); q = torch.randn(Mr, d, device=dev)
+    S = int(os.environ.get("S", 21))
+    L = np.full(Mr, S, np.int32); st = (np.arange(Mr) * S).astype(np.int32)
+    kv = torch.randn(Mr * S, 2 * d, device=dev); q = torch.randn(Mr, d, device=dev)
     S, Ln = torch.from_numpy(st).to(dev), torch.from_numpy(L).to(dev)
     oq = torch.empty(Mr, d, dtype=torch.int8, device=dev)
     for _ in range(4):
