@@ -27,12 +27,14 @@ namespace mnmt {
 
 static int num_sms();
 bool gemm_persistent(int M, int N, int bn);
+__constant__ int c_trigger_mode = 0;   // TEMP A/B: 0 epilogue warp 2 at tmem_full, 1 MMA warp after commit
 
 constexpr int BM = 128;           // MMA M (rows of A per tile)
 constexpr int BK = 128;           // K bytes per stage = one 128B swizzle atom row
 constexpr int EPI_WARPS = 8;      // two warps per TMEM lane quarter, splitting the columns
 constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
-constexpr int EPI_STAGE_LD = 33;                       // padded row stride (floats)
+constexpr int EPI_STAGE_LD = 36;                       // row stride (floats): 16-byte rows, and
+                                                       // conflict-free STS.128 / LDS.128
 constexpr int EPI_STAGE_FLOATS = 32 * EPI_STAGE_LD;    // per epilogue warp
 constexpr int EPI_STAGE_BYTES = EPI_WARPS * EPI_STAGE_FLOATS * 4;
 constexpr int LNC_MAX_CLUSTER = 8;                     // portable cluster size limit
@@ -49,6 +51,18 @@ struct GemmCfg {
 
 // Exact (float)acc for |acc| < 2^22 without the quarter-rate I2F: place acc in the
 // mantissa of 1.5 * 2^23 and subtract.  Used when K <= 256 (|acc| <= 127^2 * 256 < 2^22).
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// debug trace (GemmArgs::trace): CTA (0,0) records entry, after the PDL wait, operands landed,
+// accumulator complete, epilogue done
+#define GEMM_TRACE(i)                                                              \
+  do {                                                                             \
+    if (args.trace && blockIdx.x == 0 && blockIdx.y == 0) args.trace[i] = gtimer(); \
+  } while (0)
+
 __device__ __forceinline__ float acc_to_float(int32_t acc, bool small) {
   return small ? __fsub_rn(__int_as_float(0x4B400000 + acc), 12582912.0f) : __int2float_rn(acc);
 }
@@ -69,14 +83,16 @@ __device__ __forceinline__ void upk2(unsigned long long r, float& a, float& b) {
 
 // v[j] = fmaf((float)acc[j], s, bias[j]) for one 32-column chunk.
 // Fast path (K <= 256, whole chunk in range): exact magic-number conversion + packed ops.
-__device__ __forceinline__ void dequant32(const GemmArgs& args, int n, bool fast,
+// bsrc: the bias indexed by global column (args.bias, or the CTA's shared-memory copy shifted by
+// its first column) or null.
+__device__ __forceinline__ void dequant32(const GemmArgs& args, const float* bsrc, int n, bool fast,
                                           const int32_t (&acc)[32], float (&v)[32]) {
   if (fast) {
     float bias[32];
-    if (args.bias) {
+    if (bsrc) {
 #pragma unroll
       for (int j = 0; j < 32; j += 4) {
-        const float4 b4 = __ldg(reinterpret_cast<const float4*>(args.bias + n + j));
+        const float4 b4 = *reinterpret_cast<const float4*>(bsrc + n + j);
         bias[j] = b4.x; bias[j + 1] = b4.y; bias[j + 2] = b4.z; bias[j + 3] = b4.w;
       }
     } else {
@@ -97,7 +113,7 @@ __device__ __forceinline__ void dequant32(const GemmArgs& args, int n, bool fast
     const bool small = args.K <= 256;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      const float b = (args.bias && n + j < args.N) ? __ldg(args.bias + n + j) : 0.0f;
+      const float b = (bsrc && n + j < args.N) ? bsrc[n + j] : 0.0f;
       v[j] = __fmaf_rn(acc_to_float(acc[j], small), args.scale, b);
     }
   }
@@ -107,9 +123,9 @@ __device__ __forceinline__ void dequant32(const GemmArgs& args, int n, bool fast
 // store, or running argmax.  fp32 outputs go through a padded per-warp smem tile so each
 // store instruction writes four full 128-byte lines.
 template <int EPI>
-__device__ __forceinline__ void epi_store_chunk(const GemmArgs& args, int row, bool row_ok, int n,
-                                                const int32_t (&acc)[32], float& best_v,
-                                                int& best_j, float* stage) {
+__device__ __forceinline__ void epi_store_chunk(const GemmArgs& args, const float* bsrc, int row,
+                                                bool row_ok, int n, const int32_t (&acc)[32],
+                                                float& best_v, int& best_j, float* stage) {
   const bool full = n + 32 <= args.N;
   const bool fast = full && args.K <= 256;
   if constexpr (EPI == EPI_ARGMAX) {
@@ -117,7 +133,7 @@ __device__ __forceinline__ void epi_store_chunk(const GemmArgs& args, int row, b
     // chunk beats the running best, and a strictly greater value is required, so among
     // equal logits the lowest column wins (R15).
     float v[32];
-    dequant32(args, n, fast, acc, v);
+    dequant32(args, bsrc, n, fast, acc, v);
     if (!full) {
 #pragma unroll
       for (int j = 0; j < 32; ++j)
@@ -147,7 +163,7 @@ __device__ __forceinline__ void epi_store_chunk(const GemmArgs& args, int row, b
     }
   } else {
     float v[32];
-    dequant32(args, n, fast, acc, v);
+    dequant32(args, bsrc, n, fast, acc, v);
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       if constexpr (EPI == EPI_RELU_Q || EPI == EPI_RELU_F32_Q) v[j] = relu(v[j]);
@@ -156,22 +172,24 @@ __device__ __forceinline__ void epi_store_chunk(const GemmArgs& args, int row, b
     if constexpr (EPI == EPI_F32 || EPI == EPI_F32_Q || EPI == EPI_RELU_F32_Q || EPI == EPI_SIGMOID) {
       // stage [32 rows][32 cols] then write rows cooperatively (8 lanes x float4 per row)
       const int lane = threadIdx.x & 31;
+      if (threadIdx.x == 64) GEMM_TRACE(7);   // warp 2 lane 0: dequant done
+      const unsigned okm = __ballot_sync(0xffffffffu, row_ok);   // live rows of this warp
 #pragma unroll
-      for (int j = 0; j < 32; ++j) stage[lane * EPI_STAGE_LD + j] = v[j];
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(stage + lane * EPI_STAGE_LD + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
       __syncwarp();
+      if (threadIdx.x == 64) GEMM_TRACE(8);   // staged
       const int row0 = row - lane;
       const int blk = n / args.col_block;   // 32-column chunks never straddle a block (16 | col_block)
       float* base = args.out_f + (int64_t)blk * args.block_stride + (n - blk * args.col_block);
       const int sub = lane >> 3, c4 = (lane & 7) * 4;
 #pragma unroll
       for (int it = 0; it < 8; ++it) {
+        if (((okm >> (4 * it)) & 0xFu) == 0) continue;   // warp-uniform: no live row in the group
         const int r = it * 4 + sub;
-        const bool ok = __shfl_sync(0xffffffffu, row_ok ? 1 : 0, r) != 0;
-        if (ok && n + c4 < args.N) {
-          const float* sr = stage + r * EPI_STAGE_LD + c4;
+        if (((okm >> r) & 1u) && n + c4 < args.N)
           *reinterpret_cast<float4*>(base + (int64_t)(row0 + r) * args.ldo + c4) =
-              make_float4(sr[0], sr[1], sr[2], sr[3]);
-        }
+              *reinterpret_cast<const float4*>(stage + r * EPI_STAGE_LD + c4);
       }
       __syncwarp();
     }
@@ -326,6 +344,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __shared__ __align__(8) uint64_t tmem_full_bar;
   __shared__ uint32_t tmem_slot;
   __shared__ double ln_part[EPI == EPI_LN ? 256 : 1];
+  __shared__ __align__(16) float bias_s[BN];   // the tile's bias, staged before the PDL wait
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -334,6 +353,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int num_kb = (args.K + BK - 1) / BK;
   // ring depth chosen at launch (dynamic smem); at most Cfg::STAGES
   const int stages = min(Cfg::STAGES, num_kb);
+  if (threadIdx.x == 0) GEMM_TRACE(0);
 
   // 1024-byte aligned stage ring (required by the 128B swizzle atom).
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -358,9 +378,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tma_load_2d(sb + j * 64 * BK, &tmB, &full_bar[s], s * BK, n0 + j * 64);
     }
   }
-  // TMEM does not depend on the previous kernel either: allocate before the wait
+  // TMEM and the bias do not depend on the previous kernel either: both before the wait
   if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(&tmem_slot);
+  if (args.bias && warp >= 2)
+    for (int i = (int)threadIdx.x - 64; i < BN; i += 32 * EPI_WARPS)
+      bias_s[i] = n0 + i < args.N ? __ldg(args.bias + n0 + i) : 0.0f;
   pdl_wait();   // everything below may read the previous kernel's outputs
+  if (threadIdx.x == 0) GEMM_TRACE(1);
   // The A tiles of the first ring stages are requested right away, in parallel with the
   // live-row read (rows beyond it are loaded but never stored; an idle tile drains them).
   if (warp == 0 && lane == 0) {
@@ -410,6 +434,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int kb = 0; kb < num_kb; ++kb) {
         const int s = kb % stages;
         mbar_wait(&full_bar[s], (kb / stages) & 1);
+        if (kb == 0) GEMM_TRACE(2);
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
         const uint32_t sb = sa + Cfg::A_BYTES;
@@ -424,6 +449,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mma_commit(&empty_bar[s]);  // smem stage free once these MMAs have read it
       }
       mma_commit(&tmem_full_bar);   // accumulator complete
+      if (c_trigger_mode == 1) pdl_launch_dependents();   // all MMAs issued
     }
   } else {
     // ---------------- epilogue: warps 2..9; TMEM lane quarter = warp % 4 (hardware rule),
@@ -435,7 +461,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     constexpr int HALF = BN / 2;
     mbar_wait(&tmem_full_bar, 0);
     tc_fence_after();
-    if (warp == 2 && lane == 0) pdl_launch_dependents();   // (measured: earlier is slower)
+    if (warp == 2 && lane == 0) GEMM_TRACE(3);
+    if (c_trigger_mode == 0 && warp == 2 && lane == 0) pdl_launch_dependents();   // (measured: at entry is slower)
     const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + half * HALF;
     float* stage = reinterpret_cast<float*>(smem + stages * Cfg::STAGE_BYTES) +
                    (warp - 2) * EPI_STAGE_FLOATS;
@@ -450,18 +477,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tmem_ld16(t_row + c, *reinterpret_cast<int32_t(*)[16]>(acc));
       tmem_ld16(t_row + c + 16, *reinterpret_cast<int32_t(*)[16]>(acc + 16));
       tmem_ld_wait();
+      if (c == 0 && warp == 2 && lane == 0) GEMM_TRACE(6);
       const int n = n0 + half * HALF + c;
       if (n >= args.N) break;  // warp-uniform
-      epi_store_chunk<EPI>(args, row, row_ok, n, acc, best_v, best_j, stage);
+      epi_store_chunk<EPI>(args, args.bias ? bias_s - n0 : nullptr, row, row_ok, n, acc, best_v,
+                           best_j, stage);
     }
     if constexpr (EPI == EPI_ARGMAX) {
       if (row_ok && best_j >= 0) atomicMax(args.keys + row, argmax_key(best_v, (uint32_t)best_j));
     }
+    if (warp == 2 && lane == 0) GEMM_TRACE(4);   // this warp's stores issued
   }
 
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+  if (warp == 1 && lane == 0) GEMM_TRACE(5);     // after the barrier and the dealloc
 }
 
 // ------------------------------------------------------------------ cluster LayerNorm variant
@@ -856,7 +887,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tmem_ld_wait();
         const int n = n0 + half * HALF + c;
         if (n >= args.N) break;
-        epi_store_chunk<EPI>(args, row, row_ok, n, acc, best_v, best_j, stage);
+        epi_store_chunk<EPI>(args, args.bias, row, row_ok, n, acc, best_v, best_j, stage);
       }
       if constexpr (EPI == EPI_ARGMAX) {
         if (row_ok && best_j >= 0) atomicMax(args.keys + row, argmax_key(best_v, (uint32_t)best_j));
@@ -1022,6 +1053,11 @@ cudaError_t gemm_init() {
 
 static cudaError_t gemm_init_all() {
   cudaError_t e;
+  {
+    const char* v = getenv("MNMT_TRIG");
+    const int m = v ? atoi(v) : 0;
+    if ((e = cudaMemcpyToSymbol(c_trigger_mode, &m, sizeof m)) != cudaSuccess) return e;
+  }
   if ((e = cudaFuncSetAttribute(k_gemm_lnc<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 GemmCfg<64>::STAGES * GemmCfg<64>::STAGE_BYTES + 1024)) != cudaSuccess)
     return e;

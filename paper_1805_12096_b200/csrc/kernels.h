@@ -37,6 +37,7 @@ struct GemmArgs {
   int64_t block_stride;
   unsigned long long* keys;    // [rows] for EPI_ARGMAX
   int pers_grid;               // persistent variant: CTA cap (0 = one per SM)
+  unsigned long long* trace;   // debug: CTA (0,0) %globaltimer stamps [9] (null = off)
   LnArgs ln;                   // EPI_LN: residual / gate inputs, gamma, beta, outputs, AAN
 };
 

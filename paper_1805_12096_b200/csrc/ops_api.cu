@@ -1,6 +1,7 @@
 // ops_api.cu — op-level C ABI (include/mnmt_ops.h): each decode-path kernel on caller memory.
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "../../include/mnmt_ops.h"
 #include "kernels.h"
@@ -164,3 +165,62 @@ mnmt_status mnmt_op_attention(const float* q, int64_t ldq, const float* kv, int6
 }
 
 }  // extern "C"
+
+// Debug: a chain of `n` identical int8 GEMMs (M x N x K, EPI_F32, A -> out, PDL, captured in a CUDA
+// graph) replayed once; res[0] = mean per-launch time (us); res[1..5] = CTA (0,0)'s stamps relative
+// to its entry: after the PDL wait, operands landed, accumulator complete, warp 2's stores issued,
+// after the final barrier + TMEM dealloc; res[6] = entry-to-entry; res[7] = next kernel's wait
+// release minus our end.  Not part of the documented ABI.
+extern "C" mnmt_status mnmt_debug_gemm_chain(const int8_t* A, const int8_t* W, int32_t M, int32_t N,
+                                            int32_t K, float* out, int32_t n, double* res6) {
+  if (!A || !W || !out || n < 2 || !res6) return arg_error("mnmt_debug_gemm_chain: bad arguments");
+  cudaError_t e = gemm_init();
+  if (e != cudaSuccess) return cuda_status(e, "gemm_init");
+  CUtensorMap ta, tb;
+  if (!make_tmap_i8(&ta, A, M, K) || !make_tmap_i8(&tb, W, N, K)) return arg_error("tensor map");
+  unsigned long long* tr = nullptr;
+  if ((e = cudaMalloc(&tr, (size_t)n * 9 * 8)) != cudaSuccess) return cuda_status(e, "malloc");
+  cudaStream_t st;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  cudaGraph_t g;
+  cudaGraphExec_t ge;
+  cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  for (int i = 0; i < n; ++i) {
+    GemmArgs a{};
+    a.M = M; a.N = N; a.K = K; a.scale = 1.0f / 4032.25f; a.clip = 2.0f; a.sigma = 63.5f;
+    a.out_f = out; a.ldo = N; a.col_block = N; a.trace = tr + (size_t)i * 9;
+    launch_gemm_i8(ta, tb, a, EPI_F32, 0, st);
+  }
+  e = cudaStreamEndCapture(st, &g);
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&ge, g, 0);
+  if (e == cudaSuccess) e = cudaGraphLaunch(ge, st);   // warm
+  cudaEvent_t a0, a1;
+  cudaEventCreate(&a0);
+  cudaEventCreate(&a1);
+  if (e == cudaSuccess) e = cudaEventRecord(a0, st);
+  if (e == cudaSuccess) e = cudaGraphLaunch(ge, st);
+  if (e == cudaSuccess) e = cudaEventRecord(a1, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  std::vector<unsigned long long> h((size_t)n * 9);
+  if (e == cudaSuccess) e = cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a0, a1);
+  double acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = 1; i + 1 < n; ++i) {
+    const unsigned long long* t = h.data() + (size_t)i * 9;
+    for (int k = 0; k < 5; ++k) acc[k] += (double)(t[k + 1] - t[0]);
+    acc[5] += (double)(t[0] - h[(size_t)(i - 1) * 9]);
+    acc[6] += (double)(h[(size_t)(i + 1) * 9 + 1]) - (double)t[5];   // next kernel's wait release - our end
+    for (int k = 0; k < 3; ++k) acc[7 + k] += (double)(t[6 + k] - t[0]);
+  }
+  res6[0] = 1000.0 * ms / n;
+  for (int k = 0; k < 10; ++k) res6[k + 1] = acc[k] / (n - 2) / 1000.0;
+  cudaGraphExecDestroy(ge);
+  cudaGraphDestroy(g);
+  cudaEventDestroy(a0);
+  cudaEventDestroy(a1);
+  cudaStreamDestroy(st);
+  cudaFree(tr);
+  return cuda_status(e, "gemm chain");
+}
+
