@@ -340,6 +340,9 @@ def main():
     ap.add_argument("--lane-tiers", type=int, default=40,
                     help="0: deal sentences round-robin to lanes; 10*p: contiguous length tiers "
                          "of equal sum S^p (scheduling only)")
+    ap.add_argument("--rowfuse", type=int, default=0,
+                    help="steps with <= this many padded rows use the fused per-row AAN and "
+                         "source-attention blocks (0 = off)")
     ap.add_argument("--green-sms", type=int, default=56,
                     help="SM partition (green context) of the critical lane; 0 = shared SMs")
     ap.add_argument("--pers-reserve", type=int, default=16,
@@ -371,7 +374,7 @@ def main():
                     "max_concurrent_rows": args.max_concurrent_rows, "lanes": args.lanes,
                     "fuse_ln": args.fuse_ln, "steps_per_graph": args.steps_per_graph,
                     "lane_tiers": args.lane_tiers, "pers_reserve": args.pers_reserve,
-                    "green_sms": args.green_sms,
+                    "green_sms": args.green_sms, "rowfuse": args.rowfuse,
                     "step_engine": "persistent cooperative kernel" if args.megakernel else "kernel-per-op CUDA graph"}
 
     if args.impl == "reference":
@@ -400,6 +403,7 @@ def main():
     model.set_option("lane_tiers", args.lane_tiers)
     model.set_option("pers_reserve", args.pers_reserve)
     model.set_option("green_sms", args.green_sms)
+    model.set_option("rowfuse", args.rowfuse)
     sset = synth.newstest_set(seed=2014 + rank)          # weak scaling: one set per GPU
     stream = torch.cuda.current_stream()
     dev = torch.device("cuda", local)

@@ -8,6 +8,8 @@ from paper_1805_12096_b200 import mnmt as M
 dims = synth.PRESETS["small-aan"]
 m = M.Model(dims, synth.make_weights(dims, 1))
 m.set_option("max_concurrent_rows", 4096)
+for k, v in (a.split("=") for a in sys.argv[1:]):
+    m.set_option(k, int(v))
 dev = torch.device("cuda:0"); st = torch.cuda.current_stream()
 ss = synth.newstest_set(seed=2014)
 order = np.argsort(ss.lengths, kind="stable")

@@ -91,6 +91,17 @@ def test_tiny_teacher_forced(dims):
 
 
 @pytest.mark.parametrize("dims", TINY_VARIANTS, ids=lambda d: d.name)
+def test_tiny_teacher_forced_rowfused(dims):
+    """The fused per-row AAN / source-attention blocks (option rowfuse): every intermediate
+    (x1, x2, x3 of every layer, every step) within tolerance of the oracle, ids bit-exact."""
+    w, om, gm = pair(dims, 11)
+    gm.set_option("rowfuse", 1 << 20)
+    ss, forced, foff = forced_case(dims, 9, 0, 13, 0, 17, seed=3)
+    tot, ex, fl = run_forced_parity(dims, w, om, gm, ss, forced, foff)
+    assert ex == tot, f"{tot - ex} flagged near-ties"
+
+
+@pytest.mark.parametrize("dims", TINY_VARIANTS, ids=lambda d: d.name)
 def test_tiny_teacher_forced_persistent_kernel(dims):
     """Teacher forcing through the persistent step kernel (no dumps): per-step ids bit-exact."""
     w, om, gm = pair(dims, 13)
@@ -112,13 +123,15 @@ def test_tiny_free_running(dims):
     ref = om.decode_many(ss, 4)
     # persistent step kernel (grid-wide phases; row-local phases on a capped grid) and one
     # kernel per op (graph)
-    for mk, rl, ctas, cl in ((1, 0, 0, 0), (1, 1, 8, 0), (1, 0, 16, 1), (0, 0, 0, 0)):
+    for mk, rl, ctas, cl, rf in ((1, 0, 0, 0, 0), (1, 1, 8, 0, 0), (1, 0, 16, 1, 0), (0, 0, 0, 0, 0),
+                                 (0, 0, 0, 0, 1 << 20)):
         gm.set_option("megakernel", mk)
         gm.set_option("rowlocal", rl)
         gm.set_option("mk_ctas", ctas)
         gm.set_option("mk_cluster", cl)   # grid = one 16-CTA cluster, cluster barriers
+        gm.set_option("rowfuse", rf)      # fused per-row AAN / source-attention blocks
         got = gm.decode(ss)
-        assert all(np.array_equal(a, b) for a, b in zip(got, ref)), (mk, rl, ctas, cl)
+        assert all(np.array_equal(a, b) for a, b in zip(got, ref)), (mk, rl, ctas, cl, rf)
 
 
 def test_config0_tiny192_aan():
@@ -181,6 +194,9 @@ def test_batch_and_order_invariance():
                 assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, 64), base))
                 gm.set_option("green_sms", 0)
         gm.set_option("lane_tiers", 0)
+    gm.set_option("rowfuse", 1 << 20)     # fused per-row AAN / source-attention blocks
+    assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, 333), base))
+    gm.set_option("rowfuse", 0)
     for k in (3, 8):                       # several decoder steps per CUDA graph
         gm.set_option("steps_per_graph", k)
         assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, 333), base))
