@@ -27,7 +27,6 @@ namespace mnmt {
 
 static int num_sms();
 bool gemm_persistent(int M, int N, int bn);
-__constant__ int c_trigger_mode = 0;   // TEMP A/B: 0 epilogue warp 2 at tmem_full, 1 MMA warp after commit
 
 constexpr int BM = 128;           // MMA M (rows of A per tile)
 constexpr int BK = 128;           // K bytes per stage = one 128B swizzle atom row
@@ -449,7 +448,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mma_commit(&empty_bar[s]);  // smem stage free once these MMAs have read it
       }
       mma_commit(&tmem_full_bar);   // accumulator complete
-      if (c_trigger_mode == 1) pdl_launch_dependents();   // all MMAs issued
     }
   } else {
     // ---------------- epilogue: warps 2..9; TMEM lane quarter = warp % 4 (hardware rule),
@@ -462,7 +460,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     mbar_wait(&tmem_full_bar, 0);
     tc_fence_after();
     if (warp == 2 && lane == 0) GEMM_TRACE(3);
-    if (c_trigger_mode == 0 && warp == 2 && lane == 0) pdl_launch_dependents();   // (measured: at entry is slower)
+    // dependents launch once the accumulator is complete (measured: at entry is slower, and
+    // from the MMA warp after its last commit no different)
+    if (warp == 2 && lane == 0) pdl_launch_dependents();
     const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + half * HALF;
     float* stage = reinterpret_cast<float*>(smem + stages * Cfg::STAGE_BYTES) +
                    (warp - 2) * EPI_STAGE_FLOATS;
@@ -1053,11 +1053,6 @@ cudaError_t gemm_init() {
 
 static cudaError_t gemm_init_all() {
   cudaError_t e;
-  {
-    const char* v = getenv("MNMT_TRIG");
-    const int m = v ? atoi(v) : 0;
-    if ((e = cudaMemcpyToSymbol(c_trigger_mode, &m, sizeof m)) != cudaSuccess) return e;
-  }
   if ((e = cudaFuncSetAttribute(k_gemm_lnc<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 GemmCfg<64>::STAGES * GemmCfg<64>::STAGE_BYTES + 1024)) != cudaSuccess)
     return e;
