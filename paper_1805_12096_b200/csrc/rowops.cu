@@ -130,6 +130,113 @@ __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn(AttnArgs a) {
   attn_row_head(a, r, h, sc_dyn + (size_t)wi * (a.span + 64), a.span, pst, pln);
 }
 
+// Source attention split over NS warps per (row, head) for long spans (A7): warp w of a group
+// scores the 32-position chunks w, w + NS, ...; the row max is exchanged first, so every
+// p_j = exp(s_j - max) is the value of the one-warp kernel; Z and the context are per-warp
+// partial sums (positions in order inside a warp) combined in warp order (R25).
+template <int NS>
+__global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn_split(AttnArgs a) {
+  constexpr int G = ATTN_WARPS / NS;                      // (row, head) groups per CTA
+  extern __shared__ __align__(16) double as_smem[];
+  const int span = a.span;
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = wi / NS, w = wi % NS;
+  double* sc = as_smem + (size_t)g * span;                // [G][span] scores, then p
+  double* pm = as_smem + (size_t)G * span;                // [G][NS] partial max, then partial Z
+  double* pacc = pm + G * NS;                             // [G][NS][64] partial contexts
+  pdl_wait();
+  pdl_trigger_early();
+  const int64_t gw = (int64_t)blockIdx.x * G + g;
+  const int r = (int)(gw / a.H), h = (int)(gw - (int64_t)r * a.H);
+  const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
+  if ((int64_t)blockIdx.x * G / a.H >= n_live) return;    // uniform: no live row in this CTA
+  const bool live = r < n_live;
+  const int dh = a.dh;
+  int start = 0, len = 0;
+  if (live) {
+    start = a.live_start ? a.live_start[r] : a.kv_start[a.live[r]];
+    len = a.live_start ? a.live_len[r] : a.kv_len[a.live[r]];
+  }
+  const float* q = a.q + (int64_t)(live ? r : 0) * a.ldq + h * dh;
+  const float* K = a.kv + (int64_t)start * a.ldkv + a.k_off + h * dh;
+  const float* V = a.kv + (int64_t)start * a.ldkv + a.v_off + h * dh;
+  const double inv_sqrt = 1.0 / sqrt((double)dh);
+  // ---- scores of this warp's chunks, local max
+  double mx = -INFINITY;
+  for (int j0 = w * 32; j0 < len; j0 += NS * 32) {
+    const int j = j0 + lane;
+    if (j < len) {
+      const float* kr = K + (int64_t)j * a.ldkv;
+      double dot = 0.0;
+      for (int c = 0; c < dh; c += 4) {
+        const float4 k4 = *reinterpret_cast<const float4*>(kr + c);
+        const float4 q4 = *reinterpret_cast<const float4*>(q + c);
+        dot = __fma_rn((double)q4.x, (double)k4.x, dot);
+        dot = __fma_rn((double)q4.y, (double)k4.y, dot);
+        dot = __fma_rn((double)q4.z, (double)k4.z, dot);
+        dot = __fma_rn((double)q4.w, (double)k4.w, dot);
+      }
+      const double sj = __dmul_rn(dot, inv_sqrt);
+      sc[j] = sj;
+      mx = fmax(mx, sj);
+    }
+  }
+  mx = warp_max_f64(mx);
+  if (lane == 0) pm[g * NS + w] = mx;
+  __syncthreads();
+  double m = -INFINITY;
+  for (int k = 0; k < NS; ++k) m = fmax(m, pm[g * NS + k]);
+  __syncthreads();   // pm is reused for the partial Z below
+  // ---- p_j and the partial normaliser
+  double z = 0.0;
+  for (int j0 = w * 32; j0 < len; j0 += NS * 32) {
+    const int j = j0 + lane;
+    if (j < len) {
+      const double p = exp(__dsub_rn(sc[j], m));
+      sc[j] = p;
+      z = __dadd_rn(z, p);
+    }
+  }
+  z = warp_sum_f64(z);
+  if (lane == 0) pm[g * NS + w] = z;
+  __syncwarp();
+  // ---- partial context over this warp's positions, in order
+  for (int c = lane; c < dh; c += 32) {
+    double acc = 0.0;
+    for (int j0 = w * 32; j0 < len; j0 += NS * 32) {
+      const int je = min(j0 + 32, len);
+      int j = j0;
+      for (; j + 4 <= je; j += 4) {
+        const double v0 = V[(int64_t)(j + 0) * a.ldkv + c], v1 = V[(int64_t)(j + 1) * a.ldkv + c];
+        const double v2 = V[(int64_t)(j + 2) * a.ldkv + c], v3 = V[(int64_t)(j + 3) * a.ldkv + c];
+        acc = __fma_rn(sc[j + 0], v0, acc);
+        acc = __fma_rn(sc[j + 1], v1, acc);
+        acc = __fma_rn(sc[j + 2], v2, acc);
+        acc = __fma_rn(sc[j + 3], v3, acc);
+      }
+      for (; j < je; ++j) acc = __fma_rn(sc[j], (double)V[(int64_t)j * a.ldkv + c], acc);
+    }
+    pacc[(g * NS + w) * 64 + c] = acc;
+  }
+  __syncthreads();
+  if (w != 0 || !live) return;
+  double zt = 0.0;
+  for (int k = 0; k < NS; ++k) zt = __dadd_rn(zt, pm[g * NS + k]);
+  int8_t* out = a.out_q + (int64_t)r * a.d + h * dh;
+  for (int c = lane; c < dh; c += 32) {
+    double acc = 0.0;
+    for (int k = 0; k < NS; ++k) acc = __dadd_rn(acc, pacc[(g * NS + k) * 64 + c]);
+    const float ctx = len > 0 ? (float)__ddiv_rn(acc, zt) : 0.0f;
+    out[c] = (int8_t)q8(ctx, a.clip, a.sigma);
+    if (a.out_f) a.out_f[(int64_t)r * a.d + h * dh + c] = ctx;
+  }
+}
+
+inline size_t attn_split_smem(int ns, int span) {
+  const int G = ATTN_WARPS / ns;
+  return ((size_t)G * span + (size_t)G * ns + (size_t)G * ns * 64) * sizeof(double);
+}
+
 constexpr int FIN_THREADS = 1024;
 
 __global__ void __launch_bounds__(FIN_THREADS) k_finish(FinishArgs a) {
@@ -400,6 +507,12 @@ cudaError_t attn_init() {   // once per device
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              ATTN_WARPS * (MNMT_MAX_KV + 64) * (int)sizeof(double));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn_split<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)attn_split_smem(2, MNMT_MAX_KV));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn_split<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)attn_split_smem(4, MNMT_MAX_KV));
   if (e == cudaSuccess) e = set_carveouts();
   if (e == cudaSuccess) {
     const char* pe = getenv("MNMT_PDL_EARLY");
@@ -416,6 +529,15 @@ cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
   AttnArgs b = a;
   if (b.span <= 0 || b.span > MNMT_MAX_KV) b.span = MNMT_MAX_KV;
   if (b.dh > 64 || (b.dh & 3)) return cudaErrorInvalidValue;
+  // long source spans at small row counts: several warps per (row, head) (measured: -6 % per
+  // step at 64 rows with 100-word sources; at 206 rows the extra warps cost more than they save)
+  const int ns = (b.mode == ATTN_SRC && b.n <= 128) ? (b.span >= 128 ? 4 : b.span >= 64 ? 2 : 1) : 1;
+  if (ns == 2 || ns == 4) {
+    const int G = ATTN_WARPS / ns;
+    const dim3 grid((unsigned)((warps + G - 1) / G)), block(ATTN_WARPS * 32);
+    return ns == 2 ? launch_pdl(k_attn_split<2>, grid, block, attn_split_smem(2, b.span), st, b)
+                   : launch_pdl(k_attn_split<4>, grid, block, attn_split_smem(4, b.span), st, b);
+  }
   const dim3 grid((unsigned)((warps + ATTN_WARPS - 1) / ATTN_WARPS)), block(ATTN_WARPS * 32);
   return launch_pdl(k_attn, grid, block, (size_t)ATTN_WARPS * (b.span + 64) * 8, st, b);
 }

@@ -90,6 +90,17 @@ def test_tiny_teacher_forced(dims):
     assert ex == tot, f"{tot - ex} flagged near-ties"
 
 
+@pytest.mark.parametrize("lo,hi", [(30, 90), (60, 140)], ids=["split2", "split4"])
+def test_long_sources_split_attention(lo, hi):
+    """Long source spans take the split source-attention kernel (2 or 4 warps per (row, head),
+    R25): every intermediate within tolerance of the oracle, ids bit-exact."""
+    dims = TINY_VARIANTS[0]
+    w, om, gm = pair(dims, 21)
+    ss, forced, foff = forced_case(dims, 7, lo, hi, 2, 6, seed=9)
+    tot, ex, fl = run_forced_parity(dims, w, om, gm, ss, forced, foff)
+    assert ex == tot, f"{tot - ex} flagged near-ties"
+
+
 @pytest.mark.parametrize("dims", TINY_VARIANTS, ids=lambda d: d.name)
 def test_tiny_teacher_forced_rowfused(dims):
     """The fused per-row AAN / source-attention blocks (option rowfuse): every intermediate
