@@ -26,7 +26,7 @@
 namespace mnmt {
 
 static int num_sms();
-bool gemm_persistent(int M, int N, int bn);
+bool gemm_persistent(int M, int N, int bn, int sms = 0);
 
 constexpr int BM = 128;           // MMA M (rows of A per tile)
 constexpr int BK = 128;           // K bytes per stage = one 128B swizzle atom row
@@ -941,21 +941,23 @@ bool pdl_enabled() {
 
 // Persistent tile loop once the grid would exceed two waves of one CTA per SM
 // (env MNMT_GEMM_PERSISTENT=0/1 forces it off/on for A/B tests).
-bool gemm_persistent(int M, int N, int bn) {
+// sms: the SMs the launch may use (a lane's partition / pers_grid cap); 0 = the device's.
+bool gemm_persistent(int M, int N, int bn, int sms) {
   static const int force = [] {
     const char* e = getenv("MNMT_GEMM_PERSISTENT");
     return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
   if (force >= 0) return force == 1;
   const long tiles = (long)((M + BM - 1) / BM) * ((N + bn - 1) / bn);
-  return tiles > 2L * num_sms();
+  return tiles > 2L * (sms > 0 ? sms : num_sms());
 }
 
-int gemm_pick_bn(int M, int N) {
+int gemm_pick_bn(int M, int N, int sms) {
+  const int S = sms > 0 ? sms : num_sms();
   const int mt = (M + BM - 1) / BM;
-  if ((long)mt * ((N + 255) / 256) > 2L * num_sms()) return 256;   // persistent, widest tile
-  if (((N + 255) / 256) * mt >= 148) return 256;
-  if (((N + 127) / 128) * mt >= 74) return 128;
+  if ((long)mt * ((N + 255) / 256) > 2L * S) return 256;   // persistent, widest tile
+  if (((N + 255) / 256) * mt >= S) return 256;
+  if (((N + 127) / 128) * mt >= S / 2) return 128;
   return 64;
 }
 
@@ -991,7 +993,7 @@ static cudaError_t launch_pers_t(const CUtensorMap& tmA, const CUtensorMap& tmB,
 template <int BN, int EPI>
 static cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                             cudaStream_t st) {
-  if (gemm_persistent(a.M, a.N, BN)) return launch_pers_t<BN, EPI>(tmA, tmB, a, st);
+  if (gemm_persistent(a.M, a.N, BN, a.pers_grid)) return launch_pers_t<BN, EPI>(tmA, tmB, a, st);
   using Cfg = GemmCfg<BN>;
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM);
   const int num_kb = (a.K + BK - 1) / BK;
@@ -1144,7 +1146,7 @@ cudaError_t launch_gemm_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const
     if (a.N == 256) return launch_np<256, EPI_LN>(tmA, tmB, a, st);
     return cudaErrorInvalidValue;
   }
-  if (bn == 0) bn = gemm_pick_bn(a.M, a.N);
+  if (bn == 0) bn = gemm_pick_bn(a.M, a.N, a.pers_grid);
   switch (bn) {
     case 64: return launch_bn<64>(tmA, tmB, a, epi, st);
     case 128: return launch_bn<128>(tmA, tmB, a, epi, st);

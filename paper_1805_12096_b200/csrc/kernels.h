@@ -50,7 +50,7 @@ bool make_tmap_i8(CUtensorMap* map, const void* base, int64_t rows, int64_t K);
 cudaError_t launch_gemm_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                            int epi, int bn, cudaStream_t st);
 
-int gemm_pick_bn(int M, int N);   // 64, 128 or 256
+int gemm_pick_bn(int M, int N, int sms = 0);   // 64, 128 or 256 (sms: SM budget, 0 = device)
 int gemm_lnc_bn(int d);           // EPI_LNC tile width for N = d (0: not supported)
 
 // Programmatic dependent launch on every kernel (env MNMT_NO_PDL=1 disables; A/B testing).
