@@ -464,6 +464,156 @@ typedef struct {
     int8_t *out_codes;   /* [T][d] Q(dec_out): the output-layer A operand */
 } orc_trace;
 
+/* The decoder state of ONE hypothesis (one sentence for greedy decoding):
+ * the AAN running sums C_l (R6; C_l = 0 before t = 1) or the self-attention
+ * cache of positions 1..t. */
+typedef struct {
+    float *C;            /* [L][d] */
+    float *Ks, *Vs;      /* [L][Tcap][d] (decoder == 0) */
+    int Tcap;
+} orc_dstate;
+
+static void dstate_init(const orc_model *m, orc_dstate *s, int Tcap) {
+    const orc_cfg *c = &m->c;
+    int d = c->d_model, L = c->dec_layers;
+    s->Tcap = Tcap > 0 ? Tcap : 1;
+    s->C = (float *)calloc((size_t)L * d, sizeof(float));
+    s->Ks = s->Vs = NULL;
+    if (c->decoder == 0) {
+        s->Ks = (float *)calloc((size_t)L * s->Tcap * d, sizeof(float));
+        s->Vs = (float *)calloc((size_t)L * s->Tcap * d, sizeof(float));
+    }
+}
+static void dstate_copy(const orc_model *m, orc_dstate *dst, const orc_dstate *src) {
+    const orc_cfg *c = &m->c;
+    size_t n = (size_t)c->dec_layers * c->d_model;
+    memcpy(dst->C, src->C, sizeof(float) * n);
+    if (c->decoder == 0) {
+        memcpy(dst->Ks, src->Ks, sizeof(float) * n * src->Tcap);
+        memcpy(dst->Vs, src->Vs, sizeof(float) * n * src->Tcap);
+    }
+}
+static void dstate_free(orc_dstate *s) { free(s->C); free(s->Ks); free(s->Vs); }
+
+/* Scratch rows of one decoder step. */
+typedef struct {
+    float *y, *g, *a, *t1, *gi, *gf, *r, *x1, *x2, *ctx, *h, *pe, *qs;
+    int8_t *qa, *qy;
+} orc_scratch;
+
+static void scratch_init(const orc_model *m, orc_scratch *w) {
+    int d = m->c.d_model, F = m->c.d_ffn;
+    float **f[] = {&w->y, &w->g, &w->a, &w->t1, &w->gi, &w->gf, &w->r, &w->x1, &w->x2,
+                   &w->ctx, &w->pe, &w->qs};
+    for (size_t i = 0; i < sizeof(f) / sizeof(f[0]); ++i) *f[i] = (float *)malloc(sizeof(float) * d);
+    w->h = (float *)malloc(sizeof(float) * F);
+    w->qa = (int8_t *)malloc((size_t)(F > d ? F : d));
+    w->qy = (int8_t *)malloc((size_t)d);
+}
+static void scratch_free(orc_scratch *w) {
+    free(w->y); free(w->g); free(w->a); free(w->t1); free(w->gi); free(w->gf); free(w->r);
+    free(w->x1); free(w->x2); free(w->ctx); free(w->pe); free(w->qs); free(w->h); free(w->qa);
+    free(w->qy);
+}
+
+/* One decoder step t of one hypothesis (A5-A8): input in_id (< 0: the start
+ * symbol, R13) at position t-1; updates the state; the last layer's output is
+ * left in w->y.  kv: the source keys/values [L][2][S][d] (orc_encode).
+ * layer_out: optional [L][3][d] x1, x2, x3 of every layer. */
+static void dec_step(const orc_model *m, const float *kv, int S, orc_dstate *st, int in_id,
+                     int t, orc_scratch *w, float *layer_out) {
+    const orc_cfg *c = &m->c;
+    int d = c->d_model, F = c->d_ffn, H = c->n_heads, L = c->dec_layers;
+    float clip = c->clip, s = orc_dequant_scale(clip);
+    float *y = w->y, *g = w->g, *a = w->a, *t1 = w->t1, *gi = w->gi, *gf = w->gf;
+    float *x1 = w->x1, *x2 = w->x2, *ctx = w->ctx, *h = w->h, *qs = w->qs;
+    int8_t *qa = w->qa, *qy = w->qy;
+    /* A5: decoder input y = emb(id_{t-1}, t-1); zero embedding at t=1 (R13). */
+    embed(m, in_id, t - 1, y, w->pe);
+    for (int l = 0; l < L; ++l) {
+        const orc_dec_layer *D = &m->dec[l];
+        if (c->decoder == 1) {
+            /* A6: AAN.  C <- fl(C + y); g = fl(C / t) (R6, R7). */
+            orc_aan_step(st->C + (int64_t)l * d, y, t, d, g);
+            if (c->aan_ffn_depth == 0) {
+                memcpy(a, g, sizeof(float) * d);
+            } else {
+                orc_quantize(g, d, clip, qa);
+                lin1(&D->a1, qa, s, t1);
+                if (c->aan_ffn_depth == 1) {
+                    for (int k = 0; k < d; ++k) a[k] = t1[k] > 0.0f ? t1[k] : 0.0f;
+                } else {
+                    for (int k = 0; k < d; ++k) qa[k] = orc_q(t1[k] > 0.0f ? t1[k] : 0.0f, clip);
+                    lin1(&D->a2, qa, s, a);
+                }
+            }
+            if (c->aan_gate) {
+                /* Gate (R8): i = sig(W_i y + b_i), f = sig(W_f a + b_f), z = i*y + f*a. */
+                orc_quantize(y, d, clip, qy);
+                lin1(&D->gi, qy, s, gi);
+                orc_quantize(a, d, clip, qa);
+                lin1(&D->gf, qa, s, gf);
+                orc_sigmoid_array(gi, d, gi);
+                orc_sigmoid_array(gf, d, gf);
+                orc_residual_ln(y, a, gi, gf, d, D->ln1.g, D->ln1.b, c->ln_eps, x1);
+            } else {
+                orc_residual_ln(y, a, NULL, NULL, d, D->ln1.g, D->ln1.b, c->ln_eps, x1);
+            }
+        } else {
+            /* A6': self-attention over positions 1..t with a KV cache. */
+            float *Kl = st->Ks + (int64_t)l * st->Tcap * d, *Vl = st->Vs + (int64_t)l * st->Tcap * d;
+            orc_quantize(y, d, clip, qy);
+            lin1(&D->q, qy, s, qs);
+            lin1(&D->k, qy, s, Kl + (int64_t)(t - 1) * d);
+            lin1(&D->v, qy, s, Vl + (int64_t)(t - 1) * d);
+            orc_attention(qs, Kl, Vl, d, t, d, H, ctx);
+            orc_quantize(ctx, d, clip, qa);
+            lin1(&D->o, qa, s, a);
+            orc_residual_ln(y, a, NULL, NULL, d, D->ln1.g, D->ln1.b, c->ln_eps, x1);
+        }
+        /* A7: source attention. */
+        orc_quantize(x1, d, clip, qa);
+        lin1(&D->sq, qa, s, qs);
+        if (S > 0) {
+            orc_attention(qs, kv + ((int64_t)l * 2 + 0) * S * d, kv + ((int64_t)l * 2 + 1) * S * d,
+                          d, S, d, H, ctx);
+        } else {
+            memset(ctx, 0, sizeof(float) * d);
+        }
+        orc_quantize(ctx, d, clip, qa);
+        lin1(&D->so, qa, s, a);
+        orc_residual_ln(x1, a, NULL, NULL, d, D->ln2.g, D->ln2.b, c->ln_eps, x2);
+        /* A8: FFN; ReLU output goes straight to int8 codes. */
+        orc_quantize(x2, d, clip, qa);
+        lin1(&D->f1, qa, s, h);
+        for (int k = 0; k < F; ++k) qa[k] = orc_q(h[k] > 0.0f ? h[k] : 0.0f, clip);
+        lin1(&D->f2, qa, s, a);
+        orc_residual_ln(x2, a, NULL, NULL, d, D->ln3.g, D->ln3.b, c->ln_eps, y);
+        if (layer_out) {
+            float *dst = layer_out + (int64_t)l * 3 * d;
+            memcpy(dst, x1, sizeof(float) * d);
+            memcpy(dst + d, x2, sizeof(float) * d);
+            memcpy(dst + 2 * d, y, sizeof(float) * d);
+        }
+    }
+}
+
+/* A9: tied output projection: logit_j = fmaf((float)acc_j, s, b_j)
+ * with acc_j = sum_k Q(y)_k * Q(E)[j,k]; out_bias = 0: b_j = 0 (R14).
+ * qy receives Q(y). */
+static void out_logits(const orc_model *m, const float *y, int8_t *qy, float *logits) {
+    const orc_cfg *c = &m->c;
+    int d = c->d_model, V = c->vocab;
+    float s = orc_dequant_scale(c->clip);
+    orc_quantize(y, d, c->clip, qy);
+    for (int j = 0; j < V; ++j) {
+        int32_t acc = 0;
+        const int8_t *er = m->qE + (int64_t)j * d;
+        for (int k = 0; k < d; ++k) acc += (int32_t)qy[k] * (int32_t)er[k];
+        logits[j] = fmaf((float)acc, s, c->out_bias ? m->out_b[j] : 0.0f);
+    }
+}
+
 /* Greedy decode of ONE sentence (beam 1, softmax skipped, "select the
  * output word with highest activation").
  * forced == NULL: free-running; stop at EOS (not emitted) or t == max_len (R16).
@@ -473,110 +623,29 @@ typedef struct {
 int orc_decode_one(const orc_model *m, const int32_t *src, int S, int max_len,
                    const int32_t *forced, int32_t *out_ids, orc_trace *tr) {
     const orc_cfg *c = &m->c;
-    int d = c->d_model, F = c->d_ffn, H = c->n_heads, L = c->dec_layers, V = c->vocab;
-    float clip = c->clip, s = orc_dequant_scale(clip);
+    int d = c->d_model, L = c->dec_layers, V = c->vocab;
     if (!m->quantized) return -4;
     if (max_len < 0) return -1;
     for (int i = 0; i < S; ++i) if (src[i] < 0 || src[i] >= V) return -3;
     if (forced) for (int i = 0; i + 1 < max_len; ++i) if (forced[i] < 0 || forced[i] >= V) return -3;
     float *kv = (float *)malloc(sizeof(float) * (size_t)L * 2 * (S > 0 ? S : 1) * d);
     if (S > 0) orc_encode(m, src, S, NULL, kv);
-    float *C = (float *)calloc((size_t)L * d, sizeof(float));       /* AAN state (R6) */
-    int Tcap = max_len > 0 ? max_len : 1;
-    float *Ks = NULL, *Vs = NULL;
-    if (c->decoder == 0) {
-        Ks = (float *)malloc(sizeof(float) * (size_t)L * Tcap * d);
-        Vs = (float *)malloc(sizeof(float) * (size_t)L * Tcap * d);
-    }
-    float *y = (float *)malloc(sizeof(float) * d), *g = (float *)malloc(sizeof(float) * d);
-    float *a = (float *)malloc(sizeof(float) * d), *t1 = (float *)malloc(sizeof(float) * d);
-    float *gi = (float *)malloc(sizeof(float) * d), *gf = (float *)malloc(sizeof(float) * d);
-    float *r = (float *)malloc(sizeof(float) * d), *x1 = (float *)malloc(sizeof(float) * d);
-    float *x2 = (float *)malloc(sizeof(float) * d), *ctx = (float *)malloc(sizeof(float) * d);
-    float *h = (float *)malloc(sizeof(float) * F), *pe = (float *)malloc(sizeof(float) * d);
-    float *qs = (float *)malloc(sizeof(float) * d);
-    int8_t *qa = (int8_t *)malloc((size_t)(F > d ? F : d)), *qy = (int8_t *)malloc((size_t)d);
+    orc_dstate st;
+    dstate_init(m, &st, max_len);
+    orc_scratch w;
+    scratch_init(m, &w);
+    float *logits = (float *)malloc(sizeof(float) * (size_t)V);
     int n_out = 0, prev = -1;
     for (int t = 1; t <= max_len; ++t) {
-        /* A5: decoder input y = emb(id_{t-1}, t-1); zero embedding at t=1 (R13). */
         int in_id = t == 1 ? -1 : (forced ? forced[t - 2] : prev);
-        embed(m, in_id, t - 1, y, pe);
-        for (int l = 0; l < L; ++l) {
-            const orc_dec_layer *D = &m->dec[l];
-            if (c->decoder == 1) {
-                /* A6: AAN.  C <- fl(C + y); g = fl(C / t) (R6, R7). */
-                orc_aan_step(C + (int64_t)l * d, y, t, d, g);
-                if (c->aan_ffn_depth == 0) {
-                    memcpy(a, g, sizeof(float) * d);
-                } else {
-                    orc_quantize(g, d, clip, qa);
-                    lin1(&D->a1, qa, s, t1);
-                    if (c->aan_ffn_depth == 1) {
-                        for (int k = 0; k < d; ++k) a[k] = t1[k] > 0.0f ? t1[k] : 0.0f;
-                    } else {
-                        for (int k = 0; k < d; ++k) qa[k] = orc_q(t1[k] > 0.0f ? t1[k] : 0.0f, clip);
-                        lin1(&D->a2, qa, s, a);
-                    }
-                }
-                if (c->aan_gate) {
-                    /* Gate (R8): i = sig(W_i y + b_i), f = sig(W_f a + b_f), z = i*y + f*a. */
-                    orc_quantize(y, d, clip, qy);
-                    lin1(&D->gi, qy, s, gi);
-                    orc_quantize(a, d, clip, qa);
-                    lin1(&D->gf, qa, s, gf);
-                    orc_sigmoid_array(gi, d, gi);
-                    orc_sigmoid_array(gf, d, gf);
-                    orc_residual_ln(y, a, gi, gf, d, D->ln1.g, D->ln1.b, c->ln_eps, x1);
-                } else {
-                    orc_residual_ln(y, a, NULL, NULL, d, D->ln1.g, D->ln1.b, c->ln_eps, x1);
-                }
-            } else {
-                /* A6': self-attention over positions 1..t with a KV cache. */
-                float *Kl = Ks + (int64_t)l * Tcap * d, *Vl = Vs + (int64_t)l * Tcap * d;
-                orc_quantize(y, d, clip, qy);
-                lin1(&D->q, qy, s, qs);
-                lin1(&D->k, qy, s, Kl + (int64_t)(t - 1) * d);
-                lin1(&D->v, qy, s, Vl + (int64_t)(t - 1) * d);
-                orc_attention(qs, Kl, Vl, d, t, d, H, ctx);
-                orc_quantize(ctx, d, clip, qa);
-                lin1(&D->o, qa, s, a);
-                orc_residual_ln(y, a, NULL, NULL, d, D->ln1.g, D->ln1.b, c->ln_eps, x1);
-            }
-            /* A7: source attention. */
-            orc_quantize(x1, d, clip, qa);
-            lin1(&D->sq, qa, s, qs);
-            if (S > 0) {
-                orc_attention(qs, kv + ((int64_t)l * 2 + 0) * S * d, kv + ((int64_t)l * 2 + 1) * S * d,
-                              d, S, d, H, ctx);
-            } else {
-                memset(ctx, 0, sizeof(float) * d);
-            }
-            orc_quantize(ctx, d, clip, qa);
-            lin1(&D->so, qa, s, a);
-            orc_residual_ln(x1, a, NULL, NULL, d, D->ln2.g, D->ln2.b, c->ln_eps, x2);
-            /* A8: FFN; ReLU output goes straight to int8 codes. */
-            orc_quantize(x2, d, clip, qa);
-            lin1(&D->f1, qa, s, h);
-            for (int k = 0; k < F; ++k) qa[k] = orc_q(h[k] > 0.0f ? h[k] : 0.0f, clip);
-            lin1(&D->f2, qa, s, a);
-            orc_residual_ln(x2, a, NULL, NULL, d, D->ln3.g, D->ln3.b, c->ln_eps, y);
-            if (tr && tr->layer_out) {
-                float *dst = tr->layer_out + (((int64_t)(t - 1) * L + l) * 3) * d;
-                memcpy(dst, x1, sizeof(float) * d);
-                memcpy(dst + d, x2, sizeof(float) * d);
-                memcpy(dst + 2 * d, y, sizeof(float) * d);
-            }
-        }
-        /* A9: tied output projection + argmax, softmax skipped.
-         * logit_j = fmaf((float)acc_j, s, b_j); lowest j wins ties (R15). */
-        orc_quantize(y, d, clip, qy);
+        dec_step(m, kv, S, &st, in_id, t, &w,
+                 tr && tr->layer_out ? tr->layer_out + (int64_t)(t - 1) * L * 3 * d : NULL);
+        /* A9: argmax of the logits, softmax skipped; lowest j wins ties (R15). */
+        out_logits(m, w.y, w.qy, logits);
         int best = -1, second = -1;
         float bv = 0.0f, sv = 0.0f;
         for (int j = 0; j < V; ++j) {
-            int32_t acc = 0;
-            const int8_t *er = m->qE + (int64_t)j * d;
-            for (int k = 0; k < d; ++k) acc += (int32_t)qy[k] * (int32_t)er[k];
-            float lg = fmaf((float)acc, s, c->out_bias ? m->out_b[j] : 0.0f);
+            float lg = logits[j];
             if (best < 0 || lg > bv) { second = best; sv = bv; best = j; bv = lg; }
             else if (second < 0 || lg > sv) { second = j; sv = lg; }
         }
@@ -585,8 +654,8 @@ int orc_decode_one(const orc_model *m, const int32_t *src, int S, int max_len,
             if (tr->ids) tr->ids[i] = best;
             if (tr->second) tr->second[i] = second;
             if (tr->margin) tr->margin[i] = second >= 0 ? (float)((double)bv - (double)sv) : INFINITY;
-            if (tr->dec_out) memcpy(tr->dec_out + (int64_t)i * d, y, sizeof(float) * d);
-            if (tr->out_codes) memcpy(tr->out_codes + (int64_t)i * d, qy, (size_t)d);
+            if (tr->dec_out) memcpy(tr->dec_out + (int64_t)i * d, w.y, sizeof(float) * d);
+            if (tr->out_codes) memcpy(tr->out_codes + (int64_t)i * d, w.qy, (size_t)d);
         }
         if (forced) {
             out_ids[n_out++] = best;
@@ -597,9 +666,179 @@ int orc_decode_one(const orc_model *m, const int32_t *src, int S, int max_len,
             prev = best;
         }
     }
-    free(kv); free(C); free(Ks); free(Vs); free(y); free(g); free(a); free(t1); free(gi); free(gf);
-    free(r); free(x1); free(x2); free(ctx); free(h); free(pe); free(qs); free(qa); free(qy);
+    free(kv); free(logits);
+    dstate_free(&st);
+    scratch_free(&w);
     return n_out;
+}
+
+/* ------------------------------------------------------------ beam search */
+/* log-softmax of one row of logits (readings R26-R27):
+ * M = max_j l_j; Z = sum_j exp((double)l_j - M) in ascending j, fp64;
+ * lse = fl32(M + log Z); log p_j = fl32(l_j - lse). */
+float orc_logsumexp(const float *l, int n) {
+    float M = l[0];
+    for (int j = 1; j < n; ++j) if (l[j] > M) M = l[j];
+    double Z = 0.0;
+    for (int j = 0; j < n; ++j) Z += exp((double)l[j] - (double)M);
+    return (float)((double)M + log(Z));
+}
+
+typedef struct {
+    orc_dstate st;
+    int32_t *toks;     /* [max_len] emitted ids */
+    int len;
+    float score;       /* sum of fp32 log-probabilities (R27) */
+} orc_hyp;
+
+/* Candidate order (R28): score desc, then logit desc, then hypothesis rank asc,
+ * then id asc.  Returns 1 if candidate a ranks before b. */
+static int cand_before(float sa, float la, int ka, int ja, float sb, float lb, int kb, int jb) {
+    if (sa != sb) return sa > sb;
+    if (la != lb) return la > lb;
+    if (ka != kb) return ka < kb;
+    return ja < jb;
+}
+
+/* Beam search of ONE sentence with beam size b (the b=2 systems of
+ * Table 3 rows 6 and 12), in the plain textbook form:
+ *   - step 1 expands the start hypothesis; every later step expands each live
+ *     hypothesis k over log-softmax(logits) (R26);
+ *   - a candidate (k, j) scores fl32(score_k + log p_j) (R27); the top
+ *     b - (finished so far) candidates in the order of R28 are kept;
+ *   - a kept candidate with j = EOS is set aside as finished (EOS not emitted);
+ *     at t = max_len every kept candidate is finished;
+ *   - the search ends when no live hypothesis remains;
+ *   - the finished list is stably sorted by descending score (no length
+ *     normalization).
+ * Outputs up to b hypotheses: ids of hypothesis r at hyp_ids[r * max_len ...],
+ * hyp_len[r], hyp_score[r].  Returns their number (0 when max_len == 0) or <0. */
+int orc_beam_one(const orc_model *m, const int32_t *src, int S, int max_len, int b,
+                 int32_t *hyp_ids, int32_t *hyp_len, float *hyp_score) {
+    const orc_cfg *c = &m->c;
+    int d = c->d_model, L = c->dec_layers, V = c->vocab;
+    if (!m->quantized) return -4;
+    if (max_len < 0 || b < 1 || b > V) return -1;
+    for (int i = 0; i < S; ++i) if (src[i] < 0 || src[i] >= V) return -3;
+    if (max_len == 0) return 0;
+    float *kv = (float *)malloc(sizeof(float) * (size_t)L * 2 * (S > 0 ? S : 1) * d);
+    if (S > 0) orc_encode(m, src, S, NULL, kv);
+    orc_scratch w;
+    scratch_init(m, &w);
+    orc_hyp *live = (orc_hyp *)calloc((size_t)b, sizeof(orc_hyp));
+    orc_hyp *next = (orc_hyp *)calloc((size_t)b, sizeof(orc_hyp));
+    for (int k = 0; k < b; ++k) {
+        dstate_init(m, &live[k].st, max_len);
+        dstate_init(m, &next[k].st, max_len);
+        live[k].toks = (int32_t *)calloc((size_t)max_len, sizeof(int32_t));
+        next[k].toks = (int32_t *)calloc((size_t)max_len, sizeof(int32_t));
+    }
+    float *logits = (float *)malloc(sizeof(float) * (size_t)b * V);
+    float *cand = (float *)malloc(sizeof(float) * (size_t)b * V);
+    char *taken = (char *)malloc((size_t)b * V);
+    int n_live = 1, n_fin = 0;
+    live[0].len = 0;
+    live[0].score = 0.0f;
+    for (int t = 1; t <= max_len && n_live > 0; ++t) {
+        /* expand every live hypothesis: logits, log-softmax, candidate scores */
+        for (int k = 0; k < n_live; ++k) {
+            int in_id = t == 1 ? -1 : live[k].toks[live[k].len - 1];
+            dec_step(m, kv, S, &live[k].st, in_id, t, &w, NULL);
+            float *lk = logits + (int64_t)k * V;
+            out_logits(m, w.y, w.qy, lk);
+            float lse = orc_logsumexp(lk, V);
+            for (int j = 0; j < V; ++j) {
+                float lp = lk[j] - lse;
+                cand[(int64_t)k * V + j] = live[k].score + lp;
+            }
+        }
+        /* keep the best b - n_fin candidates, in rank order (repeated scans) */
+        int n_keep = b - n_fin, n_next = 0;
+        memset(taken, 0, (size_t)n_live * V);
+        for (int r = 0; r < n_keep; ++r) {
+            int bk = -1, bj = -1;
+            for (int k = 0; k < n_live; ++k)
+                for (int j = 0; j < V; ++j) {
+                    int64_t i = (int64_t)k * V + j;
+                    if (taken[i]) continue;
+                    if (bk < 0 || cand_before(cand[i], logits[i], k, j,
+                                              cand[(int64_t)bk * V + bj], logits[(int64_t)bk * V + bj], bk, bj)) {
+                        bk = k; bj = j;
+                    }
+                }
+            taken[(int64_t)bk * V + bj] = 1;
+            float sc = cand[(int64_t)bk * V + bj];
+            const orc_hyp *p = &live[bk];
+            if (bj == c->eos_id || t == max_len) {
+                int32_t *dst = hyp_ids + (int64_t)n_fin * max_len;
+                memcpy(dst, p->toks, sizeof(int32_t) * (size_t)p->len);
+                int len = p->len;
+                if (bj != c->eos_id) dst[len++] = bj;   /* EOS is not emitted (R16) */
+                hyp_len[n_fin] = len;
+                hyp_score[n_fin] = sc;
+                ++n_fin;
+            } else {
+                orc_hyp *q = &next[n_next++];
+                dstate_copy(m, &q->st, &p->st);
+                memcpy(q->toks, p->toks, sizeof(int32_t) * (size_t)p->len);
+                q->toks[p->len] = bj;
+                q->len = p->len + 1;
+                q->score = sc;
+            }
+        }
+        orc_hyp *tmp = live; live = next; next = tmp;
+        n_live = n_next;
+    }
+    /* stable insertion sort of the finished list by descending score */
+    for (int i = 1; i < n_fin; ++i) {
+        float sc = hyp_score[i];
+        int len = hyp_len[i];
+        int32_t *row = (int32_t *)malloc(sizeof(int32_t) * (size_t)max_len);
+        memcpy(row, hyp_ids + (int64_t)i * max_len, sizeof(int32_t) * (size_t)max_len);
+        int j = i - 1;
+        while (j >= 0 && hyp_score[j] < sc) {
+            hyp_score[j + 1] = hyp_score[j];
+            hyp_len[j + 1] = hyp_len[j];
+            memcpy(hyp_ids + (int64_t)(j + 1) * max_len, hyp_ids + (int64_t)j * max_len,
+                   sizeof(int32_t) * (size_t)max_len);
+            --j;
+        }
+        hyp_score[j + 1] = sc;
+        hyp_len[j + 1] = len;
+        memcpy(hyp_ids + (int64_t)(j + 1) * max_len, row, sizeof(int32_t) * (size_t)max_len);
+        free(row);
+    }
+    for (int k = 0; k < b; ++k) {
+        dstate_free(&live[k].st); dstate_free(&next[k].st);
+        free(live[k].toks); free(next[k].toks);
+    }
+    free(live); free(next); free(logits); free(cand); free(taken); free(kv);
+    scratch_free(&w);
+    return n_fin;
+}
+
+/* Beam search of n independent sentences (OpenMP over sentences, timing only).
+ * Sentence i's hypotheses occupy hyp_ids[b * out_off[i] + r * max_len[i] ...],
+ * hyp_len / hyp_score [i * b + r], n_hyp[i]; out_off = prefix sum of max_len. */
+int orc_beam_many(const orc_model *m, const int32_t *src_ids, const int64_t *src_off, int n,
+                  const int32_t *max_len, int b, int32_t *hyp_ids, int32_t *hyp_len,
+                  float *hyp_score, int32_t *n_hyp, int nthreads) {
+    int64_t *oo = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+    oo[0] = 0;
+    for (int i = 0; i < n; ++i) oo[i + 1] = oo[i] + max_len[i];
+    int err = 0;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1)
+#endif
+    for (int i = 0; i < n; ++i) {
+        int r = orc_beam_one(m, src_ids + src_off[i], (int)(src_off[i + 1] - src_off[i]), max_len[i],
+                             b, hyp_ids + (int64_t)b * oo[i], hyp_len + (int64_t)i * b,
+                             hyp_score + (int64_t)i * b);
+        if (r < 0) err = -r; else n_hyp[i] = r;
+    }
+    free(oo);
+    return err;
 }
 
 /* Decode n independent sentences (rows are independent: static scales,

@@ -72,6 +72,12 @@ def lib():
         L.orc_decode_one.argtypes = [P, P, C.c_int, C.c_int, P, P, C.POINTER(Trace)]
         L.orc_decode_many.restype = C.c_int
         L.orc_decode_many.argtypes = [P, P, P, C.c_int, P, P, P, C.c_int]
+        L.orc_beam_one.restype = C.c_int
+        L.orc_beam_one.argtypes = [P, P, C.c_int, C.c_int, C.c_int, P, P, P]
+        L.orc_beam_many.restype = C.c_int
+        L.orc_beam_many.argtypes = [P, P, P, C.c_int, P, C.c_int, P, P, P, P, C.c_int]
+        L.orc_logsumexp.restype = C.c_float
+        L.orc_logsumexp.argtypes = [P, C.c_int]
         L.orc_max_threads.restype = C.c_int
         L.orc_batch_by_words.restype = C.c_int
         L.orc_batch_by_words.argtypes = [P, C.c_int, C.c_int, P, P, P]
@@ -281,6 +287,42 @@ class OracleModel:
         ids = out[:n].copy()
         return (ids, res) if trace else ids
 
+    def beam_one(self, src: np.ndarray, max_len: int, beam: int):
+        """Beam search of one sentence (R26-R29).
+        Returns [(ids, score)] sorted by descending score (<= beam entries)."""
+        src = np.ascontiguousarray(src, dtype=np.int32)
+        T = max(int(max_len), 0)
+        ids = np.zeros(max(beam * T, 1), np.int32)
+        ln = np.zeros(beam, np.int32)
+        sc = np.zeros(beam, np.float32)
+        n = lib().orc_beam_one(self.h, _p(src), src.shape[0], T, int(beam), _p(ids), _p(ln), _p(sc))
+        if n < 0:
+            raise ValueError(f"oracle: beam status {-n}")
+        return [(ids[r * T:r * T + ln[r]].copy(), float(sc[r])) for r in range(n)]
+
+    def beam_many(self, sset, beam: int, nthreads: int = 0):
+        """Beam search of every sentence of a SentenceSet; list of n-best lists."""
+        n = sset.n
+        ml = np.ascontiguousarray(sset.max_len, dtype=np.int32)
+        ids = np.zeros(max(int(ml.sum()) * beam, 1), np.int32)
+        ln = np.zeros(max(n * beam, 1), np.int32)
+        sc = np.zeros(max(n * beam, 1), np.float32)
+        nh = np.zeros(max(n, 1), np.int32)
+        src = np.ascontiguousarray(sset.ids, dtype=np.int32)
+        offs = np.ascontiguousarray(sset.offsets, dtype=np.int64)
+        st = lib().orc_beam_many(self.h, _p(src), _p(offs), n, _p(ml), int(beam), _p(ids), _p(ln),
+                                 _p(sc), _p(nh), nthreads)
+        if st:
+            raise ValueError(f"oracle: beam_many status {st}")
+        res = []
+        o = 0
+        for i in range(n):
+            T = int(ml[i])
+            res.append([(ids[beam * o + r * T: beam * o + r * T + ln[i * beam + r]].copy(),
+                         float(sc[i * beam + r])) for r in range(nh[i])])
+            o += T
+        return res
+
     def decode_many(self, sset, nthreads: int = 0):
         """Free-running greedy decode of a SentenceSet; returns list of id arrays."""
         n = sset.n
@@ -299,6 +341,12 @@ class OracleModel:
             res.append(out[o:o + out_len[i]].copy())
             o += int(ml[i])
         return res
+
+
+def logsumexp(logits: np.ndarray) -> float:
+    """fl32(M + log sum_j exp(l_j - M)) of one row (reading R26)."""
+    l = np.ascontiguousarray(logits, dtype=np.float32)
+    return float(lib().orc_logsumexp(_p(l), l.size))
 
 
 def max_threads() -> int:
