@@ -119,6 +119,28 @@ mnmt_status mnmt_translate(mnmt_model* m, const int32_t* src_ids, const int64_t*
                            int32_t* out_ids, int64_t out_cap, int32_t* out_len, uint32_t flags,
                            void* cuda_stream);
 
+/* Beam search over the same word-budget batches as mnmt_translate: the
+ * b = 2 / 4 systems of Table 3 (rows 5, 6, 8, 9, 11, 12).  Per step,
+ * every live hypothesis is expanded over log-softmax(logits) (lse = fl32(M + log sum exp(l - M)),
+ * fp64 sum, R26); a candidate scores fl32(score + fl32(l_j - lse)) (R27); per sentence the best
+ * beam - (finished so far) candidates are kept in the order (score desc, logit desc, hypothesis
+ * rank asc, id asc) (R28); a kept EOS candidate is finished (EOS not emitted), and at step
+ * max_len[i] every kept candidate is; the search of a sentence ends when it has beam finished
+ * hypotheses.  No length normalisation.  Decoder state (AAN running sums, self-attention cache
+ * through per-position ancestor rows, R29) follows each hypothesis.
+ * beam: 1..8 (1 = greedy decoding through the log-softmax path; ids equal mnmt_translate's).
+ * Outputs, sentence i in INPUT order, O_i = sum_{k<i} max_len[k]:
+ *   hypothesis r (r < n_hyp[i], by descending score) at out_ids[beam * O_i + r * max_len[i] ...],
+ *   length out_len[i * beam + r], score out_score[i * beam + r] (fp32 sum of log-probabilities).
+ * n_hyp[i] = beam when max_len[i] >= 1, else 0.  out_cap >= beam * sum(max_len).
+ * flags & MNMT_DEVICE_IO: src_ids and every output are device pointers.
+ * Errors as mnmt_translate; MNMT_ERR_ARG for beam outside 1..8 or beam > vocab. */
+mnmt_status mnmt_beam_translate(mnmt_model* m, const int32_t* src_ids, const int64_t* src_off_host,
+                                int32_t n, const int32_t* max_len_host, int32_t word_budget,
+                                int32_t beam, int32_t* out_ids, int64_t out_cap, int32_t* out_len,
+                                float* out_score, int32_t* n_hyp, uint32_t flags,
+                                void* cuda_stream);
+
 /* Teacher-forced decode (test hook for the parity protocol):
  * sentence i runs T_i = forced_off[i+1] - forced_off[i] steps; the input at step
  * t >= 2 is forced_ids[forced_off[i] + t - 2]; argmax_ids[forced_off[i] + t - 1]

@@ -332,6 +332,81 @@ __device__ __forceinline__ void ln_epilogue(const GemmArgs& a, uint32_t t_row, i
   }
 }
 
+// EPI_TOPK (beam search, F1): one 32-column chunk at a time, the row's running maximum m,
+// the fp64 sum z = sum exp(v - m) (rescaled by exp(m_old - m_new) when a chunk raises m) and
+// the TOPK_MAX largest (v, column) in descending v, ascending column on ties (columns arrive
+// in ascending order and only a strictly larger value displaces an entry).
+template <int BN>
+__device__ __forceinline__ void topk_epilogue(const GemmArgs& args, const float* bsrc, uint32_t t_row,
+                                              int row, bool row_ok, int half, int n0) {
+  constexpr int HALF = BN / 2;
+  float tv[TOPK_MAX];
+  int tj[TOPK_MAX];
+#pragma unroll
+  for (int i = 0; i < TOPK_MAX; ++i) { tv[i] = -INFINITY; tj[i] = -1; }
+  float run_m = -INFINITY;
+  double z = 0.0;
+#pragma unroll 1
+  for (int c = 0; c < HALF; c += 32) {
+    int32_t acc[32];
+    tmem_ld16(t_row + c, *reinterpret_cast<int32_t(*)[16]>(acc));
+    tmem_ld16(t_row + c + 16, *reinterpret_cast<int32_t(*)[16]>(acc + 16));
+    tmem_ld_wait();
+    const int n = n0 + half * HALF + c;
+    if (n >= args.N) break;   // warp-uniform
+    const bool full = n + 32 <= args.N;
+    float v[32];
+    dequant32(args, bsrc, n, full && args.K <= 256, acc, v);
+    if (!full) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (n + j >= args.N) v[j] = -INFINITY;
+    }
+    float cm = v[0];
+#pragma unroll
+    for (int j = 1; j < 32; ++j) cm = fmaxf(cm, v[j]);
+    if (cm > run_m) {
+      if (run_m != -INFINITY) z = __dmul_rn(z, exp(__dsub_rn((double)run_m, (double)cm)));
+      run_m = cm;
+    }
+    const double md = (double)run_m;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) z = __dadd_rn(z, exp(__dsub_rn((double)v[j], md)));
+    if (cm > tv[TOPK_MAX - 1]) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (v[j] > tv[TOPK_MAX - 1]) {
+          float cv = v[j];
+          int cj = n + j;
+          bool sh = false;
+#pragma unroll
+          for (int i = 0; i < TOPK_MAX; ++i) {
+            const bool take = sh || cv > tv[i];
+            const float ov = tv[i];
+            const int oj = tj[i];
+            tv[i] = take ? cv : ov;
+            tj[i] = take ? cj : oj;
+            cv = take ? ov : cv;
+            cj = take ? oj : cj;
+            sh = take;
+          }
+        }
+      }
+    }
+  }
+  if (row_ok) {
+    TopkPart* p = args.part + (int64_t)row * args.part_ld + blockIdx.x * 2 + half;
+    p->m = run_m;
+    p->pad = 0;
+    p->z = z;
+#pragma unroll
+    for (int i = 0; i < TOPK_MAX; ++i) {
+      p->v[i] = tv[i];
+      p->j[i] = tj[i];
+    }
+  }
+}
+
 template <int BN, int EPI>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_gemm_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -470,6 +545,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int best_j = -1;
     if constexpr (EPI == EPI_LN) {
       ln_epilogue<BN>(args, t_row, row, row_ok, half, q * 32 + lane, ln_part);
+    } else if constexpr (EPI == EPI_TOPK) {
+      topk_epilogue<BN>(args, args.bias ? bias_s - n0 : nullptr, t_row, row, row_ok, half, n0);
     } else
 #pragma unroll 1
     for (int c = 0; c < HALF; c += 32) {
@@ -1064,6 +1141,9 @@ static cudaError_t gemm_init_all() {
   if ((e = set_attr_bn<64>()) != cudaSuccess) return e;
   if ((e = set_attr_bn<128>()) != cudaSuccess) return e;
   if ((e = set_attr_ln()) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_gemm_i8<TOPK_BN, EPI_TOPK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                GemmCfg<TOPK_BN>::smem_for(GemmCfg<TOPK_BN>::STAGES))) != cudaSuccess)
+    return e;
   return set_attr_bn<256>();
 }
 
@@ -1140,6 +1220,10 @@ cudaError_t launch_gemm_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const
       case 128: return launch_lnc<128>(tmA, tmB, a, st);
     }
     return cudaErrorInvalidValue;
+  }
+  if (epi == EPI_TOPK) {   // fixed tile (the partial layout depends on it), never persistent
+    if (a.part_ld < 2 * ((a.N + TOPK_BN - 1) / TOPK_BN)) return cudaErrorInvalidValue;
+    return launch_np<TOPK_BN, EPI_TOPK>(tmA, tmB, a, st);
   }
   if (epi == EPI_LN) {   // one CTA owns whole rows: BN = N = d
     if (a.N == 192) return launch_np<192, EPI_LN>(tmA, tmB, a, st);

@@ -20,6 +20,20 @@ enum Epi : int {
   EPI_LN = 7,         // full rows (BN = N = d): v = GEMM output; r = x + v (or the AAN gate
                       // form with v = f-gate logit); out = LN(r), Q(out), next-layer AAN step
   EPI_LNC = 8,        // as EPI_LN, rows owned by a cluster of N / BN CTAs (gemm_lnc_bn)
+  EPI_TOPK = 9,       // beam search (F1): per (row, N-tile half) the running max m, the fp64
+                      // sum z = sum exp(v - m) and the TOPK_MAX largest (v, col) -> part[]
+};
+
+// Beam-search partial of one row over one half of one N tile (EPI_TOPK).  v sorted by
+// descending value, ties by ascending column; unused entries v = -inf, j = -1.
+constexpr int TOPK_MAX = 8;
+constexpr int TOPK_BN = 256;   // N tile of the EPI_TOPK launch: 2 partials per tile
+struct __align__(16) TopkPart {
+  float m;          // max v of the range (-inf: empty)
+  int32_t pad;
+  double z;         // sum over the range of exp((double)v - m)
+  float v[TOPK_MAX];
+  int32_t j[TOPK_MAX];
 };
 
 struct GemmArgs {
@@ -39,6 +53,8 @@ struct GemmArgs {
   int pers_grid;               // persistent variant: CTA cap (0 = one per SM)
   unsigned long long* trace;   // debug: CTA (0,0) %globaltimer stamps [9] (null = off)
   LnArgs ln;                   // EPI_LN: residual / gate inputs, gamma, beta, outputs, AAN
+  TopkPart* part;              // EPI_TOPK: [rows][part_ld] partials (part_ld >= 2 * N tiles)
+  int part_ld;
 };
 
 // Tensor map over a row-major int8 matrix [rows x K] (K contiguous, K % 16 == 0):

@@ -22,6 +22,7 @@
 
 #include "../../include/mnmt.h"
 #include "../../include/mnmt_ops.h"
+#include "beam.h"
 #include "kernels.h"
 #include "rowops.h"
 #include "rowfused.h"
@@ -95,6 +96,15 @@ struct Workspace {
   int8_t *cy = nullptr, *cg = nullptr, *ch1 = nullptr, *ca = nullptr, *cx1 = nullptr;
   int8_t *cctxd = nullptr, *cx2 = nullptr, *chd = nullptr;
   CUtensorMap tm_cy, tm_cg, tm_ch1, tm_ca, tm_cx1, tm_cctxd, tm_cx2, tm_chd;
+  // beam search (F1; allocated on first use by beam_ensure, sized B_cap x T_cap)
+  std::vector<void*> beam_allocs;
+  int64_t beam_rows = 0, beam_T = 0;
+  TopkPart* part = nullptr;
+  int part_ld = 0;
+  float *row_lse = nullptr, *row_v = nullptr, *hscore = nullptr, *child_score = nullptr;
+  int32_t *row_j = nullptr, *sent_row0 = nullptr, *sent_nlive = nullptr, *sent_nfin = nullptr;
+  int32_t *sent_list = nullptr, *child_par = nullptr, *child_tok = nullptr, *hist = nullptr;
+  int32_t* anc = nullptr;
 };
 
 // Job-level device buffers shared by all lanes.
@@ -107,6 +117,8 @@ struct JobBuf {
   int32_t* meta = nullptr;      // token metadata of all batches: idx|pos|start|len per batch
   int32_t* rmeta32 = nullptr;   // row metadata of all batches: [start|len|max_len|len_idx|order] x B_b
   int64_t* rmeta64 = nullptr;   // [out_off|forced_off] x B_b
+  float* out_score = nullptr;   // beam search: [n x beam] hypothesis scores
+  int32_t* n_hyp = nullptr;     // beam search: [n] hypotheses per sentence
 };
 
 // A lane = one independent decoder (workspace + stream + step graphs).  Rows are
@@ -172,6 +184,7 @@ struct mnmt_model {
   int cur_pers_grid = 0;               // (launch state) persistent-GEMM CTA cap of the lane being issued
   int lane_tiers = 0;                  // option: 0 = deal sentences round-robin to lanes;
                                        // p*10 = contiguous length tiers of equal sum S^p
+  int beam = 0;                        // (call state) beam size of the running call; 0 = greedy
 };
 
 namespace {
@@ -325,6 +338,7 @@ static void lane_free(Lane& L) {
   for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
   L.graphs.clear();
   for (void* p : L.ws.allocs) cudaFree(p);
+  for (void* p : L.ws.beam_allocs) cudaFree(p);
   L.ws = Workspace();
   if (L.d_phases) cudaFree(L.d_phases);
   if (L.d_tmaps) cudaFree(L.d_tmaps);
@@ -481,7 +495,82 @@ static mnmt_status jb_ensure(mnmt_model* m, int64_t O, int64_t N, int64_t tok, i
   CKS(dalloc(z.allocs, &z.meta, mc));
   CKS(dalloc(z.allocs, &z.rmeta32, 5 * rc));
   CKS(dalloc(z.allocs, &z.rmeta64, 2 * rc));
+  CKS(dalloc(z.allocs, &z.out_score, Nc));
+  CKS(dalloc(z.allocs, &z.n_hyp, Nc));
   return MNMT_OK;
+}
+
+// Beam-search buffers of a lane (F1): TOPK partials and per-row / per-slot / per-sentence
+// state for the lane's B_cap rows and T_cap steps.
+static mnmt_status beam_ensure(mnmt_model* m, Lane& Ln) {
+  Workspace& w = Ln.ws;
+  if (w.beam_rows >= w.B_cap && w.beam_T >= w.T_cap) return MNMT_OK;
+  CK(cudaDeviceSynchronize());
+  for (void* p : w.beam_allocs) cudaFree(p);
+  w.beam_allocs.clear();
+  for (auto& kv : Ln.graphs) cudaGraphExecDestroy(kv.second);
+  Ln.graphs.clear();
+  const int64_t R = w.B_cap, T = w.T_cap;
+  auto& A = w.beam_allocs;
+  w.part_ld = 2 * ((m->c.vocab + TOPK_BN - 1) / TOPK_BN);
+  CKS(dalloc(A, &w.part, R * w.part_ld));
+  CKS(dalloc(A, &w.row_lse, R));
+  CKS(dalloc(A, &w.row_v, R * TOPK_MAX));
+  CKS(dalloc(A, &w.row_j, R * TOPK_MAX));
+  for (int32_t** p : {&w.sent_row0, &w.sent_nlive, &w.sent_nfin, &w.sent_list, &w.child_par,
+                      &w.child_tok})
+    CKS(dalloc(A, p, R));
+  CKS(dalloc(A, &w.hscore, R));
+  CKS(dalloc(A, &w.child_score, R));
+  CKS(dalloc(A, &w.hist, R * T));
+  if (m->c.decoder == 0) CKS(dalloc(A, &w.anc, R * T));
+  w.beam_rows = R;
+  w.beam_T = T;
+  return MNMT_OK;
+}
+
+static BeamArgs beam_args(mnmt_model* m, Lane& Ln, int n) {
+  auto& w = Ln.ws;
+  BeamArgs b{};
+  b.beam = m->beam;
+  b.n = n;
+  b.ctrl = w.ctrl;
+  b.live = w.live;
+  b.prev_live = w.prev_live;
+  b.live_start = w.live_start;
+  b.live_len = w.live_len;
+  b.row_start = w.row_start;
+  b.row_len = w.row_len;
+  b.max_len = w.max_len;
+  b.out_off = w.out_off;
+  b.len_idx = w.len_idx;
+  b.eos = m->c.eos_id;
+  b.part = w.part;
+  b.part_ld = w.part_ld;
+  b.n_part = 2 * ((m->c.vocab + TOPK_BN - 1) / TOPK_BN);
+  b.row_lse = w.row_lse;
+  b.row_v = w.row_v;
+  b.row_j = w.row_j;
+  b.sent_row0 = w.sent_row0;
+  b.sent_nlive = w.sent_nlive;
+  b.sent_nfin = w.sent_nfin;
+  b.sent_list = w.sent_list;
+  b.hscore = w.hscore;
+  b.child_par = w.child_par;
+  b.child_tok = w.child_tok;
+  b.child_score = w.child_score;
+  b.hist = w.hist;
+  b.anc = w.anc;
+  b.t_cap = (int)w.T_cap;
+  b.C = m->c.decoder == 1 ? w.C : nullptr;
+  b.c_stride = w.B_cap * m->c.d_model;
+  b.L = m->c.dec_layers;
+  b.d = m->c.d_model;
+  b.out_ids = m->jb.out_ids;
+  b.out_len = m->jb.out_len;
+  b.out_score = m->jb.out_score;
+  b.n_hyp = m->jb.n_hyp;
+  return b;
 }
 
 // Grows a lane's workspace to hold M tokens, B rows, T steps, O forced ids.
@@ -707,7 +796,7 @@ static bool rowfuse_active(const mnmt_model* m, int n) {
   const auto& c = m->c;
   const int d = c.d_model, H = c.n_heads, dh = d / H;
   const int nt = std::max(d, 32 * H);
-  return m->rowfuse > 0 && n <= m->rowfuse && d % 32 == 0 && nt <= 1024 && dh <= 64 && dh % 4 == 0;
+  return m->beam == 0 && m->rowfuse > 0 && n <= m->rowfuse && d % 32 == 0 && nt <= 1024 && dh <= 64 && dh % 4 == 0;
 }
 
 // One decoder step for up to `n` live rows (A5-A10).  Returns kernels launched via *nlaunch.
@@ -834,6 +923,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
         at.k_off = 0;
         at.v_off = d;
         at.t_cap = (int)w.T_cap;
+        at.anc = m->beam > 0 ? w.anc : nullptr;
         at.clip = c.clip;
         at.sigma = sigma_of(m);
         at.out_q = w.cctxd;
@@ -926,6 +1016,30 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
       k += 3;
     }
     if (hook && (e = hook->layer(m, l)) != cudaSuccess) return e;
+  }
+  if (m->beam > 0) {
+    // beam search (F1): output GEMM with per-tile log-sum-exp partials and top-k (EPI_TOPK),
+    // then row merge, per-sentence selection + compaction, state reorder (beam.h)
+    GemmArgs a{};
+    a.M = n;
+    a.M_dyn = nd;
+    a.N = c.vocab;
+    a.K = d;
+    a.scale = scale_of(m);
+    a.bias = c.out_bias ? m->out_b : nullptr;
+    a.clip = c.clip;
+    a.sigma = sigma_of(m);
+    a.col_block = c.vocab;
+    a.part = w.part;
+    a.part_ld = w.part_ld;
+    if ((e = launch_gemm_i8(w.tm_cy, m->tmE, a, EPI_TOPK, 0, st)) != cudaSuccess) return e;
+    const BeamArgs ba = beam_args(m, Ln, n);
+    if ((e = launch_beam_rows(ba, st)) != cudaSuccess) return e;
+    if ((e = launch_beam_select(ba, st)) != cudaSuccess) return e;
+    if ((e = launch_beam_reorder(ba, st)) != cudaSuccess) return e;
+    k += 4;
+    *nlaunch += k;
+    return cudaSuccess;
   }
   // A9: tied output projection fused with the argmax (softmax skipped)
   {
@@ -1408,8 +1522,12 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
                       &launches));
     if (c.decoder == 1)
       CK(cudaMemsetAsync(w.C, 0, (size_t)c.dec_layers * w.B_cap * d * sizeof(float), st));
-    CK(launch_decode_init(w.ctrl, w.live, B, w.keys, w.row_start, w.row_len, w.live_start,
-                          w.live_len, st));
+    if (m->beam > 0) {
+      CK(launch_beam_init(beam_args(m, Ln, B), B, st));
+    } else {
+      CK(launch_decode_init(w.ctrl, w.live, B, w.keys, w.row_start, w.row_len, w.live_start,
+                            w.live_len, st));
+    }
     launches += 1;
     const int npad = (B + 127) / 128 * 128;
     // attention scratch is sized by the longest span a step can attend (source length, or the
@@ -1427,11 +1545,12 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
     // max_len, so step t needs at most alive[t-1] rows -> the smallest cached graph that fits
     // (with rowfuse: multiples of 16 below 128 rows, so the fused blocks can key on the row count;
     // otherwise 128, measured 0.5 % faster)
+    const int rows_per = std::max(1, m->beam);   // beam search: up to beam rows per sentence
     auto pad_at = [&](int t) {
-      const int a = b.alive[t];
+      const int a = b.alive[t] * rows_per;
       return (a < 128 && m->rowfuse > 0) ? std::max(16, (a + 15) / 16 * 16) : (a + 127) / 128 * 128;
     };
-    if (m->megakernel && (!hook || hook->megakernel_ok())) {
+    if (m->megakernel && m->beam == 0 && (!hook || hook->megakernel_ok())) {
       if (!Ln.d_phases || Ln.prog_forced != forced || Ln.prog_out != m->jb.out_ids)
         CKS(build_program(m, Ln, forced));
       StepArgs sa{};
@@ -1467,7 +1586,7 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
       const int K = std::max(1, m->steps_per_graph);
       for (int t = 0; t < b.T;) {
         const int np = pad_at(t), k = std::min(K, b.T - t);
-        const int64_t key = (int64_t)np * 64 + k;
+        const int64_t key = ((int64_t)np * 64 + k) * 16 + m->beam;
         auto it = Ln.graphs.find(key);
         if (it == Ln.graphs.end()) {
           cudaGraph_t g;
@@ -1492,7 +1611,12 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
         t += k;
       }
     } else {
-      for (int t = 0; t < b.T; ++t) CK(launch_step(m, Ln, npad, forced, hook, &launches));
+      const int nrows = (B * rows_per + 127) / 128 * 128;
+      for (int t = 0; t < b.T; ++t) CK(launch_step(m, Ln, nrows, forced, hook, &launches));
+    }
+    if (m->beam > 0) {
+      CK(launch_beam_final(beam_args(m, Ln, B), B, st));
+      launches += 1;
     }
     steps += b.T;
   }
@@ -1513,7 +1637,9 @@ static mnmt_status ensure_lanes(mnmt_model* m, const Job& job, int64_t forced_O)
   for (size_t li = 0; li < job.lane_M.size(); ++li) {
     if (job.lane_B[li] == 0) continue;
     CKS(lane_init(m, m->lanes[li], (int)li));
-    CKS(lane_ensure(m, m->lanes[li], job.lane_M[li], job.lane_B[li], job.lane_T[li], forced_O));
+    CKS(lane_ensure(m, m->lanes[li], job.lane_M[li], job.lane_B[li] * std::max(1, m->beam),
+                    job.lane_T[li], forced_O));
+    if (m->beam > 0) CKS(beam_ensure(m, m->lanes[li]));
   }
   return MNMT_OK;
 }
@@ -1741,13 +1867,21 @@ mnmt_status mnmt_batch_by_words(const int32_t* len, int32_t n, int32_t budget, i
 static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const int64_t* src_off,
                                   int32_t n, const int32_t* max_len, int32_t budget,
                                   bool sorted_batches, int32_t* out_ids, int64_t out_cap,
-                                  int32_t* out_len, uint32_t flags, void* cuda_stream) {
+                                  int32_t* out_len, uint32_t flags, void* cuda_stream,
+                                  int32_t beam = 0, float* out_score = nullptr,
+                                  int32_t* n_hyp = nullptr) {
   if (!m) { set_err("NULL model"); return MNMT_ERR_ARG; }
   mnmt_status s;
   if ((s = check_inputs(m, src_off, n, max_len)) != MNMT_OK) return s;
+  if (beam < 0 || beam > TOPK_MAX || beam > m->c.vocab) {
+    set_err("beam must be in 1..%d (and <= vocab)", TOPK_MAX);
+    return MNMT_ERR_ARG;
+  }
+  if (beam > 0 && n > 0 && (!out_score || !n_hyp)) { set_err("NULL beam outputs"); return MNMT_ERR_ARG; }
   const bool dev_io = (flags & MNMT_DEVICE_IO) != 0;
+  const int64_t bm = std::max(1, beam);   // output slots per sentence
   int64_t O = 0, ntok = n > 0 ? src_off[n] : 0;
-  for (int i = 0; i < n; ++i) O += max_len[i];
+  for (int i = 0; i < n; ++i) O += max_len[i] * bm;
   if (out_cap < O) { set_err("out_cap %lld < sum(max_len) %lld", (long long)out_cap, (long long)O); return MNMT_ERR_CAPACITY; }
   if (n > 0 && (!src_ids && ntok > 0)) { set_err("NULL src_ids"); return MNMT_ERR_ARG; }
   if (n > 0 && (!out_len || (!out_ids && O > 0))) { set_err("NULL outputs"); return MNMT_ERR_ARG; }
@@ -1814,9 +1948,14 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
   Job job;
   plan_job(src_off, n, max_len, rows, lanes_of, (int)m->lanes.size(), job);
   plan_rows(job, src_off, max_len, false, nullptr);
-  if ((s = jb_ensure(m, std::max<int64_t>(O, 1), std::max(n, 1), std::max<int64_t>(ntok, 1),
-                     (int64_t)job.meta.size(), job.rows_total)) != MNMT_OK)
+  if ((s = jb_ensure(m, std::max<int64_t>(O, 1), std::max<int64_t>((int64_t)n * bm, 1),
+                     std::max<int64_t>(ntok, 1), (int64_t)job.meta.size(), job.rows_total)) != MNMT_OK)
     return fail(m, s);
+  m->beam = beam;
+  struct BeamReset {
+    mnmt_model* m;
+    ~BeamReset() { m->beam = 0; }
+  } beam_reset{m};
   if ((s = ensure_lanes(m, job, 1)) != MNMT_OK) return fail(m, s);
   auto& w = m->jb;
   if ((s = upload_job(m, job)) != MNMT_OK) return fail(m, s);
@@ -1834,17 +1973,28 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
     CK(cudaStreamSynchronize(m->st));
     if (hbad) { set_err("%d source ids out of range", hbad); return MNMT_ERR_VOCAB; }
   }
-  CK(cudaMemsetAsync(w.out_len, 0, (size_t)n * 4, m->st));
+  CK(cudaMemsetAsync(w.out_len, 0, (size_t)n * bm * 4, m->st));
+  if (beam > 0) {
+    CK(cudaMemsetAsync(w.n_hyp, 0, (size_t)n * 4, m->st));
+    CK(cudaMemsetAsync(w.out_score, 0, (size_t)n * bm * 4, m->st));
+  }
   if ((s = run_job(m, job, false, nullptr, true)) != MNMT_OK) return fail(m, s);
-  if (O > 0)
-    CK(cudaMemcpyAsync(out_ids, w.out_ids, O * 4, dev_io ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, m->st));
-  if (n > 0)
-    CK(cudaMemcpyAsync(out_len, w.out_len, (size_t)n * 4, dev_io ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, m->st));
-  if (!dev_io) m->stats.d2h_bytes += O * 4 + (int64_t)n * 4;
+  const cudaMemcpyKind dk = dev_io ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (O > 0) CK(cudaMemcpyAsync(out_ids, w.out_ids, O * 4, dk, m->st));
+  if (n > 0) CK(cudaMemcpyAsync(out_len, w.out_len, (size_t)n * bm * 4, dk, m->st));
+  if (beam > 0 && n > 0) {
+    CK(cudaMemcpyAsync(out_score, w.out_score, (size_t)n * bm * 4, dk, m->st));
+    CK(cudaMemcpyAsync(n_hyp, w.n_hyp, (size_t)n * 4, dk, m->st));
+  }
+  if (!dev_io) m->stats.d2h_bytes += O * 4 + (int64_t)n * bm * 4 + (beam > 0 ? (int64_t)n * (bm + 1) * 4 : 0);
   if ((s = end_call(m, cuda_stream)) != MNMT_OK) return fail(m, s);
   if (!dev_io) {
     int64_t words = 0;
-    for (int i = 0; i < n; ++i) words += out_len[i];
+    if (beam > 0) {
+      for (int i = 0; i < n; ++i) words += n_hyp[i] > 0 ? out_len[(int64_t)i * bm] : 0;   // best hypothesis
+    } else {
+      for (int i = 0; i < n; ++i) words += out_len[i];
+    }
     m->stats.target_words = words;
   }
   return MNMT_OK;
@@ -1863,6 +2013,17 @@ mnmt_status mnmt_translate(mnmt_model* m, const int32_t* src_ids, const int64_t*
   if (budget < 1) { set_err("word_budget < 1"); return MNMT_ERR_ARG; }
   return translate_impl(m, src_ids, src_off, n, max_len, budget, true, out_ids, out_cap, out_len,
                         flags, cuda_stream);
+}
+
+mnmt_status mnmt_beam_translate(mnmt_model* m, const int32_t* src_ids, const int64_t* src_off,
+                                int32_t n, const int32_t* max_len, int32_t word_budget,
+                                int32_t beam, int32_t* out_ids, int64_t out_cap, int32_t* out_len,
+                                float* out_score, int32_t* n_hyp, uint32_t flags,
+                                void* cuda_stream) {
+  if (word_budget < 1) { set_err("word_budget < 1"); return MNMT_ERR_ARG; }
+  if (beam < 1) { set_err("beam < 1"); return MNMT_ERR_ARG; }
+  return translate_impl(m, src_ids, src_off, n, max_len, word_budget, true, out_ids, out_cap,
+                        out_len, flags, cuda_stream, beam, out_score, n_hyp);
 }
 
 }  // extern "C"

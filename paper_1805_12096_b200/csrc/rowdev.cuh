@@ -160,10 +160,13 @@ __device__ __forceinline__ double to_f64(double x) { return x; }
 // KT = float: K/V rows in global memory (each element converted once, when used);
 // KT = double: K/V already converted (staged in shared memory by the caller).
 // qd: per-warp scratch of dh doubles (the query converted once).
-template <typename KT>
+// IND: rows[j] is the row of position j (beam search: the self-attention cache rows of a
+// hypothesis' ancestors, R29); otherwise position j is row j.
+template <typename KT, bool IND = false>
 __device__ __forceinline__ void warp_attend(const float* __restrict__ q, const KT* k, const KT* v,
                                             int64_t ld, int len, int dh, double* sc, double* qd,
-                                            float clip, float sigma, int8_t* out_q, float* out_f) {
+                                            float clip, float sigma, int8_t* out_q, float* out_f,
+                                            const int32_t* rows = nullptr) {
   const int lane = threadIdx.x & 31;
   if constexpr (sizeof(KT) == 8) {   // reused K/V: convert the query once as well
     for (int c = lane; c < dh; c += 32) qd[c] = (double)q[c];
@@ -172,7 +175,7 @@ __device__ __forceinline__ void warp_attend(const float* __restrict__ q, const K
   const double inv_sqrt = 1.0 / sqrt((double)dh);
   double mx = -INFINITY;
   for (int j = lane; j < len; j += 32) {
-    const KT* kr = k + (int64_t)j * ld;
+    const KT* kr = k + (int64_t)(IND ? rows[j] : j) * ld;
     double dot = 0.0;
     for (int c = 0; c < dh; c += 4) {
       double kk[4], qq[4];
@@ -205,6 +208,17 @@ __device__ __forceinline__ void warp_attend(const float* __restrict__ q, const K
   }
   z = warp_sum_f64(z);
   __syncwarp();
+  if constexpr (IND) {
+    for (int c = lane; c < dh; c += 32) {
+      double acc = 0.0;
+      for (int j = 0; j < len; ++j) acc = __fma_rn(sc[j], to_f64(v[(int64_t)rows[j] * ld + c]), acc);
+      const float ctx = len > 0 ? (float)__ddiv_rn(acc, z) : 0.0f;
+      out_q[c] = (int8_t)q8(ctx, clip, sigma);
+      if (out_f) out_f[c] = ctx;
+    }
+    __syncwarp();
+    return;
+  }
   for (int c = lane; c < dh; c += 32) {
     double acc = 0.0;
     int j = 0;
@@ -255,6 +269,17 @@ __device__ __forceinline__ void attn_row_head(const AttnArgs a, int r, int h, do
     for (int c = lane; c < dh; c += 32) {
       dst[a.k_off + c] = q[a.d + c];        // k at qkv columns [d, 2d)
       dst[a.v_off + c] = q[2 * a.d + c];    // v at qkv columns [2d, 3d)
+    }
+    if (a.anc) {
+      // beam search (R29): positions 0..t-2 live in the rows of the hypothesis' ancestors,
+      // position t-1 in its own slot's row (written above)
+      int32_t* rows = a.anc + (int64_t)orig * a.t_cap;
+      if (lane == 0) rows[t - 1] = start + t - 1;
+      __syncwarp();
+      warp_attend<float, true>(q, a.kv + a.k_off + h * dh, a.kv + a.v_off + h * dh, a.ldkv, len, dh,
+                               sc, sc + span, a.clip, a.sigma, a.out_q + (int64_t)r * a.d + h * dh,
+                               a.out_f ? a.out_f + (int64_t)r * a.d + h * dh : nullptr, rows);
+      return;
     }
     __syncwarp();
   }

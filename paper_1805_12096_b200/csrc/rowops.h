@@ -71,6 +71,7 @@ struct AttnArgs {
   const int32_t* live_start;   // optional (src): kv_start / kv_len in compact row order
   const int32_t* live_len;
   int t_cap;                // self mode: cache rows per sentence
+  int32_t* anc;             // self mode, beam search: [slot][t_cap] cache row of each position (R29)
   float clip, sigma;
   int8_t* out_q;            // Q(ctx) [n x d]
   float* out_f;             // optional fp32 ctx (tests)

@@ -47,7 +47,8 @@ class Stats(C.Structure):
 
 EXPORTS = [
     "mnmt_config_default", "mnmt_model_create", "mnmt_model_set_param", "mnmt_model_quantize",
-    "mnmt_batch_by_words", "mnmt_decode", "mnmt_translate", "mnmt_decode_forced",
+    "mnmt_batch_by_words", "mnmt_decode", "mnmt_translate", "mnmt_beam_translate",
+    "mnmt_decode_forced",
     "mnmt_get_stats", "mnmt_last_error", "mnmt_model_destroy", "mnmt_model_set_option",
     "mnmt_op_quantize", "mnmt_op_gemm_i8", "mnmt_op_argmax_ids", "mnmt_op_layernorm",
     "mnmt_op_aan_step", "mnmt_op_embed", "mnmt_op_attention", "mnmt_debug_phase_profile",
@@ -74,6 +75,7 @@ def lib():
     L.mnmt_batch_by_words.argtypes = [P, I32, I32, P, P, P]
     L.mnmt_decode.argtypes = [P, P, P, I32, P, P, I64, P, P]
     L.mnmt_translate.argtypes = [P, P, P, I32, P, I32, P, I64, P, C.c_uint32, P]
+    L.mnmt_beam_translate.argtypes = [P, P, P, I32, P, I32, I32, P, I64, P, P, P, C.c_uint32, P]
     L.mnmt_decode_forced.argtypes = [P, P, P, I32, P, P, P, C.c_uint32, P, I64, P]
     L.mnmt_get_stats.argtypes = [P, C.POINTER(Stats)]
     L.mnmt_model_set_option.argtypes = [P, C.c_char_p, I64]
@@ -216,6 +218,39 @@ class Model:
         _check(lib().mnmt_translate(self.h, _p(ids), _p(offs), n, _p(ml), budget, _p(out),
                                     out.size, _p(out_len), 0, _stream_ptr(stream)))
         return self._split(out, out_len, ml)
+
+    def beam_translate(self, sset, budget: int, beam: int, stream=None):
+        """Beam search of the whole job (host buffers; include/mnmt.h mnmt_beam_translate).
+        Returns, per sentence in input order, [(ids, score)] by descending score."""
+        n = sset.n
+        ml = np.ascontiguousarray(sset.max_len, np.int32)
+        out = np.zeros(max(int(ml.sum()) * beam, 1), np.int32)
+        out_len = np.zeros(max(n * beam, 1), np.int32)
+        out_score = np.zeros(max(n * beam, 1), np.float32)
+        n_hyp = np.zeros(max(n, 1), np.int32)
+        ids = np.ascontiguousarray(sset.ids, np.int32)
+        offs = np.ascontiguousarray(sset.offsets, np.int64)
+        _check(lib().mnmt_beam_translate(self.h, _p(ids), _p(offs), n, _p(ml), budget, beam,
+                                         _p(out), out.size, _p(out_len), _p(out_score), _p(n_hyp),
+                                         0, _stream_ptr(stream)))
+        res, o = [], 0
+        for i in range(n):
+            T = int(ml[i])
+            res.append([(out[beam * o + r * T: beam * o + r * T + out_len[i * beam + r]].copy(),
+                         float(out_score[i * beam + r])) for r in range(n_hyp[i])])
+            o += T
+        return res
+
+    def beam_translate_device(self, ids_ptr: int, offsets: np.ndarray, max_len: np.ndarray,
+                              budget: int, beam: int, out_ptr: int, out_cap: int,
+                              out_len_ptr: int, out_score_ptr: int, n_hyp_ptr: int,
+                              stream=None) -> None:
+        """Beam search with ids and outputs resident in HBM (MNMT_DEVICE_IO)."""
+        offs = np.ascontiguousarray(offsets, np.int64)
+        ml = np.ascontiguousarray(max_len, np.int32)
+        _check(lib().mnmt_beam_translate(self.h, ids_ptr, _p(offs), len(ml), _p(ml), budget, beam,
+                                         out_ptr, out_cap, out_len_ptr, out_score_ptr, n_hyp_ptr,
+                                         DEVICE_IO, _stream_ptr(stream)))
 
     def translate_device(self, ids_ptr: int, offsets: np.ndarray, max_len: np.ndarray,
                          budget: int, out_ptr: int, out_cap: int, out_len_ptr: int,
