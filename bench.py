@@ -104,7 +104,14 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- oracle legs
-def oracle_sample(sset, dims, weights, seconds: float, seed: int = 99):
+def _oracle_run(om, subset, beam):
+    """Target words of one oracle pass (beam > 1: words of each sentence's best hypothesis)."""
+    if beam > 1:
+        return sum(len(h[0][0]) if h else 0 for h in om.beam_many(subset, beam, 0))
+    return sum(len(o) for o in om.decode_many(subset, 0))
+
+
+def oracle_sample(sset, dims, weights, seconds: float, seed: int = 99, beam: int = 1):
     """Decode a seeded random sample of the workload with the oracle, sized to ~`seconds`.
     Returns (target words/s, threads, description)."""
     import oracle.oracle as O
@@ -114,18 +121,17 @@ def oracle_sample(sset, dims, weights, seconds: float, seed: int = 99):
     perm = rng.permutation(sset.n)
     probe = sset.subset(perm[:max(threads, 8)])
     t0 = time.perf_counter()
-    out = om.decode_many(probe, 0)
+    w_probe = _oracle_run(om, probe, beam)
     dt = time.perf_counter() - t0
-    w_probe = sum(len(o) for o in out)
     rate = w_probe / max(dt, 1e-9)
     mean_len = float(np.mean(probe.max_len))
     n = int(min(sset.n, max(len(probe.max_len), rate * seconds / max(mean_len, 1.0))))
     samp = sset.subset(perm[:n])
     t0 = time.perf_counter()
-    out = om.decode_many(samp, 0)
+    words = _oracle_run(om, samp, beam)
     dt = time.perf_counter() - t0
-    words = sum(len(o) for o in out)
-    desc = (f"oracle greedy decode of {n} of {sset.n} sentences (seeded random sample, "
+    mode = "greedy" if beam <= 1 else f"beam-{beam}"
+    desc = (f"oracle {mode} decode of {n} of {sset.n} sentences (seeded random sample, "
             f"{int(samp.lengths.sum())} source / {words} target words, one batch per sentence, "
             f"OpenMP over sentences) in {dt:.1f} s")
     return words / dt, threads, desc, dt
@@ -142,22 +148,21 @@ def run_reference(args, dims, weights, sset, workload_cfg):
     # size one step to ~8 s of CPU work
     probe = sset.subset(perm[:max(threads, 8)])
     t0 = time.perf_counter()
-    out = om.decode_many(probe, 0)
-    rate = sum(len(o) for o in out) / max(time.perf_counter() - t0, 1e-9)
+    rate = _oracle_run(om, probe, args.beam) / max(time.perf_counter() - t0, 1e-9)
     n = int(min(sset.n, max(len(probe.max_len), rate * 8.0 / max(float(np.mean(probe.max_len)), 1.0))))
     samp = sset.subset(perm[:n])
     for _ in range(args.warmup):
-        om.decode_many(samp, 0)
+        _oracle_run(om, samp, args.beam)
     t0 = time.perf_counter()
     words = 0
     for _ in range(args.steps):
-        words += sum(len(o) for o in om.decode_many(samp, 0))
+        words += _oracle_run(om, samp, args.beam)
     dt = time.perf_counter() - t0
     value = words / dt
-    desc = (f"oracle greedy decode of the same {n}-sentence seeded sample of the workload per step "
+    desc = (f"oracle {'greedy' if args.beam <= 1 else f'beam-{args.beam}'} decode of the same {n}-sentence seeded sample of the workload per step "
             f"({int(samp.lengths.sum())} source words)")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": metric_name(args.beam), "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8/f32/f64",
         "data": "synthetic (seeded random-init weights, newstest2014-shaped ids)",
@@ -211,12 +216,14 @@ def live_rows_profile(sset, budget, max_concurrent_rows=0):
     return rows
 
 
-def roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr):
-    """A9: output projection fused with argmax, at the workload's mean live-row count."""
+def roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr, beam=0):
+    """A9: output projection fused with argmax (beam > 0: with the beam-search log-sum-exp +
+    top-8 epilogue, EPI_TOPK, at beam x the mean live-row count), at the workload's mean
+    live-row count."""
     import torch
     from paper_1805_12096_b200 import mnmt as M
     rows = live_rows_profile(sset, budget, mcr)
-    Mr = int(round(np.mean(rows)))
+    Mr = int(round(np.mean(rows) * max(1, beam)))
     d, V = dims.d_model, dims.vocab
     dev = torch.device("cuda", torch.cuda.current_device())
     E = torch.from_numpy(weights["emb.E"]).to(dev)
@@ -226,16 +233,24 @@ def roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr):
     qa = torch.empty((Mr, d), dtype=torch.int8, device=dev)
     M.op_quantize(x.data_ptr(), Mr * d, dims.clip, qa.data_ptr(), stream)
     b = torch.from_numpy(weights["out.b"]).to(dev)
-    keys = torch.zeros(Mr, dtype=torch.int64, device=dev)
+    if beam:
+        part_ld = 2 * ((V + 255) // 256)
+        keys = torch.empty(Mr * part_ld * M.TOPK_RECORD_BYTES, dtype=torch.uint8, device=dev)
+    else:
+        keys = torch.zeros(Mr, dtype=torch.int64, device=dev)
+    epi = M.EPI_TOPK if beam else M.EPI_ARGMAX
 
     def fn(st):
         M.op_gemm_i8(qa.data_ptr(), qE.data_ptr(), Mr, V, d, b.data_ptr(), dims.clip,
-                     M.EPI_ARGMAX, keys.data_ptr(), None, 0, st)
+                     epi, keys.data_ptr(), None, beam if beam in (2, 4) else 0, st)
     ms = time_kernel(fn, 200, stream)
     ops = 2.0 * Mr * V * d
     peak = 2.0 * peaks["bf16_tflops"]          # int8 dense = 2x bf16 (nominal 4.5 / 2.25)
     ach = ops / (ms * 1e-3) / 1e12
-    return {"kernel": "k_gemm_i8<EPI_ARGMAX> (A9 output GEMM + argmax)", "bound": "tensor",
+    name = (f"k_gemm_i8<256, EPI_TOPK{beam if beam in (2, 4) else ''}> (A9 beam output GEMM + "
+            f"fp64 log-sum-exp + top-{beam if beam in (2, 4) else 8})" if beam
+            else "k_gemm_i8<EPI_ARGMAX> (A9 output GEMM + argmax)")
+    return {"kernel": name, "bound": "tensor",
             "achieved": ach, "peak": peak, "unit": "TOP/s (int8)", "frac": ach / peak,
             "traffic": None, "shape": f"M={Mr} (mean live rows/step) N={V} K={d}",
             "ms_per_launch": ms, "launches_per_step": len(rows),
@@ -243,13 +258,13 @@ def roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr):
             "peak_source": f"{peaks['source']} bf16 burst x2"}
 
 
-def roofline_dxd_gemm(dims, sset, budget, peaks, stream, mcr):
+def roofline_dxd_gemm(dims, sset, budget, peaks, stream, mcr, mult=1):
     """A6-A7: the decoder's d x d projections (AAN FFN, gates, source q/o): 6 per layer per step,
     at the workload's mean live-row count."""
     import torch
     from paper_1805_12096_b200 import mnmt as M
     rows = live_rows_profile(sset, budget, mcr)
-    Mr = max(1, int(round(np.mean(rows))))
+    Mr = max(1, int(round(np.mean(rows) * mult)))   # mult: beam (hypotheses per sentence)
     d = dims.d_model
     dev = torch.device("cuda", torch.cuda.current_device())
     A = torch.randint(-127, 128, (Mr, d), dtype=torch.int8, device=dev)
@@ -273,14 +288,14 @@ def roofline_dxd_gemm(dims, sset, budget, peaks, stream, mcr):
             "peak_source": f"{peaks['source']} bf16 burst x2"}
 
 
-def roofline_src_attn(dims, sset, budget, peaks, stream, mcr):
+def roofline_src_attn(dims, sset, budget, peaks, stream, mcr, mult=1):
     """A7: source attention over the fp32 K/V cache, rows = the workload's mean live rows per
     step, drawn (seeded) from the set so the source-length mix matches."""
     import torch
     from paper_1805_12096_b200 import mnmt as M
     rows = live_rows_profile(sset, budget, mcr)
-    n_rows = max(1, int(round(np.mean(rows))))
-    idx = np.random.default_rng(3).choice(sset.n, size=min(n_rows, sset.n), replace=False)
+    n_rows = max(1, int(round(np.mean(rows) * mult)))
+    idx = np.random.default_rng(3).choice(sset.n, size=n_rows, replace=n_rows > sset.n)
     L = sset.lengths[idx].astype(np.int32)
     starts = np.concatenate([[0], np.cumsum(L)[:-1]]).astype(np.int32)
     d, H = dims.d_model, dims.n_heads
@@ -322,6 +337,10 @@ def ncu_traffic(key, shape):
 
 
 # ---------------------------------------------------------------------------- main
+def metric_name(beam: int) -> str:
+    return METRIC if beam <= 1 else f"target words/sec beam-{beam} decode (best hypothesis), 1 B200"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -333,6 +352,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--beam", type=int, default=1,
+                    help="1 (default): greedy decode, the headline; 2..8: beam search "
+                         "(SURVEY 8(f) F1, mnmt_beam_translate); words = best hypothesis")
+    ap.add_argument("--beam-fused", type=int, default=0,
+                    help="beam search: 1 = log-sum-exp / top-k fused into the output GEMM epilogue")
     ap.add_argument("--megakernel", type=int, default=0,
                     help="1: persistent step kernel per batch; 0: one kernel per op (CUDA graph)")
     ap.add_argument("--lanes", type=int, default=3,
@@ -369,7 +393,7 @@ def main():
                                f"decoder={'AAN' if dims.decoder else 'self-attn'}",
                     "sentences_per_gpu": synth.NEWSTEST_SENTENCES,
                     "source_words_per_gpu": synth.NEWSTEST_TOKENS, "word_budget": budget,
-                    "beam": 1, "max_len": "source length", "parallelism": f"dp{args.gpus}",
+                    "beam": args.beam, "beam_fused": args.beam_fused, "max_len": "source length", "parallelism": f"dp{args.gpus}",
                     "l2": "flushed between timed steps (512 MiB write)",
                     "max_concurrent_rows": args.max_concurrent_rows, "lanes": args.lanes,
                     "fuse_ln": args.fuse_ln, "steps_per_graph": args.steps_per_graph,
@@ -404,26 +428,39 @@ def main():
     model.set_option("pers_reserve", args.pers_reserve)
     model.set_option("green_sms", args.green_sms)
     model.set_option("rowfuse", args.rowfuse)
+    model.set_option("beam_fused", args.beam_fused)
     sset = synth.newstest_set(seed=2014 + rank)          # weak scaling: one set per GPU
     stream = torch.cuda.current_stream()
     dev = torch.device("cuda", local)
     ids_dev = torch.from_numpy(sset.ids).to(dev)
-    cap = int(sset.max_len.sum())
+    beam = args.beam
+    nb = max(1, beam)
+    cap = int(sset.max_len.sum()) * nb
     out_dev = torch.zeros(cap, dtype=torch.int32, device=dev)
-    len_dev = torch.zeros(sset.n, dtype=torch.int32, device=dev)
+    len_dev = torch.zeros(sset.n * nb, dtype=torch.int32, device=dev)
+    score_dev = torch.zeros(sset.n * nb, dtype=torch.float32, device=dev)
+    nhyp_dev = torch.zeros(sset.n, dtype=torch.int32, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
     def step():
-        model.translate_device(ids_dev.data_ptr(), sset.offsets, sset.max_len, budget,
-                               out_dev.data_ptr(), cap, len_dev.data_ptr(), stream)
-        if dist_on:
-            D.gather_ids(out_dev, len_dev)
+        if beam > 1:
+            model.beam_translate_device(ids_dev.data_ptr(), sset.offsets, sset.max_len, budget,
+                                        beam, out_dev.data_ptr(), cap, len_dev.data_ptr(),
+                                        score_dev.data_ptr(), nhyp_dev.data_ptr(), stream)
+        else:
+            model.translate_device(ids_dev.data_ptr(), sset.offsets, sset.max_len, budget,
+                                   out_dev.data_ptr(), cap, len_dev.data_ptr(), stream)
+            if dist_on:
+                D.gather_ids(out_dev, len_dev)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     launches_per_step = model.stats()["gpu_launches"]
-    words_rank = int(len_dev.sum().item())
+    if beam > 1:   # words of each sentence's best hypothesis
+        words_rank = int((len_dev.view(sset.n, nb)[:, 0] * (nhyp_dev > 0)).sum().item())
+    else:
+        words_rank = int(len_dev.sum().item())
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -453,7 +490,12 @@ def main():
     value = words_total * args.steps / (ms_max / 1000.0)
 
     # ---- e2e: the public host-buffer call (H2D of ids, D2H of ids inside the timed region)
-    model.translate(sset, budget, stream)
+    def host_call():
+        if beam > 1:
+            return model.beam_translate(sset, budget, beam, stream)
+        return model.translate(sset, budget, stream)
+
+    host_call()
     torch.cuda.synchronize()
     st = model.stats()
     e_ms = []
@@ -461,8 +503,8 @@ def main():
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        outs = model.translate(sset, budget, stream)
-        if dist_on:
+        outs = host_call()
+        if dist_on and beam <= 1:
             flat, lens = D.pack_ids(outs, sset.max_len)
             D.gather_ids(torch.from_numpy(flat).to(dev), torch.from_numpy(lens).to(dev))
         torch.cuda.synchronize()
@@ -477,9 +519,10 @@ def main():
     if rank == 0 and not args.no_roofline:
         peaks = load_peaks()
         mcr = args.max_concurrent_rows
-        cands = [roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr),
-                 roofline_src_attn(dims, sset, budget, peaks, stream, mcr),
-                 roofline_dxd_gemm(dims, sset, budget, peaks, stream, mcr)]
+        cands = [roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr,
+                                   beam if beam > 1 else 0),
+                 roofline_src_attn(dims, sset, budget, peaks, stream, mcr, nb),
+                 roofline_dxd_gemm(dims, sset, budget, peaks, stream, mcr, nb)]
         cands[1]["launches_per_step"] = len(live_rows_profile(sset, budget, mcr)) * dims.dec_layers
         cands[1]["ms_per_step_est"] = cands[1]["ms_per_launch"] * cands[1]["launches_per_step"]
         for key, c in zip(("out", "attn", "dxd"), cands):
@@ -489,12 +532,12 @@ def main():
         roof["other"] = {c["kernel"]: {"frac": c["frac"], "ms_per_step_est": c["ms_per_step_est"]}
                          for c in cands if c is not roof}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, cores, desc, _ = oracle_sample(sset, dims, weights, args.cpu_seconds)
+        v, cores, desc, _ = oracle_sample(sset, dims, weights, args.cpu_seconds, beam=beam)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": metric_name(beam), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int8 products (s32 acc), f32 activations, f64 reductions",
             "data": "synthetic (seeded random-init weights, newstest2014-shaped length-sorted ids)",

@@ -195,6 +195,9 @@ mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids_host,
  *                          cluster and its phases synchronise with cluster barriers.
  *   "mk_ctas"              grid cap of the persistent step kernel (0 = one CTA per SM).
  *   "profile_phases"       1 = the persistent kernel stamps every phase (mnmt_debug_phase_*).
+ *   "beam_fused"           beam search: 1 = log-sum-exp partials and top-k fused into the output
+ *                          GEMM epilogue (EPI_TOPK*, logits never reach HBM); 0 (default, measured
+ *                          faster) = fp32 logits written by the GEMM, reduced by one CTA per row.
  * Errors: MNMT_ERR_ARG (unknown name or negative value). */
 mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, int64_t value);
 

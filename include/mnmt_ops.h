@@ -35,6 +35,11 @@ mnmt_status mnmt_op_quantize(const float* x_dev, int64_t n, float clip, int8_t* 
 #define MNMT_EPI_SIGMOID 4    /* out fp32 = sigmoid(v) (fp64 exp, R20)             */
 #define MNMT_EPI_ARGMAX 5     /* out u64 [M] = max over columns of packed (v, col); caller zeroes it */
 #define MNMT_EPI_ACC 6        /* out int32 [M x N] = exact s32 accumulator         */
+#define MNMT_EPI_TOPK 9       /* beam search (F1): out = [M][2 * ceil(N / 256)] records of 80 bytes,
+                               * one per (row, 128-column half tile): {float m; int32 pad; double z;
+                               * float v[8]; int32 j[8]} = max v, sum exp(v - m) in fp64, the 8
+                               * largest (v, column) by (v desc, column asc); n_tile = 2 / 4 keeps
+                               * only the 2 / 4 largest (the rest empty: v = -inf, column = -1) */
 
 /* dotint(quant(A), quant(B^T)) = A . W^T on the int8 tensor cores (R3):
  * A [M x K] codes, W [N x K] codes (K % 16 == 0), bias [N] fp32 or NULL.

@@ -113,6 +113,148 @@ __global__ void __launch_bounds__(BEAM_ROWS_WARPS * 32) k_beam_rows(BeamArgs a) 
   if (lane == 0) a.row_lse[r] = lse;
 }
 
+// exp(x) for x <= 0 in fp64 (same construction as the GEMM epilogue's exp_neg; R26).
+__device__ const double c_beam_exp2_64[64] = {
+    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284, 1.0442737824274138,
+    1.0556451783605572, 1.0671404006768237, 1.0787607977571199, 1.0905077326652577,
+    1.102382583307841, 1.1143867425958924, 1.1265216186082418, 1.1387886347566916,
+    1.1511892299529827, 1.1637248587775775, 1.1763969916502812, 1.189207115002721,
+    1.202156731452703, 1.215247359980469, 1.22848053610687, 1.241857812073484,
+    1.255380757024691, 1.2690509571917332, 1.2828700160787783, 1.2968395546510096,
+    1.3109612115247644, 1.3252366431597413, 1.339667524053303, 1.3542555469368927,
+    1.3690024229745905, 1.383909881963832, 1.3989796725383112, 1.4142135623730951,
+    1.42961333839197, 1.4451808069770467, 1.460917794180647, 1.4768261459394993,
+    1.4929077282912648, 1.5091644275934228, 1.5255981507445384, 1.5422108254079407,
+    1.559004400237837, 1.5759808451078865, 1.593142151342267, 1.6104903319492543,
+    1.6280274218573478, 1.645755478153965, 1.6636765803267364, 1.681792830507429,
+    1.7001063537185235, 1.718619298122478, 1.7373338352737062, 1.7562521603732995,
+    1.7753764925265212, 1.7947090750031072, 1.8142521755003989, 1.8340080864093424,
+    1.8539791250833855, 1.8741676341103, 1.8945759815869656, 1.9152065613971474,
+    1.9360617934922943, 1.9571441241754002, 1.978456026387951};
+
+__device__ __forceinline__ double beam_exp_neg(double x, const double* tab) {
+  if (x < -707.0) return 0.0;
+  const double kd = rint(x * 92.33248261689366);
+  double r = fma(kd, -0.01083042469326756, x);
+  r = fma(kd, -2.9815858269852933e-12, r);
+  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int k = (int)kd;
+  const double v = p * tab[k & 63];
+  return __hiloint2double(__double2hiint(v) + ((k >> 6) << 20), __double2loint(v));
+}
+
+constexpr int BEAM_LOGITS_THREADS = 512;
+
+// One CTA per live row of materialised logits: the row maximum M (pass 1), then
+// Z = sum exp((double)l - M) in fp64 per thread (4 partial sums) + block tree, and the row's
+// top-beam (value desc, id asc) from per-thread sorted lists merged in beam block rounds.
+template <int TK>
+__global__ void __launch_bounds__(BEAM_LOGITS_THREADS) k_beam_logits(BeamArgs a) {
+  __shared__ double tab[64];
+  __shared__ double zs[BEAM_LOGITS_THREADS / 32];
+  __shared__ float ms[BEAM_LOGITS_THREADS / 32];
+  __shared__ unsigned long long ks[BEAM_LOGITS_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = BEAM_LOGITS_THREADS / 32;
+  if (tid < 64) tab[tid] = c_beam_exp2_64[tid];
+  pdl_wait();
+  pdl_launch_dependents();
+  const int r = blockIdx.x;
+  if (r >= a.ctrl[0]) return;   // block-uniform
+  const float* L = a.logits + (int64_t)r * a.ld_logits;
+  const int V = a.V, V4 = V >> 2;
+  const float4* L4 = reinterpret_cast<const float4*>(L);
+  // pass 1: maximum and per-thread top-TK
+  float mx = -INFINITY;
+  float tv[TK];
+  int tj[TK];
+#pragma unroll
+  for (int i = 0; i < TK; ++i) { tv[i] = -INFINITY; tj[i] = -1; }
+  auto ins = [&](float cv, int cj) {
+    bool sh = false;
+#pragma unroll
+    for (int i = 0; i < TK; ++i) {
+      const bool take = sh || cv > tv[i];
+      const float ov = tv[i];
+      const int oj = tj[i];
+      tv[i] = take ? cv : ov;
+      tj[i] = take ? cj : oj;
+      cv = take ? ov : cv;
+      cj = take ? oj : cj;
+      sh = take;
+    }
+  };
+  for (int q = tid; q < V4; q += BEAM_LOGITS_THREADS) {   // columns ascending per thread
+    const float4 x = L4[q];
+    mx = fmaxf(mx, fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w)));
+    if (x.x > tv[TK - 1]) ins(x.x, 4 * q);
+    if (x.y > tv[TK - 1]) ins(x.y, 4 * q + 1);
+    if (x.z > tv[TK - 1]) ins(x.z, 4 * q + 2);
+    if (x.w > tv[TK - 1]) ins(x.w, 4 * q + 3);
+  }
+  for (int j = 4 * V4 + tid; j < V; j += BEAM_LOGITS_THREADS) {
+    const float x = L[j];
+    mx = fmaxf(mx, x);
+    if (x > tv[TK - 1]) ins(x, j);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) ms[w] = mx;
+  __syncthreads();
+  mx = ms[0];
+  for (int i = 1; i < nw; ++i) mx = fmaxf(mx, ms[i]);
+  // pass 2: Z (the row is re-read from L2)
+  const double md = (double)mx;
+  double zp[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int q = tid; q < V4; q += BEAM_LOGITS_THREADS) {
+    const float4 x = L4[q];
+    zp[0] = __dadd_rn(zp[0], beam_exp_neg(__dsub_rn((double)x.x, md), tab));
+    zp[1] = __dadd_rn(zp[1], beam_exp_neg(__dsub_rn((double)x.y, md), tab));
+    zp[2] = __dadd_rn(zp[2], beam_exp_neg(__dsub_rn((double)x.z, md), tab));
+    zp[3] = __dadd_rn(zp[3], beam_exp_neg(__dsub_rn((double)x.w, md), tab));
+  }
+  for (int j = 4 * V4 + tid; j < V; j += BEAM_LOGITS_THREADS)
+    zp[0] = __dadd_rn(zp[0], beam_exp_neg(__dsub_rn((double)L[j], md), tab));
+  double z = __dadd_rn(__dadd_rn(zp[0], zp[1]), __dadd_rn(zp[2], zp[3]));
+  z = warp_sum_f64(z);
+  if (lane == 0) zs[w] = z;
+  __syncthreads();
+  if (tid == 0) {
+    double Z = 0.0;
+    for (int i = 0; i < nw; ++i) Z = __dadd_rn(Z, zs[i]);
+    a.row_lse[r] = (float)__dadd_rn(md, log(Z));
+  }
+  // top-beam: beam rounds of a block-wide packed (value, lowest id) maximum over list heads
+  int head = 0;
+  for (int i = 0; i < a.beam; ++i) {
+    float hv = -INFINITY;
+    int hj = -1;
+#pragma unroll
+    for (int u = 0; u < TK; ++u)
+      if (u == head) { hv = tv[u]; hj = tj[u]; }
+    const unsigned long long key = hj >= 0 ? argmax_key(hv, (uint32_t)hj) : 0ull;
+    unsigned long long mk = key;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, mk, o);
+      mk = other > mk ? other : mk;
+    }
+    __syncthreads();
+    if (lane == 0) ks[w] = mk;
+    __syncthreads();
+    mk = ks[0];
+    for (int u = 1; u < nw; ++u) mk = ks[u] > mk ? ks[u] : mk;
+    if (key == mk && mk != 0ull) {   // exactly one thread holds the winning (value, id)
+      ++head;
+      a.row_v[(int64_t)r * TOPK_MAX + i] = hv;
+      a.row_j[(int64_t)r * TOPK_MAX + i] = hj;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ selection + compaction
 // Block-wide exclusive scan of one int per thread (blockDim multiple of 32, <= 1024).
 __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int& total) {
@@ -368,6 +510,14 @@ cudaError_t launch_beam_rows(const BeamArgs& a, cudaStream_t st) {
   if (a.n <= 0) return cudaSuccess;
   return launch_pdl(k_beam_rows, dim3((a.n + BEAM_ROWS_WARPS - 1) / BEAM_ROWS_WARPS),
                     dim3(32 * BEAM_ROWS_WARPS), 0, st, a);
+}
+cudaError_t launch_beam_logits(const BeamArgs& a, cudaStream_t st) {
+  if (a.n <= 0) return cudaSuccess;
+  if (a.beam <= 2)
+    return launch_pdl(k_beam_logits<2>, dim3(a.n), dim3(BEAM_LOGITS_THREADS), 0, st, a);
+  if (a.beam <= 4)
+    return launch_pdl(k_beam_logits<4>, dim3(a.n), dim3(BEAM_LOGITS_THREADS), 0, st, a);
+  return launch_pdl(k_beam_logits<8>, dim3(a.n), dim3(BEAM_LOGITS_THREADS), 0, st, a);
 }
 cudaError_t launch_beam_select(const BeamArgs& a, cudaStream_t st) {
   return launch_pdl(k_beam_select, dim3(1), dim3(BEAM_SELECT_THREADS), 0, st, a);

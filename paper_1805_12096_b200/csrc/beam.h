@@ -50,6 +50,9 @@ struct BeamArgs {
   float* C;                  // AAN running sums [L][c_stride] (slot rows of d), or null
   int64_t c_stride;
   int L, d;
+  const float* logits;       // beam_fused = 0: fp32 logits [rows][V] of the step (EPI_F32 GEMM)
+  int V;
+  int64_t ld_logits;         // row stride of logits (V rounded up to 16: aligned float4 rows)
   int32_t* out_ids;          // job outputs (see mnmt_beam_translate)
   int32_t* out_len;
   float* out_score;
@@ -58,9 +61,10 @@ struct BeamArgs {
 
 cudaError_t launch_beam_init(const BeamArgs& a, int n_sent, cudaStream_t st);
 cudaError_t launch_beam_rows(const BeamArgs& a, cudaStream_t st);
+// Same outputs as k_beam_rows, from materialised fp32 logits: one CTA per live row.
+cudaError_t launch_beam_logits(const BeamArgs& a, cudaStream_t st);
 cudaError_t launch_beam_select(const BeamArgs& a, cudaStream_t st);
 cudaError_t launch_beam_reorder(const BeamArgs& a, cudaStream_t st);
 cudaError_t launch_beam_final(const BeamArgs& a, int n_sent, cudaStream_t st);
-cudaError_t beam_init_attrs();   // dynamic smem of k_beam_reorder (once per device)
 
 }  // namespace mnmt

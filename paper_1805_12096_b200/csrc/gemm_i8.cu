@@ -332,18 +332,65 @@ __device__ __forceinline__ void ln_epilogue(const GemmArgs& a, uint32_t t_row, i
   }
 }
 
-// EPI_TOPK (beam search, F1): one 32-column chunk at a time, the row's running maximum m,
+// EPI_TOPK* (beam search, F1): one 32-column chunk at a time, the row's running maximum m,
 // the fp64 sum z = sum exp(v - m) (rescaled by exp(m_old - m_new) when a chunk raises m) and
-// the TOPK_MAX largest (v, column) in descending v, ascending column on ties (columns arrive
-// in ascending order and only a strictly larger value displaces an entry).
-template <int BN>
+// the TK largest (v, column) in descending v, ascending column on ties (columns arrive in
+// ascending order and only a strictly larger value displaces an entry).
+__host__ __device__ constexpr bool is_topk(int epi) {
+  return epi == EPI_TOPK || epi == EPI_TOPK2 || epi == EPI_TOPK4;
+}
+__host__ __device__ constexpr int topk_k(int epi) {
+  return epi == EPI_TOPK2 ? 2 : epi == EPI_TOPK4 ? 4 : TOPK_MAX;
+}
+
+// 2^(i/64), i = 0..63, correctly rounded (staged in shared memory by the TOPK epilogue)
+__device__ const double c_exp2_64[64] = {
+    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284, 1.0442737824274138,
+    1.0556451783605572, 1.0671404006768237, 1.0787607977571199, 1.0905077326652577,
+    1.102382583307841, 1.1143867425958924, 1.1265216186082418, 1.1387886347566916,
+    1.1511892299529827, 1.1637248587775775, 1.1763969916502812, 1.189207115002721,
+    1.202156731452703, 1.215247359980469, 1.22848053610687, 1.241857812073484,
+    1.255380757024691, 1.2690509571917332, 1.2828700160787783, 1.2968395546510096,
+    1.3109612115247644, 1.3252366431597413, 1.339667524053303, 1.3542555469368927,
+    1.3690024229745905, 1.383909881963832, 1.3989796725383112, 1.4142135623730951,
+    1.42961333839197, 1.4451808069770467, 1.460917794180647, 1.4768261459394993,
+    1.4929077282912648, 1.5091644275934228, 1.5255981507445384, 1.5422108254079407,
+    1.559004400237837, 1.5759808451078865, 1.593142151342267, 1.6104903319492543,
+    1.6280274218573478, 1.645755478153965, 1.6636765803267364, 1.681792830507429,
+    1.7001063537185235, 1.718619298122478, 1.7373338352737062, 1.7562521603732995,
+    1.7753764925265212, 1.7947090750031072, 1.8142521755003989, 1.8340080864093424,
+    1.8539791250833855, 1.8741676341103, 1.8945759815869656, 1.9152065613971474,
+    1.9360617934922943, 1.9571441241754002, 1.978456026387951};
+
+// exp(x) for x <= 0 in fp64 (relative error ~2 ulp; R26): x = k ln2/64 + r with |r| <= ln2/128,
+// exp(x) = 2^floor(k/64) * 2^((k mod 64)/64) * e^r, e^r by its degree-5 Taylor polynomial
+// (truncation < 4e-17).  k ln2/64 is split hi (32 significant bits, so k*hi is exact) + lo.
+// x < -707: 0 (the sums it feeds are >= 1, so such terms are far below their last bit).
+__device__ __forceinline__ double exp_neg(double x, const double* tab) {
+  if (x < -707.0) return 0.0;
+  const double kd = rint(x * 92.33248261689366);          // 64 / ln2
+  double r = fma(kd, -0.01083042469326756, x);             // ln2/64, high 32 bits
+  r = fma(kd, -2.9815858269852933e-12, r);                 // ln2/64, low part
+  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int k = (int)kd;
+  const double v = p * tab[k & 63];
+  // multiply by 2^(k >> 6) through the exponent field (v in [0.99, 2), result normal)
+  return __hiloint2double(__double2hiint(v) + ((k >> 6) << 20), __double2loint(v));
+}
+
+template <int BN, int TK>
 __device__ __forceinline__ void topk_epilogue(const GemmArgs& args, const float* bsrc, uint32_t t_row,
-                                              int row, bool row_ok, int half, int n0) {
+                                              int row, bool row_ok, int half, int n0,
+                                              const double* tab) {
   constexpr int HALF = BN / 2;
-  float tv[TOPK_MAX];
-  int tj[TOPK_MAX];
+  float tv[TK];
+  int tj[TK];
 #pragma unroll
-  for (int i = 0; i < TOPK_MAX; ++i) { tv[i] = -INFINITY; tj[i] = -1; }
+  for (int i = 0; i < TK; ++i) { tv[i] = -INFINITY; tj[i] = -1; }
   float run_m = -INFINITY;
   double z = 0.0;
 #pragma unroll 1
@@ -366,21 +413,25 @@ __device__ __forceinline__ void topk_epilogue(const GemmArgs& args, const float*
 #pragma unroll
     for (int j = 1; j < 32; ++j) cm = fmaxf(cm, v[j]);
     if (cm > run_m) {
-      if (run_m != -INFINITY) z = __dmul_rn(z, exp(__dsub_rn((double)run_m, (double)cm)));
+      if (run_m != -INFINITY) z = __dmul_rn(z, exp_neg(__dsub_rn((double)run_m, (double)cm), tab));
       run_m = cm;
     }
+    // four independent partial sums (columns j mod 4), combined in a fixed order
     const double md = (double)run_m;
+    double zp[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int j = 0; j < 32; ++j) z = __dadd_rn(z, exp(__dsub_rn((double)v[j], md)));
-    if (cm > tv[TOPK_MAX - 1]) {
+    for (int j = 0; j < 32; ++j)
+      if (v[j] != -INFINITY) zp[j & 3] = __dadd_rn(zp[j & 3], exp_neg(__dsub_rn((double)v[j], md), tab));
+    z = __dadd_rn(z, __dadd_rn(__dadd_rn(zp[0], zp[1]), __dadd_rn(zp[2], zp[3])));
+    if (cm > tv[TK - 1]) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        if (v[j] > tv[TOPK_MAX - 1]) {
+        if (v[j] > tv[TK - 1]) {
           float cv = v[j];
           int cj = n + j;
           bool sh = false;
 #pragma unroll
-          for (int i = 0; i < TOPK_MAX; ++i) {
+          for (int i = 0; i < TK; ++i) {
             const bool take = sh || cv > tv[i];
             const float ov = tv[i];
             const int oj = tj[i];
@@ -401,8 +452,8 @@ __device__ __forceinline__ void topk_epilogue(const GemmArgs& args, const float*
     p->z = z;
 #pragma unroll
     for (int i = 0; i < TOPK_MAX; ++i) {
-      p->v[i] = tv[i];
-      p->j[i] = tj[i];
+      p->v[i] = i < TK ? tv[i < TK ? i : 0] : -INFINITY;
+      p->j[i] = i < TK ? tj[i < TK ? i : 0] : -1;
     }
   }
 }
@@ -418,6 +469,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __shared__ __align__(8) uint64_t tmem_full_bar;
   __shared__ uint32_t tmem_slot;
   __shared__ double ln_part[EPI == EPI_LN ? 256 : 1];
+  __shared__ double exp_tab[is_topk(EPI) ? 64 : 1];   // 2^(i/64) for exp_neg (EPI_TOPK*)
   __shared__ __align__(16) float bias_s[BN];   // the tile's bias, staged before the PDL wait
 
   const uint32_t warp = warp_id();
@@ -454,6 +506,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
   // TMEM and the bias do not depend on the previous kernel either: both before the wait
   if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(&tmem_slot);
+  if constexpr (is_topk(EPI)) {
+    if (warp >= 2 && threadIdx.x - 64 < 64) exp_tab[threadIdx.x - 64] = c_exp2_64[threadIdx.x - 64];
+  }
   if (args.bias && warp >= 2)
     for (int i = (int)threadIdx.x - 64; i < BN; i += 32 * EPI_WARPS)
       bias_s[i] = n0 + i < args.N ? __ldg(args.bias + n0 + i) : 0.0f;
@@ -545,8 +600,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int best_j = -1;
     if constexpr (EPI == EPI_LN) {
       ln_epilogue<BN>(args, t_row, row, row_ok, half, q * 32 + lane, ln_part);
-    } else if constexpr (EPI == EPI_TOPK) {
-      topk_epilogue<BN>(args, args.bias ? bias_s - n0 : nullptr, t_row, row, row_ok, half, n0);
+    } else if constexpr (is_topk(EPI)) {
+      topk_epilogue<BN, topk_k(EPI)>(args, args.bias ? bias_s - n0 : nullptr, t_row, row, row_ok,
+                                     half, n0, exp_tab);
     } else
 #pragma unroll 1
     for (int c = 0; c < HALF; c += 32) {
@@ -1141,9 +1197,11 @@ static cudaError_t gemm_init_all() {
   if ((e = set_attr_bn<64>()) != cudaSuccess) return e;
   if ((e = set_attr_bn<128>()) != cudaSuccess) return e;
   if ((e = set_attr_ln()) != cudaSuccess) return e;
-  if ((e = cudaFuncSetAttribute(k_gemm_i8<TOPK_BN, EPI_TOPK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                GemmCfg<TOPK_BN>::smem_for(GemmCfg<TOPK_BN>::STAGES))) != cudaSuccess)
-    return e;
+  for (const void* f : {(const void*)k_gemm_i8<TOPK_BN, EPI_TOPK>, (const void*)k_gemm_i8<TOPK_BN, EPI_TOPK2>,
+                        (const void*)k_gemm_i8<TOPK_BN, EPI_TOPK4>})
+    if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  GemmCfg<TOPK_BN>::smem_for(GemmCfg<TOPK_BN>::STAGES))) != cudaSuccess)
+      return e;
   return set_attr_bn<256>();
 }
 
@@ -1221,8 +1279,10 @@ cudaError_t launch_gemm_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const
     }
     return cudaErrorInvalidValue;
   }
-  if (epi == EPI_TOPK) {   // fixed tile (the partial layout depends on it), never persistent
+  if (is_topk(epi)) {   // fixed tile (the partial layout depends on it), never persistent
     if (a.part_ld < 2 * ((a.N + TOPK_BN - 1) / TOPK_BN)) return cudaErrorInvalidValue;
+    if (epi == EPI_TOPK2) return launch_np<TOPK_BN, EPI_TOPK2>(tmA, tmB, a, st);
+    if (epi == EPI_TOPK4) return launch_np<TOPK_BN, EPI_TOPK4>(tmA, tmB, a, st);
     return launch_np<TOPK_BN, EPI_TOPK>(tmA, tmB, a, st);
   }
   if (epi == EPI_LN) {   // one CTA owns whole rows: BN = N = d

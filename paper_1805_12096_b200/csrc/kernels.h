@@ -22,6 +22,8 @@ enum Epi : int {
   EPI_LNC = 8,        // as EPI_LN, rows owned by a cluster of N / BN CTAs (gemm_lnc_bn)
   EPI_TOPK = 9,       // beam search (F1): per (row, N-tile half) the running max m, the fp64
                       // sum z = sum exp(v - m) and the TOPK_MAX largest (v, col) -> part[]
+  EPI_TOPK2 = 10,     // as EPI_TOPK with the 2 / 4 largest (beam <= 2 / <= 4; the other
+  EPI_TOPK4 = 11,     // record entries are empty)
 };
 
 // Beam-search partial of one row over one half of one N tile (EPI_TOPK).  v sorted by

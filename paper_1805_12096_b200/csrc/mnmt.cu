@@ -105,6 +105,7 @@ struct Workspace {
   int32_t *row_j = nullptr, *sent_row0 = nullptr, *sent_nlive = nullptr, *sent_nfin = nullptr;
   int32_t *sent_list = nullptr, *child_par = nullptr, *child_tok = nullptr, *hist = nullptr;
   int32_t* anc = nullptr;
+  float* logits = nullptr;   // [B_cap][V] (beam_fused = 0)
 };
 
 // Job-level device buffers shared by all lanes.
@@ -185,6 +186,8 @@ struct mnmt_model {
   int lane_tiers = 0;                  // option: 0 = deal sentences round-robin to lanes;
                                        // p*10 = contiguous length tiers of equal sum S^p
   int beam = 0;                        // (call state) beam size of the running call; 0 = greedy
+  int beam_fused = 0;                  // option: 1 = log-sum-exp / top-k in the output GEMM epilogue
+                                       // (EPI_TOPK*), 0 = fp32 logits + k_beam_logits (faster)
 };
 
 namespace {
@@ -524,6 +527,7 @@ static mnmt_status beam_ensure(mnmt_model* m, Lane& Ln) {
   CKS(dalloc(A, &w.child_score, R));
   CKS(dalloc(A, &w.hist, R * T));
   if (m->c.decoder == 0) CKS(dalloc(A, &w.anc, R * T));
+  CKS(dalloc(A, &w.logits, R * (((int64_t)m->c.vocab + 15) / 16 * 16)));
   w.beam_rows = R;
   w.beam_T = T;
   return MNMT_OK;
@@ -566,6 +570,9 @@ static BeamArgs beam_args(mnmt_model* m, Lane& Ln, int n) {
   b.c_stride = w.B_cap * m->c.d_model;
   b.L = m->c.dec_layers;
   b.d = m->c.d_model;
+  b.logits = w.logits;
+  b.V = m->c.vocab;
+  b.ld_logits = ((int64_t)m->c.vocab + 15) / 16 * 16;
   b.out_ids = m->jb.out_ids;
   b.out_len = m->jb.out_len;
   b.out_score = m->jb.out_score;
@@ -1030,11 +1037,20 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
     a.clip = c.clip;
     a.sigma = sigma_of(m);
     a.col_block = c.vocab;
-    a.part = w.part;
-    a.part_ld = w.part_ld;
-    if ((e = launch_gemm_i8(w.tm_cy, m->tmE, a, EPI_TOPK, 0, st)) != cudaSuccess) return e;
     const BeamArgs ba = beam_args(m, Ln, n);
-    if ((e = launch_beam_rows(ba, st)) != cudaSuccess) return e;
+    if (m->beam_fused) {
+      a.part = w.part;
+      a.part_ld = w.part_ld;
+      const int epi = m->beam <= 2 ? EPI_TOPK2 : m->beam <= 4 ? EPI_TOPK4 : EPI_TOPK;
+      if ((e = launch_gemm_i8(w.tm_cy, m->tmE, a, epi, 0, st)) != cudaSuccess) return e;
+      if ((e = launch_beam_rows(ba, st)) != cudaSuccess) return e;
+    } else {
+      a.out_f = w.logits;
+      a.ldo = ba.ld_logits;
+      a.pers_grid = m->cur_pers_grid;
+      if ((e = launch_gemm_i8(w.tm_cy, m->tmE, a, EPI_F32, 0, st)) != cudaSuccess) return e;
+      if ((e = launch_beam_logits(ba, st)) != cudaSuccess) return e;
+    }
     if ((e = launch_beam_select(ba, st)) != cudaSuccess) return e;
     if ((e = launch_beam_reorder(ba, st)) != cudaSuccess) return e;
     k += 4;
@@ -2208,6 +2224,15 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
     if (value < 0 || value > 128) { set_err("pers_reserve must be in [0, 128]"); return MNMT_ERR_ARG; }
     m->pers_reserve = (int)value;
     for (Lane& L : m->lanes) {   // captured graphs encode the old grid sizes
+      for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
+      L.graphs.clear();
+    }
+    return MNMT_OK;
+  }
+  if (std::string(name) == "beam_fused") {
+    if (value < 0 || value > 1) { set_err("beam_fused must be 0 or 1"); return MNMT_ERR_ARG; }
+    m->beam_fused = (int)value;
+    for (Lane& L : m->lanes) {   // captured graphs encode the old kernel sequence
       for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
       L.graphs.clear();
     }

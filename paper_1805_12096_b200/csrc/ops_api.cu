@@ -40,12 +40,14 @@ mnmt_status mnmt_op_gemm_i8(const int8_t* A, const int8_t* W, int32_t M, int32_t
                             int32_t n_tile, void* stream) {
   if (!A || !W || !out || M < 1 || N < 1 || K < 16 || K % 16 || !(clip > 0.0f))
     return arg_error("mnmt_op_gemm_i8: bad arguments (K must be a positive multiple of 16)");
-  if (epi < MNMT_EPI_F32 || epi > MNMT_EPI_ACC) return arg_error("mnmt_op_gemm_i8: bad epilogue");
-  if (epi != MNMT_EPI_ARGMAX && N % 16) return arg_error("mnmt_op_gemm_i8: N % 16 != 0");
+  if ((epi < MNMT_EPI_F32 || epi > MNMT_EPI_ACC) && epi != MNMT_EPI_TOPK)
+    return arg_error("mnmt_op_gemm_i8: bad epilogue");
+  if (epi != MNMT_EPI_ARGMAX && epi != MNMT_EPI_TOPK && N % 16) return arg_error("mnmt_op_gemm_i8: N % 16 != 0");
   if ((epi == MNMT_EPI_F32_Q || epi == MNMT_EPI_RELU_F32_Q) && !out2)
     return arg_error("mnmt_op_gemm_i8: epilogue needs out2");
-  if (n_tile != 0 && n_tile != 64 && n_tile != 128 && n_tile != 256)
+  if (epi != MNMT_EPI_TOPK && n_tile != 0 && n_tile != 64 && n_tile != 128 && n_tile != 256)
     return arg_error("mnmt_op_gemm_i8: n_tile must be 0, 64, 128 or 256");
+  int n_tile_topk = 0;
   if (cudaError_t e = gemm_init(); e != cudaSuccess) return cuda_status(e, "gemm init");
   CUtensorMap ta, tb;
   if (!make_tmap_i8(&ta, A, M, K) || !make_tmap_i8(&tb, W, N, K))
@@ -69,7 +71,16 @@ mnmt_status mnmt_op_gemm_i8(const int8_t* A, const int8_t* W, int32_t M, int32_t
     case MNMT_EPI_RELU_Q: a.out_q = (int8_t*)out; break;
     case MNMT_EPI_ARGMAX: a.keys = (unsigned long long*)out; break;
     case MNMT_EPI_ACC: a.out_i = (int32_t*)out; break;
+    case MNMT_EPI_TOPK:
+      a.part = (TopkPart*)out;
+      a.part_ld = 2 * ((N + TOPK_BN - 1) / TOPK_BN);
+      n_tile_topk = n_tile;
+      n_tile = 0;
+      break;
   }
+  // MNMT_EPI_TOPK keeps the 8 largest per record; n_tile 2 / 4 selects the top-2 / top-4 variant
+  if (epi == MNMT_EPI_TOPK && n_tile_topk == 2) epi = EPI_TOPK2;
+  if (epi == MNMT_EPI_TOPK && n_tile_topk == 4) epi = EPI_TOPK4;
   return cuda_status(launch_gemm_i8(ta, tb, a, epi, n_tile, (cudaStream_t)stream), "gemm_i8");
 }
 

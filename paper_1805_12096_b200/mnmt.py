@@ -21,6 +21,8 @@ DEVICE_IO = 1
 
 DUMP_ENC_OUT, DUMP_SRC_KV, DUMP_DEC_OUT, DUMP_OUT_CODES, DUMP_LAYERS = 1, 2, 4, 8, 16
 EPI_F32, EPI_F32_Q, EPI_RELU_Q, EPI_RELU_F32_Q, EPI_SIGMOID, EPI_ARGMAX, EPI_ACC = range(7)
+EPI_TOPK = 9            # beam search partials (include/mnmt_ops.h); 80-byte records
+TOPK_RECORD_BYTES = 80
 
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_DIM", 3: "ERR_VOCAB", 4: "ERR_STATE",
           5: "ERR_CAPACITY", 6: "ERR_CUDA", 7: "ERR_OOM"}

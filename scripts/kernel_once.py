@@ -1,5 +1,5 @@
 """One launch (after warm-up) of a decoder kernel at the bench shape, for ncu.
-usage: KERNEL=dxd|out|attn M=630 python scripts/kernel_once.py"""
+usage: KERNEL=dxd|out|topk|attn M=630 python scripts/kernel_once.py"""
 import os, sys
 import numpy as np
 import torch
@@ -9,7 +9,14 @@ k = os.environ.get("KERNEL", "dxd")
 Mr = int(os.environ.get("M", 630))
 d, V, H = 256, 36000, 8
 dev = torch.device("cuda:0")
-if k in ("dxd", "out"):
+if k == "topk":   # beam-search output GEMM (EPI_TOPK partials)
+    A = torch.randint(-127, 128, (Mr, d), dtype=torch.int8, device=dev)
+    W = torch.randint(-127, 128, (V, d), dtype=torch.int8, device=dev)
+    b = torch.zeros(V, device=dev)
+    out = torch.empty(Mr * 2 * ((V + 255) // 256) * M.TOPK_RECORD_BYTES, dtype=torch.uint8, device=dev)
+    for _ in range(4):
+        M.op_gemm_i8(A.data_ptr(), W.data_ptr(), Mr, V, d, b.data_ptr(), 2.0, M.EPI_TOPK, out.data_ptr(), None, int(os.environ.get("TOPK", 8)), None)
+elif k in ("dxd", "out"):
     N = d if k == "dxd" else V
     A = torch.randint(-127, 128, (Mr, d), dtype=torch.int8, device=dev)
     W = torch.randint(-127, 128, (N, d), dtype=torch.int8, device=dev)

@@ -58,8 +58,10 @@ def test_beam_matches_oracle(dims, beam):
     w, om, gm = pair(dims, 31)
     ss = synth.random_set(23, 1, 14, seed=9, vocab=dims.vocab)
     ref = om.beam_many(ss, beam, 4)
-    got = gm.beam_translate(ss, 40, beam)
-    assert compare(got, ref, dims.name) == beam * ss.n
+    for fused in (0, 1):   # logits + row reduction, or log-sum-exp / top-k in the GEMM epilogue
+        gm.set_option("beam_fused", fused)
+        got = gm.beam_translate(ss, 40, beam)
+        assert compare(got, ref, f"{dims.name} fused={fused}") == beam * ss.n
 
 
 @pytest.mark.parametrize("dims", VARIANTS[:4], ids=lambda d: d.name)
@@ -83,7 +85,8 @@ def test_beam8_and_edges():
     ss = synth.random_set(30, 0, 20, seed=11, vocab=dims.vocab)
     ss.max_len[:] = np.random.default_rng(4).integers(0, 12, size=ss.n)
     ss.max_len[:3] = [0, 1, 2]
-    for beam in (3, 8):
+    for beam, fused in ((3, 0), (8, 0), (8, 1)):
+        gm.set_option("beam_fused", fused)
         ref = om.beam_many(ss, beam, 4)
         got = gm.beam_translate(ss, 25, beam)
         compare(got, ref, f"b{beam}")
@@ -120,7 +123,10 @@ def test_beam_small_aan_36k_vocab():
     w, om, gm = pair(dims, 1, emb_scale=0.5)
     ss = synth.random_set(6, 3, 16, seed=13)
     for beam in (2, 4):
-        compare(gm.beam_translate(ss, 8192, beam), om.beam_many(ss, beam, 0), f"small b{beam}")
+        ref = om.beam_many(ss, beam, 0)
+        for fused in (0, 1):
+            gm.set_option("beam_fused", fused)
+            compare(gm.beam_translate(ss, 8192, beam), ref, f"small b{beam} fused={fused}")
 
 
 def test_beam_errors():
