@@ -45,9 +45,14 @@ typedef struct {
     int32_t eos_id;         /* R16 */
     float clip;             /* c = 2 */
     float ln_eps;           /* R10 */
+    int32_t arith;          /* integer products (oracle only):
+                             * 0 = int8 codes, exact int32 accumulation (R3; the GPU path);
+                             * 1 = int8 codes, saturating int16 accumulation of adjacent pairs
+                             *     ("accumulated in 16-bit integers with saturation");
+                             * 2 = int16 codes RNE(x * 2^10), wrapping int32 accumulation */
 } orc_cfg;
 
-typedef struct { float *W, *b; int8_t *qW; int out, in; } orc_lin;
+typedef struct { float *W, *b; int16_t *qW; int out, in; } orc_lin;   /* codes of arith (int8 range for 0/1) */
 typedef struct { float *g, *b; } orc_ln;
 typedef struct { orc_lin q, k, v, o, f1, f2; orc_ln ln1, ln2; } orc_enc_layer;
 typedef struct {
@@ -61,7 +66,7 @@ typedef struct {
 typedef struct {
     orc_cfg c;
     float *E, *out_b;                /* tied embedding [V x d] */
-    int8_t *qE;
+    int16_t *qE;
     orc_enc_layer enc[ORC_MAX_LAYERS];
     orc_dec_layer dec[ORC_MAX_LAYERS];
     int quantized;
@@ -100,22 +105,75 @@ void orc_gemm_acc(const int8_t *a, const int8_t *w, int M, int N, int K, int32_t
         }
 }
 
-/* lin(qa; W, b)[j] = fmaf((float)acc_j, s, b_j)  (R5). b may be NULL (= 0). */
-static void lin1(const orc_lin *L, const int8_t *qa, float s, float *out) {
-    for (int j = 0; j < L->out; ++j) {
-        int32_t acc = 0;
-        const int8_t *wr = L->qW + (int64_t)j * L->in;
-        for (int k = 0; k < L->in; ++k) acc += (int32_t)qa[k] * (int32_t)wr[k];
-        out[j] = fmaf((float)acc, s, L->b ? L->b[j] : 0.0f);
-    }
-}
-
 /* lin over M rows: out[i][j] = fmaf((float)sum_k qa[i][k] qw[j][k], s, b[j]) (R5). */
 void orc_linear(const int8_t *qa, const int8_t *qw, int M, int N, int K, const float *b,
                 float clip, float *out) {
-    orc_lin L = {NULL, (float *)b, (int8_t *)qw, N, K};
     float s = orc_dequant_scale(clip);
-    for (int i = 0; i < M; ++i) lin1(&L, qa + (int64_t)i * K, s, out + (int64_t)i * N);
+    for (int i = 0; i < M; ++i)
+        for (int j = 0; j < N; ++j) {
+            int32_t acc = 0;
+            for (int k = 0; k < K; ++k)
+                acc += (int32_t)qa[(int64_t)i * K + k] * (int32_t)qw[(int64_t)j * K + k];
+            out[(int64_t)i * N + j] = fmaf((float)acc, s, b ? b[j] : 0.0f);
+        }
+}
+
+/* ------------------------------------------------ F4: integer arithmetic variants */
+/* int16 quantization of P:L92 ("multiplying parameters and inputs by 2^10 before rounding
+ * to signed integers"): RNE(x * 1024) (R1's rounding), saturated to +-32767. */
+int16_t orc_q16(float x) {
+    float y = nearbyintf(x * 1024.0f);   /* x * 2^10 is exact */
+    if (y > 32767.0f) y = 32767.0f;
+    if (y < -32767.0f) y = -32767.0f;
+    return (int16_t)y;
+}
+
+static int16_t code1(const orc_cfg *c, float x) {
+    return c->arith == 2 ? orc_q16(x) : (int16_t)orc_q(x, c->clip);
+}
+static void qcodes(const orc_cfg *c, const float *x, int64_t n, int16_t *out) {
+    for (int64_t i = 0; i < n; ++i) out[i] = code1(c, x[i]);
+}
+/* dequantization scale of a product: s = c^2/127^2 (int8, R2) or 2^-20 (int16). */
+static float code_scale(const orc_cfg *c) {
+    return c->arith == 2 ? (float)(1.0 / 1048576.0) : orc_dequant_scale(c->clip);
+}
+
+static int16_t sat16(int32_t v) { return (int16_t)(v > 32767 ? 32767 : v < -32768 ? -32768 : v); }
+
+/* One dot product of codes under arithmetic `arith`:
+ *   0: exact int32 sum;
+ *   1: k in adjacent pairs, p = sat16(a0*b0 + a1*b1), acc = sat16(acc + p), ascending pairs
+ *      (the pair-then-accumulate order of vpmaddubsw + vpaddsw; odd K padded with a zero);
+ *   2: products in int32, sum wrapping modulo 2^32 (no 32-bit saturating add in AVX512F,
+ *      P:L92), ascending k. */
+int32_t orc_dot_codes(int arith, const int16_t *a, const int16_t *w, int K) {
+    if (arith == 1) {
+        int16_t acc = 0;
+        for (int k = 0; k < K; k += 2) {
+            int32_t p = (int32_t)a[k] * w[k];
+            if (k + 1 < K) p += (int32_t)a[k + 1] * w[k + 1];
+            acc = sat16((int32_t)acc + (int32_t)sat16(p));
+        }
+        return acc;
+    }
+    if (arith == 2) {
+        uint32_t acc = 0;
+        for (int k = 0; k < K; ++k) acc += (uint32_t)((int32_t)a[k] * (int32_t)w[k]);
+        return (int32_t)acc;
+    }
+    int32_t acc = 0;
+    for (int k = 0; k < K; ++k) acc += (int32_t)a[k] * (int32_t)w[k];
+    return acc;
+}
+
+/* lin(qa; W, b)[j] = fmaf((float)acc_j, s, b_j)  (R5). b may be NULL (= 0). */
+static void lin1(const orc_cfg *c, const orc_lin *L, const int16_t *qa, float *out) {
+    float s = code_scale(c);
+    for (int j = 0; j < L->out; ++j) {
+        int32_t acc = orc_dot_codes(c->arith, qa, L->qW + (int64_t)j * L->in, L->in);
+        out[j] = fmaf((float)acc, s, L->b ? L->b[j] : 0.0f);
+    }
 }
 
 void orc_sigmoid_array(const float *x, int64_t n, float *out);
@@ -374,10 +432,11 @@ int orc_model_quantize(orc_model *m) {
         if (!D->ln1.g || !D->ln1.b || !D->ln2.g || !D->ln2.b || !D->ln3.g || !D->ln3.b) return 4;
     }
     int64_t nE = (int64_t)c->vocab * c->d_model;
-    m->qE = (int8_t *)malloc((size_t)nE);
-    orc_quantize(m->E, nE, clip, m->qE);
+    (void)clip;
+    m->qE = (int16_t *)malloc(sizeof(int16_t) * (size_t)nE);
+    qcodes(c, m->E, nE, m->qE);
 #define QL(L) do { if ((L).W) { int64_t n_ = (int64_t)(L).out * (L).in; \
-        (L).qW = (int8_t *)malloc((size_t)n_); orc_quantize((L).W, n_, clip, (L).qW); } } while (0)
+        (L).qW = (int16_t *)malloc(sizeof(int16_t) * (size_t)n_); qcodes(c, (L).W, n_, (L).qW); } } while (0)
     for (int l = 0; l < c->enc_layers; ++l) {
         orc_enc_layer *e = &m->enc[l];
         QL(e->q); QL(e->k); QL(e->v); QL(e->o); QL(e->f1); QL(e->f2);
@@ -402,7 +461,6 @@ int orc_model_quantize(orc_model *m) {
 int orc_encode(const orc_model *m, const int32_t *src, int S, float *enc_out, float *kv) {
     const orc_cfg *c = &m->c;
     int d = c->d_model, F = c->d_ffn, H = c->n_heads;
-    float clip = c->clip, s = orc_dequant_scale(clip);
     if (!m->quantized) return 4;
     for (int i = 0; i < S; ++i) if (src[i] < 0 || src[i] >= c->vocab) return 3;
     float *x = (float *)malloc(sizeof(float) * (size_t)S * d);
@@ -413,28 +471,28 @@ int orc_encode(const orc_model *m, const int32_t *src, int S, float *enc_out, fl
     float *o = (float *)malloc(sizeof(float) * d);
     float *r = (float *)malloc(sizeof(float) * d);
     float *h = (float *)malloc(sizeof(float) * F);
-    int8_t *qa = (int8_t *)malloc((size_t)(F > d ? F : d));
+    int16_t *qa = (int16_t *)malloc(sizeof(int16_t) * (size_t)(F > d ? F : d));
     float *pe = (float *)malloc(sizeof(float) * d);
     for (int i = 0; i < S; ++i) embed(m, src[i], i, x + (int64_t)i * d, pe);
     for (int l = 0; l < c->enc_layers; ++l) {
         const orc_enc_layer *e = &m->enc[l];
         for (int i = 0; i < S; ++i) {
-            orc_quantize(x + (int64_t)i * d, d, clip, qa);
-            lin1(&e->q, qa, s, Q + (int64_t)i * d);
-            lin1(&e->k, qa, s, Kt + (int64_t)i * d);
-            lin1(&e->v, qa, s, Vt + (int64_t)i * d);
+            qcodes(c, x + (int64_t)i * d, d, qa);
+            lin1(c, &e->q, qa, Q + (int64_t)i * d);
+            lin1(c, &e->k, qa, Kt + (int64_t)i * d);
+            lin1(c, &e->v, qa, Vt + (int64_t)i * d);
         }
         for (int i = 0; i < S; ++i) {
             float *xi = x + (int64_t)i * d;
             orc_attention(Q + (int64_t)i * d, Kt, Vt, d, S, d, H, ctx);
-            orc_quantize(ctx, d, clip, qa);
-            lin1(&e->o, qa, s, o);
+            qcodes(c, ctx, d, qa);
+            lin1(c, &e->o, qa, o);
             orc_residual_ln(xi, o, NULL, NULL, d, e->ln1.g, e->ln1.b, c->ln_eps, r);
             memcpy(xi, r, sizeof(float) * d);
-            orc_quantize(xi, d, clip, qa);
-            lin1(&e->f1, qa, s, h);
-            for (int k = 0; k < F; ++k) qa[k] = orc_q(h[k] > 0.0f ? h[k] : 0.0f, clip);
-            lin1(&e->f2, qa, s, o);
+            qcodes(c, xi, d, qa);
+            lin1(c, &e->f1, qa, h);
+            for (int k = 0; k < F; ++k) qa[k] = code1(c, h[k] > 0.0f ? h[k] : 0.0f);
+            lin1(c, &e->f2, qa, o);
             orc_residual_ln(xi, o, NULL, NULL, d, e->ln2.g, e->ln2.b, c->ln_eps, r);
             memcpy(xi, r, sizeof(float) * d);
         }
@@ -444,9 +502,9 @@ int orc_encode(const orc_model *m, const int32_t *src, int S, float *enc_out, fl
         for (int l = 0; l < c->dec_layers; ++l) {
             const orc_dec_layer *D = &m->dec[l];
             for (int i = 0; i < S; ++i) {
-                orc_quantize(x + (int64_t)i * d, d, clip, qa);
-                lin1(&D->sk, qa, s, kv + (((int64_t)l * 2 + 0) * S + i) * d);
-                lin1(&D->sv, qa, s, kv + (((int64_t)l * 2 + 1) * S + i) * d);
+                qcodes(c, x + (int64_t)i * d, d, qa);
+                lin1(c, &D->sk, qa, kv + (((int64_t)l * 2 + 0) * S + i) * d);
+                lin1(c, &D->sv, qa, kv + (((int64_t)l * 2 + 1) * S + i) * d);
             }
         }
     }
@@ -498,7 +556,7 @@ static void dstate_free(orc_dstate *s) { free(s->C); free(s->Ks); free(s->Vs); }
 /* Scratch rows of one decoder step. */
 typedef struct {
     float *y, *g, *a, *t1, *gi, *gf, *r, *x1, *x2, *ctx, *h, *pe, *qs;
-    int8_t *qa, *qy;
+    int16_t *qa, *qy;
 } orc_scratch;
 
 static void scratch_init(const orc_model *m, orc_scratch *w) {
@@ -507,8 +565,8 @@ static void scratch_init(const orc_model *m, orc_scratch *w) {
                    &w->ctx, &w->pe, &w->qs};
     for (size_t i = 0; i < sizeof(f) / sizeof(f[0]); ++i) *f[i] = (float *)malloc(sizeof(float) * d);
     w->h = (float *)malloc(sizeof(float) * F);
-    w->qa = (int8_t *)malloc((size_t)(F > d ? F : d));
-    w->qy = (int8_t *)malloc((size_t)d);
+    w->qa = (int16_t *)malloc(sizeof(int16_t) * (size_t)(F > d ? F : d));
+    w->qy = (int16_t *)malloc(sizeof(int16_t) * (size_t)d);
 }
 static void scratch_free(orc_scratch *w) {
     free(w->y); free(w->g); free(w->a); free(w->t1); free(w->gi); free(w->gf); free(w->r);
@@ -524,10 +582,9 @@ static void dec_step(const orc_model *m, const float *kv, int S, orc_dstate *st,
                      int t, orc_scratch *w, float *layer_out) {
     const orc_cfg *c = &m->c;
     int d = c->d_model, F = c->d_ffn, H = c->n_heads, L = c->dec_layers;
-    float clip = c->clip, s = orc_dequant_scale(clip);
     float *y = w->y, *g = w->g, *a = w->a, *t1 = w->t1, *gi = w->gi, *gf = w->gf;
     float *x1 = w->x1, *x2 = w->x2, *ctx = w->ctx, *h = w->h, *qs = w->qs;
-    int8_t *qa = w->qa, *qy = w->qy;
+    int16_t *qa = w->qa, *qy = w->qy;
     /* A5: decoder input y = emb(id_{t-1}, t-1); zero embedding at t=1 (R13). */
     embed(m, in_id, t - 1, y, w->pe);
     for (int l = 0; l < L; ++l) {
@@ -538,21 +595,21 @@ static void dec_step(const orc_model *m, const float *kv, int S, orc_dstate *st,
             if (c->aan_ffn_depth == 0) {
                 memcpy(a, g, sizeof(float) * d);
             } else {
-                orc_quantize(g, d, clip, qa);
-                lin1(&D->a1, qa, s, t1);
+                qcodes(c, g, d, qa);
+                lin1(c, &D->a1, qa, t1);
                 if (c->aan_ffn_depth == 1) {
                     for (int k = 0; k < d; ++k) a[k] = t1[k] > 0.0f ? t1[k] : 0.0f;
                 } else {
-                    for (int k = 0; k < d; ++k) qa[k] = orc_q(t1[k] > 0.0f ? t1[k] : 0.0f, clip);
-                    lin1(&D->a2, qa, s, a);
+                    for (int k = 0; k < d; ++k) qa[k] = code1(c, t1[k] > 0.0f ? t1[k] : 0.0f);
+                    lin1(c, &D->a2, qa, a);
                 }
             }
             if (c->aan_gate) {
                 /* Gate (R8): i = sig(W_i y + b_i), f = sig(W_f a + b_f), z = i*y + f*a. */
-                orc_quantize(y, d, clip, qy);
-                lin1(&D->gi, qy, s, gi);
-                orc_quantize(a, d, clip, qa);
-                lin1(&D->gf, qa, s, gf);
+                qcodes(c, y, d, qy);
+                lin1(c, &D->gi, qy, gi);
+                qcodes(c, a, d, qa);
+                lin1(c, &D->gf, qa, gf);
                 orc_sigmoid_array(gi, d, gi);
                 orc_sigmoid_array(gf, d, gf);
                 orc_residual_ln(y, a, gi, gf, d, D->ln1.g, D->ln1.b, c->ln_eps, x1);
@@ -562,32 +619,32 @@ static void dec_step(const orc_model *m, const float *kv, int S, orc_dstate *st,
         } else {
             /* A6': self-attention over positions 1..t with a KV cache. */
             float *Kl = st->Ks + (int64_t)l * st->Tcap * d, *Vl = st->Vs + (int64_t)l * st->Tcap * d;
-            orc_quantize(y, d, clip, qy);
-            lin1(&D->q, qy, s, qs);
-            lin1(&D->k, qy, s, Kl + (int64_t)(t - 1) * d);
-            lin1(&D->v, qy, s, Vl + (int64_t)(t - 1) * d);
+            qcodes(c, y, d, qy);
+            lin1(c, &D->q, qy, qs);
+            lin1(c, &D->k, qy, Kl + (int64_t)(t - 1) * d);
+            lin1(c, &D->v, qy, Vl + (int64_t)(t - 1) * d);
             orc_attention(qs, Kl, Vl, d, t, d, H, ctx);
-            orc_quantize(ctx, d, clip, qa);
-            lin1(&D->o, qa, s, a);
+            qcodes(c, ctx, d, qa);
+            lin1(c, &D->o, qa, a);
             orc_residual_ln(y, a, NULL, NULL, d, D->ln1.g, D->ln1.b, c->ln_eps, x1);
         }
         /* A7: source attention. */
-        orc_quantize(x1, d, clip, qa);
-        lin1(&D->sq, qa, s, qs);
+        qcodes(c, x1, d, qa);
+        lin1(c, &D->sq, qa, qs);
         if (S > 0) {
             orc_attention(qs, kv + ((int64_t)l * 2 + 0) * S * d, kv + ((int64_t)l * 2 + 1) * S * d,
                           d, S, d, H, ctx);
         } else {
             memset(ctx, 0, sizeof(float) * d);
         }
-        orc_quantize(ctx, d, clip, qa);
-        lin1(&D->so, qa, s, a);
+        qcodes(c, ctx, d, qa);
+        lin1(c, &D->so, qa, a);
         orc_residual_ln(x1, a, NULL, NULL, d, D->ln2.g, D->ln2.b, c->ln_eps, x2);
         /* A8: FFN; ReLU output goes straight to int8 codes. */
-        orc_quantize(x2, d, clip, qa);
-        lin1(&D->f1, qa, s, h);
-        for (int k = 0; k < F; ++k) qa[k] = orc_q(h[k] > 0.0f ? h[k] : 0.0f, clip);
-        lin1(&D->f2, qa, s, a);
+        qcodes(c, x2, d, qa);
+        lin1(c, &D->f1, qa, h);
+        for (int k = 0; k < F; ++k) qa[k] = code1(c, h[k] > 0.0f ? h[k] : 0.0f);
+        lin1(c, &D->f2, qa, a);
         orc_residual_ln(x2, a, NULL, NULL, d, D->ln3.g, D->ln3.b, c->ln_eps, y);
         if (layer_out) {
             float *dst = layer_out + (int64_t)l * 3 * d;
@@ -601,15 +658,13 @@ static void dec_step(const orc_model *m, const float *kv, int S, orc_dstate *st,
 /* A9: tied output projection: logit_j = fmaf((float)acc_j, s, b_j)
  * with acc_j = sum_k Q(y)_k * Q(E)[j,k]; out_bias = 0: b_j = 0 (R14).
  * qy receives Q(y). */
-static void out_logits(const orc_model *m, const float *y, int8_t *qy, float *logits) {
+static void out_logits(const orc_model *m, const float *y, int16_t *qy, float *logits) {
     const orc_cfg *c = &m->c;
     int d = c->d_model, V = c->vocab;
-    float s = orc_dequant_scale(c->clip);
-    orc_quantize(y, d, c->clip, qy);
+    float s = code_scale(c);
+    qcodes(c, y, d, qy);
     for (int j = 0; j < V; ++j) {
-        int32_t acc = 0;
-        const int8_t *er = m->qE + (int64_t)j * d;
-        for (int k = 0; k < d; ++k) acc += (int32_t)qy[k] * (int32_t)er[k];
+        int32_t acc = orc_dot_codes(c->arith, qy, m->qE + (int64_t)j * d, d);
         logits[j] = fmaf((float)acc, s, c->out_bias ? m->out_b[j] : 0.0f);
     }
 }
@@ -655,7 +710,8 @@ int orc_decode_one(const orc_model *m, const int32_t *src, int S, int max_len,
             if (tr->second) tr->second[i] = second;
             if (tr->margin) tr->margin[i] = second >= 0 ? (float)((double)bv - (double)sv) : INFINITY;
             if (tr->dec_out) memcpy(tr->dec_out + (int64_t)i * d, w.y, sizeof(float) * d);
-            if (tr->out_codes) memcpy(tr->out_codes + (int64_t)i * d, w.qy, (size_t)d);
+            if (tr->out_codes)
+                for (int k = 0; k < d; ++k) tr->out_codes[(int64_t)i * d + k] = (int8_t)w.qy[k];
         }
         if (forced) {
             out_ids[n_out++] = best;

@@ -32,7 +32,7 @@ class Cfg(C.Structure):
                 ("enc_layers", C.c_int32), ("dec_layers", C.c_int32), ("vocab", C.c_int32),
                 ("decoder", C.c_int32), ("aan_ffn_depth", C.c_int32), ("aan_gate", C.c_int32),
                 ("out_bias", C.c_int32), ("eos_id", C.c_int32), ("clip", C.c_float),
-                ("ln_eps", C.c_float)]
+                ("ln_eps", C.c_float), ("arith", C.c_int32)]
 
 
 class Trace(C.Structure):
@@ -76,6 +76,8 @@ def lib():
         L.orc_beam_one.argtypes = [P, P, C.c_int, C.c_int, C.c_int, P, P, P]
         L.orc_beam_many.restype = C.c_int
         L.orc_beam_many.argtypes = [P, P, P, C.c_int, P, C.c_int, P, P, P, P, C.c_int]
+        L.orc_q16.restype = C.c_int16; L.orc_q16.argtypes = [C.c_float]
+        L.orc_dot_codes.restype = C.c_int32; L.orc_dot_codes.argtypes = [C.c_int, P, P, C.c_int]
         L.orc_logsumexp.restype = C.c_float
         L.orc_logsumexp.argtypes = [P, C.c_int]
         L.orc_max_threads.restype = C.c_int
@@ -89,9 +91,25 @@ def _p(a: Optional[np.ndarray]):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
-def cfg_from_dims(m) -> Cfg:
+# Integer arithmetic of the products (oracle only): the GPU path is ARITH_S32.
+ARITH_S32, ARITH_SAT16, ARITH_INT16 = 0, 1, 2
+
+
+def cfg_from_dims(m, arith: int = ARITH_S32) -> Cfg:
     return Cfg(m.d_model, m.d_ffn, m.n_heads, m.enc_layers, m.dec_layers, m.vocab, m.decoder,
-               m.aan_ffn_depth, m.aan_gate, m.out_bias, m.eos_id, m.clip, m.ln_eps)
+               m.aan_ffn_depth, m.aan_gate, m.out_bias, m.eos_id, m.clip, m.ln_eps, arith)
+
+
+def q16(x: float) -> int:
+    """int16 code RNE(x * 2^10), saturated."""
+    return int(lib().orc_q16(float(x)))
+
+
+def dot_codes(arith: int, a, w) -> int:
+    """One dot product of codes under the given arithmetic (0 exact, 1 sat16 pairs, 2 wrap32)."""
+    a = np.ascontiguousarray(a, dtype=np.int16); w = np.ascontiguousarray(w, dtype=np.int16)
+    assert a.shape == w.shape
+    return int(lib().orc_dot_codes(int(arith), _p(a), _p(w), a.size))
 
 
 # ------------------------------------------------------------------ scalars / kernels
@@ -220,9 +238,9 @@ def param_count(m) -> int:
 class OracleModel:
     """The oracle's model: set every parameter, quantize once."""
 
-    def __init__(self, dims, weights: Optional[Dict[str, np.ndarray]] = None):
+    def __init__(self, dims, weights: Optional[Dict[str, np.ndarray]] = None, arith: int = ARITH_S32):
         self.dims = dims
-        self._cfg = cfg_from_dims(dims)
+        self._cfg = cfg_from_dims(dims, arith)
         self.h = lib().orc_model_new(C.byref(self._cfg))
         if not self.h:
             raise ValueError("oracle: bad config")
