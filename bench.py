@@ -216,7 +216,7 @@ def live_rows_profile(sset, budget, max_concurrent_rows=0):
     return rows
 
 
-def roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr, beam=0):
+def roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr, beam=0, fused=1):
     """A9: output projection fused with argmax (beam > 0: with the beam-search log-sum-exp +
     top-8 epilogue, EPI_TOPK, at beam x the mean live-row count), at the workload's mean
     live-row count."""
@@ -233,22 +233,27 @@ def roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr, beam=0):
     qa = torch.empty((Mr, d), dtype=torch.int8, device=dev)
     M.op_quantize(x.data_ptr(), Mr * d, dims.clip, qa.data_ptr(), stream)
     b = torch.from_numpy(weights["out.b"]).to(dev)
-    if beam:
+    if beam and fused:
         part_ld = 2 * ((V + 255) // 256)
         keys = torch.empty(Mr * part_ld * M.TOPK_RECORD_BYTES, dtype=torch.uint8, device=dev)
+        epi = M.EPI_TOPK
+    elif beam:   # materialised logits (beam_fused = 0): the GEMM writes fp32 [rows x V]
+        keys = torch.empty((Mr, V), dtype=torch.float32, device=dev)
+        epi = M.EPI_F32
     else:
         keys = torch.zeros(Mr, dtype=torch.int64, device=dev)
-    epi = M.EPI_TOPK if beam else M.EPI_ARGMAX
+        epi = M.EPI_ARGMAX
 
     def fn(st):
         M.op_gemm_i8(qa.data_ptr(), qE.data_ptr(), Mr, V, d, b.data_ptr(), dims.clip,
-                     epi, keys.data_ptr(), None, beam if beam in (2, 4) else 0, st)
+                     epi, keys.data_ptr(), None, beam if (beam in (2, 4) and fused) else 0, st)
     ms = time_kernel(fn, 200, stream)
     ops = 2.0 * Mr * V * d
     peak = 2.0 * peaks["bf16_tflops"]          # int8 dense = 2x bf16 (nominal 4.5 / 2.25)
     ach = ops / (ms * 1e-3) / 1e12
     name = (f"k_gemm_i8<256, EPI_TOPK{beam if beam in (2, 4) else ''}> (A9 beam output GEMM + "
-            f"fp64 log-sum-exp + top-{beam if beam in (2, 4) else 8})" if beam
+            f"fp64 log-sum-exp + top-{beam if beam in (2, 4) else 8})" if beam and fused
+            else "k_gemm_i8<EPI_F32> (A9 beam output GEMM writing fp32 logits)" if beam
             else "k_gemm_i8<EPI_ARGMAX> (A9 output GEMM + argmax)")
     return {"kernel": name, "bound": "tensor",
             "achieved": ach, "peak": peak, "unit": "TOP/s (int8)", "frac": ach / peak,
@@ -520,7 +525,7 @@ def main():
         peaks = load_peaks()
         mcr = args.max_concurrent_rows
         cands = [roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr,
-                                   beam if beam > 1 else 0),
+                                   beam if beam > 1 else 0, args.beam_fused),
                  roofline_src_attn(dims, sset, budget, peaks, stream, mcr, nb),
                  roofline_dxd_gemm(dims, sset, budget, peaks, stream, mcr, nb)]
         cands[1]["launches_per_step"] = len(live_rows_profile(sset, budget, mcr)) * dims.dec_layers

@@ -675,8 +675,25 @@ static void out_logits(const orc_model *m, const float *y, int16_t *qy, float *l
  * forced != NULL: teacher forcing for max_len steps; the input at step t >= 2
  * is forced[t-2]; every step's argmax is recorded in trace/out_ids.
  * Returns the number of ids written to out_ids, or <0 on error. */
+static int decode_impl(const orc_model *m, const int32_t *src, int S, int max_len,
+                       const int32_t *forced, const int32_t *sl, int n_sl, int32_t *out_ids,
+                       orc_trace *tr);
+
 int orc_decode_one(const orc_model *m, const int32_t *src, int S, int max_len,
                    const int32_t *forced, int32_t *out_ids, orc_trace *tr) {
+    return decode_impl(m, src, S, max_len, forced, NULL, 0, out_ids, tr);
+}
+
+/* Greedy decode restricted to a vocabulary shortlist: the argmax runs
+ * over the ids sl[0..n_sl) only (ascending, so the lowest id still wins ties, R15). */
+int orc_decode_one_sl(const orc_model *m, const int32_t *src, int S, int max_len,
+                      const int32_t *sl, int n_sl, int32_t *out_ids) {
+    return decode_impl(m, src, S, max_len, NULL, sl, n_sl, out_ids, NULL);
+}
+
+static int decode_impl(const orc_model *m, const int32_t *src, int S, int max_len,
+                       const int32_t *forced, const int32_t *sl, int n_sl, int32_t *out_ids,
+                       orc_trace *tr) {
     const orc_cfg *c = &m->c;
     int d = c->d_model, L = c->dec_layers, V = c->vocab;
     if (!m->quantized) return -4;
@@ -699,7 +716,8 @@ int orc_decode_one(const orc_model *m, const int32_t *src, int S, int max_len,
         out_logits(m, w.y, w.qy, logits);
         int best = -1, second = -1;
         float bv = 0.0f, sv = 0.0f;
-        for (int j = 0; j < V; ++j) {
+        for (int u = 0; u < (sl ? n_sl : V); ++u) {
+            int j = sl ? sl[u] : u;
             float lg = logits[j];
             if (best < 0 || lg > bv) { second = best; sv = bv; best = j; bv = lg; }
             else if (second < 0 || lg > sv) { second = j; sv = lg; }
@@ -914,6 +932,54 @@ int orc_decode_many(const orc_model *m, const int32_t *src_ids, const int64_t *s
     for (int i = 0; i < n; ++i) {
         int r = orc_decode_one(m, src_ids + src_off[i], (int)(src_off[i + 1] - src_off[i]),
                                max_len[i], NULL, out_ids + oo[i], NULL);
+        if (r < 0) err = -r; else out_len[i] = r;
+    }
+    free(oo);
+    return err;
+}
+
+/* ------------------------------------------------------------ shortlist (F2) */
+/* Vocabulary shortlist of one batch ("the union of the 100 most frequent target words and
+ * the 100 most probable translations for every source word in a batch"):
+ *   freq[0..n_freq)                      the most frequent target ids (in frequency order)
+ *   lex[s * k_lex + 0..k_lex)            the most probable translations of source id s
+ * shortlist = freq ∪ {lex[s][k] : s a source id of the batch} ∪ {EOS, UNK}, deduplicated,
+ * ascending.  Ids outside [0, V) are ignored.  Writes out[0..count) (capacity V), returns count. */
+int orc_build_shortlist(int V, const int32_t *freq, int n_freq, const int32_t *lex, int k_lex,
+                        const int32_t *src_ids, int64_t n_src, int eos, int unk, int32_t *out) {
+    char *in = (char *)calloc((size_t)V, 1);
+    for (int i = 0; i < n_freq; ++i) if (freq[i] >= 0 && freq[i] < V) in[freq[i]] = 1;
+    for (int64_t t = 0; t < n_src; ++t) {
+        int s = src_ids[t];
+        if (s < 0 || s >= V) continue;
+        for (int k = 0; k < k_lex; ++k) {
+            int j = lex[(int64_t)s * k_lex + k];
+            if (j >= 0 && j < V) in[j] = 1;
+        }
+    }
+    if (eos >= 0 && eos < V) in[eos] = 1;
+    if (unk >= 0 && unk < V) in[unk] = 1;
+    int n = 0;
+    for (int j = 0; j < V; ++j) if (in[j]) out[n++] = j;
+    free(in);
+    return n;
+}
+
+/* orc_decode_many with every sentence restricted to the same shortlist (one batch). */
+int orc_decode_many_sl(const orc_model *m, const int32_t *src_ids, const int64_t *src_off, int n,
+                       const int32_t *max_len, const int32_t *sl, int n_sl, int32_t *out_ids,
+                       int32_t *out_len, int nthreads) {
+    int64_t *oo = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+    oo[0] = 0;
+    for (int i = 0; i < n; ++i) oo[i + 1] = oo[i] + max_len[i];
+    int err = 0;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1)
+#endif
+    for (int i = 0; i < n; ++i) {
+        int r = orc_decode_one_sl(m, src_ids + src_off[i], (int)(src_off[i + 1] - src_off[i]),
+                                  max_len[i], sl, n_sl, out_ids + oo[i]);
         if (r < 0) err = -r; else out_len[i] = r;
     }
     free(oo);

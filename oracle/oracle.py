@@ -76,6 +76,11 @@ def lib():
         L.orc_beam_one.argtypes = [P, P, C.c_int, C.c_int, C.c_int, P, P, P]
         L.orc_beam_many.restype = C.c_int
         L.orc_beam_many.argtypes = [P, P, P, C.c_int, P, C.c_int, P, P, P, P, C.c_int]
+        L.orc_build_shortlist.restype = C.c_int
+        L.orc_build_shortlist.argtypes = [C.c_int, P, C.c_int, P, C.c_int, P, C.c_int64, C.c_int,
+                                          C.c_int, P]
+        L.orc_decode_many_sl.restype = C.c_int
+        L.orc_decode_many_sl.argtypes = [P, P, P, C.c_int, P, P, C.c_int, P, P, C.c_int]
         L.orc_q16.restype = C.c_int16; L.orc_q16.argtypes = [C.c_float]
         L.orc_dot_codes.restype = C.c_int32; L.orc_dot_codes.argtypes = [C.c_int, P, P, C.c_int]
         L.orc_logsumexp.restype = C.c_float
@@ -341,6 +346,25 @@ class OracleModel:
             o += T
         return res
 
+    def decode_many_sl(self, sset, shortlist: np.ndarray, nthreads: int = 0):
+        """decode_many with every sentence restricted to `shortlist` (one batch, F2)."""
+        n = sset.n
+        ml = np.ascontiguousarray(sset.max_len, dtype=np.int32)
+        out = np.zeros(max(int(ml.sum()), 1), np.int32)
+        out_len = np.zeros(max(n, 1), np.int32)
+        ids = np.ascontiguousarray(sset.ids, dtype=np.int32)
+        offs = np.ascontiguousarray(sset.offsets, dtype=np.int64)
+        sl = np.ascontiguousarray(shortlist, dtype=np.int32)
+        st = lib().orc_decode_many_sl(self.h, _p(ids), _p(offs), n, _p(ml), _p(sl), sl.size,
+                                      _p(out), _p(out_len), nthreads)
+        if st:
+            raise ValueError(f"oracle: decode_many_sl status {st}")
+        res, o = [], 0
+        for i in range(n):
+            res.append(out[o:o + out_len[i]].copy())
+            o += int(ml[i])
+        return res
+
     def decode_many(self, sset, nthreads: int = 0):
         """Free-running greedy decode of a SentenceSet; returns list of id arrays."""
         n = sset.n
@@ -359,6 +383,19 @@ class OracleModel:
             res.append(out[o:o + out_len[i]].copy())
             o += int(ml[i])
         return res
+
+
+def build_shortlist(V: int, freq: np.ndarray, lex: np.ndarray, src_ids: np.ndarray,
+                    eos: int = 0, unk: int = 1) -> np.ndarray:
+    """Batch shortlist: freq ∪ lex rows of the batch's source ids ∪ {EOS,
+    UNK}, ascending.  lex: [V x k_lex] int32."""
+    freq = np.ascontiguousarray(freq, np.int32)
+    lex = np.ascontiguousarray(lex, np.int32)
+    src = np.ascontiguousarray(src_ids, np.int32)
+    out = np.zeros(V, np.int32)
+    n = lib().orc_build_shortlist(V, _p(freq), freq.size, _p(lex), lex.shape[1] if lex.ndim == 2 else 0,
+                                  _p(src), src.size, eos, unk, _p(out))
+    return out[:n].copy()
 
 
 def logsumexp(logits: np.ndarray) -> float:

@@ -1,5 +1,6 @@
 """One full translation job (after 2 warm-up jobs) inside an NVTX range "job", for an ncu
-launch list of exactly one job:  ncu --nvtx --nvtx-include "job/" ... python scripts/job_once.py"""
+launch list of exactly one job:  ncu --nvtx --nvtx-include "job/" ... python scripts/job_once.py
+(env PRESET, MCR, BEAM)"""
 import os, sys
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -13,7 +14,16 @@ dev = torch.device("cuda:0"); st = torch.cuda.current_stream()
 ids = torch.from_numpy(ss.ids).to(dev)
 cap = int(ss.max_len.sum())
 out = torch.zeros(cap, dtype=torch.int32, device=dev); ln = torch.zeros(ss.n, dtype=torch.int32, device=dev)
-f = lambda: m.translate_device(ids.data_ptr(), ss.offsets, ss.max_len, 8192, out.data_ptr(), cap, ln.data_ptr(), st)
+beam = int(os.environ.get("BEAM", 0))   # > 0: beam search job (mnmt_beam_translate)
+if beam:
+    out = torch.zeros(cap * beam, dtype=torch.int32, device=dev)
+    ln = torch.zeros(ss.n * beam, dtype=torch.int32, device=dev)
+    sc = torch.zeros(ss.n * beam, dtype=torch.float32, device=dev)
+    nh = torch.zeros(ss.n, dtype=torch.int32, device=dev)
+    f = lambda: m.beam_translate_device(ids.data_ptr(), ss.offsets, ss.max_len, 8192, beam, out.data_ptr(),
+                                        cap * beam, ln.data_ptr(), sc.data_ptr(), nh.data_ptr(), st)
+else:
+    f = lambda: m.translate_device(ids.data_ptr(), ss.offsets, ss.max_len, 8192, out.data_ptr(), cap, ln.data_ptr(), st)
 f(); f(); torch.cuda.synchronize()
 torch.cuda.nvtx.range_push("job"); f(); torch.cuda.nvtx.range_pop(); torch.cuda.synchronize()
 s = m.stats(); print("launches", s["gpu_launches"], "steps", s["decode_steps"], "words", int(ln.sum()))

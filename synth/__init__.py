@@ -212,3 +212,27 @@ def uniform_activations(shape, seed: int = 3, scale: float = 2.5) -> np.ndarray:
     """Generic fp32 operand for kernel-level parity (values beyond +-clip included)."""
     rng = np.random.default_rng(seed)
     return rng.uniform(-scale, scale, size=shape).astype(np.float32)
+
+
+def shortlist_tables(vocab: int = VOCAB, n_freq: int = 100, k_lex: int = 100, seed: int = 85,
+                     zipf: float = 1.1):
+    """Synthetic lexical shortlist tables (SPEC.md:L497 format):
+    `freq` = the n_freq most frequent target ids (a seeded frequency ranking of the vocabulary),
+    `lex` [vocab x k_lex] = for every source id, k_lex distinct target ids in descending
+    translation probability, drawn from a Zipf(zipf) law over the frequency ranking (frequent
+    words are likely translations of many source words, so batch unions overlap).  Random
+    numbers only; the union itself is the method's and lives in oracle/ and the CUDA path."""
+    rng = np.random.default_rng(seed)
+    rank = rng.permutation(vocab).astype(np.int32)         # rank[r] = id of the r-th most frequent
+    cdf = np.cumsum(1.0 / np.arange(1, vocab + 1, dtype=np.float64) ** zipf)
+    cdf /= cdf[-1]
+    draws = np.minimum(np.searchsorted(cdf, rng.random((vocab, 3 * k_lex))), vocab - 1)
+    lex = np.empty((vocab, k_lex), np.int32)
+    for s in range(vocab):
+        _, first = np.unique(draws[s], return_index=True)
+        r = draws[s][np.sort(first)][:k_lex]               # distinct ranks in draw order
+        if r.size < k_lex:                                 # top up with uniform distinct ranks
+            extra = rng.permutation(np.setdiff1d(np.arange(vocab), r))[:k_lex - r.size]
+            r = np.concatenate([r, extra])
+        lex[s] = rank[r]
+    return rank[:n_freq].copy(), lex
