@@ -104,18 +104,56 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- oracle legs
-def _oracle_run(om, subset, beam):
-    """Target words of one oracle pass (beam > 1: words of each sentence's best hypothesis)."""
+def _oracle_run(om, subset, beam, sl=None):
+    """Target words of one oracle pass (beam > 1: words of each sentence's best hypothesis;
+    sl: the shortlist of every sentence's word-budget batch, decoded batch by batch)."""
+    if sl is not None:
+        return _oracle_run_sl(om, subset, *sl)
     if beam > 1:
         return sum(len(h[0][0]) if h else 0 for h in om.beam_many(subset, beam, 0))
     return sum(len(o) for o in om.decode_many(subset, 0))
 
 
-def oracle_sample(sset, dims, weights, seconds: float, seed: int = 99, beam: int = 1):
+def _oracle_run_sl(om, subset, bb_of, lists):
+    """F2 oracle leg: the sample's sentences grouped by their word-budget batch, each group
+    decoded over that batch's shortlist (orc_decode_many_sl)."""
+    idx = subset.idx
+    words = 0
+    for b in sorted(set(bb_of[idx].tolist())):
+        sub = subset.sset.subset(idx[bb_of[idx] == b])
+        words += sum(len(o) for o in om.decode_many_sl(sub, lists[b], 0))
+    return words
+
+
+class _Sample:
+    """A subset that remembers its indices (for the shortlist leg)."""
+    def __init__(self, sset, idx):
+        self.sset, self.idx = sset, np.asarray(idx)
+        sub = sset.subset(self.idx)
+        self.max_len, self.lengths = sub.max_len, sub.lengths
+
+
+def oracle_shortlists(sset, dims, budget, freq, lex):
+    """Per sentence its word-budget batch and per batch its shortlist."""
+    import oracle.oracle as O
+    order, off = O.batch_by_words(sset.lengths, budget)
+    bb_of = np.empty(sset.n, np.int64)
+    lists = []
+    for b in range(len(off) - 1):
+        rows = order[off[b]:off[b + 1]]
+        bb_of[rows] = b
+        lists.append(O.build_shortlist(dims.vocab, freq, lex, sset.subset(rows).ids,
+                                       eos=dims.eos_id, unk=1))
+    return bb_of, lists
+
+
+def oracle_sample(sset, dims, weights, seconds: float, seed: int = 99, beam: int = 1, sl=None):
     """Decode a seeded random sample of the workload with the oracle, sized to ~`seconds`.
     Returns (target words/s, threads, description)."""
     import oracle.oracle as O
     om = O.OracleModel(dims, weights)
+    if sl is not None:
+        return _oracle_sample_sl(om, O, sset, seconds, seed, sl)
     threads = O.max_threads()
     rng = np.random.default_rng(seed)
     perm = rng.permutation(sset.n)
@@ -134,6 +172,23 @@ def oracle_sample(sset, dims, weights, seconds: float, seed: int = 99, beam: int
     desc = (f"oracle {mode} decode of {n} of {sset.n} sentences (seeded random sample, "
             f"{int(samp.lengths.sum())} source / {words} target words, one batch per sentence, "
             f"OpenMP over sentences) in {dt:.1f} s")
+    return words / dt, threads, desc, dt
+
+
+def _oracle_sample_sl(om, O, sset, seconds, seed, sl):
+    threads = O.max_threads()
+    perm = np.random.default_rng(seed).permutation(sset.n)
+    probe = _Sample(sset, perm[:max(threads, 8)])
+    t0 = time.perf_counter()
+    rate = _oracle_run(om, probe, 1, sl) / max(time.perf_counter() - t0, 1e-9)
+    n = int(min(sset.n, max(len(probe.idx), rate * seconds / max(float(np.mean(probe.max_len)), 1.0))))
+    samp = _Sample(sset, perm[:n])
+    t0 = time.perf_counter()
+    words = _oracle_run(om, samp, 1, sl)
+    dt = time.perf_counter() - t0
+    desc = (f"oracle greedy decode restricted to each sentence's batch shortlist (P:L85) of {n} of "
+            f"{sset.n} sentences (seeded random sample, {int(samp.lengths.sum())} source / {words} "
+            f"target words, OpenMP over sentences) in {dt:.1f} s")
     return words / dt, threads, desc, dt
 
 
@@ -216,10 +271,11 @@ def live_rows_profile(sset, budget, max_concurrent_rows=0):
     return rows
 
 
-def roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr, beam=0, fused=1):
+def roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr, beam=0, fused=1,
+                      n_cols=None):
     """A9: output projection fused with argmax (beam > 0: with the beam-search log-sum-exp +
     top-8 epilogue, EPI_TOPK, at beam x the mean live-row count), at the workload's mean
-    live-row count."""
+    live-row count (n_cols: the mean shortlist size, F2)."""
     import torch
     from paper_1805_12096_b200 import mnmt as M
     rows = live_rows_profile(sset, budget, mcr)
@@ -244,20 +300,22 @@ def roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr, beam=0, f
         keys = torch.zeros(Mr, dtype=torch.int64, device=dev)
         epi = M.EPI_ARGMAX
 
+    N = int(n_cols) if n_cols else V
+
     def fn(st):
-        M.op_gemm_i8(qa.data_ptr(), qE.data_ptr(), Mr, V, d, b.data_ptr(), dims.clip,
+        M.op_gemm_i8(qa.data_ptr(), qE.data_ptr(), Mr, N, d, b.data_ptr(), dims.clip,
                      epi, keys.data_ptr(), None, beam if (beam in (2, 4) and fused) else 0, st)
     ms = time_kernel(fn, 200, stream)
-    ops = 2.0 * Mr * V * d
+    ops = 2.0 * Mr * N * d
     peak = 2.0 * peaks["bf16_tflops"]          # int8 dense = 2x bf16 (nominal 4.5 / 2.25)
     ach = ops / (ms * 1e-3) / 1e12
     name = (f"k_gemm_i8<256, EPI_TOPK{beam if beam in (2, 4) else ''}> (A9 beam output GEMM + "
             f"fp64 log-sum-exp + top-{beam if beam in (2, 4) else 8})" if beam and fused
             else "k_gemm_i8<EPI_F32> (A9 beam output GEMM writing fp32 logits)" if beam
-            else "k_gemm_i8<EPI_ARGMAX> (A9 output GEMM + argmax)")
+            else "k_gemm_i8<EPI_ARGMAX> (A9 output GEMM + argmax" + (", shortlist)" if n_cols else ")"))
     return {"kernel": name, "bound": "tensor",
             "achieved": ach, "peak": peak, "unit": "TOP/s (int8)", "frac": ach / peak,
-            "traffic": None, "shape": f"M={Mr} (mean live rows/step) N={V} K={d}",
+            "traffic": None, "shape": f"M={Mr} (mean live rows/step) N={N} K={d}",
             "ms_per_launch": ms, "launches_per_step": len(rows),
             "ms_per_step_est": ms * len(rows) * 1.0,
             "peak_source": f"{peaks['source']} bf16 burst x2"}
@@ -342,7 +400,9 @@ def ncu_traffic(key, shape):
 
 
 # ---------------------------------------------------------------------------- main
-def metric_name(beam: int) -> str:
+def metric_name(beam: int, shortlist: bool = False) -> str:
+    if shortlist:
+        return "target words/sec greedy decode with batch vocabulary shortlist (100 frequent + 100 per source word), 1 B200"
     return METRIC if beam <= 1 else f"target words/sec beam-{beam} decode (best hypothesis), 1 B200"
 
 
@@ -360,6 +420,9 @@ def main():
     ap.add_argument("--beam", type=int, default=1,
                     help="1 (default): greedy decode, the headline; 2..8: beam search "
                          "(SURVEY 8(f) F1, mnmt_beam_translate); words = best hypothesis")
+    ap.add_argument("--shortlist", action="store_true",
+                    help="greedy decode with each batch's vocabulary shortlist (SURVEY 8(f) F2, "
+                         "P:L85; synthetic Zipf tables, 100 frequent + 100 per source word)")
     ap.add_argument("--beam-fused", type=int, default=0,
                     help="beam search: 1 = log-sum-exp / top-k fused into the output GEMM epilogue")
     ap.add_argument("--megakernel", type=int, default=0,
@@ -398,7 +461,8 @@ def main():
                                f"decoder={'AAN' if dims.decoder else 'self-attn'}",
                     "sentences_per_gpu": synth.NEWSTEST_SENTENCES,
                     "source_words_per_gpu": synth.NEWSTEST_TOKENS, "word_budget": budget,
-                    "beam": args.beam, "beam_fused": args.beam_fused, "max_len": "source length", "parallelism": f"dp{args.gpus}",
+                    "beam": args.beam, "beam_fused": args.beam_fused,
+                    "shortlist": "100 frequent + 100 per source word (synthetic Zipf tables, seed 85)" if args.shortlist else None, "max_len": "source length", "parallelism": f"dp{args.gpus}",
                     "l2": "flushed between timed steps (512 MiB write)",
                     "max_concurrent_rows": args.max_concurrent_rows, "lanes": args.lanes,
                     "fuse_ln": args.fuse_ln, "steps_per_graph": args.steps_per_graph,
@@ -435,6 +499,12 @@ def main():
     model.set_option("rowfuse", args.rowfuse)
     model.set_option("beam_fused", args.beam_fused)
     sset = synth.newstest_set(seed=2014 + rank)          # weak scaling: one set per GPU
+    use_sl = bool(args.shortlist)
+    if use_sl:
+        if args.beam > 1:
+            raise SystemExit("--shortlist is greedy only")
+        sl_freq, sl_lex = synth.shortlist_tables(dims.vocab, 100, 100, seed=85)
+        model.set_shortlist(sl_freq, sl_lex)
     stream = torch.cuda.current_stream()
     dev = torch.device("cuda", local)
     ids_dev = torch.from_numpy(sset.ids).to(dev)
@@ -454,7 +524,8 @@ def main():
                                         score_dev.data_ptr(), nhyp_dev.data_ptr(), stream)
         else:
             model.translate_device(ids_dev.data_ptr(), sset.offsets, sset.max_len, budget,
-                                   out_dev.data_ptr(), cap, len_dev.data_ptr(), stream)
+                                   out_dev.data_ptr(), cap, len_dev.data_ptr(), stream,
+                                   shortlist=use_sl)
             if dist_on:
                 D.gather_ids(out_dev, len_dev)
 
@@ -498,7 +569,7 @@ def main():
     def host_call():
         if beam > 1:
             return model.beam_translate(sset, budget, beam, stream)
-        return model.translate(sset, budget, stream)
+        return model.translate(sset, budget, stream, shortlist=use_sl)
 
     host_call()
     torch.cuda.synchronize()
@@ -521,11 +592,14 @@ def main():
 
     roof = None
     cpu = None
+    sl_lists = None
     if rank == 0 and not args.no_roofline:
         peaks = load_peaks()
-        mcr = args.max_concurrent_rows
+        mcr = 0 if use_sl else args.max_concurrent_rows   # shortlist: one batch per wave
+        sl_lists = oracle_shortlists(sset, dims, budget, sl_freq, sl_lex) if use_sl else None
+        n_cols = float(np.mean([len(x) for x in sl_lists[1]])) if use_sl else None
         cands = [roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr,
-                                   beam if beam > 1 else 0, args.beam_fused),
+                                   beam if beam > 1 else 0, args.beam_fused, n_cols),
                  roofline_src_attn(dims, sset, budget, peaks, stream, mcr, nb),
                  roofline_dxd_gemm(dims, sset, budget, peaks, stream, mcr, nb)]
         cands[1]["launches_per_step"] = len(live_rows_profile(sset, budget, mcr)) * dims.dec_layers
@@ -537,12 +611,13 @@ def main():
         roof["other"] = {c["kernel"]: {"frac": c["frac"], "ms_per_step_est": c["ms_per_step_est"]}
                          for c in cands if c is not roof}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, cores, desc, _ = oracle_sample(sset, dims, weights, args.cpu_seconds, beam=beam)
+        sl = (sl_lists or oracle_shortlists(sset, dims, budget, sl_freq, sl_lex)) if use_sl else None
+        v, cores, desc, _ = oracle_sample(sset, dims, weights, args.cpu_seconds, beam=beam, sl=sl)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
 
     if rank == 0:
         line = {
-            "metric": metric_name(beam), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": metric_name(beam, use_sl), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int8 products (s32 acc), f32 activations, f64 reductions",
             "data": "synthetic (seeded random-init weights, newstest2014-shaped length-sorted ids)",

@@ -114,10 +114,30 @@ mnmt_status mnmt_decode(mnmt_model* m, const int32_t* src_ids_host, const int64_
  * ids are already resident in HBM; offsets and max_len stay host arrays).
  * Errors as mnmt_decode. */
 #define MNMT_DEVICE_IO 1u
+/* flags & MNMT_SHORTLIST: vocabulary shortlist ("the union of the 100
+ * most frequent target words and the 100 most probable translations for every source word in a
+ * batch").  Every word-budget batch decodes with the argmax restricted to its
+ * shortlist = freq ∪ {lex[s][k] : s a source id of the batch} ∪ {eos_id, MNMT_UNK_ID} (the
+ * tables of mnmt_model_set_shortlist; ids outside [0, vocab) ignored), ascending, so the lowest
+ * id still wins ties (R15, R32-R34).  Each word-budget batch then forms its own decode wave
+ * (max_concurrent_rows is not applied).  Greedy only.
+ * Errors: MNMT_ERR_STATE without tables, MNMT_ERR_ARG with beam search. */
+#define MNMT_SHORTLIST 2u
+#define MNMT_UNK_ID 1   /* reserved ids EOS/UNK/PAD = 0/1/2 */
 mnmt_status mnmt_translate(mnmt_model* m, const int32_t* src_ids, const int64_t* src_off_host,
                            int32_t n, const int32_t* max_len_host, int32_t word_budget,
                            int32_t* out_ids, int64_t out_cap, int32_t* out_len, uint32_t flags,
                            void* cuda_stream);
+
+/* Shortlist tables (S:L435-443, S:L497 format), copied to the device:
+ *   freq[0..n_freq)          the most frequent target ids (host int32; any order)
+ *   lex[s * k_lex + k]       the k_lex most probable translations of source id s, s < vocab
+ *                            (host int32 [vocab x k_lex]; entries outside [0, vocab), e.g. -1
+ *                            as padding, are ignored)
+ * Replaces earlier tables.  Errors: MNMT_ERR_ARG (negative sizes, NULL non-empty table),
+ * MNMT_ERR_CUDA. */
+mnmt_status mnmt_model_set_shortlist(mnmt_model* m, const int32_t* freq, int32_t n_freq,
+                                     const int32_t* lex, int32_t k_lex);
 
 /* Beam search over the same word-budget batches as mnmt_translate: the
  * b = 2 / 4 systems of Table 3 (rows 5, 6, 8, 9, 11, 12).  Per step,

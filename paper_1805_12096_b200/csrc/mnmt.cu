@@ -26,6 +26,7 @@
 #include "kernels.h"
 #include "rowops.h"
 #include "rowfused.h"
+#include "shortlist.h"
 #include "stepkernel.h"
 
 using namespace mnmt;
@@ -106,6 +107,13 @@ struct Workspace {
   int32_t *sent_list = nullptr, *child_par = nullptr, *child_tok = nullptr, *hist = nullptr;
   int32_t* anc = nullptr;
   float* logits = nullptr;   // [B_cap][V] (beam_fused = 0)
+  // vocabulary shortlist (F2; allocated on first use by sl_lane_ensure): the decode unit's
+  // shortlist rows of the int8 E and of the output bias, and column -> id
+  std::vector<void*> sl_allocs;
+  int8_t* sl_q = nullptr;
+  float* sl_b = nullptr;
+  int32_t* sl_map = nullptr;
+  CUtensorMap tm_sl;
 };
 
 // Job-level device buffers shared by all lanes.
@@ -120,6 +128,14 @@ struct JobBuf {
   int64_t* rmeta64 = nullptr;   // [out_off|forced_off] x B_b
   float* out_score = nullptr;   // beam search: [n x beam] hypothesis scores
   int32_t* n_hyp = nullptr;     // beam search: [n] hypotheses per sentence
+  // vocabulary shortlist (F2): per word-budget batch bitmap, ascending ids and count, and the
+  // batch-major sentence spans the bitmap kernel walks
+  std::vector<void*> sl_allocs;
+  int64_t sl_bb_cap = 0, sl_sent_cap = 0;
+  uint32_t* sl_bits = nullptr;  // [bb][ceil(V/32)]
+  int32_t* sl_ids = nullptr;    // [bb][V]
+  int32_t* sl_n = nullptr;      // [bb]
+  int32_t* sl_span = nullptr;   // [start | len] x sentences (batch-major), then bb_off [bb + 1]
 };
 
 // A lane = one independent decoder (workspace + stream + step graphs).  Rows are
@@ -144,6 +160,7 @@ struct Lane {
   std::vector<int> phase_types;             // host copy, for profiling
   unsigned long long* d_timing = nullptr;   // phase timestamps of the last launch (option)
   int64_t timing_steps = 0;
+  int sl_n = 0;                             // columns of the shortlisted output GEMM (0 = full V)
 };
 
 }  // namespace
@@ -188,6 +205,12 @@ struct mnmt_model {
   int beam = 0;                        // (call state) beam size of the running call; 0 = greedy
   int beam_fused = 0;                  // option: 1 = log-sum-exp / top-k in the output GEMM epilogue
                                        // (EPI_TOPK*), 0 = fp32 logits + k_beam_logits (faster)
+  // vocabulary shortlist tables (F2, mnmt_model_set_shortlist)
+  int32_t *sl_freq = nullptr, *sl_lex = nullptr;
+  int sl_nfreq = 0, sl_k = 0;
+  bool sl_tables = false;
+  bool sl_active = false;              // (call state) MNMT_SHORTLIST
+  std::vector<int32_t> sl_count;       // (call state) shortlist size of each word-budget batch
 };
 
 namespace {
@@ -342,6 +365,8 @@ static void lane_free(Lane& L) {
   L.graphs.clear();
   for (void* p : L.ws.allocs) cudaFree(p);
   for (void* p : L.ws.beam_allocs) cudaFree(p);
+  for (void* p : L.ws.sl_allocs) cudaFree(p);
+  L.sl_n = 0;
   L.ws = Workspace();
   if (L.d_phases) cudaFree(L.d_phases);
   if (L.d_tmaps) cudaFree(L.d_tmaps);
@@ -357,6 +382,7 @@ static void lane_free(Lane& L) {
 
 static void jb_free(mnmt_model* m) {
   for (void* p : m->jb.allocs) cudaFree(p);
+  for (void* p : m->jb.sl_allocs) cudaFree(p);
   m->jb = JobBuf();
 }
 
@@ -530,6 +556,79 @@ static mnmt_status beam_ensure(mnmt_model* m, Lane& Ln) {
   CKS(dalloc(A, &w.logits, R * (((int64_t)m->c.vocab + 15) / 16 * 16)));
   w.beam_rows = R;
   w.beam_T = T;
+  return MNMT_OK;
+}
+
+// Shortlist operand of a lane (F2): [V x d] int8 rows + bias + id map, allocated once.
+static mnmt_status sl_lane_ensure(mnmt_model* m, Lane& Ln) {
+  Workspace& w = Ln.ws;
+  if (w.sl_q) return MNMT_OK;
+  const int64_t V = m->c.vocab, d = m->c.d_model;
+  CKS(dalloc(w.sl_allocs, &w.sl_q, V * d));
+  CKS(dalloc(w.sl_allocs, &w.sl_b, V));
+  CKS(dalloc(w.sl_allocs, &w.sl_map, V));
+  if (!make_tmap_i8(&w.tm_sl, w.sl_q, V, d)) { set_err("tensor map (shortlist) failed"); return MNMT_ERR_CUDA; }
+  return MNMT_OK;
+}
+
+// Job-level shortlist buffers for n_bb word-budget batches of n sentences.
+static mnmt_status sl_job_ensure(mnmt_model* m, int64_t n_bb, int64_t n) {
+  JobBuf& j = m->jb;
+  if (n_bb <= j.sl_bb_cap && n <= j.sl_sent_cap) return MNMT_OK;
+  CK(cudaDeviceSynchronize());
+  for (void* p : j.sl_allocs) cudaFree(p);
+  j.sl_allocs.clear();
+  const int64_t V = m->c.vocab, W = (V + 31) / 32;
+  j.sl_bb_cap = std::max(n_bb, j.sl_bb_cap);
+  j.sl_sent_cap = std::max(n, j.sl_sent_cap);
+  CKS(dalloc(j.sl_allocs, &j.sl_bits, j.sl_bb_cap * W));
+  CKS(dalloc(j.sl_allocs, &j.sl_ids, j.sl_bb_cap * V));
+  CKS(dalloc(j.sl_allocs, &j.sl_n, j.sl_bb_cap));
+  CKS(dalloc(j.sl_allocs, &j.sl_span, 2 * j.sl_sent_cap + j.sl_bb_cap + 1));
+  return MNMT_OK;
+}
+
+// Builds the shortlist of every word-budget batch of the job on the device (one bitmap pass,
+// one compaction) and reads the sizes back (one synchronisation per job, before decoding; the
+// output GEMM's N is a launch parameter of the step graphs).  bb_sents: batch-major sentence
+// indices; bb_off: [n_bb + 1].
+static mnmt_status sl_build_job(mnmt_model* m, const int64_t* src_off,
+                                const std::vector<int32_t>& bb_sents,
+                                const std::vector<int32_t>& bb_off) {
+  const int n_bb = (int)bb_off.size() - 1;
+  const int64_t ns = (int64_t)bb_sents.size();
+  CKS(sl_job_ensure(m, n_bb, ns));
+  JobBuf& j = m->jb;
+  std::vector<int32_t> span(2 * ns + n_bb + 1);
+  for (int64_t i = 0; i < ns; ++i) {
+    const int s = bb_sents[i];
+    span[i] = (int32_t)src_off[s];
+    span[ns + i] = (int32_t)(src_off[s + 1] - src_off[s]);
+  }
+  std::copy(bb_off.begin(), bb_off.end(), span.begin() + 2 * ns);
+  CK(cudaMemcpyAsync(j.sl_span, span.data(), span.size() * 4, cudaMemcpyHostToDevice, m->st));
+  m->stats.h2d_bytes += (int64_t)span.size() * 4;
+  SlMarkArgs a{};
+  a.V = m->c.vocab;
+  a.W = (m->c.vocab + 31) / 32;
+  a.src_ids = j.src_ids;
+  a.sent_start = j.sl_span;
+  a.sent_len = j.sl_span + ns;
+  a.bb_off = j.sl_span + 2 * ns;
+  a.freq = m->sl_freq;
+  a.n_freq = m->sl_nfreq;
+  a.lex = m->sl_lex;
+  a.k_lex = m->sl_k;
+  a.eos = m->c.eos_id;
+  a.unk = MNMT_UNK_ID;
+  a.bits = j.sl_bits;
+  CK(launch_sl_build(a, n_bb, j.sl_ids, j.sl_n, m->st));
+  m->stats.gpu_launches += 2;
+  m->sl_count.assign(n_bb, 0);
+  if (n_bb > 0) {
+    CK(cudaMemcpyAsync(m->sl_count.data(), j.sl_n, n_bb * 4, cudaMemcpyDeviceToHost, m->st));
+    CK(cudaStreamSynchronize(m->st));
+  }
   return MNMT_OK;
 }
 
@@ -1060,18 +1159,21 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
   // A9: tied output projection fused with the argmax (softmax skipped)
   {
     GemmArgs a{};
+    // shortlist (F2): the GEMM runs over the decode unit's Ln.sl_n gathered rows of qE
+    const bool sl = Ln.sl_n > 0;
     a.M = n;
     a.M_dyn = nd;
-    a.N = c.vocab;
+    a.N = sl ? Ln.sl_n : c.vocab;
     a.K = d;
     a.scale = scale_of(m);
-    a.bias = c.out_bias ? m->out_b : nullptr;
+    a.bias = c.out_bias ? (sl ? w.sl_b : m->out_b) : nullptr;
     a.clip = c.clip;
     a.sigma = sigma_of(m);
-    a.col_block = c.vocab;
+    a.col_block = a.N;
     a.keys = w.keys;
     a.pers_grid = m->cur_pers_grid;
-    if ((e = launch_gemm_i8(w.tm_cy, m->tmE, a, EPI_ARGMAX, 0, st)) != cudaSuccess) return e;
+    if ((e = launch_gemm_i8(w.tm_cy, sl ? w.tm_sl : m->tmE, a, EPI_ARGMAX, 0, st)) != cudaSuccess)
+      return e;
   }
   // A10: finish + compaction
   FinishArgs fa{};
@@ -1092,6 +1194,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
   fa.row_len = w.row_len;
   fa.live_start = w.live_start;
   fa.live_len = w.live_len;
+  fa.id_map = Ln.sl_n > 0 ? w.sl_map : nullptr;
   if ((e = launch_finish(fa, st)) != cudaSuccess) return e;
   k += 2;
   *nlaunch += k;
@@ -1350,6 +1453,7 @@ struct Batch {
   int T = 0;                  // max steps
   int lane = 0;               // decoder lane (stream) that runs this batch
   int S_max = 1;              // longest source sentence
+  int bb = -1;                // word-budget batch (shortlist scope, F2), -1 = none
   std::vector<int32_t> alive; // alive[t-1] = rows with max_len >= t (upper bound of live rows)
   // encoder attention launches: {first index into the length-sorted row order, rows, longest}
   std::vector<std::array<int, 3>> enc_buckets;
@@ -1385,7 +1489,8 @@ static mnmt_status check_inputs(mnmt_model* m, const int64_t* src_off, int32_t n
 
 static void plan_job(const int64_t* src_off, int32_t n, const int32_t* max_len,
                      const std::vector<std::vector<int32_t>>& batch_rows,
-                     const std::vector<int>& batch_lane, int n_lanes, Job& job) {
+                     const std::vector<int>& batch_lane, int n_lanes, Job& job,
+                     const std::vector<int>* batch_bb = nullptr) {
   job.lane_M.assign(n_lanes, 0);
   job.lane_B.assign(n_lanes, 0);
   job.lane_T.assign(n_lanes, 0);
@@ -1397,6 +1502,7 @@ static void plan_job(const int64_t* src_off, int32_t n, const int32_t* max_len,
   for (const auto& rows_all : batch_rows) {
     Batch b;
     b.lane = batch_lane.empty() ? 0 : batch_lane[bi_in];
+    b.bb = batch_bb ? (*batch_bb)[bi_in] : -1;
     ++bi_in;
     for (int32_t s : rows_all)
       if (max_len[s] > 0) b.rows.push_back(s);   // max_len 0: nothing to decode
@@ -1545,6 +1651,16 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
                             w.live_len, st));
     }
     launches += 1;
+    if (m->sl_active && b.bb >= 0) {
+      const int nsl = m->sl_count[b.bb];
+      CK(launch_sl_gather(m->jb.sl_ids + (int64_t)b.bb * c.vocab, nsl, m->qE,
+                          c.out_bias ? m->out_b : nullptr, (int)d, w.sl_q,
+                          c.out_bias ? w.sl_b : nullptr, w.sl_map, st));
+      launches += 1;
+      Ln.sl_n = nsl;
+    } else {
+      Ln.sl_n = 0;
+    }
     const int npad = (B + 127) / 128 * 128;
     // attention scratch is sized by the longest span a step can attend (source length, or the
     // step count for the self-attention decoder); it only grows, and captured graphs are
@@ -1566,7 +1682,7 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
       const int a = b.alive[t] * rows_per;
       return (a < 128 && m->rowfuse > 0) ? std::max(16, (a + 15) / 16 * 16) : (a + 127) / 128 * 128;
     };
-    if (m->megakernel && m->beam == 0 && (!hook || hook->megakernel_ok())) {
+    if (m->megakernel && m->beam == 0 && Ln.sl_n == 0 && (!hook || hook->megakernel_ok())) {
       if (!Ln.d_phases || Ln.prog_forced != forced || Ln.prog_out != m->jb.out_ids)
         CKS(build_program(m, Ln, forced));
       StepArgs sa{};
@@ -1602,7 +1718,7 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
       const int K = std::max(1, m->steps_per_graph);
       for (int t = 0; t < b.T;) {
         const int np = pad_at(t), k = std::min(K, b.T - t);
-        const int64_t key = ((int64_t)np * 64 + k) * 16 + m->beam;
+        const int64_t key = (((int64_t)np * 64 + k) * 16 + m->beam) * ((int64_t)c.vocab + 1) + Ln.sl_n;
         auto it = Ln.graphs.find(key);
         if (it == Ln.graphs.end()) {
           cudaGraph_t g;
@@ -1619,6 +1735,11 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
           cudaGraphExec_t ge;
           CK(cudaGraphInstantiate(&ge, g, 0));
           cudaGraphDestroy(g);
+          if (Ln.graphs.size() >= 2048) {   // bound the cache (shortlist sizes vary per batch)
+            CK(cudaStreamSynchronize(st));
+            for (auto& kv : Ln.graphs) cudaGraphExecDestroy(kv.second);
+            Ln.graphs.clear();
+          }
           it = Ln.graphs.emplace(key, ge).first;
           Ln.launches_per_step = per_step;
         }
@@ -1656,6 +1777,7 @@ static mnmt_status ensure_lanes(mnmt_model* m, const Job& job, int64_t forced_O)
     CKS(lane_ensure(m, m->lanes[li], job.lane_M[li], job.lane_B[li] * std::max(1, m->beam),
                     job.lane_T[li], forced_O));
     if (m->beam > 0) CKS(beam_ensure(m, m->lanes[li]));
+    if (m->sl_active) CKS(sl_lane_ensure(m, m->lanes[li]));
   }
   return MNMT_OK;
 }
@@ -1895,6 +2017,12 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
   }
   if (beam > 0 && n > 0 && (!out_score || !n_hyp)) { set_err("NULL beam outputs"); return MNMT_ERR_ARG; }
   const bool dev_io = (flags & MNMT_DEVICE_IO) != 0;
+  const bool use_sl = (flags & MNMT_SHORTLIST) != 0;
+  if (use_sl && (beam > 0 || !sorted_batches)) {
+    set_err("MNMT_SHORTLIST: greedy mnmt_translate only");
+    return MNMT_ERR_ARG;
+  }
+  if (use_sl && !m->sl_tables) { set_err("MNMT_SHORTLIST before mnmt_model_set_shortlist"); return MNMT_ERR_STATE; }
   const int64_t bm = std::max(1, beam);   // output slots per sentence
   int64_t O = 0, ntok = n > 0 ? src_off[n] : 0;
   for (int i = 0; i < n; ++i) O += max_len[i] * bm;
@@ -1905,7 +2033,8 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
   DeviceGuard g(m->dev);
   if ((s = begin_call(m, cuda_stream)) != MNMT_OK) return fail(m, s);
   std::vector<std::vector<int32_t>> rows;
-  std::vector<int> lanes_of;
+  std::vector<int> lanes_of, bb_of;
+  std::vector<int32_t> bb_sents, bb_off(1, 0);   // shortlist scopes (F2): word-budget batches
   if (sorted_batches) {
     if (budget < 1) { set_err("word_budget < 1"); return MNMT_ERR_ARG; }
     std::vector<int32_t> L(n), order(std::max(n, 1)), off(n + 2);
@@ -1919,8 +2048,11 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
     const int P = std::max(1, m->n_lanes);
     for (int b = 0; b < nb;) {
       int e = b + 1;
-      if (m->max_concurrent_rows > 0)
+      // with a shortlist every wave is one word-budget batch: the batch is the shortlist's scope
+      if (m->max_concurrent_rows > 0 && !use_sl)
         while (e < nb && off[e + 1] - off[b] <= m->max_concurrent_rows) ++e;
+      for (int i = off[b]; i < off[e]; ++i) bb_sents.push_back(order[i]);
+      bb_off.push_back((int32_t)bb_sents.size());
       if (m->lane_tiers > 0 && P > 1) {
         // contiguous length tiers: lane li takes the li-th of P equal shares of
         // sum_i S_i^p (p = lane_tiers / 10) in length order, so the long-sentence tail runs on
@@ -1954,6 +2086,7 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
           }
         }
       }
+      bb_of.resize(rows.size(), (int)bb_off.size() - 2);
       b = e;
     }
   } else {
@@ -1962,15 +2095,16 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
     lanes_of.push_back(0);
   }
   Job job;
-  plan_job(src_off, n, max_len, rows, lanes_of, (int)m->lanes.size(), job);
+  plan_job(src_off, n, max_len, rows, lanes_of, (int)m->lanes.size(), job, use_sl ? &bb_of : nullptr);
   plan_rows(job, src_off, max_len, false, nullptr);
   if ((s = jb_ensure(m, std::max<int64_t>(O, 1), std::max<int64_t>((int64_t)n * bm, 1),
                      std::max<int64_t>(ntok, 1), (int64_t)job.meta.size(), job.rows_total)) != MNMT_OK)
     return fail(m, s);
   m->beam = beam;
+  m->sl_active = use_sl;
   struct BeamReset {
     mnmt_model* m;
-    ~BeamReset() { m->beam = 0; }
+    ~BeamReset() { m->beam = 0; m->sl_active = false; }
   } beam_reset{m};
   if ((s = ensure_lanes(m, job, 1)) != MNMT_OK) return fail(m, s);
   auto& w = m->jb;
@@ -1989,6 +2123,7 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
     CK(cudaStreamSynchronize(m->st));
     if (hbad) { set_err("%d source ids out of range", hbad); return MNMT_ERR_VOCAB; }
   }
+  if (use_sl && (s = sl_build_job(m, src_off, bb_sents, bb_off)) != MNMT_OK) return fail(m, s);
   CK(cudaMemsetAsync(w.out_len, 0, (size_t)n * bm * 4, m->st));
   if (beam > 0) {
     CK(cudaMemsetAsync(w.n_hyp, 0, (size_t)n * 4, m->st));
@@ -2029,6 +2164,31 @@ mnmt_status mnmt_translate(mnmt_model* m, const int32_t* src_ids, const int64_t*
   if (budget < 1) { set_err("word_budget < 1"); return MNMT_ERR_ARG; }
   return translate_impl(m, src_ids, src_off, n, max_len, budget, true, out_ids, out_cap, out_len,
                         flags, cuda_stream);
+}
+
+mnmt_status mnmt_model_set_shortlist(mnmt_model* m, const int32_t* freq, int32_t n_freq,
+                                     const int32_t* lex, int32_t k_lex) {
+  if (!m) { set_err("NULL model"); return MNMT_ERR_ARG; }
+  if (m->failed) { set_err("handle failed earlier (fail-stop)"); return MNMT_ERR_STATE; }
+  if (n_freq < 0 || k_lex < 0 || (n_freq > 0 && !freq) || (k_lex > 0 && !lex)) {
+    set_err("bad shortlist tables (n_freq, k_lex >= 0; non-NULL when non-empty)");
+    return MNMT_ERR_ARG;
+  }
+  DeviceGuard g(m->dev);
+  CK(cudaDeviceSynchronize());
+  if (m->sl_freq) cudaFree(m->sl_freq);
+  if (m->sl_lex) cudaFree(m->sl_lex);
+  m->sl_freq = m->sl_lex = nullptr;
+  m->sl_tables = false;
+  const int64_t nl = (int64_t)m->c.vocab * k_lex;
+  CK(cudaMalloc(&m->sl_freq, std::max<int64_t>(n_freq, 1) * 4));
+  CK(cudaMalloc(&m->sl_lex, std::max<int64_t>(nl, 1) * 4));
+  if (n_freq > 0) CK(cudaMemcpy(m->sl_freq, freq, (size_t)n_freq * 4, cudaMemcpyHostToDevice));
+  if (nl > 0) CK(cudaMemcpy(m->sl_lex, lex, (size_t)nl * 4, cudaMemcpyHostToDevice));
+  m->sl_nfreq = n_freq;
+  m->sl_k = k_lex;
+  m->sl_tables = true;
+  return MNMT_OK;
 }
 
 mnmt_status mnmt_beam_translate(mnmt_model* m, const int32_t* src_ids, const int64_t* src_off,
@@ -2364,6 +2524,8 @@ extern "C" void mnmt_model_destroy(mnmt_model* m) {
       lane_streams_free(L);
     }
     jb_free(m);
+    if (m->sl_freq) cudaFree(m->sl_freq);
+    if (m->sl_lex) cudaFree(m->sl_lex);
     for (void* p : m->allocs) cudaFree(p);
     for (auto& gc : m->green)
       if (gc) green_api().destroy(gc);

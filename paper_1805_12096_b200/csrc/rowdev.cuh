@@ -309,7 +309,8 @@ __device__ __forceinline__ void finish_block(const FinishArgs a, int32_t* warp_c
       orig = a.live[r];
       const unsigned long long key = a.keys[r];
       a.keys[r] = 0ull;
-      const int id = (int)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull));
+      int id = (int)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull));
+      if (a.id_map) id = a.id_map[id];
       const int ml = a.max_len[orig];
       int32_t* out = a.out_ids + a.out_off[orig];
       if (a.forced) {

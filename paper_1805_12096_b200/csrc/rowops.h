@@ -108,6 +108,7 @@ struct FinishArgs {
   const int32_t* row_len;
   int32_t* live_start;
   int32_t* live_len;
+  const int32_t* id_map;    // shortlist (F2): GEMM column -> vocabulary id, or null
 };
 
 cudaError_t launch_quantize(const float* x, int64_t n, float clip, int8_t* out, cudaStream_t st);

@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libmnmt.so")
 ABI_VERSION = 1
 MAX_SPAN = 512
 DEVICE_IO = 1
+SHORTLIST = 2
 
 DUMP_ENC_OUT, DUMP_SRC_KV, DUMP_DEC_OUT, DUMP_OUT_CODES, DUMP_LAYERS = 1, 2, 4, 8, 16
 EPI_F32, EPI_F32_Q, EPI_RELU_Q, EPI_RELU_F32_Q, EPI_SIGMOID, EPI_ARGMAX, EPI_ACC = range(7)
@@ -50,6 +51,7 @@ class Stats(C.Structure):
 EXPORTS = [
     "mnmt_config_default", "mnmt_model_create", "mnmt_model_set_param", "mnmt_model_quantize",
     "mnmt_batch_by_words", "mnmt_decode", "mnmt_translate", "mnmt_beam_translate",
+    "mnmt_model_set_shortlist",
     "mnmt_decode_forced",
     "mnmt_get_stats", "mnmt_last_error", "mnmt_model_destroy", "mnmt_model_set_option",
     "mnmt_op_quantize", "mnmt_op_gemm_i8", "mnmt_op_argmax_ids", "mnmt_op_layernorm",
@@ -77,6 +79,7 @@ def lib():
     L.mnmt_batch_by_words.argtypes = [P, I32, I32, P, P, P]
     L.mnmt_decode.argtypes = [P, P, P, I32, P, P, I64, P, P]
     L.mnmt_translate.argtypes = [P, P, P, I32, P, I32, P, I64, P, C.c_uint32, P]
+    L.mnmt_model_set_shortlist.argtypes = [P, P, I32, P, I32]
     L.mnmt_beam_translate.argtypes = [P, P, P, I32, P, I32, I32, P, I64, P, P, P, C.c_uint32, P]
     L.mnmt_decode_forced.argtypes = [P, P, P, I32, P, P, P, C.c_uint32, P, I64, P]
     L.mnmt_get_stats.argtypes = [P, C.POINTER(Stats)]
@@ -209,8 +212,16 @@ class Model:
                                  _p(out_len), _stream_ptr(stream)))
         return self._split(out, out_len, ml)
 
-    def translate(self, sset, budget: int, stream=None) -> List[np.ndarray]:
-        """The whole job (host buffers): batch_by_words + decode of every batch."""
+    def set_shortlist(self, freq: np.ndarray, lex: np.ndarray) -> None:
+        """Shortlist tables (F2): freq [n_freq] ids, lex [vocab x k_lex] ids (include/mnmt.h)."""
+        freq = np.ascontiguousarray(freq, np.int32)
+        lex = np.ascontiguousarray(lex, np.int32)
+        k = lex.shape[1] if lex.ndim == 2 else 0
+        _check(lib().mnmt_model_set_shortlist(self.h, _p(freq), freq.size, _p(lex), k))
+
+    def translate(self, sset, budget: int, stream=None, shortlist: bool = False) -> List[np.ndarray]:
+        """The whole job (host buffers): batch_by_words + decode of every batch (shortlist:
+        each batch's argmax restricted to its vocabulary shortlist, MNMT_SHORTLIST)."""
         n = sset.n
         ml = np.ascontiguousarray(sset.max_len, np.int32)
         out = np.zeros(max(int(ml.sum()), 1), np.int32)
@@ -218,7 +229,8 @@ class Model:
         ids = np.ascontiguousarray(sset.ids, np.int32)
         offs = np.ascontiguousarray(sset.offsets, np.int64)
         _check(lib().mnmt_translate(self.h, _p(ids), _p(offs), n, _p(ml), budget, _p(out),
-                                    out.size, _p(out_len), 0, _stream_ptr(stream)))
+                                    out.size, _p(out_len), SHORTLIST if shortlist else 0,
+                                    _stream_ptr(stream)))
         return self._split(out, out_len, ml)
 
     def beam_translate(self, sset, budget: int, beam: int, stream=None):
@@ -256,12 +268,13 @@ class Model:
 
     def translate_device(self, ids_ptr: int, offsets: np.ndarray, max_len: np.ndarray,
                          budget: int, out_ptr: int, out_cap: int, out_len_ptr: int,
-                         stream=None) -> None:
+                         stream=None, shortlist: bool = False) -> None:
         """The whole job with ids already resident in HBM (MNMT_DEVICE_IO)."""
         offs = np.ascontiguousarray(offsets, np.int64)
         ml = np.ascontiguousarray(max_len, np.int32)
         _check(lib().mnmt_translate(self.h, ids_ptr, _p(offs), len(ml), _p(ml), budget, out_ptr,
-                                    out_cap, out_len_ptr, DEVICE_IO, _stream_ptr(stream)))
+                                    out_cap, out_len_ptr, DEVICE_IO | (SHORTLIST if shortlist else 0),
+                                    _stream_ptr(stream)))
 
     def decode_forced(self, sset, forced: np.ndarray, forced_off: np.ndarray,
                       dump_mask: int = 0, stream=None):
