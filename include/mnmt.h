@@ -119,8 +119,9 @@ mnmt_status mnmt_decode(mnmt_model* m, const int32_t* src_ids_host, const int64_
  * batch").  Every word-budget batch decodes with the argmax restricted to its
  * shortlist = freq ∪ {lex[s][k] : s a source id of the batch} ∪ {eos_id, MNMT_UNK_ID} (the
  * tables of mnmt_model_set_shortlist; ids outside [0, vocab) ignored), ascending, so the lowest
- * id still wins ties (R15, R32-R34).  Each word-budget batch then forms its own decode wave
- * (max_concurrent_rows is not applied).  Greedy only.
+ * id still wins ties (R15, R32-R34).  Batches co-scheduled in one decode wave (at most 64
+ * with a shortlist) share one output GEMM over the union of their shortlists, each row masked
+ * to its own batch's columns, so ids do not depend on the scheduling.  Greedy only.
  * Errors: MNMT_ERR_STATE without tables, MNMT_ERR_ARG with beam search. */
 #define MNMT_SHORTLIST 2u
 #define MNMT_UNK_ID 1   /* reserved ids EOS/UNK/PAD = 0/1/2 */

@@ -67,9 +67,6 @@ __device__ __forceinline__ float acc_to_float(int32_t acc, bool small) {
 }
 
 
-// One 32-column chunk of the 32 rows of this warp (lane = row): dequant + fused op +
-// store, or running argmax.  fp32 outputs go through a padded per-warp smem tile so each
-// store instruction writes four full 128-byte lines.
 // Packed fp32 pairs (sm_100a FFMA2 / FADD2): each half is one IEEE round-to-nearest op.
 __device__ __forceinline__ unsigned long long pk2(float a, float b) {
   unsigned long long r;
@@ -118,13 +115,33 @@ __device__ __forceinline__ void dequant32(const GemmArgs& args, const float* bsr
   }
 }
 
+// Shortlist (F2): the row's group words for the HALF columns from nb (one 32-bit word per
+// 32-column chunk, zero past N), so the epilogue masks with no further loads.
+template <int HALF>
+__device__ __forceinline__ void sl_words(const GemmArgs& args, int row, bool row_ok, int nb,
+                                         uint32_t (&w)[HALF / 32]) {
+  if (!args.colbits) {
+#pragma unroll
+    for (int c = 0; c < HALF / 32; ++c) w[c] = 0xffffffffu;
+    return;
+  }
+  const int g = row_ok ? args.row_grp[args.row_live ? args.row_live[row] : row] : 0;
+  const uint32_t* gb = args.colbits + (int64_t)g * args.colbits_ld;
+#pragma unroll
+  for (int c = 0; c < HALF / 32; ++c) {
+    const int n = nb + c * 32;
+    w[c] = n < args.N ? gb[n >> 5] : 0u;
+  }
+}
+
 // One 32-column chunk of the 32 rows of this warp (lane = row): dequant + fused op +
 // store, or running argmax.  fp32 outputs go through a padded per-warp smem tile so each
 // store instruction writes four full 128-byte lines.
 template <int EPI>
 __device__ __forceinline__ void epi_store_chunk(const GemmArgs& args, const float* bsrc, int row,
                                                 bool row_ok, int n, const int32_t (&acc)[32],
-                                                float& best_v, int& best_j, float* stage) {
+                                                float& best_v, int& best_j, float* stage,
+                                                uint32_t slw = 0xffffffffu) {
   const bool full = n + 32 <= args.N;
   const bool fast = full && args.K <= 256;
   if constexpr (EPI == EPI_ARGMAX) {
@@ -133,7 +150,12 @@ __device__ __forceinline__ void epi_store_chunk(const GemmArgs& args, const floa
     // equal logits the lowest column wins (R15).
     float v[32];
     dequant32(args, bsrc, n, fast, acc, v);
-    if (!full) {
+    if (args.colbits) {   // shortlist union: only the columns of the row's own batch (F2);
+      // slw = the row's group word of this chunk (zero past N), loaded before the MMA wait
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (!((slw >> j) & 1u)) v[j] = -INFINITY;
+    } else if (!full) {
 #pragma unroll
       for (int j = 0; j < 32; ++j)
         if (n + j >= args.N) v[j] = -INFINITY;
@@ -587,6 +609,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int row = m0 + q * 32 + lane;
     const bool row_ok = row < M_live;
     constexpr int HALF = BN / 2;
+    uint32_t slw[HALF / 32];
+    if constexpr (EPI == EPI_ARGMAX) sl_words<HALF>(args, row, row_ok, n0 + half * HALF, slw);
     mbar_wait(&tmem_full_bar, 0);
     tc_fence_after();
     if (warp == 2 && lane == 0) GEMM_TRACE(3);
@@ -614,7 +638,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int n = n0 + half * HALF + c;
       if (n >= args.N) break;  // warp-uniform
       epi_store_chunk<EPI>(args, args.bias ? bias_s - n0 : nullptr, row, row_ok, n, acc, best_v,
-                           best_j, stage);
+                           best_j, stage, EPI == EPI_ARGMAX ? slw[c / 32] : 0u);
     }
     if constexpr (EPI == EPI_ARGMAX) {
       if (row_ok && best_j >= 0) atomicMax(args.keys + row, argmax_key(best_v, (uint32_t)best_j));
@@ -1003,6 +1027,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int m0 = (t / n_tiles) * BM, n0 = (t % n_tiles) * BN;
       const int row = m0 + q * 32 + lane;
       const bool row_ok = row < M_live;
+      uint32_t slw[HALF / 32];
+      if constexpr (EPI == EPI_ARGMAX) sl_words<HALF>(args, row, row_ok, n0 + half * HALF, slw);
       mbar_wait(&tfull_bar[ab], aph);
       tc_fence_after();
       if (first && warp == 2 && lane == 0) pdl_launch_dependents();
@@ -1020,7 +1046,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tmem_ld_wait();
         const int n = n0 + half * HALF + c;
         if (n >= args.N) break;
-        epi_store_chunk<EPI>(args, args.bias, row, row_ok, n, acc, best_v, best_j, stage);
+        epi_store_chunk<EPI>(args, args.bias, row, row_ok, n, acc, best_v, best_j, stage,
+                             EPI == EPI_ARGMAX ? slw[c / 32] : 0u);
       }
       if constexpr (EPI == EPI_ARGMAX) {
         if (row_ok && best_j >= 0) atomicMax(args.keys + row, argmax_key(best_v, (uint32_t)best_j));

@@ -52,6 +52,13 @@ struct GemmArgs {
   int col_block;               // scatter: out + (n / col_block) * block_stride + m * ldo + n % col_block
   int64_t block_stride;
   unsigned long long* keys;    // [rows] for EPI_ARGMAX
+  // EPI_ARGMAX over a shortlist union (F2): column n is a candidate for row r only if bit n % 32
+  // of colbits[g * colbits_ld + n / 32] is set, g = row_grp[row_live[r]] (colbits null: every
+  // column)
+  const uint32_t* colbits;
+  int colbits_ld;
+  const int32_t* row_grp;
+  const int32_t* row_live;
   int pers_grid;               // persistent variant: CTA cap (0 = one per SM)
   unsigned long long* trace;   // debug: CTA (0,0) %globaltimer stamps [9] (null = off)
   LnArgs ln;                   // EPI_LN: residual / gate inputs, gamma, beta, outputs, AAN

@@ -15,6 +15,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <map>
 #include <numeric>
 #include <string>
@@ -113,6 +114,8 @@ struct Workspace {
   int8_t* sl_q = nullptr;
   float* sl_b = nullptr;
   int32_t* sl_map = nullptr;
+  uint32_t* sl_bits = nullptr;             // [SL_MAX_GROUPS][ceil(V/32)] per-group column bitmaps
+  int32_t* sl_rgrp = nullptr;              // [B_cap] batch row -> group in the wave
   CUtensorMap tm_sl;
 };
 
@@ -131,11 +134,13 @@ struct JobBuf {
   // vocabulary shortlist (F2): per word-budget batch bitmap, ascending ids and count, and the
   // batch-major sentence spans the bitmap kernel walks
   std::vector<void*> sl_allocs;
-  int64_t sl_bb_cap = 0, sl_sent_cap = 0;
+  int64_t sl_bb_cap = 0, sl_sent_cap = 0, sl_wave_cap = 0, sl_rows_cap = 0;
   uint32_t* sl_bits = nullptr;  // [bb][ceil(V/32)]
-  int32_t* sl_ids = nullptr;    // [bb][V]
-  int32_t* sl_n = nullptr;      // [bb]
-  int32_t* sl_span = nullptr;   // [start | len] x sentences (batch-major), then bb_off [bb + 1]
+  int32_t* sl_ids = nullptr;    // [wave][V] union of the wave's shortlists, ascending
+  unsigned long long* sl_mask = nullptr;   // [wave][V] per column: bit g = in group g's list
+  int32_t* sl_n = nullptr;      // [wave]
+  int32_t* sl_span = nullptr;   // [start | len] x sentences (batch-major), bb_off, wave_off
+  int32_t* sl_rgrp = nullptr;   // [job rows] group (batch within its wave) of every row
 };
 
 // A lane = one independent decoder (workspace + stream + step graphs).  Rows are
@@ -210,7 +215,8 @@ struct mnmt_model {
   int sl_nfreq = 0, sl_k = 0;
   bool sl_tables = false;
   bool sl_active = false;              // (call state) MNMT_SHORTLIST
-  std::vector<int32_t> sl_count;       // (call state) shortlist size of each word-budget batch
+  std::vector<int32_t> sl_count;       // (call state) union size of each decode wave
+  std::vector<int32_t> sl_groups;      // (call state) word-budget batches of each decode wave
 };
 
 namespace {
@@ -567,47 +573,61 @@ static mnmt_status sl_lane_ensure(mnmt_model* m, Lane& Ln) {
   CKS(dalloc(w.sl_allocs, &w.sl_q, V * d));
   CKS(dalloc(w.sl_allocs, &w.sl_b, V));
   CKS(dalloc(w.sl_allocs, &w.sl_map, V));
+  CKS(dalloc(w.sl_allocs, &w.sl_bits, (int64_t)SL_MAX_GROUPS * ((V + 31) / 32)));
+  CKS(dalloc(w.sl_allocs, &w.sl_rgrp, w.B_cap));
   if (!make_tmap_i8(&w.tm_sl, w.sl_q, V, d)) { set_err("tensor map (shortlist) failed"); return MNMT_ERR_CUDA; }
   return MNMT_OK;
 }
 
-// Job-level shortlist buffers for n_bb word-budget batches of n sentences.
-static mnmt_status sl_job_ensure(mnmt_model* m, int64_t n_bb, int64_t n) {
+// Job-level shortlist buffers.
+static mnmt_status sl_job_ensure(mnmt_model* m, int64_t n_bb, int64_t n, int64_t n_waves,
+                                 int64_t rows) {
   JobBuf& j = m->jb;
-  if (n_bb <= j.sl_bb_cap && n <= j.sl_sent_cap) return MNMT_OK;
+  if (n_bb <= j.sl_bb_cap && n <= j.sl_sent_cap && n_waves <= j.sl_wave_cap && rows <= j.sl_rows_cap)
+    return MNMT_OK;
   CK(cudaDeviceSynchronize());
   for (void* p : j.sl_allocs) cudaFree(p);
   j.sl_allocs.clear();
   const int64_t V = m->c.vocab, W = (V + 31) / 32;
   j.sl_bb_cap = std::max(n_bb, j.sl_bb_cap);
   j.sl_sent_cap = std::max(n, j.sl_sent_cap);
+  j.sl_wave_cap = std::max(n_waves, j.sl_wave_cap);
+  j.sl_rows_cap = std::max(rows, j.sl_rows_cap);
   CKS(dalloc(j.sl_allocs, &j.sl_bits, j.sl_bb_cap * W));
-  CKS(dalloc(j.sl_allocs, &j.sl_ids, j.sl_bb_cap * V));
-  CKS(dalloc(j.sl_allocs, &j.sl_n, j.sl_bb_cap));
-  CKS(dalloc(j.sl_allocs, &j.sl_span, 2 * j.sl_sent_cap + j.sl_bb_cap + 1));
+  CKS(dalloc(j.sl_allocs, &j.sl_ids, j.sl_wave_cap * V));
+  CKS(dalloc(j.sl_allocs, &j.sl_mask, j.sl_wave_cap * V));
+  CKS(dalloc(j.sl_allocs, &j.sl_n, j.sl_wave_cap));
+  CKS(dalloc(j.sl_allocs, &j.sl_span, 2 * j.sl_sent_cap + j.sl_bb_cap + j.sl_wave_cap + 2));
+  CKS(dalloc(j.sl_allocs, &j.sl_rgrp, std::max<int64_t>(j.sl_rows_cap, 1)));
   return MNMT_OK;
 }
 
-// Builds the shortlist of every word-budget batch of the job on the device (one bitmap pass,
-// one compaction) and reads the sizes back (one synchronisation per job, before decoding; the
-// output GEMM's N is a launch parameter of the step graphs).  bb_sents: batch-major sentence
-// indices; bb_off: [n_bb + 1].
+// Builds every word-budget batch's shortlist and every decode wave's union (with per-column
+// group masks) on the device, and reads the union sizes back (one synchronisation per job,
+// before decoding: the output GEMM's N is a launch parameter of the step graphs).
+// bb_sents: batch-major sentence indices; bb_off: [n_bb + 1]; wave_off: [n_waves + 1] first
+// batch of each wave; rgrp: group of every job row (rmeta row order).
 static mnmt_status sl_build_job(mnmt_model* m, const int64_t* src_off,
                                 const std::vector<int32_t>& bb_sents,
-                                const std::vector<int32_t>& bb_off) {
-  const int n_bb = (int)bb_off.size() - 1;
+                                const std::vector<int32_t>& bb_off,
+                                const std::vector<int32_t>& wave_off,
+                                const std::vector<int32_t>& rgrp) {
+  const int n_bb = (int)bb_off.size() - 1, n_waves = (int)wave_off.size() - 1;
   const int64_t ns = (int64_t)bb_sents.size();
-  CKS(sl_job_ensure(m, n_bb, ns));
+  CKS(sl_job_ensure(m, n_bb, ns, n_waves, (int64_t)rgrp.size()));
   JobBuf& j = m->jb;
-  std::vector<int32_t> span(2 * ns + n_bb + 1);
+  std::vector<int32_t> span(2 * ns + n_bb + 1 + n_waves + 1);
   for (int64_t i = 0; i < ns; ++i) {
     const int s = bb_sents[i];
     span[i] = (int32_t)src_off[s];
     span[ns + i] = (int32_t)(src_off[s + 1] - src_off[s]);
   }
   std::copy(bb_off.begin(), bb_off.end(), span.begin() + 2 * ns);
+  std::copy(wave_off.begin(), wave_off.end(), span.begin() + 2 * ns + n_bb + 1);
   CK(cudaMemcpyAsync(j.sl_span, span.data(), span.size() * 4, cudaMemcpyHostToDevice, m->st));
-  m->stats.h2d_bytes += (int64_t)span.size() * 4;
+  if (!rgrp.empty())
+    CK(cudaMemcpyAsync(j.sl_rgrp, rgrp.data(), rgrp.size() * 4, cudaMemcpyHostToDevice, m->st));
+  m->stats.h2d_bytes += (int64_t)(span.size() + rgrp.size()) * 4;
   SlMarkArgs a{};
   a.V = m->c.vocab;
   a.W = (m->c.vocab + 31) / 32;
@@ -622,11 +642,14 @@ static mnmt_status sl_build_job(mnmt_model* m, const int64_t* src_off,
   a.eos = m->c.eos_id;
   a.unk = MNMT_UNK_ID;
   a.bits = j.sl_bits;
-  CK(launch_sl_build(a, n_bb, j.sl_ids, j.sl_n, m->st));
+  CK(launch_sl_build(a, n_bb, j.sl_span + 2 * ns + n_bb + 1, n_waves, j.sl_ids, j.sl_mask,
+                     j.sl_n, m->st));
   m->stats.gpu_launches += 2;
-  m->sl_count.assign(n_bb, 0);
-  if (n_bb > 0) {
-    CK(cudaMemcpyAsync(m->sl_count.data(), j.sl_n, n_bb * 4, cudaMemcpyDeviceToHost, m->st));
+  m->sl_count.assign(n_waves, 0);
+  m->sl_groups.resize(n_waves);
+  for (int i = 0; i < n_waves; ++i) m->sl_groups[i] = wave_off[i + 1] - wave_off[i];
+  if (n_waves > 0) {
+    CK(cudaMemcpyAsync(m->sl_count.data(), j.sl_n, n_waves * 4, cudaMemcpyDeviceToHost, m->st));
     CK(cudaStreamSynchronize(m->st));
   }
   return MNMT_OK;
@@ -1171,6 +1194,13 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
     a.sigma = sigma_of(m);
     a.col_block = a.N;
     a.keys = w.keys;
+    static const bool sl_nomask = getenv("MNMT_SL_NOMASK") != nullptr;   // A/B only (wrong ids
+    if (sl && !sl_nomask) {                                                // unless 1 group)
+      a.colbits = w.sl_bits;
+      a.colbits_ld = (c.vocab + 31) / 32;
+      a.row_grp = w.sl_rgrp;
+      a.row_live = w.live;
+    }
     a.pers_grid = m->cur_pers_grid;
     if ((e = launch_gemm_i8(w.tm_cy, sl ? w.tm_sl : m->tmE, a, EPI_ARGMAX, 0, st)) != cudaSuccess)
       return e;
@@ -1453,7 +1483,7 @@ struct Batch {
   int T = 0;                  // max steps
   int lane = 0;               // decoder lane (stream) that runs this batch
   int S_max = 1;              // longest source sentence
-  int bb = -1;                // word-budget batch (shortlist scope, F2), -1 = none
+  int bb = -1;                // shortlist (F2): decode wave whose union this unit uses, -1 = none
   std::vector<int32_t> alive; // alive[t-1] = rows with max_len >= t (upper bound of live rows)
   // encoder attention launches: {first index into the length-sorted row order, rows, longest}
   std::vector<std::array<int, 3>> enc_buckets;
@@ -1653,9 +1683,12 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
     launches += 1;
     if (m->sl_active && b.bb >= 0) {
       const int nsl = m->sl_count[b.bb];
-      CK(launch_sl_gather(m->jb.sl_ids + (int64_t)b.bb * c.vocab, nsl, m->qE,
+      CK(launch_sl_gather(m->jb.sl_ids + (int64_t)b.bb * c.vocab,
+                          m->jb.sl_mask + (int64_t)b.bb * c.vocab, nsl, m->sl_groups[b.bb], m->qE,
                           c.out_bias ? m->out_b : nullptr, (int)d, w.sl_q,
-                          c.out_bias ? w.sl_b : nullptr, w.sl_map, st));
+                          c.out_bias ? w.sl_b : nullptr, w.sl_map, w.sl_bits,
+                          (c.vocab + 31) / 32, st));
+      CK(cudaMemcpyAsync(w.sl_rgrp, m->jb.sl_rgrp + job.r0[bi], B * 4, cudaMemcpyDeviceToDevice, st));
       launches += 1;
       Ln.sl_n = nsl;
     } else {
@@ -2033,8 +2066,10 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
   DeviceGuard g(m->dev);
   if ((s = begin_call(m, cuda_stream)) != MNMT_OK) return fail(m, s);
   std::vector<std::vector<int32_t>> rows;
-  std::vector<int> lanes_of, bb_of;
-  std::vector<int32_t> bb_sents, bb_off(1, 0);   // shortlist scopes (F2): word-budget batches
+  std::vector<int> lanes_of, wave_of;
+  // shortlist scopes (F2): word-budget batches (sentences batch-major), waves of batches, and
+  // every sentence's group (batch index within its wave)
+  std::vector<int32_t> bb_sents, bb_off(1, 0), wave_off(1, 0), grp_of(std::max(n, 1), 0);
   if (sorted_batches) {
     if (budget < 1) { set_err("word_budget < 1"); return MNMT_ERR_ARG; }
     std::vector<int32_t> L(n), order(std::max(n, 1)), off(n + 2);
@@ -2048,11 +2083,19 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
     const int P = std::max(1, m->n_lanes);
     for (int b = 0; b < nb;) {
       int e = b + 1;
-      // with a shortlist every wave is one word-budget batch: the batch is the shortlist's scope
-      if (m->max_concurrent_rows > 0 && !use_sl)
-        while (e < nb && off[e + 1] - off[b] <= m->max_concurrent_rows) ++e;
-      for (int i = off[b]; i < off[e]; ++i) bb_sents.push_back(order[i]);
-      bb_off.push_back((int32_t)bb_sents.size());
+      // with a shortlist a wave holds at most SL_MAX_GROUPS batches (bits of a column mask)
+      if (m->max_concurrent_rows > 0)
+        while (e < nb && off[e + 1] - off[b] <= m->max_concurrent_rows &&
+               (!use_sl || e - b < SL_MAX_GROUPS))
+          ++e;
+      for (int bb = b; bb < e; ++bb) {
+        for (int i = off[bb]; i < off[bb + 1]; ++i) {
+          bb_sents.push_back(order[i]);
+          grp_of[order[i]] = bb - b;
+        }
+        bb_off.push_back((int32_t)bb_sents.size());
+      }
+      wave_off.push_back(e);
       if (m->lane_tiers > 0 && P > 1) {
         // contiguous length tiers: lane li takes the li-th of P equal shares of
         // sum_i S_i^p (p = lane_tiers / 10) in length order, so the long-sentence tail runs on
@@ -2086,7 +2129,7 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
           }
         }
       }
-      bb_of.resize(rows.size(), (int)bb_off.size() - 2);
+      wave_of.resize(rows.size(), (int)wave_off.size() - 2);
       b = e;
     }
   } else {
@@ -2095,8 +2138,15 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
     lanes_of.push_back(0);
   }
   Job job;
-  plan_job(src_off, n, max_len, rows, lanes_of, (int)m->lanes.size(), job, use_sl ? &bb_of : nullptr);
+  plan_job(src_off, n, max_len, rows, lanes_of, (int)m->lanes.size(), job, use_sl ? &wave_of : nullptr);
   plan_rows(job, src_off, max_len, false, nullptr);
+  std::vector<int32_t> rgrp;
+  if (use_sl) {
+    rgrp.assign(job.rows_total, 0);
+    for (size_t bi = 0; bi < job.batches.size(); ++bi)
+      for (size_t i = 0; i < job.batches[bi].rows.size(); ++i)
+        rgrp[job.r0[bi] + i] = grp_of[job.batches[bi].rows[i]];
+  }
   if ((s = jb_ensure(m, std::max<int64_t>(O, 1), std::max<int64_t>((int64_t)n * bm, 1),
                      std::max<int64_t>(ntok, 1), (int64_t)job.meta.size(), job.rows_total)) != MNMT_OK)
     return fail(m, s);
@@ -2123,7 +2173,8 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
     CK(cudaStreamSynchronize(m->st));
     if (hbad) { set_err("%d source ids out of range", hbad); return MNMT_ERR_VOCAB; }
   }
-  if (use_sl && (s = sl_build_job(m, src_off, bb_sents, bb_off)) != MNMT_OK) return fail(m, s);
+  if (use_sl && (s = sl_build_job(m, src_off, bb_sents, bb_off, wave_off, rgrp)) != MNMT_OK)
+    return fail(m, s);
   CK(cudaMemsetAsync(w.out_len, 0, (size_t)n * bm * 4, m->st));
   if (beam > 0) {
     CK(cudaMemsetAsync(w.n_hyp, 0, (size_t)n * 4, m->st));

@@ -5,13 +5,18 @@
 // Per word-budget batch b (the paper's batch):
 //   k_sl_mark     bitmap[b] |= freq ∪ {lex[s][k] : s a source id of b} ∪ {EOS, UNK}
 //                 (ids outside [0, V) ignored), one CTA group per batch, atomicOr into V/32 words;
-//   k_sl_compact  one CTA per batch: ids of the set bits in ascending order (block prefix scan
-//                 of the word popcounts) -> sl_ids[b][0..n_b), n_b -> sl_n[b];
-//   k_sl_gather   per decode unit: the n_b rows of the memoized int8 E (and of the output bias)
-//                 copied into the lane's contiguous [n_b x d] operand, plus the id map, so the
-//                 output GEMM + argmax runs over n_b columns and k_finish maps column -> id.
-// Integer work only: bit-exact by construction.  The shortlist is ascending, so the lowest
-// column on an argmax tie is the lowest id (R15).
+// Per decode wave w (up to SL_MAX_GROUPS consecutive batches decoded together):
+//   k_sl_wave     one CTA per wave: U_w = the union of its batches' bitmaps, in ascending id
+//                 order (block prefix scan of the word popcounts) -> ids[w][0..n_w), and per
+//                 column u the group mask  mask[w][u] bit g = (U_w[u] is in batch b0 + g's list);
+//   k_sl_gather   per decode unit: the n_w rows of the memoized int8 E (and of the output bias)
+//                 copied into the lane's contiguous [n_w x d] operand with the id map, and the
+//                 masks transposed into one column bitmap per group (a warp ballot per 32
+//                 columns), so the output GEMM + argmax runs over n_w columns, each row only
+//                 over the columns of its own batch's shortlist (one 32-bit word per 32-column
+//                 chunk), and k_finish maps column -> id.
+// Integer work only: bit-exact by construction.  The union is ascending and a row's allowed
+// columns are exactly its batch's shortlist, so the lowest id still wins ties (R15).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -32,12 +37,21 @@ struct SlMarkArgs {
   uint32_t* bits;            // [n_bb][W], zeroed by the caller
 };
 
-cudaError_t launch_sl_build(const SlMarkArgs& a, int n_bb, int32_t* sl_ids /*[n_bb][V]*/,
-                            int32_t* sl_n /*[n_bb]*/, cudaStream_t st);
+constexpr int SL_MAX_GROUPS = 64;   // batches per decode wave (bits of a column mask)
 
-// dst_q[r] = qE[ids[r]] (d int8), dst_b[r] = bias[ids[r]] (bias may be null), dst_map[r] = ids[r],
-// r < n; d % 16 == 0.
-cudaError_t launch_sl_gather(const int32_t* ids, int n, const int8_t* qE, const float* bias, int d,
-                             int8_t* dst_q, float* dst_b, int32_t* dst_map, cudaStream_t st);
+// Marks every batch's bitmap, then builds every wave's union, ids and masks.
+// wave_off: [n_waves + 1] first batch of each wave.
+cudaError_t launch_sl_build(const SlMarkArgs& a, int n_bb, const int32_t* wave_off, int n_waves,
+                            int32_t* wave_ids /*[n_waves][V]*/,
+                            unsigned long long* wave_mask /*[n_waves][V]*/,
+                            int32_t* wave_n /*[n_waves]*/, cudaStream_t st);
+
+// r < n: dst_q[r] = qE[ids[r]] (d int8), dst_b[r] = bias[ids[r]] (dst_b null: skipped),
+// dst_map[r] = ids[r]; for g < n_groups, bit r % 32 of dst_bits[g * ld + r / 32] = bit g of
+// mask[r] (ld >= ceil(n / 32)); d % 16 == 0.
+cudaError_t launch_sl_gather(const int32_t* ids, const unsigned long long* mask, int n,
+                             int n_groups, const int8_t* qE, const float* bias, int d,
+                             int8_t* dst_q, float* dst_b, int32_t* dst_map, uint32_t* dst_bits,
+                             int ld, cudaStream_t st);
 
 }  // namespace mnmt

@@ -70,8 +70,8 @@ def test_shortlist_matches_oracle(dims, n_freq, k_lex, budget):
 
 
 def test_shortlist_scheduling_options():
-    """Tiered lanes, green contexts, co-scheduling (not applied with a shortlist) and the
-    persistent step kernel option (bypassed) change no id."""
+    """Tiered lanes, green contexts, co-scheduled waves and the persistent step kernel option
+    (bypassed) change no id."""
     dims = ModelDims("t192-aan-v1000", 192, 384, 8, vocab=1000, enc_layers=2, dec_layers=2)
     w = synth.make_weights(dims, seed=42, emb_scale=0.05)
     om, gm = O.OracleModel(dims, w), M.Model(dims, w)
@@ -89,6 +89,25 @@ def test_shortlist_scheduling_options():
     gm.set_option("megakernel", 0)
     # a plain call after shortlisted ones is the unrestricted decode again
     check(gm.translate(ss, 120), om.decode_many(ss, 4), "plain after shortlist")
+
+
+@pytest.mark.parametrize("budget", [1, 25, 300])
+def test_shortlist_co_scheduled_waves(budget):
+    """Many word-budget batches per decode wave (budget 1: one sentence per batch, 150 batches,
+    so waves hit the 64-group cap): one output GEMM over the wave's union, every row masked to
+    its own batch's shortlist."""
+    dims = ModelDims("t192-aan-v1000", 192, 384, 8, vocab=1000, enc_layers=2, dec_layers=2)
+    w = synth.make_weights(dims, seed=45, emb_scale=0.05)
+    om, gm = O.OracleModel(dims, w), M.Model(dims, w)
+    freq, lex = synth.shortlist_tables(dims.vocab, 20, 8, seed=11)
+    gm.set_shortlist(freq, lex)
+    ss = synth.random_set(150, 1, 30, seed=16, vocab=dims.vocab)
+    ref, _ = oracle_shortlist_job(om, dims, ss, budget, freq, lex)
+    gm.set_option("max_concurrent_rows", 4096)
+    check(gm.translate(ss, budget, shortlist=True), ref, ("waves", budget))
+    gm.set_option("lanes", 3)
+    gm.set_option("lane_tiers", 40)
+    check(gm.translate(ss, budget, shortlist=True), ref, ("waves+tiers", budget))
 
 
 def test_full_vocabulary_shortlist_is_plain_greedy():
