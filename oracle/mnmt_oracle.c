@@ -50,6 +50,9 @@ typedef struct {
                              * 1 = int8 codes, saturating int16 accumulation of adjacent pairs
                              *     ("accumulated in 16-bit integers with saturation");
                              * 2 = int16 codes RNE(x * 2^10), wrapping int32 accumulation */
+    int32_t src_kv_bf16;    /* 1 = each source key / value element is
+                             * rounded to the nearest bfloat16 (ties to even) after its
+                             * projection; attention then uses the rounded values */
 } orc_cfg;
 
 typedef struct { float *W, *b; int16_t *qW; int out, in; } orc_lin;   /* codes of arith (int8 range for 0/1) */
@@ -75,6 +78,19 @@ typedef struct {
 /* ------------------------------------------------------------- scalars */
 /* sigma = 127/c, s = c^2/127^2 ("scaled linearly to [-127,127]"; R2). */
 float orc_sigma(float clip) { return 127.0f / clip; }
+
+/* Nearest bfloat16 of a finite fp32 x, ties to even (R35): bfloat16 keeps the
+ * sign, the 8 exponent bits and the top 7 mantissa bits of the fp32 encoding, so x is rounded
+ * to a multiple of 2^16 in its bit pattern; the returned float is that bfloat16 value. */
+float orc_bf16(float x) {
+    uint32_t u;
+    memcpy(&u, &x, 4);
+    uint32_t low = u & 0xFFFFu, keep = u & 0xFFFF0000u;
+    if (low > 0x8000u || (low == 0x8000u && (keep & 0x10000u))) keep += 0x10000u;   /* round up */
+    float r;
+    memcpy(&r, &keep, 4);
+    return r;
+}
 float orc_dequant_scale(float clip) {
     return (float)(((double)clip * (double)clip) / (127.0 * 127.0));
 }
@@ -506,6 +522,9 @@ int orc_encode(const orc_model *m, const int32_t *src, int S, float *enc_out, fl
                 lin1(c, &D->sk, qa, kv + (((int64_t)l * 2 + 0) * S + i) * d);
                 lin1(c, &D->sv, qa, kv + (((int64_t)l * 2 + 1) * S + i) * d);
             }
+            if (c->src_kv_bf16)
+                for (int64_t k = 0; k < 2 * (int64_t)S * d; ++k)
+                    kv[(int64_t)l * 2 * S * d + k] = orc_bf16(kv[(int64_t)l * 2 * S * d + k]);
         }
     }
     free(x); free(Q); free(Kt); free(Vt); free(ctx); free(o); free(r); free(h); free(qa); free(pe);

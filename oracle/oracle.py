@@ -32,7 +32,7 @@ class Cfg(C.Structure):
                 ("enc_layers", C.c_int32), ("dec_layers", C.c_int32), ("vocab", C.c_int32),
                 ("decoder", C.c_int32), ("aan_ffn_depth", C.c_int32), ("aan_gate", C.c_int32),
                 ("out_bias", C.c_int32), ("eos_id", C.c_int32), ("clip", C.c_float),
-                ("ln_eps", C.c_float), ("arith", C.c_int32)]
+                ("ln_eps", C.c_float), ("arith", C.c_int32), ("src_kv_bf16", C.c_int32)]
 
 
 class Trace(C.Structure):
@@ -76,6 +76,8 @@ def lib():
         L.orc_beam_one.argtypes = [P, P, C.c_int, C.c_int, C.c_int, P, P, P]
         L.orc_beam_many.restype = C.c_int
         L.orc_beam_many.argtypes = [P, P, P, C.c_int, P, C.c_int, P, P, P, P, C.c_int]
+        L.orc_bf16.restype = C.c_float
+        L.orc_bf16.argtypes = [C.c_float]
         L.orc_build_shortlist.restype = C.c_int
         L.orc_build_shortlist.argtypes = [C.c_int, P, C.c_int, P, C.c_int, P, C.c_int64, C.c_int,
                                           C.c_int, P]
@@ -102,7 +104,8 @@ ARITH_S32, ARITH_SAT16, ARITH_INT16 = 0, 1, 2
 
 def cfg_from_dims(m, arith: int = ARITH_S32) -> Cfg:
     return Cfg(m.d_model, m.d_ffn, m.n_heads, m.enc_layers, m.dec_layers, m.vocab, m.decoder,
-               m.aan_ffn_depth, m.aan_gate, m.out_bias, m.eos_id, m.clip, m.ln_eps, arith)
+               m.aan_ffn_depth, m.aan_gate, m.out_bias, m.eos_id, m.clip, m.ln_eps, arith,
+               getattr(m, "kv_bf16", 0))
 
 
 def q16(x: float) -> int:
@@ -118,6 +121,11 @@ def dot_codes(arith: int, a, w) -> int:
 
 
 # ------------------------------------------------------------------ scalars / kernels
+def bf16(x: float) -> float:
+    """Nearest bfloat16 of a finite fp32 value, ties to even (F3, R35)."""
+    return float(lib().orc_bf16(float(np.float32(x))))
+
+
 def sigma(clip: float = 2.0) -> float:
     return lib().orc_sigma(clip)
 

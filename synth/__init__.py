@@ -41,6 +41,7 @@ class ModelDims:
     eos_id: int = EOS_ID
     clip: float = 2.0
     ln_eps: float = 1e-6        # DESIGN.md reading R10
+    kv_bf16: int = 0            # 1: source K/V rounded to bf16 (R35)
 
 
 PRESETS: Dict[str, ModelDims] = {

@@ -25,6 +25,17 @@ def q8(x, clip=2.0):
     return np.rint(np.clip(x, np.float32(-clip), np.float32(clip)) * sig).astype(np.int8)
 
 
+def bf16_round(x):
+    """Nearest bfloat16 (ties to even) by arithmetic, not bit patterns: a normal value keeps 8
+    significant bits (frexp mantissa in [0.5, 1) scaled by 2^8, rint = half-even); below
+    2^-126 the bfloat16 grid is the fixed subnormal step 2^-133."""
+    x = np.asarray(x, np.float64)
+    m, e = np.frexp(x)
+    normal = np.ldexp(np.rint(np.ldexp(m, 8)), e - 8)
+    sub = np.rint(np.ldexp(x, 133)) * 2.0 ** -133
+    return np.where(np.abs(x) < 2.0 ** -126, sub, normal).astype(np.float32)
+
+
 def dq_scale(clip=2.0):
     return np.float32(clip * clip / (127.0 * 127.0))
 
@@ -115,6 +126,8 @@ class ParallelModel:
         qx = q8(x, c)
         kv = np.stack([np.stack([self.L(f"dec.{l}.src.k", qx), self.L(f"dec.{l}.src.v", qx)])
                        for l in range(m.dec_layers)])
+        if getattr(m, "kv_bf16", 0):
+            kv = bf16_round(kv)
         return x, kv
 
     def forced(self, src, forced, T):

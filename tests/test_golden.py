@@ -88,3 +88,8 @@ def test_shortlist_examples(orc):
         src = np.array(_ids(fields["src"], V), np.int32)
         got = orc.build_shortlist(V, freq, lex, src)
         assert got.tolist() == _ids(fields["expect"], V), ln
+
+
+def test_bf16_rounding_examples(orc):
+    for r in rows("bf16_rounding.txt"):
+        assert orc.bf16(float(r[0])) == float(r[1]), r

@@ -23,6 +23,9 @@ def tiny_variants():
                   aan_ffn_depth=0, aan_gate=0),
         ModelDims("t-self", 32, 64, 4, vocab=64, enc_layers=2, dec_layers=2, decoder=0),
         ModelDims("t-nobias", 24, 48, 3, vocab=50, enc_layers=1, dec_layers=3, out_bias=0),
+        ModelDims("t-kvbf16", 32, 64, 4, vocab=64, enc_layers=2, dec_layers=2, kv_bf16=1),
+        ModelDims("t-self-kvbf16", 32, 64, 4, vocab=64, enc_layers=2, dec_layers=2, decoder=0,
+                  kv_bf16=1),
     ]
 
 
@@ -349,3 +352,33 @@ def test_embed_rows(orc):
     assert np.array_equal(out[0], orc.pe(0, 16))           # start symbol: PE(0) only (R13)
     assert np.array_equal(out[1], RP.embed(E, [3], 5, 16)[0])
     assert np.array_equal(out[2], RP.embed(E, [19], 7, 16)[0])
+
+
+# --------------------------------------------------------------- bf16 source K/V
+def test_bf16_rounding_matches_arithmetic_form(orc):
+    """The oracle's bit-pattern rounding == the frexp/rint formulation in tests/ref_parallel.py,
+    on random values, exact ties, and values next to ties."""
+    rng = np.random.default_rng(5)
+    x = np.concatenate([rng.standard_normal(3000).astype(np.float32) * 3,
+                        rng.uniform(-1e-30, 1e-30, 200).astype(np.float32),
+                        (1 + np.arange(256) / 256.0 + 2.0 ** -9).astype(np.float32),    # ties
+                        (1 + np.arange(256) / 256.0 + 2.0 ** -9 + 2.0 ** -22).astype(np.float32)])
+    got = np.array([orc.bf16(v) for v in x], np.float32)
+    assert np.array_equal(got, RP.bf16_round(x))
+    assert np.all(got.view(np.uint32) & 0xFFFF == 0)
+    assert np.all(np.abs(got - x) <= np.abs(x) * 2.0 ** -8 + 1e-38)      # half-ulp bound
+
+
+def test_kv_bf16_oracle_keys_are_bf16_and_rounded_fp32(tiny_models):
+    """F3: K/V of a kv_bf16 model are exactly the bf16 rounding of the fp32 model's K/V."""
+    for m, w, om, pm in tiny_models:
+        if not m.kv_bf16:
+            continue
+        src = synth.random_set(1, 11, 11, seed=4, vocab=m.vocab).ids
+        _, kv16 = om.encode(src)
+        m32 = ModelDims(m.name + "-f32", m.d_model, m.d_ffn, m.n_heads, decoder=m.decoder,
+                        vocab=m.vocab, enc_layers=m.enc_layers, dec_layers=m.dec_layers)
+        _, kv32 = type(om)(m32, w).encode(src)
+        assert np.all(kv16.view(np.uint32) & 0xFFFF == 0)
+        assert np.array_equal(kv16, RP.bf16_round(kv32))
+        assert not np.array_equal(kv16, kv32)
