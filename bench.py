@@ -217,7 +217,7 @@ def run_reference(args, dims, weights, sset, workload_cfg):
     desc = (f"oracle {'greedy' if args.beam <= 1 else f'beam-{args.beam}'} decode of the same {n}-sentence seeded sample of the workload per step "
             f"({int(samp.lengths.sum())} source words)")
     line = {
-        "impl": "reference", "metric": metric_name(args.beam), "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": metric_name(args.beam, False, bool(args.kv_bf16)), "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8/f32/f64",
         "data": "synthetic (seeded random-init weights, newstest2014-shaped ids)",
@@ -352,8 +352,8 @@ def roofline_dxd_gemm(dims, sset, budget, peaks, stream, mcr, mult=1):
 
 
 def roofline_src_attn(dims, sset, budget, peaks, stream, mcr, mult=1):
-    """A7: source attention over the fp32 K/V cache, rows = the workload's mean live rows per
-    step, drawn (seeded) from the set so the source-length mix matches."""
+    """A7: source attention over the fp32 (kv_bf16: bf16, F3) K/V cache, rows = the workload's
+    mean live rows per step, drawn (seeded) from the set so the source-length mix matches."""
     import torch
     from paper_1805_12096_b200 import mnmt as M
     rows = live_rows_profile(sset, budget, mcr)
@@ -364,19 +364,25 @@ def roofline_src_attn(dims, sset, budget, peaks, stream, mcr, mult=1):
     d, H = dims.d_model, dims.n_heads
     n = len(idx)
     dev = torch.device("cuda", torch.cuda.current_device())
+    kv16 = bool(getattr(dims, "kv_bf16", 0))
     kv = torch.randn((int(L.sum()), 2 * d), device=dev)
+    if kv16:
+        kv = kv.to(torch.bfloat16)
     q = torch.randn((n, d), device=dev)
     st, ln = torch.from_numpy(starts).to(dev), torch.from_numpy(L).to(dev)
     oq = torch.empty((n, d), dtype=torch.int8, device=dev)
 
     def fn(s_):
-        M.op_attention(q.data_ptr(), d, kv.data_ptr(), 2 * d, 0, d, st.data_ptr(), ln.data_ptr(),
-                       n, d, H, dims.clip, oq.data_ptr(), None, s_)
+        op = M.op_attention_bf16 if kv16 else M.op_attention
+        op(q.data_ptr(), d, kv.data_ptr(), 2 * d, 0, d, st.data_ptr(), ln.data_ptr(),
+           n, d, H, dims.clip, oq.data_ptr(), None, s_)
     ms = time_kernel(fn, 200, stream)
-    bytes_ = float(8 * d * L.sum() + n * (4 * d + d))   # K,V fp32 + q fp32 + codes
+    # K,V (fp32 or bf16) + q fp32 + codes
+    bytes_ = float((4 if kv16 else 8) * d * L.sum() + n * (4 * d + d))
     ach = bytes_ / (ms * 1e-3) / 1e9
     peak = peaks["hbm_gbs"]
-    return {"kernel": "k_attn (A7 source attention, fp64 accumulate)", "bound": "hbm",
+    return {"kernel": "k_attn (A7 source attention, fp64 accumulate" + (", bf16 K/V)" if kv16 else ")"),
+            "bound": "hbm",
             "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
             "shape": f"rows={n} S_mean={L.mean():.1f} d={d} H={H} (one layer)",
             "ms_per_launch": ms, "peak_source": peaks["source"]}
@@ -400,7 +406,9 @@ def ncu_traffic(key, shape):
 
 
 # ---------------------------------------------------------------------------- main
-def metric_name(beam: int, shortlist: bool = False) -> str:
+def metric_name(beam: int, shortlist: bool = False, kv16: bool = False) -> str:
+    if kv16 and beam <= 1 and not shortlist:
+        return "target words/sec greedy decode with bf16 source keys/values (F3), 1 B200"
     if shortlist:
         return "target words/sec greedy decode with batch vocabulary shortlist (100 frequent + 100 per source word), 1 B200"
     return METRIC if beam <= 1 else f"target words/sec beam-{beam} decode (best hypothesis), 1 B200"
@@ -423,6 +431,8 @@ def main():
     ap.add_argument("--shortlist", action="store_true",
                     help="greedy decode with each batch's vocabulary shortlist (SURVEY 8(f) F2, "
                          "P:L85; synthetic Zipf tables, 100 frequent + 100 per source word)")
+    ap.add_argument("--kv-bf16", action="store_true",
+                    help="source keys / values rounded to bf16 (SURVEY 8(f) F3, src_kv_bf16 = 1)")
     ap.add_argument("--beam-fused", type=int, default=0,
                     help="beam search: 1 = log-sum-exp / top-k fused into the output GEMM epilogue")
     ap.add_argument("--megakernel", type=int, default=0,
@@ -455,6 +465,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     preset, budget, cfg_ref = WORKLOADS[args.workload]
     dims = synth.PRESETS[preset]
+    if args.kv_bf16:
+        import dataclasses
+        dims = dataclasses.replace(dims, name=dims.name + "-kvbf16", kv_bf16=1)
     workload_cfg = {"workload": args.workload, "baseline_config": cfg_ref,
                     "student": f"{preset}: d={dims.d_model} F={dims.d_ffn} H={dims.n_heads} "
                                f"L={dims.enc_layers}+{dims.dec_layers} V={dims.vocab} "
@@ -462,6 +475,7 @@ def main():
                     "sentences_per_gpu": synth.NEWSTEST_SENTENCES,
                     "source_words_per_gpu": synth.NEWSTEST_TOKENS, "word_budget": budget,
                     "beam": args.beam, "beam_fused": args.beam_fused,
+                    "src_kv": "bf16 (F3)" if args.kv_bf16 else "fp32",
                     "shortlist": "100 frequent + 100 per source word (synthetic Zipf tables, seed 85)" if args.shortlist else None, "max_len": "source length", "parallelism": f"dp{args.gpus}",
                     "l2": "flushed between timed steps (512 MiB write)",
                     "max_concurrent_rows": args.max_concurrent_rows, "lanes": args.lanes,
@@ -617,7 +631,7 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": metric_name(beam, use_sl), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": metric_name(beam, use_sl, bool(args.kv_bf16)), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int8 products (s32 acc), f32 activations, f64 reductions",
             "data": "synthetic (seeded random-init weights, newstest2014-shaped length-sorted ids)",

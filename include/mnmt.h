@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define MNMT_ABI_VERSION 1
+#define MNMT_ABI_VERSION 2
 
 typedef enum {
   MNMT_OK = 0,
@@ -63,6 +63,9 @@ typedef struct {
   int32_t eos_id;         /* end-of-sentence id, default 0 (R16) */
   float clip;             /* quantization clip c = 2.0 */
   float ln_eps;           /* LayerNorm epsilon, default 1e-6 (R10) */
+  int32_t src_kv_bf16;    /* 0 (default): the source keys / values K_l, V_l are fp32 (R4);
+                           * 1: they are rounded (RNE) to bf16 once per batch and source
+                           * attention reads them at half the bytes */
 } mnmt_config;
 
 typedef struct mnmt_model mnmt_model;   /* opaque; owns all of its device memory */

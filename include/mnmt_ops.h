@@ -81,6 +81,14 @@ mnmt_status mnmt_op_attention(const float* q_dev, int64_t ldq, const float* kv_d
                               const int32_t* kv_len_dev, int32_t n, int32_t d, int32_t H,
                               float clip, int8_t* out_q_dev, float* out_f_dev, void* stream);
 
+/* As mnmt_op_attention with bf16 keys / values: kv16 holds bfloat16 bit
+ * patterns (uint16) in the same layout (strides and offsets in elements, multiples of 4). */
+mnmt_status mnmt_op_attention_bf16(const float* q_dev, int64_t ldq, const uint16_t* kv16_dev,
+                                   int64_t ldkv, int32_t k_off, int32_t v_off,
+                                   const int32_t* kv_start_dev, const int32_t* kv_len_dev,
+                                   int32_t n, int32_t d, int32_t H, float clip, int8_t* out_q_dev,
+                                   float* out_f_dev, void* stream);
+
 /* Profiling hook: with model option "profile_phases" = 1, the persistent step kernel of
  * lane 0 stamps %globaltimer after every grid barrier.  out_ns_by_type[k] receives the
  * nanoseconds spent in phases of type k (0 GEMM, 1 embed, 2 LayerNorm, 3 attention,

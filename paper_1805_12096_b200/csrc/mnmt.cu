@@ -83,6 +83,7 @@ struct Workspace {
   std::vector<void*> allocs;
   // encoder (token rows)
   float *x = nullptr, *qkv = nullptr, *o = nullptr, *kv = nullptr;
+  bf16s* kv16 = nullptr;   // src_kv_bf16 (F3): bf16 copy of kv read by source attention
   int8_t *cx = nullptr, *cctx = nullptr, *ch = nullptr;
   CUtensorMap tm_cx, tm_cctx, tm_ch;
   // decoder (compact live rows)
@@ -324,6 +325,7 @@ static const char* cfg_problem(const mnmt_config* c) {
   if (c->eos_id < 0 || c->eos_id >= c->vocab) return "eos_id out of range";
   if (!(c->clip > 0.0f) || !std::isfinite(c->clip)) return "clip must be > 0";
   if (!(c->ln_eps >= 0.0f)) return "ln_eps must be >= 0";
+  if (c->src_kv_bf16 != 0 && c->src_kv_bf16 != 1) return "src_kv_bf16 must be 0 or 1";
   return nullptr;
 }
 
@@ -720,6 +722,7 @@ static mnmt_status lane_ensure(mnmt_model* m, Lane& Ln, int64_t M, int64_t B, in
   CKS(dalloc(A, &z.qkv, Mc * 3 * d));
   CKS(dalloc(A, &z.o, Mc * d));
   CKS(dalloc(A, &z.kv, L * Mc * 2 * d));
+  if (c.src_kv_bf16) CKS(dalloc(A, &z.kv16, L * Mc * 2 * d));
   CKS(dalloc(A, &z.cx, Mc * d));
   CKS(dalloc(A, &z.cctx, Mc * d));
   CKS(dalloc(A, &z.ch, Mc * F));
@@ -908,6 +911,12 @@ static cudaError_t launch_encoder(mnmt_model* m, Lane& Ln, int M, const int32_t*
                 w.M_cap * 2 * d)) != cudaSuccess)
     return e;
   ++*nlaunch;
+  if (c.src_kv_bf16) {   // F3 (R35): K/V rounded to bf16 once per batch; attention reads kv16
+    if ((e = launch_kv_bf16(w.kv, w.kv16, c.dec_layers, (int64_t)M * 2 * d, w.M_cap * 2 * d, st)) !=
+        cudaSuccess)
+      return e;
+    ++*nlaunch;
+  }
   return cudaSuccess;
 }
 
@@ -1110,6 +1119,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
       as.q = w.qs;
       as.ldq = d;
       as.kv = w.kv + (int64_t)l * w.M_cap * 2 * d;
+      as.kv16 = c.src_kv_bf16 ? w.kv16 + (int64_t)l * w.M_cap * 2 * d : nullptr;
       as.ldkv = 2 * d;
       as.k_off = 0;
       as.v_off = d;
@@ -1391,6 +1401,7 @@ static mnmt_status build_program(mnmt_model* m, Lane& Ln, bool forced) {
       as.q = w.qs;
       as.ldq = d;
       as.kv = w.kv + (int64_t)l * w.M_cap * 2 * d;
+      as.kv16 = c.src_kv_bf16 ? w.kv16 + (int64_t)l * w.M_cap * 2 * d : nullptr;
       as.ldkv = 2 * d;
       as.k_off = 0;
       as.v_off = d;
@@ -1868,6 +1879,7 @@ void mnmt_config_default(mnmt_config* c, int32_t d_model, int32_t d_ffn, int32_t
   c->eos_id = 0;
   c->clip = 2.0f;
   c->ln_eps = 1e-6f;
+  c->src_kv_bf16 = 0;
 }
 
 mnmt_status mnmt_model_create(const mnmt_config* cfg, int32_t cuda_device, mnmt_model** out) {

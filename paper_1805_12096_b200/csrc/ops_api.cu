@@ -175,6 +175,35 @@ mnmt_status mnmt_op_attention(const float* q, int64_t ldq, const float* kv, int6
   return cuda_status(launch_attn(a, (cudaStream_t)stream), "attention");
 }
 
+mnmt_status mnmt_op_attention_bf16(const float* q, int64_t ldq, const uint16_t* kv16, int64_t ldkv,
+                                   int32_t k_off, int32_t v_off, const int32_t* kv_start,
+                                   const int32_t* kv_len, int32_t n, int32_t d, int32_t H,
+                                   float clip, int8_t* out_q, float* out_f, void* stream) {
+  if (n < 0 || H < 1 || d % H || (d / H) % 4 || d / H > 64 || !q || !kv16 || !kv_start ||
+      !kv_len || !out_q || ldq % 4 || ldkv % 4 || k_off % 4 || v_off % 4 || !(clip > 0.0f))
+    return arg_error("mnmt_op_attention_bf16: bad arguments");
+  if (cudaError_t e = attn_init(); e != cudaSuccess) return cuda_status(e, "attention init");
+  AttnArgs a{};
+  a.mode = ATTN_ENC;
+  a.n = n;
+  a.H = H;
+  a.dh = d / H;
+  a.d = d;
+  a.q = q;
+  a.ldq = ldq;
+  a.kv16 = reinterpret_cast<const bf16s*>(kv16);
+  a.ldkv = ldkv;
+  a.k_off = k_off;
+  a.v_off = v_off;
+  a.kv_start = kv_start;
+  a.kv_len = kv_len;
+  a.clip = clip;
+  a.sigma = sigma_of(clip);
+  a.out_q = out_q;
+  a.out_f = out_f;
+  return cuda_status(launch_attn(a, (cudaStream_t)stream), "attention (bf16 K/V)");
+}
+
 }  // extern "C"
 
 // Debug: a chain of `n` identical int8 GEMMs (M x N x K, EPI_F32, A -> out, PDL, captured in a CUDA

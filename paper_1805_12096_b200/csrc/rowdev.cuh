@@ -156,8 +156,22 @@ __device__ __forceinline__ void ln_row(const LnArgs a, int r) {
 // over the positions in order (V loads issued 4 ahead).
 __device__ __forceinline__ double to_f64(float x) { return (double)x; }
 __device__ __forceinline__ double to_f64(double x) { return x; }
+// bf16 storage of the source keys / values: the upper half of an fp32
+__device__ __forceinline__ double to_f64(bf16s x) { return (double)__uint_as_float((uint32_t)x.u << 16); }
+// four consecutive K elements (16-byte fp32 or 8-byte bf16 load), widened exactly to fp64
+__device__ __forceinline__ void ld4_f64(const float* p, double (&o)[4]) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+__device__ __forceinline__ void ld4_f64(const bf16s* p, double (&o)[4]) {
+  const uint2 v = *reinterpret_cast<const uint2*>(p);
+  o[0] = (double)__uint_as_float(v.x << 16);
+  o[1] = (double)__uint_as_float(v.x & 0xffff0000u);
+  o[2] = (double)__uint_as_float(v.y << 16);
+  o[3] = (double)__uint_as_float(v.y & 0xffff0000u);
+}
 
-// KT = float: K/V rows in global memory (each element converted once, when used);
+// KT = float / bf16s: K/V rows in global memory (each element converted once, when used);
 // KT = double: K/V already converted (staged in shared memory by the caller).
 // qd: per-warp scratch of dh doubles (the query converted once).
 // IND: rows[j] is the row of position j (beam search: the self-attention cache rows of a
@@ -179,10 +193,9 @@ __device__ __forceinline__ void warp_attend(const float* __restrict__ q, const K
     double dot = 0.0;
     for (int c = 0; c < dh; c += 4) {
       double kk[4], qq[4];
-      if constexpr (sizeof(KT) == 4) {
-        const float4 k4 = *reinterpret_cast<const float4*>(kr + c);
+      if constexpr (sizeof(KT) <= 4) {
+        ld4_f64(kr + c, kk);
         const float4 q4 = *reinterpret_cast<const float4*>(q + c);   // same address in all lanes
-        kk[0] = k4.x; kk[1] = k4.y; kk[2] = k4.z; kk[3] = k4.w;
         qq[0] = q4.x; qq[1] = q4.y; qq[2] = q4.z; qq[3] = q4.w;
       } else {
         const double2 a = *reinterpret_cast<const double2*>(kr + c);
@@ -282,6 +295,14 @@ __device__ __forceinline__ void attn_row_head(const AttnArgs a, int r, int h, do
       return;
     }
     __syncwarp();
+  }
+  if (a.kv16) {   // bf16 source K/V (F3): same layout, half the bytes
+    const bf16s* K16 = a.kv16 + (int64_t)start * a.ldkv + a.k_off + h * dh;
+    const bf16s* V16 = a.kv16 + (int64_t)start * a.ldkv + a.v_off + h * dh;
+    warp_attend<bf16s>(q, K16, V16, a.ldkv, len, dh, sc, sc + span, a.clip, a.sigma,
+                       a.out_q + (int64_t)r * a.d + h * dh,
+                       a.out_f ? a.out_f + (int64_t)r * a.d + h * dh : nullptr);
+    return;
   }
   const float* K = a.kv + (int64_t)start * a.ldkv + a.k_off + h * dh;
   const float* V = a.kv + (int64_t)start * a.ldkv + a.v_off + h * dh;

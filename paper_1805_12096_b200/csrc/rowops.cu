@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn(AttnArgs a) {
 // scores the 32-position chunks w, w + NS, ...; the row max is exchanged first, so every
 // p_j = exp(s_j - max) is the value of the one-warp kernel; Z and the context are per-warp
 // partial sums (positions in order inside a warp) combined in warp order (R25).
-template <int NS>
+template <int NS, typename KT>
 __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn_split(AttnArgs a) {
   constexpr int G = ATTN_WARPS / NS;                      // (row, head) groups per CTA
   extern __shared__ __align__(16) double as_smem[];
@@ -158,23 +158,26 @@ __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn_split(AttnArgs a) {
     len = a.live_start ? a.live_len[r] : a.kv_len[a.live[r]];
   }
   const float* q = a.q + (int64_t)(live ? r : 0) * a.ldq + h * dh;
-  const float* K = a.kv + (int64_t)start * a.ldkv + a.k_off + h * dh;
-  const float* V = a.kv + (int64_t)start * a.ldkv + a.v_off + h * dh;
+  const KT* kvb;
+  if constexpr (sizeof(KT) == 2) kvb = a.kv16; else kvb = a.kv;   // bf16 source K/V (F3)
+  const KT* K = kvb + (int64_t)start * a.ldkv + a.k_off + h * dh;
+  const KT* V = kvb + (int64_t)start * a.ldkv + a.v_off + h * dh;
   const double inv_sqrt = 1.0 / sqrt((double)dh);
   // ---- scores of this warp's chunks, local max
   double mx = -INFINITY;
   for (int j0 = w * 32; j0 < len; j0 += NS * 32) {
     const int j = j0 + lane;
     if (j < len) {
-      const float* kr = K + (int64_t)j * a.ldkv;
+      const KT* kr = K + (int64_t)j * a.ldkv;
       double dot = 0.0;
       for (int c = 0; c < dh; c += 4) {
-        const float4 k4 = *reinterpret_cast<const float4*>(kr + c);
+        double kk[4];
+        ld4_f64(kr + c, kk);
         const float4 q4 = *reinterpret_cast<const float4*>(q + c);
-        dot = __fma_rn((double)q4.x, (double)k4.x, dot);
-        dot = __fma_rn((double)q4.y, (double)k4.y, dot);
-        dot = __fma_rn((double)q4.z, (double)k4.z, dot);
-        dot = __fma_rn((double)q4.w, (double)k4.w, dot);
+        dot = __fma_rn((double)q4.x, kk[0], dot);
+        dot = __fma_rn((double)q4.y, kk[1], dot);
+        dot = __fma_rn((double)q4.z, kk[2], dot);
+        dot = __fma_rn((double)q4.w, kk[3], dot);
       }
       const double sj = __dmul_rn(dot, inv_sqrt);
       sc[j] = sj;
@@ -207,14 +210,16 @@ __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn_split(AttnArgs a) {
       const int je = min(j0 + 32, len);
       int j = j0;
       for (; j + 4 <= je; j += 4) {
-        const double v0 = V[(int64_t)(j + 0) * a.ldkv + c], v1 = V[(int64_t)(j + 1) * a.ldkv + c];
-        const double v2 = V[(int64_t)(j + 2) * a.ldkv + c], v3 = V[(int64_t)(j + 3) * a.ldkv + c];
+        const double v0 = to_f64(V[(int64_t)(j + 0) * a.ldkv + c]);
+        const double v1 = to_f64(V[(int64_t)(j + 1) * a.ldkv + c]);
+        const double v2 = to_f64(V[(int64_t)(j + 2) * a.ldkv + c]);
+        const double v3 = to_f64(V[(int64_t)(j + 3) * a.ldkv + c]);
         acc = __fma_rn(sc[j + 0], v0, acc);
         acc = __fma_rn(sc[j + 1], v1, acc);
         acc = __fma_rn(sc[j + 2], v2, acc);
         acc = __fma_rn(sc[j + 3], v3, acc);
       }
-      for (; j < je; ++j) acc = __fma_rn(sc[j], (double)V[(int64_t)j * a.ldkv + c], acc);
+      for (; j < je; ++j) acc = __fma_rn(sc[j], to_f64(V[(int64_t)j * a.ldkv + c]), acc);
     }
     pacc[(g * NS + w) * 64 + c] = acc;
   }
@@ -508,10 +513,16 @@ cudaError_t attn_init() {   // once per device
     e = cudaFuncSetAttribute(k_attn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              ATTN_WARPS * (MNMT_MAX_KV + 64) * (int)sizeof(double));
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_attn_split<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(k_attn_split<2, bf16s>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)attn_split_smem(2, MNMT_MAX_KV));
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_attn_split<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(k_attn_split<4, bf16s>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)attn_split_smem(4, MNMT_MAX_KV));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn_split<2, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)attn_split_smem(2, MNMT_MAX_KV));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn_split<4, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)attn_split_smem(4, MNMT_MAX_KV));
   if (e == cudaSuccess) e = set_carveouts();
   if (e == cudaSuccess) {
@@ -521,6 +532,31 @@ cudaError_t attn_init() {   // once per device
   }
   if (e == cudaSuccess && dev >= 0 && dev < 64) done[dev] = true;
   return e;
+}
+
+// Source K/V to bf16 (F3, R35): kv16 = RNE bf16 of kv, and kv itself rounded to the same value
+// (so every reader of the fp32 copy sees the rounded keys / values).  L slices of n elements
+// at stride `stride`.
+__global__ void k_kv_bf16(float* __restrict__ kv, bf16s* __restrict__ kv16, int64_t n,
+                          int64_t stride) {
+  pdl_wait();
+  pdl_trigger_early();
+  const int64_t off = (int64_t)blockIdx.y * stride;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = __float_as_uint(kv[off + i]);
+    const uint32_t r = (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;   // RNE (finite inputs)
+    kv16[off + i].u = (uint16_t)(r >> 16);
+    kv[off + i] = __uint_as_float(r);
+  }
+}
+
+cudaError_t launch_kv_bf16(float* kv, bf16s* kv16, int L, int64_t n, int64_t stride,
+                           cudaStream_t st) {
+  if (n <= 0 || L <= 0) return cudaSuccess;
+  int64_t bx = (n + 255) / 256;
+  if (bx > 148 * 4) bx = 148 * 4;
+  return launch_pdl(k_kv_bf16, dim3((unsigned)bx, L), dim3(256), 0, st, kv, kv16, n, stride);
 }
 
 cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
@@ -535,8 +571,11 @@ cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
   if (ns == 2 || ns == 4) {
     const int G = ATTN_WARPS / ns;
     const dim3 grid((unsigned)((warps + G - 1) / G)), block(ATTN_WARPS * 32);
-    return ns == 2 ? launch_pdl(k_attn_split<2>, grid, block, attn_split_smem(2, b.span), st, b)
-                   : launch_pdl(k_attn_split<4>, grid, block, attn_split_smem(4, b.span), st, b);
+    if (b.kv16)
+      return ns == 2 ? launch_pdl(k_attn_split<2, bf16s>, grid, block, attn_split_smem(2, b.span), st, b)
+                     : launch_pdl(k_attn_split<4, bf16s>, grid, block, attn_split_smem(4, b.span), st, b);
+    return ns == 2 ? launch_pdl(k_attn_split<2, float>, grid, block, attn_split_smem(2, b.span), st, b)
+                   : launch_pdl(k_attn_split<4, float>, grid, block, attn_split_smem(4, b.span), st, b);
   }
   const dim3 grid((unsigned)((warps + ATTN_WARPS - 1) / ATTN_WARPS)), block(ATTN_WARPS * 32);
   return launch_pdl(k_attn, grid, block, (size_t)ATTN_WARPS * (b.span + 64) * 8, st, b);

@@ -52,6 +52,8 @@ struct LnArgs {
 
 enum AttnMode : int { ATTN_ENC = 0, ATTN_SRC = 1, ATTN_SELF = 2 };
 
+struct bf16s { uint16_t u; };   // bf16 bits (source K/V storage, F3)
+
 struct AttnArgs {
   int mode;
   int span;                 // longest attended span of the launch (<= MNMT_MAX_KV; sizes smem)
@@ -64,6 +66,7 @@ struct AttnArgs {
   int64_t ldq;
   const float* kv;          // key/value rows, row stride ldkv; K at +k_off, V at +v_off
   float* kv_w;              // self mode: writable cache (same as kv)
+  const bf16s* kv16;        // src mode, optional: bf16 copy of kv (same layout), read instead (F3)
   int64_t ldkv;
   int k_off, v_off;
   const int32_t* kv_start;  // enc: [row]; src: [orig]
@@ -120,6 +123,7 @@ cudaError_t launch_embed_src(const int32_t* ids, const int32_t* idx, const int32
 cudaError_t launch_embed_tgt(const EmbedTgtArgs& a, int rows, cudaStream_t st);
 cudaError_t launch_ln(const LnArgs& a, cudaStream_t st);
 cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st);
+cudaError_t launch_kv_bf16(float* kv, bf16s* kv16, int L, int64_t n, int64_t stride, cudaStream_t st);
 cudaError_t launch_attn_enc(const EncAttnArgs& a, cudaStream_t st);
 cudaError_t attn_init();   // dynamic-smem attribute (call once per device, outside capture)
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t st);

@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmnmt.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 MAX_SPAN = 512
 DEVICE_IO = 1
 SHORTLIST = 2
@@ -40,7 +40,7 @@ class Config(C.Structure):
                 ("n_heads", C.c_int32), ("enc_layers", C.c_int32), ("dec_layers", C.c_int32),
                 ("vocab", C.c_int32), ("decoder", C.c_int32), ("aan_ffn_depth", C.c_int32),
                 ("aan_gate", C.c_int32), ("out_bias", C.c_int32), ("eos_id", C.c_int32),
-                ("clip", C.c_float), ("ln_eps", C.c_float)]
+                ("clip", C.c_float), ("ln_eps", C.c_float), ("src_kv_bf16", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -55,7 +55,7 @@ EXPORTS = [
     "mnmt_decode_forced",
     "mnmt_get_stats", "mnmt_last_error", "mnmt_model_destroy", "mnmt_model_set_option",
     "mnmt_op_quantize", "mnmt_op_gemm_i8", "mnmt_op_argmax_ids", "mnmt_op_layernorm",
-    "mnmt_op_aan_step", "mnmt_op_embed", "mnmt_op_attention", "mnmt_debug_phase_profile",
+    "mnmt_op_aan_step", "mnmt_op_embed", "mnmt_op_attention", "mnmt_op_attention_bf16", "mnmt_debug_phase_profile",
 ]
 
 _lib = None
@@ -95,6 +95,7 @@ def lib():
     L.mnmt_op_aan_step.argtypes = [P, P, I32, I32, I32, F, P, P, P]
     L.mnmt_op_embed.argtypes = [P, I32, P, P, I32, F, P, P, P]
     L.mnmt_op_attention.argtypes = [P, I64, P, I64, I32, I32, P, P, I32, I32, I32, F, P, P, P]
+    L.mnmt_op_attention_bf16.argtypes = [P, I64, P, I64, I32, I32, P, P, I32, I32, I32, F, P, P, P]
     L.mnmt_debug_phase_profile.argtypes = [P, P, I32, P]
     for name in EXPORTS:
         fn = getattr(L, name)
@@ -119,6 +120,7 @@ def config_from_dims(m) -> Config:
     for f in ("d_model", "d_ffn", "n_heads", "enc_layers", "dec_layers", "vocab", "decoder",
               "aan_ffn_depth", "aan_gate", "out_bias", "eos_id", "clip", "ln_eps"):
         setattr(c, f, getattr(m, f))
+    c.src_kv_bf16 = getattr(m, "kv_bf16", 0)
     return c
 
 
@@ -347,3 +349,10 @@ def op_attention(q_ptr, ldq, kv_ptr, ldkv, k_off, v_off, start_ptr, len_ptr, n, 
                  out_q_ptr, out_f_ptr=None, stream=None) -> None:
     _check(lib().mnmt_op_attention(q_ptr, ldq, kv_ptr, ldkv, k_off, v_off, start_ptr, len_ptr, n,
                                    d, H, clip, out_q_ptr, out_f_ptr, _stream_ptr(stream)))
+
+
+def op_attention_bf16(q_ptr, ldq, kv16_ptr, ldkv, k_off, v_off, start_ptr, len_ptr, n, d, H, clip,
+                      out_q_ptr, out_f_ptr=None, stream=None) -> None:
+    _check(lib().mnmt_op_attention_bf16(q_ptr, ldq, kv16_ptr, ldkv, k_off, v_off, start_ptr,
+                                        len_ptr, n, d, H, clip, out_q_ptr, out_f_ptr,
+                                        _stream_ptr(stream)))
