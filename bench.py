@@ -41,6 +41,17 @@ WORKLOADS = {
     "big-newstest-8192w": ("big", 8192, "configs[3]"),
 }
 DEFAULT_WORKLOAD = "small-aan-newstest-8192w"
+# Per-workload launch options (scheduling only: ids are identical for every setting), from the
+# green_sms x lane_tiers sweep on one B200 (profiles/r1_sweep_green_tiers.txt): the critical
+# lane's SM partition pays off for the smaller students and costs the big one (its bulk lanes
+# need every SM).
+WORKLOAD_OPTS = {
+    "small-aan-newstest-8192w": {"green_sms": 48, "lane_tiers": 40},
+    "tiny192-aan-newstest-8192w": {"green_sms": 56, "lane_tiers": 40},
+    "base-newstest-8192w": {"green_sms": 24, "lane_tiers": 40},
+    "base-aan-newstest-8192w": {"green_sms": 40, "lane_tiers": 35},
+    "big-newstest-8192w": {"green_sms": 0, "lane_tiers": 25},
+}
 L2_FLUSH_BYTES = 512 << 20   # > 126 MB L2
 
 
@@ -439,14 +450,15 @@ def main():
                     help="1: persistent step kernel per batch; 0: one kernel per op (CUDA graph)")
     ap.add_argument("--lanes", type=int, default=3,
                     help="independent decoder lanes (streams) per GPU (scheduling only)")
-    ap.add_argument("--lane-tiers", type=int, default=40,
+    ap.add_argument("--lane-tiers", type=int, default=None,
                     help="0: deal sentences round-robin to lanes; 10*p: contiguous length tiers "
-                         "of equal sum S^p (scheduling only)")
+                         "of equal sum S^p (scheduling only; default: per workload)")
     ap.add_argument("--rowfuse", type=int, default=0,
                     help="steps with <= this many padded rows use the fused per-row AAN and "
                          "source-attention blocks (0 = off)")
-    ap.add_argument("--green-sms", type=int, default=56,
-                    help="SM partition (green context) of the critical lane; 0 = shared SMs")
+    ap.add_argument("--green-sms", type=int, default=None,
+                    help="SM partition (green context) of the critical lane; 0 = shared SMs "
+                         "(default: per workload)")
     ap.add_argument("--pers-reserve", type=int, default=16,
                     help="SMs the persistent GEMMs of non-critical lanes leave free")
     ap.add_argument("--steps-per-graph", type=int, default=1,
@@ -459,6 +471,11 @@ def main():
                          "(scheduling only; 0 = one batch at a time)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    for k, v in WORKLOAD_OPTS.get(args.workload, {}).items():
+        if getattr(args, k) is None:
+            setattr(args, k, v)
+    args.green_sms = 56 if args.green_sms is None else args.green_sms
+    args.lane_tiers = 40 if args.lane_tiers is None else args.lane_tiers
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
