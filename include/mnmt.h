@@ -203,7 +203,9 @@ mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids_host,
  *                          producing GEMM: 1 = one CTA owns whole rows (d = 192, 256);
  *                          2 = the d / BN N-tiles of a row block form a thread-block cluster
  *                          and exchange row statistics through distributed shared memory;
- *                          0 (default, measured faster): separate LayerNorm kernels.
+ *                          3 = as 1 for the decoder's d x d producers only (f-gate, source-
+ *                          attention output); FFN2 keeps its split-N GEMM + LayerNorm kernel;
+ *                          0 (default): separate LayerNorm kernels.
  *   "rowlocal"             persistent kernel only: 1 = GEMM/LayerNorm/embedding phases split by
  *                          128-row tile (CTA barriers between them), 0 (default) = split over the
  *                          grid with grid barriers.

@@ -15,6 +15,7 @@
 //               tcgen05.ld 32 lanes x 32 columns -> registers -> fused op -> HBM.
 // Rows beyond the live-row count (M_dyn, read on device) are computed but never stored,
 // and whole M-tiles beyond it exit before allocating TMEM.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cudaTypedefs.h>
@@ -22,6 +23,7 @@
 #include "kernels.h"
 #include "numerics.cuh"
 #include "ptx.cuh"
+#include "rowdev.cuh"
 
 namespace mnmt {
 
@@ -240,117 +242,41 @@ __device__ __forceinline__ void epi_store_chunk(const GemmArgs& args, const floa
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-// Full-row LayerNorm epilogue (EPI_LN, BN = d): the 8 epilogue warps hold the tile's 128
-// rows as two column halves per row.  Pass 1 forms the residual r (written to the output
-// row as scratch), passes 2-3 form the fp64 statistics (R20) with the two halves combined
-// through shared memory, pass 3 writes LN(r), Q(LN(r)) and the next layer's AAN step --
-// the arithmetic of ln_row / k_ln, with the row sums split into two ordered halves.
+// Full-row LayerNorm epilogue (EPI_LN, BN = N = d: this CTA owns whole rows).  Once the
+// accumulator is complete the pipeline's shared memory is free: phase A dequantises the tile
+// (fmaf(acc, s, b), the EPI_F32 arithmetic) into a [128][BN + 4] fp32 tile there (thread = row,
+// 16-byte stores, conflict-free); phase B runs the k_ln row (ln_row: residual or AAN gate, fp64
+// statistics, R20; codes; next-layer AAN step) one warp per live row with coalesced global
+// accesses, reading the GEMM output row from the tile.  Same arithmetic as GEMM + k_ln.
+constexpr int LN_TILE_LD_PAD = 4;
 template <int BN>
-__device__ __forceinline__ void ln_epilogue(const GemmArgs& a, uint32_t t_row, int row,
-                                            bool row_ok, int half, int rl, double* part) {
-  constexpr int HALF = BN / 2;
-  const LnArgs& L = a.ln;
-  const bool small = a.K <= 256;
-  const int c0 = half * HALF;
-  const int64_t off = (int64_t)row * BN;
-  const bool gate = L.gi != nullptr;
-  // ---- pass 1: residual (+ gate), sum
-  double s = 0.0;
+constexpr int ln_tile_bytes() { return BM * (BN + LN_TILE_LD_PAD) * 4; }
+
+template <int BN>
+__device__ __forceinline__ void ln_epilogue(const GemmArgs& a, uint32_t t_row, int half, int rl,
+                                            float* tile, int m0, int M_live, int ew) {
+  constexpr int HALF = BN / 2, LD = BN + LN_TILE_LD_PAD;
+  const bool fast = a.K <= 256;
 #pragma unroll 1
   for (int c = 0; c < HALF; c += 32) {
     int32_t acc[32];
     tmem_ld16(t_row + c, *reinterpret_cast<int32_t(*)[16]>(acc));
     tmem_ld16(t_row + c + 16, *reinterpret_cast<int32_t(*)[16]>(acc + 16));
     tmem_ld_wait();
-    if (row_ok) {
-#pragma unroll 4
-      for (int j = 0; j < 32; ++j) {
-        const int col = c0 + c + j;
-        const float v = __fmaf_rn(acc_to_float(acc[j], small), a.scale, a.bias ? __ldg(a.bias + col) : 0.0f);
-        const float x = L.x[off + col];
-        float r;
-        if (gate) {
-          // AAN gate (R8): i = sigmoid(gi logit), f = sigmoid(v); z = fl(fl(i*y) + fl(f*a))
-          const float iy = __fmul_rn(sigmoid_f64(L.gi[off + col]), x);
-          const float fa = __fmul_rn(sigmoid_f64(v), L.delta[off + col]);
-          r = __fadd_rn(x, __fadd_rn(iy, fa));
-        } else {
-          r = __fadd_rn(x, v);
-        }
-        L.out[off + col] = r;
-        s = __dadd_rn(s, (double)r);
-      }
-    }
+    const int n = half * HALF + c;
+    float v[32];
+    dequant32(a, a.bias, n, fast, acc, v);
+    float* dst = tile + rl * LD + n;
+#pragma unroll
+    for (int j = 0; j < 32; j += 4)
+      *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
   }
-  part[half * 128 + rl] = s;
   epi_bar();
-  const double mu = __ddiv_rn(__dadd_rn(part[rl], part[128 + rl]), (double)BN);
-  epi_bar();
-  // ---- pass 2: variance
-  double qv = 0.0;
-  if (row_ok) {
-#pragma unroll 4
-    for (int j = 0; j < HALF; ++j) {
-      const double t = __dsub_rn((double)L.out[off + c0 + j], mu);
-      qv = __dadd_rn(qv, __dmul_rn(t, t));
-    }
-  }
-  part[half * 128 + rl] = qv;
-  epi_bar();
-  const double var = __ddiv_rn(__dadd_rn(part[rl], part[128 + rl]), (double)BN);
-  epi_bar();
-  const double inv = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(var, (double)L.eps)));
-  if (!row_ok) return;
-  // ---- pass 3: output, codes, AAN step of the next layer
-  const int orig = L.aan.C ? L.live[row] : 0;
-  const float tf = L.aan.C ? (float)L.ctrl[1] : 1.0f;
+  constexpr int NV = (BN / 4 + 31) / 32;
 #pragma unroll 1
-  for (int c = 0; c < HALF; c += 16) {
-    float o[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int col = c0 + c + j;
-      const double r = (double)L.out[off + col];
-      o[j] = (float)__dadd_rn(__dmul_rn(__dmul_rn(__dsub_rn(r, mu), inv), (double)L.gamma[col]),
-                              (double)L.beta[col]);
-    }
-#pragma unroll
-    for (int j = 0; j < 16; j += 4)
-      *reinterpret_cast<float4*>(L.out + off + c0 + c + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
-    if (L.out_q) {
-      uint32_t w[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        w[j] = (uint32_t)(q8(o[4 * j], L.clip, L.sigma) & 0xff) |
-               ((uint32_t)(q8(o[4 * j + 1], L.clip, L.sigma) & 0xff) << 8) |
-               ((uint32_t)(q8(o[4 * j + 2], L.clip, L.sigma) & 0xff) << 16) |
-               ((uint32_t)(q8(o[4 * j + 3], L.clip, L.sigma) & 0xff) << 24);
-      *reinterpret_cast<uint4*>(L.out_q + off + c0 + c) = make_uint4(w[0], w[1], w[2], w[3]);
-    }
-    if (L.aan.C) {
-      // AAN step (R6, R7): C <- fl(C + y); g = fl(C / t)
-      float* Cr = L.aan.C + (int64_t)orig * BN + c0 + c;
-      float g[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float cv = __fadd_rn(Cr[j], o[j]);
-        Cr[j] = cv;
-        g[j] = __fdiv_rn(cv, tf);
-      }
-      if (L.aan.g_f)
-#pragma unroll
-        for (int j = 0; j < 16; ++j) L.aan.g_f[off + c0 + c + j] = g[j];
-      if (L.aan.g_q) {
-        uint32_t w[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          w[j] = (uint32_t)(q8(g[4 * j], L.aan.clip, L.aan.sigma) & 0xff) |
-                 ((uint32_t)(q8(g[4 * j + 1], L.aan.clip, L.aan.sigma) & 0xff) << 8) |
-                 ((uint32_t)(q8(g[4 * j + 2], L.aan.clip, L.aan.sigma) & 0xff) << 16) |
-                 ((uint32_t)(q8(g[4 * j + 3], L.aan.clip, L.aan.sigma) & 0xff) << 24);
-        *reinterpret_cast<uint4*>(L.aan.g_q + off + c0 + c) = make_uint4(w[0], w[1], w[2], w[3]);
-      }
-    }
+  for (int rr = ew; rr < BM; rr += EPI_WARPS) {
+    if (m0 + rr >= M_live) break;   // warp-uniform
+    ln_row<NV>(a.ln, m0 + rr, tile + rr * LD);
   }
 }
 
@@ -490,7 +416,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __shared__ __align__(8) uint64_t empty_bar[Cfg::STAGES];
   __shared__ __align__(8) uint64_t tmem_full_bar;
   __shared__ uint32_t tmem_slot;
-  __shared__ double ln_part[EPI == EPI_LN ? 256 : 1];
   __shared__ double exp_tab[is_topk(EPI) ? 64 : 1];   // 2^(i/64) for exp_neg (EPI_TOPK*)
   __shared__ __align__(16) float bias_s[BN];   // the tile's bias, staged before the PDL wait
 
@@ -623,7 +548,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     float best_v = -INFINITY;
     int best_j = -1;
     if constexpr (EPI == EPI_LN) {
-      ln_epilogue<BN>(args, t_row, row, row_ok, half, q * 32 + lane, ln_part);
+      ln_epilogue<BN>(args, t_row, half, q * 32 + lane, reinterpret_cast<float*>(smem), m0,
+                      M_live, warp - 2);
     } else if constexpr (is_topk(EPI)) {
       topk_epilogue<BN, topk_k(EPI)>(args, args.bias ? bias_s - n0 : nullptr, t_row, row, row_ok,
                                      half, n0, exp_tab);
@@ -1196,10 +1122,12 @@ static cudaError_t gemm_init_all();
 // device (once per device).  Must run before any launch (never inside a stream capture).
 static cudaError_t set_attr_ln() {
   cudaError_t e = cudaFuncSetAttribute(k_gemm_i8<192, EPI_LN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       GemmCfg<192>::smem_for(GemmCfg<192>::STAGES));
+                                       std::max(GemmCfg<192>::smem_for(GemmCfg<192>::STAGES),
+                                                1024 + ln_tile_bytes<192>()));
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_gemm_i8<256, EPI_LN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              GemmCfg<256>::smem_for(GemmCfg<256>::STAGES));
+                              std::max(GemmCfg<256>::smem_for(GemmCfg<256>::STAGES),
+                                       1024 + ln_tile_bytes<256>()));
 }
 
 cudaError_t gemm_init() {
@@ -1257,6 +1185,8 @@ static cudaError_t launch_np(const CUtensorMap& tmA, const CUtensorMap& tmB, con
   cfg.gridDim = dim3((a.N + BN - 1) / BN, (a.M + BM - 1) / BM);
   cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = Cfg::smem_for(num_kb < Cfg::STAGES ? num_kb : Cfg::STAGES);
+  if constexpr (EPI == EPI_LN)   // the LayerNorm tile reuses the pipeline's shared memory
+    cfg.dynamicSmemBytes = std::max<size_t>(cfg.dynamicSmemBytes, 1024 + ln_tile_bytes<BN>());
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -793,6 +793,11 @@ static bool fuse_ln(const mnmt_model* m) {
   if (m->fuse_ln == 2) return gemm_lnc_bn(m->c.d_model) != 0;
   return (m->c.d_model == 192 || m->c.d_model == 256) && m->fuse_ln == 1;
 }
+// fuse_ln = 3: only the decoder's d x d producers (f-gate -> gate LayerNorm, source-attention
+// output -> LayerNorm 2) own whole rows; FFN2 (K = F) keeps its split-N GEMM + k_ln
+static bool fuse_ln_dd(const mnmt_model* m) {
+  return fuse_ln(m) || ((m->c.d_model == 192 || m->c.d_model == 256) && m->fuse_ln == 3);
+}
 
 static cudaError_t gemm_ln(mnmt_model* m, cudaStream_t st, const CUtensorMap& tmA, const Lin& W,
                            int M, const int32_t* M_dyn, const LnArgs& ln) {
@@ -1026,7 +1031,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
           l1 = ln_args(m, w, n, nd, w.y, a_f, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
           l1.gi = w.gi;
           l1.gf = w.gf;
-          if (fuse_ln(m)) {
+          if (fuse_ln_dd(m)) {
             // f-gate GEMM with the gate combine + LayerNorm in its epilogue (reads gi: join first)
             if (fork && (e = cudaStreamWaitEvent(st, Ln.ev_join, 0)) != cudaSuccess) return e;
             if ((e = gemm_ln(m, st, tm_a, D.gf, n, nd, l1)) != cudaSuccess) return e;
@@ -1034,7 +1039,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
           } else {
             if ((e = gemm(m, st, tm_a, D.gf, n, nd, EPI_F32, w.gf, nullptr, d)) != cudaSuccess) return e;
           }
-          if (fork && !fuse_ln(m) && (e = cudaStreamWaitEvent(st, Ln.ev_join, 0)) != cudaSuccess)
+          if (fork && !fuse_ln_dd(m) && (e = cudaStreamWaitEvent(st, Ln.ev_join, 0)) != cudaSuccess)
             return e;   // join before the gate LayerNorm reads gi
           k += 2;
         } else {
@@ -1132,7 +1137,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
       as.out_q = w.cctxd;
       if ((e = launch_attn(as, st)) != cudaSuccess) return e;
       LnArgs l2 = ln_args(m, w, n, nd, w.x1, w.od, D.ln[1][0], D.ln[1][1], w.x2, w.cx2);
-      if (fuse_ln(m)) {
+      if (fuse_ln_dd(m)) {
         if ((e = gemm_ln(m, st, w.tm_cctxd, D.so, n, nd, l2)) != cudaSuccess) return e;
         k += 3;
       } else {
@@ -2435,7 +2440,7 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
     return MNMT_OK;
   }
   if (std::string(name) == "fuse_ln") {
-    if (value > 2) { set_err("fuse_ln must be 0, 1 or 2"); return MNMT_ERR_ARG; }
+    if (value > 3) { set_err("fuse_ln must be 0, 1, 2 or 3"); return MNMT_ERR_ARG; }
     m->fuse_ln = (int)value;
     for (Lane& L : m->lanes) {   // captured graphs encode the old kernel sequence
       for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);

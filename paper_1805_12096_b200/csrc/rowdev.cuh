@@ -78,8 +78,10 @@ __device__ __forceinline__ void embed_tgt_row(const EmbedTgtArgs a, int r) {
 // ------------------------------------------------------------------ residual + LayerNorm (+AAN)
 // r < a.n (static bound); rows at or beyond the live count are computed but not stored, so
 // every load of the row is issued without waiting for the live-count read.
+// vsm (optional, fused GEMM epilogue): the producing GEMM's output row staged in shared memory,
+// read in place of delta (or of the f-gate logits gf in the gate form).
 template <int NV>
-__device__ __forceinline__ void ln_row(const LnArgs a, int r) {
+__device__ __forceinline__ void ln_row(const LnArgs a, int r, const float* vsm = nullptr) {
   const int lane = threadIdx.x & 31, d = a.d, d4 = d >> 2;
   const int64_t off = (int64_t)r * d;
   const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
@@ -96,14 +98,14 @@ __device__ __forceinline__ void ln_row(const LnArgs a, int r) {
       if (a.gi) {
         // AAN gate (R8): i = sigmoid(gi), f = sigmoid(gf) from the gate GEMMs' logits;
         // z = fl(fl(i*y) + fl(f*a)), residual r = fl(y + z)
-        float4 li = ld4(a.gi + off + 4 * c4), lf = ld4(a.gf + off + 4 * c4);
+        float4 li = ld4(a.gi + off + 4 * c4), lf = vsm ? ld4(vsm + 4 * c4) : ld4(a.gf + off + 4 * c4);
         float4 si = make_float4(sigmoid_f64(li.x), sigmoid_f64(li.y), sigmoid_f64(li.z), sigmoid_f64(li.w));
         float4 sf = make_float4(sigmoid_f64(lf.x), sigmoid_f64(lf.y), sigmoid_f64(lf.z), sigmoid_f64(lf.w));
         float4 iy = mul4(si, x);
         float4 fa = mul4(sf, ld4(a.delta + off + 4 * c4));
         z = add4(iy, fa);
       } else {
-        z = ld4(a.delta + off + 4 * c4);
+        z = vsm ? ld4(vsm + 4 * c4) : ld4(a.delta + off + 4 * c4);
       }
       v[i] = add4(x, z);
       s = __dadd_rn(s, (double)v[i].x);

@@ -112,6 +112,20 @@ def test_tiny_teacher_forced_rowfused(dims):
     assert ex == tot, f"{tot - ex} flagged near-ties"
 
 
+@pytest.mark.parametrize("fuse", [1, 3])
+@pytest.mark.parametrize("dims", [d for d in TINY_VARIANTS if d.d_model in (192, 256)],
+                         ids=lambda d: d.name)
+def test_teacher_forced_fused_layernorm(dims, fuse):
+    """LayerNorm in the producing GEMM's epilogue (fuse_ln 1: every full-row producer incl. the
+    encoder; 3: the decoder's d x d producers): every intermediate within tolerance of the
+    oracle, ids bit-exact."""
+    w, om, gm = pair(dims, 11)
+    gm.set_option("fuse_ln", fuse)
+    ss, forced, foff = forced_case(dims, 9, 0, 13, 0, 17, seed=3)
+    tot, ex, fl = run_forced_parity(dims, w, om, gm, ss, forced, foff)
+    assert ex == tot, f"{tot - ex} flagged near-ties"
+
+
 @pytest.mark.parametrize("dims", TINY_VARIANTS, ids=lambda d: d.name)
 def test_tiny_teacher_forced_persistent_kernel(dims):
     """Teacher forcing through the persistent step kernel (no dumps): per-step ids bit-exact."""
@@ -189,7 +203,8 @@ def test_batch_and_order_invariance():
     base = gm.translate(ss, 1 << 20)
     for budget in (1, 64, 333, 4096):
         assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, budget), base))
-    for fuse in (0, 1, 2):                 # LayerNorm unfused, fused per CTA, fused per cluster
+    for fuse in (0, 1, 2, 3):              # LayerNorm unfused, fused per CTA (all / d x d
+                                           # producers only), fused per cluster
         gm.set_option("fuse_ln", fuse)
         assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, 333), base))
     for lanes in (1, 2, 3):                # concurrent decoder lanes: identical ids
