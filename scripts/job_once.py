@@ -1,6 +1,6 @@
 """One full translation job (after 2 warm-up jobs) inside an NVTX range "job", for an ncu
 launch list of exactly one job:  ncu --nvtx --nvtx-include "job/" ... python scripts/job_once.py
-(env PRESET, MCR, BEAM)"""
+(env PRESET, MCR, BEAM, OPTS = bench launch options)"""
 import os, sys
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -9,6 +9,10 @@ from paper_1805_12096_b200 import mnmt as M
 dims = synth.PRESETS[os.environ.get("PRESET", "small-aan")]
 m = M.Model(dims, synth.make_weights(dims, 1))
 m.set_option("max_concurrent_rows", int(os.environ.get("MCR", 4096)))
+# bench.py's launch options for the workload (env OPTS="lanes=3,lane_tiers=40,...")
+for kv in filter(None, os.environ.get("OPTS", "lanes=3,lane_tiers=40,green_sms=48,pers_reserve=16").split(",")):
+    k, v = kv.split("=")
+    m.set_option(k, int(v))
 ss = synth.newstest_set(seed=2014)
 dev = torch.device("cuda:0"); st = torch.cuda.current_stream()
 ids = torch.from_numpy(ss.ids).to(dev)
