@@ -626,7 +626,7 @@ def main():
     sl_lists = None
     if rank == 0 and not args.no_roofline:
         peaks = load_peaks()
-        mcr = 0 if use_sl else args.max_concurrent_rows   # shortlist: one batch per wave
+        mcr = args.max_concurrent_rows
         sl_lists = oracle_shortlists(sset, dims, budget, sl_freq, sl_lex) if use_sl else None
         n_cols = float(np.mean([len(x) for x in sl_lists[1]])) if use_sl else None
         cands = [roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr,

@@ -9,8 +9,9 @@ from paper_1805_12096_b200 import mnmt as M
 dims = synth.PRESETS[os.environ.get("PRESET", "small-aan")]
 m = M.Model(dims, synth.make_weights(dims, 1))
 m.set_option("max_concurrent_rows", int(os.environ.get("MCR", 4096)))
-# bench.py's launch options for the workload (env OPTS="lanes=3,lane_tiers=40,...")
-for kv in filter(None, os.environ.get("OPTS", "lanes=3,lane_tiers=40,green_sms=48,pers_reserve=16").split(",")):
+# bench.py's launch options for the workload (env OPTS="lanes=3,lane_tiers=40,..."); the default
+# omits green_sms: kernels in a green context are not profiled by ncu
+for kv in filter(None, os.environ.get("OPTS", "lanes=3,lane_tiers=40,pers_reserve=16").split(",")):
     k, v = kv.split("=")
     m.set_option(k, int(v))
 ss = synth.newstest_set(seed=2014)
