@@ -196,11 +196,13 @@ class Model:
 
     @staticmethod
     def _split(out: np.ndarray, out_len: np.ndarray, max_len: np.ndarray) -> List[np.ndarray]:
-        res, o = [], 0
-        for i in range(len(max_len)):
-            res.append(out[o:o + out_len[i]].copy())
-            o += int(max_len[i])
-        return res
+        """Per-sentence id arrays: views into `out` (a fresh buffer of this call)."""
+        n = len(max_len)
+        offs = np.zeros(n + 1, np.int64)
+        np.cumsum(max_len, out=offs[1:])
+        starts = offs[:-1].tolist()
+        ends = (offs[:-1] + out_len[:n]).tolist()
+        return [out[a:b] for a, b in zip(starts, ends)]
 
     def decode(self, sset, stream=None) -> List[np.ndarray]:
         """All sentences of `sset` as one batch, in the given order."""
