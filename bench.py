@@ -635,7 +635,8 @@ def main():
                  roofline_dxd_gemm(dims, sset, budget, peaks, stream, mcr, nb)]
         cands[1]["launches_per_step"] = len(live_rows_profile(sset, budget, mcr)) * dims.dec_layers
         cands[1]["ms_per_step_est"] = cands[1]["ms_per_launch"] * cands[1]["launches_per_step"]
-        for key, c in zip(("out", "attn", "dxd"), cands):
+        keys = ("out", "attn16" if getattr(dims, "kv_bf16", 0) else "attn", "dxd")
+        for key, c in zip(keys, cands):
             c["traffic"], c["traffic_source"] = ncu_traffic(key, c["shape"])
         roof = max(cands, key=lambda c: c["ms_per_step_est"])
         roof["share_of_step_est"] = roof["ms_per_step_est"] / (ms_max / args.steps)

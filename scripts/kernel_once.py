@@ -1,5 +1,5 @@
 """One launch (after warm-up) of a decoder kernel at the bench shape, for ncu.
-usage: KERNEL=dxd|out|topk|attn M=630 python scripts/kernel_once.py"""
+usage: KERNEL=dxd|out|topk|attn|attn16 M=630 python scripts/kernel_once.py"""
 import os, sys
 import numpy as np
 import torch
@@ -29,8 +29,11 @@ else:
     S = int(os.environ.get("S", 21))
     L = np.full(Mr, S, np.int32); st = (np.arange(Mr) * S).astype(np.int32)
     kv = torch.randn(Mr * S, 2 * d, device=dev); q = torch.randn(Mr, d, device=dev)
+    if k == "attn16":   # bf16 source K/V (F3)
+        kv = kv.to(torch.bfloat16)
+    op = M.op_attention_bf16 if k == "attn16" else M.op_attention
     S, Ln = torch.from_numpy(st).to(dev), torch.from_numpy(L).to(dev)
     oq = torch.empty(Mr, d, dtype=torch.int8, device=dev)
     for _ in range(4):
-        M.op_attention(q.data_ptr(), d, kv.data_ptr(), 2 * d, 0, d, S.data_ptr(), Ln.data_ptr(), Mr, d, H, 2.0, oq.data_ptr(), None, None)
+        op(q.data_ptr(), d, kv.data_ptr(), 2 * d, 0, d, S.data_ptr(), Ln.data_ptr(), Mr, d, H, 2.0, oq.data_ptr(), None, None)
 torch.cuda.synchronize()
