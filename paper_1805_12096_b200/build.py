@@ -51,5 +51,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
+EXAMPLE_SRC = os.path.join(HERE, "..", "examples", "mnmt_translate.c")
+EXAMPLE_BIN = os.path.join(HERE, "..", "examples", "mnmt_translate")
+
+
+def build_example() -> str:
+    """The plain C client of the ABI (examples/mnmt_translate.c), linked against libmnmt.so."""
+    if os.path.exists(EXAMPLE_BIN) and os.path.getmtime(EXAMPLE_BIN) >= max(
+            os.path.getmtime(EXAMPLE_SRC), os.path.getmtime(OUT)):
+        return EXAMPLE_BIN
+    subprocess.check_call(["gcc", "-O2", "-Wall", "-std=c11",
+                           "-I", os.path.join(HERE, "..", "include"), EXAMPLE_SRC,
+                           "-L", HERE, "-lmnmt", "-Wl,-rpath,$ORIGIN/../paper_1805_12096_b200",
+                           "-o", EXAMPLE_BIN])
+    return EXAMPLE_BIN
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

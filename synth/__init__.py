@@ -237,3 +237,32 @@ def shortlist_tables(vocab: int = VOCAB, n_freq: int = 100, k_lex: int = 100, se
             r = np.concatenate([r, extra])
         lex[s] = rank[r]
     return rank[:n_freq].copy(), lex
+
+
+# ---------------------------------------------------------------- files for the C client
+# (examples/mnmt_translate.c): plain binary records, little-endian.
+def write_weights_bin(path: str, m: ModelDims, weights: Dict[str, np.ndarray]) -> None:
+    """{int32 name_len, name, int64 numel, float32[numel]} for every parameter of the manifest."""
+    with open(path, "wb") as f:
+        for name in param_shapes(m):
+            a = np.ascontiguousarray(weights[name], np.float32).ravel()
+            b = name.encode()
+            f.write(np.int32(len(b)).tobytes() + b + np.int64(a.size).tobytes() + a.tobytes())
+
+
+def write_sentences_bin(path: str, sset: "SentenceSet") -> None:
+    """{int32 n, int64 offsets[n+1], int32 ids[offsets[n]], int32 max_len[n]}."""
+    with open(path, "wb") as f:
+        f.write(np.int32(sset.n).tobytes() + np.ascontiguousarray(sset.offsets, np.int64).tobytes()
+                + np.ascontiguousarray(sset.ids, np.int32).tobytes()
+                + np.ascontiguousarray(sset.max_len, np.int32).tobytes())
+
+
+def write_shortlist_bin(path: str, freq: np.ndarray, lex: np.ndarray) -> None:
+    """{int32 n_freq, int32 freq[n_freq], int32 k_lex, int32 lex[vocab * k_lex]}."""
+    freq = np.ascontiguousarray(freq, np.int32)
+    lex = np.ascontiguousarray(lex, np.int32)
+    with open(path, "wb") as f:
+        f.write(np.int32(freq.size).tobytes() + freq.tobytes() + np.int32(lex.shape[1]).tobytes()
+                + lex.tobytes())
+
