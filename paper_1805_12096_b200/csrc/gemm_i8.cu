@@ -43,7 +43,8 @@ constexpr int LNC_MAX_CLUSTER = 8;                     // portable cluster size 
 template <int BN>
 struct GemmCfg {
   static constexpr int A_BYTES = BM * BK;
-  static constexpr int B_BYTES = BN * BK;
+  static constexpr int B_ROWS = BN < 64 ? 64 : BN;   // TMA box is 64 rows: BN = 32 loads 64
+  static constexpr int B_BYTES = B_ROWS * BK;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (190 * 1024 / STAGE_BYTES) > 8 ? 8 : (190 * 1024 / STAGE_BYTES);
   static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
@@ -83,24 +84,25 @@ __device__ __forceinline__ void upk2(unsigned long long r, float& a, float& b) {
 // Fast path (K <= 256, whole chunk in range): exact magic-number conversion + packed ops.
 // bsrc: the bias indexed by global column (args.bias, or the CTA's shared-memory copy shifted by
 // its first column) or null.
+template <int CW = 32>
 __device__ __forceinline__ void dequant32(const GemmArgs& args, const float* bsrc, int n, bool fast,
                                           const int32_t (&acc)[32], float (&v)[32]) {
   if (fast) {
     float bias[32];
     if (bsrc) {
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
+      for (int j = 0; j < CW; j += 4) {
         const float4 b4 = *reinterpret_cast<const float4*>(bsrc + n + j);
         bias[j] = b4.x; bias[j + 1] = b4.y; bias[j + 2] = b4.z; bias[j + 3] = b4.w;
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) bias[j] = 0.0f;
+      for (int j = 0; j < CW; ++j) bias[j] = 0.0f;
     }
     const unsigned long long negc = pk2(-12582912.0f, -12582912.0f);
     const unsigned long long s2 = pk2(args.scale, args.scale);
 #pragma unroll
-    for (int j = 0; j < 32; j += 2) {
+    for (int j = 0; j < CW; j += 2) {
       unsigned long long t = pk2(__int_as_float(0x4B400000 + acc[j]), __int_as_float(0x4B400000 + acc[j + 1]));
       asm("add.rn.f32x2 %0, %0, %1;" : "+l"(t) : "l"(negc));
       unsigned long long r;
@@ -110,7 +112,7 @@ __device__ __forceinline__ void dequant32(const GemmArgs& args, const float* bsr
   } else {
     const bool small = args.K <= 256;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
+    for (int j = 0; j < CW; ++j) {
       const float b = (bsrc && n + j < args.N) ? bsrc[n + j] : 0.0f;
       v[j] = __fmaf_rn(acc_to_float(acc[j], small), args.scale, b);
     }
@@ -139,12 +141,14 @@ __device__ __forceinline__ void sl_words(const GemmArgs& args, int row, bool row
 // One 32-column chunk of the 32 rows of this warp (lane = row): dequant + fused op +
 // store, or running argmax.  fp32 outputs go through a padded per-warp smem tile so each
 // store instruction writes four full 128-byte lines.
-template <int EPI>
+template <int EPI, int CW = 32>
 __device__ __forceinline__ void epi_store_chunk(const GemmArgs& args, const float* bsrc, int row,
                                                 bool row_ok, int n, const int32_t (&acc)[32],
                                                 float& best_v, int& best_j, float* stage,
                                                 uint32_t slw = 0xffffffffu) {
-  const bool full = n + 32 <= args.N;
+  static_assert(CW == 32 || (CW == 16 && EPI != EPI_ARGMAX && EPI != EPI_ACC),
+                "16-column chunks: the fp32 / code epilogues only");
+  const bool full = n + CW <= args.N;
   const bool fast = full && args.K <= 256;
   if constexpr (EPI == EPI_ARGMAX) {
     // Branch-free chunk maximum; the lowest column holding it is searched only when the
@@ -186,30 +190,32 @@ __device__ __forceinline__ void epi_store_chunk(const GemmArgs& args, const floa
     }
   } else {
     float v[32];
-    dequant32(args, bsrc, n, fast, acc, v);
+    dequant32<CW>(args, bsrc, n, fast, acc, v);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
+    for (int j = 0; j < CW; ++j) {
       if constexpr (EPI == EPI_RELU_Q || EPI == EPI_RELU_F32_Q) v[j] = relu(v[j]);
       if constexpr (EPI == EPI_SIGMOID) v[j] = sigmoid_f64(v[j]);
     }
     if constexpr (EPI == EPI_F32 || EPI == EPI_F32_Q || EPI == EPI_RELU_F32_Q || EPI == EPI_SIGMOID) {
-      // stage [32 rows][32 cols] then write rows cooperatively (8 lanes x float4 per row)
+      // stage [32 rows][CW cols] then write rows cooperatively (CW / 4 lanes x float4 per row)
       const int lane = threadIdx.x & 31;
       if (threadIdx.x == 64) GEMM_TRACE(7);   // warp 2 lane 0: dequant done
       const unsigned okm = __ballot_sync(0xffffffffu, row_ok);   // live rows of this warp
 #pragma unroll
-      for (int j = 0; j < 32; j += 4)
+      for (int j = 0; j < CW; j += 4)
         *reinterpret_cast<float4*>(stage + lane * EPI_STAGE_LD + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
       __syncwarp();
       if (threadIdx.x == 64) GEMM_TRACE(8);   // staged
       const int row0 = row - lane;
-      const int blk = n / args.col_block;   // 32-column chunks never straddle a block (16 | col_block)
+      const int blk = n / args.col_block;   // chunks never straddle a block (16 | col_block)
       float* base = args.out_f + (int64_t)blk * args.block_stride + (n - blk * args.col_block);
-      const int sub = lane >> 3, c4 = (lane & 7) * 4;
+      constexpr int LPR = CW / 4, RPI = 32 / LPR;   // lanes per row, rows per store instruction
+      constexpr unsigned GM = (1u << RPI) - 1u;
+      const int sub = lane / LPR, c4 = (lane % LPR) * 4;
 #pragma unroll
-      for (int it = 0; it < 8; ++it) {
-        if (((okm >> (4 * it)) & 0xFu) == 0) continue;   // warp-uniform: no live row in the group
-        const int r = it * 4 + sub;
+      for (int it = 0; it < 32 / RPI; ++it) {
+        if (((okm >> (RPI * it)) & GM) == 0) continue;   // warp-uniform: no live row in the group
+        const int r = it * RPI + sub;
         if (((okm >> r) & 1u) && n + c4 < args.N)
           *reinterpret_cast<float4*>(base + (int64_t)(row0 + r) * args.ldo + c4) =
               *reinterpret_cast<const float4*>(stage + r * EPI_STAGE_LD + c4);
@@ -219,7 +225,7 @@ __device__ __forceinline__ void epi_store_chunk(const GemmArgs& args, const floa
     if constexpr (EPI == EPI_F32_Q || EPI == EPI_RELU_Q || EPI == EPI_RELU_F32_Q) {
       if (row_ok) {
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {          // two 16-column groups (N % 16 == 0)
+        for (int g = 0; g < CW / 16; ++g) {    // 16-column groups (N % 16 == 0)
           const int ng = n + 16 * g;
           if (ng >= args.N) break;
           const float* vg = v + 16 * g;
@@ -447,7 +453,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_arrive_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
       uint8_t* sb = smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES;
 #pragma unroll
-      for (int j = 0; j < BN / 64; ++j)
+      for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
         tma_load_2d(sb + j * 64 * BK, &tmB, &full_bar[s], s * BK, n0 + j * 64);
     }
   }
@@ -497,7 +503,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mbar_wait(&empty_bar[s], ((kb / stages) - 1) & 1);
         mbar_arrive_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
 #pragma unroll
-        for (int j = 0; j < BN / 64; ++j)
+        for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
           tma_load_2d(sb + j * 64 * BK, &tmB, &full_bar[s], kb * BK, n0 + j * 64);
         tma_load_2d(sa, &tmA, &full_bar[s], kb * BK, m0);
         tma_load_2d(sa + 64 * BK, &tmA, &full_bar[s], kb * BK, m0 + 64);
@@ -534,7 +540,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int row = m0 + q * 32 + lane;
     const bool row_ok = row < M_live;
     constexpr int HALF = BN / 2;
-    uint32_t slw[HALF / 32];
+    constexpr int CW = HALF < 32 ? 16 : 32;   // chunk width (BN = 32: 16 columns per warp)
+    uint32_t slw[HALF >= 32 ? HALF / 32 : 1];
     if constexpr (EPI == EPI_ARGMAX) sl_words<HALF>(args, row, row_ok, n0 + half * HALF, slw);
     mbar_wait(&tmem_full_bar, 0);
     tc_fence_after();
@@ -555,16 +562,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                                      half, n0, exp_tab);
     } else
 #pragma unroll 1
-    for (int c = 0; c < HALF; c += 32) {
+    for (int c = 0; c < HALF; c += CW) {
       int32_t acc[32];
       tmem_ld16(t_row + c, *reinterpret_cast<int32_t(*)[16]>(acc));
-      tmem_ld16(t_row + c + 16, *reinterpret_cast<int32_t(*)[16]>(acc + 16));
+      if constexpr (CW == 32) tmem_ld16(t_row + c + 16, *reinterpret_cast<int32_t(*)[16]>(acc + 16));
       tmem_ld_wait();
       if (c == 0 && warp == 2 && lane == 0) GEMM_TRACE(6);
       const int n = n0 + half * HALF + c;
       if (n >= args.N) break;  // warp-uniform
-      epi_store_chunk<EPI>(args, args.bias ? bias_s - n0 : nullptr, row, row_ok, n, acc, best_v,
-                           best_j, stage, EPI == EPI_ARGMAX ? slw[c / 32] : 0u);
+      if constexpr (CW == 32)
+        epi_store_chunk<EPI>(args, args.bias ? bias_s - n0 : nullptr, row, row_ok, n, acc, best_v,
+                             best_j, stage, EPI == EPI_ARGMAX ? slw[c / 32] : 0u);
+      else
+        epi_store_chunk<EPI, 16>(args, args.bias ? bias_s - n0 : nullptr, row, row_ok, n, acc,
+                                 best_v, best_j, stage);
     }
     if constexpr (EPI == EPI_ARGMAX) {
       if (row_ok && best_j >= 0) atomicMax(args.keys + row, argmax_key(best_v, (uint32_t)best_j));
@@ -625,7 +636,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_arrive_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
       uint8_t* sb = smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES;
 #pragma unroll
-      for (int j = 0; j < BN / 64; ++j)
+      for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
         tma_load_2d(sb + j * 64 * BK, &tmB, &full_bar[s], s * BK, n0 + j * 64);
     }
   }
@@ -665,7 +676,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mbar_wait(&empty_bar[s], ((kb / stages) - 1) & 1);
         mbar_arrive_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
 #pragma unroll
-        for (int j = 0; j < BN / 64; ++j)
+        for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
           tma_load_2d(sb + j * 64 * BK, &tmB, &full_bar[s], kb * BK, n0 + j * 64);
         tma_load_2d(sa, &tmA, &full_bar[s], kb * BK, m0);
         tma_load_2d(sa + 64 * BK, &tmA, &full_bar[s], kb * BK, m0 + 64);
@@ -1079,7 +1090,8 @@ static cudaError_t launch_pers_t(const CUtensorMap& tmA, const CUtensorMap& tmB,
 template <int BN, int EPI>
 static cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                             cudaStream_t st) {
-  if (gemm_persistent(a.M, a.N, BN, a.pers_grid)) return launch_pers_t<BN, EPI>(tmA, tmB, a, st);
+  if constexpr (BN >= 64)   // BN = 32 (16-column epilogue chunks) is never persistent
+    if (gemm_persistent(a.M, a.N, BN, a.pers_grid)) return launch_pers_t<BN, EPI>(tmA, tmB, a, st);
   using Cfg = GemmCfg<BN>;
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM);
   const int num_kb = (a.K + BK - 1) / BK;
@@ -1104,6 +1116,18 @@ static cudaError_t set_attr() {
   return cudaFuncSetAttribute(k_gemm_pers<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               PersCfg<BN>::SMEM);
 }
+// BN = 32 (non-persistent, fp32 / code epilogues only): 16 columns per epilogue warp
+static cudaError_t set_attr_bn32() {
+  for (const void* f : {(const void*)k_gemm_i8<32, EPI_F32>, (const void*)k_gemm_i8<32, EPI_F32_Q>,
+                        (const void*)k_gemm_i8<32, EPI_RELU_Q>, (const void*)k_gemm_i8<32, EPI_RELU_F32_Q>,
+                        (const void*)k_gemm_i8<32, EPI_SIGMOID>}) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         GemmCfg<32>::smem_for(GemmCfg<32>::STAGES));
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 template <int BN>
 static cudaError_t set_attr_bn() {
   cudaError_t e;
@@ -1149,6 +1173,7 @@ static cudaError_t gemm_init_all() {
   if ((e = cudaFuncSetAttribute(k_gemm_lnc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 GemmCfg<128>::STAGES * GemmCfg<128>::STAGE_BYTES + 1024)) != cudaSuccess)
     return e;
+  if ((e = set_attr_bn32()) != cudaSuccess) return e;
   if ((e = set_attr_bn<64>()) != cudaSuccess) return e;
   if ((e = set_attr_bn<128>()) != cudaSuccess) return e;
   if ((e = set_attr_ln()) != cudaSuccess) return e;
@@ -1248,7 +1273,28 @@ cudaError_t launch_gemm_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const
     return cudaErrorInvalidValue;
   }
   if (bn == 0) bn = gemm_pick_bn(a.M, a.N, a.pers_grid);
+  // 32-wide tiles halve each epilogue warp's columns where the 64-wide grid is small
+  // (env MNMT_BN32=0 disables; A/B)
+  static const bool bn32 = [] {
+    const char* e = getenv("MNMT_BN32");
+    return !(e && e[0] == '0');
+  }();
+  if (bn32 && bn == 64 && (epi == EPI_F32 || epi == EPI_F32_Q || epi == EPI_RELU_Q ||
+                           epi == EPI_RELU_F32_Q || epi == EPI_SIGMOID)) {
+    const int tiles64 = ((a.N + 63) / 64) * ((a.M + BM - 1) / BM);
+    const int sms = a.pers_grid > 0 ? a.pers_grid : num_sms();   // the launch's SM budget
+    if (tiles64 * 2 <= sms && a.N % 32 == 0) bn = 32;
+  }
   switch (bn) {
+    case 32:
+      switch (epi) {
+        case EPI_F32: return launch_t<32, EPI_F32>(tmA, tmB, a, st);
+        case EPI_F32_Q: return launch_t<32, EPI_F32_Q>(tmA, tmB, a, st);
+        case EPI_RELU_Q: return launch_t<32, EPI_RELU_Q>(tmA, tmB, a, st);
+        case EPI_RELU_F32_Q: return launch_t<32, EPI_RELU_F32_Q>(tmA, tmB, a, st);
+        case EPI_SIGMOID: return launch_t<32, EPI_SIGMOID>(tmA, tmB, a, st);
+      }
+      return cudaErrorInvalidValue;
     case 64: return launch_bn<64>(tmA, tmB, a, epi, st);
     case 128: return launch_bn<128>(tmA, tmB, a, epi, st);
     case 256: return launch_bn<256>(tmA, tmB, a, epi, st);

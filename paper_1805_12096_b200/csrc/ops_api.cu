@@ -1,6 +1,7 @@
 // ops_api.cu — op-level C ABI (include/mnmt_ops.h): each decode-path kernel on caller memory.
 #include <cstdio>
 #include <string>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/mnmt_ops.h"
@@ -224,12 +225,14 @@ extern "C" mnmt_status mnmt_debug_gemm_chain(const int8_t* A, const int8_t* W, i
   cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
   cudaGraph_t g;
   cudaGraphExec_t ge;
+  const char* ebn = getenv("MNMT_CHAIN_BN");   // N tile override (64 / 128 / 256), A/B only
+  const int bn = ebn ? atoi(ebn) : 0;
   cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
   for (int i = 0; i < n; ++i) {
     GemmArgs a{};
     a.M = M; a.N = N; a.K = K; a.scale = 1.0f / 4032.25f; a.clip = 2.0f; a.sigma = 63.5f;
     a.out_f = out; a.ldo = N; a.col_block = N; a.trace = tr + (size_t)i * 9;
-    launch_gemm_i8(ta, tb, a, EPI_F32, 0, st);
+    launch_gemm_i8(ta, tb, a, EPI_F32, bn, st);
   }
   e = cudaStreamEndCapture(st, &g);
   if (e == cudaSuccess) e = cudaGraphInstantiate(&ge, g, 0);

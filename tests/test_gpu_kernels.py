@@ -64,6 +64,7 @@ def test_gemm_acc_bitexact(Mr, N, K, bn):
 
 @pytest.mark.parametrize("epi", [M.EPI_F32, M.EPI_F32_Q, M.EPI_RELU_Q, M.EPI_RELU_F32_Q, M.EPI_SIGMOID])
 @pytest.mark.parametrize("Mr,N,K", [(5, 256, 256), (260, 2048, 512), (131, 512, 2048),
+                                    (70, 160, 256), (1, 32, 64),   # 32-wide tiles, ragged N
                                     (4700, 2048, 256)])   # last: persistent kernel
 def test_gemm_epilogues_bitexact(epi, Mr, N, K):
     rng = np.random.default_rng(epi * 100 + Mr)
