@@ -1283,7 +1283,9 @@ cudaError_t launch_gemm_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const
                            epi == EPI_RELU_F32_Q || epi == EPI_SIGMOID)) {
     const int tiles64 = ((a.N + 63) / 64) * ((a.M + BM - 1) / BM);
     const int sms = a.pers_grid > 0 ? a.pers_grid : num_sms();   // the launch's SM budget
-    if (tiles64 * 2 <= sms && a.N % 32 == 0) bn = 32;
+    // K <= 512 only: the 32-wide tile still receives a 64-row B box, which costs more than
+    // it saves for deep K (measured: big student 126 -> 131 ms per job without this bound)
+    if (tiles64 * 2 <= sms && a.N % 32 == 0 && a.K <= 512) bn = 32;
   }
   switch (bn) {
     case 32:
