@@ -354,7 +354,10 @@ def roofline_dxd_gemm(dims, sset, budget, peaks, stream, mcr, mult=1):
     peak = 2.0 * peaks["bf16_tflops"]
     ach = ops / (ms * 1e-3) / 1e12
     per_step = 6 * dims.dec_layers if dims.decoder == 1 else 5 * dims.dec_layers
-    return {"kernel": "k_gemm_i8<64, EPI_F32> (decoder d x d projections)", "bound": "tensor",
+    # the library's tile choice (gemm_i8.cu launch_gemm_i8): 32-wide tiles when the 64-wide grid
+    # fills less than half of the SMs and K <= 512, else 64 (N = d, small row counts)
+    bn = 32 if (((d + 63) // 64) * ((Mr + 127) // 128) * 2 <= 148 and d <= 512) else 64
+    return {"kernel": f"k_gemm_i8<{bn}, EPI_F32> (decoder d x d projections)", "bound": "tensor",
             "achieved": ach, "peak": peak, "unit": "TOP/s (int8)", "frac": ach / peak,
             "traffic": None, "shape": f"M={Mr} (mean live rows/step) N={d} K={d}",
             "ms_per_launch": ms, "launches_per_step": len(rows) * per_step,
