@@ -466,6 +466,9 @@ def main():
                     help="SMs the persistent GEMMs of non-critical lanes leave free")
     ap.add_argument("--steps-per-graph", type=int, default=1,
                     help="decoder steps captured per CUDA graph (scheduling only)")
+    ap.add_argument("--fin-embed", type=int, default=0,
+                    help="row bound up to which k_finish also embeds the next step's rows "
+                         "(one launch per step less; 0 = separate k_embed_tgt always)")
     ap.add_argument("--fuse-ln", type=int, default=0,
                     help="LayerNorm in the producing GEMM's epilogue: 0 separate kernels, "
                          "1 one CTA per row block (d <= 256), 2 a CTA cluster per row block")
@@ -500,6 +503,7 @@ def main():
                     "l2": "flushed between timed steps (512 MiB write)",
                     "max_concurrent_rows": args.max_concurrent_rows, "lanes": args.lanes,
                     "fuse_ln": args.fuse_ln, "steps_per_graph": args.steps_per_graph,
+                    "fin_embed": args.fin_embed,
                     "lane_tiers": args.lane_tiers, "pers_reserve": args.pers_reserve,
                     "green_sms": args.green_sms, "rowfuse": args.rowfuse,
                     "step_engine": "persistent cooperative kernel" if args.megakernel else "kernel-per-op CUDA graph"}
@@ -527,6 +531,7 @@ def main():
     model.set_option("megakernel", args.megakernel)
     model.set_option("fuse_ln", args.fuse_ln)
     model.set_option("steps_per_graph", args.steps_per_graph)
+    model.set_option("fin_embed", args.fin_embed)
     model.set_option("lane_tiers", args.lane_tiers)
     model.set_option("pers_reserve", args.pers_reserve)
     model.set_option("green_sms", args.green_sms)

@@ -153,7 +153,7 @@ struct Lane {
   cudaStream_t side = nullptr;                 // fork stream for independent GEMMs (graph branch)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::map<int64_t, cudaGraphExec_t> graphs;   // key: padded live-row bound
-  int64_t launches_per_step = 0;
+  std::map<int64_t, int64_t> graph_launches;   // kernels per launch of graphs[key]
   int span_cap = 0;                            // attention span the step kernels are sized for
   int kind = -1;                               // streams from: 0 runtime, 1 critical / 2 bulk green context
   // persistent step kernel program (built for this lane's workspace)
@@ -197,6 +197,7 @@ struct mnmt_model {
   int fuse_ln = 0;                     // option: LayerNorm fused into full-row GEMM epilogues
   int rowlocal = 0;                    // option: row-local phases in the persistent step kernel (measured slower)
   int steps_per_graph = 1;             // option: decoder steps captured per CUDA graph
+  int fin_embed = 0;                   // option: row bound up to which k_finish embeds the next step (measured slower)
   int mk_ctas = 0;                     // option: persistent step kernel grid cap (0 = one per SM)
   int mk_cluster = 0;                  // option: persistent step kernel grid = one cluster (mk_ctas <= 16)
   int green_sms = 0;                   // option: SMs of the critical lane's green context (0 = off)
@@ -943,8 +944,10 @@ static bool rowfuse_active(const mnmt_model* m, int n) {
 }
 
 // One decoder step for up to `n` live rows (A5-A10).  Returns kernels launched via *nlaunch.
+// embed: launch A5 (k_embed_tgt) at the start (false: the previous step's k_finish did it);
+// fin_embed: k_finish embeds the next step's rows in the same CTA (greedy only).
 static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, StepHook* hook,
-                               int64_t* nlaunch) {
+                               int64_t* nlaunch, bool embed = true, bool fin_embed = false) {
   auto& w = Ln.ws;
   cudaStream_t st = Ln.st;
   const auto& c = m->c;
@@ -964,8 +967,10 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
   ea.y = w.y;
   ea.yq = w.cy;
   ea.aan = aan_for_layer(m, w, 0);
-  if ((e = launch_embed_tgt(ea, n, st)) != cudaSuccess) return e;
-  ++k;
+  if (embed) {
+    if ((e = launch_embed_tgt(ea, n, st)) != cudaSuccess) return e;
+    ++k;
+  }
   for (int l = 0; l < L; ++l) {
     const DecLayer& D = m->dec[l];
     // small live-row counts: the AAN block (A6) and the source-attention block (A7) as fused
@@ -1240,6 +1245,10 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
   fa.live_start = w.live_start;
   fa.live_len = w.live_len;
   fa.id_map = Ln.sl_n > 0 ? w.sl_map : nullptr;
+  if (fin_embed) {
+    fa.emb = ea;
+    fa.emb.n = n;
+  }
   if ((e = launch_finish(fa, st)) != cudaSuccess) return e;
   k += 2;
   *nlaunch += k;
@@ -1764,20 +1773,26 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
     } else if (use_graphs && !hook) {
       // k consecutive steps per graph (PDL chains the kernels inside a graph, not across
       // graph launches), sized for the first step's row bound (rows only decrease)
+      // fin_embed: at row bounds <= m->fin_embed the step's k_finish also embeds the next
+      // step's rows (rows only decrease, so every later graph of the batch does too), and a
+      // graph whose predecessor did so starts without k_embed_tgt
       const int K = std::max(1, m->steps_per_graph);
+      bool prev_fused = false;
       for (int t = 0; t < b.T;) {
         const int np = pad_at(t), k = std::min(K, b.T - t);
-        const int64_t key = (((int64_t)np * 64 + k) * 16 + m->beam) * ((int64_t)c.vocab + 1) + Ln.sl_n;
+        const bool fuse = m->beam == 0 && np <= m->fin_embed;
+        const bool first_embed = !prev_fused;
+        const int64_t key =
+            ((((int64_t)np * 64 + k) * 16 + m->beam) * ((int64_t)c.vocab + 1) + Ln.sl_n) * 4 +
+            (fuse ? 2 : 0) + (first_embed ? 1 : 0);
         auto it = Ln.graphs.find(key);
         if (it == Ln.graphs.end()) {
           cudaGraph_t g;
           CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
           int64_t per_step = 0;
           cudaError_t e = cudaSuccess;
-          for (int u = 0; u < k && e == cudaSuccess; ++u) {
-            per_step = 0;
-            e = launch_step(m, Ln, np, forced, nullptr, &per_step);
-          }
+          for (int u = 0; u < k && e == cudaSuccess; ++u)
+            e = launch_step(m, Ln, np, forced, nullptr, &per_step, u == 0 ? first_embed : !fuse, fuse);
           cudaError_t e2 = cudaStreamEndCapture(st, &g);
           CK(e);
           CK(e2);
@@ -1790,10 +1805,11 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
             Ln.graphs.clear();
           }
           it = Ln.graphs.emplace(key, ge).first;
-          Ln.launches_per_step = per_step;
+          Ln.graph_launches[key] = per_step;
         }
         CK(cudaGraphLaunch(it->second, st));
-        launches += (int64_t)k * Ln.launches_per_step;
+        launches += Ln.graph_launches[key];
+        prev_fused = fuse;
         t += k;
       }
     } else {
@@ -2501,6 +2517,11 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
   if (std::string(name) == "lane_tiers") {
     if (value < 0 || value > 100) { set_err("lane_tiers must be in [0, 100]"); return MNMT_ERR_ARG; }
     m->lane_tiers = (int)value;
+    return MNMT_OK;
+  }
+  if (std::string(name) == "fin_embed") {
+    if (value < 0 || value > (1 << 20)) { set_err("fin_embed must be in [0, 2^20]"); return MNMT_ERR_ARG; }
+    m->fin_embed = (int)value;   // graph keys carry the variant, so cached graphs stay valid
     return MNMT_OK;
   }
   if (std::string(name) == "steps_per_graph") {

@@ -244,12 +244,21 @@ inline size_t attn_split_smem(int ns, int span) {
 
 constexpr int FIN_THREADS = 1024;
 
+// NV > 0: the next step's embedding (A5) follows the compaction in the same CTA, warp per
+// row, reading the ctrl / live / prev_live values this block has just written (visible
+// after finish_block's closing barrier).  Saves one dependent launch per step at small row
+// counts, where the embedding is a few rows per warp.
+template <int NV>
 __global__ void __launch_bounds__(FIN_THREADS) k_finish(FinishArgs a) {
   __shared__ int32_t warp_cnt[32];
   __shared__ int32_t base_s;
   pdl_wait();
   pdl_trigger_early();
   finish_block(a, warp_cnt, base_s);
+  if constexpr (NV > 0) {
+    const int nw = blockDim.x >> 5;
+    for (int r = threadIdx.x >> 5; r < a.emb.n; r += nw) embed_tgt_row<NV>(a.emb, r);
+  }
 }
 
 // Encoder self-attention: one CTA per (sentence, head).  The sentence's K and V head
@@ -489,7 +498,9 @@ static cudaError_t set_carveouts() {
                        (const void*)k_embed_tgt<1>, (const void*)k_embed_tgt<2>,
                        (const void*)k_embed_tgt<4>, (const void*)k_embed_tgt<8>,
                        (const void*)k_ln<1>, (const void*)k_ln<2>, (const void*)k_ln<4>, (const void*)k_ln<8>,
-                       (const void*)k_attn, (const void*)k_attn_enc, (const void*)k_finish,
+                       (const void*)k_attn, (const void*)k_attn_enc, (const void*)k_finish<0>,
+                       (const void*)k_finish<1>, (const void*)k_finish<2>,
+                       (const void*)k_finish<4>, (const void*)k_finish<8>,
                        (const void*)k_decode_init};
   for (const void* f : fns) {
     cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -594,7 +605,14 @@ cudaError_t launch_attn_enc(const EncAttnArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t st) {
-  return launch_pdl(k_finish, dim3(1), dim3(FIN_THREADS), 0, st, a);
+  if (a.emb.n <= 0) return launch_pdl(k_finish<0>, dim3(1), dim3(FIN_THREADS), 0, st, a);
+  switch (nv_for(a.emb.d)) {
+    case 1: return launch_pdl(k_finish<1>, dim3(1), dim3(FIN_THREADS), 0, st, a);
+    case 2: return launch_pdl(k_finish<2>, dim3(1), dim3(FIN_THREADS), 0, st, a);
+    case 4: return launch_pdl(k_finish<4>, dim3(1), dim3(FIN_THREADS), 0, st, a);
+    case 8: return launch_pdl(k_finish<8>, dim3(1), dim3(FIN_THREADS), 0, st, a);
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_decode_init(int32_t* ctrl, int32_t* live, int B, unsigned long long* keys,

@@ -112,6 +112,9 @@ struct FinishArgs {
   int32_t* live_start;
   int32_t* live_len;
   const int32_t* id_map;    // shortlist (F2): GEMM column -> vocabulary id, or null
+  // optional: the next step's target embedding (A5) in the same CTA after the compaction
+  // (emb.n > 0: rows [0, emb.n) warp per row; the step graph then omits k_embed_tgt)
+  EmbedTgtArgs emb;
 };
 
 cudaError_t launch_quantize(const float* x, int64_t n, float clip, int8_t* out, cudaStream_t st);

@@ -159,6 +159,31 @@ def test_tiny_free_running(dims):
         assert all(np.array_equal(a, b) for a, b in zip(got, ref)), (mk, rl, ctas, cl, rf)
 
 
+@pytest.mark.parametrize("dims", TINY_VARIANTS, ids=lambda d: d.name)
+def test_finish_embeds_next_step(dims):
+    """Option fin_embed (A5 inside k_finish after the compaction, the step graph then starts
+    without k_embed_tgt): off, at every row bound and at the default bound, with one and several
+    steps per graph, free-running and teacher-forced ids bit-exact vs the oracle."""
+    w, om, gm = pair(dims, 14)
+    ss = synth.random_set(150, 1, 19, seed=6, vocab=dims.vocab)   # 256-row pad, then 128
+    ref = om.decode_many(ss, 4)
+    fs, forced, foff = forced_case(dims, 11, 0, 13, 0, 17, seed=5)
+    for fe in (0, 128, 1 << 20):
+        gm.set_option("fin_embed", fe)
+        for k in (1, 3):
+            gm.set_option("steps_per_graph", k)
+            got = gm.decode(ss)
+            assert all(np.array_equal(a, b) for a, b in zip(got, ref)), (fe, k)
+            ids, _ = gm.decode_forced(fs, forced, foff, 0)
+            for i in range(fs.n):
+                T = int(foff[i + 1] - foff[i])
+                oids = om.decode_one(fs.ids[fs.offsets[i]:fs.offsets[i + 1]], T,
+                                     forced=forced[foff[i]:foff[i + 1]])
+                assert np.array_equal(ids[foff[i]:foff[i + 1]], oids), (fe, k, i)
+    gm.set_option("steps_per_graph", 1)
+    gm.set_option("fin_embed", 0)
+
+
 def test_config0_tiny192_aan():
     """BASELINE configs[0]: tiny-192 AAN, 36k vocab, 4 sentences of length 20."""
     dims = synth.PRESETS["tiny192-aan"]
