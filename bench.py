@@ -45,12 +45,15 @@ DEFAULT_WORKLOAD = "small-aan-newstest-8192w"
 # green_sms x lane_tiers sweep on one B200 (profiles/r1_sweep_green_tiers.txt): the critical
 # lane's SM partition pays off for the smaller students and costs the big one (its bulk lanes
 # need every SM).
+# smallm / smallm_kmax: the small-M (IDP4A, <= 32 live rows) GEMM path's row bound and deepest K
+# per workload, from the A/B in profiles/r1_ab_smallm.txt (small-aan: +2 % with FFN2's K = 2048
+# included; the others neutral or slower, so off).
 WORKLOAD_OPTS = {
-    "small-aan-newstest-8192w": {"green_sms": 48, "lane_tiers": 40},
-    "tiny192-aan-newstest-8192w": {"green_sms": 56, "lane_tiers": 40},
-    "base-newstest-8192w": {"green_sms": 24, "lane_tiers": 40},
-    "base-aan-newstest-8192w": {"green_sms": 40, "lane_tiers": 35},
-    "big-newstest-8192w": {"green_sms": 0, "lane_tiers": 25},
+    "small-aan-newstest-8192w": {"green_sms": 48, "lane_tiers": 40, "smallm": 32, "smallm_kmax": 2048},
+    "tiny192-aan-newstest-8192w": {"green_sms": 56, "lane_tiers": 40, "smallm": 0, "smallm_kmax": 512},
+    "base-newstest-8192w": {"green_sms": 24, "lane_tiers": 40, "smallm": 0, "smallm_kmax": 512},
+    "base-aan-newstest-8192w": {"green_sms": 40, "lane_tiers": 35, "smallm": 32, "smallm_kmax": 512},
+    "big-newstest-8192w": {"green_sms": 0, "lane_tiers": 25, "smallm": 0, "smallm_kmax": 512},
 }
 L2_FLUSH_BYTES = 512 << 20   # > 126 MB L2
 
@@ -466,6 +469,11 @@ def main():
                     help="SMs the persistent GEMMs of non-critical lanes leave free")
     ap.add_argument("--steps-per-graph", type=int, default=1,
                     help="decoder steps captured per CUDA graph (scheduling only)")
+    ap.add_argument("--smallm", type=int, default=None,
+                    help="row bound of the small-M IDP4A GEMM path (0 = tcgen05 always; "
+                         "default per workload)")
+    ap.add_argument("--smallm-kmax", type=int, default=None,
+                    help="deepest K of the small-M path (default per workload)")
     ap.add_argument("--fin-embed", type=int, default=0,
                     help="row bound up to which k_finish also embeds the next step's rows "
                          "(one launch per step less; 0 = separate k_embed_tgt always)")
@@ -503,7 +511,8 @@ def main():
                     "l2": "flushed between timed steps (512 MiB write)",
                     "max_concurrent_rows": args.max_concurrent_rows, "lanes": args.lanes,
                     "fuse_ln": args.fuse_ln, "steps_per_graph": args.steps_per_graph,
-                    "fin_embed": args.fin_embed,
+                    "fin_embed": args.fin_embed, "smallm": args.smallm,
+                    "smallm_kmax": args.smallm_kmax,
                     "lane_tiers": args.lane_tiers, "pers_reserve": args.pers_reserve,
                     "green_sms": args.green_sms, "rowfuse": args.rowfuse,
                     "step_engine": "persistent cooperative kernel" if args.megakernel else "kernel-per-op CUDA graph"}
@@ -532,6 +541,8 @@ def main():
     model.set_option("fuse_ln", args.fuse_ln)
     model.set_option("steps_per_graph", args.steps_per_graph)
     model.set_option("fin_embed", args.fin_embed)
+    model.set_option("smallm", 32 if args.smallm is None else args.smallm)
+    model.set_option("smallm_kmax", 512 if args.smallm_kmax is None else args.smallm_kmax)
     model.set_option("lane_tiers", args.lane_tiers)
     model.set_option("pers_reserve", args.pers_reserve)
     model.set_option("green_sms", args.green_sms)

@@ -210,6 +210,15 @@ mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids_host,
  *                          128-row tile (CTA barriers between them), 0 (default) = split over the
  *                          grid with grid barriers.
  *   "steps_per_graph"      1..63 consecutive decoder steps captured in one CUDA graph (default 1).
+ *   "smallm"               0..32 row bound (default 32): greedy decoder steps with at most this many
+ *                          live rows run their fp32 / code-output GEMMs with K <= "smallm_kmax" as
+ *                          IDP4A CUDA-core kernels (same s32 accumulators, same epilogue arithmetic,
+ *                          bit-identical outputs); 0: tcgen05 always.  Process-wide (env
+ *                          MNMT_SMALLM sets the initial value).
+ *   "smallm_kmax"          deepest K the small-M path takes (default 512, process-wide).
+ *   "fin_embed"            row bound up to which the step's finish kernel also embeds the next
+ *                          step's rows (A5), removing k_embed_tgt from the step graph; 0 (default,
+ *                          measured faster) = separate embedding kernel.
  *   "lane_tiers"           0 (default): a wave's sentences are dealt round-robin to the lanes;
  *                          10*p: contiguous length tiers of equal sum S_i^p, the last lane (the
  *                          longest sentences, the job's critical path) on the highest-priority stream.

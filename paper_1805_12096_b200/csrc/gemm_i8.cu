@@ -1251,9 +1251,168 @@ int gemm_lnc_bn(int d) {
   return 0;
 }
 
+// ------------------------------------------------------------------ small-M path
+// At <= 32 live rows a decoder GEMM is latency-bound: the tcgen05 kernel's A-tile TMA round
+// trip, MMA commit and TMEM load sit on the critical path of every launch (DESIGN 12.3).
+// k_gemm_smallm computes the same s32 accumulators with IDP4A on CUDA cores: lane = row,
+// warp = (column, K segment), CN = 8 / S columns per CTA, S K segments per column combined
+// in shared memory.  Integer sums are exact in any order, and the epilogue is the tcgen05
+// kernel's arithmetic element by element (v = fmaf(float(acc), s, b), then ReLU / sigmoid /
+// Q), so outputs are bit-identical.  The weight row segment (constant) is loaded before the
+// PDL wait; A rows are read straight from L2 after it.
+template <int EPI, int S, int CPW>
+__global__ void __launch_bounds__(256) k_gemm_smallm(const GemmArgs args) {
+  constexpr int CN = 8 / S, CT = CN * CPW;   // column groups / columns per CTA
+  extern __shared__ __align__(16) int8_t wsm[];   // [CT][K] the CTA's weight rows
+  __shared__ int32_t red[8][CPW][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cw = warp % CN, seg = warp / CN;
+  const int nbase = blockIdx.x * CT;
+  const int K = args.K, KS = K / S, k0 = seg * KS, k16 = K >> 4;
+  // constant operands before the PDL wait: weight rows staged in shared memory, bias
+  const int ncols = min(CT, args.N - nbase);
+  for (int i = threadIdx.x; i < ncols * k16; i += 256) {
+    const int c = i / k16, kk = i - c * k16;
+    *reinterpret_cast<uint4*>(wsm + c * K + 16 * kk) =
+        __ldg(reinterpret_cast<const uint4*>(args.b_ptr + (int64_t)(nbase + c) * K + 16 * kk));
+  }
+  float b[CPW];
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) {
+    const int n = nbase + cw * CPW + c;
+    b[c] = (args.bias && seg == 0 && n < args.N) ? __ldg(args.bias + n) : 0.0f;
+  }
+  pdl_wait();
+  __syncthreads();   // weights staged
+  const int n_live = args.M_dyn ? min(args.M, *args.M_dyn) : args.M;
+  const bool row_ok = lane < n_live;
+  int32_t acc[CPW];
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) acc[c] = 0;
+  if (row_ok) {
+    const int8_t* arow = args.a_ptr + (int64_t)lane * args.lda + k0;
+    const int8_t* wb = wsm + (cw * CPW) * K + k0;
+    for (int k = 0; k < KS; k += 64) {
+      uint4 av[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k + 16 * u < KS) av[u] = *reinterpret_cast<const uint4*>(arow + k + 16 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (k + 16 * u < KS) {
+#pragma unroll
+          for (int c = 0; c < CPW; ++c) {   // broadcast reads: every lane the same address
+            const uint4 wv = *reinterpret_cast<const uint4*>(wb + c * K + k + 16 * u);
+            acc[c] = __dp4a((int)av[u].x, (int)wv.x, acc[c]);
+            acc[c] = __dp4a((int)av[u].y, (int)wv.y, acc[c]);
+            acc[c] = __dp4a((int)av[u].z, (int)wv.z, acc[c]);
+            acc[c] = __dp4a((int)av[u].w, (int)wv.w, acc[c]);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) red[warp][c][lane] = acc[c];
+  __syncthreads();
+  if (threadIdx.x == 0) pdl_launch_dependents();
+  if (seg != 0 || !row_ok) return;   // no block-wide barrier below
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) {
+    const int n = nbase + cw * CPW + c;
+    if (n >= args.N) break;
+    int32_t a = 0;
+#pragma unroll
+    for (int g = 0; g < S; ++g) a += red[g * CN + cw][c][lane];
+    float v = __fmaf_rn(acc_to_float(a, K <= 256), args.scale, b[c]);
+    if constexpr (EPI == EPI_RELU_Q || EPI == EPI_RELU_F32_Q) v = relu(v);
+    if constexpr (EPI == EPI_SIGMOID) v = sigmoid_f64(v);
+    if constexpr (EPI == EPI_F32 || EPI == EPI_F32_Q || EPI == EPI_RELU_F32_Q || EPI == EPI_SIGMOID) {
+      const int blk = n / args.col_block;
+      args.out_f[(int64_t)blk * args.block_stride + (int64_t)lane * args.ldo + (n - blk * args.col_block)] = v;
+    }
+    if constexpr (EPI == EPI_F32_Q || EPI == EPI_RELU_Q || EPI == EPI_RELU_F32_Q)
+      args.out_q[(int64_t)lane * args.ldo + n] = (int8_t)q8(v, args.clip, args.sigma);
+  }
+}
+
+static int g_smallm = [] {   // row bound of the small-M path (0 = off)
+  const char* e = getenv("MNMT_SMALLM");
+  const int v = e ? atoi(e) : 16;
+  return v < 0 ? 0 : v > SMALLM_MAX ? SMALLM_MAX : v;
+}();
+void gemm_set_smallm(int rows) { g_smallm = rows < 0 ? 0 : rows > SMALLM_MAX ? SMALLM_MAX : rows; }
+// deepest K the small-M path takes: at K >= 1024 (the big student) every CTA's A reads and
+// weight staging outweigh the tcgen05 kernel's latency (measured: big 123.4 -> 126-129 ms)
+static int g_smallm_kmax = 512;
+void gemm_set_smallm_kmax(int k) { g_smallm_kmax = k; }
+int gemm_smallm() { return g_smallm; }
+
+template <int EPI, int CPW>
+static cudaError_t launch_smallm_c(const GemmArgs& a, int S, cudaStream_t st) {
+  const int CT = (8 / S) * CPW;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((a.N + CT - 1) / CT);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = (size_t)CT * a.K;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  switch (S) {
+    case 1: return cudaLaunchKernelEx(&cfg, k_gemm_smallm<EPI, 1, CPW>, a);
+    case 2: return cudaLaunchKernelEx(&cfg, k_gemm_smallm<EPI, 2, CPW>, a);
+    case 4: return cudaLaunchKernelEx(&cfg, k_gemm_smallm<EPI, 4, CPW>, a);
+    case 8: return cudaLaunchKernelEx(&cfg, k_gemm_smallm<EPI, 8, CPW>, a);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// CPW columns per warp: 4, or 8 where the 4-column grid would exceed 64 CTAs (wide N) or K is
+// deep (every CTA reads all live rows of A, so fewer, wider CTAs cut the redundant A traffic)
+// The grid must fit the launch's SM budget in one wave (3 resident CTAs per SM): in a small
+// SM partition a multi-wave small-M grid is slower than the tcgen05 kernel (measured: base
+// self-attention student, 24-SM critical lane, 66.4 -> 71.5 ms per job without this bound).
+template <int EPI>
+static cudaError_t launch_smallm_e(const GemmArgs& a, int S, cudaStream_t st) {
+  const int cn = 8 / S;
+  const int ctas4 = (a.N + cn * 4 - 1) / (cn * 4), ctas8 = (a.N + cn * 8 - 1) / (cn * 8);
+  const int cap = 3 * (a.pers_grid > 0 ? a.pers_grid : num_sms());
+  const bool fit8 = (size_t)cn * 8 * a.K <= 48 * 1024, fit4 = (size_t)cn * 4 * a.K <= 48 * 1024;
+  if (fit8 && (ctas4 > 64 || a.K >= 1024 || (ctas4 > cap && ctas8 <= cap)))
+    return ctas8 <= cap ? launch_smallm_c<EPI, 8>(a, S, st) : cudaErrorNotSupported;
+  if (!fit4 || ctas4 > cap) return cudaErrorNotSupported;
+  return launch_smallm_c<EPI, 4>(a, S, st);
+}
+
+// Returns cudaErrorNotSupported when the launch does not qualify (the caller takes the
+// tcgen05 path).
+static cudaError_t launch_smallm(const GemmArgs& a, int epi, cudaStream_t st) {
+  if (!g_smallm || !a.a_ptr || !a.b_ptr || a.M > g_smallm || a.M > SMALLM_MAX || a.K > g_smallm_kmax)
+    return cudaErrorNotSupported;
+  if (a.K % 16 || a.lda % 16 || ((uintptr_t)a.a_ptr & 15) || ((uintptr_t)a.b_ptr & 15))
+    return cudaErrorNotSupported;
+  int S = 8;   // K segments per column: the largest power of two <= 8 leaving >= 64 bytes
+  while (S > 1 && ((a.K % S) || (a.K / S) % 16 || a.K / S < 64)) S >>= 1;
+  switch (epi) {
+    case EPI_F32: return launch_smallm_e<EPI_F32>(a, S, st);
+    case EPI_F32_Q: return launch_smallm_e<EPI_F32_Q>(a, S, st);
+    case EPI_RELU_Q: return launch_smallm_e<EPI_RELU_Q>(a, S, st);
+    case EPI_RELU_F32_Q: return launch_smallm_e<EPI_RELU_F32_Q>(a, S, st);
+    case EPI_SIGMOID: return launch_smallm_e<EPI_SIGMOID>(a, S, st);
+  }
+  return cudaErrorNotSupported;
+}
+
 cudaError_t launch_gemm_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                            int epi, int bn, cudaStream_t st) {
   if (a.M <= 0 || a.N <= 0) return cudaSuccess;
+  {
+    const cudaError_t e = launch_smallm(a, epi, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (epi == EPI_LNC) {   // the N tiles of an M tile form a cluster that owns whole rows
     switch (gemm_lnc_bn(a.N)) {
       case 64: return launch_lnc<64>(tmA, tmB, a, st);

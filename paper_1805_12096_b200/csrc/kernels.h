@@ -64,7 +64,20 @@ struct GemmArgs {
   LnArgs ln;                   // EPI_LN: residual / gate inputs, gamma, beta, outputs, AAN
   TopkPart* part;              // EPI_TOPK: [rows][part_ld] partials (part_ld >= 2 * N tiles)
   int part_ld;
+  // optional raw operands (row-major codes, K contiguous) for the small-M path: with
+  // M <= the small-M row bound (<= SMALLM_MAX), a_ptr and b_ptr set, the fp32 / code epilogues
+  // run as a CUDA-core IDP4A kernel (k_gemm_smallm) instead of the tcgen05 one
+  const int8_t* a_ptr;
+  int64_t lda;
+  const int8_t* b_ptr;         // [N x K]
 };
+
+constexpr int SMALLM_MAX = 32;
+// Small-M path row bound (0 = off; default 32; env MNMT_SMALLM or the model option "smallm")
+// and deepest K (default 512; option "smallm_kmax").
+void gemm_set_smallm(int rows);
+void gemm_set_smallm_kmax(int k);
+int gemm_smallm();
 
 // Tensor map over a row-major int8 matrix [rows x K] (K contiguous, K % 16 == 0):
 // box {128 bytes, 64 rows}, 128-byte swizzle (the UMMA K-major SW128 atom).

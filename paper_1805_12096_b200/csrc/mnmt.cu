@@ -767,8 +767,11 @@ static mnmt_status lane_ensure(mnmt_model* m, Lane& Ln, int64_t M, int64_t B, in
 static cudaError_t gemm(mnmt_model* m, cudaStream_t st, const CUtensorMap& tmA, const Lin& W, int M,
                         const int32_t* M_dyn, int epi, float* out_f, int8_t* out_q, int64_t ldo,
                         unsigned long long* keys = nullptr, int col_block = 0,
-                        int64_t block_stride = 0) {
+                        int64_t block_stride = 0, const int8_t* A = nullptr) {
   GemmArgs a{};
+  a.a_ptr = A;   // raw A codes [M x W.in] (small-M path), or null
+  a.lda = W.in;
+  a.b_ptr = W.q;
   a.M = M;
   a.M_dyn = M_dyn;
   a.N = W.out;
@@ -785,6 +788,13 @@ static cudaError_t gemm(mnmt_model* m, cudaStream_t st, const CUtensorMap& tmA, 
   a.keys = keys;
   a.pers_grid = m->cur_pers_grid;
   return launch_gemm_i8(tmA, W.tm, a, epi, 0, st);
+}
+
+// Decoder GEMM that may take the small-M path (A also passed as a raw pointer).
+static cudaError_t gemm_r(mnmt_model* m, cudaStream_t st, const CUtensorMap& tmA, const int8_t* A,
+                          const Lin& W, int M, const int32_t* M_dyn, int epi, float* out_f,
+                          int8_t* out_q, int64_t ldo) {
+  return gemm(m, st, tmA, W, M, M_dyn, epi, out_f, out_q, ldo, nullptr, 0, 0, A);
 }
 
 // Fused GEMM + residual (+gate) + LayerNorm + Q (+ next-layer AAN) when one CTA can own
@@ -1017,12 +1027,12 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
           if ((e = cudaEventRecord(Ln.ev_join, Ln.side)) != cudaSuccess) return e;
         }
         if (c.aan_ffn_depth == 2) {
-          if ((e = gemm(m, st, w.tm_cg, D.a1, n, nd, EPI_RELU_Q, nullptr, w.ch1, d)) != cudaSuccess) return e;
-          if ((e = gemm(m, st, w.tm_ch1, D.a2, n, nd, EPI_F32_Q, w.a, w.ca, d)) != cudaSuccess) return e;
+          if ((e = gemm_r(m, st, w.tm_cg, w.cg, D.a1, n, nd, EPI_RELU_Q, nullptr, w.ch1, d)) != cudaSuccess) return e;
+          if ((e = gemm_r(m, st, w.tm_ch1, w.ch1, D.a2, n, nd, EPI_F32_Q, w.a, w.ca, d)) != cudaSuccess) return e;
           a_f = w.a;
           k += 2;
         } else if (c.aan_ffn_depth == 1) {
-          if ((e = gemm(m, st, w.tm_cg, D.a1, n, nd, EPI_RELU_F32_Q, w.a, w.ca, d)) != cudaSuccess) return e;
+          if ((e = gemm_r(m, st, w.tm_cg, w.cg, D.a1, n, nd, EPI_RELU_F32_Q, w.a, w.ca, d)) != cudaSuccess) return e;
           a_f = w.a;
           k += 1;
         }
@@ -1030,8 +1040,9 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
           // gate (R8): logits W_i Q(y) + b_i and W_f Q(a) + b_f (for -ffn, Q(a) = Q(g));
           // the sigmoids are applied in the gate-LayerNorm kernel
           const CUtensorMap& tm_a = c.aan_ffn_depth == 0 ? w.tm_cg : w.tm_ca;
+          const int8_t* a_ptr = c.aan_ffn_depth == 0 ? w.cg : w.ca;
           if (!fork) {
-            if ((e = gemm(m, st, w.tm_cy, D.gi, n, nd, EPI_F32, w.gi, nullptr, d)) != cudaSuccess) return e;
+            if ((e = gemm_r(m, st, w.tm_cy, w.cy, D.gi, n, nd, EPI_F32, w.gi, nullptr, d)) != cudaSuccess) return e;
           }
           l1 = ln_args(m, w, n, nd, w.y, a_f, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
           l1.gi = w.gi;
@@ -1042,7 +1053,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
             if ((e = gemm_ln(m, st, tm_a, D.gf, n, nd, l1)) != cudaSuccess) return e;
             l1_done = true;
           } else {
-            if ((e = gemm(m, st, tm_a, D.gf, n, nd, EPI_F32, w.gf, nullptr, d)) != cudaSuccess) return e;
+            if ((e = gemm_r(m, st, tm_a, a_ptr, D.gf, n, nd, EPI_F32, w.gf, nullptr, d)) != cudaSuccess) return e;
           }
           if (fork && !fuse_ln_dd(m) && (e = cudaStreamWaitEvent(st, Ln.ev_join, 0)) != cudaSuccess)
             return e;   // join before the gate LayerNorm reads gi
@@ -1052,7 +1063,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
         }
       } else {
         // A6': self-attention with a KV cache
-        if ((e = gemm(m, st, w.tm_cy, D.qkv, n, nd, EPI_F32, w.qkvd, nullptr, 3 * d)) != cudaSuccess) return e;
+        if ((e = gemm_r(m, st, w.tm_cy, w.cy, D.qkv, n, nd, EPI_F32, w.qkvd, nullptr, 3 * d)) != cudaSuccess) return e;
         AttnArgs at{};
         at.mode = ATTN_SELF;
         at.span = Ln.span_cap;
@@ -1076,7 +1087,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
         at.sigma = sigma_of(m);
         at.out_q = w.cctxd;
         if ((e = launch_attn(at, st)) != cudaSuccess) return e;
-        if ((e = gemm(m, st, w.tm_cctxd, D.o, n, nd, EPI_F32, w.od, nullptr, d)) != cudaSuccess) return e;
+        if ((e = gemm_r(m, st, w.tm_cctxd, w.cctxd, D.o, n, nd, EPI_F32, w.od, nullptr, d)) != cudaSuccess) return e;
         k += 3;
         l1 = ln_args(m, w, n, nd, w.y, w.od, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
       }
@@ -1115,7 +1126,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
       ++k;
     } else {
       // A7: source attention
-      if ((e = gemm(m, st, w.tm_cx1, D.sq, n, nd, EPI_F32, w.qs, nullptr, d)) != cudaSuccess) return e;
+      if ((e = gemm_r(m, st, w.tm_cx1, w.cx1, D.sq, n, nd, EPI_F32, w.qs, nullptr, d)) != cudaSuccess) return e;
       AttnArgs as{};
       as.mode = ATTN_SRC;
       as.span = Ln.span_cap;
@@ -1146,21 +1157,21 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
         if ((e = gemm_ln(m, st, w.tm_cctxd, D.so, n, nd, l2)) != cudaSuccess) return e;
         k += 3;
       } else {
-        if ((e = gemm(m, st, w.tm_cctxd, D.so, n, nd, EPI_F32, w.od, nullptr, d)) != cudaSuccess) return e;
+        if ((e = gemm_r(m, st, w.tm_cctxd, w.cctxd, D.so, n, nd, EPI_F32, w.od, nullptr, d)) != cudaSuccess) return e;
         if ((e = launch_ln(l2, st)) != cudaSuccess) return e;
         k += 4;
       }
     }
     if (hook && (e = hook->x2(m, l)) != cudaSuccess) return e;
     // A8: FFN
-    if ((e = gemm(m, st, w.tm_cx2, D.f1, n, nd, EPI_RELU_Q, nullptr, w.chd, c.d_ffn)) != cudaSuccess) return e;
+    if ((e = gemm_r(m, st, w.tm_cx2, w.cx2, D.f1, n, nd, EPI_RELU_Q, nullptr, w.chd, c.d_ffn)) != cudaSuccess) return e;
     LnArgs l3 = ln_args(m, w, n, nd, w.x2, w.f, D.ln[2][0], D.ln[2][1], w.y, w.cy);
     l3.aan = aan_for_layer(m, w, l + 1);
     if (fuse_ln(m)) {
       if ((e = gemm_ln(m, st, w.tm_chd, D.f2, n, nd, l3)) != cudaSuccess) return e;
       k += 2;
     } else {
-      if ((e = gemm(m, st, w.tm_chd, D.f2, n, nd, EPI_F32, w.f, nullptr, d)) != cudaSuccess) return e;
+      if ((e = gemm_r(m, st, w.tm_chd, w.chd, D.f2, n, nd, EPI_F32, w.f, nullptr, d)) != cudaSuccess) return e;
       if ((e = launch_ln(l3, st)) != cudaSuccess) return e;
       k += 3;
     }
@@ -1738,6 +1749,7 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
     const int rows_per = std::max(1, m->beam);   // beam search: up to beam rows per sentence
     auto pad_at = [&](int t) {
       const int a = b.alive[t] * rows_per;
+      if (a <= gemm_smallm() && m->beam == 0 && !(m->rowfuse > 0)) return gemm_smallm();   // small-M GEMMs
       return (a < 128 && m->rowfuse > 0) ? std::max(16, (a + 15) / 16 * 16) : (a + 127) / 128 * 128;
     };
     if (m->megakernel && m->beam == 0 && Ln.sl_n == 0 && (!hook || hook->megakernel_ok())) {
@@ -1813,7 +1825,8 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
         t += k;
       }
     } else {
-      const int nrows = (B * rows_per + 127) / 128 * 128;
+      const int nrows = (B * rows_per <= gemm_smallm() && m->beam == 0 && !(m->rowfuse > 0))
+                            ? gemm_smallm() : (B * rows_per + 127) / 128 * 128;
       for (int t = 0; t < b.T; ++t) CK(launch_step(m, Ln, nrows, forced, hook, &launches));
     }
     if (m->beam > 0) {
@@ -2517,6 +2530,24 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
   if (std::string(name) == "lane_tiers") {
     if (value < 0 || value > 100) { set_err("lane_tiers must be in [0, 100]"); return MNMT_ERR_ARG; }
     m->lane_tiers = (int)value;
+    return MNMT_OK;
+  }
+  if (std::string(name) == "smallm") {
+    if (value < 0 || value > SMALLM_MAX) { set_err("smallm must be in [0, 32]"); return MNMT_ERR_ARG; }
+    gemm_set_smallm((int)value);   // process-wide (a GEMM launch setting)
+    for (Lane& L : m->lanes) {     // captured graphs encode the old kernel sequence
+      for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
+      L.graphs.clear();
+    }
+    return MNMT_OK;
+  }
+  if (std::string(name) == "smallm_kmax") {
+    if (value < 0 || value > (1 << 16)) { set_err("smallm_kmax must be in [0, 65536]"); return MNMT_ERR_ARG; }
+    gemm_set_smallm_kmax((int)value);   // process-wide
+    for (Lane& L : m->lanes) {
+      for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
+      L.graphs.clear();
+    }
     return MNMT_OK;
   }
   if (std::string(name) == "fin_embed") {

@@ -184,6 +184,67 @@ def test_finish_embeds_next_step(dims):
     gm.set_option("fin_embed", 0)
 
 
+@pytest.mark.parametrize("dims", TINY_VARIANTS, ids=lambda d: d.name)
+def test_small_m_gemms_teacher_forced(dims):
+    """Small-M path (live rows <= the "smallm" bound: IDP4A k_gemm_smallm for the decoder's
+    fp32 / code GEMMs, K split into 1, 2 or 4 segments by these widths) on and off: every intermediate within
+    tolerance of the oracle, ids bit-exact, and the two paths' ids identical."""
+    w, om, gm = pair(dims, 15)
+    ss, forced, foff = forced_case(dims, 9, 0, 13, 0, 17, seed=8)
+    got = {}
+    for bound in (32, 16, 0):    # row bound of the small-M path (9 rows: on, on, off)
+        gm.set_option("smallm", bound)
+        tot, ex, fl = run_forced_parity(dims, w, om, gm, ss, forced, foff)
+        assert ex == tot, (bound, f"{tot - ex} flagged near-ties")
+        got[bound], _ = gm.decode_forced(ss, forced, foff, 0)
+    gm.set_option("smallm", 32)
+    assert np.array_equal(got[0], got[32]) and np.array_equal(got[0], got[16])
+
+
+@pytest.mark.parametrize("preset", ["small-aan", "base"])
+def test_small_m_gemms_paper_students(preset):
+    """The paper's student widths (K = 256 / 512 / 2048: 4 and 8 K segments, the deep-K loop
+    with smallm_kmax raised):
+    teacher-forced layer dumps against the oracle and free-running ids equal to the oracle with
+    the small-M path, and equal to the tcgen05 path's."""
+    dims = synth.PRESETS[preset]
+    w, om, gm = pair(dims, 16)
+    gm.set_option("smallm_kmax", 2048)
+    ss, forced, foff = forced_case(dims, 5, 1, 9, 1, 6, seed=10)
+    tot, ex, fl = run_forced_parity(dims, w, om, gm, ss, forced, foff)
+    assert ex == tot, f"{tot - ex} flagged near-ties"
+    fs = synth.random_set(7, 1, 8, seed=12, vocab=dims.vocab)
+    ref = om.decode_many(fs, 4)
+    got = gm.decode(fs)
+    assert all(np.array_equal(a, b) for a, b in zip(got, ref))
+    gm.set_option("smallm", 0)
+    assert all(np.array_equal(a, b) for a, b in zip(gm.decode(fs), ref))
+    gm.set_option("smallm", 32)
+    gm.set_option("smallm_kmax", 512)
+    assert all(np.array_equal(a, b) for a, b in zip(gm.decode(fs), ref))
+
+
+def test_small_m_gemms_big_student():
+    """big (K = 1024 / 4096: 8 segments of 128 / 512 bytes): the small-M path's ids and final
+    decoder states equal the tcgen05 path's on a teacher-forced batch (both GPU paths; the
+    tcgen05 one is oracle-checked elsewhere)."""
+    dims = synth.PRESETS["big"]
+    w = synth.make_weights(dims, seed=17)
+    gm = M.Model(dims, w)
+    ss, forced, foff = forced_case(dims, 6, 1, 12, 1, 8, seed=11)
+    mask = M.DUMP_DEC_OUT | M.DUMP_OUT_CODES
+    out = {}
+    gm.set_option("smallm_kmax", 4096)   # off by default at these depths (slower)
+    for on in (1, 0):
+        gm.set_option("smallm", 32 if on else 0)
+        out[on] = gm.decode_forced(ss, forced, foff, mask)
+    gm.set_option("smallm", 32)
+    gm.set_option("smallm_kmax", 512)
+    assert np.array_equal(out[0][0], out[1][0])
+    np.testing.assert_array_equal(out[0][1]["dec_out"], out[1][1]["dec_out"])
+    np.testing.assert_array_equal(out[0][1]["out_codes"], out[1][1]["out_codes"])
+
+
 def test_config0_tiny192_aan():
     """BASELINE configs[0]: tiny-192 AAN, 36k vocab, 4 sentences of length 20."""
     dims = synth.PRESETS["tiny192-aan"]
