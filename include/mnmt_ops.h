@@ -44,7 +44,8 @@ mnmt_status mnmt_op_quantize(const float* x_dev, int64_t n, float clip, int8_t* 
 /* dotint(quant(A), quant(B^T)) = A . W^T on the int8 tensor cores (R3):
  * A [M x K] codes, W [N x K] codes (K % 16 == 0), bias [N] fp32 or NULL.
  * For EPI_F32* / SIGMOID / ACC, N % 16 == 0; out row stride = N.
- * n_tile = 0 (auto), 64, 128 or 256. */
+ * n_tile = 0 (auto), 64, 128 or 256; -1 = the small-M CUDA-core kernel (IDP4A, same s32 sums and
+ * epilogue arithmetic; M <= 32, EPI_F32 .. EPI_SIGMOID, A and W 16-byte aligned). */
 mnmt_status mnmt_op_gemm_i8(const int8_t* A_dev, const int8_t* W_dev, int32_t M, int32_t N,
                             int32_t K, const float* bias_dev, float clip, int32_t epilogue,
                             void* out_dev, void* out2_dev, int32_t n_tile, void* stream);

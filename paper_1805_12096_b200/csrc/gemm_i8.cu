@@ -1379,7 +1379,7 @@ template <int EPI>
 static cudaError_t launch_smallm_e(const GemmArgs& a, int S, cudaStream_t st) {
   const int cn = 8 / S;
   const int ctas4 = (a.N + cn * 4 - 1) / (cn * 4), ctas8 = (a.N + cn * 8 - 1) / (cn * 8);
-  const int cap = 3 * (a.pers_grid > 0 ? a.pers_grid : num_sms());
+  const int cap = a.smallm_force ? (1 << 30) : 3 * (a.pers_grid > 0 ? a.pers_grid : num_sms());
   const bool fit8 = (size_t)cn * 8 * a.K <= 48 * 1024, fit4 = (size_t)cn * 4 * a.K <= 48 * 1024;
   if (fit8 && (ctas4 > 64 || a.K >= 1024 || (ctas4 > cap && ctas8 <= cap)))
     return ctas8 <= cap ? launch_smallm_c<EPI, 8>(a, S, st) : cudaErrorNotSupported;
@@ -1390,7 +1390,8 @@ static cudaError_t launch_smallm_e(const GemmArgs& a, int S, cudaStream_t st) {
 // Returns cudaErrorNotSupported when the launch does not qualify (the caller takes the
 // tcgen05 path).
 static cudaError_t launch_smallm(const GemmArgs& a, int epi, cudaStream_t st) {
-  if (!g_smallm || !a.a_ptr || !a.b_ptr || a.M > g_smallm || a.M > SMALLM_MAX || a.K > g_smallm_kmax)
+  if (!a.a_ptr || !a.b_ptr || a.M > SMALLM_MAX) return cudaErrorNotSupported;
+  if (!a.smallm_force && (!g_smallm || a.M > g_smallm || a.K > g_smallm_kmax))
     return cudaErrorNotSupported;
   if (a.K % 16 || a.lda % 16 || ((uintptr_t)a.a_ptr & 15) || ((uintptr_t)a.b_ptr & 15))
     return cudaErrorNotSupported;

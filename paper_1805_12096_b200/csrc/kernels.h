@@ -70,6 +70,7 @@ struct GemmArgs {
   const int8_t* a_ptr;
   int64_t lda;
   const int8_t* b_ptr;         // [N x K]
+  int smallm_force;            // op level: take the small-M path whenever it can run (M <= 32)
 };
 
 constexpr int SMALLM_MAX = 32;

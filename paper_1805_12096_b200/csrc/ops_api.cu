@@ -46,8 +46,11 @@ mnmt_status mnmt_op_gemm_i8(const int8_t* A, const int8_t* W, int32_t M, int32_t
   if (epi != MNMT_EPI_ARGMAX && epi != MNMT_EPI_TOPK && N % 16) return arg_error("mnmt_op_gemm_i8: N % 16 != 0");
   if ((epi == MNMT_EPI_F32_Q || epi == MNMT_EPI_RELU_F32_Q) && !out2)
     return arg_error("mnmt_op_gemm_i8: epilogue needs out2");
-  if (epi != MNMT_EPI_TOPK && n_tile != 0 && n_tile != 64 && n_tile != 128 && n_tile != 256)
-    return arg_error("mnmt_op_gemm_i8: n_tile must be 0, 64, 128 or 256");
+  const bool small = n_tile == -1;   // the small-M CUDA-core kernel (k_gemm_smallm)
+  if (small && (M > 32 || epi > MNMT_EPI_SIGMOID || (uintptr_t)A % 16 || (uintptr_t)W % 16))
+    return arg_error("mnmt_op_gemm_i8: n_tile -1 needs M <= 32, an fp32 / code epilogue and 16-byte aligned A, W");
+  if (epi != MNMT_EPI_TOPK && n_tile != 0 && n_tile != 64 && n_tile != 128 && n_tile != 256 && !small)
+    return arg_error("mnmt_op_gemm_i8: n_tile must be -1, 0, 64, 128 or 256");
   int n_tile_topk = 0;
   if (cudaError_t e = gemm_init(); e != cudaSuccess) return cuda_status(e, "gemm init");
   CUtensorMap ta, tb;
@@ -64,6 +67,13 @@ mnmt_status mnmt_op_gemm_i8(const int8_t* A, const int8_t* W, int32_t M, int32_t
   a.ldo = N;
   a.col_block = N;
   a.block_stride = 0;
+  if (small) {
+    a.a_ptr = A;
+    a.lda = K;
+    a.b_ptr = W;
+    a.smallm_force = 1;
+    n_tile = 0;
+  }
   switch (epi) {
     case MNMT_EPI_F32:
     case MNMT_EPI_SIGMOID: a.out_f = (float*)out; break;

@@ -24,7 +24,8 @@ elif k in ("dxd", "out"):
     out = torch.empty((Mr, N) if k == "dxd" else (Mr,), dtype=torch.float32 if k == "dxd" else torch.int64, device=dev)
     epi = M.EPI_F32 if k == "dxd" else M.EPI_ARGMAX
     for _ in range(4):
-        M.op_gemm_i8(A.data_ptr(), W.data_ptr(), Mr, N, d, b.data_ptr(), 2.0, epi, out.data_ptr(), None, 0, None)
+        M.op_gemm_i8(A.data_ptr(), W.data_ptr(), Mr, N, d, b.data_ptr(), 2.0, epi, out.data_ptr(), None,
+                     int(os.environ.get("NTILE", 0)), None)   # NTILE=-1: the small-M kernel
 else:
     S = int(os.environ.get("S", 21))
     L = np.full(Mr, S, np.int32); st = (np.arange(Mr) * S).astype(np.int32)

@@ -96,6 +96,44 @@ def test_gemm_epilogues_bitexact(epi, Mr, N, K):
         assert np.array_equal(of.cpu().numpy(), O.sigmoid_array(v))
 
 
+@pytest.mark.parametrize("epi", [M.EPI_F32, M.EPI_F32_Q, M.EPI_RELU_Q, M.EPI_RELU_F32_Q, M.EPI_SIGMOID])
+@pytest.mark.parametrize("Mr,N,K,bias", [(1, 256, 256, True), (7, 2048, 256, True), (32, 256, 2048, True),
+                                         (32, 512, 512, False), (19, 48, 96, True), (32, 16, 16, True),
+                                         (13, 1024, 4096, True), (32, 208, 192, True)])
+def test_gemm_small_m_bitexact(epi, Mr, N, K, bias):
+    """k_gemm_smallm (n_tile -1: IDP4A, lane = row, S K segments, 4 / 8 columns per warp,
+    ragged column tiles) equals the oracle's fmaf((float)acc, s, b) and the epilogue's ReLU /
+    sigmoid / Q element by element."""
+    rng = np.random.default_rng(epi * 1000 + Mr * 7 + K)
+    x = rng.normal(0, 1.0, size=(Mr, K)).astype(np.float32)
+    W = rng.uniform(-0.08, 0.08, size=(N, K)).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, size=N).astype(np.float32) if bias else None
+    qa, qw = O.quantize(x), O.quantize(W)
+    v = O.linear(qa, qw, b, CLIP)
+    A, Wd = to_dev(qa), to_dev(qw)
+    bd = to_dev(b) if bias else None
+    of = empty((Mr, N), torch.float32)
+    oq = empty((Mr, N), torch.int8)
+    bp = ptr(bd) if bias else None
+    if epi == M.EPI_RELU_Q:
+        M.op_gemm_i8(ptr(A), ptr(Wd), Mr, N, K, bp, CLIP, epi, ptr(oq), None, -1)
+    else:
+        M.op_gemm_i8(ptr(A), ptr(Wd), Mr, N, K, bp, CLIP, epi, ptr(of), ptr(oq), -1)
+    sync()
+    r = np.maximum(v, np.float32(0))
+    if epi in (M.EPI_F32, M.EPI_F32_Q):
+        assert np.array_equal(of.cpu().numpy(), v)
+    if epi == M.EPI_F32_Q:
+        assert np.array_equal(oq.cpu().numpy(), O.quantize(v))
+    if epi == M.EPI_RELU_Q:
+        assert np.array_equal(oq.cpu().numpy(), O.quantize(r))
+    if epi == M.EPI_RELU_F32_Q:
+        assert np.array_equal(of.cpu().numpy(), r)
+        assert np.array_equal(oq.cpu().numpy(), O.quantize(r))
+    if epi == M.EPI_SIGMOID:
+        assert np.array_equal(of.cpu().numpy(), O.sigmoid_array(v))
+
+
 @pytest.mark.parametrize("Mr,N,K,bias", [(3, 50, 32, True), (200, 36000, 256, True),
                                          (129, 36000, 192, False), (390, 36000, 512, True),
                                          (650, 36000, 256, True)])   # persistent kernel
