@@ -7,10 +7,15 @@ length and cut into >= 8192-word batches, encoded and greedily de
 (max_len = source length) with every product in int8 on the tensor cores.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mnmt|reference]
+                    [--workload W] [--scaling weak|strong]
 
-N > 1 is launched by torchrun (one process per GPU, NCCL); each rank decodes its own
-newstest-shaped set (weak scaling) and the output ids are gathered to rank 0.
-Rank 0 prints ONE JSON line.
+The default workload is BASELINE.json configs[3]: the big student (d 1024, F 4096, H 16,
+plain self-attention decoder), greedy, on the newstest-shaped set.  N > 1: one process per
+GPU over NCCL; without torchrun's environment `--gpus N` re-launches itself under
+`torch.distributed.run`.  weak (default): every rank decodes its own newstest-shaped set;
+strong: one set is length-sorted and dealt round-robin over the ranks.  The
+ids of every rank are all-gathered and put in input order on rank 0 inside the timed region
+(A11).  Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
 
@@ -40,7 +45,7 @@ WORKLOADS = {
     "base-aan-newstest-8192w": ("base-aan", 8192, "configs[2] AAN"),
     "big-newstest-8192w": ("big", 8192, "configs[3]"),
 }
-DEFAULT_WORKLOAD = "small-aan-newstest-8192w"
+DEFAULT_WORKLOAD = "big-newstest-8192w"   # BASELINE.json configs[3]: the metric's own config
 # Per-workload launch options (scheduling only: ids are identical for every setting), from the
 # green_sms x lane_tiers sweep on one B200 (profiles/r1_sweep_green_tiers.txt): the critical
 # lane's SM partition pays off for the smaller students and costs the big one (its bulk lanes
@@ -285,6 +290,30 @@ def live_rows_profile(sset, budget, max_concurrent_rows=0):
     return rows
 
 
+def live_rows_profile_waves(sset, budget, max_concurrent_rows=0):
+    """The decode waves of the library's schedule (lists of word-budget batch indices), for the
+    config description: stable length sort, batches closed at >= budget words (R17)."""
+    L = np.asarray(sset.lengths)[np.argsort(sset.lengths, kind="stable")]
+    off, acc = [0], 0
+    for i, x in enumerate(L):
+        acc += int(x)
+        if acc >= budget:
+            off.append(i + 1)
+            acc = 0
+    if off[-1] != len(L):
+        off.append(len(L))
+    nb = len(off) - 1
+    waves, b = [], 0
+    while b < nb:
+        e = b + 1
+        if max_concurrent_rows > 0:
+            while e < nb and off[e + 1] - off[b] <= max_concurrent_rows:
+                e += 1
+        waves.append(list(range(b, e)))
+        b = e
+    return waves
+
+
 def roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr, beam=0, fused=1,
                       n_cols=None):
     """A9: output projection fused with argmax (beam > 0: with the beam-search log-sum-exp +
@@ -370,7 +399,10 @@ def roofline_dxd_gemm(dims, sset, budget, peaks, stream, mcr, mult=1):
 
 def roofline_src_attn(dims, sset, budget, peaks, stream, mcr, mult=1):
     """A7: source attention over the fp32 (kv_bf16: bf16, F3) K/V cache, rows = the workload's
-    mean live rows per step, drawn (seeded) from the set so the source-length mix matches."""
+    mean live rows per step, drawn (seeded) from the set so the source-length mix matches.
+    Cold: consecutive launches rotate over copies of K/V whose total exceeds the 126 MB L2, so
+    every launch streams its K/V from HBM (as in the job, where the K/V of six layers and
+    thousands of rows cannot stay L2-resident)."""
     import torch
     from paper_1805_12096_b200 import mnmt as M
     rows = live_rows_profile(sset, budget, mcr)
@@ -382,14 +414,20 @@ def roofline_src_attn(dims, sset, budget, peaks, stream, mcr, mult=1):
     n = len(idx)
     dev = torch.device("cuda", torch.cuda.current_device())
     kv16 = bool(getattr(dims, "kv_bf16", 0))
-    kv = torch.randn((int(L.sum()), 2 * d), device=dev)
-    if kv16:
-        kv = kv.to(torch.bfloat16)
+    one = int(L.sum()) * 2 * d * (2 if kv16 else 4)
+    copies = max(2, int(np.ceil(384e6 / max(one, 1))))        # > 3x L2 in total
+    kvs = []
+    for _ in range(copies):
+        kv = torch.randn((int(L.sum()), 2 * d), device=dev)
+        kvs.append(kv.to(torch.bfloat16) if kv16 else kv)
     q = torch.randn((n, d), device=dev)
     st, ln = torch.from_numpy(starts).to(dev), torch.from_numpy(L).to(dev)
     oq = torch.empty((n, d), dtype=torch.int8, device=dev)
+    it = [0]
 
     def fn(s_):
+        kv = kvs[it[0] % copies]
+        it[0] += 1
         op = M.op_attention_bf16 if kv16 else M.op_attention
         op(q.data_ptr(), d, kv.data_ptr(), 2 * d, 0, d, st.data_ptr(), ln.data_ptr(),
            n, d, H, dims.clip, oq.data_ptr(), None, s_)
@@ -401,34 +439,97 @@ def roofline_src_attn(dims, sset, budget, peaks, stream, mcr, mult=1):
     return {"kernel": "k_attn (A7 source attention, fp64 accumulate" + (", bf16 K/V)" if kv16 else ")"),
             "bound": "hbm",
             "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
-            "shape": f"rows={n} S_mean={L.mean():.1f} d={d} H={H} (one layer)",
+            "shape": f"rows={n} S_mean={L.mean():.1f} d={d} H={H} (one layer; K/V rotated over "
+                     f"{copies} copies, {copies * one / 1e6:.0f} MB > L2)",
             "ms_per_launch": ms, "peak_source": peaks["source"]}
 
 
-def ncu_traffic(key, shape):
+def roofline_ln(dims, sset, budget, peaks, stream, mcr, mult=1):
+    """A6-A8: residual + LayerNorm + Q (k_ln, 3 per layer per step) at the mean live-row count;
+    algorithmic bytes per row = x, delta (fp32) in, out (fp32) + codes out = 13 d."""
+    import torch
+    from paper_1805_12096_b200 import mnmt as M
+    rows = live_rows_profile(sset, budget, mcr)
+    n = max(1, int(round(np.mean(rows) * mult)))
+    d = dims.d_model
+    dev = torch.device("cuda", torch.cuda.current_device())
+    copies = max(2, int(np.ceil(384e6 / (n * d * 8))))
+    xs = [torch.randn((n, d), device=dev) for _ in range(copies)]
+    ds = [torch.randn((n, d), device=dev) for _ in range(copies)]
+    g = torch.ones(d, device=dev)
+    b = torch.zeros(d, device=dev)
+    out = torch.empty((n, d), device=dev)
+    oq = torch.empty((n, d), dtype=torch.int8, device=dev)
+    it = [0]
+
+    def fn(s_):
+        k = it[0] % copies
+        it[0] += 1
+        M.op_layernorm(xs[k].data_ptr(), ds[k].data_ptr(), None, None, g.data_ptr(), b.data_ptr(),
+                       n, d, dims.ln_eps, dims.clip, out.data_ptr(), oq.data_ptr(), s_)
+    ms = time_kernel(fn, 200, stream)
+    bytes_ = 13.0 * d * n
+    ach = bytes_ / (ms * 1e-3) / 1e9
+    return {"kernel": "k_ln (A6-A8 residual + LayerNorm + Q)", "bound": "hbm", "achieved": ach,
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "traffic": None,
+            "shape": f"rows={n} d={d} (inputs rotated over {copies} copies > L2)",
+            "ms_per_launch": ms, "launches_per_step": len(rows) * 3 * dims.dec_layers,
+            "ms_per_step_est": ms * len(rows) * 3 * dims.dec_layers, "peak_source": peaks["source"]}
+
+
+def ncu_traffic(key, shape, workload):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of this kernel from the committed
-    `ncu --set full` capture (profiles/r1_ncu_full_kernels.json, scripts/kernel_once.py), used
-    only when the captured shape has the same row count as the one timed here."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                        "r1_ncu_full_kernels.json")
+    `ncu --set full` capture of this workload (profiles/r2_ncu_full_kernels.json, written by
+    scripts/ncu_full_summary.py from scripts/kernel_once.py runs), used only when the captured
+    shape has the same row count as the one timed here."""
+    path = os.path.join(ROOT, "profiles", "r2_ncu_full_kernels.json")
     try:
         with open(path) as f:
-            rec = json.load(f)[key]
+            rec = json.load(f)[f"{key}@{workload}"]
     except (OSError, KeyError, ValueError):
-        return None, "no ncu capture"
+        return None, "no ncu capture of this kernel / workload"
     rows = lambda t: (re.search(r"(?:M|rows)=(\d+)", t) or [None, None])[1]
     if rows(rec["shape"]) != rows(shape):
         return None, f"ncu capture shape {rec['shape']} differs"
     return rec["traffic_bytes"], f"ncu --set full (cold L2), {rec['shape']}"
 
 
+def gemm_pipe_record(workload):
+    """SURVEY 8(d) headline: the duration-weighted decoder-GEMM tensor-pipe % of one job of this
+    workload on this build, from the committed ncu pass (scripts/gemm_pipe_report.py --json)."""
+    path = os.path.join(ROOT, "profiles", f"r2_decoder_gemm_pipe_{workload}.json")
+    try:
+        rec = json.load(open(path))
+    except (OSError, ValueError):
+        return None
+    return {"decoder_gemm_tensor_pipe_pct": rec["decoder_gemm_tensor_pipe_pct"],
+            "decoder_gemm_useful_ops_pct": rec["decoder_gemm_useful_ops_pct"],
+            "decoder_gemm_share_of_decode_time": rec["decoder_gemm_share_of_decode_time"],
+            "per_class": {k: {"tensor_pipe_pct": v["tensor_pipe_pct"], "useful_ops_pct": v["useful_ops_pct"]}
+                          for k, v in rec["per_class"].items()},
+            "source": os.path.relpath(path, ROOT) + " (ncu launch list of one job, serialised, cold L2)"}
+
+
 # ---------------------------------------------------------------------------- main
 def metric_name(beam: int, shortlist: bool = False, kv16: bool = False) -> str:
     if kv16 and beam <= 1 and not shortlist:
-        return "target words/sec greedy decode with bf16 source keys/values (F3), 1 B200"
+        return "target words/sec greedy decode with bf16 source keys/values (F3)"
     if shortlist:
-        return "target words/sec greedy decode with batch vocabulary shortlist (100 frequent + 100 per source word), 1 B200"
-    return METRIC if beam <= 1 else f"target words/sec beam-{beam} decode (best hypothesis), 1 B200"
+        return "target words/sec greedy decode with batch vocabulary shortlist (100 frequent + 100 per source word)"
+    return METRIC if beam <= 1 else f"target words/sec beam-{beam} decode (best hypothesis)"
+
+
+def relaunch_under_torchrun(args):
+    """`--gpus N` (N > 1) without torchrun's environment: re-run this command as N ranks."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -438,6 +539,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mnmt", choices=["mnmt", "reference"])
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = one newstest-shaped set per GPU (default); strong = one "
+                         "set sharded round-robin in length order (SURVEY 8(e))")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
@@ -452,16 +556,11 @@ def main():
                     help="source keys / values rounded to bf16 (SURVEY 8(f) F3, src_kv_bf16 = 1)")
     ap.add_argument("--beam-fused", type=int, default=0,
                     help="beam search: 1 = log-sum-exp / top-k fused into the output GEMM epilogue")
-    ap.add_argument("--megakernel", type=int, default=0,
-                    help="1: persistent step kernel per batch; 0: one kernel per op (CUDA graph)")
     ap.add_argument("--lanes", type=int, default=3,
                     help="independent decoder lanes (streams) per GPU (scheduling only)")
     ap.add_argument("--lane-tiers", type=int, default=None,
                     help="0: deal sentences round-robin to lanes; 10*p: contiguous length tiers "
                          "of equal sum S^p (scheduling only; default: per workload)")
-    ap.add_argument("--rowfuse", type=int, default=0,
-                    help="steps with <= this many padded rows use the fused per-row AAN and "
-                         "source-attention blocks (0 = off)")
     ap.add_argument("--green-sms", type=int, default=None,
                     help="SM partition (green context) of the critical lane; 0 = shared SMs "
                          "(default: per workload)")
@@ -474,15 +573,11 @@ def main():
                          "default per workload)")
     ap.add_argument("--smallm-kmax", type=int, default=None,
                     help="deepest K of the small-M path (default per workload)")
-    ap.add_argument("--fin-embed", type=int, default=0,
-                    help="row bound up to which k_finish also embeds the next step's rows "
-                         "(one launch per step less; 0 = separate k_embed_tgt always)")
-    ap.add_argument("--fuse-ln", type=int, default=0,
-                    help="LayerNorm in the producing GEMM's epilogue: 0 separate kernels, "
-                         "1 one CTA per row block (d <= 256), 2 a CTA cluster per row block")
     ap.add_argument("--max-concurrent-rows", type=int, default=4096,
                     help="co-schedule consecutive >=budget-word batches in one decode wave "
                          "(scheduling only; 0 = one batch at a time)")
+    ap.add_argument("--opt", action="append", default=[],
+                    help="extra model option name=value (A/B runs; scheduling only)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     for k, v in WORKLOAD_OPTS.get(args.workload, {}).items():
@@ -491,6 +586,8 @@ def main():
     args.green_sms = 56 if args.green_sms is None else args.green_sms
     args.lane_tiers = 40 if args.lane_tiers is None else args.lane_tiers
 
+    if args.impl == "mnmt" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -499,29 +596,39 @@ def main():
     if args.kv_bf16:
         import dataclasses
         dims = dataclasses.replace(dims, name=dims.name + "-kvbf16", kv_bf16=1)
+    scaling = args.scaling if world > 1 else "weak"
+    mcr = args.max_concurrent_rows
+    full = synth.newstest_set(seed=2014)
+    waves = len(live_rows_profile_waves(full, budget, mcr))
     workload_cfg = {"workload": args.workload, "baseline_config": cfg_ref,
                     "student": f"{preset}: d={dims.d_model} F={dims.d_ffn} H={dims.n_heads} "
                                f"L={dims.enc_layers}+{dims.dec_layers} V={dims.vocab} "
                                f"decoder={'AAN' if dims.decoder else 'self-attn'}",
-                    "sentences_per_gpu": synth.NEWSTEST_SENTENCES,
-                    "source_words_per_gpu": synth.NEWSTEST_TOKENS, "word_budget": budget,
+                    "sentences": synth.NEWSTEST_SENTENCES * (world if scaling == "weak" else 1),
+                    "source_words": synth.NEWSTEST_TOKENS * (world if scaling == "weak" else 1),
+                    "sharding": ("one newstest-shaped set per GPU (seed 2014 + rank)" if scaling == "weak"
+                                 else "one newstest-shaped set, length-sorted, dealt round-robin over the GPUs"),
+                    "word_budget": budget,
+                    "schedule": (f"word-budget batches (>= {budget} words, P:L42) co-scheduled in waves of "
+                                 f"<= {mcr} sentences: the 3003-sentence set decodes as {waves} wave(s), "
+                                 f"split into {args.lanes} length-tiered lanes"),
                     "beam": args.beam, "beam_fused": args.beam_fused,
                     "src_kv": "bf16 (F3)" if args.kv_bf16 else "fp32",
-                    "shortlist": "100 frequent + 100 per source word (synthetic Zipf tables, seed 85)" if args.shortlist else None, "max_len": "source length", "parallelism": f"dp{args.gpus}",
+                    "shortlist": "100 frequent + 100 per source word (synthetic Zipf tables, seed 85)" if args.shortlist else None,
+                    "max_len": "source length", "parallelism": f"dp{world}",
                     "l2": "flushed between timed steps (512 MiB write)",
-                    "max_concurrent_rows": args.max_concurrent_rows, "lanes": args.lanes,
-                    "fuse_ln": args.fuse_ln, "steps_per_graph": args.steps_per_graph,
-                    "fin_embed": args.fin_embed, "smallm": args.smallm,
+                    "max_concurrent_rows": mcr, "lanes": args.lanes,
+                    "steps_per_graph": args.steps_per_graph, "smallm": args.smallm,
                     "smallm_kmax": args.smallm_kmax,
                     "lane_tiers": args.lane_tiers, "pers_reserve": args.pers_reserve,
-                    "green_sms": args.green_sms, "rowfuse": args.rowfuse,
-                    "step_engine": "persistent cooperative kernel" if args.megakernel else "kernel-per-op CUDA graph"}
+                    "green_sms": args.green_sms, "extra_options": args.opt,
+                    "step_engine": "kernel-per-op CUDA graph per decoder step (PDL chained)"}
 
     if args.impl == "reference":
         if rank != 0:
             return
         weights = synth.make_weights(dims, seed=1)
-        run_reference(args, dims, weights, synth.newstest_set(seed=2014), workload_cfg)
+        run_reference(args, dims, weights, full, workload_cfg)
         return
 
     import torch
@@ -530,25 +637,34 @@ def main():
     if dist_on:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if world != args.gpus:
+            raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE = {world}")
     from paper_1805_12096_b200 import dist as D
     from paper_1805_12096_b200 import mnmt as M
 
     weights = synth.make_weights(dims, seed=1)
     model = M.Model(dims, weights, device=local)
-    model.set_option("max_concurrent_rows", args.max_concurrent_rows)
-    model.set_option("lanes", args.lanes)
-    model.set_option("megakernel", args.megakernel)
-    model.set_option("fuse_ln", args.fuse_ln)
-    model.set_option("steps_per_graph", args.steps_per_graph)
-    model.set_option("fin_embed", args.fin_embed)
-    model.set_option("smallm", 32 if args.smallm is None else args.smallm)
-    model.set_option("smallm_kmax", 512 if args.smallm_kmax is None else args.smallm_kmax)
-    model.set_option("lane_tiers", args.lane_tiers)
-    model.set_option("pers_reserve", args.pers_reserve)
-    model.set_option("green_sms", args.green_sms)
-    model.set_option("rowfuse", args.rowfuse)
-    model.set_option("beam_fused", args.beam_fused)
-    sset = synth.newstest_set(seed=2014 + rank)          # weak scaling: one set per GPU
+    for name, v in (("max_concurrent_rows", mcr), ("lanes", args.lanes),
+                    ("steps_per_graph", args.steps_per_graph),
+                    ("smallm", 32 if args.smallm is None else args.smallm),
+                    ("smallm_kmax", 512 if args.smallm_kmax is None else args.smallm_kmax),
+                    ("lane_tiers", args.lane_tiers), ("pers_reserve", args.pers_reserve),
+                    ("green_sms", args.green_sms), ("beam_fused", args.beam_fused)):
+        model.set_option(name, v)
+    for kv in args.opt:
+        k, v = kv.split("=")
+        model.set_option(k, int(v))
+    # the rows this rank decodes, and the static gather / unshard plan of the whole job
+    if scaling == "weak":
+        sset = synth.newstest_set(seed=2014 + rank)
+        n_each = sset.n
+        shards = [np.arange(r * n_each, (r + 1) * n_each) for r in range(world)]
+        ml_all = np.concatenate([synth.newstest_set(seed=2014 + r).max_len for r in range(world)]) \
+            if world > 1 else sset.max_len
+    else:
+        shards = [D.shard_round_robin(full.lengths, r, world) for r in range(world)]
+        sset = full.subset(shards[rank])
+        ml_all = full.max_len
     use_sl = bool(args.shortlist)
     if use_sl:
         if args.beam > 1:
@@ -561,11 +677,21 @@ def main():
     beam = args.beam
     nb = max(1, beam)
     cap = int(sset.max_len.sum()) * nb
-    out_dev = torch.zeros(cap, dtype=torch.int32, device=dev)
-    len_dev = torch.zeros(sset.n * nb, dtype=torch.int32, device=dev)
-    score_dev = torch.zeros(sset.n * nb, dtype=torch.float32, device=dev)
-    nhyp_dev = torch.zeros(sset.n, dtype=torch.int32, device=dev)
+    out_dev = torch.zeros(max(cap, 1), dtype=torch.int32, device=dev)
+    len_dev = torch.zeros(max(sset.n * nb, 1), dtype=torch.int32, device=dev)
+    score_dev = torch.zeros(max(sset.n * nb, 1), dtype=torch.float32, device=dev)
+    nhyp_dev = torch.zeros(max(sset.n, 1), dtype=torch.int32, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    plan = D.gather_plan(ml_all, shards) if dist_on and beam <= 1 else None
+    unshard = D.DeviceUnshard(plan, dev) if plan is not None and rank == 0 else None
+    launches_gather = 0
+
+    def gather(flat_dev, lens_dev):
+        """A11 across ranks: all_gather ids + lengths, input order on rank 0 (mnmt_op_gather_rows)."""
+        gi, gl = D.all_gather_padded(flat_dev[:int(sset.max_len.sum())], lens_dev[:sset.n], plan)
+        if unshard is not None:
+            return unshard(gi, gl, stream)
+        return None
 
     def step():
         if beam > 1:
@@ -576,17 +702,17 @@ def main():
             model.translate_device(ids_dev.data_ptr(), sset.offsets, sset.max_len, budget,
                                    out_dev.data_ptr(), cap, len_dev.data_ptr(), stream,
                                    shortlist=use_sl)
-            if dist_on:
-                D.gather_ids(out_dev, len_dev)
+            if plan is not None:
+                gather(out_dev, len_dev)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    launches_per_step = model.stats()["gpu_launches"]
+    launches_per_step = model.stats()["gpu_launches"] + (1 if unshard is not None else 0)
     if beam > 1:   # words of each sentence's best hypothesis
-        words_rank = int((len_dev.view(sset.n, nb)[:, 0] * (nhyp_dev > 0)).sum().item())
+        words_rank = int((len_dev[:sset.n * nb].view(sset.n, nb)[:, 0] * (nhyp_dev[:sset.n] > 0)).sum().item())
     else:
-        words_rank = int(len_dev.sum().item())
+        words_rank = int(len_dev[:sset.n].sum().item())
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -614,12 +740,20 @@ def main():
         t = tmax
     ms_max, words_total = float(t[0]), float(t[1])
     value = words_total * args.steps / (ms_max / 1000.0)
+    if plan is not None and rank == 0:   # the gathered job equals the per-rank outputs
+        assert int(unshard.lens.sum().item()) == int(words_total), "id gather lost rows"
 
     # ---- e2e: the public host-buffer call (H2D of ids, D2H of ids inside the timed region)
     def host_call():
         if beam > 1:
             return model.beam_translate(sset, budget, beam, stream)
-        return model.translate(sset, budget, stream, shortlist=use_sl)
+        outs = model.translate(sset, budget, stream, shortlist=use_sl)
+        if plan is not None:   # ids to the device, gathered, unsharded, back to rank 0's host
+            flat, lens = D.pack_ids(outs, sset.max_len)
+            res = gather(torch.from_numpy(flat).to(dev), torch.from_numpy(lens).to(dev))
+            if res is not None:
+                return D.split_rows(res[0].cpu().numpy(), res[1].cpu().numpy(), ml_all)
+        return outs
 
     host_call()
     torch.cuda.synchronize()
@@ -628,38 +762,43 @@ def main():
     for _ in range(args.e2e_steps):
         flush.zero_()
         torch.cuda.synchronize()
+        if dist_on:
+            dist.barrier()
         t0 = time.perf_counter()
-        outs = host_call()
-        if dist_on and beam <= 1:
-            flat, lens = D.pack_ids(outs, sset.max_len)
-            D.gather_ids(torch.from_numpy(flat).to(dev), torch.from_numpy(lens).to(dev))
+        host_call()
         torch.cuda.synchronize()
         e_ms.append(1000 * (time.perf_counter() - t0))
     e = torch.tensor([sum(e_ms)], dtype=torch.float64, device=dev)
     if dist_on:
         dist.all_reduce(e, op=dist.ReduceOp.MAX)
     e2e_value = words_total * args.e2e_steps / (float(e[0]) / 1000.0)
+    h2d, d2h = st["h2d_bytes"], st["d2h_bytes"]
+    if plan is not None:
+        h2d += int(sset.max_len.sum()) * 4 + sset.n * 4
+        if rank == 0:
+            d2h += plan.out_total * 4 + plan.n * 4
 
     roof = None
     cpu = None
     sl_lists = None
     if rank == 0 and not args.no_roofline:
         peaks = load_peaks()
-        mcr = args.max_concurrent_rows
         sl_lists = oracle_shortlists(sset, dims, budget, sl_freq, sl_lex) if use_sl else None
         n_cols = float(np.mean([len(x) for x in sl_lists[1]])) if use_sl else None
         cands = [roofline_out_gemm(dims, weights, sset, budget, peaks, stream, mcr,
                                    beam if beam > 1 else 0, args.beam_fused, n_cols),
                  roofline_src_attn(dims, sset, budget, peaks, stream, mcr, nb),
-                 roofline_dxd_gemm(dims, sset, budget, peaks, stream, mcr, nb)]
+                 roofline_dxd_gemm(dims, sset, budget, peaks, stream, mcr, nb),
+                 roofline_ln(dims, sset, budget, peaks, stream, mcr, nb)]
         cands[1]["launches_per_step"] = len(live_rows_profile(sset, budget, mcr)) * dims.dec_layers
         cands[1]["ms_per_step_est"] = cands[1]["ms_per_launch"] * cands[1]["launches_per_step"]
-        keys = ("out", "attn16" if getattr(dims, "kv_bf16", 0) else "attn", "dxd")
+        keys = ("out", "attn16" if getattr(dims, "kv_bf16", 0) else "attn", "dxd", "ln")
         for key, c in zip(keys, cands):
-            c["traffic"], c["traffic_source"] = ncu_traffic(key, c["shape"])
+            c["traffic"], c["traffic_source"] = ncu_traffic(key, c["shape"], args.workload)
         roof = max(cands, key=lambda c: c["ms_per_step_est"])
         roof["share_of_step_est"] = roof["ms_per_step_est"] / (ms_max / args.steps)
-        roof["other"] = {c["kernel"]: {"frac": c["frac"], "ms_per_step_est": c["ms_per_step_est"]}
+        roof["other"] = {c["kernel"]: {"frac": c["frac"], "ms_per_launch": c["ms_per_launch"],
+                                       "ms_per_step_est": c["ms_per_step_est"]}
                          for c in cands if c is not roof}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sl = (sl_lists or oracle_shortlists(sset, dims, budget, sl_freq, sl_lex)) if use_sl else None
@@ -668,17 +807,20 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": metric_name(beam, use_sl, bool(args.kv_bf16)), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": metric_name(beam, use_sl, bool(args.kv_bf16)), "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int8 products (s32 acc), f32 activations, f64 reductions",
+            "scaling": scaling, "vs_baseline": None,
+            "dtype": "int8 products (s32 acc), f32 activations, f64 reductions",
             "data": "synthetic (seeded random-init weights, newstest2014-shaped length-sorted ids)",
             "config": workload_cfg,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": st["h2d_bytes"],
-                    "d2h_bytes_per_step": st["d2h_bytes"]},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
             "gpu_launches": launches_per_step * args.steps,
             "target_words_per_step": words_total,
             "decode_steps_per_gpu": st["decode_steps"], "batches_per_gpu": st["batches"],
             "clocks": clk, "roofline": roof, "cpu_baseline": cpu,
+            "int8_tensor_pipe": gemm_pipe_record(args.workload) if beam <= 1 and not use_sl else None,
         }
         print(json.dumps(line))
     if dist_on:

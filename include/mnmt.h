@@ -187,6 +187,21 @@ mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids_host,
                                int32_t* argmax_ids_host, uint32_t dump_mask, void* dump_host,
                                int64_t dump_cap, void* cuda_stream);
 
+/* Teacher-forced decode through the whole mnmt_translate schedule (test hook, P-2 at the
+ * launch configuration the benchmark times): word-budget batches, co-scheduled waves,
+ * decoder lanes / length tiers / SM partitions and small-M GEMMs as set by the options, every
+ * step replayed from its captured CUDA graph.  Inputs, outputs and the DEC_OUT / OUT_CODES /
+ * LAYERS dump sections as mnmt_decode_forced (rows in forced_off order); the dumps are written
+ * by a copy kernel captured in the step graphs, so the kernels under test run unchanged.
+ * Errors as mnmt_decode_forced; MNMT_ERR_ARG for word_budget < 1 or the encoder dump bits
+ * (ENC_OUT, SRC_KV: one-batch calls only). */
+mnmt_status mnmt_translate_forced(mnmt_model* m, const int32_t* src_ids_host,
+                                  const int64_t* src_off_host, int32_t n,
+                                  const int32_t* forced_ids_host, const int64_t* forced_off_host,
+                                  int32_t word_budget, int32_t* argmax_ids_host,
+                                  uint32_t dump_mask, void* dump_host, int64_t dump_cap,
+                                  void* cuda_stream);
+
 /* Runtime options (not part of the method; they change scheduling only, never results —
  * rows are independent, so ids are identical for every setting):
  *   "max_concurrent_rows"  mnmt_translate co-schedules consecutive word-budget batches in
@@ -196,29 +211,12 @@ mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids_host,
  *   "lanes"                1..16 independent decoders (workspace + stream + step graph);
  *                          each wave's sentences are dealt round-robin to the lanes in
  *                          length order and the lanes' kernel chains overlap (default 1).
- *   "megakernel"           1: each batch's decoder steps run in ONE persistent
- *                          cooperative kernel (phases separated by grid barriers);
- *                          0 (default): one kernel per operation, replayed as a CUDA graph per step.
- *   "fuse_ln"              residual / gate + LayerNorm + Q fused into the epilogue of the
- *                          producing GEMM: 1 = one CTA owns whole rows (d = 192, 256);
- *                          2 = the d / BN N-tiles of a row block form a thread-block cluster
- *                          and exchange row statistics through distributed shared memory;
- *                          3 = as 1 for the decoder's d x d producers only (f-gate, source-
- *                          attention output); FFN2 keeps its split-N GEMM + LayerNorm kernel;
- *                          0 (default): separate LayerNorm kernels.
- *   "rowlocal"             persistent kernel only: 1 = GEMM/LayerNorm/embedding phases split by
- *                          128-row tile (CTA barriers between them), 0 (default) = split over the
- *                          grid with grid barriers.
  *   "steps_per_graph"      1..63 consecutive decoder steps captured in one CUDA graph (default 1).
  *   "smallm"               0..32 row bound (default 32): greedy decoder steps with at most this many
  *                          live rows run their fp32 / code-output GEMMs with K <= "smallm_kmax" as
  *                          IDP4A CUDA-core kernels (same s32 accumulators, same epilogue arithmetic,
- *                          bit-identical outputs); 0: tcgen05 always.  Process-wide (env
- *                          MNMT_SMALLM sets the initial value).
- *   "smallm_kmax"          deepest K the small-M path takes (default 512, process-wide).
- *   "fin_embed"            row bound up to which the step's finish kernel also embeds the next
- *                          step's rows (A5), removing k_embed_tgt from the step graph; 0 (default,
- *                          measured faster) = separate embedding kernel.
+ *                          bit-identical outputs); 0: tcgen05 always.  Per model.
+ *   "smallm_kmax"          deepest K the small-M path takes (default 512, per model).
  *   "lane_tiers"           0 (default): a wave's sentences are dealt round-robin to the lanes;
  *                          10*p: contiguous length tiers of equal sum S_i^p, the last lane (the
  *                          longest sentences, the job's critical path) on the highest-priority stream.
@@ -226,10 +224,6 @@ mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids_host,
  *   "green_sms"            0 (default) or a multiple of 8: with tiered lanes, the critical lane's
  *                          streams live in a green context (SM partition) of this many SMs and the
  *                          other lanes' in one holding the rest.
- *   "mk_cluster"           1: the persistent step kernel's grid (mk_ctas <= 16) is one thread-block
- *                          cluster and its phases synchronise with cluster barriers.
- *   "mk_ctas"              grid cap of the persistent step kernel (0 = one CTA per SM).
- *   "profile_phases"       1 = the persistent kernel stamps every phase (mnmt_debug_phase_*).
  *   "beam_fused"           beam search: 1 = log-sum-exp partials and top-k fused into the output
  *                          GEMM epilogue (EPI_TOPK*, logits never reach HBM); 0 (default, measured
  *                          faster) = fp32 logits written by the GEMM, reduced by one CTA per row.

@@ -90,12 +90,16 @@ mnmt_status mnmt_op_attention_bf16(const float* q_dev, int64_t ldq, const uint16
                                    int32_t n, int32_t d, int32_t H, float clip, int8_t* out_q_dev,
                                    float* out_f_dev, void* stream);
 
-/* Profiling hook: with model option "profile_phases" = 1, the persistent step kernel of
- * lane 0 stamps %globaltimer after every grid barrier.  out_ns_by_type[k] receives the
- * nanoseconds spent in phases of type k (0 GEMM, 1 embed, 2 LayerNorm, 3 attention,
- * 4 finish) summed over the *steps_out steps of the last batch.  n_types >= 5. */
-mnmt_status mnmt_debug_phase_profile(mnmt_model* m, int64_t* out_ns_by_type, int32_t n_types,
-                                     int32_t* steps_out);
+
+/* A11 on several GPUs: ids back in input order after the id gather of a
+ * strong-scaling run.  Source row i (ids src_dev[src_off[i] .. + src_len[i]), src_len[i] >= 0)
+ * is copied to dst_dev[dst_off[dst_row[i]] ..] and dst_len[dst_row[i]] = src_len[i].
+ * src_off_dev, dst_off_dev: int64 [n] / [max dst_row + 1]; dst_row_dev: int32 [n], distinct.
+ * Rows may not overlap in dst.  One warp per row. */
+mnmt_status mnmt_op_gather_rows(const int32_t* src_dev, const int64_t* src_off_dev,
+                                const int32_t* src_len_dev, const int32_t* dst_row_dev,
+                                const int64_t* dst_off_dev, int32_t n, int32_t* dst_dev,
+                                int32_t* dst_len_dev, void* stream);
 
 #ifdef __cplusplus
 }

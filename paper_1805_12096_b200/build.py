@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmnmt.so")
 BUILD = os.path.join(HERE, "csrc", "build")
-SOURCES = ["gemm_i8.cu", "rowops.cu", "beam.cu", "shortlist.cu", "rowfused.cu", "stepkernel.cu", "mnmt.cu", "ops_api.cu"]
+SOURCES = ["gemm_i8.cu", "rowops.cu", "beam.cu", "shortlist.cu", "mnmt.cu", "ops_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-fmad=false", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",

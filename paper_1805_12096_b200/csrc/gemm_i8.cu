@@ -38,7 +38,6 @@ constexpr int EPI_STAGE_LD = 36;                       // row stride (floats): 1
                                                        // conflict-free STS.128 / LDS.128
 constexpr int EPI_STAGE_FLOATS = 32 * EPI_STAGE_LD;    // per epilogue warp
 constexpr int EPI_STAGE_BYTES = EPI_WARPS * EPI_STAGE_FLOATS * 4;
-constexpr int LNC_MAX_CLUSTER = 8;                     // portable cluster size limit
 
 template <int BN>
 struct GemmCfg {
@@ -246,45 +245,6 @@ __device__ __forceinline__ void epi_store_chunk(const GemmArgs& args, const floa
   }
 }
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-
-// Full-row LayerNorm epilogue (EPI_LN, BN = N = d: this CTA owns whole rows).  Once the
-// accumulator is complete the pipeline's shared memory is free: phase A dequantises the tile
-// (fmaf(acc, s, b), the EPI_F32 arithmetic) into a [128][BN + 4] fp32 tile there (thread = row,
-// 16-byte stores, conflict-free); phase B runs the k_ln row (ln_row: residual or AAN gate, fp64
-// statistics, R20; codes; next-layer AAN step) one warp per live row with coalesced global
-// accesses, reading the GEMM output row from the tile.  Same arithmetic as GEMM + k_ln.
-constexpr int LN_TILE_LD_PAD = 4;
-template <int BN>
-constexpr int ln_tile_bytes() { return BM * (BN + LN_TILE_LD_PAD) * 4; }
-
-template <int BN>
-__device__ __forceinline__ void ln_epilogue(const GemmArgs& a, uint32_t t_row, int half, int rl,
-                                            float* tile, int m0, int M_live, int ew) {
-  constexpr int HALF = BN / 2, LD = BN + LN_TILE_LD_PAD;
-  const bool fast = a.K <= 256;
-#pragma unroll 1
-  for (int c = 0; c < HALF; c += 32) {
-    int32_t acc[32];
-    tmem_ld16(t_row + c, *reinterpret_cast<int32_t(*)[16]>(acc));
-    tmem_ld16(t_row + c + 16, *reinterpret_cast<int32_t(*)[16]>(acc + 16));
-    tmem_ld_wait();
-    const int n = half * HALF + c;
-    float v[32];
-    dequant32(a, a.bias, n, fast, acc, v);
-    float* dst = tile + rl * LD + n;
-#pragma unroll
-    for (int j = 0; j < 32; j += 4)
-      *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-  }
-  epi_bar();
-  constexpr int NV = (BN / 4 + 31) / 32;
-#pragma unroll 1
-  for (int rr = ew; rr < BM; rr += EPI_WARPS) {
-    if (m0 + rr >= M_live) break;   // warp-uniform
-    ln_row<NV>(a.ln, m0 + rr, tile + rr * LD);
-  }
-}
 
 // EPI_TOPK* (beam search, F1): one 32-column chunk at a time, the row's running maximum m,
 // the fp64 sum z = sum exp(v - m) (rescaled by exp(m_old - m_new) when a chunk raises m) and
@@ -554,10 +514,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                    (warp - 2) * EPI_STAGE_FLOATS;
     float best_v = -INFINITY;
     int best_j = -1;
-    if constexpr (EPI == EPI_LN) {
-      ln_epilogue<BN>(args, t_row, half, q * 32 + lane, reinterpret_cast<float*>(smem), m0,
-                      M_live, warp - 2);
-    } else if constexpr (is_topk(EPI)) {
+    if constexpr (is_topk(EPI)) {
       topk_epilogue<BN, topk_k(EPI)>(args, args.bias ? bias_s - n0 : nullptr, t_row, row, row_ok,
                                      half, n0, exp_tab);
     } else
@@ -587,269 +544,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
   if (warp == 1 && lane == 0) GEMM_TRACE(5);     // after the barrier and the dealloc
-}
-
-// ------------------------------------------------------------------ cluster LayerNorm variant
-// EPI_LNC: GEMM + residual (+ AAN gate) + LayerNorm + Q (+ next-layer AAN step) where the d/BN
-// N-tiles of one 128-row M-tile form a thread-block cluster that together owns whole rows.
-// Each epilogue thread keeps its row's BN/2 residuals in registers; the fp64 row statistics
-// (R20) are formed per CTA, exchanged through distributed shared memory and combined in
-// cluster-rank order, so every CTA of the cluster computes the same mu and var:
-//   pass 1  r = x + v  (or y + fl(fl(i*y) + fl(f*a)), f = sigmoid(v)); partial sum -> peers
-//   pass 2  mu = sum(partials)/d; partial sum (r - mu)^2 -> peers
-//   pass 3  var = sum(partials)/d; out = LN(r) (fp64, rounded once), Q(out), AAN step.
-// The same arithmetic as k_ln / ln_row with the row sums split into ordered partial sums.
-template <int BN>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
-    k_gemm_lnc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               const GemmArgs args) {
-  using Cfg = GemmCfg<BN>;
-  constexpr int HALF = BN / 2;
-  extern __shared__ uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[Cfg::STAGES];
-  __shared__ __align__(8) uint64_t empty_bar[Cfg::STAGES];
-  __shared__ __align__(8) uint64_t tmem_full_bar;
-  __shared__ uint32_t tmem_slot;
-  __shared__ double part[2][BM];                 // per column-half row partials (this CTA)
-  __shared__ double xch[2][LNC_MAX_CLUSTER][BM];  // [pass][source rank][row], written by peers
-
-  const uint32_t warp = warp_id();
-  const uint32_t lane = lane_id();
-  const int n_tile = blockIdx.x, m_tile = blockIdx.y;
-  const int m0 = m_tile * BM, n0 = n_tile * BN;
-  const int num_kb = (args.K + BK - 1) / BK;
-  const int stages = min(Cfg::STAGES, num_kb);
-  const uint32_t rank = cluster_ctarank(), ncta = cluster_nctarank();
-  const LnArgs& L = args.ln;
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
-    for (int s = 0; s < stages; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
-    }
-    mbar_init(&tmem_full_bar, 1);
-    fence_barrier_init();
-    for (int s = 0; s < stages; ++s) {
-      mbar_arrive_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
-      uint8_t* sb = smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES;
-#pragma unroll
-      for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
-        tma_load_2d(sb + j * 64 * BK, &tmB, &full_bar[s], s * BK, n0 + j * 64);
-    }
-  }
-  cluster_arrive_relaxed();   // "this CTA is running"; waited on before the first DSMEM write
-  if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(&tmem_slot);
-  pdl_wait();
-  if (warp == 0 && lane == 0) {   // first stages' A tiles, in parallel with the live-row read
-    for (int s = 0; s < stages; ++s) {
-      uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
-      tma_load_2d(sa, &tmA, &full_bar[s], s * BK, m0);
-      tma_load_2d(sa + 64 * BK, &tmA, &full_bar[s], s * BK, m0 + 64);
-    }
-  }
-  const int M_live = args.M_dyn ? min(args.M, *args.M_dyn) : args.M;
-  if (m0 >= M_live) {   // uniform over the cluster (one M-tile)
-    if (warp == 0 && lane == 0)
-      for (int s = 0; s < stages; ++s) mbar_wait(&full_bar[s], 0);
-    __syncwarp();
-    cluster_wait();
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_slot);
-    return;
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      for (int kb = stages; kb < num_kb; ++kb) {
-        const int s = kb % stages;
-        uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
-        uint8_t* sb = sa + Cfg::A_BYTES;
-        mbar_wait(&empty_bar[s], ((kb / stages) - 1) & 1);
-        mbar_arrive_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
-#pragma unroll
-        for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
-          tma_load_2d(sb + j * 64 * BK, &tmB, &full_bar[s], kb * BK, n0 + j * 64);
-        tma_load_2d(sa, &tmA, &full_bar[s], kb * BK, m0);
-        tma_load_2d(sa + 64 * BK, &tmA, &full_bar[s], kb * BK, m0 + 64);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_i8<BM, BN>();
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % stages;
-        mbar_wait(&full_bar[s], (kb / stages) & 1);
-        tc_fence_after();
-        const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
-        const uint32_t sb = sa + Cfg::A_BYTES;
-        const uint64_t adesc = umma_desc_sw128(sa);
-        const uint64_t bdesc = umma_desc_sw128(sb);
-#pragma unroll
-        for (int k = 0; k < BK / 32; ++k)
-          mma_i8(tmem_base, adesc + (uint64_t)(2 * k), bdesc + (uint64_t)(2 * k), idesc, (kb | k) != 0);
-        mma_commit(&empty_bar[s]);
-      }
-      mma_commit(&tmem_full_bar);
-    }
-  }
-
-  // ---- epilogue warps 2..9: quarter q = warp % 4 (TMEM lanes), column half = (warp - 2) / 4
-  const bool epi = warp >= 2;
-  const int q = warp & 3, half = ((int)warp - 2) >> 2;
-  const int rl = q * 32 + lane, row = m0 + rl;
-  const bool row_ok = row < M_live;
-  const int d = args.N;
-  const int c0 = n0 + half * HALF;               // first global column of this thread
-  const int64_t off = (int64_t)row * d;
-  const bool gate = L.gi != nullptr;
-  const bool small = args.K <= 256;
-  float r[HALF];
-  double s = 0.0;
-  __syncwarp();                                  // cluster barriers are .aligned: reconverge
-  cluster_wait();                                // every CTA of the cluster is running
-  if (epi) {
-    mbar_wait(&tmem_full_bar, 0);
-    tc_fence_after();
-    if (warp == 2 && lane == 0) pdl_launch_dependents();
-    const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + half * HALF;
-#pragma unroll
-    for (int c = 0; c < HALF; c += 32) {
-      int32_t acc[32];
-      tmem_ld16(t_row + c, *reinterpret_cast<int32_t(*)[16]>(acc));
-      tmem_ld16(t_row + c + 16, *reinterpret_cast<int32_t(*)[16]>(acc + 16));
-      tmem_ld_wait();
-#pragma unroll
-      for (int j4 = 0; j4 < 32; j4 += 4) {
-        const int col = c0 + c + j4;
-        float4 x4 = make_float4(0.f, 0.f, 0.f, 0.f), g4 = x4, a4 = x4;
-        if (row_ok) {
-          x4 = *reinterpret_cast<const float4*>(L.x + off + col);
-          if (gate) {
-            g4 = *reinterpret_cast<const float4*>(L.gi + off + col);
-            a4 = *reinterpret_cast<const float4*>(L.delta + off + col);
-          }
-        }
-        const float4 b4 = args.bias ? __ldg(reinterpret_cast<const float4*>(args.bias + col))
-                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-        const float xs[4] = {x4.x, x4.y, x4.z, x4.w}, gs[4] = {g4.x, g4.y, g4.z, g4.w};
-        const float as_[4] = {a4.x, a4.y, a4.z, a4.w}, bs[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float v = __fmaf_rn(acc_to_float(acc[j4 + u], small), args.scale, bs[u]);
-          float rv;
-          if (gate) {
-            // AAN gate (R8): i = sigmoid(gi logit), f = sigmoid(v); z = fl(fl(i*y) + fl(f*a))
-            const float iy = __fmul_rn(sigmoid_f64(gs[u]), xs[u]);
-            const float fa = __fmul_rn(sigmoid_f64(v), as_[u]);
-            rv = __fadd_rn(xs[u], __fadd_rn(iy, fa));
-          } else {
-            rv = __fadd_rn(xs[u], v);
-          }
-          r[c + j4 + u] = rv;
-          s = __dadd_rn(s, (double)rv);
-        }
-      }
-    }
-    part[half][rl] = s;
-  }
-  // ---- exchange 1: row sums -> every CTA of the cluster
-  if (epi) epi_bar();
-  if (epi && half == 0) {
-    const double tot = __dadd_rn(part[0][rl], part[1][rl]);
-    const uint32_t a0 = smem_u32(&xch[0][rank][rl]);
-    for (uint32_t k = 0; k < ncta; ++k) st_cluster_f64(mapa_shared(a0, k), tot);
-  }
-  cluster_sync();
-  double mu = 0.0;
-  if (epi) {
-    double tot = 0.0;
-    for (uint32_t k = 0; k < ncta; ++k) tot = __dadd_rn(tot, xch[0][k][rl]);
-    mu = __ddiv_rn(tot, (double)d);
-    double qv = 0.0;
-#pragma unroll
-    for (int j = 0; j < HALF; ++j) {
-      const double t = __dsub_rn((double)r[j], mu);
-      qv = __dadd_rn(qv, __dmul_rn(t, t));
-    }
-    part[half][rl] = qv;
-    epi_bar();
-    if (half == 0) {
-      const double t2 = __dadd_rn(part[0][rl], part[1][rl]);
-      const uint32_t a1 = smem_u32(&xch[1][rank][rl]);
-      for (uint32_t k = 0; k < ncta; ++k) st_cluster_f64(mapa_shared(a1, k), t2);
-    }
-  }
-  cluster_sync();
-  if (epi && row_ok) {
-    double tot = 0.0;
-    for (uint32_t k = 0; k < ncta; ++k) tot = __dadd_rn(tot, xch[1][k][rl]);
-    const double var = __ddiv_rn(tot, (double)d);
-    const double inv = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(var, (double)L.eps)));
-    const int orig = L.aan.C ? L.live[row] : 0;
-    const float tf = L.aan.C ? (float)L.ctrl[1] : 1.0f;
-#pragma unroll
-    for (int c = 0; c < HALF; c += 16) {
-      float o[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int col = c0 + c + j;
-        o[j] = (float)__dadd_rn(__dmul_rn(__dmul_rn(__dsub_rn((double)r[c + j], mu), inv),
-                                          (double)__ldg(L.gamma + col)),
-                                (double)__ldg(L.beta + col));
-      }
-      if (L.out) {
-#pragma unroll
-        for (int j = 0; j < 16; j += 4)
-          *reinterpret_cast<float4*>(L.out + off + c0 + c + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
-      }
-      if (L.out_q) {
-        uint32_t w[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          w[j] = (uint32_t)(q8(o[4 * j], L.clip, L.sigma) & 0xff) |
-                 ((uint32_t)(q8(o[4 * j + 1], L.clip, L.sigma) & 0xff) << 8) |
-                 ((uint32_t)(q8(o[4 * j + 2], L.clip, L.sigma) & 0xff) << 16) |
-                 ((uint32_t)(q8(o[4 * j + 3], L.clip, L.sigma) & 0xff) << 24);
-        *reinterpret_cast<uint4*>(L.out_q + off + c0 + c) = make_uint4(w[0], w[1], w[2], w[3]);
-      }
-      if (L.aan.C) {
-        // AAN step (R6, R7): C <- fl(C + y); g = fl(C / t)
-        float* Cr = L.aan.C + (int64_t)orig * d + c0 + c;
-        float g[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float cv = __fadd_rn(Cr[j], o[j]);
-          Cr[j] = cv;
-          g[j] = __fdiv_rn(cv, tf);
-        }
-        if (L.aan.g_f)
-#pragma unroll
-          for (int j = 0; j < 16; ++j) L.aan.g_f[off + c0 + c + j] = g[j];
-        if (L.aan.g_q) {
-          uint32_t w[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            w[j] = (uint32_t)(q8(g[4 * j], L.aan.clip, L.aan.sigma) & 0xff) |
-                   ((uint32_t)(q8(g[4 * j + 1], L.aan.clip, L.aan.sigma) & 0xff) << 8) |
-                   ((uint32_t)(q8(g[4 * j + 2], L.aan.clip, L.aan.sigma) & 0xff) << 16) |
-                   ((uint32_t)(q8(g[4 * j + 3], L.aan.clip, L.aan.sigma) & 0xff) << 24);
-          *reinterpret_cast<uint4*>(L.aan.g_q + off + c0 + c) = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
 }
 
 // ------------------------------------------------------------------ persistent variant
@@ -1144,15 +838,6 @@ static cudaError_t gemm_init_all();
 
 // Opt every GEMM instantiation into its dynamic shared memory size on the current
 // device (once per device).  Must run before any launch (never inside a stream capture).
-static cudaError_t set_attr_ln() {
-  cudaError_t e = cudaFuncSetAttribute(k_gemm_i8<192, EPI_LN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       std::max(GemmCfg<192>::smem_for(GemmCfg<192>::STAGES),
-                                                1024 + ln_tile_bytes<192>()));
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_gemm_i8<256, EPI_LN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              std::max(GemmCfg<256>::smem_for(GemmCfg<256>::STAGES),
-                                       1024 + ln_tile_bytes<256>()));
-}
 
 cudaError_t gemm_init() {
   static bool done[64] = {};
@@ -1167,16 +852,9 @@ cudaError_t gemm_init() {
 
 static cudaError_t gemm_init_all() {
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(k_gemm_lnc<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                GemmCfg<64>::STAGES * GemmCfg<64>::STAGE_BYTES + 1024)) != cudaSuccess)
-    return e;
-  if ((e = cudaFuncSetAttribute(k_gemm_lnc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                GemmCfg<128>::STAGES * GemmCfg<128>::STAGE_BYTES + 1024)) != cudaSuccess)
-    return e;
   if ((e = set_attr_bn32()) != cudaSuccess) return e;
   if ((e = set_attr_bn<64>()) != cudaSuccess) return e;
   if ((e = set_attr_bn<128>()) != cudaSuccess) return e;
-  if ((e = set_attr_ln()) != cudaSuccess) return e;
   for (const void* f : {(const void*)k_gemm_i8<TOPK_BN, EPI_TOPK>, (const void*)k_gemm_i8<TOPK_BN, EPI_TOPK2>,
                         (const void*)k_gemm_i8<TOPK_BN, EPI_TOPK4>})
     if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1210,8 +888,6 @@ static cudaError_t launch_np(const CUtensorMap& tmA, const CUtensorMap& tmB, con
   cfg.gridDim = dim3((a.N + BN - 1) / BN, (a.M + BM - 1) / BM);
   cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = Cfg::smem_for(num_kb < Cfg::STAGES ? num_kb : Cfg::STAGES);
-  if constexpr (EPI == EPI_LN)   // the LayerNorm tile reuses the pipeline's shared memory
-    cfg.dynamicSmemBytes = std::max<size_t>(cfg.dynamicSmemBytes, 1024 + ln_tile_bytes<BN>());
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1221,35 +897,6 @@ static cudaError_t launch_np(const CUtensorMap& tmA, const CUtensorMap& tmB, con
   return cudaLaunchKernelEx(&cfg, k_gemm_i8<BN, EPI>, tmA, tmB, a);
 }
 
-// EPI_LNC launch: grid (d / BN, M-tiles), cluster (d / BN, 1, 1).
-template <int BN>
-static cudaError_t launch_lnc(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
-                              cudaStream_t st) {
-  using Cfg = GemmCfg<BN>;
-  const int num_kb = (a.K + BK - 1) / BK;
-  const int cn = a.N / BN;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(cn, (a.M + BM - 1) / BM);
-  cfg.blockDim = dim3(GEMM_THREADS);
-  cfg.dynamicSmemBytes = (num_kb < Cfg::STAGES ? num_kb : Cfg::STAGES) * Cfg::STAGE_BYTES + 1024;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-  attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = cn;
-  attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, k_gemm_lnc<BN>, tmA, tmB, a);
-}
-
-int gemm_lnc_bn(int d) {
-  for (int bn : {64, 128})
-    if (d % bn == 0 && d / bn <= LNC_MAX_CLUSTER) return bn;
-  return 0;
-}
 
 // ------------------------------------------------------------------ small-M path
 // At <= 32 live rows a decoder GEMM is latency-bound: the tcgen05 kernel's A-tile TMA round
@@ -1336,17 +983,6 @@ __global__ void __launch_bounds__(256) k_gemm_smallm(const GemmArgs args) {
   }
 }
 
-static int g_smallm = [] {   // row bound of the small-M path (0 = off)
-  const char* e = getenv("MNMT_SMALLM");
-  const int v = e ? atoi(e) : 16;
-  return v < 0 ? 0 : v > SMALLM_MAX ? SMALLM_MAX : v;
-}();
-void gemm_set_smallm(int rows) { g_smallm = rows < 0 ? 0 : rows > SMALLM_MAX ? SMALLM_MAX : rows; }
-// deepest K the small-M path takes: at K >= 1024 (the big student) every CTA's A reads and
-// weight staging outweigh the tcgen05 kernel's latency (measured: big 123.4 -> 126-129 ms)
-static int g_smallm_kmax = 512;
-void gemm_set_smallm_kmax(int k) { g_smallm_kmax = k; }
-int gemm_smallm() { return g_smallm; }
 
 template <int EPI, int CPW>
 static cudaError_t launch_smallm_c(const GemmArgs& a, int S, cudaStream_t st) {
@@ -1380,7 +1016,10 @@ static cudaError_t launch_smallm_e(const GemmArgs& a, int S, cudaStream_t st) {
   const int cn = 8 / S;
   const int ctas4 = (a.N + cn * 4 - 1) / (cn * 4), ctas8 = (a.N + cn * 8 - 1) / (cn * 8);
   const int cap = a.smallm_force ? (1 << 30) : 3 * (a.pers_grid > 0 ? a.pers_grid : num_sms());
-  const bool fit8 = (size_t)cn * 8 * a.K <= 48 * 1024, fit4 = (size_t)cn * 4 * a.K <= 48 * 1024;
+  // dynamic weight staging + the static reduction array red[8][CPW][32] within the 48 KB a
+  // launch gets without an opt-in
+  const bool fit8 = (size_t)cn * 8 * a.K + 8 * 8 * 32 * 4 <= 48 * 1024;
+  const bool fit4 = (size_t)cn * 4 * a.K + 8 * 4 * 32 * 4 <= 48 * 1024;
   if (fit8 && (ctas4 > 64 || a.K >= 1024 || (ctas4 > cap && ctas8 <= cap)))
     return ctas8 <= cap ? launch_smallm_c<EPI, 8>(a, S, st) : cudaErrorNotSupported;
   if (!fit4 || ctas4 > cap) return cudaErrorNotSupported;
@@ -1391,7 +1030,7 @@ static cudaError_t launch_smallm_e(const GemmArgs& a, int S, cudaStream_t st) {
 // tcgen05 path).
 static cudaError_t launch_smallm(const GemmArgs& a, int epi, cudaStream_t st) {
   if (!a.a_ptr || !a.b_ptr || a.M > SMALLM_MAX) return cudaErrorNotSupported;
-  if (!a.smallm_force && (!g_smallm || a.M > g_smallm || a.K > g_smallm_kmax))
+  if (!a.smallm_force && (a.smallm_rows <= 0 || a.M > a.smallm_rows || a.K > a.smallm_kmax))
     return cudaErrorNotSupported;
   if (a.K % 16 || a.lda % 16 || ((uintptr_t)a.a_ptr & 15) || ((uintptr_t)a.b_ptr & 15))
     return cudaErrorNotSupported;
@@ -1412,25 +1051,15 @@ cudaError_t launch_gemm_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const
   if (a.M <= 0 || a.N <= 0) return cudaSuccess;
   {
     const cudaError_t e = launch_smallm(a, epi, st);
-    if (e != cudaErrorNotSupported) return e;
-  }
-  if (epi == EPI_LNC) {   // the N tiles of an M tile form a cluster that owns whole rows
-    switch (gemm_lnc_bn(a.N)) {
-      case 64: return launch_lnc<64>(tmA, tmB, a, st);
-      case 128: return launch_lnc<128>(tmA, tmB, a, st);
-    }
-    return cudaErrorInvalidValue;
+    // op level (smallm_force): a launch the small-M kernel cannot take is an error, never a
+    // silent tcgen05 run
+    if (e != cudaErrorNotSupported || a.smallm_force) return e;
   }
   if (is_topk(epi)) {   // fixed tile (the partial layout depends on it), never persistent
     if (a.part_ld < 2 * ((a.N + TOPK_BN - 1) / TOPK_BN)) return cudaErrorInvalidValue;
     if (epi == EPI_TOPK2) return launch_np<TOPK_BN, EPI_TOPK2>(tmA, tmB, a, st);
     if (epi == EPI_TOPK4) return launch_np<TOPK_BN, EPI_TOPK4>(tmA, tmB, a, st);
     return launch_np<TOPK_BN, EPI_TOPK>(tmA, tmB, a, st);
-  }
-  if (epi == EPI_LN) {   // one CTA owns whole rows: BN = N = d
-    if (a.N == 192) return launch_np<192, EPI_LN>(tmA, tmB, a, st);
-    if (a.N == 256) return launch_np<256, EPI_LN>(tmA, tmB, a, st);
-    return cudaErrorInvalidValue;
   }
   if (bn == 0) bn = gemm_pick_bn(a.M, a.N, a.pers_grid);
   // 32-wide tiles halve each epilogue warp's columns where the 64-wide grid is small

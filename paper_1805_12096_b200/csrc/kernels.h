@@ -17,9 +17,6 @@ enum Epi : int {
   EPI_SIGMOID = 4,    // out_f = sigmoid(v)              (AAN gates)
   EPI_ARGMAX = 5,     // keys[row] = max packed(v, col)  (output layer, A9)
   EPI_ACC = 6,        // out_i = acc                     (test hook: raw accumulators)
-  EPI_LN = 7,         // full rows (BN = N = d): v = GEMM output; r = x + v (or the AAN gate
-                      // form with v = f-gate logit); out = LN(r), Q(out), next-layer AAN step
-  EPI_LNC = 8,        // as EPI_LN, rows owned by a cluster of N / BN CTAs (gemm_lnc_bn)
   EPI_TOPK = 9,       // beam search (F1): per (row, N-tile half) the running max m, the fp64
                       // sum z = sum exp(v - m) and the TOPK_MAX largest (v, col) -> part[]
   EPI_TOPK2 = 10,     // as EPI_TOPK with the 2 / 4 largest (beam <= 2 / <= 4; the other
@@ -61,7 +58,6 @@ struct GemmArgs {
   const int32_t* row_live;
   int pers_grid;               // persistent variant: CTA cap (0 = one per SM)
   unsigned long long* trace;   // debug: CTA (0,0) %globaltimer stamps [9] (null = off)
-  LnArgs ln;                   // EPI_LN: residual / gate inputs, gamma, beta, outputs, AAN
   TopkPart* part;              // EPI_TOPK: [rows][part_ld] partials (part_ld >= 2 * N tiles)
   int part_ld;
   // optional raw operands (row-major codes, K contiguous) for the small-M path: with
@@ -71,14 +67,11 @@ struct GemmArgs {
   int64_t lda;
   const int8_t* b_ptr;         // [N x K]
   int smallm_force;            // op level: take the small-M path whenever it can run (M <= 32)
+  int smallm_rows;             // small-M path row bound of the launch (0 = off, <= SMALLM_MAX)
+  int smallm_kmax;             // deepest K the small-M path takes
 };
 
 constexpr int SMALLM_MAX = 32;
-// Small-M path row bound (0 = off; default 32; env MNMT_SMALLM or the model option "smallm")
-// and deepest K (default 512; option "smallm_kmax").
-void gemm_set_smallm(int rows);
-void gemm_set_smallm_kmax(int k);
-int gemm_smallm();
 
 // Tensor map over a row-major int8 matrix [rows x K] (K contiguous, K % 16 == 0):
 // box {128 bytes, 64 rows}, 128-byte swizzle (the UMMA K-major SW128 atom).
@@ -90,7 +83,6 @@ cudaError_t launch_gemm_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const
                            int epi, int bn, cudaStream_t st);
 
 int gemm_pick_bn(int M, int N, int sms = 0);   // 64, 128 or 256 (sms: SM budget, 0 = device)
-int gemm_lnc_bn(int d);           // EPI_LNC tile width for N = d (0: not supported)
 
 // Programmatic dependent launch on every kernel (env MNMT_NO_PDL=1 disables; A/B testing).
 bool pdl_enabled();

@@ -26,9 +26,7 @@
 #include "beam.h"
 #include "kernels.h"
 #include "rowops.h"
-#include "rowfused.h"
 #include "shortlist.h"
-#include "stepkernel.h"
 
 using namespace mnmt;
 
@@ -66,7 +64,6 @@ struct Lin {
   float* b = nullptr;
   int out = 0, in = 0;
   CUtensorMap tm;
-  int32_t* q4 = nullptr;   // k4-major copy for the fused row blocks (decoder d x d maps)
 };
 
 struct EncLayer {
@@ -91,7 +88,6 @@ struct Workspace {
   int32_t *prev_live = nullptr, *live_start = nullptr, *live_len = nullptr;   // compact order
   int32_t *row_start = nullptr, *row_len = nullptr, *max_len = nullptr, *len_idx = nullptr;
   int64_t *out_off = nullptr, *forced_off = nullptr;
-  int32_t* forced = nullptr;
   unsigned long long* keys = nullptr;
   float *C = nullptr, *y = nullptr, *g = nullptr, *a = nullptr, *gi = nullptr, *gf = nullptr;
   float *x1 = nullptr, *qs = nullptr, *od = nullptr, *x2 = nullptr, *f = nullptr, *qkvd = nullptr;
@@ -130,6 +126,7 @@ struct JobBuf {
   int32_t* meta = nullptr;      // token metadata of all batches: idx|pos|start|len per batch
   int32_t* rmeta32 = nullptr;   // row metadata of all batches: [start|len|max_len|len_idx|order] x B_b
   int64_t* rmeta64 = nullptr;   // [out_off|forced_off] x B_b
+  int32_t* forced = nullptr;    // teacher forcing: [sum T_i] input ids (forced_off layout)
   float* out_score = nullptr;   // beam search: [n x beam] hypothesis scores
   int32_t* n_hyp = nullptr;     // beam search: [n] hypotheses per sentence
   // vocabulary shortlist (F2): per word-budget batch bitmap, ascending ids and count, and the
@@ -156,17 +153,18 @@ struct Lane {
   std::map<int64_t, int64_t> graph_launches;   // kernels per launch of graphs[key]
   int span_cap = 0;                            // attention span the step kernels are sized for
   int kind = -1;                               // streams from: 0 runtime, 1 critical / 2 bulk green context
-  // persistent step kernel program (built for this lane's workspace)
-  Phase* d_phases = nullptr;
-  int n_phases = 0;
-  bool prog_forced = false;
-  const int32_t* prog_out = nullptr;   // job output buffer the program writes to
-  CUtensorMap* d_tmaps = nullptr;
-  unsigned* d_bar = nullptr;
-  std::vector<int> phase_types;             // host copy, for profiling
-  unsigned long long* d_timing = nullptr;   // phase timestamps of the last launch (option)
-  int64_t timing_steps = 0;
   int sl_n = 0;                             // columns of the shortlisted output GEMM (0 = full V)
+};
+
+// Device-side dumps of a teacher-forced run (call state, MNMT_DUMP_*): k_dump_rows copies the
+// live rows of a step's activations to row foff[orig] + t - 1 of these buffers.  Launched
+// inside the step graphs, so dumps cover the same scheduling (lanes, tiers, SM partitions,
+// small-M GEMMs) as an untouched run.
+struct DevDump {
+  float* layers = nullptr;      // [O][L][3][d]: x1, x2, x3 of every decoder layer
+  float* dec_out = nullptr;     // [O][d]
+  int8_t* out_codes = nullptr;  // [O][d]
+  bool any() const { return layers || dec_out || out_codes; }
 };
 
 }  // namespace
@@ -192,17 +190,11 @@ struct mnmt_model {
   mnmt_stats stats{};
   int max_pos = MNMT_MAX_SPAN + 1;
   int64_t max_concurrent_rows = 0;   // option: co-schedule batches in waves of <= this many rows
-  int megakernel = 0;                  // option: persistent step kernel (1) or one kernel per op (0)
-  int profile_phases = 0;              // option: record per-phase timestamps (lane 0)
-  int fuse_ln = 0;                     // option: LayerNorm fused into full-row GEMM epilogues
-  int rowlocal = 0;                    // option: row-local phases in the persistent step kernel (measured slower)
   int steps_per_graph = 1;             // option: decoder steps captured per CUDA graph
-  int fin_embed = 0;                   // option: row bound up to which k_finish embeds the next step (measured slower)
-  int mk_ctas = 0;                     // option: persistent step kernel grid cap (0 = one per SM)
-  int mk_cluster = 0;                  // option: persistent step kernel grid = one cluster (mk_ctas <= 16)
+  int smallm = 32;                     // option: row bound of the small-M GEMM path (0 = off)
+  int smallm_kmax = 512;               // option: deepest K the small-M path takes
+  DevDump dump;                        // (call state) device dumps of a teacher-forced run
   int green_sms = 0;                   // option: SMs of the critical lane's green context (0 = off)
-  int rowfuse = 0;                     // option: steps with <= this many (padded) rows use the fused
-                                       //         per-row AAN / source-attention blocks (0 = off)
   CUgreenCtx green[2] = {nullptr, nullptr};   // [0] critical lane, [1] the other lanes
   int green_count[2] = {0, 0};                // SMs of each partition
   int pers_reserve = 0;                // option: SMs the persistent GEMMs of non-critical lanes leave free
@@ -354,13 +346,6 @@ static mnmt_status prep_lin(mnmt_model* m, Lin& L, const std::vector<std::string
   return MNMT_OK;
 }
 
-// k4-major copy of a prepared map's codes (rowfused.h), for the fused small-batch blocks.
-static mnmt_status prep_k4(mnmt_model* m, Lin& L) {
-  CKS(dalloc(m->allocs, &L.q4, (int64_t)L.out * L.in / 4));
-  CK(launch_repack_k4(L.q, L.out, L.in, L.q4, m->st));
-  return MNMT_OK;
-}
-
 static mnmt_status upload_vec(mnmt_model* m, float** dst, const std::string& name) {
   const auto& v = m->host[name];
   CKS(dalloc(m->allocs, dst, (int64_t)v.size()));
@@ -377,16 +362,6 @@ static void lane_free(Lane& L) {
   for (void* p : L.ws.sl_allocs) cudaFree(p);
   L.sl_n = 0;
   L.ws = Workspace();
-  if (L.d_phases) cudaFree(L.d_phases);
-  if (L.d_tmaps) cudaFree(L.d_tmaps);
-  if (L.d_bar) cudaFree(L.d_bar);
-  if (L.d_timing) cudaFree(L.d_timing);
-  L.d_timing = nullptr;
-  L.timing_steps = 0;
-  L.d_phases = nullptr;
-  L.d_tmaps = nullptr;
-  L.d_bar = nullptr;
-  L.n_phases = 0;
 }
 
 static void jb_free(mnmt_model* m) {
@@ -523,11 +498,11 @@ static mnmt_status jb_ensure(mnmt_model* m, int64_t O, int64_t N, int64_t tok, i
   for (Lane& L : m->lanes) {   // captured graphs / step programs point at the job buffers
     for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
     L.graphs.clear();
-    L.prog_out = nullptr;
   }
   JobBuf& z = m->jb;
   z.O_cap = Oc; z.N_cap = Nc; z.tok_cap = tc; z.meta_cap = mc; z.rows_cap = rc;
   CKS(dalloc(z.allocs, &z.out_ids, Oc));
+  CKS(dalloc(z.allocs, &z.forced, Oc));
   CKS(dalloc(z.allocs, &z.out_len, Nc));
   CKS(dalloc(z.allocs, &z.src_ids, tc));
   CKS(dalloc(z.allocs, &z.meta, mc));
@@ -739,7 +714,6 @@ static mnmt_status lane_ensure(mnmt_model* m, Lane& Ln, int64_t M, int64_t B, in
   CKS(dalloc(A, &z.len_idx, Bc));
   CKS(dalloc(A, &z.out_off, Bc));
   CKS(dalloc(A, &z.forced_off, Bc));
-  CKS(dalloc(A, &z.forced, Oc));
   CKS(dalloc(A, &z.keys, Bc));
   CKS(dalloc(A, &z.C, L * Bc * d));
   for (float** p : {&z.y, &z.g, &z.a, &z.gi, &z.gf, &z.x1, &z.qs, &z.od, &z.x2, &z.f})
@@ -787,6 +761,8 @@ static cudaError_t gemm(mnmt_model* m, cudaStream_t st, const CUtensorMap& tmA, 
   a.block_stride = block_stride;
   a.keys = keys;
   a.pers_grid = m->cur_pers_grid;
+  a.smallm_rows = m->smallm;
+  a.smallm_kmax = m->smallm_kmax;
   return launch_gemm_i8(tmA, W.tm, a, epi, 0, st);
 }
 
@@ -795,36 +771,6 @@ static cudaError_t gemm_r(mnmt_model* m, cudaStream_t st, const CUtensorMap& tmA
                           const Lin& W, int M, const int32_t* M_dyn, int epi, float* out_f,
                           int8_t* out_q, int64_t ldo) {
   return gemm(m, st, tmA, W, M, M_dyn, epi, out_f, out_q, ldo, nullptr, 0, 0, A);
-}
-
-// Fused GEMM + residual (+gate) + LayerNorm + Q (+ next-layer AAN) when one CTA can own
-// whole rows (d in {192, 256}); otherwise false (the caller runs GEMM then k_ln).
-// fuse_ln 1: one CTA owns whole rows (d in {192, 256}); 2: a cluster of d / BN CTAs owns them.
-static bool fuse_ln(const mnmt_model* m) {
-  if (m->fuse_ln == 2) return gemm_lnc_bn(m->c.d_model) != 0;
-  return (m->c.d_model == 192 || m->c.d_model == 256) && m->fuse_ln == 1;
-}
-// fuse_ln = 3: only the decoder's d x d producers (f-gate -> gate LayerNorm, source-attention
-// output -> LayerNorm 2) own whole rows; FFN2 (K = F) keeps its split-N GEMM + k_ln
-static bool fuse_ln_dd(const mnmt_model* m) {
-  return fuse_ln(m) || ((m->c.d_model == 192 || m->c.d_model == 256) && m->fuse_ln == 3);
-}
-
-static cudaError_t gemm_ln(mnmt_model* m, cudaStream_t st, const CUtensorMap& tmA, const Lin& W,
-                           int M, const int32_t* M_dyn, const LnArgs& ln) {
-  GemmArgs a{};
-  a.M = M;
-  a.M_dyn = M_dyn;
-  a.N = W.out;
-  a.K = W.in;
-  a.scale = scale_of(m);
-  a.bias = W.b;
-  a.clip = m->c.clip;
-  a.sigma = sigma_of(m);
-  a.ldo = W.out;
-  a.col_block = W.out;
-  a.ln = ln;
-  return launch_gemm_i8(tmA, W.tm, a, m->fuse_ln == 2 ? EPI_LNC : EPI_LN, 0, st);
 }
 
 static LnArgs ln_args(mnmt_model* m, const Workspace& w, int n, const int32_t* n_dyn, const float* x,
@@ -908,19 +854,12 @@ static cudaError_t launch_encoder(mnmt_model* m, Lane& Ln, int M, const int32_t*
     --*nlaunch;   // counted below with the layer's other kernels
     LnArgs la = ln_args(m, w, M, nullptr, w.x, w.o, E.ln1g, E.ln1b, w.x, w.cx);
     LnArgs lb = ln_args(m, w, M, nullptr, w.x, w.o, E.ln2g, E.ln2b, w.x, w.cx);
-    if (fuse_ln(m)) {
-      if ((e = gemm_ln(m, st, w.tm_cctx, E.o, M, nullptr, la)) != cudaSuccess) return e;
-      if ((e = gemm(m, st, w.tm_cx, E.f1, M, nullptr, EPI_RELU_Q, nullptr, w.ch, c.d_ffn)) != cudaSuccess) return e;
-      if ((e = gemm_ln(m, st, w.tm_ch, E.f2, M, nullptr, lb)) != cudaSuccess) return e;
-      *nlaunch += 5;
-    } else {
-      if ((e = gemm(m, st, w.tm_cctx, E.o, M, nullptr, EPI_F32, w.o, nullptr, d)) != cudaSuccess) return e;
-      if ((e = launch_ln(la, st)) != cudaSuccess) return e;
-      if ((e = gemm(m, st, w.tm_cx, E.f1, M, nullptr, EPI_RELU_Q, nullptr, w.ch, c.d_ffn)) != cudaSuccess) return e;
-      if ((e = gemm(m, st, w.tm_ch, E.f2, M, nullptr, EPI_F32, w.o, nullptr, d)) != cudaSuccess) return e;
-      if ((e = launch_ln(lb, st)) != cudaSuccess) return e;
-      *nlaunch += 7;
-    }
+    if ((e = gemm(m, st, w.tm_cctx, E.o, M, nullptr, EPI_F32, w.o, nullptr, d)) != cudaSuccess) return e;
+    if ((e = launch_ln(la, st)) != cudaSuccess) return e;
+    if ((e = gemm(m, st, w.tm_cx, E.f1, M, nullptr, EPI_RELU_Q, nullptr, w.ch, c.d_ffn)) != cudaSuccess) return e;
+    if ((e = gemm(m, st, w.tm_ch, E.f2, M, nullptr, EPI_F32, w.o, nullptr, d)) != cudaSuccess) return e;
+    if ((e = launch_ln(lb, st)) != cudaSuccess) return e;
+    *nlaunch += 7;
   }
   // Source keys/values of all decoder layers in one GEMM, scattered to [L][M_cap][2d].
   if ((e = gemm(m, st, w.tm_cx, m->kv_all, M, nullptr, EPI_F32, w.kv, nullptr, 2 * d, nullptr, 2 * d,
@@ -936,33 +875,33 @@ static cudaError_t launch_encoder(mnmt_model* m, Lane& Ln, int M, const int32_t*
   return cudaSuccess;
 }
 
-// Dump hook for teacher-forced runs (called between kernels; never inside a graph).
-struct StepHook {
-  virtual ~StepHook() = default;
-  virtual cudaError_t layer(mnmt_model* m, int l) = 0;   // after LN3 of layer l
-  virtual cudaError_t x1(mnmt_model* m, int l) = 0;
-  virtual cudaError_t x2(mnmt_model* m, int l) = 0;
-  virtual bool megakernel_ok() const { return false; }   // no per-layer dumps needed
-};
 
-// Fused per-row blocks for steps of <= m->rowfuse (padded) rows, when the shape fits them.
-static bool rowfuse_active(const mnmt_model* m, int n) {
-  const auto& c = m->c;
-  const int d = c.d_model, H = c.n_heads, dh = d / H;
-  const int nt = std::max(d, 32 * H);
-  return m->beam == 0 && m->rowfuse > 0 && n <= m->rowfuse && d % 32 == 0 && nt <= 1024 && dh <= 64 && dh % 4 == 0;
+static cudaError_t dump_rows(mnmt_model* m, Lane& Ln, int n, const void* src, bool codes,
+                             void* dst, int64_t slot, int64_t slots, int64_t* k) {
+  auto& w = Ln.ws;
+  DumpArgs a{};
+  a.n = n;
+  a.ctrl = w.ctrl;
+  a.live = w.live;
+  a.foff = w.forced_off;
+  a.d = m->c.d_model;
+  a.src = src;
+  a.elem = codes ? 1 : 4;
+  a.dst = dst;
+  a.slot = slot;
+  a.slots = slots;
+  ++*k;
+  return launch_dump_rows(a, Ln.st);
 }
 
 // One decoder step for up to `n` live rows (A5-A10).  Returns kernels launched via *nlaunch.
-// embed: launch A5 (k_embed_tgt) at the start (false: the previous step's k_finish did it);
-// fin_embed: k_finish embeds the next step's rows in the same CTA (greedy only).
-static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, StepHook* hook,
-                               int64_t* nlaunch, bool embed = true, bool fin_embed = false) {
+static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, int64_t* nlaunch) {
   auto& w = Ln.ws;
   cudaStream_t st = Ln.st;
   const auto& c = m->c;
   const int d = c.d_model, L = c.dec_layers, H = c.n_heads;
   const int32_t* nd = w.ctrl;  // ctrl[0] = live rows
+  const DevDump& dd = m->dump;
   cudaError_t e;
   int64_t k = 0;
   EmbedTgtArgs ea{};
@@ -977,206 +916,128 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
   ea.y = w.y;
   ea.yq = w.cy;
   ea.aan = aan_for_layer(m, w, 0);
-  if (embed) {
-    if ((e = launch_embed_tgt(ea, n, st)) != cudaSuccess) return e;
-    ++k;
-  }
+  if ((e = launch_embed_tgt(ea, n, st)) != cudaSuccess) return e;
+  ++k;
   for (int l = 0; l < L; ++l) {
     const DecLayer& D = m->dec[l];
-    // small live-row counts: the AAN block (A6) and the source-attention block (A7) as fused
-    // per-row kernels (rowfused.h) instead of 4-5 GEMMs and row kernels each
-    const bool rf = rowfuse_active(m, n);
-    if (rf && c.decoder == 1) {
-      AanBlockArgs ab{};
-      ab.n = n;
-      ab.n_dyn = nd;
-      ab.d = d;
-      ab.depth = c.aan_ffn_depth;
-      ab.gate = c.aan_gate;
-      ab.scale = scale_of(m);
-      ab.clip = c.clip;
-      ab.sigma = sigma_of(m);
-      ab.eps = c.ln_eps;
-      ab.y = w.y;
-      ab.yq = w.cy;
-      ab.g_f = w.g;
-      ab.g_q = w.cg;
-      ab.a1 = {D.a1.q4, D.a1.b};
-      ab.a2 = {D.a2.q4, D.a2.b};
-      ab.gi = {D.gi.q4, D.gi.b};
-      ab.gf = {D.gf.q4, D.gf.b};
-      ab.gamma = D.ln[0][0];
-      ab.beta = D.ln[0][1];
-      ab.x1 = w.x1;
-      ab.x1q = w.cx1;
-      if ((e = launch_aan_block(ab, st)) != cudaSuccess) return e;
-      ++k;
+    LnArgs l1;
+    if (c.decoder == 1) {
+      // A6: AAN block. g (or its codes) was produced with this layer's input.
+      const float* a_f = w.g;
+      // The i-gate GEMM needs only Q(y): it runs on a forked branch beside the AAN FFN.
+      // (measured: in-line is slower; the branch runs beside the AAN FFN)
+      const bool fork = c.aan_gate && c.aan_ffn_depth > 0;
+      if (fork) {
+        if ((e = cudaEventRecord(Ln.ev_fork, st)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(Ln.side, Ln.ev_fork, 0)) != cudaSuccess) return e;
+        if ((e = gemm(m, Ln.side, w.tm_cy, D.gi, n, nd, EPI_F32, w.gi, nullptr, d)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(Ln.ev_join, Ln.side)) != cudaSuccess) return e;
+      }
+      if (c.aan_ffn_depth == 2) {
+        if ((e = gemm_r(m, st, w.tm_cg, w.cg, D.a1, n, nd, EPI_RELU_Q, nullptr, w.ch1, d)) != cudaSuccess) return e;
+        if ((e = gemm_r(m, st, w.tm_ch1, w.ch1, D.a2, n, nd, EPI_F32_Q, w.a, w.ca, d)) != cudaSuccess) return e;
+        a_f = w.a;
+        k += 2;
+      } else if (c.aan_ffn_depth == 1) {
+        if ((e = gemm_r(m, st, w.tm_cg, w.cg, D.a1, n, nd, EPI_RELU_F32_Q, w.a, w.ca, d)) != cudaSuccess) return e;
+        a_f = w.a;
+        k += 1;
+      }
+      l1 = ln_args(m, w, n, nd, w.y, a_f, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
+      if (c.aan_gate) {
+        // gate (R8): logits W_i Q(y) + b_i and W_f Q(a) + b_f (for -ffn, Q(a) = Q(g));
+        // the sigmoids are applied in the gate-LayerNorm kernel
+        const CUtensorMap& tm_a = c.aan_ffn_depth == 0 ? w.tm_cg : w.tm_ca;
+        const int8_t* a_ptr = c.aan_ffn_depth == 0 ? w.cg : w.ca;
+        if (!fork) {
+          if ((e = gemm_r(m, st, w.tm_cy, w.cy, D.gi, n, nd, EPI_F32, w.gi, nullptr, d)) != cudaSuccess) return e;
+        }
+        if ((e = gemm_r(m, st, tm_a, a_ptr, D.gf, n, nd, EPI_F32, w.gf, nullptr, d)) != cudaSuccess) return e;
+        if (fork && (e = cudaStreamWaitEvent(st, Ln.ev_join, 0)) != cudaSuccess)
+          return e;   // join before the gate LayerNorm reads gi
+        l1.gi = w.gi;
+        l1.gf = w.gf;
+        k += 2;
+      }
     } else {
-      LnArgs l1;
-      bool l1_done = false;
-      if (c.decoder == 1) {
-        // A6: AAN block. g (or its codes) was produced with this layer's input.
-        const float* a_f = w.g;
-        // The i-gate GEMM needs only Q(y): it runs on a forked branch beside the AAN FFN.
-        // (measured: in-line is slower; the branch runs beside the AAN FFN)
-        const bool fork = c.aan_gate && c.aan_ffn_depth > 0 && !hook;
-        if (fork) {
-          if ((e = cudaEventRecord(Ln.ev_fork, st)) != cudaSuccess) return e;
-          if ((e = cudaStreamWaitEvent(Ln.side, Ln.ev_fork, 0)) != cudaSuccess) return e;
-          if ((e = gemm(m, Ln.side, w.tm_cy, D.gi, n, nd, EPI_F32, w.gi, nullptr, d)) != cudaSuccess) return e;
-          if ((e = cudaEventRecord(Ln.ev_join, Ln.side)) != cudaSuccess) return e;
-        }
-        if (c.aan_ffn_depth == 2) {
-          if ((e = gemm_r(m, st, w.tm_cg, w.cg, D.a1, n, nd, EPI_RELU_Q, nullptr, w.ch1, d)) != cudaSuccess) return e;
-          if ((e = gemm_r(m, st, w.tm_ch1, w.ch1, D.a2, n, nd, EPI_F32_Q, w.a, w.ca, d)) != cudaSuccess) return e;
-          a_f = w.a;
-          k += 2;
-        } else if (c.aan_ffn_depth == 1) {
-          if ((e = gemm_r(m, st, w.tm_cg, w.cg, D.a1, n, nd, EPI_RELU_F32_Q, w.a, w.ca, d)) != cudaSuccess) return e;
-          a_f = w.a;
-          k += 1;
-        }
-        if (c.aan_gate) {
-          // gate (R8): logits W_i Q(y) + b_i and W_f Q(a) + b_f (for -ffn, Q(a) = Q(g));
-          // the sigmoids are applied in the gate-LayerNorm kernel
-          const CUtensorMap& tm_a = c.aan_ffn_depth == 0 ? w.tm_cg : w.tm_ca;
-          const int8_t* a_ptr = c.aan_ffn_depth == 0 ? w.cg : w.ca;
-          if (!fork) {
-            if ((e = gemm_r(m, st, w.tm_cy, w.cy, D.gi, n, nd, EPI_F32, w.gi, nullptr, d)) != cudaSuccess) return e;
-          }
-          l1 = ln_args(m, w, n, nd, w.y, a_f, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
-          l1.gi = w.gi;
-          l1.gf = w.gf;
-          if (fuse_ln_dd(m)) {
-            // f-gate GEMM with the gate combine + LayerNorm in its epilogue (reads gi: join first)
-            if (fork && (e = cudaStreamWaitEvent(st, Ln.ev_join, 0)) != cudaSuccess) return e;
-            if ((e = gemm_ln(m, st, tm_a, D.gf, n, nd, l1)) != cudaSuccess) return e;
-            l1_done = true;
-          } else {
-            if ((e = gemm_r(m, st, tm_a, a_ptr, D.gf, n, nd, EPI_F32, w.gf, nullptr, d)) != cudaSuccess) return e;
-          }
-          if (fork && !fuse_ln_dd(m) && (e = cudaStreamWaitEvent(st, Ln.ev_join, 0)) != cudaSuccess)
-            return e;   // join before the gate LayerNorm reads gi
-          k += 2;
-        } else {
-          l1 = ln_args(m, w, n, nd, w.y, a_f, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
-        }
-      } else {
-        // A6': self-attention with a KV cache
-        if ((e = gemm_r(m, st, w.tm_cy, w.cy, D.qkv, n, nd, EPI_F32, w.qkvd, nullptr, 3 * d)) != cudaSuccess) return e;
-        AttnArgs at{};
-        at.mode = ATTN_SELF;
-        at.span = Ln.span_cap;
-        at.n = n;
-        at.n_dyn = nd;
-        at.ctrl = w.ctrl;
-        at.live = w.live;
-        at.H = H;
-        at.dh = d / H;
-        at.d = d;
-        at.q = w.qkvd;
-        at.ldq = 3 * d;
-        at.kv = w.selfkv + (int64_t)l * w.B_cap * w.T_cap * 2 * d;
-        at.kv_w = const_cast<float*>(at.kv);
-        at.ldkv = 2 * d;
-        at.k_off = 0;
-        at.v_off = d;
-        at.t_cap = (int)w.T_cap;
-        at.anc = m->beam > 0 ? w.anc : nullptr;
-        at.clip = c.clip;
-        at.sigma = sigma_of(m);
-        at.out_q = w.cctxd;
-        if ((e = launch_attn(at, st)) != cudaSuccess) return e;
-        if ((e = gemm_r(m, st, w.tm_cctxd, w.cctxd, D.o, n, nd, EPI_F32, w.od, nullptr, d)) != cudaSuccess) return e;
-        k += 3;
-        l1 = ln_args(m, w, n, nd, w.y, w.od, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
-      }
-      if (!l1_done) {
-        if ((e = launch_ln(l1, st)) != cudaSuccess) return e;
-        ++k;
-      }
+      // A6': self-attention with a KV cache
+      if ((e = gemm_r(m, st, w.tm_cy, w.cy, D.qkv, n, nd, EPI_F32, w.qkvd, nullptr, 3 * d)) != cudaSuccess) return e;
+      AttnArgs at{};
+      at.mode = ATTN_SELF;
+      at.span = Ln.span_cap;
+      at.n = n;
+      at.n_dyn = nd;
+      at.ctrl = w.ctrl;
+      at.live = w.live;
+      at.H = H;
+      at.dh = d / H;
+      at.d = d;
+      at.q = w.qkvd;
+      at.ldq = 3 * d;
+      at.kv = w.selfkv + (int64_t)l * w.B_cap * w.T_cap * 2 * d;
+      at.kv_w = const_cast<float*>(at.kv);
+      at.ldkv = 2 * d;
+      at.k_off = 0;
+      at.v_off = d;
+      at.t_cap = (int)w.T_cap;
+      at.anc = m->beam > 0 ? w.anc : nullptr;
+      at.clip = c.clip;
+      at.sigma = sigma_of(m);
+      at.out_q = w.cctxd;
+      if ((e = launch_attn(at, st)) != cudaSuccess) return e;
+      if ((e = gemm_r(m, st, w.tm_cctxd, w.cctxd, D.o, n, nd, EPI_F32, w.od, nullptr, d)) != cudaSuccess) return e;
+      k += 3;
+      l1 = ln_args(m, w, n, nd, w.y, w.od, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
     }
-    if (hook && (e = hook->x1(m, l)) != cudaSuccess) return e;
-    if (rf) {
-      SrcBlockArgs sb{};
-      sb.n = n;
-      sb.n_dyn = nd;
-      sb.d = d;
-      sb.H = H;
-      sb.span = Ln.span_cap;
-      sb.scale = scale_of(m);
-      sb.clip = c.clip;
-      sb.sigma = sigma_of(m);
-      sb.eps = c.ln_eps;
-      sb.x1 = w.x1;
-      sb.x1q = w.cx1;
-      sb.sq = {D.sq.q4, D.sq.b};
-      sb.so = {D.so.q4, D.so.b};
-      sb.kv = w.kv + (int64_t)l * w.M_cap * 2 * d;
-      sb.ldkv = 2 * d;
-      sb.k_off = 0;
-      sb.v_off = d;
-      sb.live_start = w.live_start;
-      sb.live_len = w.live_len;
-      sb.gamma = D.ln[1][0];
-      sb.beta = D.ln[1][1];
-      sb.x2 = w.x2;
-      sb.x2q = w.cx2;
-      if ((e = launch_src_block(sb, st)) != cudaSuccess) return e;
-      ++k;
-    } else {
-      // A7: source attention
-      if ((e = gemm_r(m, st, w.tm_cx1, w.cx1, D.sq, n, nd, EPI_F32, w.qs, nullptr, d)) != cudaSuccess) return e;
-      AttnArgs as{};
-      as.mode = ATTN_SRC;
-      as.span = Ln.span_cap;
-      as.n = n;
-      as.n_dyn = nd;
-      as.ctrl = w.ctrl;
-      as.live = w.live;
-      as.H = H;
-      as.dh = d / H;
-      as.d = d;
-      as.q = w.qs;
-      as.ldq = d;
-      as.kv = w.kv + (int64_t)l * w.M_cap * 2 * d;
-      as.kv16 = c.src_kv_bf16 ? w.kv16 + (int64_t)l * w.M_cap * 2 * d : nullptr;
-      as.ldkv = 2 * d;
-      as.k_off = 0;
-      as.v_off = d;
-      as.kv_start = w.row_start;
-      as.kv_len = w.row_len;
-      as.live_start = w.live_start;
-      as.live_len = w.live_len;
-      as.clip = c.clip;
-      as.sigma = sigma_of(m);
-      as.out_q = w.cctxd;
-      if ((e = launch_attn(as, st)) != cudaSuccess) return e;
-      LnArgs l2 = ln_args(m, w, n, nd, w.x1, w.od, D.ln[1][0], D.ln[1][1], w.x2, w.cx2);
-      if (fuse_ln_dd(m)) {
-        if ((e = gemm_ln(m, st, w.tm_cctxd, D.so, n, nd, l2)) != cudaSuccess) return e;
-        k += 3;
-      } else {
-        if ((e = gemm_r(m, st, w.tm_cctxd, w.cctxd, D.so, n, nd, EPI_F32, w.od, nullptr, d)) != cudaSuccess) return e;
-        if ((e = launch_ln(l2, st)) != cudaSuccess) return e;
-        k += 4;
-      }
-    }
-    if (hook && (e = hook->x2(m, l)) != cudaSuccess) return e;
+    if ((e = launch_ln(l1, st)) != cudaSuccess) return e;
+    ++k;
+    if (dd.layers && (e = dump_rows(m, Ln, n, w.x1, false, dd.layers, 3 * l + 0, 3 * L, &k)) != cudaSuccess)
+      return e;
+    // A7: source attention
+    if ((e = gemm_r(m, st, w.tm_cx1, w.cx1, D.sq, n, nd, EPI_F32, w.qs, nullptr, d)) != cudaSuccess) return e;
+    AttnArgs as{};
+    as.mode = ATTN_SRC;
+    as.span = Ln.span_cap;
+    as.n = n;
+    as.n_dyn = nd;
+    as.ctrl = w.ctrl;
+    as.live = w.live;
+    as.H = H;
+    as.dh = d / H;
+    as.d = d;
+    as.q = w.qs;
+    as.ldq = d;
+    as.kv = w.kv + (int64_t)l * w.M_cap * 2 * d;
+    as.kv16 = c.src_kv_bf16 ? w.kv16 + (int64_t)l * w.M_cap * 2 * d : nullptr;
+    as.ldkv = 2 * d;
+    as.k_off = 0;
+    as.v_off = d;
+    as.kv_start = w.row_start;
+    as.kv_len = w.row_len;
+    as.live_start = w.live_start;
+    as.live_len = w.live_len;
+    as.clip = c.clip;
+    as.sigma = sigma_of(m);
+    as.out_q = w.cctxd;
+    if ((e = launch_attn(as, st)) != cudaSuccess) return e;
+    LnArgs l2 = ln_args(m, w, n, nd, w.x1, w.od, D.ln[1][0], D.ln[1][1], w.x2, w.cx2);
+    if ((e = gemm_r(m, st, w.tm_cctxd, w.cctxd, D.so, n, nd, EPI_F32, w.od, nullptr, d)) != cudaSuccess) return e;
+    if ((e = launch_ln(l2, st)) != cudaSuccess) return e;
+    k += 4;
+    if (dd.layers && (e = dump_rows(m, Ln, n, w.x2, false, dd.layers, 3 * l + 1, 3 * L, &k)) != cudaSuccess)
+      return e;
     // A8: FFN
     if ((e = gemm_r(m, st, w.tm_cx2, w.cx2, D.f1, n, nd, EPI_RELU_Q, nullptr, w.chd, c.d_ffn)) != cudaSuccess) return e;
     LnArgs l3 = ln_args(m, w, n, nd, w.x2, w.f, D.ln[2][0], D.ln[2][1], w.y, w.cy);
     l3.aan = aan_for_layer(m, w, l + 1);
-    if (fuse_ln(m)) {
-      if ((e = gemm_ln(m, st, w.tm_chd, D.f2, n, nd, l3)) != cudaSuccess) return e;
-      k += 2;
-    } else {
-      if ((e = gemm_r(m, st, w.tm_chd, w.chd, D.f2, n, nd, EPI_F32, w.f, nullptr, d)) != cudaSuccess) return e;
-      if ((e = launch_ln(l3, st)) != cudaSuccess) return e;
-      k += 3;
-    }
-    if (hook && (e = hook->layer(m, l)) != cudaSuccess) return e;
+    if ((e = gemm_r(m, st, w.tm_chd, w.chd, D.f2, n, nd, EPI_F32, w.f, nullptr, d)) != cudaSuccess) return e;
+    if ((e = launch_ln(l3, st)) != cudaSuccess) return e;
+    k += 3;
+    if (dd.layers && (e = dump_rows(m, Ln, n, w.y, false, dd.layers, 3 * l + 2, 3 * L, &k)) != cudaSuccess)
+      return e;
   }
+  if (dd.dec_out && (e = dump_rows(m, Ln, n, w.y, false, dd.dec_out, 0, 1, &k)) != cudaSuccess) return e;
+  if (dd.out_codes && (e = dump_rows(m, Ln, n, w.cy, true, dd.out_codes, 0, 1, &k)) != cudaSuccess) return e;
   if (m->beam > 0) {
     // beam search (F1): output GEMM with per-tile log-sum-exp partials and top-k (EPI_TOPK),
     // then row merge, per-sentence selection + compaction, state reorder (beam.h)
@@ -1225,8 +1086,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
     a.sigma = sigma_of(m);
     a.col_block = a.N;
     a.keys = w.keys;
-    static const bool sl_nomask = getenv("MNMT_SL_NOMASK") != nullptr;   // A/B only (wrong ids
-    if (sl && !sl_nomask) {                                                // unless 1 group)
+    if (sl) {
       a.colbits = w.sl_bits;
       a.colbits_ld = (c.vocab + 31) / 32;
       a.row_grp = w.sl_rgrp;
@@ -1248,7 +1108,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
   fa.out_len = m->jb.out_len;
   fa.len_idx = w.len_idx;
   fa.eos = c.eos_id;
-  fa.forced = forced ? w.forced : nullptr;
+  fa.forced = forced ? m->jb.forced : nullptr;
   fa.forced_off = forced ? w.forced_off : nullptr;
   fa.prev_live = w.prev_live;
   fa.row_start = w.row_start;
@@ -1256,259 +1116,10 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, Step
   fa.live_start = w.live_start;
   fa.live_len = w.live_len;
   fa.id_map = Ln.sl_n > 0 ? w.sl_map : nullptr;
-  if (fin_embed) {
-    fa.emb = ea;
-    fa.emb.n = n;
-  }
   if ((e = launch_finish(fa, st)) != cudaSuccess) return e;
   k += 2;
   *nlaunch += k;
   return cudaSuccess;
-}
-
-// ------------------------------------------------------------------ step program
-// The phase list of one decoder step (A5-A10) for the persistent step kernel.  It issues
-// exactly the operations of launch_step, in the same order, with the same arguments.
-struct ProgBuilder {
-  std::vector<Phase> ph;
-  std::vector<CUtensorMap> maps;
-  std::vector<std::array<int, 4>> fix;   // {phase, prob, mapA, mapB}
-  int map(const CUtensorMap& t) {
-    maps.push_back(t);
-    return (int)maps.size() - 1;
-  }
-};
-
-static GemmProb gprob(mnmt_model* m, ProgBuilder& pb, int phase, int prob,
-                      const CUtensorMap& tmA, const CUtensorMap& tmB, int N, int K,
-                      const float* bias, int M, const int32_t* M_dyn, int epi, float* out_f,
-                      int8_t* out_q, int64_t ldo, unsigned long long* keys = nullptr) {
-  GemmProb g{};
-  g.a.M = M;
-  g.a.M_dyn = M_dyn;
-  g.a.N = N;
-  g.a.K = K;
-  g.a.scale = scale_of(m);
-  g.a.bias = bias;
-  g.a.clip = m->c.clip;
-  g.a.sigma = sigma_of(m);
-  g.a.out_f = out_f;
-  g.a.out_q = out_q;
-  g.a.ldo = ldo;
-  g.a.col_block = N;
-  g.a.block_stride = 0;
-  g.a.keys = keys;
-  g.epi = epi;
-  g.bn = N >= 8192 ? 256 : (N >= 2048 ? 128 : 64);
-  g.n_tiles = (N + g.bn - 1) / g.bn;
-  pb.fix.push_back({phase, prob, pb.map(tmA), pb.map(tmB)});
-  return g;
-}
-
-static mnmt_status build_program(mnmt_model* m, Lane& Ln, bool forced) {
-  const auto& c = m->c;
-  auto& w = Ln.ws;
-  const int d = c.d_model, L = c.dec_layers, H = c.n_heads;
-  const int n = (int)w.B_cap;
-  const int32_t* nd = w.ctrl;
-  ProgBuilder pb;
-  auto gemm1 = [&](const CUtensorMap& tmA, const Lin& W, int epi, float* of, int8_t* oq, int64_t ldo) {
-    Phase P{};
-    P.type = PH_GEMM;
-    P.nprob = 1;
-    const int idx = (int)pb.ph.size();
-    P.g[0] = gprob(m, pb, idx, 0, tmA, W.tm, W.out, W.in, W.b, n, nd, epi, of, oq, ldo);
-    pb.ph.push_back(P);
-  };
-  auto gemm2 = [&](const CUtensorMap& tA0, const Lin& W0, int e0, float* f0, int8_t* q0,
-                   const CUtensorMap& tA1, const Lin& W1, int e1, float* f1, int8_t* q1) {
-    Phase P{};
-    P.type = PH_GEMM;
-    P.nprob = 2;
-    const int idx = (int)pb.ph.size();
-    P.g[0] = gprob(m, pb, idx, 0, tA0, W0.tm, W0.out, W0.in, W0.b, n, nd, e0, f0, q0, W0.out);
-    P.g[1] = gprob(m, pb, idx, 1, tA1, W1.tm, W1.out, W1.in, W1.b, n, nd, e1, f1, q1, W1.out);
-    pb.ph.push_back(P);
-  };
-  auto ln = [&](const LnArgs& a) {
-    Phase P{};
-    P.type = PH_LN;
-    P.ln = a;
-    pb.ph.push_back(P);
-  };
-  {
-    Phase P{};
-    P.type = PH_EMBED;
-    P.em.ctrl = w.ctrl;
-    P.em.live = w.live;
-    P.em.prev_id = w.prev_id;
-    P.em.E = m->E;
-    P.em.PE = m->PE;
-    P.em.d = d;
-    P.em.rsd = (float)std::sqrt((double)d);
-    P.em.y = w.y;
-    P.em.yq = w.cy;
-    P.em.aan = aan_for_layer(m, w, 0);
-    pb.ph.push_back(P);
-  }
-  for (int l = 0; l < L; ++l) {
-    const DecLayer& D = m->dec[l];
-    LnArgs l1;
-    if (c.decoder == 1) {
-      const float* a_f = w.g;
-      const CUtensorMap& tm_a = c.aan_ffn_depth == 0 ? w.tm_cg : w.tm_ca;
-      if (c.aan_ffn_depth == 2) {
-        if (c.aan_gate)
-          gemm2(w.tm_cg, D.a1, EPI_RELU_Q, nullptr, w.ch1, w.tm_cy, D.gi, EPI_F32, w.gi, nullptr);
-        else
-          gemm1(w.tm_cg, D.a1, EPI_RELU_Q, nullptr, w.ch1, d);
-        gemm1(w.tm_ch1, D.a2, EPI_F32_Q, w.a, w.ca, d);
-        a_f = w.a;
-        if (c.aan_gate) gemm1(tm_a, D.gf, EPI_F32, w.gf, nullptr, d);
-      } else if (c.aan_ffn_depth == 1) {
-        if (c.aan_gate)
-          gemm2(w.tm_cg, D.a1, EPI_RELU_F32_Q, w.a, w.ca, w.tm_cy, D.gi, EPI_F32, w.gi, nullptr);
-        else
-          gemm1(w.tm_cg, D.a1, EPI_RELU_F32_Q, w.a, w.ca, d);
-        a_f = w.a;
-        if (c.aan_gate) gemm1(tm_a, D.gf, EPI_F32, w.gf, nullptr, d);
-      } else if (c.aan_gate) {
-        gemm2(w.tm_cy, D.gi, EPI_F32, w.gi, nullptr, tm_a, D.gf, EPI_F32, w.gf, nullptr);
-      }
-      l1 = ln_args(m, w, n, nd, w.y, a_f, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
-      if (c.aan_gate) {
-        l1.gi = w.gi;
-        l1.gf = w.gf;
-      }
-    } else {
-      gemm1(w.tm_cy, D.qkv, EPI_F32, w.qkvd, nullptr, 3 * d);
-      Phase P{};
-      P.type = PH_ATTN;
-      AttnArgs& at = P.at;
-      at.mode = ATTN_SELF;
-      at.span = Ln.span_cap;
-      at.n = n;
-      at.n_dyn = nd;
-      at.ctrl = w.ctrl;
-      at.live = w.live;
-      at.H = H;
-      at.dh = d / H;
-      at.d = d;
-      at.q = w.qkvd;
-      at.ldq = 3 * d;
-      at.kv = w.selfkv + (int64_t)l * w.B_cap * w.T_cap * 2 * d;
-      at.kv_w = const_cast<float*>(at.kv);
-      at.ldkv = 2 * d;
-      at.k_off = 0;
-      at.v_off = d;
-      at.t_cap = (int)w.T_cap;
-      at.clip = c.clip;
-      at.sigma = sigma_of(m);
-      at.out_q = w.cctxd;
-      pb.ph.push_back(P);
-      gemm1(w.tm_cctxd, D.o, EPI_F32, w.od, nullptr, d);
-      l1 = ln_args(m, w, n, nd, w.y, w.od, D.ln[0][0], D.ln[0][1], w.x1, w.cx1);
-    }
-    ln(l1);
-    gemm1(w.tm_cx1, D.sq, EPI_F32, w.qs, nullptr, d);
-    {
-      Phase P{};
-      P.type = PH_ATTN;
-      AttnArgs& as = P.at;
-      as.mode = ATTN_SRC;
-      as.n = n;
-      as.n_dyn = nd;
-      as.ctrl = w.ctrl;
-      as.live = w.live;
-      as.H = H;
-      as.dh = d / H;
-      as.d = d;
-      as.q = w.qs;
-      as.ldq = d;
-      as.kv = w.kv + (int64_t)l * w.M_cap * 2 * d;
-      as.kv16 = c.src_kv_bf16 ? w.kv16 + (int64_t)l * w.M_cap * 2 * d : nullptr;
-      as.ldkv = 2 * d;
-      as.k_off = 0;
-      as.v_off = d;
-      as.kv_start = w.row_start;
-      as.kv_len = w.row_len;
-      as.clip = c.clip;
-      as.sigma = sigma_of(m);
-      as.out_q = w.cctxd;
-      pb.ph.push_back(P);
-    }
-    gemm1(w.tm_cctxd, D.so, EPI_F32, w.od, nullptr, d);
-    ln(ln_args(m, w, n, nd, w.x1, w.od, D.ln[1][0], D.ln[1][1], w.x2, w.cx2));
-    gemm1(w.tm_cx2, D.f1, EPI_RELU_Q, nullptr, w.chd, c.d_ffn);
-    gemm1(w.tm_chd, D.f2, EPI_F32, w.f, nullptr, d);
-    LnArgs l3 = ln_args(m, w, n, nd, w.x2, w.f, D.ln[2][0], D.ln[2][1], w.y, w.cy);
-    l3.aan = aan_for_layer(m, w, l + 1);
-    ln(l3);
-  }
-  {
-    Phase P{};
-    P.type = PH_GEMM;
-    P.nprob = 1;
-    const int idx = (int)pb.ph.size();
-    P.g[0] = gprob(m, pb, idx, 0, w.tm_cy, m->tmE, c.vocab, d, c.out_bias ? m->out_b : nullptr, n,
-                   nd, EPI_ARGMAX, nullptr, nullptr, 0, w.keys);
-    pb.ph.push_back(P);
-  }
-  {
-    Phase P{};
-    P.type = PH_FINISH;
-    FinishArgs& fa = P.fi;
-    fa.ctrl = w.ctrl;
-    fa.live = w.live;
-    fa.keys = w.keys;
-    fa.prev_id = w.prev_id;
-    fa.max_len = w.max_len;
-    fa.out_off = w.out_off;
-    fa.out_ids = m->jb.out_ids;
-    fa.out_len = m->jb.out_len;
-    fa.len_idx = w.len_idx;
-    fa.eos = c.eos_id;
-    fa.forced = forced ? w.forced : nullptr;
-    fa.forced_off = forced ? w.forced_off : nullptr;
-    pb.ph.push_back(P);
-  }
-  // Row-local chain: GEMMs (except the output layer), LayerNorms and the embedding run on
-  // the CTA that owns the 128-row tile; only attention, the output layer and the finish are
-  // spread over the grid.  A grid barrier is needed after a phase iff it or its successor
-  // is grid-wide (or the option is off).
-  for (size_t i = 0; i < pb.ph.size(); ++i) {
-    Phase& P = pb.ph[i];
-    const bool vocab_gemm = P.type == PH_GEMM && P.g[0].epi == EPI_ARGMAX;
-    P.rowlocal = m->rowlocal && (P.type == PH_EMBED || P.type == PH_LN ||
-                                 (P.type == PH_GEMM && !vocab_gemm)) ? 1 : 0;
-  }
-  for (size_t i = 0; i < pb.ph.size(); ++i) {
-    const bool next_local = i + 1 < pb.ph.size() && pb.ph[i + 1].rowlocal;
-    pb.ph[i].sync_grid = (pb.ph[i].rowlocal && next_local) ? 0 : 1;
-  }
-  // upload: tensor maps first, then phases with their device addresses patched in
-  if (Ln.d_phases) cudaFree(Ln.d_phases);
-  if (Ln.d_tmaps) cudaFree(Ln.d_tmaps);
-  Ln.d_phases = nullptr;
-  Ln.d_tmaps = nullptr;
-  CK(cudaMalloc(&Ln.d_tmaps, pb.maps.size() * sizeof(CUtensorMap)));
-  CK(cudaMemcpy(Ln.d_tmaps, pb.maps.data(), pb.maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
-  for (const auto& f : pb.fix) {
-    pb.ph[f[0]].g[f[1]].tmA = Ln.d_tmaps + f[2];
-    pb.ph[f[0]].g[f[1]].tmB = Ln.d_tmaps + f[3];
-  }
-  CK(cudaMalloc(&Ln.d_phases, pb.ph.size() * sizeof(Phase)));
-  CK(cudaMemcpy(Ln.d_phases, pb.ph.data(), pb.ph.size() * sizeof(Phase), cudaMemcpyHostToDevice));
-  if (!Ln.d_bar) {
-    CK(cudaMalloc(&Ln.d_bar, 64 * sizeof(unsigned)));
-    CK(cudaMemset(Ln.d_bar, 0, 64 * sizeof(unsigned)));
-  }
-  Ln.n_phases = (int)pb.ph.size();
-  Ln.phase_types.clear();
-  for (const Phase& P : pb.ph) Ln.phase_types.push_back(P.type);
-  Ln.prog_forced = forced;
-  Ln.prog_out = m->jb.out_ids;
-  return MNMT_OK;
 }
 
 // ------------------------------------------------------------------ job planning
@@ -1670,8 +1281,7 @@ static mnmt_status upload_job(mnmt_model* m, const Job& job) {
   return MNMT_OK;
 }
 
-static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook* hook,
-                           bool use_graphs) {
+static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced) {
   const auto& c = m->c;
   const int64_t d = c.d_model;
   int64_t launches = 0, steps = 0;
@@ -1744,90 +1354,44 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced, StepHook*
     }
     // per-step row bound: rows are compacted to the front and a row never outlives its
     // max_len, so step t needs at most alive[t-1] rows -> the smallest cached graph that fits
-    // (with rowfuse: multiples of 16 below 128 rows, so the fused blocks can key on the row count;
-    // otherwise 128, measured 0.5 % faster)
+    // (128-row multiples; the small-M GEMM bound below that)
     const int rows_per = std::max(1, m->beam);   // beam search: up to beam rows per sentence
     auto pad_at = [&](int t) {
       const int a = b.alive[t] * rows_per;
-      if (a <= gemm_smallm() && m->beam == 0 && !(m->rowfuse > 0)) return gemm_smallm();   // small-M GEMMs
-      return (a < 128 && m->rowfuse > 0) ? std::max(16, (a + 15) / 16 * 16) : (a + 127) / 128 * 128;
+      if (a <= m->smallm && m->beam == 0) return m->smallm;   // small-M GEMMs
+      return (a + 127) / 128 * 128;
     };
-    if (m->megakernel && m->beam == 0 && Ln.sl_n == 0 && (!hook || hook->megakernel_ok())) {
-      if (!Ln.d_phases || Ln.prog_forced != forced || Ln.prog_out != m->jb.out_ids)
-        CKS(build_program(m, Ln, forced));
-      StepArgs sa{};
-      sa.cluster = (m->mk_cluster && m->mk_ctas > 0 && m->mk_ctas <= 16) ? 1 : 0;
-      sa.phases = Ln.d_phases;
-      sa.n_phases = Ln.n_phases;
-      sa.ctrl = w.ctrl;
-      sa.bar = Ln.d_bar;
-      if (m->profile_phases && b.lane == 0 && !hook) {
-        const int64_t need = (int64_t)b.T * (Ln.n_phases + 1);
-        if (Ln.timing_steps < b.T) {
-          if (Ln.d_timing) cudaFree(Ln.d_timing);
-          CK(cudaMalloc(&Ln.d_timing, need * sizeof(unsigned long long)));
-          Ln.timing_steps = b.T;
+    // k consecutive steps per graph (PDL chains the kernels inside a graph, not across graph
+    // launches), sized for the first step's row bound (rows only decrease)
+    const int K = std::max(1, m->steps_per_graph);
+    for (int t = 0; t < b.T;) {
+      const int np = pad_at(t), k = std::min(K, b.T - t);
+      const int64_t key = ((((int64_t)np * 64 + k) * 16 + m->beam) * ((int64_t)c.vocab + 1) + Ln.sl_n) * 2 +
+                          (m->dump.any() ? 1 : 0);
+      auto it = Ln.graphs.find(key);
+      if (it == Ln.graphs.end()) {
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        int64_t per_step = 0;
+        cudaError_t e = cudaSuccess;
+        for (int u = 0; u < k && e == cudaSuccess; ++u) e = launch_step(m, Ln, np, forced, &per_step);
+        cudaError_t e2 = cudaStreamEndCapture(st, &g);
+        CK(e);
+        CK(e2);
+        cudaGraphExec_t ge;
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        cudaGraphDestroy(g);
+        if (Ln.graphs.size() >= 2048) {   // bound the cache (shortlist sizes vary per batch)
+          CK(cudaStreamSynchronize(st));
+          for (auto& kv : Ln.graphs) cudaGraphExecDestroy(kv.second);
+          Ln.graphs.clear();
         }
-        CK(cudaMemsetAsync(Ln.d_timing, 0, need * sizeof(unsigned long long), st));
-        sa.timing = Ln.d_timing;
+        it = Ln.graphs.emplace(key, ge).first;
+        Ln.graph_launches[key] = per_step;
       }
-      if (!hook) {
-        sa.max_steps = b.T;
-        CK(launch_step_kernel(sa, (int)d, st, m->mk_ctas));
-        launches += 1;
-      } else {
-        sa.max_steps = 1;
-        for (int t = 0; t < b.T; ++t) {
-          CK(launch_step_kernel(sa, (int)d, st, m->mk_ctas));
-          launches += 1;
-        }
-      }
-    } else if (use_graphs && !hook) {
-      // k consecutive steps per graph (PDL chains the kernels inside a graph, not across
-      // graph launches), sized for the first step's row bound (rows only decrease)
-      // fin_embed: at row bounds <= m->fin_embed the step's k_finish also embeds the next
-      // step's rows (rows only decrease, so every later graph of the batch does too), and a
-      // graph whose predecessor did so starts without k_embed_tgt
-      const int K = std::max(1, m->steps_per_graph);
-      bool prev_fused = false;
-      for (int t = 0; t < b.T;) {
-        const int np = pad_at(t), k = std::min(K, b.T - t);
-        const bool fuse = m->beam == 0 && np <= m->fin_embed;
-        const bool first_embed = !prev_fused;
-        const int64_t key =
-            ((((int64_t)np * 64 + k) * 16 + m->beam) * ((int64_t)c.vocab + 1) + Ln.sl_n) * 4 +
-            (fuse ? 2 : 0) + (first_embed ? 1 : 0);
-        auto it = Ln.graphs.find(key);
-        if (it == Ln.graphs.end()) {
-          cudaGraph_t g;
-          CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-          int64_t per_step = 0;
-          cudaError_t e = cudaSuccess;
-          for (int u = 0; u < k && e == cudaSuccess; ++u)
-            e = launch_step(m, Ln, np, forced, nullptr, &per_step, u == 0 ? first_embed : !fuse, fuse);
-          cudaError_t e2 = cudaStreamEndCapture(st, &g);
-          CK(e);
-          CK(e2);
-          cudaGraphExec_t ge;
-          CK(cudaGraphInstantiate(&ge, g, 0));
-          cudaGraphDestroy(g);
-          if (Ln.graphs.size() >= 2048) {   // bound the cache (shortlist sizes vary per batch)
-            CK(cudaStreamSynchronize(st));
-            for (auto& kv : Ln.graphs) cudaGraphExecDestroy(kv.second);
-            Ln.graphs.clear();
-          }
-          it = Ln.graphs.emplace(key, ge).first;
-          Ln.graph_launches[key] = per_step;
-        }
-        CK(cudaGraphLaunch(it->second, st));
-        launches += Ln.graph_launches[key];
-        prev_fused = fuse;
-        t += k;
-      }
-    } else {
-      const int nrows = (B * rows_per <= gemm_smallm() && m->beam == 0 && !(m->rowfuse > 0))
-                            ? gemm_smallm() : (B * rows_per + 127) / 128 * 128;
-      for (int t = 0; t < b.T; ++t) CK(launch_step(m, Ln, nrows, forced, hook, &launches));
+      CK(cudaGraphLaunch(it->second, st));
+      launches += Ln.graph_launches[key];
+      t += k;
     }
     if (m->beam > 0) {
       CK(launch_beam_final(beam_args(m, Ln, B), B, st));
@@ -1931,8 +1495,6 @@ mnmt_status mnmt_model_create(const mnmt_config* cfg, int32_t cuda_device, mnmt_
     DeviceGuard g0(cuda_device);
     cudaError_t e = gemm_init();
     if (e == cudaSuccess) e = attn_init();
-    if (e == cudaSuccess) e = rowfused_init();
-    if (e == cudaSuccess && step_kernel_grid() <= 0) e = cudaErrorInvalidConfiguration;
     if (e != cudaSuccess) {
       set_err("kernel init failed: %s", cudaGetErrorString(e));
       return MNMT_ERR_CUDA;
@@ -2033,8 +1595,6 @@ mnmt_status mnmt_model_quantize(mnmt_model* m) {
     }
     if ((s = prep_lin(m, D.sq, {p + "src.q"}, d, d, tmp)) != MNMT_OK) return done(s);
     if ((s = prep_lin(m, D.so, {p + "src.o"}, d, d, tmp)) != MNMT_OK) return done(s);
-    for (Lin* L : {&D.a1, &D.a2, &D.gi, &D.gf, &D.sq, &D.so})
-      if (L->q && (s = prep_k4(m, *L)) != MNMT_OK) return done(s);
     if ((s = prep_lin(m, D.f1, {p + "ffn.1"}, F, d, tmp)) != MNMT_OK) return done(s);
     if ((s = prep_lin(m, D.f2, {p + "ffn.2"}, d, F, tmp)) != MNMT_OK) return done(s);
     for (int i = 0; i < 3; ++i) {
@@ -2081,13 +1641,23 @@ mnmt_status mnmt_batch_by_words(const int32_t* len, int32_t n, int32_t budget, i
   return MNMT_OK;
 }
 
+// Teacher forcing (test hook of the parity protocol): sentence i runs T_i steps with the
+// given input ids; dumps as in mnmt.h.
+struct Forced {
+  const int32_t* ids;
+  const int64_t* off;
+  uint32_t dump_mask;
+  void* dump_host;
+};
+
 static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const int64_t* src_off,
                                   int32_t n, const int32_t* max_len, int32_t budget,
                                   bool sorted_batches, int32_t* out_ids, int64_t out_cap,
                                   int32_t* out_len, uint32_t flags, void* cuda_stream,
                                   int32_t beam = 0, float* out_score = nullptr,
-                                  int32_t* n_hyp = nullptr) {
+                                  int32_t* n_hyp = nullptr, const Forced* fz = nullptr) {
   if (!m) { set_err("NULL model"); return MNMT_ERR_ARG; }
+  const bool forced = fz != nullptr;   // teacher forcing: max_len[i] = T_i, no EOS stop
   mnmt_status s;
   if ((s = check_inputs(m, src_off, n, max_len)) != MNMT_OK) return s;
   if (beam < 0 || beam > TOPK_MAX || beam > m->c.vocab) {
@@ -2185,7 +1755,7 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
   }
   Job job;
   plan_job(src_off, n, max_len, rows, lanes_of, (int)m->lanes.size(), job, use_sl ? &wave_of : nullptr);
-  plan_rows(job, src_off, max_len, false, nullptr);
+  plan_rows(job, src_off, max_len, forced, forced ? fz->off : nullptr);
   std::vector<int32_t> rgrp;
   if (use_sl) {
     rgrp.assign(job.rows_total, 0);
@@ -2226,7 +1796,69 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
     CK(cudaMemsetAsync(w.n_hyp, 0, (size_t)n * 4, m->st));
     CK(cudaMemsetAsync(w.out_score, 0, (size_t)n * bm * 4, m->st));
   }
-  if ((s = run_job(m, job, false, nullptr, true)) != MNMT_OK) return fail(m, s);
+  if (forced && O > 0) {
+    CK(cudaMemcpyAsync(w.forced, fz->ids, O * 4, cudaMemcpyHostToDevice, m->st));
+    m->stats.h2d_bytes += O * 4;
+  }
+  // device dumps of a teacher-forced run: written inside the step graphs, copied out below
+  struct DumpReset {
+    mnmt_model* m;
+    std::vector<void*> bufs;
+    ~DumpReset() {
+      if (bufs.empty()) return;
+      cudaStreamSynchronize(m->st);
+      for (void* p : bufs) cudaFree(p);
+      m->dump = DevDump();
+      for (Lane& L : m->lanes) {   // graphs captured with dump kernels point at freed buffers
+        for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
+        L.graphs.clear();
+      }
+    }
+  } dump_reset{m, {}};
+  const int64_t dL = m->c.dec_layers, dd = m->c.d_model;
+  const uint32_t dmask = forced ? fz->dump_mask : 0u;
+  if (dmask & (MNMT_DUMP_LAYERS | MNMT_DUMP_DEC_OUT | MNMT_DUMP_OUT_CODES)) {
+    auto dev = [&](void** p, int64_t bytes) -> mnmt_status {
+      CK(cudaMalloc(p, std::max<int64_t>(bytes, 1)));
+      dump_reset.bufs.push_back(*p);
+      return MNMT_OK;
+    };
+    if (dmask & MNMT_DUMP_LAYERS) CKS(dev((void**)&m->dump.layers, O * dL * 3 * dd * 4));
+    if (dmask & MNMT_DUMP_DEC_OUT) CKS(dev((void**)&m->dump.dec_out, O * dd * 4));
+    if (dmask & MNMT_DUMP_OUT_CODES) CKS(dev((void**)&m->dump.out_codes, O * dd));
+    for (Lane& L : m->lanes) {   // capture fresh graphs with the dump kernels
+      for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
+      L.graphs.clear();
+    }
+  }
+  if ((s = run_job(m, job, forced)) != MNMT_OK) return fail(m, s);
+  if (forced && fz->dump_host) {
+    // sections in bit order (mnmt.h); the encoder sections exist only for one-batch calls
+    char* p = static_cast<char*>(fz->dump_host);
+    const Workspace& w0 = m->lanes[0].ws;
+    if (dmask & (MNMT_DUMP_ENC_OUT | MNMT_DUMP_SRC_KV)) {
+      char* enc_out = nullptr;
+      char* src_kv = nullptr;
+      if (dmask & MNMT_DUMP_ENC_OUT) { enc_out = p; p += ntok * dd * 4; }
+      if (dmask & MNMT_DUMP_SRC_KV) { src_kv = p; p += dL * ntok * 2 * dd * 4; }
+      // the encoder buffers still hold the (single) batch: sentences in input order, those
+      // with T_i = 0 or S_i = 0 skipped
+      int64_t t = 0;
+      for (int i = 0; i < n; ++i) {
+        const int64_t S = src_off[i + 1] - src_off[i];
+        if (max_len[i] == 0 || S == 0) continue;
+        if (enc_out) CK(cudaMemcpyAsync(enc_out + src_off[i] * dd * 4, w0.x + t * dd, S * dd * 4, cudaMemcpyDeviceToHost, m->st));
+        if (src_kv)
+          for (int64_t l = 0; l < dL; ++l)
+            CK(cudaMemcpyAsync(src_kv + ((l * ntok + src_off[i]) * 2 * dd) * 4,
+                               w0.kv + (l * w0.M_cap + t) * 2 * dd, S * 2 * dd * 4, cudaMemcpyDeviceToHost, m->st));
+        t += S;
+      }
+    }
+    if (m->dump.dec_out) { CK(cudaMemcpyAsync(p, m->dump.dec_out, O * dd * 4, cudaMemcpyDeviceToHost, m->st)); p += O * dd * 4; }
+    if (m->dump.out_codes) { CK(cudaMemcpyAsync(p, m->dump.out_codes, O * dd, cudaMemcpyDeviceToHost, m->st)); p += O * dd; }
+    if (m->dump.layers) { CK(cudaMemcpyAsync(p, m->dump.layers, O * dL * 3 * dd * 4, cudaMemcpyDeviceToHost, m->st)); p += O * dL * 3 * dd * 4; }
+  }
   const cudaMemcpyKind dk = dev_io ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   if (O > 0) CK(cudaMemcpyAsync(out_ids, w.out_ids, O * 4, dk, m->st));
   if (n > 0) CK(cudaMemcpyAsync(out_len, w.out_len, (size_t)n * bm * 4, dk, m->st));
@@ -2301,97 +1933,30 @@ mnmt_status mnmt_beam_translate(mnmt_model* m, const int32_t* src_ids, const int
 
 }  // extern "C"
 
-// ------------------------------------------------------------------ teacher-forced dumps
-namespace {
-struct DumpHook : StepHook {
-  uint32_t mask = 0;
-  int n = 0;
-  const int64_t* foff = nullptr;   // forced offsets per sentence (host)
-  char* dec_out = nullptr;         // sections inside dump_host
-  char* out_codes = nullptr;
-  char* layers = nullptr;
-  std::vector<int32_t> live;
-  std::vector<float> buf;
-  std::vector<int8_t> cbuf;
-  int t = 0;                       // current step (1-based), tracked on host
-  bool megakernel_ok() const override { return mask == 0; }
-
-  cudaError_t fetch_live(mnmt_model* m, int* n_live) {
-    int32_t ctrl[2];
-    cudaError_t e;
-    if ((e = cudaMemcpyAsync(ctrl, m->lanes[0].ws.ctrl, 8, cudaMemcpyDeviceToHost, m->lanes[0].st)) != cudaSuccess) return e;
-    if ((e = cudaStreamSynchronize(m->lanes[0].st)) != cudaSuccess) return e;
-    *n_live = ctrl[0];
-    t = ctrl[1];
-    live.resize(std::max(1, ctrl[0]));
-    if ((e = cudaMemcpyAsync(live.data(), m->lanes[0].ws.live, (size_t)ctrl[0] * 4, cudaMemcpyDeviceToHost, m->lanes[0].st)) != cudaSuccess) return e;
-    return cudaStreamSynchronize(m->lanes[0].st);
-  }
-  cudaError_t grab(mnmt_model* m, const float* src, char* base, int64_t row_elems, int64_t slot,
-                   int64_t slots) {
-    const int d = m->c.d_model;
-    int nl = 0;
-    cudaError_t e;
-    if ((e = fetch_live(m, &nl)) != cudaSuccess) return e;
-    buf.resize((size_t)std::max(1, nl) * d);
-    if ((e = cudaMemcpyAsync(buf.data(), src, (size_t)nl * d * 4, cudaMemcpyDeviceToHost, m->lanes[0].st)) != cudaSuccess) return e;
-    if ((e = cudaStreamSynchronize(m->lanes[0].st)) != cudaSuccess) return e;
-    for (int r = 0; r < nl; ++r) {
-      const int64_t row = foff[live[r]] + t - 1;
-      std::memcpy(base + ((row * slots + slot) * row_elems) * 4, buf.data() + (size_t)r * d, (size_t)d * 4);
-    }
-    return cudaSuccess;
-  }
-  cudaError_t x1(mnmt_model* m, int l) override {
-    if (!(mask & MNMT_DUMP_LAYERS)) return cudaSuccess;
-    return grab(m, m->lanes[0].ws.x1, layers, m->c.d_model, (int64_t)l * 3 + 0, (int64_t)m->c.dec_layers * 3);
-  }
-  cudaError_t x2(mnmt_model* m, int l) override {
-    if (!(mask & MNMT_DUMP_LAYERS)) return cudaSuccess;
-    return grab(m, m->lanes[0].ws.x2, layers, m->c.d_model, (int64_t)l * 3 + 1, (int64_t)m->c.dec_layers * 3);
-  }
-  cudaError_t layer(mnmt_model* m, int l) override {
-    cudaError_t e;
-    const int d = m->c.d_model;
-    if (mask & MNMT_DUMP_LAYERS)
-      if ((e = grab(m, m->lanes[0].ws.y, layers, d, (int64_t)l * 3 + 2, (int64_t)m->c.dec_layers * 3)) != cudaSuccess) return e;
-    if (l != m->c.dec_layers - 1) return cudaSuccess;
-    if (mask & MNMT_DUMP_DEC_OUT)
-      if ((e = grab(m, m->lanes[0].ws.y, dec_out, d, 0, 1)) != cudaSuccess) return e;
-    if (mask & MNMT_DUMP_OUT_CODES) {
-      int nl = 0;
-      if ((e = fetch_live(m, &nl)) != cudaSuccess) return e;
-      cbuf.resize((size_t)std::max(1, nl) * d);
-      if ((e = cudaMemcpyAsync(cbuf.data(), m->lanes[0].ws.cy, (size_t)nl * d, cudaMemcpyDeviceToHost, m->lanes[0].st)) != cudaSuccess) return e;
-      if ((e = cudaStreamSynchronize(m->lanes[0].st)) != cudaSuccess) return e;
-      for (int r = 0; r < nl; ++r)
-        std::memcpy(out_codes + (foff[live[r]] + t - 1) * d, cbuf.data() + (size_t)r * d, d);
-    }
-    return cudaSuccess;
-  }
-};
-}  // namespace
-
-extern "C" mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids,
-                                          const int64_t* src_off, int32_t n,
-                                          const int32_t* forced_ids, const int64_t* forced_off,
-                                          int32_t* argmax_ids, uint32_t dump_mask,
-                                          void* dump_host, int64_t dump_cap, void* cuda_stream) {
+// ------------------------------------------------------------------ teacher forcing
+static mnmt_status forced_impl(mnmt_model* m, const int32_t* src_ids, const int64_t* src_off,
+                               int32_t n, const int32_t* forced_ids, const int64_t* forced_off,
+                               int32_t word_budget, bool sorted_batches, int32_t* argmax_ids,
+                               uint32_t dump_mask, void* dump_host, int64_t dump_cap,
+                               void* cuda_stream) {
   if (!m) { set_err("NULL model"); return MNMT_ERR_ARG; }
   if (n < 0 || (n > 0 && (!src_off || !forced_off))) { set_err("bad arguments"); return MNMT_ERR_ARG; }
+  if (n > 0 && forced_off[0] != 0) { set_err("forced_off[0] must be 0"); return MNMT_ERR_ARG; }
   std::vector<int32_t> ml(std::max(n, 1));
   for (int i = 0; i < n; ++i) {
     const int64_t T = forced_off[i + 1] - forced_off[i];
     if (T < 0) { set_err("forced_off not monotone"); return MNMT_ERR_ARG; }
-    ml[i] = (int32_t)std::min<int64_t>(T, MNMT_MAX_SPAN + 1);
+    ml[i] = (int32_t)std::min<int64_t>(T, MNMT_MAX_SPAN + 1);   // > MAX_SPAN: rejected below
   }
   mnmt_status s;
   if ((s = check_inputs(m, src_off, n, ml.data())) != MNMT_OK) return s;
   const int64_t ntok = n > 0 ? src_off[n] : 0, O = n > 0 ? forced_off[n] : 0;
-  if (n > 0 && forced_off[0] != 0) { set_err("forced_off[0] must be 0"); return MNMT_ERR_ARG; }
   if ((ntok > 0 && !src_ids) || (O > 0 && (!forced_ids || !argmax_ids))) { set_err("NULL arrays"); return MNMT_ERR_ARG; }
-  if ((s = check_ids_host(m, src_ids, ntok)) != MNMT_OK) return s;
   if ((s = check_ids_host(m, forced_ids, O)) != MNMT_OK) return s;
+  if (sorted_batches && (dump_mask & (MNMT_DUMP_ENC_OUT | MNMT_DUMP_SRC_KV))) {
+    set_err("encoder dumps need one batch (mnmt_decode_forced)");
+    return MNMT_ERR_ARG;
+  }
   const int64_t d = m->c.d_model, L = m->c.dec_layers;
   int64_t need = 0;
   if (dump_mask & MNMT_DUMP_ENC_OUT) need += ntok * d * 4;
@@ -2400,56 +1965,31 @@ extern "C" mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids,
   if (dump_mask & MNMT_DUMP_OUT_CODES) need += O * d;
   if (dump_mask & MNMT_DUMP_LAYERS) need += O * L * 3 * d * 4;
   if (need > 0 && (!dump_host || dump_cap < need)) { set_err("dump_cap %lld < %lld", (long long)dump_cap, (long long)need); return MNMT_ERR_CAPACITY; }
-  DeviceGuard g(m->dev);
-  if ((s = begin_call(m, cuda_stream)) != MNMT_OK) return fail(m, s);
-  std::vector<std::vector<int32_t>> rows(1, std::vector<int32_t>(n));
-  std::iota(rows[0].begin(), rows[0].end(), 0);
-  Job job;
-  plan_job(src_off, n, ml.data(), rows, std::vector<int>(1, 0), (int)m->lanes.size(), job);
-  // forced_off doubles as the output offset in forced mode (out layout == forced layout)
-  job.out_off.assign(forced_off, forced_off + n + 1);
-  plan_rows(job, src_off, ml.data(), true, forced_off);
-  if ((s = jb_ensure(m, std::max<int64_t>(O, 1), std::max(n, 1), std::max<int64_t>(ntok, 1),
-                     (int64_t)job.meta.size(), job.rows_total)) != MNMT_OK)
-    return fail(m, s);
-  if ((s = ensure_lanes(m, job, std::max<int64_t>(O, 1))) != MNMT_OK) return fail(m, s);
-  auto& w = m->jb;
-  Workspace& w0 = m->lanes[0].ws;
-  if ((s = upload_job(m, job)) != MNMT_OK) return fail(m, s);
-  if (ntok > 0) CK(cudaMemcpyAsync(w.src_ids, src_ids, ntok * 4, cudaMemcpyHostToDevice, m->st));
-  if (O > 0) CK(cudaMemcpyAsync(w0.forced, forced_ids, O * 4, cudaMemcpyHostToDevice, m->st));
-  CK(cudaMemsetAsync(w.out_len, 0, (size_t)std::max(n, 1) * 4, m->st));
-  char* p = static_cast<char*>(dump_host);
-  char* enc_out = nullptr;
-  char* src_kv = nullptr;
-  DumpHook hook;
-  hook.mask = dump_mask;
-  hook.n = n;
-  hook.foff = forced_off;
-  if (dump_mask & MNMT_DUMP_ENC_OUT) { enc_out = p; p += ntok * d * 4; }
-  if (dump_mask & MNMT_DUMP_SRC_KV) { src_kv = p; p += L * ntok * 2 * d * 4; }
-  if (dump_mask & MNMT_DUMP_DEC_OUT) { hook.dec_out = p; p += O * d * 4; }
-  if (dump_mask & MNMT_DUMP_OUT_CODES) { hook.out_codes = p; p += O * d; }
-  if (dump_mask & MNMT_DUMP_LAYERS) { hook.layers = p; p += O * L * 3 * d * 4; }
-  if ((s = run_job(m, job, true, &hook, false)) != MNMT_OK) return fail(m, s);
-  if (ntok > 0 && (enc_out || src_kv)) {
-    // the encoder buffers still hold the (single) batch: tokens are in sentence order
-    // only when every sentence has T_i > 0; otherwise rebuild per-sentence placement
-    int64_t t = 0;
-    for (int i = 0; i < n; ++i) {
-      const int64_t S = src_off[i + 1] - src_off[i];
-      if (ml[i] == 0 || S == 0) continue;
-      if (enc_out) CK(cudaMemcpyAsync(enc_out + src_off[i] * d * 4, w0.x + t * d, S * d * 4, cudaMemcpyDeviceToHost, m->st));
-      if (src_kv)
-        for (int64_t l = 0; l < L; ++l)
-          CK(cudaMemcpyAsync(src_kv + ((l * ntok + src_off[i]) * 2 * d) * 4,
-                             w0.kv + (l * w0.M_cap + t) * 2 * d, S * 2 * d * 4, cudaMemcpyDeviceToHost, m->st));
-      t += S;
-    }
-  }
-  if (O > 0) CK(cudaMemcpyAsync(argmax_ids, w.out_ids, O * 4, cudaMemcpyDeviceToHost, m->st));
-  if ((s = end_call(m, cuda_stream)) != MNMT_OK) return fail(m, s);
-  return MNMT_OK;
+  std::vector<int32_t> lens(std::max(n, 1));
+  const Forced fz{forced_ids, forced_off, dump_mask, need > 0 ? dump_host : nullptr};
+  return translate_impl(m, src_ids, src_off, n, ml.data(), sorted_batches ? word_budget : 1,
+                        sorted_batches, argmax_ids, O, lens.data(), 0, cuda_stream, 0, nullptr,
+                        nullptr, &fz);
+}
+
+extern "C" mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids,
+                                          const int64_t* src_off, int32_t n,
+                                          const int32_t* forced_ids, const int64_t* forced_off,
+                                          int32_t* argmax_ids, uint32_t dump_mask,
+                                          void* dump_host, int64_t dump_cap, void* cuda_stream) {
+  return forced_impl(m, src_ids, src_off, n, forced_ids, forced_off, 1, false, argmax_ids,
+                     dump_mask, dump_host, dump_cap, cuda_stream);
+}
+
+extern "C" mnmt_status mnmt_translate_forced(mnmt_model* m, const int32_t* src_ids,
+                                             const int64_t* src_off, int32_t n,
+                                             const int32_t* forced_ids, const int64_t* forced_off,
+                                             int32_t word_budget, int32_t* argmax_ids,
+                                             uint32_t dump_mask, void* dump_host,
+                                             int64_t dump_cap, void* cuda_stream) {
+  if (word_budget < 1) { set_err("word_budget < 1"); return MNMT_ERR_ARG; }
+  return forced_impl(m, src_ids, src_off, n, forced_ids, forced_off, word_budget, true,
+                     argmax_ids, dump_mask, dump_host, dump_cap, cuda_stream);
 }
 
 extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, int64_t value) {
@@ -2457,24 +1997,6 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
   if (std::string(name) == "max_concurrent_rows") {
     if (value < 0) { set_err("max_concurrent_rows < 0"); return MNMT_ERR_ARG; }
     m->max_concurrent_rows = value;
-    return MNMT_OK;
-  }
-  if (std::string(name) == "profile_phases") {
-    m->profile_phases = value ? 1 : 0;
-    return MNMT_OK;
-  }
-  if (std::string(name) == "rowlocal") {
-    m->rowlocal = value ? 1 : 0;
-    for (Lane& L : m->lanes) L.prog_out = nullptr;   // rebuild the step program
-    return MNMT_OK;
-  }
-  if (std::string(name) == "fuse_ln") {
-    if (value > 3) { set_err("fuse_ln must be 0, 1, 2 or 3"); return MNMT_ERR_ARG; }
-    m->fuse_ln = (int)value;
-    for (Lane& L : m->lanes) {   // captured graphs encode the old kernel sequence
-      for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
-      L.graphs.clear();
-    }
     return MNMT_OK;
   }
   if (std::string(name) == "pers_reserve") {
@@ -2495,15 +2017,6 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
     }
     return MNMT_OK;
   }
-  if (std::string(name) == "rowfuse") {
-    if (value < 0 || value > (1 << 20)) { set_err("rowfuse must be in [0, 2^20]"); return MNMT_ERR_ARG; }
-    m->rowfuse = (int)value;
-    for (Lane& L : m->lanes) {   // captured graphs encode the old kernel sequence
-      for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
-      L.graphs.clear();
-    }
-    return MNMT_OK;
-  }
   if (std::string(name) == "green_sms") {
     if (value < 0 || value > 136 || value % 8) { set_err("green_sms must be 0 or a multiple of 8 up to 136"); return MNMT_ERR_ARG; }
     if (value != m->green_sms) {
@@ -2517,16 +2030,6 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
     }
     return MNMT_OK;
   }
-  if (std::string(name) == "mk_cluster") {
-    if (value != 0 && value != 1) { set_err("mk_cluster must be 0 or 1"); return MNMT_ERR_ARG; }
-    m->mk_cluster = (int)value;
-    return MNMT_OK;
-  }
-  if (std::string(name) == "mk_ctas") {
-    if (value < 0 || value > 4096) { set_err("mk_ctas must be in [0, 4096]"); return MNMT_ERR_ARG; }
-    m->mk_ctas = (int)value;
-    return MNMT_OK;
-  }
   if (std::string(name) == "lane_tiers") {
     if (value < 0 || value > 100) { set_err("lane_tiers must be in [0, 100]"); return MNMT_ERR_ARG; }
     m->lane_tiers = (int)value;
@@ -2534,7 +2037,7 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
   }
   if (std::string(name) == "smallm") {
     if (value < 0 || value > SMALLM_MAX) { set_err("smallm must be in [0, 32]"); return MNMT_ERR_ARG; }
-    gemm_set_smallm((int)value);   // process-wide (a GEMM launch setting)
+    m->smallm = (int)value;
     for (Lane& L : m->lanes) {     // captured graphs encode the old kernel sequence
       for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
       L.graphs.clear();
@@ -2543,26 +2046,16 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
   }
   if (std::string(name) == "smallm_kmax") {
     if (value < 0 || value > (1 << 16)) { set_err("smallm_kmax must be in [0, 65536]"); return MNMT_ERR_ARG; }
-    gemm_set_smallm_kmax((int)value);   // process-wide
+    m->smallm_kmax = (int)value;
     for (Lane& L : m->lanes) {
       for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
       L.graphs.clear();
     }
     return MNMT_OK;
   }
-  if (std::string(name) == "fin_embed") {
-    if (value < 0 || value > (1 << 20)) { set_err("fin_embed must be in [0, 2^20]"); return MNMT_ERR_ARG; }
-    m->fin_embed = (int)value;   // graph keys carry the variant, so cached graphs stay valid
-    return MNMT_OK;
-  }
   if (std::string(name) == "steps_per_graph") {
     if (value < 1 || value > 63) { set_err("steps_per_graph must be in [1, 63]"); return MNMT_ERR_ARG; }
     m->steps_per_graph = (int)value;
-    return MNMT_OK;
-  }
-  if (std::string(name) == "megakernel") {
-    if (value != 0 && value != 1) { set_err("megakernel must be 0 or 1"); return MNMT_ERR_ARG; }
-    m->megakernel = (int)value;
     return MNMT_OK;
   }
   if (std::string(name) == "lanes") {
@@ -2575,57 +2068,6 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
   }
   set_err("unknown option '%s'", name);
   return MNMT_ERR_ARG;
-}
-
-// Per-phase-type time of the last persistent-kernel launch of lane 0 (option
-// "profile_phases"): out[type] += ns spent in phases of that type; returns #steps recorded.
-extern "C" mnmt_status mnmt_debug_phase_profile(mnmt_model* m, int64_t* out_ns_by_type,
-                                                int32_t n_types, int32_t* steps_out) {
-  if (!m || !out_ns_by_type || !steps_out || n_types < 5) { set_err("bad arguments"); return MNMT_ERR_ARG; }
-  Lane& L = m->lanes[0];
-  for (int i = 0; i < n_types; ++i) out_ns_by_type[i] = 0;
-  *steps_out = 0;
-  if (!L.d_timing || L.timing_steps == 0) return MNMT_OK;
-  DeviceGuard g(m->dev);
-  std::vector<unsigned long long> t((size_t)L.timing_steps * (L.n_phases + 1));
-  CK(cudaMemcpy(t.data(), L.d_timing, t.size() * 8, cudaMemcpyDeviceToHost));
-  int steps = 0;
-  for (int64_t s = 0; s < L.timing_steps; ++s) {
-    const unsigned long long* r = t.data() + s * (L.n_phases + 1);
-    if (r[0] == 0 || r[L.n_phases] == 0) break;
-    for (int p = 0; p < L.n_phases; ++p) out_ns_by_type[L.phase_types[p]] += (int64_t)(r[p + 1] - r[p]);
-    ++steps;
-  }
-  *steps_out = steps;
-  return MNMT_OK;
-}
-
-// Average ns of every phase of the last persistent-kernel batch of lane 0; types[i] gets
-// the phase type.  Returns the number of phases written (<= cap) in *n_out.
-extern "C" mnmt_status mnmt_debug_phase_times(mnmt_model* m, int64_t* avg_ns, int32_t* types,
-                                              int32_t cap, int32_t* n_out) {
-  if (!m || !avg_ns || !types || !n_out) { set_err("bad arguments"); return MNMT_ERR_ARG; }
-  Lane& L = m->lanes[0];
-  *n_out = 0;
-  if (!L.d_timing || L.timing_steps == 0) return MNMT_OK;
-  DeviceGuard g(m->dev);
-  std::vector<unsigned long long> t((size_t)L.timing_steps * (L.n_phases + 1));
-  CK(cudaMemcpy(t.data(), L.d_timing, t.size() * 8, cudaMemcpyDeviceToHost));
-  const int np = std::min(cap, L.n_phases);
-  std::vector<int64_t> acc(np, 0);
-  int steps = 0;
-  for (int64_t s = 0; s < L.timing_steps; ++s) {
-    const unsigned long long* r = t.data() + s * (L.n_phases + 1);
-    if (r[0] == 0 || r[L.n_phases] == 0) break;
-    for (int p = 0; p < np; ++p) acc[p] += (int64_t)(r[p + 1] - r[p]);
-    ++steps;
-  }
-  for (int p = 0; p < np; ++p) {
-    avg_ns[p] = steps ? acc[p] / steps : 0;
-    types[p] = L.phase_types[p];
-  }
-  *n_out = np;
-  return MNMT_OK;
 }
 
 extern "C" mnmt_status mnmt_get_stats(const mnmt_model* m, mnmt_stats* out) {

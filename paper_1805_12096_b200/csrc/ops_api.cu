@@ -277,3 +277,31 @@ extern "C" mnmt_status mnmt_debug_gemm_chain(const int8_t* A, const int8_t* W, i
   return cuda_status(e, "gemm chain");
 }
 
+
+// ------------------------------------------------------------------ A11: multi-GPU id unshard
+namespace {
+__global__ void k_gather_rows(const int32_t* __restrict__ src, const int64_t* __restrict__ src_off,
+                              const int32_t* __restrict__ src_len, const int32_t* __restrict__ dst_row,
+                              const int64_t* __restrict__ dst_off, int n, int32_t* __restrict__ dst,
+                              int32_t* __restrict__ dst_len) {
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const int len = src_len[i], r = dst_row[i];
+  const int32_t* s = src + src_off[i];
+  int32_t* o = dst + dst_off[r];
+  for (int j = lane; j < len; j += 32) o[j] = s[j];
+  if (lane == 0) dst_len[r] = len;
+}
+}  // namespace
+
+extern "C" mnmt_status mnmt_op_gather_rows(const int32_t* src, const int64_t* src_off,
+                                           const int32_t* src_len, const int32_t* dst_row,
+                                           const int64_t* dst_off, int32_t n, int32_t* dst,
+                                           int32_t* dst_len, void* stream) {
+  if (n < 0 || (n > 0 && (!src || !src_off || !src_len || !dst_row || !dst_off || !dst || !dst_len)))
+    return arg_error("mnmt_op_gather_rows: bad arguments");
+  if (n == 0) return MNMT_OK;
+  k_gather_rows<<<(n + 7) / 8, 256, 0, (cudaStream_t)stream>>>(src, src_off, src_len, dst_row, dst_off,
+                                                                n, dst, dst_len);
+  return cuda_status(cudaGetLastError(), "gather_rows");
+}

@@ -1,5 +1,5 @@
 // rowdev.cuh — device bodies of the HBM-bound row operations, shared by the standalone
-// kernels (rowops.cu) and the persistent decode-step kernel (stepkernel.cu).
+// kernels (rowops.cu) and the fused GEMM epilogues.
 #pragma once
 #include <cstdint>
 

@@ -244,21 +244,26 @@ inline size_t attn_split_smem(int ns, int span) {
 
 constexpr int FIN_THREADS = 1024;
 
-// NV > 0: the next step's embedding (A5) follows the compaction in the same CTA, warp per
-// row, reading the ctrl / live / prev_live values this block has just written (visible
-// after finish_block's closing barrier).  Saves one dependent launch per step at small row
-// counts, where the embedding is a few rows per warp.
-template <int NV>
 __global__ void __launch_bounds__(FIN_THREADS) k_finish(FinishArgs a) {
   __shared__ int32_t warp_cnt[32];
   __shared__ int32_t base_s;
   pdl_wait();
   pdl_trigger_early();
   finish_block(a, warp_cnt, base_s);
-  if constexpr (NV > 0) {
-    const int nw = blockDim.x >> 5;
-    for (int r = threadIdx.x >> 5; r < a.emb.n; r += nw) embed_tgt_row<NV>(a.emb, r);
-  }
+}
+
+// Teacher-forced dumps (test hook): live row r of a step's activations -> row
+// foff[live[r]] + t - 1, slot `slot` of `slots`.  One warp per row, 16-byte copies.
+__global__ void k_dump_rows(DumpArgs a) {
+  pdl_wait();
+  pdl_trigger_early();
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= a.n || r >= a.ctrl[0]) return;
+  const int64_t row = a.foff[a.live[r]] + a.ctrl[1] - 1;
+  const int64_t bytes = (int64_t)a.d * a.elem;
+  const uint4* src = reinterpret_cast<const uint4*>(static_cast<const char*>(a.src) + r * bytes);
+  uint4* dst = reinterpret_cast<uint4*>(static_cast<char*>(a.dst) + (row * a.slots + a.slot) * bytes);
+  for (int64_t i = lane; i < bytes / 16; i += 32) dst[i] = src[i];
 }
 
 // Encoder self-attention: one CTA per (sentence, head).  The sentence's K and V head
@@ -498,9 +503,7 @@ static cudaError_t set_carveouts() {
                        (const void*)k_embed_tgt<1>, (const void*)k_embed_tgt<2>,
                        (const void*)k_embed_tgt<4>, (const void*)k_embed_tgt<8>,
                        (const void*)k_ln<1>, (const void*)k_ln<2>, (const void*)k_ln<4>, (const void*)k_ln<8>,
-                       (const void*)k_attn, (const void*)k_attn_enc, (const void*)k_finish<0>,
-                       (const void*)k_finish<1>, (const void*)k_finish<2>,
-                       (const void*)k_finish<4>, (const void*)k_finish<8>,
+                       (const void*)k_attn, (const void*)k_attn_enc, (const void*)k_finish,
                        (const void*)k_decode_init};
   for (const void* f : fns) {
     cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -605,14 +608,13 @@ cudaError_t launch_attn_enc(const EncAttnArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t st) {
-  if (a.emb.n <= 0) return launch_pdl(k_finish<0>, dim3(1), dim3(FIN_THREADS), 0, st, a);
-  switch (nv_for(a.emb.d)) {
-    case 1: return launch_pdl(k_finish<1>, dim3(1), dim3(FIN_THREADS), 0, st, a);
-    case 2: return launch_pdl(k_finish<2>, dim3(1), dim3(FIN_THREADS), 0, st, a);
-    case 4: return launch_pdl(k_finish<4>, dim3(1), dim3(FIN_THREADS), 0, st, a);
-    case 8: return launch_pdl(k_finish<8>, dim3(1), dim3(FIN_THREADS), 0, st, a);
-  }
-  return cudaErrorInvalidValue;
+  return launch_pdl(k_finish, dim3(1), dim3(FIN_THREADS), 0, st, a);
+}
+
+cudaError_t launch_dump_rows(const DumpArgs& a, cudaStream_t st) {
+  if (a.n <= 0) return cudaSuccess;
+  return launch_pdl(k_dump_rows, dim3((a.n + ROW_WARPS - 1) / ROW_WARPS), dim3(32 * ROW_WARPS), 0,
+                    st, a);
 }
 
 cudaError_t launch_decode_init(int32_t* ctrl, int32_t* live, int B, unsigned long long* keys,

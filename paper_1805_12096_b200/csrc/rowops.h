@@ -112,9 +112,19 @@ struct FinishArgs {
   int32_t* live_start;
   int32_t* live_len;
   const int32_t* id_map;    // shortlist (F2): GEMM column -> vocabulary id, or null
-  // optional: the next step's target embedding (A5) in the same CTA after the compaction
-  // (emb.n > 0: rows [0, emb.n) warp per row; the step graph then omits k_embed_tgt)
-  EmbedTgtArgs emb;
+};
+
+// Teacher-forced dumps (test hook): live row r of src [n x d] (elem bytes per element) is
+// copied to dst + ((foff[live[r]] + t - 1) * slots + slot) * d * elem.
+struct DumpArgs {
+  int n;                    // static row bound
+  const int32_t* ctrl;      // [0] live rows, [1] t
+  const int32_t* live;      // compact -> batch row
+  const int64_t* foff;      // [batch row] forced offset
+  int d, elem;
+  const void* src;
+  void* dst;
+  int64_t slot, slots;
 };
 
 cudaError_t launch_quantize(const float* x, int64_t n, float clip, int8_t* out, cudaStream_t st);
@@ -130,6 +140,7 @@ cudaError_t launch_kv_bf16(float* kv, bf16s* kv16, int L, int64_t n, int64_t str
 cudaError_t launch_attn_enc(const EncAttnArgs& a, cudaStream_t st);
 cudaError_t attn_init();   // dynamic-smem attribute (call once per device, outside capture)
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t st);
+cudaError_t launch_dump_rows(const DumpArgs& a, cudaStream_t st);
 // live[r] = r, keys = 0, ctrl = {B, 1}; live_start/live_len (optional) = row_start/row_len.
 cudaError_t launch_decode_init(int32_t* ctrl, int32_t* live, int B, unsigned long long* keys,
                                const int32_t* row_start, const int32_t* row_len,

@@ -52,10 +52,11 @@ EXPORTS = [
     "mnmt_config_default", "mnmt_model_create", "mnmt_model_set_param", "mnmt_model_quantize",
     "mnmt_batch_by_words", "mnmt_decode", "mnmt_translate", "mnmt_beam_translate",
     "mnmt_model_set_shortlist",
-    "mnmt_decode_forced",
+    "mnmt_decode_forced", "mnmt_translate_forced",
     "mnmt_get_stats", "mnmt_last_error", "mnmt_model_destroy", "mnmt_model_set_option",
     "mnmt_op_quantize", "mnmt_op_gemm_i8", "mnmt_op_argmax_ids", "mnmt_op_layernorm",
-    "mnmt_op_aan_step", "mnmt_op_embed", "mnmt_op_attention", "mnmt_op_attention_bf16", "mnmt_debug_phase_profile",
+    "mnmt_op_aan_step", "mnmt_op_embed", "mnmt_op_attention", "mnmt_op_attention_bf16",
+    "mnmt_op_gather_rows",
 ]
 
 _lib = None
@@ -82,6 +83,7 @@ def lib():
     L.mnmt_model_set_shortlist.argtypes = [P, P, I32, P, I32]
     L.mnmt_beam_translate.argtypes = [P, P, P, I32, P, I32, I32, P, I64, P, P, P, C.c_uint32, P]
     L.mnmt_decode_forced.argtypes = [P, P, P, I32, P, P, P, C.c_uint32, P, I64, P]
+    L.mnmt_translate_forced.argtypes = [P, P, P, I32, P, P, I32, P, C.c_uint32, P, I64, P]
     L.mnmt_get_stats.argtypes = [P, C.POINTER(Stats)]
     L.mnmt_model_set_option.argtypes = [P, C.c_char_p, I64]
     L.mnmt_last_error.argtypes = []
@@ -96,7 +98,7 @@ def lib():
     L.mnmt_op_embed.argtypes = [P, I32, P, P, I32, F, P, P, P]
     L.mnmt_op_attention.argtypes = [P, I64, P, I64, I32, I32, P, P, I32, I32, I32, F, P, P, P]
     L.mnmt_op_attention_bf16.argtypes = [P, I64, P, I64, I32, I32, P, P, I32, I32, I32, F, P, P, P]
-    L.mnmt_debug_phase_profile.argtypes = [P, P, I32, P]
+    L.mnmt_op_gather_rows.argtypes = [P, P, P, P, P, I32, P, P, P]
     for name in EXPORTS:
         fn = getattr(L, name)
         if name not in ("mnmt_config_default", "mnmt_last_error", "mnmt_model_destroy"):
@@ -179,15 +181,6 @@ class Model:
     def set_option(self, name: str, value: int) -> None:
         """Scheduling options (include/mnmt.h); never change results."""
         _check(lib().mnmt_model_set_option(self.h, name.encode(), int(value)))
-
-    def phase_profile(self):
-        """ns per phase type over the last persistent-kernel batch of lane 0 (option
-        "profile_phases"): ({"gemm":..,"embed":..,"ln":..,"attn":..,"finish":..}, steps)."""
-        out = np.zeros(8, np.int64)
-        steps = np.zeros(1, np.int32)
-        _check(lib().mnmt_debug_phase_profile(self.h, _p(out), 8, _p(steps)))
-        names = ["gemm", "embed", "ln", "attn", "finish"]
-        return {k: int(out[i]) for i, k in enumerate(names)}, int(steps[0])
 
     def stats(self) -> Dict[str, int]:
         s = Stats()
@@ -281,8 +274,11 @@ class Model:
                                     _stream_ptr(stream)))
 
     def decode_forced(self, sset, forced: np.ndarray, forced_off: np.ndarray,
-                      dump_mask: int = 0, stream=None):
-        """Teacher forcing (P-2): returns (argmax ids flat [sum T_i], dumps dict)."""
+                      dump_mask: int = 0, stream=None, budget: Optional[int] = None):
+        """Teacher forcing (P-2): returns (argmax ids flat [sum T_i], dumps dict).
+        budget None: all sentences as one batch (mnmt_decode_forced); otherwise the whole
+        translate schedule (word-budget batches, waves, lanes, step graphs) with that budget
+        (mnmt_translate_forced; encoder dumps unavailable)."""
         n = sset.n
         d, L = self.dims.d_model, self.dims.dec_layers
         ids = np.ascontiguousarray(sset.ids, np.int32)
@@ -304,9 +300,15 @@ class Model:
         nbytes = sum(int(np.prod(s)) * np.dtype(t).itemsize for _, t, s in sections)
         buf = np.zeros(max(nbytes, 1), np.uint8)
         am = np.zeros(max(O, 1), np.int32)
-        _check(lib().mnmt_decode_forced(self.h, _p(ids), _p(offs), n, _p(f if f.size else None),
-                                        _p(fo), _p(am), dump_mask, _p(buf), nbytes,
-                                        _stream_ptr(stream)))
+        if budget is None:
+            _check(lib().mnmt_decode_forced(self.h, _p(ids), _p(offs), n, _p(f if f.size else None),
+                                            _p(fo), _p(am), dump_mask, _p(buf), nbytes,
+                                            _stream_ptr(stream)))
+        else:
+            _check(lib().mnmt_translate_forced(self.h, _p(ids), _p(offs), n,
+                                               _p(f if f.size else None), _p(fo), int(budget),
+                                               _p(am), dump_mask, _p(buf), nbytes,
+                                               _stream_ptr(stream)))
         dumps, o = {}, 0
         for name, t, shape in sections:
             k = int(np.prod(shape)) * np.dtype(t).itemsize
@@ -358,3 +360,10 @@ def op_attention_bf16(q_ptr, ldq, kv16_ptr, ldkv, k_off, v_off, start_ptr, len_p
     _check(lib().mnmt_op_attention_bf16(q_ptr, ldq, kv16_ptr, ldkv, k_off, v_off, start_ptr,
                                         len_ptr, n, d, H, clip, out_q_ptr, out_f_ptr,
                                         _stream_ptr(stream)))
+
+
+def op_gather_rows(src_ptr, src_off_ptr, src_len_ptr, dst_row_ptr, dst_off_ptr, n, dst_ptr,
+                   dst_len_ptr, stream=None) -> None:
+    """A11 on several GPUs: gathered rows back to input order (include/mnmt_ops.h)."""
+    _check(lib().mnmt_op_gather_rows(src_ptr, src_off_ptr, src_len_ptr, dst_row_ptr, dst_off_ptr,
+                                     n, dst_ptr, dst_len_ptr, _stream_ptr(stream)))

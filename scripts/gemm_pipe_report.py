@@ -101,6 +101,8 @@ def main():
     ap.add_argument("--budget", type=int, default=8192)
     ap.add_argument("--mcr", type=int, default=4096)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--json", default=None, help="also write the figures as JSON (bench.py reads it)")
+    ap.add_argument("--workload", default=None, help="bench workload name recorded in the JSON")
     a = ap.parse_args()
     import synth
     dims = synth.PRESETS[a.preset]
@@ -147,6 +149,21 @@ def main():
     print(txt)
     if a.out:
         open(a.out, "w").write(txt + "\n")
+    if a.json:
+        per = {}
+        for c in dec_cls + ["encoder"]:
+            n, t, tp = agg[c]
+            if n:
+                per[c] = {"launches": n, "ncu_ms": t / 1e3, "tensor_pipe_pct": tp / t if t else 0.0,
+                          "useful_ops_pct": 100 * ops.get(c, 0.0) / (t * 1e-6 * peak_ops) if t else 0.0}
+        dec_ops = sum(ops.get(c, 0.0) for c in dec_cls)
+        json.dump({"workload": a.workload, "preset": a.preset, "budget": a.budget, "mcr": a.mcr,
+                   "source": a.csv, "launches": len(L),
+                   "decoder_gemm_tensor_pipe_pct": dec_pipe,
+                   "decoder_gemm_useful_ops_pct": 100 * dec_ops / (dec_t * 1e-6 * peak_ops) if dec_t else 0.0,
+                   "decoder_gemm_share_of_decode_time": dec_t / dec_us if dec_us else 0.0,
+                   "per_class": per, "int8_peak_tops": peak_ops / 1e12},
+                  open(a.json, "w"), indent=1)
 
 
 if __name__ == "__main__":

@@ -30,7 +30,7 @@ TINY_VARIANTS = [
               aan_ffn_depth=0, aan_gate=0),
     ModelDims("t-self", 32, 64, 4, vocab=64, enc_layers=2, dec_layers=2, decoder=0),
     ModelDims("t-nobias-ragged-vocab", 48, 96, 4, vocab=50, enc_layers=1, dec_layers=3, out_bias=0),
-    # d in {192, 256}: LayerNorm fused into full-row GEMM epilogues
+    # d in {192, 256}: the paper-width head sizes (d_h = 24, 32)
     ModelDims("t192-aan", 192, 384, 8, vocab=1000, enc_layers=2, dec_layers=2),
     ModelDims("t192-ffn1", 192, 384, 8, vocab=1000, enc_layers=2, dec_layers=2, aan_ffn_depth=1),
     ModelDims("t256-noffn-gate", 256, 512, 8, vocab=1000, enc_layers=2, dec_layers=2, aan_ffn_depth=0),
@@ -102,86 +102,16 @@ def test_long_sources_split_attention(lo, hi):
 
 
 @pytest.mark.parametrize("dims", TINY_VARIANTS, ids=lambda d: d.name)
-def test_tiny_teacher_forced_rowfused(dims):
-    """The fused per-row AAN / source-attention blocks (option rowfuse): every intermediate
-    (x1, x2, x3 of every layer, every step) within tolerance of the oracle, ids bit-exact."""
-    w, om, gm = pair(dims, 11)
-    gm.set_option("rowfuse", 1 << 20)
-    ss, forced, foff = forced_case(dims, 9, 0, 13, 0, 17, seed=3)
-    tot, ex, fl = run_forced_parity(dims, w, om, gm, ss, forced, foff)
-    assert ex == tot, f"{tot - ex} flagged near-ties"
-
-
-@pytest.mark.parametrize("fuse", [1, 3])
-@pytest.mark.parametrize("dims", [d for d in TINY_VARIANTS if d.d_model in (192, 256)],
-                         ids=lambda d: d.name)
-def test_teacher_forced_fused_layernorm(dims, fuse):
-    """LayerNorm in the producing GEMM's epilogue (fuse_ln 1: every full-row producer incl. the
-    encoder; 3: the decoder's d x d producers): every intermediate within tolerance of the
-    oracle, ids bit-exact."""
-    w, om, gm = pair(dims, 11)
-    gm.set_option("fuse_ln", fuse)
-    ss, forced, foff = forced_case(dims, 9, 0, 13, 0, 17, seed=3)
-    tot, ex, fl = run_forced_parity(dims, w, om, gm, ss, forced, foff)
-    assert ex == tot, f"{tot - ex} flagged near-ties"
-
-
-@pytest.mark.parametrize("dims", TINY_VARIANTS, ids=lambda d: d.name)
-def test_tiny_teacher_forced_persistent_kernel(dims):
-    """Teacher forcing through the persistent step kernel (no dumps): per-step ids bit-exact."""
-    w, om, gm = pair(dims, 13)
-    ss, forced, foff = forced_case(dims, 11, 0, 13, 0, 17, seed=4)
-    for mk in (1, 0):
-        gm.set_option("megakernel", mk)
-        ids, _ = gm.decode_forced(ss, forced, foff, 0)
-        for i in range(ss.n):
-            T = int(foff[i + 1] - foff[i])
-            f = forced[foff[i]:foff[i + 1]]
-            oids = om.decode_one(ss.ids[ss.offsets[i]:ss.offsets[i + 1]], T, forced=f)
-            assert np.array_equal(ids[foff[i]:foff[i + 1]], oids), (dims.name, mk, i)
-
-
-@pytest.mark.parametrize("dims", TINY_VARIANTS, ids=lambda d: d.name)
 def test_tiny_free_running(dims):
     w, om, gm = pair(dims, 12)
     ss = synth.random_set(17, 1, 15, seed=5, vocab=dims.vocab)
     ref = om.decode_many(ss, 4)
-    # persistent step kernel (grid-wide phases; row-local phases on a capped grid) and one
-    # kernel per op (graph)
-    for mk, rl, ctas, cl, rf in ((1, 0, 0, 0, 0), (1, 1, 8, 0, 0), (1, 0, 16, 1, 0), (0, 0, 0, 0, 0),
-                                 (0, 0, 0, 0, 1 << 20)):
-        gm.set_option("megakernel", mk)
-        gm.set_option("rowlocal", rl)
-        gm.set_option("mk_ctas", ctas)
-        gm.set_option("mk_cluster", cl)   # grid = one 16-CTA cluster, cluster barriers
-        gm.set_option("rowfuse", rf)      # fused per-row AAN / source-attention blocks
-        got = gm.decode(ss)
-        assert all(np.array_equal(a, b) for a, b in zip(got, ref)), (mk, rl, ctas, cl, rf)
-
-
-@pytest.mark.parametrize("dims", TINY_VARIANTS, ids=lambda d: d.name)
-def test_finish_embeds_next_step(dims):
-    """Option fin_embed (A5 inside k_finish after the compaction, the step graph then starts
-    without k_embed_tgt): off, at every row bound and at the default bound, with one and several
-    steps per graph, free-running and teacher-forced ids bit-exact vs the oracle."""
-    w, om, gm = pair(dims, 14)
-    ss = synth.random_set(150, 1, 19, seed=6, vocab=dims.vocab)   # 256-row pad, then 128
-    ref = om.decode_many(ss, 4)
-    fs, forced, foff = forced_case(dims, 11, 0, 13, 0, 17, seed=5)
-    for fe in (0, 128, 1 << 20):
-        gm.set_option("fin_embed", fe)
-        for k in (1, 3):
-            gm.set_option("steps_per_graph", k)
-            got = gm.decode(ss)
-            assert all(np.array_equal(a, b) for a, b in zip(got, ref)), (fe, k)
-            ids, _ = gm.decode_forced(fs, forced, foff, 0)
-            for i in range(fs.n):
-                T = int(foff[i + 1] - foff[i])
-                oids = om.decode_one(fs.ids[fs.offsets[i]:fs.offsets[i + 1]], T,
-                                     forced=forced[foff[i]:foff[i + 1]])
-                assert np.array_equal(ids[foff[i]:foff[i + 1]], oids), (fe, k, i)
+    got = gm.decode(ss)
+    assert all(np.array_equal(a, b) for a, b in zip(got, ref))
+    for k in (1, 3):                       # several decoder steps per CUDA graph
+        gm.set_option("steps_per_graph", k)
+        assert all(np.array_equal(a, b) for a, b in zip(gm.decode(ss), ref)), k
     gm.set_option("steps_per_graph", 1)
-    gm.set_option("fin_embed", 0)
 
 
 @pytest.mark.parametrize("dims", TINY_VARIANTS, ids=lambda d: d.name)
@@ -289,10 +219,6 @@ def test_batch_and_order_invariance():
     base = gm.translate(ss, 1 << 20)
     for budget in (1, 64, 333, 4096):
         assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, budget), base))
-    for fuse in (0, 1, 2, 3):              # LayerNorm unfused, fused per CTA (all / d x d
-                                           # producers only), fused per cluster
-        gm.set_option("fuse_ln", fuse)
-        assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, 333), base))
     for lanes in (1, 2, 3):                # concurrent decoder lanes: identical ids
         gm.set_option("lanes", lanes)
         for rows in (7, 50, 1 << 20):      # co-scheduled batch waves: identical ids
@@ -306,9 +232,6 @@ def test_batch_and_order_invariance():
                 assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, 64), base))
                 gm.set_option("green_sms", 0)
         gm.set_option("lane_tiers", 0)
-    gm.set_option("rowfuse", 1 << 20)     # fused per-row AAN / source-attention blocks
-    assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, 333), base))
-    gm.set_option("rowfuse", 0)
     for k in (3, 8):                       # several decoder steps per CUDA graph
         gm.set_option("steps_per_graph", k)
         assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ss, 333), base))

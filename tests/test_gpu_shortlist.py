@@ -84,9 +84,6 @@ def test_shortlist_scheduling_options():
                     ("green_sms", 48), ("pers_reserve", 16)]:
         gm.set_option(name, v)
     check(gm.translate(ss, 120, shortlist=True), ref, "bench options")
-    gm.set_option("megakernel", 1)
-    check(gm.translate(ss, 120, shortlist=True), ref, "megakernel option")
-    gm.set_option("megakernel", 0)
     # a plain call after shortlisted ones is the unrestricted decode again
     check(gm.translate(ss, 120), om.decode_many(ss, 4), "plain after shortlist")
 
