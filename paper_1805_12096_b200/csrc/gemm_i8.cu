@@ -38,6 +38,7 @@ constexpr int EPI_STAGE_LD = 36;                       // row stride (floats): 1
                                                        // conflict-free STS.128 / LDS.128
 constexpr int EPI_STAGE_FLOATS = 32 * EPI_STAGE_LD;    // per epilogue warp
 constexpr int EPI_STAGE_BYTES = EPI_WARPS * EPI_STAGE_FLOATS * 4;
+constexpr int GEMM_SMEM_MAX = 220 * 1024;                // dynamic smem cap of a split-K launch
 
 template <int BN>
 struct GemmCfg {
@@ -48,7 +49,16 @@ struct GemmCfg {
   static constexpr int STAGES = (190 * 1024 / STAGE_BYTES) > 8 ? 8 : (190 * 1024 / STAGE_BYTES);
   static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
   static constexpr int smem_for(int stages) { return stages * STAGE_BYTES + 1024 + EPI_STAGE_BYTES; }
+  // split-K (gridDim.z > 1, one cluster along z): the s32 partials of CTAs z > 0 are added
+  // into CTA 0's [128][BN + 1] buffer (exact integer adds: the order cannot matter)
+  static constexpr int RED_LD = BN + 1;
+  static constexpr int RED_BYTES = BM * RED_LD * 4;
 };
+
+// Split-K partial accumulation into the cluster leader's buffer (distributed shared memory).
+__device__ __forceinline__ void red_add_cluster_s32(uint32_t addr, int32_t v) {
+  asm volatile("red.relaxed.cluster.shared::cluster.add.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 
 // Exact (float)acc for |acc| < 2^22 without the quarter-rate I2F: place acc in the
 // mantissa of 1.5 * 2^23 and subtract.  Used when K <= 256 (|acc| <= 127^2 * 256 < 2^22).
@@ -389,14 +399,28 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const uint32_t lane = lane_id();
   const int n_tile = blockIdx.x, m_tile = blockIdx.y;
   const int m0 = m_tile * BM, n0 = n_tile * BN;
-  const int num_kb = (args.K + BK - 1) / BK;
-  // ring depth chosen at launch (dynamic smem); at most Cfg::STAGES
-  const int stages = min(Cfg::STAGES, num_kb);
+  // split-K: the ks CTAs of a cluster (along z) take consecutive K-block ranges; CTA z = 0
+  // reduces (launch_t guarantees every range is non-empty)
+  const int ks = gridDim.z, kz = blockIdx.z;
+  const int kb_all = (args.K + BK - 1) / BK, kb_per = (kb_all + ks - 1) / ks;
+  const int kb0 = kz * kb_per;
+  const int num_kb = min(kb_all, kb0 + kb_per) - kb0;
+  // ring depth chosen at launch (dynamic smem; the same layout in every CTA of a cluster)
+  const int ring = min(min(Cfg::STAGES, kb_per), args.ring_cap > 0 ? args.ring_cap : Cfg::STAGES);
+  const int stages = min(ring, num_kb);
   if (threadIdx.x == 0) GEMM_TRACE(0);
 
   // 1024-byte aligned stage ring (required by the 128B swizzle atom).
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
+  int32_t* red = reinterpret_cast<int32_t*>(smem + ring * Cfg::STAGE_BYTES + EPI_STAGE_BYTES);
+  if (ks > 1) {
+    if (kz == 0) {   // the leader's partial buffer starts at zero
+      for (int i = threadIdx.x; i < Cfg::RED_BYTES / 16; i += GEMM_THREADS)
+        reinterpret_cast<int4*>(red)[i] = make_int4(0, 0, 0, 0);
+    }
+    cluster_arrive();   // phase 1 (release): the leader's buffer is zeroed; waited on before use
+  }
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -414,7 +438,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint8_t* sb = smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES;
 #pragma unroll
       for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
-        tma_load_2d(sb + j * 64 * BK, &tmB, &full_bar[s], s * BK, n0 + j * 64);
+        tma_load_2d(sb + j * 64 * BK, &tmB, &full_bar[s], (kb0 + s) * BK, n0 + j * 64);
     }
   }
   // TMEM and the bias do not depend on the previous kernel either: both before the wait
@@ -432,12 +456,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
       uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
-      tma_load_2d(sa, &tmA, &full_bar[s], s * BK, m0);
-      tma_load_2d(sa + 64 * BK, &tmA, &full_bar[s], s * BK, m0 + 64);
+      tma_load_2d(sa, &tmA, &full_bar[s], (kb0 + s) * BK, m0);
+      tma_load_2d(sa + 64 * BK, &tmA, &full_bar[s], (kb0 + s) * BK, m0 + 64);
     }
   }
   const int M_live = args.M_dyn ? min(args.M, *args.M_dyn) : args.M;
-  if (m0 >= M_live) {
+  if (m0 >= M_live) {   // (uniform over a split-K cluster: one M tile)
     // Tile has no live rows.  Complete the in-flight copies before leaving.
     if (warp == 0 && lane == 0)
       for (int s = 0; s < stages; ++s) mbar_wait(&full_bar[s], 0);
@@ -464,10 +488,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mbar_arrive_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
 #pragma unroll
         for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
-          tma_load_2d(sb + j * 64 * BK, &tmB, &full_bar[s], kb * BK, n0 + j * 64);
-        tma_load_2d(sa, &tmA, &full_bar[s], kb * BK, m0);
-        tma_load_2d(sa + 64 * BK, &tmA, &full_bar[s], kb * BK, m0 + 64);
+          tma_load_2d(sb + j * 64 * BK, &tmB, &full_bar[s], (kb0 + kb) * BK, n0 + j * 64);
+        tma_load_2d(sa, &tmA, &full_bar[s], (kb0 + kb) * BK, m0);
+        tma_load_2d(sa + 64 * BK, &tmA, &full_bar[s], (kb0 + kb) * BK, m0 + 64);
       }
+    }
+    __syncwarp();
+    if (ks > 1) {   // phase 1 wait + phase 2 (partials added) of the split-K exchange
+      cluster_wait();
+      cluster_arrive();
+      cluster_wait();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -492,6 +522,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       mma_commit(&tmem_full_bar);   // accumulator complete
     }
+    __syncwarp();
+    if (ks > 1) {
+      cluster_wait();
+      cluster_arrive();
+      cluster_wait();
+    }
   } else {
     // ---------------- epilogue: warps 2..9; TMEM lane quarter = warp % 4 (hardware rule),
     // column half = (warp - 2) / 4.
@@ -510,11 +546,36 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // from the MMA warp after its last commit no different)
     if (warp == 2 && lane == 0) pdl_launch_dependents();
     const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + half * HALF;
-    float* stage = reinterpret_cast<float*>(smem + stages * Cfg::STAGE_BYTES) +
+    float* stage = reinterpret_cast<float*>(smem + ring * Cfg::STAGE_BYTES) +
                    (warp - 2) * EPI_STAGE_FLOATS;
     float best_v = -INFINITY;
     int best_j = -1;
-    if constexpr (is_topk(EPI)) {
+    const int rl = q * 32 + lane;   // row within the tile (TMEM lane)
+    if (ks > 1) {
+      // split-K exchange: CTAs z > 0 add the live lane quarters of their partial accumulators
+      // into the leader's buffer; the leader adds the buffer to its own before the epilogue
+      __syncwarp();
+      cluster_wait();   // phase 1: the leader's buffer is zeroed (and every CTA is running)
+      if (kz > 0 && m0 + q * 32 < M_live) {
+        constexpr int CWX = HALF < 32 ? 16 : 32;
+        const uint32_t base = mapa_shared(smem_u32(red + rl * Cfg::RED_LD + half * HALF), 0);
+#pragma unroll 1
+        for (int c = 0; c < HALF; c += CWX) {
+          int32_t acc[32];
+          tmem_ld16(t_row + c, *reinterpret_cast<int32_t(*)[16]>(acc));
+          if constexpr (CWX == 32) tmem_ld16(t_row + c + 16, *reinterpret_cast<int32_t(*)[16]>(acc + 16));
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < CWX; ++j) red_add_cluster_s32(base + 4 * (c + j), acc[j]);
+        }
+      }
+      __syncwarp();
+      cluster_arrive();   // phase 2 (release): partials added
+      cluster_wait();
+    }
+    if (ks > 1 && kz > 0) {
+      // partials delivered; nothing to store
+    } else if constexpr (is_topk(EPI)) {
       topk_epilogue<BN, topk_k(EPI)>(args, args.bias ? bias_s - n0 : nullptr, t_row, row, row_ok,
                                      half, n0, exp_tab);
     } else
@@ -524,6 +585,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tmem_ld16(t_row + c, *reinterpret_cast<int32_t(*)[16]>(acc));
       if constexpr (CW == 32) tmem_ld16(t_row + c + 16, *reinterpret_cast<int32_t(*)[16]>(acc + 16));
       tmem_ld_wait();
+      if (ks > 1) {   // + the other K ranges' partials (exact s32)
+        const int32_t* rp = red + rl * Cfg::RED_LD + half * HALF + c;
+#pragma unroll
+        for (int j = 0; j < CW; ++j) acc[j] += rp[j];
+      }
       if (c == 0 && warp == 2 && lane == 0) GEMM_TRACE(6);
       const int n = n0 + half * HALF + c;
       if (n >= args.N) break;  // warp-uniform
@@ -537,6 +603,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if constexpr (EPI == EPI_ARGMAX) {
       if (row_ok && best_j >= 0) atomicMax(args.keys + row, argmax_key(best_v, (uint32_t)best_j));
     }
+    (void)rl;
     if (warp == 2 && lane == 0) GEMM_TRACE(4);   // this warp's stores issued
   }
 
@@ -781,31 +848,72 @@ static cudaError_t launch_pers_t(const CUtensorMap& tmA, const CUtensorMap& tmB,
   return cudaLaunchKernelEx(&cfg, k_gemm_pers<BN, EPI>, tmA, tmB, a);
 }
 
+// Split-K factor of a non-persistent launch: deep K (>= 1024) and a grid that leaves most SMs
+// idle (the decoder GEMMs of the big student at small row counts, where each CTA would stream
+// its whole K range alone).  Powers of two up to 8 (portable cluster size) while the split grid
+// fits the launch's SM budget and every CTA keeps >= 1 K block.  Env MNMT_SPLITK=0 disables
+// (A/B), MNMT_SPLITK_KMIN sets the shallowest K (default 1024).
+static int gemm_split_k(const GemmArgs& a, int bn, int epi) {
+  static const int mode = [] {
+    const char* e = getenv("MNMT_SPLITK");
+    return e ? atoi(e) : 0;
+  }();
+  static const int kmin = [] {
+    const char* e = getenv("MNMT_SPLITK_KMIN");
+    return e ? atoi(e) : 1024;
+  }();
+  if (!mode || bn > 128 || a.K < kmin) return 1;
+  if (!(epi == EPI_F32 || epi == EPI_F32_Q || epi == EPI_RELU_Q || epi == EPI_RELU_F32_Q ||
+        epi == EPI_SIGMOID || epi == EPI_ACC))
+    return 1;
+  const int sms = a.pers_grid > 0 ? a.pers_grid : num_sms();
+  const long tiles = (long)((a.N + bn - 1) / bn) * ((a.M + BM - 1) / BM);
+  const int kb_all = (a.K + BK - 1) / BK;
+  int ks = 1;
+  while (ks < 8 && tiles * ks * 2 <= sms && kb_all >= ks * 2) ks *= 2;
+  while (ks > 1 && kb_all - (ks - 1) * ((kb_all + ks - 1) / ks) < 1) ks /= 2;   // no empty range
+  return ks;
+}
+
 template <int BN, int EPI>
 static cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                             cudaStream_t st) {
   if constexpr (BN >= 64)   // BN = 32 (16-column epilogue chunks) is never persistent
     if (gemm_persistent(a.M, a.N, BN, a.pers_grid)) return launch_pers_t<BN, EPI>(tmA, tmB, a, st);
   using Cfg = GemmCfg<BN>;
-  dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM);
-  const int num_kb = (a.K + BK - 1) / BK;
+  const int ks = gemm_split_k(a, BN, EPI);
+  dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, ks);
+  const int num_kb = (a.K + BK - 1) / BK, kb_per = (num_kb + ks - 1) / ks;
+  GemmArgs b = a;
+  int ring = kb_per < Cfg::STAGES ? kb_per : Cfg::STAGES;
+  size_t smem = Cfg::smem_for(ring);
+  if (ks > 1) {   // + the leader's partial buffer; the ring shrinks to fit
+    const int cap = (int)((GEMM_SMEM_MAX - 1024 - EPI_STAGE_BYTES - Cfg::RED_BYTES) / Cfg::STAGE_BYTES);
+    if (ring > cap) ring = cap;
+    b.ring_cap = ring;
+    smem = Cfg::smem_for(ring) + Cfg::RED_BYTES;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(GEMM_THREADS);
-  cfg.dynamicSmemBytes = Cfg::smem_for(num_kb < Cfg::STAGES ? num_kb : Cfg::STAGES);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = ks;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_gemm_i8<BN, EPI>, tmA, tmB, a);
+  cfg.numAttrs = ks > 1 ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, k_gemm_i8<BN, EPI>, tmA, tmB, b);
 }
 
 template <int BN, int EPI>
 static cudaError_t set_attr() {
   cudaError_t e = cudaFuncSetAttribute(k_gemm_i8<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       GemmCfg<BN>::smem_for(GemmCfg<BN>::STAGES));
+                                       std::max<int>(GemmCfg<BN>::smem_for(GemmCfg<BN>::STAGES), GEMM_SMEM_MAX));
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_gemm_pers<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               PersCfg<BN>::SMEM);
@@ -816,7 +924,7 @@ static cudaError_t set_attr_bn32() {
                         (const void*)k_gemm_i8<32, EPI_RELU_Q>, (const void*)k_gemm_i8<32, EPI_RELU_F32_Q>,
                         (const void*)k_gemm_i8<32, EPI_SIGMOID>}) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         GemmCfg<32>::smem_for(GemmCfg<32>::STAGES));
+                                         std::max<int>(GemmCfg<32>::smem_for(GemmCfg<32>::STAGES), GEMM_SMEM_MAX));
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

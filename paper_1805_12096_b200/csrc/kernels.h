@@ -69,6 +69,7 @@ struct GemmArgs {
   int smallm_force;            // op level: take the small-M path whenever it can run (M <= 32)
   int smallm_rows;             // small-M path row bound of the launch (0 = off, <= SMALLM_MAX)
   int smallm_kmax;             // deepest K the small-M path takes
+  int ring_cap;                // (launch-internal) TMA ring depth cap of a split-K launch
 };
 
 constexpr int SMALLM_MAX = 32;

@@ -148,6 +148,82 @@ __device__ __forceinline__ void ln_row(const LnArgs a, int r, const float* vsm =
   }
 }
 
+// ------------------------------------------------------------------ residual + LayerNorm, W warps per row
+// For wide rows (d = 256 W: 8 elements per thread, float4 columns lane + 32 w and that + d/8)
+// the row is split over W warps so the fp64 sums run as short per-thread chains: per-thread
+// partial sums (its elements in order), warp tree, then the W warp partials combined in warp
+// order through shared memory (red: [rows per block][W] doubles).  Same arithmetic as ln_row
+// (R20: fp64 sums in another order, one rounding to fp32).
+template <int W>
+__device__ __forceinline__ void ln_row_split(const LnArgs a, int r, double* red, bool store) {
+  const int tid = threadIdx.x % (32 * W), wr = tid >> 5, lane = threadIdx.x & 31;
+  const int d = a.d;
+  const int64_t off = (int64_t)r * d;
+  const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
+  const int orig = a.aan.C ? a.live[r] : 0;
+  const float tf = a.aan.C ? (float)a.ctrl[1] : 1.0f;
+  const int c0 = 4 * tid, c1 = 4 * (tid + 32 * W);   // the thread's two float4 columns
+  float4 v[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int c = i ? c1 : c0;
+    const float4 x = ld4(a.x + off + c);
+    float4 z;
+    if (a.gi) {
+      // AAN gate (R8): r = fl(y + fl(fl(s(gi) * y) + fl(s(gf) * a)))
+      const float4 li = ld4(a.gi + off + c), lf = ld4(a.gf + off + c);
+      const float4 si = make_float4(sigmoid_f64(li.x), sigmoid_f64(li.y), sigmoid_f64(li.z), sigmoid_f64(li.w));
+      const float4 sf = make_float4(sigmoid_f64(lf.x), sigmoid_f64(lf.y), sigmoid_f64(lf.z), sigmoid_f64(lf.w));
+      z = add4(mul4(si, x), mul4(sf, ld4(a.delta + off + c)));
+    } else {
+      z = ld4(a.delta + off + c);
+    }
+    v[i] = add4(x, z);
+  }
+  double s = __dadd_rn(__dadd_rn(__dadd_rn((double)v[0].x, (double)v[0].y), (double)v[0].z), (double)v[0].w);
+  s = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(s, (double)v[1].x), (double)v[1].y), (double)v[1].z), (double)v[1].w);
+  s = warp_sum_f64(s);
+  if (lane == 0) red[wr] = s;
+  __syncthreads();
+  double tot = red[0];
+#pragma unroll
+  for (int k = 1; k < W; ++k) tot = __dadd_rn(tot, red[k]);
+  const double mu = __ddiv_rn(tot, (double)d);
+  double q = 0.0;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double t0 = __dsub_rn((double)v[i].x, mu), t1 = __dsub_rn((double)v[i].y, mu);
+    const double t2 = __dsub_rn((double)v[i].z, mu), t3 = __dsub_rn((double)v[i].w, mu);
+    q = __dadd_rn(q, __dmul_rn(t0, t0));
+    q = __dadd_rn(q, __dmul_rn(t1, t1));
+    q = __dadd_rn(q, __dmul_rn(t2, t2));
+    q = __dadd_rn(q, __dmul_rn(t3, t3));
+  }
+  q = warp_sum_f64(q);
+  __syncthreads();   // every thread has read red[] (mean) before it is reused
+  if (lane == 0) red[wr] = q;
+  __syncthreads();
+  double qt = red[0];
+#pragma unroll
+  for (int k = 1; k < W; ++k) qt = __dadd_rn(qt, red[k]);
+  const double var = __ddiv_rn(qt, (double)d);
+  const double inv = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(var, (double)a.eps)));
+  if (!store || r >= n_live) return;   // after the last barrier
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int c = i ? c1 : c0;
+    const float4 g = ld4(a.gamma + c), b = ld4(a.beta + c);
+    float4 o;
+    o.x = (float)__dadd_rn(__dmul_rn(__dmul_rn(__dsub_rn((double)v[i].x, mu), inv), (double)g.x), (double)b.x);
+    o.y = (float)__dadd_rn(__dmul_rn(__dmul_rn(__dsub_rn((double)v[i].y, mu), inv), (double)g.y), (double)b.y);
+    o.z = (float)__dadd_rn(__dmul_rn(__dmul_rn(__dsub_rn((double)v[i].z, mu), inv), (double)g.z), (double)b.z);
+    o.w = (float)__dadd_rn(__dmul_rn(__dmul_rn(__dsub_rn((double)v[i].w, mu), inv), (double)g.w), (double)b.w);
+    if (a.out) st4(a.out + off + c, o);
+    if (a.out_q) *reinterpret_cast<uint32_t*>(a.out_q + off + c) = q8x4(o, a.clip, a.sigma);
+    if (a.aan.C) aan4(a.aan.C + (int64_t)orig * d, o, tf, a.aan, off, c);
+  }
+}
+
 // ------------------------------------------------------------------ attention
 // fp64 scores / softmax / context (R20).  Dot products run over the head dimension in
 // order and context sums over positions in order (the plain definition); the max and the

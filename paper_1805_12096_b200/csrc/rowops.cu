@@ -110,6 +110,20 @@ __global__ void k_ln(LnArgs a) {
   ln_row<NV>(a, r);   // checks the live-row count itself, after issuing its loads
 }
 
+// Wide rows (d = 256 W, W >= 2): W warps per row, 256-thread blocks (256 / (32 W) rows each).
+template <int W>
+__global__ void __launch_bounds__(256) k_ln_split(LnArgs a) {
+  __shared__ double red[256 / 32];
+  pdl_wait();
+  pdl_trigger_early();
+  constexpr int RPB = 256 / (32 * W);
+  const int rb = threadIdx.x / (32 * W);
+  const int r = blockIdx.x * RPB + rb;
+  // rows past the static bound compute a clamped row (every thread reaches every barrier)
+  // and store nothing
+  ln_row_split<W>(a, min(r, a.n - 1), red + rb * W, r < a.n);
+}
+
 constexpr int ATTN_WARPS = 8;
 
 // Decoder (SRC, SELF) and op-level (ENC) attention: one warp per (row, head) (warp_attend).
@@ -482,6 +496,17 @@ cudaError_t launch_embed_tgt(const EmbedTgtArgs& a_in, int rows, cudaStream_t st
 
 cudaError_t launch_ln(const LnArgs& a, cudaStream_t st) {
   if (a.n <= 0) return cudaSuccess;
+  // wide rows: W = d / 256 warps per row (env MNMT_LN_SPLIT=0: warp per row, A/B)
+  static const bool split = [] {
+    const char* e = getenv("MNMT_LN_SPLIT");
+    return !(e && e[0] == '0');
+  }();
+  if (split && (a.d == 512 || a.d == 1024)) {
+    const int W = a.d / 256, rpb = 256 / (32 * W);
+    dim3 grid((a.n + rpb - 1) / rpb), block(256);
+    return W == 2 ? launch_pdl(k_ln_split<2>, grid, block, 0, st, a)
+                  : launch_pdl(k_ln_split<4>, grid, block, 0, st, a);
+  }
   dim3 grid((a.n + ROW_WARPS - 1) / ROW_WARPS), block(32 * ROW_WARPS);
   switch (nv_for(a.d)) {
     case 1: return launch_pdl(k_ln<1>, grid, block, 0, st, a);

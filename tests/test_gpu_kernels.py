@@ -62,8 +62,31 @@ def test_gemm_acc_bitexact(Mr, N, K, bn):
     assert np.array_equal(out.cpu().numpy(), O.gemm_acc(a, w))
 
 
+# split-K (K >= 1024 on a grid that leaves SMs idle): the K blocks of one output tile are spread
+# over a cluster of 2 / 4 / 8 CTAs whose s32 partials are added in the leader's shared memory
+SPLIT_K_SHAPES = [
+    (1, 1024, 1024, 64),      # 16 tiles x 8 (one K block per CTA)
+    (128, 1024, 4096, 64),    # 16 x 8, four K blocks each
+    (100, 3072, 1024, 0),     # 48 x 2
+    (200, 1024, 2048, 128),   # 2 M tiles x 8 N tiles x 8
+    (37, 4096, 1024, 0),      # 64 x 2
+    (70, 1024, 1040, 64),     # ragged K: 9 blocks -> 2 ranges of 5 / 4
+    (257, 1024, 1024, 64),    # three M tiles, a ragged one
+]
+
+
+@pytest.mark.parametrize("Mr,N,K,bn", SPLIT_K_SHAPES)
+def test_gemm_split_k_acc_bitexact(Mr, N, K, bn):
+    a = rand_codes((Mr, K), Mr + K + 1)
+    w = rand_codes((N, K), N + 9)
+    out = empty((Mr, N), torch.int32)
+    M.op_gemm_i8(ptr(to_dev(a)), ptr(to_dev(w)), Mr, N, K, None, CLIP, M.EPI_ACC, ptr(out), None, bn)
+    sync()
+    assert np.array_equal(out.cpu().numpy(), O.gemm_acc(a, w))
+
+
 @pytest.mark.parametrize("epi", [M.EPI_F32, M.EPI_F32_Q, M.EPI_RELU_Q, M.EPI_RELU_F32_Q, M.EPI_SIGMOID])
-@pytest.mark.parametrize("Mr,N,K", [(5, 256, 256), (260, 2048, 512), (131, 512, 2048),
+@pytest.mark.parametrize("Mr,N,K", [(5, 256, 256), (33, 1024, 1024), (120, 1024, 4096), (260, 2048, 512), (131, 512, 2048),
                                     (70, 160, 256), (1, 32, 64),   # 32-wide tiles, ragged N
                                     (4700, 2048, 256)])   # last: persistent kernel
 def test_gemm_epilogues_bitexact(epi, Mr, N, K):
