@@ -175,12 +175,16 @@ mnmt_status mnmt_beam_translate(mnmt_model* m, const int32_t* src_ids, const int
  *   MNMT_DUMP_DEC_OUT   fp32 [sum T_i][d]         last decoder layer output per step
  *   MNMT_DUMP_OUT_CODES int8 [sum T_i][d]         Q(dec_out): the output-layer operand
  *   MNMT_DUMP_LAYERS    fp32 [sum T_i][L][3][d]   x1, x2, x3 of every decoder layer
+ *   MNMT_DUMP_MARGIN    fp32 [sum T_i]            top2_margin: largest minus second largest
+ *                                                 output logit of the step (near-tie flag of
+ *                                                 the parity protocol), (float)((double)v1 - v2)
  * Errors as mnmt_decode; MNMT_ERR_CAPACITY if dump_cap is too small. */
 #define MNMT_DUMP_ENC_OUT 1u
 #define MNMT_DUMP_SRC_KV 2u
 #define MNMT_DUMP_DEC_OUT 4u
 #define MNMT_DUMP_OUT_CODES 8u
 #define MNMT_DUMP_LAYERS 16u
+#define MNMT_DUMP_MARGIN 32u
 mnmt_status mnmt_decode_forced(mnmt_model* m, const int32_t* src_ids_host,
                                const int64_t* src_off_host, int32_t n,
                                const int32_t* forced_ids_host, const int64_t* forced_off_host,

@@ -49,15 +49,16 @@ struct GemmCfg {
   static constexpr int STAGES = (190 * 1024 / STAGE_BYTES) > 8 ? 8 : (190 * 1024 / STAGE_BYTES);
   static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
   static constexpr int smem_for(int stages) { return stages * STAGE_BYTES + 1024 + EPI_STAGE_BYTES; }
-  // split-K (gridDim.z > 1, one cluster along z): the s32 partials of CTAs z > 0 are added
-  // into CTA 0's [128][BN + 1] buffer (exact integer adds: the order cannot matter)
-  static constexpr int RED_LD = BN + 1;
-  static constexpr int RED_BYTES = BM * RED_LD * 4;
+  // split-K (gridDim.z > 1, one cluster along z): CTA z > 0 stores its s32 partial tile into
+  // slot z - 1 of CTA 0's buffer [ks - 1][128][BN + 4]; CTA 0 adds the slots (exact integers)
+  static constexpr int RED_LD = BN + 4;
+  static constexpr int RED_SLOT_BYTES = BM * RED_LD * 4;
 };
 
-// Split-K partial accumulation into the cluster leader's buffer (distributed shared memory).
-__device__ __forceinline__ void red_add_cluster_s32(uint32_t addr, int32_t v) {
-  asm volatile("red.relaxed.cluster.shared::cluster.add.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+// 16-byte store into another CTA's shared memory (distributed shared memory).
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, int32_t a, int32_t b, int32_t c, int32_t d) {
+  asm volatile("st.shared::cluster.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d) : "memory");
 }
 
 // Exact (float)acc for |acc| < 2^22 without the quarter-rate I2F: place acc in the
@@ -414,13 +415,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   int32_t* red = reinterpret_cast<int32_t*>(smem + ring * Cfg::STAGE_BYTES + EPI_STAGE_BYTES);
-  if (ks > 1) {
-    if (kz == 0) {   // the leader's partial buffer starts at zero
-      for (int i = threadIdx.x; i < Cfg::RED_BYTES / 16; i += GEMM_THREADS)
-        reinterpret_cast<int4*>(red)[i] = make_int4(0, 0, 0, 0);
-    }
-    cluster_arrive();   // phase 1 (release): the leader's buffer is zeroed; waited on before use
-  }
+  if (ks > 1) cluster_arrive_relaxed();   // phase 1: this CTA is running (DSMEM valid)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -555,10 +550,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // split-K exchange: CTAs z > 0 add the live lane quarters of their partial accumulators
       // into the leader's buffer; the leader adds the buffer to its own before the epilogue
       __syncwarp();
-      cluster_wait();   // phase 1: the leader's buffer is zeroed (and every CTA is running)
+      cluster_wait();   // phase 1: every CTA of the cluster is running
       if (kz > 0 && m0 + q * 32 < M_live) {
         constexpr int CWX = HALF < 32 ? 16 : 32;
-        const uint32_t base = mapa_shared(smem_u32(red + rl * Cfg::RED_LD + half * HALF), 0);
+        const uint32_t base = mapa_shared(
+            smem_u32(red + (kz - 1) * (Cfg::RED_SLOT_BYTES / 4) + rl * Cfg::RED_LD + half * HALF), 0);
 #pragma unroll 1
         for (int c = 0; c < HALF; c += CWX) {
           int32_t acc[32];
@@ -566,7 +562,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if constexpr (CWX == 32) tmem_ld16(t_row + c + 16, *reinterpret_cast<int32_t(*)[16]>(acc + 16));
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < CWX; ++j) red_add_cluster_s32(base + 4 * (c + j), acc[j]);
+          for (int j = 0; j < CWX; j += 4)
+            st_cluster_v4(base + 4 * (c + j), acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
         }
       }
       __syncwarp();
@@ -586,9 +583,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if constexpr (CW == 32) tmem_ld16(t_row + c + 16, *reinterpret_cast<int32_t(*)[16]>(acc + 16));
       tmem_ld_wait();
       if (ks > 1) {   // + the other K ranges' partials (exact s32)
-        const int32_t* rp = red + rl * Cfg::RED_LD + half * HALF + c;
+        for (int z = 1; z < ks; ++z) {
+          const int4* rp = reinterpret_cast<const int4*>(red + (z - 1) * (Cfg::RED_SLOT_BYTES / 4) +
+                                                         rl * Cfg::RED_LD + half * HALF + c);
 #pragma unroll
-        for (int j = 0; j < CW; ++j) acc[j] += rp[j];
+          for (int j = 0; j < CW / 4; ++j) {
+            const int4 p = rp[j];
+            acc[4 * j] += p.x; acc[4 * j + 1] += p.y; acc[4 * j + 2] += p.z; acc[4 * j + 3] += p.w;
+          }
+        }
       }
       if (c == 0 && warp == 2 && lane == 0) GEMM_TRACE(6);
       const int n = n0 + half * HALF + c;
@@ -848,21 +851,26 @@ static cudaError_t launch_pers_t(const CUtensorMap& tmA, const CUtensorMap& tmB,
   return cudaLaunchKernelEx(&cfg, k_gemm_pers<BN, EPI>, tmA, tmB, a);
 }
 
-// Split-K factor of a non-persistent launch: deep K (>= 1024) and a grid that leaves most SMs
-// idle (the decoder GEMMs of the big student at small row counts, where each CTA would stream
-// its whole K range alone).  Powers of two up to 8 (portable cluster size) while the split grid
-// fits the launch's SM budget and every CTA keeps >= 1 K block.  Env MNMT_SPLITK=0 disables
-// (A/B), MNMT_SPLITK_KMIN sets the shallowest K (default 1024).
+// Split-K factor of a non-persistent launch: deep K and a grid that leaves most SMs idle (FFN2
+// of the base / big students at small row counts, where each CTA would stream its whole
+// K = F range alone).  Powers of two while the split grid fits the launch's SM budget, every
+// CTA keeps >= 1 K block and the leader's partial slots fit its shared memory (<= 4 for
+// BN = 64).  Measured (profiles/r2_gemm_splitk.txt, warm PDL chain): big FFN2 (K = 4096)
+// 10.5 -> 6.0 us at <= 32 rows, 10.7 -> 8.7 at 128; base FFN2 (K = 2048) 6.5 -> 5.0 at <= 32
+// rows but 6.7 -> 7.6 at 128; K = 1024 neutral at <= 32 rows and slower at 128-256 (the
+// partial tiles cross distributed shared memory).  Hence: K >= 4096, or K >= 2048 with a
+// <= 32-row bound.  Env MNMT_SPLITK=0 disables (A/B), MNMT_SPLITK_KMIN overrides the rule's K.
 static int gemm_split_k(const GemmArgs& a, int bn, int epi) {
   static const int mode = [] {
     const char* e = getenv("MNMT_SPLITK");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : 1;
   }();
   static const int kmin = [] {
     const char* e = getenv("MNMT_SPLITK_KMIN");
-    return e ? atoi(e) : 1024;
+    return e ? atoi(e) : 0;
   }();
-  if (!mode || bn > 128 || a.K < kmin) return 1;
+  if (!mode || bn > 128) return 1;
+  if (kmin > 0 ? a.K < kmin : !(a.K >= 4096 || (a.K >= 2048 && a.M <= 32))) return 1;
   if (!(epi == EPI_F32 || epi == EPI_F32_Q || epi == EPI_RELU_Q || epi == EPI_RELU_F32_Q ||
         epi == EPI_SIGMOID || epi == EPI_ACC))
     return 1;
@@ -870,7 +878,11 @@ static int gemm_split_k(const GemmArgs& a, int bn, int epi) {
   const long tiles = (long)((a.N + bn - 1) / bn) * ((a.M + BM - 1) / BM);
   const int kb_all = (a.K + BK - 1) / BK;
   int ks = 1;
-  while (ks < 8 && tiles * ks * 2 <= sms && kb_all >= ks * 2) ks *= 2;
+  // the leader holds ks - 1 partial slots next to its ring and epilogue staging
+  const int slot = BM * (bn + 4) * 4;
+  while (ks < 8 && tiles * ks * 2 <= sms && kb_all >= ks * 2 &&
+         (long)(2 * ks - 1) * slot + 1024 + EPI_STAGE_BYTES + 2 * (BM + 64) * BK <= GEMM_SMEM_MAX)
+    ks *= 2;
   while (ks > 1 && kb_all - (ks - 1) * ((kb_all + ks - 1) / ks) < 1) ks /= 2;   // no empty range
   return ks;
 }
@@ -888,10 +900,11 @@ static cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
   int ring = kb_per < Cfg::STAGES ? kb_per : Cfg::STAGES;
   size_t smem = Cfg::smem_for(ring);
   if (ks > 1) {   // + the leader's partial buffer; the ring shrinks to fit
-    const int cap = (int)((GEMM_SMEM_MAX - 1024 - EPI_STAGE_BYTES - Cfg::RED_BYTES) / Cfg::STAGE_BYTES);
+    const int red_bytes = (ks - 1) * Cfg::RED_SLOT_BYTES;
+    const int cap = (int)((GEMM_SMEM_MAX - 1024 - EPI_STAGE_BYTES - red_bytes) / Cfg::STAGE_BYTES);
     if (ring > cap) ring = cap;
     b.ring_cap = ring;
-    smem = Cfg::smem_for(ring) + Cfg::RED_BYTES;
+    smem = Cfg::smem_for(ring) + red_bytes;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;

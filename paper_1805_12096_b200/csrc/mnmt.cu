@@ -164,7 +164,8 @@ struct DevDump {
   float* layers = nullptr;      // [O][L][3][d]: x1, x2, x3 of every decoder layer
   float* dec_out = nullptr;     // [O][d]
   int8_t* out_codes = nullptr;  // [O][d]
-  bool any() const { return layers || dec_out || out_codes; }
+  float* margin = nullptr;      // [O]: top-1 minus top-2 logit of each step
+  bool any() const { return layers || dec_out || out_codes || margin; }
 };
 
 }  // namespace
@@ -1071,6 +1072,26 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, int6
     *nlaunch += k;
     return cudaSuccess;
   }
+  if (dd.margin) {
+    // test hook: the step's top-2 logit margin from an EPI_TOPK2 pass over the same operands
+    GemmArgs a{};
+    a.M = n;
+    a.M_dyn = nd;
+    a.N = c.vocab;
+    a.K = d;
+    a.scale = scale_of(m);
+    a.bias = c.out_bias ? m->out_b : nullptr;
+    a.clip = c.clip;
+    a.sigma = sigma_of(m);
+    a.col_block = c.vocab;
+    a.part = w.part;
+    a.part_ld = w.part_ld;
+    if ((e = launch_gemm_i8(w.tm_cy, m->tmE, a, EPI_TOPK2, 0, st)) != cudaSuccess) return e;
+    if ((e = launch_top2_margin(w.part, w.part_ld, 2 * ((c.vocab + TOPK_BN - 1) / TOPK_BN), n, w.ctrl,
+                                w.live, w.forced_off, dd.margin, st)) != cudaSuccess)
+      return e;
+    k += 2;
+  }
   // A9: tied output projection fused with the argmax (softmax skipped)
   {
     GemmArgs a{};
@@ -1817,7 +1838,7 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
   } dump_reset{m, {}};
   const int64_t dL = m->c.dec_layers, dd = m->c.d_model;
   const uint32_t dmask = forced ? fz->dump_mask : 0u;
-  if (dmask & (MNMT_DUMP_LAYERS | MNMT_DUMP_DEC_OUT | MNMT_DUMP_OUT_CODES)) {
+  if (dmask & (MNMT_DUMP_LAYERS | MNMT_DUMP_DEC_OUT | MNMT_DUMP_OUT_CODES | MNMT_DUMP_MARGIN)) {
     auto dev = [&](void** p, int64_t bytes) -> mnmt_status {
       CK(cudaMalloc(p, std::max<int64_t>(bytes, 1)));
       dump_reset.bufs.push_back(*p);
@@ -1826,6 +1847,11 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
     if (dmask & MNMT_DUMP_LAYERS) CKS(dev((void**)&m->dump.layers, O * dL * 3 * dd * 4));
     if (dmask & MNMT_DUMP_DEC_OUT) CKS(dev((void**)&m->dump.dec_out, O * dd * 4));
     if (dmask & MNMT_DUMP_OUT_CODES) CKS(dev((void**)&m->dump.out_codes, O * dd));
+    if (dmask & MNMT_DUMP_MARGIN) {
+      CKS(dev((void**)&m->dump.margin, O * 4));
+      for (size_t li = 0; li < m->lanes.size(); ++li)   // the EPI_TOPK2 partials
+        if (li < job.lane_B.size() && job.lane_B[li] > 0) CKS(beam_ensure(m, m->lanes[li]));
+    }
     for (Lane& L : m->lanes) {   // capture fresh graphs with the dump kernels
       for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
       L.graphs.clear();
@@ -1858,6 +1884,7 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
     if (m->dump.dec_out) { CK(cudaMemcpyAsync(p, m->dump.dec_out, O * dd * 4, cudaMemcpyDeviceToHost, m->st)); p += O * dd * 4; }
     if (m->dump.out_codes) { CK(cudaMemcpyAsync(p, m->dump.out_codes, O * dd, cudaMemcpyDeviceToHost, m->st)); p += O * dd; }
     if (m->dump.layers) { CK(cudaMemcpyAsync(p, m->dump.layers, O * dL * 3 * dd * 4, cudaMemcpyDeviceToHost, m->st)); p += O * dL * 3 * dd * 4; }
+    if (m->dump.margin) { CK(cudaMemcpyAsync(p, m->dump.margin, O * 4, cudaMemcpyDeviceToHost, m->st)); p += O * 4; }
   }
   const cudaMemcpyKind dk = dev_io ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   if (O > 0) CK(cudaMemcpyAsync(out_ids, w.out_ids, O * 4, dk, m->st));
@@ -1964,6 +1991,7 @@ static mnmt_status forced_impl(mnmt_model* m, const int32_t* src_ids, const int6
   if (dump_mask & MNMT_DUMP_DEC_OUT) need += O * d * 4;
   if (dump_mask & MNMT_DUMP_OUT_CODES) need += O * d;
   if (dump_mask & MNMT_DUMP_LAYERS) need += O * L * 3 * d * 4;
+  if (dump_mask & MNMT_DUMP_MARGIN) need += O * 4;
   if (need > 0 && (!dump_host || dump_cap < need)) { set_err("dump_cap %lld < %lld", (long long)dump_cap, (long long)need); return MNMT_ERR_CAPACITY; }
   std::vector<int32_t> lens(std::max(n, 1));
   const Forced fz{forced_ids, forced_off, dump_mask, need > 0 ? dump_host : nullptr};

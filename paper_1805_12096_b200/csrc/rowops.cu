@@ -551,6 +551,7 @@ cudaError_t attn_init() {   // once per device
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              ATTN_WARPS * (MNMT_MAX_KV + 64) * (int)sizeof(double));
+
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn_split<2, bf16s>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)attn_split_smem(2, MNMT_MAX_KV));
@@ -603,6 +604,7 @@ cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
   const int64_t warps = (int64_t)a.n * a.H;
   AttnArgs b = a;
   if (b.span <= 0 || b.span > MNMT_MAX_KV) b.span = MNMT_MAX_KV;
+
   if (b.dh > 64 || (b.dh & 3)) return cudaErrorInvalidValue;
   // long source spans at small row counts: several warps per (row, head) (measured: -6 % per
   // step at 64 rows with 100-word sources; at 206 rows the extra warps cost more than they save)
@@ -617,7 +619,8 @@ cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
                    : launch_pdl(k_attn_split<4, float>, grid, block, attn_split_smem(4, b.span), st, b);
   }
   const dim3 grid((unsigned)((warps + ATTN_WARPS - 1) / ATTN_WARPS)), block(ATTN_WARPS * 32);
-  return launch_pdl(k_attn, grid, block, (size_t)ATTN_WARPS * (b.span + 64) * 8, st, b);
+  const size_t smem = (size_t)ATTN_WARPS * (b.span + 64) * 8;
+  return launch_pdl(k_attn, grid, block, smem, st, b);
 }
 
 cudaError_t launch_attn_enc(const EncAttnArgs& a, cudaStream_t st) {
@@ -634,6 +637,43 @@ cudaError_t launch_attn_enc(const EncAttnArgs& a, cudaStream_t st) {
 
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t st) {
   return launch_pdl(k_finish, dim3(1), dim3(FIN_THREADS), 0, st, a);
+}
+
+// One warp per live row: each lane keeps the two largest values of its partials (a multiset:
+// equal values both count), then a warp merge.
+__global__ void k_top2_margin(const TopkPart* __restrict__ part, int part_ld, int n_part, int n,
+                              const int32_t* ctrl, const int32_t* live, const int64_t* foff,
+                              float* dst) {
+  pdl_wait();
+  pdl_trigger_early();
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= n || r >= ctrl[0]) return;
+  float a = -INFINITY, b = -INFINITY;   // a >= b
+  for (int p = lane; p < n_part; p += 32) {
+    const TopkPart& P = part[(int64_t)r * part_ld + p];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float v = P.v[i];
+      if (v > a) { b = a; a = v; } else if (v > b) { b = v; }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const float oa = __shfl_xor_sync(0xffffffffu, a, o), ob = __shfl_xor_sync(0xffffffffu, b, o);
+    const float hi = fmaxf(a, oa), lo = fminf(a, oa);
+    b = fmaxf(lo, fmaxf(b, ob));
+    a = hi;
+  }
+  if (lane == 0)
+    dst[foff[live[r]] + ctrl[1] - 1] = b == -INFINITY ? INFINITY : (float)__dsub_rn((double)a, (double)b);
+}
+
+cudaError_t launch_top2_margin(const TopkPart* part, int part_ld, int n_part, int n,
+                               const int32_t* ctrl, const int32_t* live, const int64_t* foff,
+                               float* dst, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  return launch_pdl(k_top2_margin, dim3((n + ROW_WARPS - 1) / ROW_WARPS), dim3(32 * ROW_WARPS), 0, st,
+                    part, part_ld, n_part, n, ctrl, live, foff, dst);
 }
 
 cudaError_t launch_dump_rows(const DumpArgs& a, cudaStream_t st) {

@@ -141,6 +141,14 @@ cudaError_t launch_attn_enc(const EncAttnArgs& a, cudaStream_t st);
 cudaError_t attn_init();   // dynamic-smem attribute (call once per device, outside capture)
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t st);
 cudaError_t launch_dump_rows(const DumpArgs& a, cudaStream_t st);
+// Teacher-forced top-2 margin dump (test hook): live row r's output
+// logits' largest minus second largest value, (float)((double)v1 - (double)v2), from the
+// per-tile top-2 partials of an EPI_TOPK2 output GEMM ([rows][part_ld], n_part used), written
+// to dst[foff[live[r]] + t - 1].
+struct TopkPart;
+cudaError_t launch_top2_margin(const TopkPart* part, int part_ld, int n_part, int n,
+                               const int32_t* ctrl, const int32_t* live, const int64_t* foff,
+                               float* dst, cudaStream_t st);
 // live[r] = r, keys = 0, ctrl = {B, 1}; live_start/live_len (optional) = row_start/row_len.
 cudaError_t launch_decode_init(int32_t* ctrl, int32_t* live, int B, unsigned long long* keys,
                                const int32_t* row_start, const int32_t* row_len,

@@ -20,7 +20,7 @@ MAX_SPAN = 512
 DEVICE_IO = 1
 SHORTLIST = 2
 
-DUMP_ENC_OUT, DUMP_SRC_KV, DUMP_DEC_OUT, DUMP_OUT_CODES, DUMP_LAYERS = 1, 2, 4, 8, 16
+DUMP_ENC_OUT, DUMP_SRC_KV, DUMP_DEC_OUT, DUMP_OUT_CODES, DUMP_LAYERS, DUMP_MARGIN = 1, 2, 4, 8, 16, 32
 EPI_F32, EPI_F32_Q, EPI_RELU_Q, EPI_RELU_F32_Q, EPI_SIGMOID, EPI_ARGMAX, EPI_ACC = range(7)
 EPI_TOPK = 9            # beam search partials (include/mnmt_ops.h); 80-byte records
 TOPK_RECORD_BYTES = 80
@@ -297,6 +297,8 @@ class Model:
             sections.append(("out_codes", np.int8, (O, d)))
         if dump_mask & DUMP_LAYERS:
             sections.append(("layers", np.float32, (O, L, 3, d)))
+        if dump_mask & DUMP_MARGIN:
+            sections.append(("margin", np.float32, (O,)))
         nbytes = sum(int(np.prod(s)) * np.dtype(t).itemsize for _, t, s in sections)
         buf = np.zeros(max(nbytes, 1), np.uint8)
         am = np.zeros(max(O, 1), np.int32)

@@ -104,7 +104,7 @@ def test_teacher_forced_bench_schedule(workload):
     T = forced_lengths(ss, seed=31)
     foff = np.concatenate([[0], np.cumsum(T)]).astype(np.int64)
     forced = synth.forced_targets(T.tolist(), seed=32, vocab=dims.vocab)
-    mask = M.DUMP_DEC_OUT | M.DUMP_OUT_CODES | M.DUMP_LAYERS
+    mask = M.DUMP_DEC_OUT | M.DUMP_OUT_CODES | M.DUMP_LAYERS | M.DUMP_MARGIN
     ids, dumps = gm.decode_forced(ss, forced, foff, mask, budget=budget)
     st = gm.stats()
     om = O.OracleModel(dims, w)
@@ -113,7 +113,8 @@ def test_teacher_forced_bench_schedule(workload):
     s = O.dequant_scale(dims.clip)
     tot = ex = fl = 0
     err_dec = err_layers = 0.0
-    flips = unexplained = 0
+    flips = unexplained = margin_diff = 0
+    min_margin = float("inf")
     for i, tr in enumerate(traces):
         sl = slice(int(foff[i]), int(foff[i + 1]))
         err_dec = max(err_dec, rel_err(dumps["dec_out"][sl], tr["dec_out"]))
@@ -122,17 +123,22 @@ def test_teacher_forced_bench_schedule(workload):
         unexplained += int(np.sum(boundary_explained(tr["dec_out"], tr["out_codes"], dumps["out_codes"][sl])))
         n_, e_, f_ = check_forced_steps(ids[sl], dumps["out_codes"][sl], tr, qE, s)
         tot += n_; ex += e_; fl += f_
+        same = np.all(dumps["out_codes"][sl] == tr["out_codes"], axis=1)
+        margin_diff += int(np.sum(dumps["margin"][sl][same] != tr["margin"][same]))
+        min_margin = min(min_margin, float(np.min(tr["margin"])))
     rec = {"kind": "teacher-forced (mnmt_translate_forced, bench schedule)", "workload": workload,
            "options": opts, "word_budget": budget, "sentences": int(ss.n),
            "source_span_max": int(ss.lengths.max()), "steps_total": int(tot),
            "max_live_rows_step1": int(ss.n), "decode_steps": st["decode_steps"], "batches": st["batches"],
            "ids_identical": int(ex), "near_ties_flagged": int(fl), "ids_identical_pct": 100.0 * ex / tot,
            "max_rel_err_dec_out": err_dec, "max_rel_err_layers": err_layers,
-           "output_code_flips": flips, "unexplained_code_flips": unexplained}
+           "output_code_flips": flips, "unexplained_code_flips": unexplained,
+           "top2_margin_mismatches": margin_diff, "min_oracle_top2_margin": min_margin}
     record(rec)
     assert unexplained == 0, rec
     assert err_dec <= 1e-4 and err_layers <= 1e-4, rec
     assert ex + fl == tot, rec
+    assert margin_diff == 0, rec
 
 
 def eos_student(dims, seed=5, emb_scale=0.05, t_cross=8):

@@ -54,7 +54,7 @@ def forced_case(dims, n, lo, hi, T_lo, T_hi, seed):
 
 
 def run_forced_parity(dims, w, om, gm, ss, forced, foff, layers=True):
-    mask = M.DUMP_ENC_OUT | M.DUMP_SRC_KV | M.DUMP_DEC_OUT | M.DUMP_OUT_CODES
+    mask = M.DUMP_ENC_OUT | M.DUMP_SRC_KV | M.DUMP_DEC_OUT | M.DUMP_OUT_CODES | M.DUMP_MARGIN
     if layers:
         mask |= M.DUMP_LAYERS
     ids, dumps = gm.decode_forced(ss, forced, foff, mask)
@@ -79,6 +79,9 @@ def run_forced_parity(dims, w, om, gm, ss, forced, foff, layers=True):
             np.testing.assert_allclose(dumps["layers"][sl], tr["layer_out"], rtol=1e-5, atol=1e-5)
         n_, e_, f_ = check_forced_steps(ids[sl], dumps["out_codes"][sl], tr, qE, s)
         tot += n_; ex += e_; fl += f_
+        # top2_margin: identical wherever the step's output codes are (same s32 logits)
+        same = np.all(dumps["out_codes"][sl] == tr["out_codes"], axis=1)
+        assert np.array_equal(dumps["margin"][sl][same], tr["margin"][same]), i
     return tot, ex, fl
 
 
