@@ -7,7 +7,7 @@ import pytest
 
 import oracle.oracle as O
 import synth
-from tests.gpu_util import boundary_explained, empty, ptr, sync, to_dev, zeros
+from tests.gpu_util import boundary_explained, empty, ptr, sync, to_dev, torch_dev, zeros
 
 pytestmark = pytest.mark.gpu
 
@@ -267,3 +267,30 @@ def test_attention(d, H):
     assert np.mean(got == ref) > 0.9999
     np.testing.assert_allclose(got, ref, rtol=1e-6, atol=1e-7)
     assert not boundary_explained(ref, O.quantize(ref), oq.cpu().numpy()).any()
+
+
+# ------------------------------------------------------------------ A11 across GPUs (unshard)
+def test_gather_rows():
+    """mnmt_op_gather_rows puts the all-gathered rows of a strong-scaling job back in input order:
+    the same result as the plan's numpy twin (paper_1805_12096_b200.dist.unshard_host)."""
+    from paper_1805_12096_b200 import dist as D
+    rng = np.random.default_rng(4)
+    n, world = 300, 4
+    ml = rng.integers(0, 30, size=n)
+    outs = [rng.integers(3, 36000, size=rng.integers(0, m + 1)).astype(np.int32) for m in ml]
+    shards = [D.shard_round_robin(rng.integers(1, 50, size=n), r, world) for r in range(world)]
+    plan = D.gather_plan(ml, shards)
+    gi = np.zeros(plan.world * plan.id_cap, np.int32)
+    gl = np.zeros(plan.world * plan.n_cap, np.int32)
+    for r, s in enumerate(shards):
+        f, l = D.pack_ids([outs[i] for i in s], ml[s])
+        gi[r * plan.id_cap:r * plan.id_cap + len(f)] = f
+        gl[r * plan.n_cap:r * plan.n_cap + len(l)] = l
+    un = D.DeviceUnshard(plan, torch_dev())
+    ids, ln = un(to_dev(gi), to_dev(gl))
+    sync()
+    ref_ids, ref_ln = D.unshard_host(gi, gl, plan)
+    ln_h = ln.cpu().numpy()
+    assert np.array_equal(ln_h, ref_ln)
+    got = D.split_rows(ids.cpu().numpy(), ln_h, ml)
+    assert all(np.array_equal(a, b) for a, b in zip(got, outs))
