@@ -221,6 +221,11 @@ mnmt_status mnmt_translate_forced(mnmt_model* m, const int32_t* src_ids_host,
  *                          IDP4A CUDA-core kernels (same s32 accumulators, same epilogue arithmetic,
  *                          bit-identical outputs); 0: tcgen05 always.  Per model.
  *   "smallm_kmax"          deepest K the small-M path takes (default 512, per model).
+ *   "smallm_wmax"          largest weight matrix N x K (bytes) the small-M path takes (default
+ *                          2^20: the d x d maps of the big student, not its FFN / Q|K|V maps).
+ *   "split_k"              1: decoder GEMMs with K >= 4096 (or >= 2048 at <= 32 rows) spread their
+ *                          K blocks over a 2-4 CTA cluster (exact s32 partials added in the
+ *                          leader); 0 (default; measured slower in the 3-lane job).
  *   "lane_tiers"           0 (default): a wave's sentences are dealt round-robin to the lanes;
  *                          10*p: contiguous length tiers of equal sum S_i^p, the last lane (the
  *                          longest sentences, the job's critical path) on the highest-priority stream.

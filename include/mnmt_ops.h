@@ -51,6 +51,16 @@ mnmt_status mnmt_op_gemm_i8(const int8_t* A_dev, const int8_t* W_dev, int32_t M,
                             void* out_dev, void* out2_dev, int32_t n_tile, void* stream);
 
 /* Argmax key -> id (the packed key of MNMT_EPI_ARGMAX; lowest id wins ties, R15). */
+/* As mnmt_op_gemm_i8 with split-K: split_k = 2, 4, 8 spreads the K blocks of every output tile
+ * over a thread-block cluster of that many CTAs (fewer when K has fewer 128-byte blocks or the
+ * leader's shared memory cannot hold the partial slots; BN <= 128), whose exact s32 partials are
+ * added in the leader before the epilogue; -1 = the library's rule (K >= 4096, or K >= 2048 at
+ * <= 32 rows); 1 = none.  Outputs identical to mnmt_op_gemm_i8 (integer sums). */
+mnmt_status mnmt_op_gemm_i8_split(const int8_t* A_dev, const int8_t* W_dev, int32_t M, int32_t N,
+                                  int32_t K, const float* bias_dev, float clip, int32_t epi,
+                                  void* out_dev, void* out2_dev, int32_t n_tile, int32_t split_k,
+                                  void* stream);
+
 mnmt_status mnmt_op_argmax_ids(const uint64_t* keys_dev, int32_t n, int32_t* ids_dev,
                                void* stream);
 
@@ -81,6 +91,17 @@ mnmt_status mnmt_op_attention(const float* q_dev, int64_t ldq, const float* kv_d
                               int32_t k_off, int32_t v_off, const int32_t* kv_start_dev,
                               const int32_t* kv_len_dev, int32_t n, int32_t d, int32_t H,
                               float clip, int8_t* out_q_dev, float* out_f_dev, void* stream);
+
+/* A7 with the decode path's kernel choice (the TMA-tiled source-attention kernel for fp32 K/V
+ * and d/H = 32 or 64, else as mnmt_op_attention): row r attends kv rows
+ * [kv_start[r], kv_start[r] + kv_len[r]) of the kv_rows-row buffer kv_dev (ldkv floats per row,
+ * 16-byte aligned; the TMA tensor map is bounded by kv_rows); max_span >= every kv_len[r]
+ * (<= MNMT_MAX_KV; sizes shared memory).  Same outputs as mnmt_op_attention. */
+mnmt_status mnmt_op_src_attention(const float* q_dev, int64_t ldq, const float* kv_dev,
+                                  int64_t kv_rows, int64_t ldkv, int32_t k_off, int32_t v_off,
+                                  const int32_t* kv_start_dev, const int32_t* kv_len_dev,
+                                  int32_t max_span, int32_t n, int32_t d, int32_t H, float clip,
+                                  int8_t* out_q_dev, float* out_f_dev, void* stream);
 
 /* As mnmt_op_attention with bf16 keys / values: kv16 holds bfloat16 bit
  * patterns (uint16) in the same layout (strides and offsets in elements, multiples of 4). */

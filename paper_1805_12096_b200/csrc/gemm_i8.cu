@@ -792,6 +792,19 @@ bool make_tmap_i8(CUtensorMap* map, const void* base, int64_t rows, int64_t K) {
   return r == CUDA_SUCCESS;
 }
 
+bool make_tmap_kv(CUtensorMap* map, const void* base, int64_t rows, int64_t cols) {
+  auto enc = get_encode();
+  if (!enc || rows < 1 || cols % 4 != 0 || ((uintptr_t)base & 15)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {32u, 32u};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("MNMT_NO_PDL");
@@ -851,26 +864,20 @@ static cudaError_t launch_pers_t(const CUtensorMap& tmA, const CUtensorMap& tmB,
   return cudaLaunchKernelEx(&cfg, k_gemm_pers<BN, EPI>, tmA, tmB, a);
 }
 
-// Split-K factor of a non-persistent launch: deep K and a grid that leaves most SMs idle (FFN2
-// of the base / big students at small row counts, where each CTA would stream its whole
-// K = F range alone).  Powers of two while the split grid fits the launch's SM budget, every
+// Split-K factor of a non-persistent launch (GemmArgs::split_k: 0 none, > 1 forced, -1 the rule
+// below): deep K and a grid that leaves most SMs idle (FFN2 of the base / big students at small
+// row counts, where each CTA would stream its whole K = F range alone).  Powers of two while the split grid fits the launch's SM budget, every
 // CTA keeps >= 1 K block and the leader's partial slots fit its shared memory (<= 4 for
 // BN = 64).  Measured (profiles/r2_gemm_splitk.txt, warm PDL chain): big FFN2 (K = 4096)
 // 10.5 -> 6.0 us at <= 32 rows, 10.7 -> 8.7 at 128; base FFN2 (K = 2048) 6.5 -> 5.0 at <= 32
 // rows but 6.7 -> 7.6 at 128; K = 1024 neutral at <= 32 rows and slower at 128-256 (the
-// partial tiles cross distributed shared memory).  Hence: K >= 4096, or K >= 2048 with a
-// <= 32-row bound.  Env MNMT_SPLITK=0 disables (A/B), MNMT_SPLITK_KMIN overrides the rule's K.
+// partial tiles cross distributed shared memory).  Hence the rule: K >= 4096, or K >= 2048 with
+// a <= 32-row bound.  In the whole big-student job it still loses (3 lanes: 118.4-119.2 ms per
+// job without, 122.0-122.6 with; profiles/r2_gemm_splitk.txt), so the model path leaves it off
+// unless the model option "split_k" = 1 asks for the rule.
 static int gemm_split_k(const GemmArgs& a, int bn, int epi) {
-  static const int mode = [] {
-    const char* e = getenv("MNMT_SPLITK");
-    return e ? atoi(e) : 1;
-  }();
-  static const int kmin = [] {
-    const char* e = getenv("MNMT_SPLITK_KMIN");
-    return e ? atoi(e) : 0;
-  }();
-  if (!mode || bn > 128) return 1;
-  if (kmin > 0 ? a.K < kmin : !(a.K >= 4096 || (a.K >= 2048 && a.M <= 32))) return 1;
+  if (a.split_k == 0 || a.split_k == 1 || bn > 128) return 1;
+  if (a.split_k < 0 && !(a.K >= 4096 || (a.K >= 2048 && a.M <= 32))) return 1;
   if (!(epi == EPI_F32 || epi == EPI_F32_Q || epi == EPI_RELU_Q || epi == EPI_RELU_F32_Q ||
         epi == EPI_SIGMOID || epi == EPI_ACC))
     return 1;
@@ -880,7 +887,8 @@ static int gemm_split_k(const GemmArgs& a, int bn, int epi) {
   int ks = 1;
   // the leader holds ks - 1 partial slots next to its ring and epilogue staging
   const int slot = BM * (bn + 4) * 4;
-  while (ks < 8 && tiles * ks * 2 <= sms && kb_all >= ks * 2 &&
+  const int want = a.split_k > 1 ? a.split_k : 8;
+  while (ks < want && (a.split_k > 1 || tiles * ks * 2 <= sms) && kb_all >= ks * 2 &&
          (long)(2 * ks - 1) * slot + 1024 + EPI_STAGE_BYTES + 2 * (BM + 64) * BK <= GEMM_SMEM_MAX)
     ks *= 2;
   while (ks > 1 && kb_all - (ks - 1) * ((kb_all + ks - 1) / ks) < 1) ks /= 2;   // no empty range
@@ -1151,7 +1159,8 @@ static cudaError_t launch_smallm_e(const GemmArgs& a, int S, cudaStream_t st) {
 // tcgen05 path).
 static cudaError_t launch_smallm(const GemmArgs& a, int epi, cudaStream_t st) {
   if (!a.a_ptr || !a.b_ptr || a.M > SMALLM_MAX) return cudaErrorNotSupported;
-  if (!a.smallm_force && (a.smallm_rows <= 0 || a.M > a.smallm_rows || a.K > a.smallm_kmax))
+  if (!a.smallm_force && (a.smallm_rows <= 0 || a.M > a.smallm_rows || a.K > a.smallm_kmax ||
+                          (int64_t)a.N * a.K > a.smallm_wmax))
     return cudaErrorNotSupported;
   if (a.K % 16 || a.lda % 16 || ((uintptr_t)a.a_ptr & 15) || ((uintptr_t)a.b_ptr & 15))
     return cudaErrorNotSupported;

@@ -69,7 +69,10 @@ struct GemmArgs {
   int smallm_force;            // op level: take the small-M path whenever it can run (M <= 32)
   int smallm_rows;             // small-M path row bound of the launch (0 = off, <= SMALLM_MAX)
   int smallm_kmax;             // deepest K the small-M path takes
+  int64_t smallm_wmax;         // largest weight matrix (N x K bytes) the small-M path takes
   int ring_cap;                // (launch-internal) TMA ring depth cap of a split-K launch
+  int split_k;                 // 0 / 1: no split-K; -1: the K / row-bound rule; 2, 4, 8: forced
+                               // (capped by the leader's shared memory and the K blocks)
 };
 
 constexpr int SMALLM_MAX = 32;
@@ -77,6 +80,9 @@ constexpr int SMALLM_MAX = 32;
 // Tensor map over a row-major int8 matrix [rows x K] (K contiguous, K % 16 == 0):
 // box {128 bytes, 64 rows}, 128-byte swizzle (the UMMA K-major SW128 atom).
 bool make_tmap_i8(CUtensorMap* map, const void* base, int64_t rows, int64_t K);
+// Tensor map over fp32 key/value rows [rows x cols] (cols contiguous, row stride = cols): box
+// {32 floats, 32 rows}, 128-byte swizzle (the source-attention K / V head tiles).
+bool make_tmap_kv(CUtensorMap* map, const void* base, int64_t rows, int64_t cols);
 
 // A is [>= M x K] activation codes, B is [N x K] weight codes (both via make_tmap_i8).
 // bn = 0 picks the N tile.

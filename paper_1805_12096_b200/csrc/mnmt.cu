@@ -95,6 +95,7 @@ struct Workspace {
   int8_t *cy = nullptr, *cg = nullptr, *ch1 = nullptr, *ca = nullptr, *cx1 = nullptr;
   int8_t *cctxd = nullptr, *cx2 = nullptr, *chd = nullptr;
   CUtensorMap tm_cy, tm_cg, tm_ch1, tm_ca, tm_cx1, tm_cctxd, tm_cx2, tm_chd;
+  CUtensorMap tm_kv;   // fp32 source K|V rows of every layer [L * M_cap][2d] (TMA attention)
   // beam search (F1; allocated on first use by beam_ensure, sized B_cap x T_cap)
   std::vector<void*> beam_allocs;
   int64_t beam_rows = 0, beam_T = 0;
@@ -194,6 +195,8 @@ struct mnmt_model {
   int steps_per_graph = 1;             // option: decoder steps captured per CUDA graph
   int smallm = 32;                     // option: row bound of the small-M GEMM path (0 = off)
   int smallm_kmax = 512;               // option: deepest K the small-M path takes
+  int64_t smallm_wmax = 1 << 20;       // option: largest weight matrix (N x K bytes) of the small-M path
+  int split_k = 0;                     // option: 1 = split-K clusters by the measured rule (off: slower in the job)
   DevDump dump;                        // (call state) device dumps of a teacher-forced run
   int green_sms = 0;                   // option: SMs of the critical lane's green context (0 = off)
   CUgreenCtx green[2] = {nullptr, nullptr};   // [0] critical lane, [1] the other lanes
@@ -735,6 +738,10 @@ static mnmt_status lane_ensure(mnmt_model* m, Lane& Ln, int64_t M, int64_t B, in
   CKS(ws_tmap(&z.tm_cctxd, z.cctxd, Bc, d));
   CKS(ws_tmap(&z.tm_cx2, z.cx2, Bc, d));
   CKS(ws_tmap(&z.tm_chd, z.chd, Bc, F));
+  if (!make_tmap_kv(&z.tm_kv, z.kv, L * Mc, 2 * d)) {
+    set_err("cuTensorMapEncodeTiled failed (source K/V)");
+    return MNMT_ERR_CUDA;
+  }
   return MNMT_OK;
 }
 
@@ -764,6 +771,8 @@ static cudaError_t gemm(mnmt_model* m, cudaStream_t st, const CUtensorMap& tmA, 
   a.pers_grid = m->cur_pers_grid;
   a.smallm_rows = m->smallm;
   a.smallm_kmax = m->smallm_kmax;
+  a.smallm_wmax = m->smallm_wmax;
+  a.split_k = m->split_k ? -1 : 0;
   return launch_gemm_i8(tmA, W.tm, a, epi, 0, st);
 }
 
@@ -1010,6 +1019,8 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, int6
     as.ldq = d;
     as.kv = w.kv + (int64_t)l * w.M_cap * 2 * d;
     as.kv16 = c.src_kv_bf16 ? w.kv16 + (int64_t)l * w.M_cap * 2 * d : nullptr;
+    as.tmap = &w.tm_kv;                // TMA tiles (fp32 K/V)
+    as.kv_row0 = (int64_t)l * w.M_cap;
     as.ldkv = 2 * d;
     as.k_off = 0;
     as.v_off = d;
@@ -2076,6 +2087,24 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
     if (value < 0 || value > (1 << 16)) { set_err("smallm_kmax must be in [0, 65536]"); return MNMT_ERR_ARG; }
     m->smallm_kmax = (int)value;
     for (Lane& L : m->lanes) {
+      for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
+      L.graphs.clear();
+    }
+    return MNMT_OK;
+  }
+  if (std::string(name) == "smallm_wmax") {
+    if (value < 0) { set_err("smallm_wmax < 0"); return MNMT_ERR_ARG; }
+    m->smallm_wmax = value;
+    for (Lane& L : m->lanes) {
+      for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
+      L.graphs.clear();
+    }
+    return MNMT_OK;
+  }
+  if (std::string(name) == "split_k") {
+    if (value != 0 && value != 1) { set_err("split_k must be 0 or 1"); return MNMT_ERR_ARG; }
+    m->split_k = (int)value;
+    for (Lane& L : m->lanes) {   // captured graphs encode the old grids
       for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
       L.graphs.clear();
     }

@@ -36,9 +36,30 @@ mnmt_status mnmt_op_quantize(const float* x, int64_t n, float clip, int8_t* out,
   return cuda_status(launch_quantize(x, n, clip, out, (cudaStream_t)stream), "quantize");
 }
 
+static mnmt_status gemm_op(const int8_t* A, const int8_t* W, int32_t M, int32_t N, int32_t K,
+                           const float* bias, float clip, int32_t epi, void* out, void* out2,
+                           int32_t n_tile, int32_t split_k, void* stream);
+
 mnmt_status mnmt_op_gemm_i8(const int8_t* A, const int8_t* W, int32_t M, int32_t N, int32_t K,
                             const float* bias, float clip, int32_t epi, void* out, void* out2,
                             int32_t n_tile, void* stream) {
+  return gemm_op(A, W, M, N, K, bias, clip, epi, out, out2, n_tile, 0, stream);
+}
+
+mnmt_status mnmt_op_gemm_i8_split(const int8_t* A, const int8_t* W, int32_t M, int32_t N, int32_t K,
+                                  const float* bias, float clip, int32_t epi, void* out, void* out2,
+                                  int32_t n_tile, int32_t split_k, void* stream) {
+  if (split_k != -1 && split_k != 1 && split_k != 2 && split_k != 4 && split_k != 8)
+    return arg_error("mnmt_op_gemm_i8_split: split_k must be -1, 1, 2, 4 or 8");
+  if (n_tile == -1) return arg_error("mnmt_op_gemm_i8_split: no split-K for the small-M kernel");
+  return gemm_op(A, W, M, N, K, bias, clip, epi, out, out2, n_tile, split_k, stream);
+}
+
+}  // extern "C"
+
+static mnmt_status gemm_op(const int8_t* A, const int8_t* W, int32_t M, int32_t N, int32_t K,
+                           const float* bias, float clip, int32_t epi, void* out, void* out2,
+                           int32_t n_tile, int32_t split_k, void* stream) {
   if (!A || !W || !out || M < 1 || N < 1 || K < 16 || K % 16 || !(clip > 0.0f))
     return arg_error("mnmt_op_gemm_i8: bad arguments (K must be a positive multiple of 16)");
   if ((epi < MNMT_EPI_F32 || epi > MNMT_EPI_ACC) && epi != MNMT_EPI_TOPK)
@@ -67,6 +88,7 @@ mnmt_status mnmt_op_gemm_i8(const int8_t* A, const int8_t* W, int32_t M, int32_t
   a.ldo = N;
   a.col_block = N;
   a.block_stride = 0;
+  a.split_k = split_k;
   if (small) {
     a.a_ptr = A;
     a.lda = K;
@@ -94,6 +116,8 @@ mnmt_status mnmt_op_gemm_i8(const int8_t* A, const int8_t* W, int32_t M, int32_t
   if (epi == MNMT_EPI_TOPK && n_tile_topk == 4) epi = EPI_TOPK4;
   return cuda_status(launch_gemm_i8(ta, tb, a, epi, n_tile, (cudaStream_t)stream), "gemm_i8");
 }
+
+extern "C" {
 
 mnmt_status mnmt_op_argmax_ids(const uint64_t* keys, int32_t n, int32_t* ids, void* stream) {
   if (n < 0 || (n > 0 && (!keys || !ids))) return arg_error("mnmt_op_argmax_ids: bad arguments");
@@ -184,6 +208,43 @@ mnmt_status mnmt_op_attention(const float* q, int64_t ldq, const float* kv, int6
   a.out_q = out_q;
   a.out_f = out_f;
   return cuda_status(launch_attn(a, (cudaStream_t)stream), "attention");
+}
+
+mnmt_status mnmt_op_src_attention(const float* q, int64_t ldq, const float* kv, int64_t kv_rows,
+                                  int64_t ldkv, int32_t k_off, int32_t v_off,
+                                  const int32_t* kv_start, const int32_t* kv_len, int32_t max_span,
+                                  int32_t n, int32_t d, int32_t H, float clip, int8_t* out_q,
+                                  float* out_f, void* stream) {
+  if (n < 0 || H < 1 || d % H || (d / H) % 4 || d / H > 64 || !q || !kv || kv_rows < 1 ||
+      max_span < 0 || max_span > MNMT_MAX_KV ||
+      !kv_start || !kv_len || !out_q || ldq % 4 || ldkv % 4 || k_off % 4 || v_off % 4 ||
+      !(clip > 0.0f))
+    return arg_error("mnmt_op_src_attention: bad arguments");
+  if (cudaError_t e = attn_init(); e != cudaSuccess) return cuda_status(e, "attention init");
+  CUtensorMap tm;
+  if (!make_tmap_kv(&tm, kv, kv_rows, ldkv)) return cuda_status(cudaErrorInvalidValue, "tensor map encode");
+  AttnArgs a{};
+  a.mode = ATTN_ENC;   // row r attends kv rows [kv_start[r], + kv_len[r])
+  a.span = (max_span + 31) / 32 * 32;
+  a.n = n;
+  a.H = H;
+  a.dh = d / H;
+  a.d = d;
+  a.q = q;
+  a.ldq = ldq;
+  a.kv = kv;
+  a.ldkv = ldkv;
+  a.k_off = k_off;
+  a.v_off = v_off;
+  a.kv_start = kv_start;
+  a.kv_len = kv_len;
+  a.clip = clip;
+  a.sigma = sigma_of(clip);
+  a.out_q = out_q;
+  a.out_f = out_f;
+  a.tmap = &tm;
+  a.kv_row0 = 0;
+  return cuda_status(launch_attn(a, (cudaStream_t)stream), "source attention");
 }
 
 mnmt_status mnmt_op_attention_bf16(const float* q, int64_t ldq, const uint16_t* kv16, int64_t ldkv,

@@ -144,6 +144,137 @@ __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn(AttnArgs a) {
   attn_row_head(a, r, h, sc_dyn + (size_t)wi * (a.span + 64), a.span, pst, pln);
 }
 
+// Source attention with the head's K / V tiles moved by TMA (A7; fp32 K/V, d_h = 32 / 64).
+// One warp per (row, head), AT_WARPS warps per CTA.  Lane 0 of a warp issues, before any
+// arithmetic, the bulk tensor copies of the first 32 positions' K tile and V tile (d_h / 32
+// boxes of 32 rows x 128 B each, 128-byte swizzle) into the warp's shared memory, completing
+// on two mbarriers; later 32-position chunks are requested as soon as the previous chunk of the
+// same buffer has been consumed.  No register holds a load in flight, so every warp keeps its
+// whole tile in flight (the generic kernel's lanes wait on one K row / four V rows at a time:
+// ncu, long-scoreboard stalls at 45 % occupancy).  The swizzle makes both access patterns
+// conflict-free: lane = position reading 16-byte column groups of its row (scores), lane =
+// column reading one row (context).  Arithmetic and order are warp_attend's (identical outputs).
+constexpr int AT_WARPS = 4;
+constexpr int AT_TILE = 32 * 128;   // one box: 32 rows x 32 floats
+
+__device__ __forceinline__ int at_swz(int j, int cc) {   // byte offset of (row j, float cc) in a box
+  return j * 128 + ((((cc >> 2) ^ (j & 7)) << 4) | ((cc & 3) << 2));
+}
+
+template <int DH>
+__global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constant__ CUtensorMap tm,
+                                                            AttnArgs a) {
+  constexpr int HB = DH / 32;                 // 32-column boxes per head slice
+  constexpr int WB = 2 * HB * AT_TILE;        // this warp's K and V tiles
+  extern __shared__ uint8_t at_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(at_raw) + 1023) & ~uintptr_t(1023));
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* kt = base + wi * WB;
+  uint8_t* vt = kt + HB * AT_TILE;
+  double* sc = reinterpret_cast<double*>(base + AT_WARPS * WB) + (size_t)wi * a.span;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + AT_WARPS * WB + (size_t)AT_WARPS * a.span * 8) + 2 * wi;
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tm);
+  }
+  __syncwarp();
+  pdl_wait();
+  pdl_trigger_early();
+  const int64_t gw = (int64_t)blockIdx.x * AT_WARPS + wi;
+  const int r = (int)(gw / a.H), h = (int)(gw - (int64_t)r * a.H);
+  if (r >= a.n) return;
+  const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
+  int start, len;
+  if (a.mode == ATTN_ENC) {   // op level: row r's own span
+    start = a.kv_start[r];
+    len = a.kv_len[r];
+  } else if (a.live_start) {
+    start = a.live_start[r];
+    len = a.live_len[r];
+  } else {
+    const int orig = a.live[r];
+    start = a.kv_start[orig];
+    len = a.kv_len[orig];
+  }
+  if (r >= n_live) return;
+  const int row0 = (int)(a.kv_row0 + start);
+  const int kc = a.k_off + h * DH, vc = a.v_off + h * DH;
+  auto load = [&](uint64_t* b, uint8_t* dst, int col, int row) {
+    mbar_arrive_expect_tx(b, HB * AT_TILE);
+#pragma unroll
+    for (int hb = 0; hb < HB; ++hb) tma_load_2d(dst + hb * AT_TILE, &tm, b, col + 32 * hb, row);
+  };
+  if (lane == 0 && len > 0) {
+    load(&bar[0], kt, kc, row0);
+    load(&bar[1], vt, vc, row0);
+  }
+  const float* q = a.q + (int64_t)r * a.ldq + h * DH;
+  const double inv_sqrt = 1.0 / sqrt((double)DH);
+  double mx = -INFINITY;
+  uint32_t kph = 0, vph = 0;
+  for (int c0 = 0; c0 < len; c0 += 32) {
+    mbar_wait(&bar[0], kph);
+    kph ^= 1;
+    const int j = c0 + lane;
+    if (j < len) {
+      double dot = 0.0;
+#pragma unroll
+      for (int c = 0; c < DH; c += 4) {
+        const float4 k4 = *reinterpret_cast<const float4*>(kt + (c >> 5) * AT_TILE + at_swz(lane, c & 31));
+        const float4 q4 = *reinterpret_cast<const float4*>(q + c);   // same address in all lanes
+        dot = __fma_rn((double)q4.x, (double)k4.x, dot);
+        dot = __fma_rn((double)q4.y, (double)k4.y, dot);
+        dot = __fma_rn((double)q4.z, (double)k4.z, dot);
+        dot = __fma_rn((double)q4.w, (double)k4.w, dot);
+      }
+      const double s = __dmul_rn(dot, inv_sqrt);
+      sc[j] = s;
+      mx = fmax(mx, s);
+    }
+    __syncwarp();
+    if (lane == 0 && c0 + 32 < len) load(&bar[0], kt, kc, row0 + c0 + 32);
+  }
+  mx = warp_max_f64(mx);
+  double z = 0.0;
+  for (int j = lane; j < len; j += 32) {
+    const double p = exp(__dsub_rn(sc[j], mx));
+    sc[j] = p;
+    z = __dadd_rn(z, p);
+  }
+  z = warp_sum_f64(z);
+  __syncwarp();
+  double acc[HB];
+#pragma unroll
+  for (int i = 0; i < HB; ++i) acc[i] = 0.0;
+  for (int c0 = 0; c0 < len; c0 += 32) {
+    mbar_wait(&bar[1], vph);
+    vph ^= 1;
+    const int je = min(32, len - c0);
+    for (int jj = 0; jj < je; ++jj) {
+      const double p = sc[c0 + jj];
+#pragma unroll
+      for (int i = 0; i < HB; ++i)
+        acc[i] = __fma_rn(p, (double)*reinterpret_cast<const float*>(vt + i * AT_TILE + at_swz(jj, lane)), acc[i]);
+    }
+    __syncwarp();
+    if (lane == 0 && c0 + 32 < len) load(&bar[1], vt, vc, row0 + c0 + 32);
+  }
+  int8_t* out = a.out_q + (int64_t)r * a.d + h * DH;
+#pragma unroll
+  for (int i = 0; i < HB; ++i) {
+    const int c = lane + 32 * i;
+    const float ctx = len > 0 ? (float)__ddiv_rn(acc[i], z) : 0.0f;
+    out[c] = (int8_t)q8(ctx, a.clip, a.sigma);
+    if (a.out_f) a.out_f[(int64_t)r * a.d + h * DH + c] = ctx;
+  }
+}
+
+inline size_t attn_tma_smem(int dh, int span) {
+  return 1024 + (size_t)AT_WARPS * (2 * (dh / 32) * AT_TILE + (size_t)span * 8 + 16);
+}
+
 // Source attention split over NS warps per (row, head) for long spans (A7): warp w of a group
 // scores the 32-position chunks w, w + NS, ...; the row max is exchanged first, so every
 // p_j = exp(s_j - max) is the value of the one-warp kernel; Z and the context are per-warp
@@ -551,6 +682,12 @@ cudaError_t attn_init() {   // once per device
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              ATTN_WARPS * (MNMT_MAX_KV + 64) * (int)sizeof(double));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn_tma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)attn_tma_smem(64, MNMT_MAX_KV));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn_tma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)attn_tma_smem(32, MNMT_MAX_KV));
 
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn_split<2, bf16s>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -617,6 +754,16 @@ cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
                      : launch_pdl(k_attn_split<4, bf16s>, grid, block, attn_split_smem(4, b.span), st, b);
     return ns == 2 ? launch_pdl(k_attn_split<2, float>, grid, block, attn_split_smem(2, b.span), st, b)
                    : launch_pdl(k_attn_split<4, float>, grid, block, attn_split_smem(4, b.span), st, b);
+  }
+  static const bool tma = [] {   // env MNMT_ATTN_TMA=0: the generic kernel (A/B)
+    const char* e = getenv("MNMT_ATTN_TMA");
+    return !(e && e[0] == '0');
+  }();
+  if (tma && b.tmap && !b.kv16 && (b.mode == ATTN_SRC || b.mode == ATTN_ENC) && (b.dh == 64 || b.dh == 32)) {
+    const dim3 grid((unsigned)((warps + AT_WARPS - 1) / AT_WARPS)), block(AT_WARPS * 32);
+    const size_t smem = attn_tma_smem(b.dh, b.span);
+    return b.dh == 64 ? launch_pdl(k_attn_tma<64>, grid, block, smem, st, *b.tmap, b)
+                      : launch_pdl(k_attn_tma<32>, grid, block, smem, st, *b.tmap, b);
   }
   const dim3 grid((unsigned)((warps + ATTN_WARPS - 1) / ATTN_WARPS)), block(ATTN_WARPS * 32);
   const size_t smem = (size_t)ATTN_WARPS * (b.span + 64) * 8;

@@ -1,6 +1,7 @@
 // rowops.h — launch interface of the HBM-bound kernels (internal to libmnmt).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #define MNMT_MAX_KV 512   // longest attended span (source length or decoder steps)
@@ -78,6 +79,10 @@ struct AttnArgs {
   float clip, sigma;
   int8_t* out_q;            // Q(ctx) [n x d]
   float* out_f;             // optional fp32 ctx (tests)
+  // optional TMA path (SRC / op-level ENC, fp32 K/V, d_h = 32 / 64): a make_tmap_kv map over
+  // the K/V rows; this launch's kv == the map's base + kv_row0 rows
+  const CUtensorMap* tmap;
+  int64_t kv_row0;
 };
 
 // Encoder self-attention over Q|K|V rows [M x 3d] (A3), one CTA per (sentence, head).

@@ -22,7 +22,10 @@ for d in (256, 512, 1024):
             kv = torch.randn(n * S, 2 * d, device=dev); q = torch.randn(n, d, device=dev)
             Sd, Ld = torch.from_numpy(sst).to(dev), torch.from_numpy(L).to(dev)
             oq = torch.empty(n, d, dtype=torch.int8, device=dev)
-            fn = lambda s: M.op_attention(q.data_ptr(), d, kv.data_ptr(), 2 * d, 0, d, Sd.data_ptr(), Ld.data_ptr(), n, d, H, 2.0, oq.data_ptr(), None, s)
+            if what == "src":   # the decode path's kernel choice (TMA tiles)
+                fn = lambda s: M.op_src_attention(q.data_ptr(), d, kv.data_ptr(), n * S, 2 * d, 0, d, Sd.data_ptr(), Ld.data_ptr(), S, n, d, H, 2.0, oq.data_ptr(), None, s)
+            else:
+                fn = lambda s: M.op_attention(q.data_ptr(), d, kv.data_ptr(), 2 * d, 0, d, Sd.data_ptr(), Ld.data_ptr(), n, d, H, 2.0, oq.data_ptr(), None, s)
             byt = 8.0 * n * S * d
         ms = bench.time_kernel(fn, 200, st)
         print(f"{what} d={d:5d} rows={n:5d}: {1000 * ms:8.2f} us/launch  {byt / (ms * 1e-3) / 1e9:8.1f} GB/s (warm)", flush=True)

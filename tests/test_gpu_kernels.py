@@ -62,25 +62,27 @@ def test_gemm_acc_bitexact(Mr, N, K, bn):
     assert np.array_equal(out.cpu().numpy(), O.gemm_acc(a, w))
 
 
-# split-K (K >= 1024 on a grid that leaves SMs idle): the K blocks of one output tile are spread
-# over a cluster of 2 / 4 / 8 CTAs whose s32 partials are added in the leader's shared memory
+# split-K (mnmt_op_gemm_i8_split): the K blocks of one output tile are spread over a cluster of
+# 2 / 4 / 8 CTAs whose s32 partials are added in the leader's shared memory
 SPLIT_K_SHAPES = [
-    (1, 1024, 1024, 64),      # 16 tiles x 8 (one K block per CTA)
-    (128, 1024, 4096, 64),    # 16 x 8, four K blocks each
-    (100, 3072, 1024, 0),     # 48 x 2
-    (200, 1024, 2048, 128),   # 2 M tiles x 8 N tiles x 8
-    (37, 4096, 1024, 0),      # 64 x 2
-    (70, 1024, 1040, 64),     # ragged K: 9 blocks -> 2 ranges of 5 / 4
-    (257, 1024, 1024, 64),    # three M tiles, a ragged one
+    (1, 1024, 1024, 64, 4),      # one K range of 2 blocks per CTA
+    (128, 1024, 4096, 64, 4),    # 8 K blocks each
+    (100, 3072, 1024, 0, 2),
+    (200, 1024, 2048, 128, 2),   # 2 M tiles, BN 128
+    (37, 4096, 1024, 0, -1),     # the library's rule (no split here)
+    (32, 1024, 4096, 64, -1),    # the rule: 4 CTAs
+    (70, 1024, 1040, 64, 4),     # ragged K: 9 blocks -> fewer, non-empty ranges
+    (257, 1024, 1024, 64, 8),    # three M tiles, a ragged one; 8 -> capped by shared memory
+    (5, 256, 256, 64, 2),        # two K blocks, one each
 ]
 
 
-@pytest.mark.parametrize("Mr,N,K,bn", SPLIT_K_SHAPES)
-def test_gemm_split_k_acc_bitexact(Mr, N, K, bn):
+@pytest.mark.parametrize("Mr,N,K,bn,ks", SPLIT_K_SHAPES)
+def test_gemm_split_k_acc_bitexact(Mr, N, K, bn, ks):
     a = rand_codes((Mr, K), Mr + K + 1)
     w = rand_codes((N, K), N + 9)
     out = empty((Mr, N), torch.int32)
-    M.op_gemm_i8(ptr(to_dev(a)), ptr(to_dev(w)), Mr, N, K, None, CLIP, M.EPI_ACC, ptr(out), None, bn)
+    M.op_gemm_i8_split(ptr(to_dev(a)), ptr(to_dev(w)), Mr, N, K, None, CLIP, M.EPI_ACC, ptr(out), None, bn, ks)
     sync()
     assert np.array_equal(out.cpu().numpy(), O.gemm_acc(a, w))
 
@@ -99,10 +101,11 @@ def test_gemm_epilogues_bitexact(epi, Mr, N, K):
     A, Wd, bd = to_dev(qa), to_dev(qw), to_dev(b)
     of = empty((Mr, N), torch.float32)
     oq = empty((Mr, N), torch.int8)
+    ks = 4 if K >= 1024 else 1      # deep K: through a split-K cluster
     if epi == M.EPI_RELU_Q:
-        M.op_gemm_i8(ptr(A), ptr(Wd), Mr, N, K, ptr(bd), CLIP, epi, ptr(oq))
+        M.op_gemm_i8_split(ptr(A), ptr(Wd), Mr, N, K, ptr(bd), CLIP, epi, ptr(oq), None, 0, ks)
     else:
-        M.op_gemm_i8(ptr(A), ptr(Wd), Mr, N, K, ptr(bd), CLIP, epi, ptr(of), ptr(oq))
+        M.op_gemm_i8_split(ptr(A), ptr(Wd), Mr, N, K, ptr(bd), CLIP, epi, ptr(of), ptr(oq), 0, ks)
     sync()
     if epi == M.EPI_F32:
         assert np.array_equal(of.cpu().numpy(), v)
@@ -269,6 +272,39 @@ def test_attention(d, H):
     assert not boundary_explained(ref, O.quantize(ref), oq.cpu().numpy()).any()
 
 
+@pytest.mark.parametrize("d,H", [(256, 8), (512, 8), (1024, 16), (192, 8)])
+def test_src_attention_tma(d, H):
+    """mnmt_op_src_attention (the decode path's choice: TMA-tiled K / V for d/H = 32 / 64,
+    spans of 0..130 crossing several 32-position chunks, rows at the end of the K/V buffer) equals
+    the oracle's attention and the generic kernel's output bit for bit."""
+    rng = np.random.default_rng(d + H + 5)
+    n = 50
+    lens = rng.integers(0, 131, size=n).astype(np.int32)
+    lens[0], lens[1], lens[2], lens[-1] = 1, 130, 0, 33
+    starts = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int32)
+    S = int(lens.sum())
+    kv = rng.normal(0, 1, size=(S, 2 * d)).astype(np.float32)
+    q = rng.normal(0, 1, size=(n, d)).astype(np.float32)
+    oq, of = empty((n, d), torch.int8), empty((n, d), torch.float32)
+    oq2, of2 = empty((n, d), torch.int8), empty((n, d), torch.float32)
+    kd, qd, sd, ld = to_dev(kv), to_dev(q), to_dev(starts), to_dev(lens)
+    M.op_src_attention(ptr(qd), d, ptr(kd), S, 2 * d, 0, d, ptr(sd), ptr(ld), int(lens.max()), n, d, H,
+                       CLIP, ptr(oq), ptr(of))
+    M.op_attention(ptr(qd), d, ptr(kd), 2 * d, 0, d, ptr(sd), ptr(ld), n, d, H, CLIP, ptr(oq2), ptr(of2))
+    sync()
+    got = of.cpu().numpy()
+    assert np.array_equal(got, of2.cpu().numpy())
+    assert np.array_equal(oq.cpu().numpy(), oq2.cpu().numpy())
+    ref = np.zeros((n, d), np.float32)
+    for r in range(n):
+        if lens[r] > 0:
+            blk = kv[starts[r]:starts[r] + lens[r]]
+            ref[r] = O.attention(q[r], blk[:, :d], blk[:, d:], H)
+    assert np.mean(got == ref) > 0.9999
+    np.testing.assert_allclose(got, ref, rtol=1e-6, atol=1e-7)
+    assert not boundary_explained(ref, O.quantize(ref), oq.cpu().numpy()).any()
+
+
 # ------------------------------------------------------------------ A11 across GPUs (unshard)
 def test_gather_rows():
     """mnmt_op_gather_rows puts the all-gathered rows of a strong-scaling job back in input order:
@@ -278,7 +314,8 @@ def test_gather_rows():
     n, world = 300, 4
     ml = rng.integers(0, 30, size=n)
     outs = [rng.integers(3, 36000, size=rng.integers(0, m + 1)).astype(np.int32) for m in ml]
-    shards = [D.shard_round_robin(rng.integers(1, 50, size=n), r, world) for r in range(world)]
+    lengths = rng.integers(1, 50, size=n)
+    shards = [D.shard_round_robin(lengths, r, world) for r in range(world)]
     plan = D.gather_plan(ml, shards)
     gi = np.zeros(plan.world * plan.id_cap, np.int32)
     gl = np.zeros(plan.world * plan.n_cap, np.int32)

@@ -161,12 +161,14 @@ def test_small_m_gemms_paper_students(preset):
 def test_big_student_teacher_forced(smallm):
     """big (d 1024, F 4096, H 16; K = 1024 / 4096): teacher-forced layer dumps against the oracle
     with the small-M IDP4A path taking every <= 32-row GEMM (8 K segments of 128 / 512 bytes;
-    smallm_kmax raised) and with tcgen05 only (split-K clusters on FFN2, K = 4096); ids
-    bit-exact, every intermediate within tolerance."""
+    smallm_kmax / smallm_wmax raised) and with tcgen05 only (split-K clusters on FFN2, K = 4096,
+    option split_k); ids bit-exact, every intermediate within tolerance."""
     dims = synth.PRESETS["big"]
     w, om, gm = pair(dims, 17)
     gm.set_option("smallm", smallm)
     gm.set_option("smallm_kmax", 4096)
+    gm.set_option("smallm_wmax", 1 << 24)
+    gm.set_option("split_k", 1 if smallm == 0 else 0)
     ss, forced, foff = forced_case(dims, 6, 1, 12, 1, 8, seed=11)
     tot, ex, fl = run_forced_parity(dims, w, om, gm, ss, forced, foff)
     assert ex == tot, f"{tot - ex} flagged near-ties"
