@@ -52,13 +52,20 @@ DEFAULT_WORKLOAD = "big-newstest-8192w"   # BASELINE.json configs[3]: the metric
 # need every SM).
 # smallm / smallm_kmax: the small-M (IDP4A, <= 32 live rows) GEMM path's row bound and deepest K
 # per workload, from the A/B in profiles/r1_ab_smallm.txt (small-aan: +2 % with FFN2's K = 2048
-# included; the others neutral or slower, so off).
+# included; the others neutral or slower, so off; big re-measured in round 2: slower).
+# attn_tma_self: self-attention decoders through the TMA-tiled kernels (profiles/r2_attn_tma_ab.txt:
+# base self-attention 65.4 -> 64.6 ms per job with the split kernel, big 111.8-112.2 -> 116.9).
 WORKLOAD_OPTS = {
-    "small-aan-newstest-8192w": {"green_sms": 48, "lane_tiers": 40, "smallm": 32, "smallm_kmax": 2048},
-    "tiny192-aan-newstest-8192w": {"green_sms": 56, "lane_tiers": 40, "smallm": 0, "smallm_kmax": 512},
-    "base-newstest-8192w": {"green_sms": 24, "lane_tiers": 40, "smallm": 0, "smallm_kmax": 512},
-    "base-aan-newstest-8192w": {"green_sms": 40, "lane_tiers": 35, "smallm": 32, "smallm_kmax": 512},
-    "big-newstest-8192w": {"green_sms": 0, "lane_tiers": 25, "smallm": 0, "smallm_kmax": 512},
+    "small-aan-newstest-8192w": {"green_sms": 48, "lane_tiers": 40, "smallm": 32, "smallm_kmax": 2048,
+                                 "attn_tma_self": 0},
+    "tiny192-aan-newstest-8192w": {"green_sms": 56, "lane_tiers": 40, "smallm": 0, "smallm_kmax": 512,
+                                   "attn_tma_self": 0},
+    "base-newstest-8192w": {"green_sms": 24, "lane_tiers": 40, "smallm": 0, "smallm_kmax": 512,
+                            "attn_tma_self": 1},
+    "base-aan-newstest-8192w": {"green_sms": 40, "lane_tiers": 35, "smallm": 32, "smallm_kmax": 512,
+                                "attn_tma_self": 0},
+    "big-newstest-8192w": {"green_sms": 0, "lane_tiers": 25, "smallm": 0, "smallm_kmax": 512,
+                           "attn_tma_self": 0},
 }
 L2_FLUSH_BYTES = 512 << 20   # > 126 MB L2
 
@@ -425,18 +432,25 @@ def roofline_src_attn(dims, sset, budget, peaks, stream, mcr, mult=1):
     oq = torch.empty((n, d), dtype=torch.int8, device=dev)
     it = [0]
 
+    rows_kv, smax = int(L.sum()), int(L.max())
+
     def fn(s_):
         kv = kvs[it[0] % copies]
         it[0] += 1
-        op = M.op_attention_bf16 if kv16 else M.op_attention
-        op(q.data_ptr(), d, kv.data_ptr(), 2 * d, 0, d, st.data_ptr(), ln.data_ptr(),
-           n, d, H, dims.clip, oq.data_ptr(), None, s_)
+        if kv16:
+            M.op_attention_bf16(q.data_ptr(), d, kv.data_ptr(), 2 * d, 0, d, st.data_ptr(), ln.data_ptr(),
+                                n, d, H, dims.clip, oq.data_ptr(), None, s_)
+        else:   # the decode path's kernel choice (k_attn_tma for d_h = 32 / 64)
+            M.op_src_attention(q.data_ptr(), d, kv.data_ptr(), rows_kv, 2 * d, 0, d, st.data_ptr(),
+                               ln.data_ptr(), smax, n, d, H, dims.clip, oq.data_ptr(), None, s_)
     ms = time_kernel(fn, 200, stream)
     # K,V (fp32 or bf16) + q fp32 + codes
     bytes_ = float((4 if kv16 else 8) * d * L.sum() + n * (4 * d + d))
     ach = bytes_ / (ms * 1e-3) / 1e9
     peak = peaks["hbm_gbs"]
-    return {"kernel": "k_attn (A7 source attention, fp64 accumulate" + (", bf16 K/V)" if kv16 else ")"),
+    tma = not kv16 and (d // H) in (32, 64)
+    return {"kernel": ("k_attn_tma" if tma else "k_attn") + " (A7 source attention, fp64 accumulate" +
+                      (", bf16 K/V)" if kv16 else ")"),
             "bound": "hbm",
             "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
             "shape": f"rows={n} S_mean={L.mean():.1f} d={d} H={H} (one layer; K/V rotated over "
@@ -573,6 +587,8 @@ def main():
                          "default per workload)")
     ap.add_argument("--smallm-kmax", type=int, default=None,
                     help="deepest K of the small-M path (default per workload)")
+    ap.add_argument("--attn-tma-self", type=int, default=None,
+                    help="self-attention through TMA tiles: 0 off, 1 split kernel, 2 all (default per workload)")
     ap.add_argument("--max-concurrent-rows", type=int, default=4096,
                     help="co-schedule consecutive >=budget-word batches in one decode wave "
                          "(scheduling only; 0 = one batch at a time)")
@@ -621,7 +637,8 @@ def main():
                     "steps_per_graph": args.steps_per_graph, "smallm": args.smallm,
                     "smallm_kmax": args.smallm_kmax,
                     "lane_tiers": args.lane_tiers, "pers_reserve": args.pers_reserve,
-                    "green_sms": args.green_sms, "extra_options": args.opt,
+                    "green_sms": args.green_sms, "attn_tma_self": args.attn_tma_self,
+                    "extra_options": args.opt,
                     "step_engine": "kernel-per-op CUDA graph per decoder step (PDL chained)"}
 
     if args.impl == "reference":
@@ -649,7 +666,8 @@ def main():
                     ("smallm", 32 if args.smallm is None else args.smallm),
                     ("smallm_kmax", 512 if args.smallm_kmax is None else args.smallm_kmax),
                     ("lane_tiers", args.lane_tiers), ("pers_reserve", args.pers_reserve),
-                    ("green_sms", args.green_sms), ("beam_fused", args.beam_fused)):
+                    ("green_sms", args.green_sms), ("beam_fused", args.beam_fused),
+                    ("attn_tma_self", args.attn_tma_self or 0)):
         model.set_option(name, v)
     for kv in args.opt:
         k, v = kv.split("=")

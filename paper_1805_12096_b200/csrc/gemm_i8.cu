@@ -460,6 +460,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // Tile has no live rows.  Complete the in-flight copies before leaving.
     if (warp == 0 && lane == 0)
       for (int s = 0; s < stages; ++s) mbar_wait(&full_bar[s], 0);
+    __syncwarp();   // bar.sync is .aligned: reconverge warp 0 after its single-lane work
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -467,6 +468,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     return;
   }
 
+  __syncwarp();   // (compute-sanitizer synccheck: divergent warp 0 at the barrier otherwise)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -610,6 +612,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (warp == 2 && lane == 0) GEMM_TRACE(4);   // this warp's stores issued
   }
 
+  __syncwarp();
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
@@ -664,6 +667,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(&tmem_slot);
+  __syncwarp();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -760,6 +764,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (ab == 0) aph ^= 1;
     }
   }
+  __syncwarp();
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);

@@ -96,6 +96,7 @@ struct Workspace {
   int8_t *cctxd = nullptr, *cx2 = nullptr, *chd = nullptr;
   CUtensorMap tm_cy, tm_cg, tm_ch1, tm_ca, tm_cx1, tm_cctxd, tm_cx2, tm_chd;
   CUtensorMap tm_kv;   // fp32 source K|V rows of every layer [L * M_cap][2d] (TMA attention)
+  CUtensorMap tm_self; // self-attention cache rows [L * B_cap * T_cap][2d] (decoder 0)
   // beam search (F1; allocated on first use by beam_ensure, sized B_cap x T_cap)
   std::vector<void*> beam_allocs;
   int64_t beam_rows = 0, beam_T = 0;
@@ -196,6 +197,7 @@ struct mnmt_model {
   int smallm = 32;                     // option: row bound of the small-M GEMM path (0 = off)
   int smallm_kmax = 512;               // option: deepest K the small-M path takes
   int64_t smallm_wmax = 1 << 20;       // option: largest weight matrix (N x K bytes) of the small-M path
+  int attn_tma_self = 0;               // option: self-attention through TMA tiles (0 / 1 / 2)
   int split_k = 0;                     // option: 1 = split-K clusters by the measured rule (off: slower in the job)
   DevDump dump;                        // (call state) device dumps of a teacher-forced run
   int green_sms = 0;                   // option: SMs of the critical lane's green context (0 = off)
@@ -738,8 +740,9 @@ static mnmt_status lane_ensure(mnmt_model* m, Lane& Ln, int64_t M, int64_t B, in
   CKS(ws_tmap(&z.tm_cctxd, z.cctxd, Bc, d));
   CKS(ws_tmap(&z.tm_cx2, z.cx2, Bc, d));
   CKS(ws_tmap(&z.tm_chd, z.chd, Bc, F));
-  if (!make_tmap_kv(&z.tm_kv, z.kv, L * Mc, 2 * d)) {
-    set_err("cuTensorMapEncodeTiled failed (source K/V)");
+  if (!make_tmap_kv(&z.tm_kv, z.kv, L * Mc, 2 * d) ||
+      (c.decoder == 0 && !make_tmap_kv(&z.tm_self, z.selfkv, L * Bc * Tc, 2 * d))) {
+    set_err("cuTensorMapEncodeTiled failed (attention K/V)");
     return MNMT_ERR_CUDA;
   }
   return MNMT_OK;
@@ -991,6 +994,9 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, int6
       at.v_off = d;
       at.t_cap = (int)w.T_cap;
       at.anc = m->beam > 0 ? w.anc : nullptr;
+      at.tmap = &w.tm_self;             // TMA tiles (greedy; beam search reads through anc)
+      at.tma_self = m->attn_tma_self;
+      at.kv_row0 = (int64_t)l * w.B_cap * w.T_cap;
       at.clip = c.clip;
       at.sigma = sigma_of(m);
       at.out_q = w.cctxd;
@@ -2095,6 +2101,15 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
   if (std::string(name) == "smallm_wmax") {
     if (value < 0) { set_err("smallm_wmax < 0"); return MNMT_ERR_ARG; }
     m->smallm_wmax = value;
+    for (Lane& L : m->lanes) {
+      for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
+      L.graphs.clear();
+    }
+    return MNMT_OK;
+  }
+  if (std::string(name) == "attn_tma_self") {
+    if (value < 0 || value > 2) { set_err("attn_tma_self must be 0, 1 or 2"); return MNMT_ERR_ARG; }
+    m->attn_tma_self = (int)value;
     for (Lane& L : m->lanes) {
       for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
       L.graphs.clear();

@@ -190,6 +190,9 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
   if (a.mode == ATTN_ENC) {   // op level: row r's own span
     start = a.kv_start[r];
     len = a.kv_len[r];
+  } else if (a.mode == ATTN_SELF) {   // cache rows of positions 1..t of this row's slot
+    start = a.live[r] * a.t_cap;
+    len = a.ctrl[1];
   } else if (a.live_start) {
     start = a.live_start[r];
     len = a.live_len[r];
@@ -199,6 +202,18 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
     len = a.kv_len[orig];
   }
   if (r >= n_live) return;
+  if (a.mode == ATTN_SELF) {
+    // append this step's k, v (head slice, qkv columns [d, 2d) / [2d, 3d)) at position t, then
+    // order the generic-proxy stores before the tensor copies that read them
+    const float* qk = a.q + (int64_t)r * a.ldq + h * DH;
+    float* dst = a.kv_w + (int64_t)(start + len - 1) * a.ldkv + h * DH;
+    for (int c = lane; c < DH; c += 32) {
+      dst[a.k_off + c] = qk[a.d + c];
+      dst[a.v_off + c] = qk[2 * a.d + c];
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncwarp();
+  }
   const int row0 = (int)(a.kv_row0 + start);
   const int kc = a.k_off + h * DH, vc = a.v_off + h * DH;
   auto load = [&](uint64_t* b, uint8_t* dst, int col, int row) {
@@ -273,6 +288,157 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
 
 inline size_t attn_tma_smem(int dh, int span) {
   return 1024 + (size_t)AT_WARPS * (2 * (dh / 32) * AT_TILE + (size_t)span * 8 + 16);
+}
+
+// Long spans at small row counts, split over NS warps per (row, head) with TMA tiles (A7 and the
+// greedy A6' self-attention; fp32 K/V, d_h = 32 / 64): one (row, head) per CTA of NS warps; warp
+// w takes the 32-position chunks w, w + NS, ... and requests each chunk's K and V tiles by bulk
+// tensor copy (the first chunk's before any arithmetic).  The row max is exchanged first; Z and
+// the context are per-warp partial sums over the warp's positions in order, combined in warp
+// order (R25) -- k_attn_split's arithmetic and order, so outputs are identical to it.  In self
+// mode warp 0 appends this step's k, v before the copies are issued.
+template <int NS, int DH>
+__global__ void __launch_bounds__(NS * 32) k_attn_split_tma(const __grid_constant__ CUtensorMap tm,
+                                                            AttnArgs a) {
+  constexpr int HB = DH / 32, WB = 2 * HB * AT_TILE;
+  extern __shared__ uint8_t ast_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ast_raw) + 1023) & ~uintptr_t(1023));
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* kt = base + w * WB;
+  uint8_t* vt = kt + HB * AT_TILE;
+  double* sc = reinterpret_cast<double*>(base + NS * WB);   // [span]
+  double* pm = sc + a.span;                                 // [NS]
+  double* pacc = pm + NS;                                   // [NS][DH]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(pacc + NS * DH) + 2 * w;
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tm);
+  }
+  __syncwarp();
+  pdl_wait();
+  pdl_trigger_early();
+  const int r = (int)(blockIdx.x / a.H), h = (int)(blockIdx.x - (int64_t)r * a.H);
+  const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
+  if (r >= n_live) return;   // uniform over the CTA
+  int start, len;
+  if (a.mode == ATTN_SELF) {
+    start = a.live[r] * a.t_cap;
+    len = a.ctrl[1];
+  } else if (a.live_start) {
+    start = a.live_start[r];
+    len = a.live_len[r];
+  } else {
+    const int orig = a.live[r];
+    start = a.kv_start[orig];
+    len = a.kv_len[orig];
+  }
+  const float* q = a.q + (int64_t)r * a.ldq + h * DH;
+  if (a.mode == ATTN_SELF) {
+    if (w == 0) {
+      float* dst = a.kv_w + (int64_t)(start + len - 1) * a.ldkv + h * DH;
+      for (int c = lane; c < DH; c += 32) {
+        dst[a.k_off + c] = q[a.d + c];
+        dst[a.v_off + c] = q[2 * a.d + c];
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __syncthreads();
+  }
+  const int row0 = (int)(a.kv_row0 + start);
+  const int kc = a.k_off + h * DH, vc = a.v_off + h * DH;
+  auto load = [&](uint64_t* b, uint8_t* dst, int col, int row) {
+    mbar_arrive_expect_tx(b, HB * AT_TILE);
+#pragma unroll
+    for (int hb = 0; hb < HB; ++hb) tma_load_2d(dst + hb * AT_TILE, &tm, b, col + 32 * hb, row);
+  };
+  if (lane == 0 && w * 32 < len) {
+    load(&bar[0], kt, kc, row0 + w * 32);
+    load(&bar[1], vt, vc, row0 + w * 32);
+  }
+  const double inv_sqrt = 1.0 / sqrt((double)DH);
+  // ---- scores of this warp's chunks, local max
+  double mx = -INFINITY;
+  uint32_t kph = 0, vph = 0;
+  for (int j0 = w * 32; j0 < len; j0 += NS * 32) {
+    mbar_wait(&bar[0], kph);
+    kph ^= 1;
+    const int j = j0 + lane;
+    if (j < len) {
+      double dot = 0.0;
+#pragma unroll
+      for (int c = 0; c < DH; c += 4) {
+        const float4 k4 = *reinterpret_cast<const float4*>(kt + (c >> 5) * AT_TILE + at_swz(lane, c & 31));
+        const float4 q4 = *reinterpret_cast<const float4*>(q + c);
+        dot = __fma_rn((double)q4.x, (double)k4.x, dot);
+        dot = __fma_rn((double)q4.y, (double)k4.y, dot);
+        dot = __fma_rn((double)q4.z, (double)k4.z, dot);
+        dot = __fma_rn((double)q4.w, (double)k4.w, dot);
+      }
+      const double sj = __dmul_rn(dot, inv_sqrt);
+      sc[j] = sj;
+      mx = fmax(mx, sj);
+    }
+    __syncwarp();
+    if (lane == 0 && j0 + NS * 32 < len) load(&bar[0], kt, kc, row0 + j0 + NS * 32);
+  }
+  mx = warp_max_f64(mx);
+  if (lane == 0) pm[w] = mx;
+  __syncthreads();
+  double m = -INFINITY;
+  for (int k = 0; k < NS; ++k) m = fmax(m, pm[k]);
+  __syncthreads();   // pm is reused for the partial Z below
+  // ---- p_j and the partial normaliser
+  double z = 0.0;
+  for (int j0 = w * 32; j0 < len; j0 += NS * 32) {
+    const int j = j0 + lane;
+    if (j < len) {
+      const double p = exp(__dsub_rn(sc[j], m));
+      sc[j] = p;
+      z = __dadd_rn(z, p);
+    }
+  }
+  z = warp_sum_f64(z);
+  if (lane == 0) pm[w] = z;
+  __syncwarp();
+  // ---- partial context over this warp's positions, in order
+  double acc[HB];
+#pragma unroll
+  for (int i = 0; i < HB; ++i) acc[i] = 0.0;
+  for (int j0 = w * 32; j0 < len; j0 += NS * 32) {
+    mbar_wait(&bar[1], vph);
+    vph ^= 1;
+    const int je = min(32, len - j0);
+    for (int jj = 0; jj < je; ++jj) {
+      const double p = sc[j0 + jj];
+#pragma unroll
+      for (int i = 0; i < HB; ++i)
+        acc[i] = __fma_rn(p, (double)*reinterpret_cast<const float*>(vt + i * AT_TILE + at_swz(jj, lane)), acc[i]);
+    }
+    __syncwarp();
+    if (lane == 0 && j0 + NS * 32 < len) load(&bar[1], vt, vc, row0 + j0 + NS * 32);
+  }
+#pragma unroll
+  for (int i = 0; i < HB; ++i) pacc[w * DH + lane + 32 * i] = acc[i];
+  __syncthreads();
+  if (w != 0) return;
+  double zt = 0.0;
+  for (int k = 0; k < NS; ++k) zt = __dadd_rn(zt, pm[k]);
+  int8_t* out = a.out_q + (int64_t)r * a.d + h * DH;
+#pragma unroll
+  for (int i = 0; i < HB; ++i) {
+    const int c = lane + 32 * i;
+    double s = 0.0;
+    for (int k = 0; k < NS; ++k) s = __dadd_rn(s, pacc[k * DH + c]);
+    const float ctx = len > 0 ? (float)__ddiv_rn(s, zt) : 0.0f;
+    out[c] = (int8_t)q8(ctx, a.clip, a.sigma);
+    if (a.out_f) a.out_f[(int64_t)r * a.d + h * DH + c] = ctx;
+  }
+}
+
+inline size_t attn_split_tma_smem(int ns, int dh, int span) {
+  return 1024 + (size_t)ns * 2 * (dh / 32) * AT_TILE + ((size_t)span + ns + (size_t)ns * dh) * 8 + 16 * ns;
 }
 
 // Source attention split over NS warps per (row, head) for long spans (A7): warp w of a group
@@ -679,6 +845,7 @@ cudaError_t attn_init() {   // once per device
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn_enc_r, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)enc_r_smem(ENC_R_MAX));
+
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              ATTN_WARPS * (MNMT_MAX_KV + 64) * (int)sizeof(double));
@@ -688,6 +855,18 @@ cudaError_t attn_init() {   // once per device
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn_tma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)attn_tma_smem(32, MNMT_MAX_KV));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn_split_tma<4, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)attn_split_tma_smem(4, 64, MNMT_MAX_KV));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn_split_tma<2, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)attn_split_tma_smem(2, 64, MNMT_MAX_KV));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn_split_tma<4, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)attn_split_tma_smem(4, 32, MNMT_MAX_KV));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn_split_tma<2, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)attn_split_tma_smem(2, 32, MNMT_MAX_KV));
 
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn_split<2, bf16s>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -745,7 +924,33 @@ cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
   if (b.dh > 64 || (b.dh & 3)) return cudaErrorInvalidValue;
   // long source spans at small row counts: several warps per (row, head) (measured: -6 % per
   // step at 64 rows with 100-word sources; at 206 rows the extra warps cost more than they save)
+  static const bool tma = [] {   // env MNMT_ATTN_TMA=0: the generic kernels (A/B)
+    const char* e = getenv("MNMT_ATTN_TMA");
+    return !(e && e[0] == '0');
+  }();
+  // self-attention through TMA tiles: AttnArgs::tma_self (model option "attn_tma_self": 0 off,
+  // 1 the split kernel for long decodes at <= 128 rows, 2 also the one-warp kernel); A/B switch
+  // MNMT_ATTN_TMA_SPLIT=0: long spans at <= 128 rows through the generic split kernel
+  const int tma_self = b.tma_self;
+  static const int tma_split = [] {
+    const char* e = getenv("MNMT_ATTN_TMA_SPLIT");
+    return e ? atoi(e) : 1;
+  }();
+  const bool use_tma = tma && b.tmap && !b.kv16 && !b.anc && (b.dh == 64 || b.dh == 32) &&
+                       (b.mode != ATTN_SELF || tma_self > 0);
   const int ns = (b.mode == ATTN_SRC && b.n <= 128) ? (b.span >= 128 ? 4 : b.span >= 64 ? 2 : 1) : 1;
+  // with TMA tiles the self-attention of long decodes splits the same way (R25)
+  const int ns_t = !tma_split ? 1 : ((b.mode == ATTN_SRC || b.mode == ATTN_SELF) && b.n <= 128)
+                       ? (b.span >= 128 ? 4 : b.span >= 64 ? 2 : 1) : 1;
+  if (use_tma && (ns_t == 2 || ns_t == 4)) {
+    const dim3 grid((unsigned)warps), block(ns_t * 32);
+    const size_t smem = attn_split_tma_smem(ns_t, b.dh, b.span);
+    if (ns_t == 4)
+      return b.dh == 64 ? launch_pdl(k_attn_split_tma<4, 64>, grid, block, smem, st, *b.tmap, b)
+                        : launch_pdl(k_attn_split_tma<4, 32>, grid, block, smem, st, *b.tmap, b);
+    return b.dh == 64 ? launch_pdl(k_attn_split_tma<2, 64>, grid, block, smem, st, *b.tmap, b)
+                      : launch_pdl(k_attn_split_tma<2, 32>, grid, block, smem, st, *b.tmap, b);
+  }
   if (ns == 2 || ns == 4) {
     const int G = ATTN_WARPS / ns;
     const dim3 grid((unsigned)((warps + G - 1) / G)), block(ATTN_WARPS * 32);
@@ -755,11 +960,7 @@ cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
     return ns == 2 ? launch_pdl(k_attn_split<2, float>, grid, block, attn_split_smem(2, b.span), st, b)
                    : launch_pdl(k_attn_split<4, float>, grid, block, attn_split_smem(4, b.span), st, b);
   }
-  static const bool tma = [] {   // env MNMT_ATTN_TMA=0: the generic kernel (A/B)
-    const char* e = getenv("MNMT_ATTN_TMA");
-    return !(e && e[0] == '0');
-  }();
-  if (tma && b.tmap && !b.kv16 && (b.mode == ATTN_SRC || b.mode == ATTN_ENC) && (b.dh == 64 || b.dh == 32)) {
+  if (use_tma && (b.mode != ATTN_SELF || tma_self == 2)) {
     const dim3 grid((unsigned)((warps + AT_WARPS - 1) / AT_WARPS)), block(AT_WARPS * 32);
     const size_t smem = attn_tma_smem(b.dh, b.span);
     return b.dh == 64 ? launch_pdl(k_attn_tma<64>, grid, block, smem, st, *b.tmap, b)

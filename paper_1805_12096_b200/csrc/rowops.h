@@ -83,6 +83,8 @@ struct AttnArgs {
   // the K/V rows; this launch's kv == the map's base + kv_row0 rows
   const CUtensorMap* tmap;
   int64_t kv_row0;
+  int tma_self;             // self mode: 0 generic kernels, 1 TMA split kernel for long decodes at
+                            // <= 128 rows, 2 also the one-warp TMA kernel (measured per workload)
 };
 
 // Encoder self-attention over Q|K|V rows [M x 3d] (A3), one CTA per (sentence, head).

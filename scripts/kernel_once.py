@@ -47,9 +47,11 @@ else:
     kv = torch.randn(Mr * S, 2 * d, device=dev); q = torch.randn(Mr, d, device=dev)
     if k == "attn16":   # bf16 source K/V (F3)
         kv = kv.to(torch.bfloat16)
-    op = M.op_attention_bf16 if k == "attn16" else M.op_attention
-    S, Ln = torch.from_numpy(st).to(dev), torch.from_numpy(L).to(dev)
+    Sd, Ln = torch.from_numpy(st).to(dev), torch.from_numpy(L).to(dev)
     oq = torch.empty(Mr, d, dtype=torch.int8, device=dev)
     for _ in range(4):
-        op(q.data_ptr(), d, kv.data_ptr(), 2 * d, 0, d, S.data_ptr(), Ln.data_ptr(), Mr, d, H, 2.0, oq.data_ptr(), None, None)
+        if k == "attn16":
+            M.op_attention_bf16(q.data_ptr(), d, kv.data_ptr(), 2 * d, 0, d, Sd.data_ptr(), Ln.data_ptr(), Mr, d, H, 2.0, oq.data_ptr(), None, None)
+        else:   # the decode path's choice (TMA tiles for d_h = 32 / 64)
+            M.op_src_attention(q.data_ptr(), d, kv.data_ptr(), Mr * S, 2 * d, 0, d, Sd.data_ptr(), Ln.data_ptr(), S, Mr, d, H, 2.0, oq.data_ptr(), None, None)
 torch.cuda.synchronize()

@@ -104,6 +104,25 @@ def test_long_sources_split_attention(lo, hi):
     assert ex == tot, f"{tot - ex} flagged near-ties"
 
 
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("dims", [d for d in TINY_VARIANTS if d.decoder == 0 and d.d_model == 256],
+                         ids=lambda d: d.name)
+def test_self_attention_tma(dims, mode):
+    """Self-attention through the TMA-tiled kernels (option attn_tma_self: 1 = the split kernel for
+    long decodes at <= 128 rows, 2 = every step; the step's k, v appended before the tensor copies
+    read them): teacher-forced intermediates within tolerance of the oracle, ids bit-exact; and
+    free-running ids with decodes long enough (70 steps) for the 2- and 4-warp splits."""
+    w, om, gm = pair(dims, 11)
+    gm.set_option("attn_tma_self", mode)
+    ss, forced, foff = forced_case(dims, 9, 0, 13, 0, 17, seed=3)
+    tot, ex, fl = run_forced_parity(dims, w, om, gm, ss, forced, foff)
+    assert ex == tot, f"{tot - ex} flagged near-ties"
+    ls = synth.random_set(12, 30, 70, seed=19, vocab=dims.vocab)
+    ls.max_len[:] = np.random.default_rng(4).integers(60, 130, size=12)
+    ref = om.decode_many(ls, 4)
+    assert all(np.array_equal(a, b) for a, b in zip(gm.translate(ls, 1 << 20), ref))
+
+
 @pytest.mark.parametrize("dims", TINY_VARIANTS, ids=lambda d: d.name)
 def test_tiny_free_running(dims):
     w, om, gm = pair(dims, 12)
