@@ -802,7 +802,7 @@ bool make_tmap_kv(CUtensorMap* map, const void* base, int64_t rows, int64_t cols
   if (!enc || rows < 1 || cols % 4 != 0 || ((uintptr_t)base & 15)) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
-  cuuint32_t box[2] = {32u, 32u};
+  cuuint32_t box[2] = {32u, 8u};
   cuuint32_t estr[2] = {1u, 1u};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

@@ -81,7 +81,7 @@ constexpr int SMALLM_MAX = 32;
 // box {128 bytes, 64 rows}, 128-byte swizzle (the UMMA K-major SW128 atom).
 bool make_tmap_i8(CUtensorMap* map, const void* base, int64_t rows, int64_t K);
 // Tensor map over fp32 key/value rows [rows x cols] (cols contiguous, row stride = cols): box
-// {32 floats, 32 rows}, 128-byte swizzle (the source-attention K / V head tiles).
+// {32 floats, 8 rows} (one 128-byte swizzle atom), 128-byte swizzle (the attention K / V tiles).
 bool make_tmap_kv(CUtensorMap* map, const void* base, int64_t rows, int64_t cols);
 
 // A is [>= M x K] activation codes, B is [N x K] weight codes (both via make_tmap_i8).

@@ -155,7 +155,8 @@ __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn(AttnArgs a) {
 // conflict-free: lane = position reading 16-byte column groups of its row (scores), lane =
 // column reading one row (context).  Arithmetic and order are warp_attend's (identical outputs).
 constexpr int AT_WARPS = 4;
-constexpr int AT_TILE = 32 * 128;   // one box: 32 rows x 32 floats
+constexpr int AT_TILE = 32 * 128;   // one 32-position chunk of 32 floats (four 8-row boxes)
+constexpr int AT_BOX = 8 * 128;     // one TMA box: 8 rows x 32 floats = one 128B-swizzle atom
 
 __device__ __forceinline__ int at_swz(int j, int cc) {   // byte offset of (row j, float cc) in a box
   return j * 128 + ((((cc >> 2) ^ (j & 7)) << 4) | ((cc & 3) << 2));
@@ -216,14 +217,17 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
   }
   const int row0 = (int)(a.kv_row0 + start);
   const int kc = a.k_off + h * DH, vc = a.v_off + h * DH;
-  auto load = [&](uint64_t* b, uint8_t* dst, int col, int row) {
-    mbar_arrive_expect_tx(b, HB * AT_TILE);
-#pragma unroll
-    for (int hb = 0; hb < HB; ++hb) tma_load_2d(dst + hb * AT_TILE, &tm, b, col + 32 * hb, row);
+  // chunk c0 (positions c0 .. c0 + 31 of the span): only the 8-row boxes holding positions < len
+  auto load = [&](uint64_t* b, uint8_t* dst, int col, int c0) {
+    const int nb = min(4, (len - c0 + 7) >> 3);
+    mbar_arrive_expect_tx(b, HB * nb * AT_BOX);
+    for (int hb = 0; hb < HB; ++hb)
+      for (int x = 0; x < nb; ++x)
+        tma_load_2d(dst + hb * AT_TILE + x * AT_BOX, &tm, b, col + 32 * hb, row0 + c0 + 8 * x);
   };
   if (lane == 0 && len > 0) {
-    load(&bar[0], kt, kc, row0);
-    load(&bar[1], vt, vc, row0);
+    load(&bar[0], kt, kc, 0);
+    load(&bar[1], vt, vc, 0);
   }
   const float* q = a.q + (int64_t)r * a.ldq + h * DH;
   const double inv_sqrt = 1.0 / sqrt((double)DH);
@@ -249,7 +253,7 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
       mx = fmax(mx, s);
     }
     __syncwarp();
-    if (lane == 0 && c0 + 32 < len) load(&bar[0], kt, kc, row0 + c0 + 32);
+    if (lane == 0 && c0 + 32 < len) load(&bar[0], kt, kc, c0 + 32);
   }
   mx = warp_max_f64(mx);
   double z = 0.0;
@@ -274,7 +278,7 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
         acc[i] = __fma_rn(p, (double)*reinterpret_cast<const float*>(vt + i * AT_TILE + at_swz(jj, lane)), acc[i]);
     }
     __syncwarp();
-    if (lane == 0 && c0 + 32 < len) load(&bar[1], vt, vc, row0 + c0 + 32);
+    if (lane == 0 && c0 + 32 < len) load(&bar[1], vt, vc, c0 + 32);
   }
   int8_t* out = a.out_q + (int64_t)r * a.d + h * DH;
 #pragma unroll
@@ -348,14 +352,17 @@ __global__ void __launch_bounds__(NS * 32) k_attn_split_tma(const __grid_constan
   }
   const int row0 = (int)(a.kv_row0 + start);
   const int kc = a.k_off + h * DH, vc = a.v_off + h * DH;
-  auto load = [&](uint64_t* b, uint8_t* dst, int col, int row) {
-    mbar_arrive_expect_tx(b, HB * AT_TILE);
-#pragma unroll
-    for (int hb = 0; hb < HB; ++hb) tma_load_2d(dst + hb * AT_TILE, &tm, b, col + 32 * hb, row);
+  // chunk c0 (positions c0 .. c0 + 31 of the span): only the 8-row boxes holding positions < len
+  auto load = [&](uint64_t* b, uint8_t* dst, int col, int c0) {
+    const int nb = min(4, (len - c0 + 7) >> 3);
+    mbar_arrive_expect_tx(b, HB * nb * AT_BOX);
+    for (int hb = 0; hb < HB; ++hb)
+      for (int x = 0; x < nb; ++x)
+        tma_load_2d(dst + hb * AT_TILE + x * AT_BOX, &tm, b, col + 32 * hb, row0 + c0 + 8 * x);
   };
   if (lane == 0 && w * 32 < len) {
-    load(&bar[0], kt, kc, row0 + w * 32);
-    load(&bar[1], vt, vc, row0 + w * 32);
+    load(&bar[0], kt, kc, w * 32);
+    load(&bar[1], vt, vc, w * 32);
   }
   const double inv_sqrt = 1.0 / sqrt((double)DH);
   // ---- scores of this warp's chunks, local max
@@ -381,7 +388,7 @@ __global__ void __launch_bounds__(NS * 32) k_attn_split_tma(const __grid_constan
       mx = fmax(mx, sj);
     }
     __syncwarp();
-    if (lane == 0 && j0 + NS * 32 < len) load(&bar[0], kt, kc, row0 + j0 + NS * 32);
+    if (lane == 0 && j0 + NS * 32 < len) load(&bar[0], kt, kc, j0 + NS * 32);
   }
   mx = warp_max_f64(mx);
   if (lane == 0) pm[w] = mx;
@@ -417,7 +424,7 @@ __global__ void __launch_bounds__(NS * 32) k_attn_split_tma(const __grid_constan
         acc[i] = __fma_rn(p, (double)*reinterpret_cast<const float*>(vt + i * AT_TILE + at_swz(jj, lane)), acc[i]);
     }
     __syncwarp();
-    if (lane == 0 && j0 + NS * 32 < len) load(&bar[1], vt, vc, row0 + j0 + NS * 32);
+    if (lane == 0 && j0 + NS * 32 < len) load(&bar[1], vt, vc, j0 + NS * 32);
   }
 #pragma unroll
   for (int i = 0; i < HB; ++i) pacc[w * DH + lane + 32 * i] = acc[i];
