@@ -173,7 +173,9 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
   uint8_t* kt = base + wi * WB;
   uint8_t* vt = kt + HB * AT_TILE;
   double* sc = reinterpret_cast<double*>(base + AT_WARPS * WB) + (size_t)wi * a.span;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(base + AT_WARPS * WB + (size_t)AT_WARPS * a.span * 8) + 2 * wi;
+  // per warp: two mbarriers, then its query (DH floats)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + AT_WARPS * WB + (size_t)AT_WARPS * a.span * 8) +
+                  (2 + DH / 2) * wi;
   if (lane == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -230,6 +232,11 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
     load(&bar[1], vt, vc, 0);
   }
   const float* q = a.q + (int64_t)r * a.ldq + h * DH;
+  // the query staged in shared memory while the tiles are in flight (the dot loop then reads
+  // only shared memory: one broadcast per float4)
+  float4* qv = reinterpret_cast<float4*>(bar + 2);
+  if (lane < DH / 4) qv[lane] = *reinterpret_cast<const float4*>(q + 4 * lane);
+  __syncwarp();
   const double inv_sqrt = 1.0 / sqrt((double)DH);
   double mx = -INFINITY;
   uint32_t kph = 0, vph = 0;
@@ -242,7 +249,7 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
 #pragma unroll
       for (int c = 0; c < DH; c += 4) {
         const float4 k4 = *reinterpret_cast<const float4*>(kt + (c >> 5) * AT_TILE + at_swz(lane, c & 31));
-        const float4 q4 = *reinterpret_cast<const float4*>(q + c);   // same address in all lanes
+        const float4 q4 = qv[c >> 2];
         dot = __fma_rn((double)q4.x, (double)k4.x, dot);
         dot = __fma_rn((double)q4.y, (double)k4.y, dot);
         dot = __fma_rn((double)q4.z, (double)k4.z, dot);
@@ -291,7 +298,7 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
 }
 
 inline size_t attn_tma_smem(int dh, int span) {
-  return 1024 + (size_t)AT_WARPS * (2 * (dh / 32) * AT_TILE + (size_t)span * 8 + 16);
+  return 1024 + (size_t)AT_WARPS * (2 * (dh / 32) * AT_TILE + (size_t)span * 8 + 16 + (size_t)dh * 4);
 }
 
 // Long spans at small row counts, split over NS warps per (row, head) with TMA tiles (A7 and the
@@ -313,7 +320,7 @@ __global__ void __launch_bounds__(NS * 32) k_attn_split_tma(const __grid_constan
   double* sc = reinterpret_cast<double*>(base + NS * WB);   // [span]
   double* pm = sc + a.span;                                 // [NS]
   double* pacc = pm + NS;                                   // [NS][DH]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(pacc + NS * DH) + 2 * w;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(pacc + NS * DH) + (2 + DH / 2) * w;   // + query
   if (lane == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -364,6 +371,10 @@ __global__ void __launch_bounds__(NS * 32) k_attn_split_tma(const __grid_constan
     load(&bar[0], kt, kc, w * 32);
     load(&bar[1], vt, vc, w * 32);
   }
+  // the query staged in shared memory while the tiles are in flight (broadcast reads)
+  float4* qv = reinterpret_cast<float4*>(bar + 2);
+  if (lane < DH / 4) qv[lane] = *reinterpret_cast<const float4*>(q + 4 * lane);
+  __syncwarp();
   const double inv_sqrt = 1.0 / sqrt((double)DH);
   // ---- scores of this warp's chunks, local max
   double mx = -INFINITY;
@@ -377,7 +388,7 @@ __global__ void __launch_bounds__(NS * 32) k_attn_split_tma(const __grid_constan
 #pragma unroll
       for (int c = 0; c < DH; c += 4) {
         const float4 k4 = *reinterpret_cast<const float4*>(kt + (c >> 5) * AT_TILE + at_swz(lane, c & 31));
-        const float4 q4 = *reinterpret_cast<const float4*>(q + c);
+        const float4 q4 = qv[c >> 2];
         dot = __fma_rn((double)q4.x, (double)k4.x, dot);
         dot = __fma_rn((double)q4.y, (double)k4.y, dot);
         dot = __fma_rn((double)q4.z, (double)k4.z, dot);
@@ -445,7 +456,8 @@ __global__ void __launch_bounds__(NS * 32) k_attn_split_tma(const __grid_constan
 }
 
 inline size_t attn_split_tma_smem(int ns, int dh, int span) {
-  return 1024 + (size_t)ns * 2 * (dh / 32) * AT_TILE + ((size_t)span + ns + (size_t)ns * dh) * 8 + 16 * ns;
+  return 1024 + (size_t)ns * 2 * (dh / 32) * AT_TILE + ((size_t)span + ns + (size_t)ns * dh) * 8 +
+         (16 + (size_t)dh * 4) * ns;
 }
 
 // Source attention split over NS warps per (row, head) for long spans (A7): warp w of a group
