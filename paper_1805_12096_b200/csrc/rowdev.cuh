@@ -260,10 +260,10 @@ __device__ __forceinline__ void warp_attend(const float* __restrict__ q, const K
                                             float clip, float sigma, int8_t* out_q, float* out_f,
                                             const int32_t* rows = nullptr) {
   const int lane = threadIdx.x & 31;
-  if constexpr (sizeof(KT) == 8) {   // reused K/V: convert the query once as well
-    for (int c = lane; c < dh; c += 32) qd[c] = (double)q[c];
-    __syncwarp();
-  }
+  // the query converted once into the warp's scratch: the dot loop then reads shared memory
+  // (broadcasts) instead of global memory inside its fp64 chain
+  for (int c = lane; c < dh; c += 32) qd[c] = (double)q[c];
+  __syncwarp();
   const double inv_sqrt = 1.0 / sqrt((double)dh);
   double mx = -INFINITY;
   for (int j = lane; j < len; j += 32) {
@@ -273,8 +273,7 @@ __device__ __forceinline__ void warp_attend(const float* __restrict__ q, const K
       double kk[4], qq[4];
       if constexpr (sizeof(KT) <= 4) {
         ld4_f64(kr + c, kk);
-        const float4 q4 = *reinterpret_cast<const float4*>(q + c);   // same address in all lanes
-        qq[0] = q4.x; qq[1] = q4.y; qq[2] = q4.z; qq[3] = q4.w;
+        qq[0] = qd[c]; qq[1] = qd[c + 1]; qq[2] = qd[c + 2]; qq[3] = qd[c + 3];
       } else {
         const double2 a = *reinterpret_cast<const double2*>(kr + c);
         const double2 b = *reinterpret_cast<const double2*>(kr + c + 2);

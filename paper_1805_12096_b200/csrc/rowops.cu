@@ -474,6 +474,7 @@ __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn_split(AttnArgs a) {
   double* sc = as_smem + (size_t)g * span;                // [G][span] scores, then p
   double* pm = as_smem + (size_t)G * span;                // [G][NS] partial max, then partial Z
   double* pacc = pm + G * NS;                             // [G][NS][64] partial contexts
+  double* qs = pacc + G * NS * 64;                        // [G][64] the group's query
   pdl_wait();
   pdl_trigger_early();
   const int64_t gw = (int64_t)blockIdx.x * G + g;
@@ -492,6 +493,10 @@ __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn_split(AttnArgs a) {
   if constexpr (sizeof(KT) == 2) kvb = a.kv16; else kvb = a.kv;   // bf16 source K/V (F3)
   const KT* K = kvb + (int64_t)start * a.ldkv + a.k_off + h * dh;
   const KT* V = kvb + (int64_t)start * a.ldkv + a.v_off + h * dh;
+  double* qg = qs + g * 64;   // the query, converted once by warp 0 of the group
+  if (w == 0)
+    for (int c = lane; c < dh; c += 32) qg[c] = (double)q[c];
+  __syncthreads();
   const double inv_sqrt = 1.0 / sqrt((double)dh);
   // ---- scores of this warp's chunks, local max
   double mx = -INFINITY;
@@ -503,11 +508,10 @@ __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn_split(AttnArgs a) {
       for (int c = 0; c < dh; c += 4) {
         double kk[4];
         ld4_f64(kr + c, kk);
-        const float4 q4 = *reinterpret_cast<const float4*>(q + c);
-        dot = __fma_rn((double)q4.x, kk[0], dot);
-        dot = __fma_rn((double)q4.y, kk[1], dot);
-        dot = __fma_rn((double)q4.z, kk[2], dot);
-        dot = __fma_rn((double)q4.w, kk[3], dot);
+        dot = __fma_rn(qg[c], kk[0], dot);
+        dot = __fma_rn(qg[c + 1], kk[1], dot);
+        dot = __fma_rn(qg[c + 2], kk[2], dot);
+        dot = __fma_rn(qg[c + 3], kk[3], dot);
       }
       const double sj = __dmul_rn(dot, inv_sqrt);
       sc[j] = sj;
@@ -569,7 +573,7 @@ __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn_split(AttnArgs a) {
 
 inline size_t attn_split_smem(int ns, int span) {
   const int G = ATTN_WARPS / ns;
-  return ((size_t)G * span + (size_t)G * ns + (size_t)G * ns * 64) * sizeof(double);
+  return ((size_t)G * span + (size_t)G * ns + (size_t)G * ns * 64 + (size_t)G * 64) * sizeof(double);
 }
 
 constexpr int FIN_THREADS = 1024;
