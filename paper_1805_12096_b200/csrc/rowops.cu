@@ -162,16 +162,20 @@ __device__ __forceinline__ int at_swz(int j, int cc) {   // byte offset of (row 
   return j * 128 + ((((cc >> 2) ^ (j & 7)) << 4) | ((cc & 3) << 2));
 }
 
-template <int DH>
+// SHARE (default): the V chunks reuse the K buffer (the first requested as soon as the last K
+// chunk's scores are formed, overlapping the normaliser): half the shared memory per warp, twice
+// the resident warps (six CTAs of 4 warps per SM instead of three), one more round trip per warp.
+// Measured: 630 rows d = 1024 33.8 -> 23.9 us (warm), big job 106.9 -> 102.0 ms.
+template <int DH, bool SHARE>
 __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constant__ CUtensorMap tm,
                                                             AttnArgs a) {
   constexpr int HB = DH / 32;                 // 32-column boxes per head slice
-  constexpr int WB = 2 * HB * AT_TILE;        // this warp's K and V tiles
+  constexpr int WB = (SHARE ? 1 : 2) * HB * AT_TILE;   // this warp's K (and V) tiles
   extern __shared__ uint8_t at_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(at_raw) + 1023) & ~uintptr_t(1023));
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* kt = base + wi * WB;
-  uint8_t* vt = kt + HB * AT_TILE;
+  uint8_t* vt = SHARE ? kt : kt + HB * AT_TILE;
   double* sc = reinterpret_cast<double*>(base + AT_WARPS * WB) + (size_t)wi * a.span;
   // per warp: two mbarriers, then its query (DH floats)
   uint64_t* bar = reinterpret_cast<uint64_t*>(base + AT_WARPS * WB + (size_t)AT_WARPS * a.span * 8) +
@@ -229,7 +233,7 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
   };
   if (lane == 0 && len > 0) {
     load(&bar[0], kt, kc, 0);
-    load(&bar[1], vt, vc, 0);
+    if constexpr (!SHARE) load(&bar[1], vt, vc, 0);
   }
   const float* q = a.q + (int64_t)r * a.ldq + h * DH;
   // the query staged in shared memory while the tiles are in flight (the dot loop then reads
@@ -262,6 +266,10 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
     __syncwarp();
     if (lane == 0 && c0 + 32 < len) load(&bar[0], kt, kc, c0 + 32);
   }
+  // SHARE: every lane has read the K buffer (the __syncwarp above); the first V chunk goes into
+  // it while the normaliser is formed
+  if constexpr (SHARE)
+    if (lane == 0 && len > 0) load(&bar[1], vt, vc, 0);
   mx = warp_max_f64(mx);
   double z = 0.0;
   for (int j = lane; j < len; j += 32) {
@@ -297,8 +305,9 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
   }
 }
 
-inline size_t attn_tma_smem(int dh, int span) {
-  return 1024 + (size_t)AT_WARPS * (2 * (dh / 32) * AT_TILE + (size_t)span * 8 + 16 + (size_t)dh * 4);
+inline size_t attn_tma_smem(int dh, int span, bool share) {
+  return 1024 + (size_t)AT_WARPS * ((share ? 1 : 2) * (dh / 32) * AT_TILE + (size_t)span * 8 + 16 +
+                                    (size_t)dh * 4);
 }
 
 // Long spans at small row counts, split over NS warps per (row, head) with TMA tiles (A7 and the
@@ -873,11 +882,17 @@ cudaError_t attn_init() {   // once per device
     e = cudaFuncSetAttribute(k_attn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              ATTN_WARPS * (MNMT_MAX_KV + 64) * (int)sizeof(double));
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_attn_tma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)attn_tma_smem(64, MNMT_MAX_KV));
+    e = cudaFuncSetAttribute(k_attn_tma<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)attn_tma_smem(64, MNMT_MAX_KV, false));
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_attn_tma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)attn_tma_smem(32, MNMT_MAX_KV));
+    e = cudaFuncSetAttribute(k_attn_tma<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)attn_tma_smem(32, MNMT_MAX_KV, false));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn_tma<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)attn_tma_smem(64, MNMT_MAX_KV, true));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn_tma<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)attn_tma_smem(32, MNMT_MAX_KV, true));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn_split_tma<4, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)attn_split_tma_smem(4, 64, MNMT_MAX_KV));
@@ -984,10 +999,17 @@ cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
                    : launch_pdl(k_attn_split<4, float>, grid, block, attn_split_smem(4, b.span), st, b);
   }
   if (use_tma && (b.mode != ATTN_SELF || tma_self == 2)) {
+    static const bool share = [] {   // V reuses the K buffer (env MNMT_ATTN_SHARE=0: separate, A/B)
+      const char* e = getenv("MNMT_ATTN_SHARE");
+      return !(e && e[0] == '0');
+    }();
     const dim3 grid((unsigned)((warps + AT_WARPS - 1) / AT_WARPS)), block(AT_WARPS * 32);
-    const size_t smem = attn_tma_smem(b.dh, b.span);
-    return b.dh == 64 ? launch_pdl(k_attn_tma<64>, grid, block, smem, st, *b.tmap, b)
-                      : launch_pdl(k_attn_tma<32>, grid, block, smem, st, *b.tmap, b);
+    const size_t smem = attn_tma_smem(b.dh, b.span, share);
+    if (share)
+      return b.dh == 64 ? launch_pdl(k_attn_tma<64, true>, grid, block, smem, st, *b.tmap, b)
+                        : launch_pdl(k_attn_tma<32, true>, grid, block, smem, st, *b.tmap, b);
+    return b.dh == 64 ? launch_pdl(k_attn_tma<64, false>, grid, block, smem, st, *b.tmap, b)
+                      : launch_pdl(k_attn_tma<32, false>, grid, block, smem, st, *b.tmap, b);
   }
   const dim3 grid((unsigned)((warps + ATTN_WARPS - 1) / ATTN_WARPS)), block(ATTN_WARPS * 32);
   const size_t smem = (size_t)ATTN_WARPS * (b.span + 64) * 8;
