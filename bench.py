@@ -53,20 +53,20 @@ DEFAULT_WORKLOAD = "big-newstest-8192w"   # BASELINE.json configs[3]: the metric
 # smallm / smallm_kmax: the small-M (IDP4A, <= 32 live rows) GEMM path's row bound and deepest K
 # per workload, from the A/B in profiles/r1_ab_smallm.txt (small-aan: +2 % with FFN2's K = 2048
 # included; the others neutral or slower, so off; big re-measured in round 2: slower).
-# attn_tma_self: self-attention decoders through the TMA-tiled kernels (profiles/r2_attn_tma_ab.txt:
-# big 111.5-112.4 -> 116.5-117.0 ms per job (split kernel) / 122.3-122.5 (every step); base
-# self-attention 65.2 / 65.2 / 67.1 ms for 0 / 1 / 2): off.
+# attn_tma_self: self-attention decoders through the TMA-tiled kernels (profiles/r2_attn_tma_ab.txt,
+# after the V tiles started reusing the K buffers: big 99.1-99.4 / 100.1-100.2 / 97.7-97.8 ms per
+# job for 0 / 1 / 2, base self-attention 59.9 / 59.2 / 56.4 ms): 2.
 WORKLOAD_OPTS = {
     "small-aan-newstest-8192w": {"green_sms": 48, "lane_tiers": 40, "smallm": 32, "smallm_kmax": 2048,
-                                 "attn_tma_self": 0},
+                                 "attn_tma_self": 2},
     "tiny192-aan-newstest-8192w": {"green_sms": 56, "lane_tiers": 40, "smallm": 0, "smallm_kmax": 512,
-                                   "attn_tma_self": 0},
+                                   "attn_tma_self": 2},
     "base-newstest-8192w": {"green_sms": 24, "lane_tiers": 40, "smallm": 0, "smallm_kmax": 512,
-                            "attn_tma_self": 0},
+                            "attn_tma_self": 2},
     "base-aan-newstest-8192w": {"green_sms": 40, "lane_tiers": 35, "smallm": 32, "smallm_kmax": 512,
-                                "attn_tma_self": 0},
+                                "attn_tma_self": 2},
     "big-newstest-8192w": {"green_sms": 0, "lane_tiers": 25, "smallm": 0, "smallm_kmax": 512,
-                           "attn_tma_self": 0},
+                           "attn_tma_self": 2},
 }
 L2_FLUSH_BYTES = 512 << 20   # > 126 MB L2
 

@@ -224,9 +224,9 @@ mnmt_status mnmt_translate_forced(mnmt_model* m, const int32_t* src_ids_host,
  *   "smallm_wmax"          largest weight matrix N x K (bytes) the small-M path takes (default
  *                          2^20: the d x d maps of the big student, not its FFN / Q|K|V maps).
  *   "attn_tma_self"        self-attention decoder: 1 = long decodes at <= 128 rows attend through
- *                          the TMA-tiled split kernel, 2 = every step through TMA tiles, 0 (default)
- *                          = the generic kernels (identical results up to fp64 summation order,
- *                          R25; measured per workload).
+ *                          the TMA-tiled split kernel, 2 (default) = every step through TMA tiles,
+ *                          0 = the generic kernels (identical results up to fp64 summation order,
+ *                          R25; measured: 2 fastest on base and big).
  *   "split_k"              1: decoder GEMMs with K >= 4096 (or >= 2048 at <= 32 rows) spread their
  *                          K blocks over a 2-4 CTA cluster (exact s32 partials added in the
  *                          leader); 0 (default; measured slower in the 3-lane job).

@@ -197,7 +197,7 @@ struct mnmt_model {
   int smallm = 32;                     // option: row bound of the small-M GEMM path (0 = off)
   int smallm_kmax = 512;               // option: deepest K the small-M path takes
   int64_t smallm_wmax = 1 << 20;       // option: largest weight matrix (N x K bytes) of the small-M path
-  int attn_tma_self = 0;               // option: self-attention through TMA tiles (0 / 1 / 2)
+  int attn_tma_self = 2;               // option: self-attention through TMA tiles (0 / 1 / 2)
   int split_k = 0;                     // option: 1 = split-K clusters by the measured rule (off: slower in the job)
   DevDump dump;                        // (call state) device dumps of a teacher-forced run
   int green_sms = 0;                   // option: SMs of the critical lane's green context (0 = off)

@@ -312,20 +312,21 @@ inline size_t attn_tma_smem(int dh, int span, bool share) {
 
 // Long spans at small row counts, split over NS warps per (row, head) with TMA tiles (A7 and the
 // greedy A6' self-attention; fp32 K/V, d_h = 32 / 64): one (row, head) per CTA of NS warps; warp
-// w takes the 32-position chunks w, w + NS, ... and requests each chunk's K and V tiles by bulk
-// tensor copy (the first chunk's before any arithmetic).  The row max is exchanged first; Z and
+// w takes the 32-position chunks w, w + NS, ... and requests each chunk's K tile by bulk tensor
+// copy (the first before any arithmetic), then its V tiles into the same buffer (the first while
+// the row max is exchanged).  The row max is exchanged first; Z and
 // the context are per-warp partial sums over the warp's positions in order, combined in warp
 // order (R25) -- k_attn_split's arithmetic and order, so outputs are identical to it.  In self
 // mode warp 0 appends this step's k, v before the copies are issued.
 template <int NS, int DH>
 __global__ void __launch_bounds__(NS * 32) k_attn_split_tma(const __grid_constant__ CUtensorMap tm,
                                                             AttnArgs a) {
-  constexpr int HB = DH / 32, WB = 2 * HB * AT_TILE;
+  constexpr int HB = DH / 32, WB = HB * AT_TILE;   // one buffer: V chunks reuse the K buffer
   extern __shared__ uint8_t ast_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ast_raw) + 1023) & ~uintptr_t(1023));
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* kt = base + w * WB;
-  uint8_t* vt = kt + HB * AT_TILE;
+  uint8_t* vt = kt;
   double* sc = reinterpret_cast<double*>(base + NS * WB);   // [span]
   double* pm = sc + a.span;                                 // [NS]
   double* pacc = pm + NS;                                   // [NS][DH]
@@ -376,10 +377,7 @@ __global__ void __launch_bounds__(NS * 32) k_attn_split_tma(const __grid_constan
       for (int x = 0; x < nb; ++x)
         tma_load_2d(dst + hb * AT_TILE + x * AT_BOX, &tm, b, col + 32 * hb, row0 + c0 + 8 * x);
   };
-  if (lane == 0 && w * 32 < len) {
-    load(&bar[0], kt, kc, w * 32);
-    load(&bar[1], vt, vc, w * 32);
-  }
+  if (lane == 0 && w * 32 < len) load(&bar[0], kt, kc, w * 32);
   // the query staged in shared memory while the tiles are in flight (broadcast reads)
   float4* qv = reinterpret_cast<float4*>(bar + 2);
   if (lane < DH / 4) qv[lane] = *reinterpret_cast<const float4*>(q + 4 * lane);
@@ -410,6 +408,8 @@ __global__ void __launch_bounds__(NS * 32) k_attn_split_tma(const __grid_constan
     __syncwarp();
     if (lane == 0 && j0 + NS * 32 < len) load(&bar[0], kt, kc, j0 + NS * 32);
   }
+  // every lane has read the buffer: the warp's first V chunk goes into it during the exchange
+  if (lane == 0 && w * 32 < len) load(&bar[1], vt, vc, w * 32);
   mx = warp_max_f64(mx);
   if (lane == 0) pm[w] = mx;
   __syncthreads();
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(NS * 32) k_attn_split_tma(const __grid_constan
 }
 
 inline size_t attn_split_tma_smem(int ns, int dh, int span) {
-  return 1024 + (size_t)ns * 2 * (dh / 32) * AT_TILE + ((size_t)span + ns + (size_t)ns * dh) * 8 +
+  return 1024 + (size_t)ns * (dh / 32) * AT_TILE + ((size_t)span + ns + (size_t)ns * dh) * 8 +
          (16 + (size_t)dh * 4) * ns;
 }
 
