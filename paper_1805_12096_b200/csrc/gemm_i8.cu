@@ -1209,7 +1209,11 @@ cudaError_t launch_gemm_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const
     const int sms = a.pers_grid > 0 ? a.pers_grid : num_sms();   // the launch's SM budget
     // K <= 512 only: the 32-wide tile still receives a 64-row B box, which costs more than
     // it saves for deep K (measured: big student 126 -> 131 ms per job without this bound)
-    if (tiles64 * 2 <= sms && a.N % 32 == 0 && a.K <= 512) bn = 32;
+    static const int bn32_kmax = [] {   // env MNMT_BN32_KMAX: deepest K of the 32-wide tiles (A/B)
+      const char* e = getenv("MNMT_BN32_KMAX");
+      return e ? atoi(e) : 512;
+    }();
+    if (tiles64 * 2 <= sms && a.N % 32 == 0 && a.K <= bn32_kmax) bn = 32;
   }
   switch (bn) {
     case 32:

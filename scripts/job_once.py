@@ -15,8 +15,8 @@ for kv in filter(None, os.environ.get("OPTS", "lanes=3,lane_tiers=40,pers_reserv
     k, v = kv.split("=")
     m.set_option(k, int(v))
 ss = synth.newstest_set(seed=2014)
-if os.environ.get("LMAX"):   # a length slice of the set (e.g. the bulk tiers: LMAX=45)
-    keep = [i for i in range(ss.n) if int(os.environ.get("LMIN", 0)) <= ss.lengths[i] <= int(os.environ["LMAX"])]
+if os.environ.get("LMAX") or os.environ.get("LMIN"):   # a length slice (bulk tiers: LMAX=45)
+    keep = [i for i in range(ss.n) if int(os.environ.get("LMIN", 0)) <= ss.lengths[i] <= int(os.environ.get("LMAX", 1 << 30))]
     ss = ss.subset(keep)
 dev = torch.device("cuda:0"); st = torch.cuda.current_stream()
 ids = torch.from_numpy(ss.ids).to(dev)
