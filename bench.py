@@ -52,20 +52,21 @@ DEFAULT_WORKLOAD = "big-newstest-8192w"   # BASELINE.json configs[3]: the metric
 # need every SM).
 # smallm / smallm_kmax: the small-M (IDP4A, <= 32 live rows) GEMM path's row bound and deepest K
 # per workload, from the A/B in profiles/r1_ab_smallm.txt (small-aan: +2 % with FFN2's K = 2048
-# included; the others neutral or slower, so off; big re-measured in round 2: slower).
+# included; the others neutral or slower, so off; big with K <= 1024 and the <= 1 MB d x d maps:
+# 91.5 -> 90.8 ms per job in round 2 (profiles/r2_sweep_big_options.txt)).
 # attn_tma_self: self-attention decoders through the TMA-tiled kernels (profiles/r2_attn_tma_ab.txt,
 # after the V tiles started reusing the K buffers: big 99.1-99.4 / 100.1-100.2 / 97.7-97.8 ms per
 # job for 0 / 1 / 2, base self-attention 59.9 / 59.2 / 56.4 ms): 2.
 WORKLOAD_OPTS = {
-    "small-aan-newstest-8192w": {"green_sms": 48, "lane_tiers": 40, "smallm": 32, "smallm_kmax": 2048,
+    "small-aan-newstest-8192w": {"lanes": 3, "green_sms": 48, "lane_tiers": 40, "smallm": 32, "smallm_kmax": 2048,
                                  "attn_tma_self": 2},
-    "tiny192-aan-newstest-8192w": {"green_sms": 56, "lane_tiers": 40, "smallm": 0, "smallm_kmax": 512,
+    "tiny192-aan-newstest-8192w": {"lanes": 3, "green_sms": 56, "lane_tiers": 40, "smallm": 0, "smallm_kmax": 512,
                                    "attn_tma_self": 2},
-    "base-newstest-8192w": {"green_sms": 24, "lane_tiers": 40, "smallm": 0, "smallm_kmax": 512,
+    "base-newstest-8192w": {"lanes": 3, "green_sms": 24, "lane_tiers": 40, "smallm": 0, "smallm_kmax": 512,
                             "attn_tma_self": 2},
-    "base-aan-newstest-8192w": {"green_sms": 40, "lane_tiers": 35, "smallm": 32, "smallm_kmax": 512,
+    "base-aan-newstest-8192w": {"lanes": 3, "green_sms": 40, "lane_tiers": 35, "smallm": 32, "smallm_kmax": 512,
                                 "attn_tma_self": 2},
-    "big-newstest-8192w": {"green_sms": 0, "lane_tiers": 25, "smallm": 0, "smallm_kmax": 512,
+    "big-newstest-8192w": {"lanes": 2, "green_sms": 0, "lane_tiers": 15, "smallm": 32, "smallm_kmax": 1024,
                            "attn_tma_self": 2},
 }
 L2_FLUSH_BYTES = 512 << 20   # > 126 MB L2
@@ -571,8 +572,8 @@ def main():
                     help="source keys / values rounded to bf16 (SURVEY 8(f) F3, src_kv_bf16 = 1)")
     ap.add_argument("--beam-fused", type=int, default=0,
                     help="beam search: 1 = log-sum-exp / top-k fused into the output GEMM epilogue")
-    ap.add_argument("--lanes", type=int, default=3,
-                    help="independent decoder lanes (streams) per GPU (scheduling only)")
+    ap.add_argument("--lanes", type=int, default=None,
+                    help="independent decoder lanes (streams) per GPU (scheduling only; default per workload)")
     ap.add_argument("--lane-tiers", type=int, default=None,
                     help="0: deal sentences round-robin to lanes; 10*p: contiguous length tiers "
                          "of equal sum S^p (scheduling only; default: per workload)")
@@ -601,6 +602,7 @@ def main():
         if getattr(args, k) is None:
             setattr(args, k, v)
     args.green_sms = 56 if args.green_sms is None else args.green_sms
+    args.lanes = 3 if args.lanes is None else args.lanes
     args.lane_tiers = 40 if args.lane_tiers is None else args.lane_tiers
 
     if args.impl == "mnmt" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:

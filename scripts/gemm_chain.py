@@ -6,7 +6,10 @@ from paper_1805_12096_b200 import mnmt as M
 L = M.lib()
 L.mnmt_debug_gemm_chain.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]
 dev = torch.device("cuda:0")
-for (Mr, N, K) in ((8, 256, 256), (128, 256, 256), (630, 256, 256), (8, 2048, 256), (8, 256, 2048), (630, 2048, 256)):
+SHAPES = ((8, 256, 256), (128, 256, 256), (630, 256, 256), (8, 2048, 256), (8, 256, 2048), (630, 2048, 256))
+if os.environ.get("SHAPES"):   # e.g. SHAPES="8x1024x1024,128x1024x1024"
+    SHAPES = tuple(tuple(int(v) for v in s.split("x")) for s in os.environ["SHAPES"].split(","))
+for (Mr, N, K) in SHAPES:
     A = torch.randint(-127, 128, (max(Mr, 128), K), dtype=torch.int8, device=dev)
     W = torch.randint(-127, 128, (N, K), dtype=torch.int8, device=dev)
     out = torch.empty(Mr, N, device=dev)
