@@ -45,7 +45,11 @@ mnmt_status mnmt_op_quantize(const float* x_dev, int64_t n, float clip, int8_t* 
  * A [M x K] codes, W [N x K] codes (K % 16 == 0), bias [N] fp32 or NULL.
  * For EPI_F32* / SIGMOID / ACC, N % 16 == 0; out row stride = N.
  * n_tile = 0 (auto), 64, 128 or 256; -1 = the small-M CUDA-core kernel (IDP4A, same s32 sums and
- * epilogue arithmetic; M <= 32, EPI_F32 .. EPI_SIGMOID, A and W 16-byte aligned). */
+ * epilogue arithmetic; M <= 32, EPI_F32 .. EPI_SIGMOID, A and W 16-byte aligned);
+ * -2 = the swap-AB tcgen05 kernel (D^T = W . A^T: W's 128-row tiles as the MMA's M operand, the
+ * M <= 128 rows of A as its N = 16 / 32 / 64 / 128 operand; same s32 sums and epilogue
+ * arithmetic; every epilogue but EPI_TOPK; A 16-byte aligned).  Argument errors (not a silent
+ * fallback) when the chosen kernel cannot take the call. */
 mnmt_status mnmt_op_gemm_i8(const int8_t* A_dev, const int8_t* W_dev, int32_t M, int32_t N,
                             int32_t K, const float* bias_dev, float clip, int32_t epilogue,
                             void* out_dev, void* out2_dev, int32_t n_tile, void* stream);
@@ -55,7 +59,9 @@ mnmt_status mnmt_op_gemm_i8(const int8_t* A_dev, const int8_t* W_dev, int32_t M,
  * over a thread-block cluster of that many CTAs (fewer when K has fewer 128-byte blocks or the
  * leader's shared memory cannot hold the partial slots; BN <= 128), whose exact s32 partials are
  * added in the leader before the epilogue; -1 = the library's rule (K >= 4096, or K >= 2048 at
- * <= 32 rows); 1 = none.  Outputs identical to mnmt_op_gemm_i8 (integer sums). */
+ * <= 32 rows); 1 = none.  With n_tile = -2 (swap-AB) split_k = 1, 2, 4, 8 caps each CTA at
+ * ceil(K blocks / split_k) K blocks (the kernel picks the power-of-two cluster that fits).
+ * Outputs identical to mnmt_op_gemm_i8 (integer sums). */
 mnmt_status mnmt_op_gemm_i8_split(const int8_t* A_dev, const int8_t* W_dev, int32_t M, int32_t N,
                                   int32_t K, const float* bias_dev, float clip, int32_t epi,
                                   void* out_dev, void* out2_dev, int32_t n_tile, int32_t split_k,

@@ -770,6 +770,242 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
 }
 
+// ------------------------------------------------------------------ swap-AB variant
+// For a handful of live rows (a decoder step of the critical lane, <= 64 rows) the 128-row A
+// tile of k_gemm_i8 is mostly padding, yet every CTA streams it from L2 after the PDL wait (the
+// per-launch critical path at deep K: 8 x 16 KB per CTA at K = 1024, DESIGN 12.3).  k_gemm_sab
+// computes the transposed product D^T = W . A^T on the same tensor cores: the 128 weight rows
+// of an N tile are the MMA's M = 128 operand (constant, all of a CTA's K blocks requested
+// before griddepcontrol.wait), the live rows are its N = MP operand (MP = 16 / 32 / 64 / 128,
+// MP x 128 bytes per K block after the wait), and the s32 accumulator D^T[n][m] lives in MP
+// TMEM columns.  Deep K is split over a cluster along z exactly as in k_gemm_i8 (partials into
+// the leader's slots, exact integer adds).  Epilogue: TMEM lane = output column n, column =
+// row m, so each epilogue warp holds 32 consecutive columns of a row and its fp32 stores are
+// full 128-byte lines without staging.  The arithmetic per element is k_gemm_i8's
+// (v = fmaf((float)acc, s, b[n]), then ReLU / sigmoid / Q / argmax key), so outputs are
+// bit-identical to the other paths.
+constexpr int SAB_STAGES = 8;   // K blocks per CTA kept in flight (the launch splits K to fit)
+template <int MP>
+struct SabCfg {
+  static constexpr int W_BYTES = BM * BK;   // 128 weight rows x 128 K bytes
+  static constexpr int A_BYTES = MP * BK;   // MP activation rows x 128 K bytes
+  static constexpr int STAGE_BYTES = W_BYTES + A_BYTES;
+  static constexpr int TMEM_COLS = MP < 32 ? 32 : MP;
+  static constexpr int RED_LD = MP + 4;     // split-K slot row stride (s32): 16-byte rows
+  static constexpr int RED_SLOT_BYTES = BM * RED_LD * 4;
+};
+
+template <int MP, int EPI>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    k_gemm_sab(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const GemmArgs args) {
+  using Cfg = SabCfg<MP>;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[SAB_STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[SAB_STAGES];
+  __shared__ __align__(8) uint64_t tmem_full_bar;
+  __shared__ uint32_t tmem_slot;
+  __shared__ float bias_s[BM];
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int n0 = blockIdx.x * BM;
+  const int ks = gridDim.z, kz = blockIdx.z;
+  const int kb_all = (args.K + BK - 1) / BK, kb_per = (kb_all + ks - 1) / ks;
+  const int kb0 = kz * kb_per;
+  const int num_kb = min(kb_all, kb0 + kb_per) - kb0;
+  const int stages = min(args.ring_cap, num_kb);   // ring depth chosen at launch
+  if (threadIdx.x == 0) GEMM_TRACE(0);
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  int32_t* red = reinterpret_cast<int32_t*>(smem + args.ring_cap * Cfg::STAGE_BYTES);
+  if (ks > 1) cluster_arrive_relaxed();   // phase 1: this CTA is running (DSMEM valid)
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&tmem_full_bar, 1);
+    fence_barrier_init();
+    // the constant weight rows of the first stages before the PDL wait
+    for (int s = 0; s < stages; ++s) {
+      mbar_arrive_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
+      uint8_t* sw = smem + s * Cfg::STAGE_BYTES;
+      tma_load_2d(sw, &tmB, &full_bar[s], (kb0 + s) * BK, n0);
+      tma_load_2d(sw + 64 * BK, &tmB, &full_bar[s], (kb0 + s) * BK, n0 + 64);
+    }
+  }
+  if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(&tmem_slot);
+  if (args.bias && warp >= 2)
+    for (int i = (int)threadIdx.x - 64; i < BM; i += 32 * EPI_WARPS)
+      bias_s[i] = n0 + i < args.N ? __ldg(args.bias + n0 + i) : 0.0f;
+  pdl_wait();
+  if (threadIdx.x == 0) GEMM_TRACE(1);
+  if (warp == 0 && lane == 0)
+    for (int s = 0; s < stages; ++s)
+      tma_load_2d(smem + s * Cfg::STAGE_BYTES + Cfg::W_BYTES, &tmA, &full_bar[s], (kb0 + s) * BK, 0);
+  const int M_live = args.M_dyn ? min(args.M, *args.M_dyn) : args.M;
+
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (stages 0..stages-1 were issued above)
+      for (int kb = stages; kb < num_kb; ++kb) {
+        const int s = kb % stages;
+        uint8_t* sw = smem + s * Cfg::STAGE_BYTES;
+        mbar_wait(&empty_bar[s], ((kb / stages) - 1) & 1);
+        mbar_arrive_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
+        tma_load_2d(sw, &tmB, &full_bar[s], (kb0 + kb) * BK, n0);
+        tma_load_2d(sw + 64 * BK, &tmB, &full_bar[s], (kb0 + kb) * BK, n0 + 64);
+        tma_load_2d(sw + Cfg::W_BYTES, &tmA, &full_bar[s], (kb0 + kb) * BK, 0);
+      }
+    }
+    __syncwarp();
+    if (ks > 1) {
+      cluster_wait();
+      cluster_arrive();
+      cluster_wait();
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer: D^T[128 x MP] (+)= W[128 x 32] . A[MP x 32]^T per step
+      constexpr uint32_t idesc = idesc_i8<BM, MP>();
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % stages;
+        mbar_wait(&full_bar[s], (kb / stages) & 1);
+        if (kb == 0) GEMM_TRACE(2);
+        tc_fence_after();
+        const uint32_t sw = smem_u32(smem + s * Cfg::STAGE_BYTES);
+        const uint64_t wdesc = umma_desc_sw128(sw);
+        const uint64_t adesc = umma_desc_sw128(sw + Cfg::W_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / 32; ++k)
+          mma_i8(tmem_base, wdesc + (uint64_t)(2 * k), adesc + (uint64_t)(2 * k), idesc, (kb | k) != 0);
+        mma_commit(&empty_bar[s]);
+      }
+      mma_commit(&tmem_full_bar);
+    }
+    __syncwarp();
+    if (ks > 1) {
+      cluster_wait();
+      cluster_arrive();
+      cluster_wait();
+    }
+  } else {
+    // ---------------- epilogue: warps 2..9; TMEM lane quarter q = warp % 4 holds output columns
+    // n0 + 32 q .. + 31 (lane = column); half = (warp - 2) / 4 takes rows [half MP/2, +MP/2)
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    constexpr int HR = MP / 2;              // rows per warp
+    constexpr int CH = HR < 16 ? 8 : 16;    // rows per tcgen05.ld
+    const int cl = q * 32 + (int)lane;      // column within the tile (TMEM lane)
+    const int n = n0 + cl;
+    const bool col_ok = n < args.N;
+    const float b = args.bias ? bias_s[cl] : 0.0f;
+    const uint32_t t_lane = tmem_base + ((uint32_t)(q * 32) << 16);
+    const int r_beg = half * HR;
+    mbar_wait(&tmem_full_bar, 0);
+    tc_fence_after();
+    if (warp == 2 && lane == 0) GEMM_TRACE(3);
+    if (warp == 2 && lane == 0) pdl_launch_dependents();
+    if (ks > 1) {
+      // split-K exchange: CTAs z > 0 store the live rows of their partial accumulators into
+      // the leader's slot z - 1; the leader adds the slots to its own before the epilogue
+      __syncwarp();
+      cluster_wait();   // phase 1: every CTA of the cluster is running
+      if (kz > 0) {
+        const uint32_t base = mapa_shared(
+            smem_u32(red + (kz - 1) * (Cfg::RED_SLOT_BYTES / 4) + cl * Cfg::RED_LD), 0);
+#pragma unroll 1
+        for (int r0 = r_beg; r0 < r_beg + HR && r0 < M_live; r0 += CH) {
+          int32_t acc[16];
+          if constexpr (CH == 16) tmem_ld16(t_lane + r0, acc);
+          else tmem_ld8(t_lane + r0, *reinterpret_cast<int32_t(*)[8]>(acc));
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < CH; j += 4)
+            st_cluster_v4(base + 4 * (r0 + j), acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        }
+      }
+      __syncwarp();
+      cluster_arrive();   // phase 2 (release): partials stored
+      cluster_wait();
+    }
+    if (!(ks > 1 && kz > 0)) {
+      const bool small = args.K <= 256;
+      int blk = 0;
+      float* obase = nullptr;
+      if constexpr (EPI == EPI_F32 || EPI == EPI_F32_Q || EPI == EPI_RELU_F32_Q || EPI == EPI_SIGMOID) {
+        blk = col_ok ? n / args.col_block : 0;
+        obase = args.out_f + (int64_t)blk * args.block_stride + (n - blk * args.col_block);
+      }
+#pragma unroll 1
+      for (int r0 = r_beg; r0 < r_beg + HR && r0 < M_live; r0 += CH) {   // warp-uniform
+        int32_t acc[16];
+        if constexpr (CH == 16) tmem_ld16(t_lane + r0, acc);
+        else tmem_ld8(t_lane + r0, *reinterpret_cast<int32_t(*)[8]>(acc));
+        tmem_ld_wait();
+        if (ks > 1) {   // + the other K ranges' partials (exact s32)
+          for (int z = 1; z < ks; ++z) {
+            const int4* rp = reinterpret_cast<const int4*>(red + (z - 1) * (Cfg::RED_SLOT_BYTES / 4) +
+                                                           cl * Cfg::RED_LD + r0);
+#pragma unroll
+            for (int j = 0; j < CH / 4; ++j) {
+              const int4 p = rp[j];
+              acc[4 * j] += p.x; acc[4 * j + 1] += p.y; acc[4 * j + 2] += p.z; acc[4 * j + 3] += p.w;
+            }
+          }
+        }
+        if (r0 == r_beg && warp == 2 && lane == 0) GEMM_TRACE(6);
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int r = r0 + j;
+          if (r >= M_live) break;   // warp-uniform
+          if constexpr (EPI == EPI_ACC) {
+            if (col_ok) args.out_i[(int64_t)r * args.ldo + n] = acc[j];
+          } else if constexpr (EPI == EPI_ARGMAX) {
+            // the row's maximum over this warp's 32 columns, lowest column on ties (R15): the
+            // packed keys are ordered exactly so
+            const float v = __fmaf_rn(acc_to_float(acc[j], small), args.scale, b);
+            unsigned long long key = col_ok ? argmax_key(v, (uint32_t)n) : 0ull;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              const unsigned long long k2 = __shfl_xor_sync(0xffffffffu, key, o);
+              key = k2 > key ? k2 : key;
+            }
+            if (lane == 0 && key) atomicMax(args.keys + r, key);
+          } else {
+            float v = __fmaf_rn(acc_to_float(acc[j], small), args.scale, b);
+            if constexpr (EPI == EPI_RELU_Q || EPI == EPI_RELU_F32_Q) v = relu(v);
+            if constexpr (EPI == EPI_SIGMOID) v = sigmoid_f64(v);
+            if (col_ok) {
+              if constexpr (EPI == EPI_F32 || EPI == EPI_F32_Q || EPI == EPI_RELU_F32_Q || EPI == EPI_SIGMOID)
+                obase[(int64_t)r * args.ldo] = v;
+              if constexpr (EPI == EPI_F32_Q || EPI == EPI_RELU_Q || EPI == EPI_RELU_F32_Q)
+                args.out_q[(int64_t)r * args.ldo + n] = (int8_t)q8(v, args.clip, args.sigma);
+            }
+          }
+        }
+      }
+    }
+    if (warp == 2 && lane == 0) GEMM_TRACE(4);
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+  if (warp == 1 && lane == 0) GEMM_TRACE(5);
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -969,6 +1205,8 @@ static cudaError_t set_attr_bn() {
 }
 
 static cudaError_t gemm_init_all();
+template <int MP>
+static cudaError_t set_attr_sab();
 
 // Opt every GEMM instantiation into its dynamic shared memory size on the current
 // device (once per device).  Must run before any launch (never inside a stream capture).
@@ -989,6 +1227,10 @@ static cudaError_t gemm_init_all() {
   if ((e = set_attr_bn32()) != cudaSuccess) return e;
   if ((e = set_attr_bn<64>()) != cudaSuccess) return e;
   if ((e = set_attr_bn<128>()) != cudaSuccess) return e;
+  if ((e = set_attr_sab<16>()) != cudaSuccess) return e;
+  if ((e = set_attr_sab<32>()) != cudaSuccess) return e;
+  if ((e = set_attr_sab<64>()) != cudaSuccess) return e;
+  if ((e = set_attr_sab<128>()) != cudaSuccess) return e;
   for (const void* f : {(const void*)k_gemm_i8<TOPK_BN, EPI_TOPK>, (const void*)k_gemm_i8<TOPK_BN, EPI_TOPK2>,
                         (const void*)k_gemm_i8<TOPK_BN, EPI_TOPK4>})
     if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1181,14 +1423,123 @@ static cudaError_t launch_smallm(const GemmArgs& a, int epi, cudaStream_t st) {
   return cudaErrorNotSupported;
 }
 
+// ------------------------------------------------------------------ swap-AB launch
+// Tensor map over the live rows of A with an MP-row box: rows beyond the launch's row bound
+// a.M are outside the map (zero-filled by the TMA, never read from memory).  Encoded on the
+// host at launch (graph capture) time; the kernel receives it by value.
+static bool make_tmap_rows(CUtensorMap* map, const void* base, int64_t rows, int64_t K, int64_t ld,
+                           int box_rows) {
+  auto enc = get_encode();
+  if (!enc || K % 16 != 0 || ld % 16 != 0 || rows < 1 || ((uintptr_t)base & 15)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// K blocks per CTA of the swap-AB launch before K is split over a cluster (env MNMT_SAB_KB, A/B)
+static int sab_kb_max() {
+  static const int v = [] {
+    const char* e = getenv("MNMT_SAB_KB");
+    const int x = e ? atoi(e) : SAB_STAGES;
+    return x < 1 ? 1 : x > SAB_STAGES ? SAB_STAGES : x;
+  }();
+  return v;
+}
+
+template <int MP, int EPI>
+static cudaError_t launch_sab_t(const CUtensorMap& tmB, const GemmArgs& a, cudaStream_t st) {
+  using Cfg = SabCfg<MP>;
+  CUtensorMap tmA;
+  if (!make_tmap_rows(&tmA, a.a_ptr, a.M, a.K, a.lda, MP)) return cudaErrorInvalidValue;
+  const int kb_all = (a.K + BK - 1) / BK;
+  const int kbm = a.sab_kb > 0 ? std::min(a.sab_kb, SAB_STAGES) : sab_kb_max();
+  int ks = 1;
+  while (ks < 8 && (kb_all + ks - 1) / ks > kbm && kb_all >= 2 * ks) ks *= 2;
+  // the leader's partial slots plus at least two ring stages must fit its shared memory
+  while (ks > 1 && (ks - 1) * Cfg::RED_SLOT_BYTES + 2 * Cfg::STAGE_BYTES + 1024 > GEMM_SMEM_MAX) ks /= 2;
+  while (ks > 1 && kb_all - (ks - 1) * ((kb_all + ks - 1) / ks) < 1) ks /= 2;   // no empty range
+  const int kb_per = (kb_all + ks - 1) / ks;
+  const int red_bytes = ks > 1 ? (ks - 1) * Cfg::RED_SLOT_BYTES : 0;
+  int ring = std::min(kb_per, SAB_STAGES);
+  const int cap = (GEMM_SMEM_MAX - 1024 - red_bytes) / Cfg::STAGE_BYTES;
+  if (cap < 1) return cudaErrorNotSupported;
+  if (ring > cap) ring = cap;
+  GemmArgs b = a;
+  b.ring_cap = ring;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((a.N + BM - 1) / BM, 1, ks);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = 1024 + (size_t)ring * Cfg::STAGE_BYTES + red_bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = ks;
+  cfg.attrs = attr;
+  cfg.numAttrs = ks > 1 ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, k_gemm_sab<MP, EPI>, tmA, tmB, b);
+}
+
+template <int MP>
+static cudaError_t launch_sab_mp(const CUtensorMap& tmB, const GemmArgs& a, int epi, cudaStream_t st) {
+  switch (epi) {
+    case EPI_F32: return launch_sab_t<MP, EPI_F32>(tmB, a, st);
+    case EPI_F32_Q: return launch_sab_t<MP, EPI_F32_Q>(tmB, a, st);
+    case EPI_RELU_Q: return launch_sab_t<MP, EPI_RELU_Q>(tmB, a, st);
+    case EPI_RELU_F32_Q: return launch_sab_t<MP, EPI_RELU_F32_Q>(tmB, a, st);
+    case EPI_SIGMOID: return launch_sab_t<MP, EPI_SIGMOID>(tmB, a, st);
+    case EPI_ARGMAX: return launch_sab_t<MP, EPI_ARGMAX>(tmB, a, st);
+    case EPI_ACC: return launch_sab_t<MP, EPI_ACC>(tmB, a, st);
+  }
+  return cudaErrorNotSupported;
+}
+
+template <int MP>
+static cudaError_t set_attr_sab() {
+  for (const void* f : {(const void*)k_gemm_sab<MP, EPI_F32>, (const void*)k_gemm_sab<MP, EPI_F32_Q>,
+                        (const void*)k_gemm_sab<MP, EPI_RELU_Q>, (const void*)k_gemm_sab<MP, EPI_RELU_F32_Q>,
+                        (const void*)k_gemm_sab<MP, EPI_SIGMOID>, (const void*)k_gemm_sab<MP, EPI_ARGMAX>,
+                        (const void*)k_gemm_sab<MP, EPI_ACC>}) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM_MAX);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// Returns cudaErrorNotSupported when the launch does not qualify (the caller takes the
+// 128-row tcgen05 path): needs the raw A pointer, a row bound <= the swap-AB bound
+// (sab_rows, or any M <= 128 under sab_force), no shortlist / beam epilogue.
+static cudaError_t launch_sab(const CUtensorMap& tmB, const GemmArgs& a, int epi, cudaStream_t st) {
+  const int bound = a.sab_force ? 128 : a.sab_rows;
+  if (!a.a_ptr || bound <= 0 || a.M > bound || a.M > 128 || a.colbits || is_topk(epi))
+    return cudaErrorNotSupported;
+  if (a.K % 16 || a.lda % 16 || ((uintptr_t)a.a_ptr & 15)) return cudaErrorNotSupported;
+  if (a.M <= 16) return launch_sab_mp<16>(tmB, a, epi, st);
+  if (a.M <= 32) return launch_sab_mp<32>(tmB, a, epi, st);
+  if (a.M <= 64) return launch_sab_mp<64>(tmB, a, epi, st);
+  return launch_sab_mp<128>(tmB, a, epi, st);
+}
+
 cudaError_t launch_gemm_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                            int epi, int bn, cudaStream_t st) {
   if (a.M <= 0 || a.N <= 0) return cudaSuccess;
-  {
+  if (!a.sab_force) {
     const cudaError_t e = launch_smallm(a, epi, st);
     // op level (smallm_force): a launch the small-M kernel cannot take is an error, never a
     // silent tcgen05 run
     if (e != cudaErrorNotSupported || a.smallm_force) return e;
+  }
+  {
+    const cudaError_t e = launch_sab(tmB, a, epi, st);
+    if (e != cudaErrorNotSupported || a.sab_force) return e;   // op level: never a silent fallback
   }
   if (is_topk(epi)) {   // fixed tile (the partial layout depends on it), never persistent
     if (a.part_ld < 2 * ((a.N + TOPK_BN - 1) / TOPK_BN)) return cudaErrorInvalidValue;

@@ -195,6 +195,8 @@ struct mnmt_model {
   int64_t max_concurrent_rows = 0;   // option: co-schedule batches in waves of <= this many rows
   int steps_per_graph = 1;             // option: decoder steps captured per CUDA graph
   int smallm = 32;                     // option: row bound of the small-M GEMM path (0 = off)
+  int sab = 0;                         // option: row bound of the swap-AB tcgen05 GEMM path (0 = off,
+                                       // <= 128); steps at <= sab rows run in 16 / 32 / 64 / 128-row graphs
   int smallm_kmax = 512;               // option: deepest K the small-M path takes
   int64_t smallm_wmax = 1 << 20;       // option: largest weight matrix (N x K bytes) of the small-M path
   int attn_tma_self = 2;               // option: self-attention through TMA tiles (0 / 1 / 2)
@@ -775,6 +777,7 @@ static cudaError_t gemm(mnmt_model* m, cudaStream_t st, const CUtensorMap& tmA, 
   a.smallm_rows = m->smallm;
   a.smallm_kmax = m->smallm_kmax;
   a.smallm_wmax = m->smallm_wmax;
+  a.sab_rows = m->sab;
   a.split_k = m->split_k ? -1 : 0;
   return launch_gemm_i8(tmA, W.tm, a, epi, 0, st);
 }
@@ -1124,6 +1127,9 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, int6
     a.sigma = sigma_of(m);
     a.col_block = a.N;
     a.keys = w.keys;
+    a.a_ptr = w.cy;   // swap-AB path at <= sab rows
+    a.lda = d;
+    a.sab_rows = m->sab;
     if (sl) {
       a.colbits = w.sl_bits;
       a.colbits_ld = (c.vocab + 31) / 32;
@@ -1396,6 +1402,7 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced) {
     const int rows_per = std::max(1, m->beam);   // beam search: up to beam rows per sentence
     auto pad_at = [&](int t) {
       const int a = b.alive[t] * rows_per;
+      if (a <= m->sab && m->beam == 0) return a <= 16 ? 16 : a <= 32 ? 32 : a <= 64 ? 64 : 128;   // swap-AB tiers
       if (a <= m->smallm && m->beam == 0) return m->smallm;   // small-M GEMMs
       return (a + 127) / 128 * 128;
     };
@@ -2084,6 +2091,15 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
     if (value < 0 || value > SMALLM_MAX) { set_err("smallm must be in [0, 32]"); return MNMT_ERR_ARG; }
     m->smallm = (int)value;
     for (Lane& L : m->lanes) {     // captured graphs encode the old kernel sequence
+      for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
+      L.graphs.clear();
+    }
+    return MNMT_OK;
+  }
+  if (std::string(name) == "sab") {
+    if (value < 0 || value > 128) { set_err("sab must be in [0, 128]"); return MNMT_ERR_ARG; }
+    m->sab = (int)value;
+    for (Lane& L : m->lanes) {     // captured graphs encode the old kernel sequence and row tiers
       for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
       L.graphs.clear();
     }

@@ -52,6 +52,7 @@ mnmt_status mnmt_op_gemm_i8_split(const int8_t* A, const int8_t* W, int32_t M, i
   if (split_k != -1 && split_k != 1 && split_k != 2 && split_k != 4 && split_k != 8)
     return arg_error("mnmt_op_gemm_i8_split: split_k must be -1, 1, 2, 4 or 8");
   if (n_tile == -1) return arg_error("mnmt_op_gemm_i8_split: no split-K for the small-M kernel");
+  if (n_tile == -2 && split_k < 1) return arg_error("mnmt_op_gemm_i8_split: swap-AB takes split_k 1, 2, 4 or 8");
   return gemm_op(A, W, M, N, K, bias, clip, epi, out, out2, n_tile, split_k, stream);
 }
 
@@ -70,8 +71,11 @@ static mnmt_status gemm_op(const int8_t* A, const int8_t* W, int32_t M, int32_t 
   const bool small = n_tile == -1;   // the small-M CUDA-core kernel (k_gemm_smallm)
   if (small && (M > 32 || epi > MNMT_EPI_SIGMOID || (uintptr_t)A % 16 || (uintptr_t)W % 16))
     return arg_error("mnmt_op_gemm_i8: n_tile -1 needs M <= 32, an fp32 / code epilogue and 16-byte aligned A, W");
-  if (epi != MNMT_EPI_TOPK && n_tile != 0 && n_tile != 64 && n_tile != 128 && n_tile != 256 && !small)
-    return arg_error("mnmt_op_gemm_i8: n_tile must be -1, 0, 64, 128 or 256");
+  const bool sab = n_tile == -2;     // the swap-AB tcgen05 kernel (k_gemm_sab)
+  if (sab && (M > 128 || epi == MNMT_EPI_TOPK || (uintptr_t)A % 16))
+    return arg_error("mnmt_op_gemm_i8: n_tile -2 needs M <= 128, a non-TOPK epilogue and 16-byte aligned A");
+  if (epi != MNMT_EPI_TOPK && n_tile != 0 && n_tile != 64 && n_tile != 128 && n_tile != 256 && !small && !sab)
+    return arg_error("mnmt_op_gemm_i8: n_tile must be -2, -1, 0, 64, 128 or 256");
   int n_tile_topk = 0;
   if (cudaError_t e = gemm_init(); e != cudaSuccess) return cuda_status(e, "gemm init");
   CUtensorMap ta, tb;
@@ -94,6 +98,16 @@ static mnmt_status gemm_op(const int8_t* A, const int8_t* W, int32_t M, int32_t 
     a.lda = K;
     a.b_ptr = W;
     a.smallm_force = 1;
+    n_tile = 0;
+  }
+  if (sab) {
+    a.a_ptr = A;
+    a.lda = K;
+    a.b_ptr = W;
+    a.sab_force = 1;
+    // split_k > 1: at most ceil(K blocks / split_k) K blocks per CTA (the cluster splits K)
+    a.sab_kb = split_k > 1 ? ((K + 127) / 128 + split_k - 1) / split_k : 0;
+    a.split_k = 0;
     n_tile = 0;
   }
   switch (epi) {

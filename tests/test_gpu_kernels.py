@@ -160,6 +160,97 @@ def test_gemm_small_m_bitexact(epi, Mr, N, K, bias):
         assert np.array_equal(of.cpu().numpy(), O.sigmoid_array(v))
 
 
+# swap-AB tcgen05 kernel (n_tile -2: W's 128-row tiles as the MMA's M operand, the M <= 128 rows
+# of A as its N = 16 / 32 / 64 / 128 operand; deep K split over a cluster)
+SAB_SHAPES = [
+    (1, 256, 256, 1), (8, 1024, 1024, 1), (16, 3072, 1024, 1), (17, 1024, 1024, 2),
+    (32, 4096, 1024, 1), (33, 1024, 4096, 1), (64, 1024, 4096, 4), (50, 208, 192, 1),
+    (100, 512, 2048, 2), (128, 1024, 1024, 8), (5, 36000, 256, 1), (29, 160, 1040, 4),
+    (63, 1024, 8192, 1),
+]
+
+
+@pytest.mark.parametrize("Mr,N,K,ks", SAB_SHAPES)
+def test_gemm_swap_ab_acc_bitexact(Mr, N, K, ks):
+    a = rand_codes((Mr, K), Mr + K + 3)
+    w = rand_codes((N, K), N + 11)
+    out = empty((Mr, N), torch.int32)
+    M.op_gemm_i8_split(ptr(to_dev(a)), ptr(to_dev(w)), Mr, N, K, None, CLIP, M.EPI_ACC, ptr(out), None, -2, ks)
+    sync()
+    assert np.array_equal(out.cpu().numpy(), O.gemm_acc(a, w))
+
+
+@pytest.mark.parametrize("epi", [M.EPI_F32, M.EPI_F32_Q, M.EPI_RELU_Q, M.EPI_RELU_F32_Q, M.EPI_SIGMOID])
+@pytest.mark.parametrize("Mr,N,K,ks,bias", [(1, 256, 256, 1, True), (12, 1024, 1024, 1, True),
+                                            (32, 1024, 4096, 4, True), (47, 2048, 512, 1, False),
+                                            (64, 4096, 1024, 2, True), (90, 160, 256, 1, True),
+                                            (128, 512, 2048, 1, True)])
+def test_gemm_swap_ab_epilogues_bitexact(epi, Mr, N, K, ks, bias):
+    """k_gemm_sab equals the oracle's fmaf((float)acc, s, b) and the ReLU / sigmoid / Q epilogue
+    element by element (ragged column tiles, split-K clusters, every row-tile width)."""
+    rng = np.random.default_rng(epi * 977 + Mr * 3 + K)
+    x = rng.normal(0, 1.0, size=(Mr, K)).astype(np.float32)
+    W = rng.uniform(-0.08, 0.08, size=(N, K)).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, size=N).astype(np.float32) if bias else None
+    qa, qw = O.quantize(x), O.quantize(W)
+    v = O.linear(qa, qw, b, CLIP)
+    A, Wd = to_dev(qa), to_dev(qw)
+    bp = ptr(to_dev(b)) if bias else None
+    of = empty((Mr, N), torch.float32)
+    oq = empty((Mr, N), torch.int8)
+    if epi == M.EPI_RELU_Q:
+        M.op_gemm_i8_split(ptr(A), ptr(Wd), Mr, N, K, bp, CLIP, epi, ptr(oq), None, -2, ks)
+    else:
+        M.op_gemm_i8_split(ptr(A), ptr(Wd), Mr, N, K, bp, CLIP, epi, ptr(of), ptr(oq), -2, ks)
+    sync()
+    r = np.maximum(v, np.float32(0))
+    if epi in (M.EPI_F32, M.EPI_F32_Q):
+        assert np.array_equal(of.cpu().numpy(), v)
+    if epi == M.EPI_F32_Q:
+        assert np.array_equal(oq.cpu().numpy(), O.quantize(v))
+    if epi == M.EPI_RELU_Q:
+        assert np.array_equal(oq.cpu().numpy(), O.quantize(r))
+    if epi == M.EPI_RELU_F32_Q:
+        assert np.array_equal(of.cpu().numpy(), r)
+        assert np.array_equal(oq.cpu().numpy(), O.quantize(r))
+    if epi == M.EPI_SIGMOID:
+        assert np.array_equal(of.cpu().numpy(), O.sigmoid_array(v))
+
+
+@pytest.mark.parametrize("Mr,N,K", [(1, 36000, 1024), (9, 36000, 256), (40, 36000, 512), (128, 50, 32)])
+def test_gemm_swap_ab_argmax_bitexact_with_ties(Mr, N, K):
+    """The swap-AB argmax epilogue (warp-wide max of packed (v, column) keys per row) picks the
+    lowest column among exact ties, as the oracle's first maximum does (R15)."""
+    rng = np.random.default_rng(Mr + N + K)
+    x = rng.normal(0, 1.0, size=(Mr, K)).astype(np.float32)
+    E = rng.uniform(-0.5, 0.5, size=(N, K)).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, size=N).astype(np.float32)
+    qa, qE = O.quantize(x), O.quantize(E)
+    best = np.argmax(O.linear(qa, qE, b, CLIP), axis=1)
+    for i in range(0, Mr, 2):   # exact ties: the winner copied to a lower and a higher column
+        j = int(best[i])
+        for j2 in ((j * 7 + 11) % N, (j + N // 2) % N, j ^ 1 if (j ^ 1) < N else j):
+            if j2 != j:
+                qE[j2] = qE[j]
+                b[j2] = b[j]
+    ref = np.argmax(O.linear(qa, qE, b, CLIP), axis=1)
+    keys = zeros((Mr,), torch.int64)
+    M.op_gemm_i8(ptr(to_dev(qa)), ptr(to_dev(qE)), Mr, N, K, ptr(to_dev(b)), CLIP, M.EPI_ARGMAX, ptr(keys), None, -2)
+    ids = empty((Mr,), torch.int32)
+    M.op_argmax_ids(ptr(keys), Mr, ptr(ids))
+    sync()
+    assert np.array_equal(ids.cpu().numpy(), ref)
+
+
+def test_gemm_swap_ab_rejects():
+    """n_tile -2 is an argument error (never a silent fallback) beyond 128 rows."""
+    a = to_dev(rand_codes((129, 64), 1))
+    w = to_dev(rand_codes((64, 64), 2))
+    out = empty((129, 64), torch.int32)
+    with pytest.raises(Exception):
+        M.op_gemm_i8(ptr(a), ptr(w), 129, 64, 64, None, CLIP, M.EPI_ACC, ptr(out), None, -2)
+
+
 @pytest.mark.parametrize("Mr,N,K,bias", [(3, 50, 32, True), (200, 36000, 256, True),
                                          (129, 36000, 192, False), (390, 36000, 512, True),
                                          (650, 36000, 256, True)])   # persistent kernel
