@@ -98,6 +98,18 @@ mnmt_status mnmt_op_attention(const float* q_dev, int64_t ldq, const float* kv_d
                               const int32_t* kv_len_dev, int32_t n, int32_t d, int32_t H,
                               float clip, int8_t* out_q_dev, float* out_f_dev, void* stream);
 
+/* A3: encoder self-attention of n_sent sentences with the encoder's kernels (R20, R24):
+ * qkv_dev [rows x 3d] holds each token's query | key | value (the fused QKV GEMM's output);
+ * sentence s is rows sent_start[s] .. sent_start[s] + sent_len[s] - 1 and attends over itself;
+ * s_max >= every sent_len (<= MNMT_MAX_KV; sizes shared memory).  out_q [rows x d] = Q(ctx).
+ * variant 0 = the library's choice, 1 = the generic warp-per-query kernel, 2 / 3 = the d/H = 64
+ * multi-query kernel with 4 / 8 queries per warp pass (s_max <= 100; argument error otherwise).
+ * Every variant computes the same values in the same order (identical codes). */
+mnmt_status mnmt_op_attention_enc(const float* qkv_dev, const int32_t* sent_start_dev,
+                                  const int32_t* sent_len_dev, int32_t n_sent, int32_t d, int32_t H,
+                                  int32_t s_max, float clip, int8_t* out_q_dev, int32_t variant,
+                                  void* stream);
+
 /* A7 with the decode path's kernel choice (the TMA-tiled source-attention kernel for fp32 K/V
  * and d/H = 32 or 64, else as mnmt_op_attention): row r attends kv rows
  * [kv_start[r], kv_start[r] + kv_len[r]) of the kv_rows-row buffer kv_dev (ldkv floats per row,

@@ -417,6 +417,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   int32_t* red = reinterpret_cast<int32_t*>(smem + ring * Cfg::STAGE_BYTES + EPI_STAGE_BYTES);
   if (ks > 1) cluster_arrive_relaxed();   // phase 1: this CTA is running (DSMEM valid)
 
+  // a_box > 0: tmA covers only the launch's a.M <= 64 rows with one a_box-row box (the rest of
+  // the A tile stays stale: those accumulator rows are never stored); b_box32: tmB has 32-row
+  // boxes (BN = 32 loads only its own weight rows)
+  const int a_bytes = args.a_box > 0 ? args.a_box * BK : Cfg::A_BYTES;
+  const int b_bytes = (BN == 32 && args.b_box32) ? 32 * BK : Cfg::B_BYTES;
+  const int tx_bytes = a_bytes + b_bytes;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -429,11 +435,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // Weights are constant for the life of the model: fetch the first stages' B tiles
     // before waiting on the previous kernel (programmatic dependent launch).
     for (int s = 0; s < stages; ++s) {
-      mbar_arrive_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
+      mbar_arrive_expect_tx(&full_bar[s], tx_bytes);
       uint8_t* sb = smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES;
+      if (BN == 32 && args.b_box32) {
+        tma_load_2d(sb, &tmB, &full_bar[s], (kb0 + s) * BK, n0);
+      } else {
 #pragma unroll
-      for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
-        tma_load_2d(sb + j * 64 * BK, &tmB, &full_bar[s], (kb0 + s) * BK, n0 + j * 64);
+        for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
+          tma_load_2d(sb + j * 64 * BK, &tmB, &full_bar[s], (kb0 + s) * BK, n0 + j * 64);
+      }
     }
   }
   // TMEM and the bias do not depend on the previous kernel either: both before the wait
@@ -452,7 +462,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int s = 0; s < stages; ++s) {
       uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
       tma_load_2d(sa, &tmA, &full_bar[s], (kb0 + s) * BK, m0);
-      tma_load_2d(sa + 64 * BK, &tmA, &full_bar[s], (kb0 + s) * BK, m0 + 64);
+      if (args.a_box == 0) tma_load_2d(sa + 64 * BK, &tmA, &full_bar[s], (kb0 + s) * BK, m0 + 64);
     }
   }
   const int M_live = args.M_dyn ? min(args.M, *args.M_dyn) : args.M;
@@ -482,12 +492,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
         uint8_t* sb = sa + Cfg::A_BYTES;
         mbar_wait(&empty_bar[s], ((kb / stages) - 1) & 1);
-        mbar_arrive_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
+        mbar_arrive_expect_tx(&full_bar[s], tx_bytes);
+        if (BN == 32 && args.b_box32) {
+          tma_load_2d(sb, &tmB, &full_bar[s], (kb0 + kb) * BK, n0);
+        } else {
 #pragma unroll
-        for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
-          tma_load_2d(sb + j * 64 * BK, &tmB, &full_bar[s], (kb0 + kb) * BK, n0 + j * 64);
+          for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
+            tma_load_2d(sb + j * 64 * BK, &tmB, &full_bar[s], (kb0 + kb) * BK, n0 + j * 64);
+        }
         tma_load_2d(sa, &tmA, &full_bar[s], (kb0 + kb) * BK, m0);
-        tma_load_2d(sa + 64 * BK, &tmA, &full_bar[s], (kb0 + kb) * BK, m0 + 64);
+        if (args.a_box == 0) tma_load_2d(sa + 64 * BK, &tmA, &full_bar[s], (kb0 + kb) * BK, m0 + 64);
       }
     }
     __syncwarp();
@@ -785,6 +799,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // (v = fmaf((float)acc, s, b[n]), then ReLU / sigmoid / Q / argmax key), so outputs are
 // bit-identical to the other paths.
 constexpr int SAB_STAGES = 8;   // K blocks per CTA kept in flight (the launch splits K to fit)
+constexpr int SAB_STAGE_LD = 36;   // epilogue staging row stride (floats): 32 columns + pad
 template <int MP>
 struct SabCfg {
   static constexpr int W_BYTES = BM * BK;   // 128 weight rows x 128 K bytes
@@ -794,6 +809,14 @@ struct SabCfg {
   static constexpr int RED_LD = MP + 4;     // split-K slot row stride (s32): 16-byte rows
   static constexpr int RED_SLOT_BYTES = BM * RED_LD * 4;
 };
+
+// acc[0..CH) = the accumulator's columns at taddr
+template <int CH>
+__device__ __forceinline__ void sab_ld_acc(uint32_t taddr, int32_t (&acc)[16]) {
+  if constexpr (CH == 16) tmem_ld16(taddr, acc);
+  else tmem_ld8(taddr, *reinterpret_cast<int32_t(*)[8]>(acc));
+  tmem_ld_wait();
+}
 
 template <int MP, int EPI>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -806,6 +829,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __shared__ __align__(8) uint64_t tmem_full_bar;
   __shared__ uint32_t tmem_slot;
   __shared__ float bias_s[BM];
+  __shared__ unsigned long long amax_s[EPI == EPI_ARGMAX ? MP : 1];   // the CTA's row maxima
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -842,6 +866,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (args.bias && warp >= 2)
     for (int i = (int)threadIdx.x - 64; i < BM; i += 32 * EPI_WARPS)
       bias_s[i] = n0 + i < args.N ? __ldg(args.bias + n0 + i) : 0.0f;
+  if constexpr (EPI == EPI_ARGMAX)
+    if (warp >= 2 && (int)threadIdx.x - 64 < MP) amax_s[threadIdx.x - 64] = 0ull;
   pdl_wait();
   if (threadIdx.x == 0) GEMM_TRACE(1);
   if (warp == 0 && lane == 0)
@@ -927,9 +953,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll 1
         for (int r0 = r_beg; r0 < r_beg + HR && r0 < M_live; r0 += CH) {
           int32_t acc[16];
-          if constexpr (CH == 16) tmem_ld16(t_lane + r0, acc);
-          else tmem_ld8(t_lane + r0, *reinterpret_cast<int32_t(*)[8]>(acc));
-          tmem_ld_wait();
+          sab_ld_acc<CH>(t_lane + r0, acc);
 #pragma unroll
           for (int j = 0; j < CH; j += 4)
             st_cluster_v4(base + 4 * (r0 + j), acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
@@ -941,18 +965,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     if (!(ks > 1 && kz > 0)) {
       const bool small = args.K <= 256;
-      int blk = 0;
-      float* obase = nullptr;
-      if constexpr (EPI == EPI_F32 || EPI == EPI_F32_Q || EPI == EPI_RELU_F32_Q || EPI == EPI_SIGMOID) {
-        blk = col_ok ? n / args.col_block : 0;
-        obase = args.out_f + (int64_t)blk * args.block_stride + (n - blk * args.col_block);
-      }
+      // per-warp staging tile [CH rows][32 columns] in the ring (free: every MMA has completed)
+      float* stage = reinterpret_cast<float*>(smem) + (warp - 2) * (16 * SAB_STAGE_LD);
+      const int nw = n0 + q * 32;                 // the warp's first column
+      const int sub = (int)lane >> 3, c4 = ((int)lane & 7) * 4;   // store phase: 4 rows x 8 lanes
 #pragma unroll 1
       for (int r0 = r_beg; r0 < r_beg + HR && r0 < M_live; r0 += CH) {   // warp-uniform
         int32_t acc[16];
-        if constexpr (CH == 16) tmem_ld16(t_lane + r0, acc);
-        else tmem_ld8(t_lane + r0, *reinterpret_cast<int32_t(*)[8]>(acc));
-        tmem_ld_wait();
+        sab_ld_acc<CH>(t_lane + r0, acc);
         if (ks > 1) {   // + the other K ranges' partials (exact s32)
           for (int z = 1; z < ks; ++z) {
             const int4* rp = reinterpret_cast<const int4*>(red + (z - 1) * (Cfg::RED_SLOT_BYTES / 4) +
@@ -965,35 +985,69 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
         if (r0 == r_beg && warp == 2 && lane == 0) GEMM_TRACE(6);
+        const int nr = min(CH, M_live - r0);   // live rows of this chunk
+        if constexpr (EPI == EPI_ACC) {
 #pragma unroll
-        for (int j = 0; j < CH; ++j) {
-          const int r = r0 + j;
-          if (r >= M_live) break;   // warp-uniform
-          if constexpr (EPI == EPI_ACC) {
-            if (col_ok) args.out_i[(int64_t)r * args.ldo + n] = acc[j];
-          } else if constexpr (EPI == EPI_ARGMAX) {
-            // the row's maximum over this warp's 32 columns, lowest column on ties (R15): the
-            // packed keys are ordered exactly so
-            const float v = __fmaf_rn(acc_to_float(acc[j], small), args.scale, b);
-            unsigned long long key = col_ok ? argmax_key(v, (uint32_t)n) : 0ull;
+          for (int j = 0; j < CH; ++j)
+            if (j < nr && col_ok) args.out_i[(int64_t)(r0 + j) * args.ldo + n] = acc[j];
+        } else if constexpr (EPI == EPI_ARGMAX) {
+          // the row's maximum over this warp's 32 columns, lowest column on ties (R15): the
+          // order key's warp maximum (redux), then the lowest lane holding it (columns ascend
+          // with the lane) -- the packed key of k_gemm_i8 maximised over the same columns
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              const unsigned long long k2 = __shfl_xor_sync(0xffffffffu, key, o);
-              key = k2 > key ? k2 : key;
+          for (int j = 0; j < CH; ++j) {
+            if (j < nr) {
+              const float v = __fmaf_rn(acc_to_float(acc[j], small), args.scale, b);
+              const uint32_t k32 = col_ok ? float_order_key(v) : 0u;
+              const uint32_t mk = __reduce_max_sync(0xffffffffu, k32);
+              const uint32_t hit = __ballot_sync(0xffffffffu, col_ok && k32 == mk);
+              if (lane == 0 && hit) {   // the CTA's maximum first (one global atomic per row)
+                const uint32_t jcol = (uint32_t)(nw + __ffs(hit) - 1);
+                atomicMax(amax_s + r0 + j,
+                          ((unsigned long long)mk << 32) | (unsigned long long)(0xFFFFFFFFu - jcol));
+              }
             }
-            if (lane == 0 && key) atomicMax(args.keys + r, key);
-          } else {
+          }
+        } else {
+          // dequant + fused op per element, staged [row][column] so each store instruction
+          // writes whole 128-byte row segments (fp32) / 32-byte code segments
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
             float v = __fmaf_rn(acc_to_float(acc[j], small), args.scale, b);
             if constexpr (EPI == EPI_RELU_Q || EPI == EPI_RELU_F32_Q) v = relu(v);
             if constexpr (EPI == EPI_SIGMOID) v = sigmoid_f64(v);
-            if (col_ok) {
-              if constexpr (EPI == EPI_F32 || EPI == EPI_F32_Q || EPI == EPI_RELU_F32_Q || EPI == EPI_SIGMOID)
-                obase[(int64_t)r * args.ldo] = v;
-              if constexpr (EPI == EPI_F32_Q || EPI == EPI_RELU_Q || EPI == EPI_RELU_F32_Q)
-                args.out_q[(int64_t)r * args.ldo + n] = (int8_t)q8(v, args.clip, args.sigma);
+            stage[j * SAB_STAGE_LD + lane] = v;
+          }
+          __syncwarp();
+          const int nc = nw + c4;
+          const bool c_ok = nc < args.N;   // N % 16 == 0: whole 4-column groups
+#pragma unroll
+          for (int it = 0; it < CH / 4; ++it) {
+            const int j = it * 4 + sub;
+            if (j < nr && c_ok) {
+              const float4 v4 = *reinterpret_cast<const float4*>(stage + j * SAB_STAGE_LD + c4);
+              const int r = r0 + j;
+              if constexpr (EPI == EPI_F32 || EPI == EPI_F32_Q || EPI == EPI_RELU_F32_Q || EPI == EPI_SIGMOID) {
+                const int blk = nc / args.col_block;   // 4-column groups never straddle a block
+                *reinterpret_cast<float4*>(args.out_f + (int64_t)blk * args.block_stride +
+                                           (int64_t)r * args.ldo + (nc - blk * args.col_block)) = v4;
+              }
+              if constexpr (EPI == EPI_F32_Q || EPI == EPI_RELU_Q || EPI == EPI_RELU_F32_Q) {
+                const uint32_t w = (uint32_t)(q8(v4.x, args.clip, args.sigma) & 0xff) |
+                                   ((uint32_t)(q8(v4.y, args.clip, args.sigma) & 0xff) << 8) |
+                                   ((uint32_t)(q8(v4.z, args.clip, args.sigma) & 0xff) << 16) |
+                                   ((uint32_t)(q8(v4.w, args.clip, args.sigma) & 0xff) << 24);
+                *reinterpret_cast<uint32_t*>(args.out_q + (int64_t)r * args.ldo + nc) = w;
+              }
             }
           }
+          __syncwarp();
         }
+      }
+      if constexpr (EPI == EPI_ARGMAX) {   // the 8 epilogue warps' row maxima -> global keys
+        named_bar_sync(1, 32 * EPI_WARPS);
+        const int i = (int)threadIdx.x - 64;
+        if (i < M_live && i < MP && amax_s[i]) atomicMax(args.keys + i, amax_s[i]);
       }
     }
     if (warp == 2 && lane == 0) GEMM_TRACE(4);
@@ -1136,16 +1190,41 @@ static int gemm_split_k(const GemmArgs& a, int bn, int epi) {
   return ks;
 }
 
+static bool make_tmap_rows(CUtensorMap* map, const void* base, int64_t rows, int64_t K, int64_t ld,
+                           int box_rows);
+
+// Live-row A boxes (env MNMT_ABOX=0 disables; A/B): a launch whose row bound a.M is <= 64 and
+// whose raw A pointer is known loads only ceil16(a.M) rows of A per K block instead of 128.
+static bool abox_on() {
+  static const bool on = [] {
+    const char* e = getenv("MNMT_ABOX");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int BN, int EPI>
-static cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
+static cudaError_t launch_t(const CUtensorMap& tmA_in, const CUtensorMap& tmB_in, const GemmArgs& a,
                             cudaStream_t st) {
   if constexpr (BN >= 64)   // BN = 32 (16-column epilogue chunks) is never persistent
-    if (gemm_persistent(a.M, a.N, BN, a.pers_grid)) return launch_pers_t<BN, EPI>(tmA, tmB, a, st);
+    if (gemm_persistent(a.M, a.N, BN, a.pers_grid)) return launch_pers_t<BN, EPI>(tmA_in, tmB_in, a, st);
   using Cfg = GemmCfg<BN>;
   const int ks = gemm_split_k(a, BN, EPI);
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, ks);
   const int num_kb = (a.K + BK - 1) / BK, kb_per = (num_kb + ks - 1) / ks;
   GemmArgs b = a;
+  CUtensorMap tmA = tmA_in, tmB = tmB_in;
+  b.a_box = 0;
+  b.b_box32 = 0;
+  if (abox_on() && a.a_ptr && a.M <= 64 && a.K % 16 == 0 && a.lda % 16 == 0) {
+    const int box = a.M <= 16 ? 16 : a.M <= 32 ? 32 : 64;
+    if (make_tmap_rows(&tmA, a.a_ptr, a.M, a.K, a.lda, box)) b.a_box = box;
+    else tmA = tmA_in;
+  }
+  if (BN == 32 && abox_on() && a.b_ptr) {
+    if (make_tmap_rows(&tmB, a.b_ptr, a.N, a.K, a.K, 32)) b.b_box32 = 1;
+    else tmB = tmB_in;
+  }
   int ring = kb_per < Cfg::STAGES ? kb_per : Cfg::STAGES;
   size_t smem = Cfg::smem_for(ring);
   if (ks > 1) {   // + the leader's partial buffer; the ring shrinks to fit
@@ -1521,6 +1600,7 @@ static cudaError_t launch_sab(const CUtensorMap& tmB, const GemmArgs& a, int epi
   const int bound = a.sab_force ? 128 : a.sab_rows;
   if (!a.a_ptr || bound <= 0 || a.M > bound || a.M > 128 || a.colbits || is_topk(epi))
     return cudaErrorNotSupported;
+  if (!a.sab_force && a.K < a.sab_kmin) return cudaErrorNotSupported;
   if (a.K % 16 || a.lda % 16 || ((uintptr_t)a.a_ptr & 15)) return cudaErrorNotSupported;
   if (a.M <= 16) return launch_sab_mp<16>(tmB, a, epi, st);
   if (a.M <= 32) return launch_sab_mp<32>(tmB, a, epi, st);
@@ -1564,7 +1644,8 @@ cudaError_t launch_gemm_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const
       const char* e = getenv("MNMT_BN32_KMAX");
       return e ? atoi(e) : 512;
     }();
-    if (tiles64 * 2 <= sms && a.N % 32 == 0 && a.K <= bn32_kmax) bn = 32;
+    if (tiles64 * 2 <= sms && a.N % 32 == 0 && (a.K <= bn32_kmax || (a.b_ptr && a.M <= 64 && abox_on())))
+      bn = 32;
   }
   switch (bn) {
     case 32:

@@ -73,8 +73,11 @@ struct GemmArgs {
   // swap-AB tcgen05 path (k_gemm_sab): with a_ptr set and M <= sab_rows, the weights are the
   // MMA's 128-row operand and the M live rows its N = 16 / 32 / 64 / 128 operand
   int sab_rows;                // row bound of the swap-AB path (0 = off, <= 128)
+  int sab_kmin;                // shallowest K the swap-AB path takes (model path; 0 = any)
   int sab_force;               // op level: take the swap-AB path for any M <= 128 (error otherwise)
   int sab_kb;                  // K blocks per CTA before K is split over a cluster (0 = default 8)
+  int a_box;                   // (launch-internal) k_gemm_i8: A loaded as one a_box-row box (0: 2 x 64)
+  int b_box32;                 // (launch-internal) k_gemm_i8<32>: B loaded as one 32-row box
   int ring_cap;                // (launch-internal) TMA ring depth cap of a split-K launch
   int split_k;                 // 0 / 1: no split-K; -1: the K / row-bound rule; 2, 4, 8: forced
                                // (capped by the leader's shared memory and the K blocks)

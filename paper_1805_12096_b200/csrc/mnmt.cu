@@ -195,6 +195,9 @@ struct mnmt_model {
   int64_t max_concurrent_rows = 0;   // option: co-schedule batches in waves of <= this many rows
   int steps_per_graph = 1;             // option: decoder steps captured per CUDA graph
   int smallm = 32;                     // option: row bound of the small-M GEMM path (0 = off)
+  int sab_kmin = 0;                    // option: shallowest K of the swap-AB path
+  int sab_out = 0;                     // option: row bound of the swap-AB output GEMM + argmax (A9)
+  int sab_kb = 0;                      // option: K blocks per swap-AB CTA before K is split (0 = 8)
   int sab = 0;                         // option: row bound of the swap-AB tcgen05 GEMM path (0 = off,
                                        // <= 128); steps at <= sab rows run in 16 / 32 / 64 / 128-row graphs
   int smallm_kmax = 512;               // option: deepest K the small-M path takes
@@ -778,6 +781,8 @@ static cudaError_t gemm(mnmt_model* m, cudaStream_t st, const CUtensorMap& tmA, 
   a.smallm_kmax = m->smallm_kmax;
   a.smallm_wmax = m->smallm_wmax;
   a.sab_rows = m->sab;
+  a.sab_kmin = m->sab_kmin;
+  a.sab_kb = m->sab_kb;
   a.split_k = m->split_k ? -1 : 0;
   return launch_gemm_i8(tmA, W.tm, a, epi, 0, st);
 }
@@ -1127,9 +1132,10 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, int6
     a.sigma = sigma_of(m);
     a.col_block = a.N;
     a.keys = w.keys;
-    a.a_ptr = w.cy;   // swap-AB path at <= sab rows
+    a.a_ptr = w.cy;   // swap-AB path at <= sab_out rows
     a.lda = d;
-    a.sab_rows = m->sab;
+    a.sab_rows = m->sab_out;
+    a.sab_kb = m->sab_kb;
     if (sl) {
       a.colbits = w.sl_bits;
       a.colbits_ld = (c.vocab + 31) / 32;
@@ -1402,7 +1408,8 @@ static mnmt_status run_job(mnmt_model* m, const Job& job, bool forced) {
     const int rows_per = std::max(1, m->beam);   // beam search: up to beam rows per sentence
     auto pad_at = [&](int t) {
       const int a = b.alive[t] * rows_per;
-      if (a <= m->sab && m->beam == 0) return a <= 16 ? 16 : a <= 32 ? 32 : a <= 64 ? 64 : 128;   // swap-AB tiers
+      if (a <= std::max(m->sab, m->sab_out) && m->beam == 0)   // swap-AB row tiers
+        return a <= 16 ? 16 : a <= 32 ? 32 : a <= 64 ? 64 : 128;
       if (a <= m->smallm && m->beam == 0) return m->smallm;   // small-M GEMMs
       return (a + 127) / 128 * 128;
     };
@@ -2100,6 +2107,24 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
     if (value < 0 || value > 128) { set_err("sab must be in [0, 128]"); return MNMT_ERR_ARG; }
     m->sab = (int)value;
     for (Lane& L : m->lanes) {     // captured graphs encode the old kernel sequence and row tiers
+      for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
+      L.graphs.clear();
+    }
+    return MNMT_OK;
+  }
+  if (std::string(name) == "sab_out" || std::string(name) == "sab_kb") {
+    if (value < 0 || value > 128) { set_err("%s must be in [0, 128]", name); return MNMT_ERR_ARG; }
+    (std::string(name) == "sab_out" ? m->sab_out : m->sab_kb) = (int)value;
+    for (Lane& L : m->lanes) {
+      for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
+      L.graphs.clear();
+    }
+    return MNMT_OK;
+  }
+  if (std::string(name) == "sab_kmin") {
+    if (value < 0 || value > (1 << 16)) { set_err("sab_kmin must be in [0, 65536]"); return MNMT_ERR_ARG; }
+    m->sab_kmin = (int)value;
+    for (Lane& L : m->lanes) {
       for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
       L.graphs.clear();
     }

@@ -93,6 +93,10 @@ static mnmt_status gemm_op(const int8_t* A, const int8_t* W, int32_t M, int32_t 
   a.col_block = N;
   a.block_stride = 0;
   a.split_k = split_k;
+  // raw operands: the launch may load only the live rows of A (a.M <= 64) and 32-row weight boxes
+  a.a_ptr = A;
+  a.lda = K;
+  a.b_ptr = W;
   if (small) {
     a.a_ptr = A;
     a.lda = K;
@@ -222,6 +226,30 @@ mnmt_status mnmt_op_attention(const float* q, int64_t ldq, const float* kv, int6
   a.out_q = out_q;
   a.out_f = out_f;
   return cuda_status(launch_attn(a, (cudaStream_t)stream), "attention");
+}
+
+mnmt_status mnmt_op_attention_enc(const float* qkv, const int32_t* sent_start, const int32_t* sent_len,
+                                  int32_t n_sent, int32_t d, int32_t H, int32_t s_max, float clip,
+                                  int8_t* out_q, int32_t variant, void* stream) {
+  if (n_sent < 0 || H < 1 || d % H || (d / H) % 4 || d / H > 64 || !qkv || !sent_start || !sent_len ||
+      !out_q || s_max < 1 || s_max > MNMT_MAX_KV || variant < 0 || variant > 3 || !(clip > 0.0f))
+    return arg_error("mnmt_op_attention_enc: bad arguments");
+  if (cudaError_t e = attn_init(); e != cudaSuccess) return cuda_status(e, "attention init");
+  EncAttnArgs a{};
+  a.qkv = qkv;
+  a.sent_start = sent_start;
+  a.sent_len = sent_len;
+  a.n_sent = n_sent;
+  a.H = H;
+  a.dh = d / H;
+  a.d = d;
+  a.s_max = s_max;
+  a.clip = clip;
+  a.sigma = sigma_of(clip);
+  a.out_q = out_q;
+  const cudaError_t e = launch_attn_enc_v(a, variant, (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported) return arg_error("mnmt_op_attention_enc: variant needs d / H = 64, s_max <= 100");
+  return cuda_status(e, "encoder attention");
 }
 
 mnmt_status mnmt_op_src_attention(const float* q, int64_t ldq, const float* kv, int64_t kv_rows,

@@ -193,6 +193,11 @@ __device__ __forceinline__ void cluster_sync() {
   cluster_wait();
 }
 
+// Named barrier `id` over `count` threads (whole warps; id 0 is __syncthreads).
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // Programmatic dependent launch.
 __device__ __forceinline__ void pdl_wait() {
   asm volatile("griddepcontrol.wait;" ::: "memory");

@@ -11,6 +11,7 @@
 //   k_attn_enc_r   encoder self-attention, lane per query row, dh <= 32, <= 128 positions (A3)
 //   k_attn_enc     encoder self-attention, warp per query row (other shapes)          (A3)
 //   k_finish       argmax decode + EOS/max_len + stable live-row compaction (A9, A10)
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <utility>
@@ -753,6 +754,143 @@ __global__ void __launch_bounds__(ENC_R_MAX) k_attn_enc_r(EncAttnArgs a) {
   }
 }
 
+// Encoder self-attention for d_h = 64 (A3; small / base / big students), QW query rows per warp
+// pass: one CTA per (sentence, head) stages the head's queries (transposed), keys and values once
+// as fp64 in shared memory; a warp takes QW queries at a time, so every K / V element read from
+// shared memory feeds QW FMAs (the one-query warp_attend is bound by shared-memory wavefronts:
+// one K load per FMA).
+//   pass 1  lane = position j (slots of 32): K row j's 64 elements in registers, 16 at a time,
+//           QW dot chains over c in order (fused, R24), the QW queries' element c read as
+//           broadcasts from QT[c][i0 .. i0 + QW);
+//   pass 2  max (warp tree), p = exp(s - max), z per lane over its positions then the warp tree;
+//   pass 3  lane = columns c, c + 32: context sums over positions in order, p read as
+//           broadcasts from P[QW][SP].
+// Every step and its order is warp_attend's (the generic encoder kernel), so outputs are
+// bit-identical to it; the arithmetic is the plain definition of R20 / R24.
+constexpr int ENC_MQ_DH = 64;
+constexpr int ENC_MQ_SMAX = 100;   // longest sentence of a launch this kernel takes (smem)
+__host__ __device__ inline int enc_mq_sp(int s_max) { return (s_max + 7) & ~7; }   // QT row length
+// shared memory (doubles): K [S][65] (rounded to even), V [S][66], QT [64][SP], P per warp [QW][SP]
+// (row paddings: the staging stores of consecutive positions j and the lane-j K reads hit
+// distinct banks)
+constexpr int ENC_MQ_LDV = ENC_MQ_DH + 2;
+__host__ __device__ inline int enc_mq_kd(int s_max) { return (s_max * (ENC_MQ_DH + 1) + 1) & ~1; }
+__host__ __device__ inline size_t enc_mq_smem(int s_max, int warps, int qw) {
+  return ((size_t)enc_mq_kd(s_max) + (size_t)s_max * ENC_MQ_LDV + (size_t)ENC_MQ_DH * enc_mq_sp(s_max) +
+          (size_t)warps * qw * enc_mq_sp(s_max)) * sizeof(double);
+}
+
+template <int QW>
+__global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn_enc_mq(EncAttnArgs a) {
+  constexpr int DH = ENC_MQ_DH, LDK = DH + 1;   // K rows padded: lanes j hit distinct banks
+  extern __shared__ __align__(16) double ems[];
+  const int nw = blockDim.x >> 5, S = a.s_max, SP = enc_mq_sp(S);
+  double* Ks = ems;                                 // [S][65]
+  double* Vs = Ks + enc_mq_kd(S);                   // [S][66]
+  double* QT = Vs + (size_t)S * ENC_MQ_LDV;         // [64][SP]
+  pdl_wait();
+  pdl_trigger_early();
+  const int s = a.sent_order ? a.sent_order[blockIdx.x] : (int)blockIdx.x, h = blockIdx.y;
+  const int d = a.d, ld3 = 3 * d;
+  const int start = a.sent_start[s], len = a.sent_len[s];
+  const float* base = a.qkv + (int64_t)start * ld3 + h * DH;
+  for (int i = threadIdx.x; i < len * (DH / 4); i += blockDim.x) {
+    const int j = i % len, c4 = (i / len) * 4;   // consecutive threads: consecutive positions
+    const float* rj = base + (int64_t)j * ld3 + c4;
+    const float4 q4 = *reinterpret_cast<const float4*>(rj);
+    const float4 k4 = *reinterpret_cast<const float4*>(rj + d);
+    const float4 v4 = *reinterpret_cast<const float4*>(rj + 2 * d);
+    double* kd = Ks + j * LDK + c4;
+    kd[0] = k4.x; kd[1] = k4.y; kd[2] = k4.z; kd[3] = k4.w;
+    *reinterpret_cast<double2*>(Vs + j * ENC_MQ_LDV + c4) = make_double2(v4.x, v4.y);
+    *reinterpret_cast<double2*>(Vs + j * ENC_MQ_LDV + c4 + 2) = make_double2(v4.z, v4.w);
+    QT[(c4 + 0) * SP + j] = q4.x; QT[(c4 + 1) * SP + j] = q4.y;
+    QT[(c4 + 2) * SP + j] = q4.z; QT[(c4 + 3) * SP + j] = q4.w;
+  }
+  for (int i = threadIdx.x; i < DH * (SP - len); i += blockDim.x)   // padding queries: zeros
+    QT[(i / (SP - len)) * SP + len + i % (SP - len)] = 0.0;
+  __syncthreads();
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* P = QT + (size_t)DH * SP + (size_t)wi * QW * SP;   // [QW][SP]
+  const double inv_sqrt = 1.0 / sqrt((double)DH);
+  for (int i0 = wi * QW; i0 < len; i0 += nw * QW) {
+    const int nq = min(QW, len - i0);
+    // ---- pass 1: scaled scores
+    double mx[QW];
+#pragma unroll
+    for (int qq = 0; qq < QW; ++qq) mx[qq] = -INFINITY;
+    for (int j = lane; j < len; j += 32) {
+      const double* kr = Ks + j * LDK;
+      double dot[QW];
+#pragma unroll
+      for (int qq = 0; qq < QW; ++qq) dot[qq] = 0.0;
+#pragma unroll 1
+      for (int c0 = 0; c0 < DH; c0 += 16) {
+        double kk[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) kk[u] = kr[c0 + u];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const double2* qp = reinterpret_cast<const double2*>(QT + (c0 + u) * SP + i0);
+#pragma unroll
+          for (int q2 = 0; q2 < QW / 2; ++q2) {
+            const double2 qv = qp[q2];   // broadcast
+            dot[2 * q2] = __fma_rn(qv.x, kk[u], dot[2 * q2]);
+            dot[2 * q2 + 1] = __fma_rn(qv.y, kk[u], dot[2 * q2 + 1]);
+          }
+        }
+      }
+#pragma unroll
+      for (int qq = 0; qq < QW; ++qq) {
+        const double sv = __dmul_rn(dot[qq], inv_sqrt);
+        P[qq * SP + j] = sv;
+        mx[qq] = fmax(mx[qq], sv);
+      }
+    }
+    // ---- pass 2: p = exp(s - max), z
+    double z[QW];
+#pragma unroll
+    for (int qq = 0; qq < QW; ++qq) {
+      mx[qq] = warp_max_f64(mx[qq]);
+      z[qq] = 0.0;
+    }
+    for (int j = lane; j < len; j += 32) {
+#pragma unroll
+      for (int qq = 0; qq < QW; ++qq) {
+        const double p = exp(__dsub_rn(P[qq * SP + j], mx[qq]));
+        P[qq * SP + j] = p;
+        z[qq] = __dadd_rn(z[qq], p);
+      }
+    }
+#pragma unroll
+    for (int qq = 0; qq < QW; ++qq) z[qq] = warp_sum_f64(z[qq]);
+    __syncwarp();
+    // ---- pass 3: context, positions in order
+    double acc[QW][2];
+#pragma unroll
+    for (int qq = 0; qq < QW; ++qq) acc[qq][0] = acc[qq][1] = 0.0;
+#pragma unroll 2
+    for (int j = 0; j < len; ++j) {
+      const double v0 = Vs[j * ENC_MQ_LDV + lane], v1 = Vs[j * ENC_MQ_LDV + lane + 32];
+#pragma unroll
+      for (int qq = 0; qq < QW; ++qq) {
+        const double p = P[qq * SP + j];   // broadcast
+        acc[qq][0] = __fma_rn(p, v0, acc[qq][0]);
+        acc[qq][1] = __fma_rn(p, v1, acc[qq][1]);
+      }
+    }
+#pragma unroll
+    for (int qq = 0; qq < QW; ++qq) {
+      if (qq < nq) {
+        int8_t* orow = a.out_q + (int64_t)(start + i0 + qq) * d + h * DH;
+        orow[lane] = (int8_t)q8((float)__ddiv_rn(acc[qq][0], z[qq]), a.clip, a.sigma);
+        orow[lane + 32] = (int8_t)q8((float)__ddiv_rn(acc[qq][1], z[qq]), a.clip, a.sigma);
+      }
+    }
+    __syncwarp();   // P reused by the next pass
+  }
+}
+
 // ------------------------------------------------------------------ decode init
 __global__ void k_decode_init(int32_t* ctrl, int32_t* live, int B, unsigned long long* keys,
                               const int32_t* row_start, const int32_t* row_len,
@@ -877,6 +1015,12 @@ cudaError_t attn_init() {   // once per device
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn_enc_r, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)enc_r_smem(ENC_R_MAX));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn_enc_mq<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)enc_mq_smem(ENC_MQ_SMAX, ATTN_WARPS, 4));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn_enc_mq<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)enc_mq_smem(ENC_MQ_SMAX, ATTN_WARPS, 8));
 
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1016,12 +1160,39 @@ cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
   return launch_pdl(k_attn, grid, block, smem, st, b);
 }
 
-cudaError_t launch_attn_enc(const EncAttnArgs& a, cudaStream_t st) {
+cudaError_t launch_attn_enc(const EncAttnArgs& a, cudaStream_t st) { return launch_attn_enc_v(a, 0, st); }
+
+cudaError_t launch_attn_enc_v(const EncAttnArgs& a, int variant, cudaStream_t st) {
   if (a.n_sent <= 0) return cudaSuccess;
   if (a.s_max < 1 || a.s_max > MNMT_MAX_KV) return cudaErrorInvalidValue;
+  if (variant == 1) {   // forced: the generic warp-per-query kernel
+    const int nw = enc_attn_warps(a.s_max);
+    return launch_pdl(k_attn_enc, dim3(a.n_sent, a.H), dim3(nw * 32), enc_attn_smem(a.dh, a.s_max, nw),
+                      st, a);
+  }
+  if (variant == 2 || variant == 3) {   // forced: the d_h = 64 multi-query kernel, QW = 4 / 8
+    if (a.dh != ENC_MQ_DH || a.s_max > ENC_MQ_SMAX) return cudaErrorNotSupported;
+    const int qw = variant == 2 ? 4 : 8;
+    const int nw = std::min(ATTN_WARPS, (a.s_max + qw - 1) / qw);
+    const size_t smem = enc_mq_smem(a.s_max, nw, qw);
+    return qw == 4 ? launch_pdl(k_attn_enc_mq<4>, dim3(a.n_sent, a.H), dim3(nw * 32), smem, st, a)
+                   : launch_pdl(k_attn_enc_mq<8>, dim3(a.n_sent, a.H), dim3(nw * 32), smem, st, a);
+  }
   if (a.dh <= 32 && (a.dh & 3) == 0 && a.s_max <= ENC_R_MAX) {
     const dim3 grid(a.n_sent, a.H), block((a.s_max + 31) / 32 * 32);
     return launch_pdl(k_attn_enc_r, grid, block, enc_r_smem(a.s_max), st, a);
+  }
+  // d_h = 64: QW queries per warp pass (env MNMT_ENC_MQ = 0 / 4 / 8 selects; default 4), as many
+  // warps as the bucket's longest sentence fills
+  static const int mq = [] {
+    const char* e = getenv("MNMT_ENC_MQ");
+    return e ? atoi(e) : 4;
+  }();
+  if (a.dh == ENC_MQ_DH && a.s_max <= ENC_MQ_SMAX && (mq == 4 || mq == 8)) {
+    const int nw = std::min(ATTN_WARPS, (a.s_max + mq - 1) / mq);
+    const size_t smem = enc_mq_smem(a.s_max, nw, mq);
+    return mq == 4 ? launch_pdl(k_attn_enc_mq<4>, dim3(a.n_sent, a.H), dim3(nw * 32), smem, st, a)
+                   : launch_pdl(k_attn_enc_mq<8>, dim3(a.n_sent, a.H), dim3(nw * 32), smem, st, a);
   }
   const int nw = enc_attn_warps(a.s_max);
   return launch_pdl(k_attn_enc, dim3(a.n_sent, a.H), dim3(nw * 32), enc_attn_smem(a.dh, a.s_max, nw),

@@ -145,6 +145,9 @@ cudaError_t launch_ln(const LnArgs& a, cudaStream_t st);
 cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st);
 cudaError_t launch_kv_bf16(float* kv, bf16s* kv16, int L, int64_t n, int64_t stride, cudaStream_t st);
 cudaError_t launch_attn_enc(const EncAttnArgs& a, cudaStream_t st);
+// variant 0: the library's choice; 1: the generic warp-per-query kernel; 2 / 3: the d_h = 64
+// multi-query kernel with 4 / 8 queries per warp pass (cudaErrorNotSupported otherwise)
+cudaError_t launch_attn_enc_v(const EncAttnArgs& a, int variant, cudaStream_t st);
 cudaError_t attn_init();   // dynamic-smem attribute (call once per device, outside capture)
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t st);
 cudaError_t launch_dump_rows(const DumpArgs& a, cudaStream_t st);

@@ -55,7 +55,7 @@ EXPORTS = [
     "mnmt_decode_forced", "mnmt_translate_forced",
     "mnmt_get_stats", "mnmt_last_error", "mnmt_model_destroy", "mnmt_model_set_option",
     "mnmt_op_quantize", "mnmt_op_gemm_i8", "mnmt_op_argmax_ids", "mnmt_op_layernorm",
-    "mnmt_op_aan_step", "mnmt_op_embed", "mnmt_op_attention", "mnmt_op_attention_bf16",
+    "mnmt_op_aan_step", "mnmt_op_embed", "mnmt_op_attention", "mnmt_op_attention_enc", "mnmt_op_attention_bf16",
     "mnmt_op_gather_rows", "mnmt_op_src_attention", "mnmt_op_gemm_i8_split",
 ]
 
@@ -97,6 +97,7 @@ def lib():
     L.mnmt_op_aan_step.argtypes = [P, P, I32, I32, I32, F, P, P, P]
     L.mnmt_op_embed.argtypes = [P, I32, P, P, I32, F, P, P, P]
     L.mnmt_op_attention.argtypes = [P, I64, P, I64, I32, I32, P, P, I32, I32, I32, F, P, P, P]
+    L.mnmt_op_attention_enc.argtypes = [P, P, P, I32, I32, I32, I32, F, P, I32, P]
     L.mnmt_op_attention_bf16.argtypes = [P, I64, P, I64, I32, I32, P, P, I32, I32, I32, F, P, P, P]
     L.mnmt_op_gather_rows.argtypes = [P, P, P, P, P, I32, P, P, P]
     L.mnmt_op_gemm_i8_split.argtypes = [P, P, I32, I32, I32, P, F, I32, P, P, I32, I32, P]
@@ -337,6 +338,12 @@ def op_gemm_i8_split(A_ptr, W_ptr, M, N, K, bias_ptr, clip, epi, out_ptr, out2_p
                      split_k=-1, stream=None) -> None:
     _check(lib().mnmt_op_gemm_i8_split(A_ptr, W_ptr, M, N, K, bias_ptr, clip, epi, out_ptr, out2_ptr,
                                        n_tile, split_k, _stream_ptr(stream)))
+
+
+def op_attention_enc(qkv_ptr, start_ptr, len_ptr, n_sent, d, H, s_max, clip, out_q_ptr, variant=0,
+                     stream=None) -> None:
+    _check(lib().mnmt_op_attention_enc(qkv_ptr, start_ptr, len_ptr, n_sent, d, H, s_max, clip,
+                                       out_q_ptr, variant, _stream_ptr(stream)))
 
 
 def op_argmax_ids(keys_ptr, n, ids_ptr, stream=None) -> None:

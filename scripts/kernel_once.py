@@ -1,5 +1,5 @@
 """One launch (after warm-up) of a decoder kernel at a bench shape, for ncu.
-usage: KERNEL=dxd|ffn1|ffn2|out|topk|attn|attn16|ln M=630 D=256 F=2048 H=8 S=21 python scripts/kernel_once.py
+usage: KERNEL=dxd|ffn1|ffn2|out|topk|attn|attn16|ln|enc M=630 D=256 F=2048 H=8 S=21 python scripts/kernel_once.py
 (NTILE=-1: the small-M GEMM kernel; NTILE=64/128/256: a fixed tcgen05 N tile)"""
 import os, sys
 import numpy as np
@@ -34,6 +34,17 @@ elif k in ("dxd", "out", "ffn1", "ffn2"):
             out.zero_()
         M.op_gemm_i8(A.data_ptr(), W.data_ptr(), Mr, N, K, b.data_ptr(), 2.0, epi, out.data_ptr(), None,
                      int(os.environ.get("NTILE", 0)), None)
+elif k == "enc":   # encoder self-attention: M sentences of 1..S tokens (env ENCV = op variant)
+    S = int(os.environ.get("S", 28))
+    rng = np.random.default_rng(5)
+    L = rng.integers(max(1, S // 3), S + 1, size=Mr).astype(np.int32); L[0] = S
+    st = np.concatenate([[0], np.cumsum(L)[:-1]]).astype(np.int32)
+    qkv = torch.randn(int(L.sum()), 3 * d, device=dev)
+    Sd, Ln = torch.from_numpy(st).to(dev), torch.from_numpy(L).to(dev)
+    oq = torch.empty(int(L.sum()), d, dtype=torch.int8, device=dev)
+    for _ in range(4):
+        M.op_attention_enc(qkv.data_ptr(), Sd.data_ptr(), Ln.data_ptr(), Mr, d, H, S, 2.0, oq.data_ptr(),
+                           int(os.environ.get("ENCV", 0)), None)
 elif k == "ln":
     x = torch.randn(Mr, d, device=dev); dl = torch.randn(Mr, d, device=dev)
     g = torch.ones(d, device=dev); bb = torch.zeros(d, device=dev)

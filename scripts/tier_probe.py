@@ -1,5 +1,6 @@
-"""Where the tiered-lane job's time goes (small-AAN newstest job, bench options): the whole job,
-the critical tier (longest sentences, last lane) alone, and the other tiers alone."""
+"""Where the tiered-lane job's time goes (newstest job, bench options): the whole job, the critical
+tier (longest sentences, last lane) alone, and the other tiers alone.
+env PRESET, LANES, TIERS, GREEN, OPTS="smallm=32,sab=32,..." (extra model options)"""
 import os, sys
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -10,6 +11,8 @@ m = M.Model(dims, synth.make_weights(dims, 1))
 dev = torch.device("cuda:0"); st = torch.cuda.current_stream()
 ss = synth.newstest_set(seed=2014)
 G, TIERS = int(os.environ.get("GREEN", 48)), int(os.environ.get("TIERS", 40))
+LANES = int(os.environ.get("LANES", 3))
+EXTRA = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in filter(None, os.environ.get("OPTS", "").split(","))}
 
 
 def t_job(sub, opts, reps=5):
@@ -27,15 +30,15 @@ def t_job(sub, opts, reps=5):
     return float(np.median(ts))
 
 
-bench = dict(max_concurrent_rows=4096, lanes=3, lane_tiers=TIERS, green_sms=G, pers_reserve=16)
+bench = dict(max_concurrent_rows=4096, lanes=LANES, lane_tiers=TIERS, green_sms=G, pers_reserve=16, **EXTRA)
 print(f"whole job, bench options: {t_job(ss, bench):.2f} ms", flush=True)
 # the tier split of mnmt_translate: contiguous length order, equal shares of sum S^p
 order = np.argsort(ss.lengths, kind="stable")
 w = ss.lengths[order].astype(np.float64) ** (TIERS / 10.0)
-cut = int(np.searchsorted(np.cumsum(w), w.sum() * 2 / 3))
+cut = int(np.searchsorted(np.cumsum(w), w.sum() * (LANES - 1) / LANES))
 crit, bulk = order[cut + 1:], order[:cut + 1]
 print(f"critical tier: {len(crit)} sentences, lengths {ss.lengths[crit].min()}..{ss.lengths[crit].max()}")
-one = dict(max_concurrent_rows=4096, lanes=1, lane_tiers=0, green_sms=0, pers_reserve=0)
+one = dict(max_concurrent_rows=4096, lanes=1, lane_tiers=0, green_sms=0, pers_reserve=0, **EXTRA)
 print(f"critical tier alone, whole GPU: {t_job(ss.subset(crit), one):.2f} ms", flush=True)
-two = dict(max_concurrent_rows=4096, lanes=2, lane_tiers=TIERS, green_sms=0, pers_reserve=0)
-print(f"other tiers alone (2 lanes), whole GPU: {t_job(ss.subset(bulk), two):.2f} ms", flush=True)
+two = dict(max_concurrent_rows=4096, lanes=max(1, LANES - 1), lane_tiers=TIERS, green_sms=0, pers_reserve=0, **EXTRA)
+print(f"other tiers alone ({max(1, LANES - 1)} lanes), whole GPU: {t_job(ss.subset(bulk), two):.2f} ms", flush=True)

@@ -363,6 +363,37 @@ def test_attention(d, H):
     assert not boundary_explained(ref, O.quantize(ref), oq.cpu().numpy()).any()
 
 
+@pytest.mark.parametrize("d,H,smax", [(256, 4, 100), (1024, 16, 40), (512, 8, 97), (1024, 16, 7)])
+def test_attention_enc_variants(d, H, smax):
+    """mnmt_op_attention_enc: the d_h = 64 multi-query encoder kernel (4 / 8 queries per warp pass,
+    sentences of 1..smax tokens, ragged last passes) writes exactly the generic warp-per-query
+    kernel's codes, and both are the oracle's Q(attention) up to boundary-explained flips."""
+    rng = np.random.default_rng(d + smax)
+    n_sent = 37
+    lens = rng.integers(1, smax + 1, size=n_sent).astype(np.int32)
+    lens[0], lens[-1] = 1, smax
+    starts = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int32)
+    rows = int(lens.sum())
+    qkv = rng.normal(0, 1, size=(rows, 3 * d)).astype(np.float32)
+    qd, sd, ld = to_dev(qkv), to_dev(starts), to_dev(lens)
+    outs = []
+    for variant in (1, 2, 3, 0):
+        oq = zeros((rows, d), torch.int8)
+        M.op_attention_enc(ptr(qd), ptr(sd), ptr(ld), n_sent, d, H, smax, CLIP, ptr(oq), variant)
+        sync()
+        outs.append(oq.cpu().numpy())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    ref = np.zeros((rows, d), np.float32)
+    for s in range(n_sent):
+        blk = qkv[starts[s]:starts[s] + lens[s]]
+        for i in range(lens[s]):
+            ref[starts[s] + i] = O.attention(blk[i, :d], blk[:, d:2 * d], blk[:, 2 * d:], H)
+    rq = O.quantize(ref)
+    assert not boundary_explained(ref, rq, outs[0]).any()
+    assert np.mean(outs[0] != rq) < 1e-4
+
+
 @pytest.mark.parametrize("d,H", [(256, 8), (512, 8), (1024, 16), (192, 8)])
 def test_src_attention_tma(d, H):
     """mnmt_op_src_attention (the decode path's choice: TMA-tiled K / V for d/H = 32 / 64,
