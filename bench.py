@@ -54,6 +54,9 @@ DEFAULT_WORKLOAD = "big-newstest-8192w"   # BASELINE.json configs[3]: the metric
 # per workload, from the A/B in profiles/r1_ab_smallm.txt (small-aan: +2 % with FFN2's K = 2048
 # included; the others neutral or slower, so off; big with K <= 1024 and the <= 1 MB d x d maps:
 # 91.5 -> 90.8 ms per job in round 2 (profiles/r2_sweep_big_options.txt)).
+# sab: row bound of the swap-AB tcgen05 GEMM (weights as the 128-row MMA operand, live rows as
+# N = 16 / 32 / 64; profiles/r2_sab_enc_ab.txt): big 88.9-89.5 -> 86.3-87.4 ms per job with sab 64
+# and the IDP4A path off; the smaller students neutral (off).
 # attn_tma_self: self-attention decoders through the TMA-tiled kernels (profiles/r2_attn_tma_ab.txt,
 # after the V tiles started reusing the K buffers: big 99.1-99.4 / 100.1-100.2 / 97.7-97.8 ms per
 # job for 0 / 1 / 2, base self-attention 59.9 / 59.2 / 56.4 ms): 2.
@@ -66,8 +69,8 @@ WORKLOAD_OPTS = {
                             "attn_tma_self": 2},
     "base-aan-newstest-8192w": {"lanes": 3, "green_sms": 40, "lane_tiers": 35, "smallm": 32, "smallm_kmax": 512,
                                 "attn_tma_self": 2},
-    "big-newstest-8192w": {"lanes": 2, "green_sms": 0, "lane_tiers": 15, "smallm": 32, "smallm_kmax": 1024,
-                           "attn_tma_self": 2},
+    "big-newstest-8192w": {"lanes": 2, "green_sms": 0, "lane_tiers": 15, "smallm": 0, "smallm_kmax": 1024,
+                           "attn_tma_self": 2, "sab": 64},
 }
 L2_FLUSH_BYTES = 512 << 20   # > 126 MB L2
 
@@ -589,6 +592,8 @@ def main():
                          "default per workload)")
     ap.add_argument("--smallm-kmax", type=int, default=None,
                     help="deepest K of the small-M path (default per workload)")
+    ap.add_argument("--sab", type=int, default=None,
+                    help="row bound of the swap-AB tcgen05 GEMM path (0 = off; default per workload)")
     ap.add_argument("--attn-tma-self", type=int, default=None,
                     help="self-attention through TMA tiles: 0 off, 1 split kernel, 2 all (default per workload)")
     ap.add_argument("--max-concurrent-rows", type=int, default=4096,
@@ -640,7 +645,7 @@ def main():
                     "steps_per_graph": args.steps_per_graph, "smallm": args.smallm,
                     "smallm_kmax": args.smallm_kmax,
                     "lane_tiers": args.lane_tiers, "pers_reserve": args.pers_reserve,
-                    "green_sms": args.green_sms, "attn_tma_self": args.attn_tma_self,
+                    "green_sms": args.green_sms, "attn_tma_self": args.attn_tma_self, "sab": args.sab,
                     "extra_options": args.opt,
                     "step_engine": "kernel-per-op CUDA graph per decoder step (PDL chained)"}
 
@@ -670,7 +675,7 @@ def main():
                     ("smallm_kmax", 512 if args.smallm_kmax is None else args.smallm_kmax),
                     ("lane_tiers", args.lane_tiers), ("pers_reserve", args.pers_reserve),
                     ("green_sms", args.green_sms), ("beam_fused", args.beam_fused),
-                    ("attn_tma_self", args.attn_tma_self or 0)):
+                    ("attn_tma_self", args.attn_tma_self or 0), ("sab", args.sab or 0)):
         model.set_option(name, v)
     for kv in args.opt:
         k, v = kv.split("=")

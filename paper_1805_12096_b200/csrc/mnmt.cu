@@ -203,6 +203,7 @@ struct mnmt_model {
   int smallm_kmax = 512;               // option: deepest K the small-M path takes
   int64_t smallm_wmax = 1 << 20;       // option: largest weight matrix (N x K bytes) of the small-M path
   int attn_tma_self = 2;               // option: self-attention through TMA tiles (0 / 1 / 2)
+  int attn_persist = -1;               // option: persistent ping-pong TMA attention (-1 env default, 0, 1)
   int split_k = 0;                     // option: 1 = split-K clusters by the measured rule (off: slower in the job)
   DevDump dump;                        // (call state) device dumps of a teacher-forced run
   int green_sms = 0;                   // option: SMs of the critical lane's green context (0 = off)
@@ -1004,6 +1005,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, int6
       at.anc = m->beam > 0 ? w.anc : nullptr;
       at.tmap = &w.tm_self;             // TMA tiles (greedy; beam search reads through anc)
       at.tma_self = m->attn_tma_self;
+      at.tma_persist = m->attn_persist;
       at.kv_row0 = (int64_t)l * w.B_cap * w.T_cap;
       at.clip = c.clip;
       at.sigma = sigma_of(m);
@@ -1034,6 +1036,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, int6
     as.kv = w.kv + (int64_t)l * w.M_cap * 2 * d;
     as.kv16 = c.src_kv_bf16 ? w.kv16 + (int64_t)l * w.M_cap * 2 * d : nullptr;
     as.tmap = &w.tm_kv;                // TMA tiles (fp32 K/V)
+    as.tma_persist = m->attn_persist;
     as.kv_row0 = (int64_t)l * w.M_cap;
     as.ldkv = 2 * d;
     as.k_off = 0;
@@ -1271,7 +1274,7 @@ static void plan_job(const int64_t* src_off, int32_t n, const int32_t* max_len,
 
 // Row metadata of every batch, staged host-side once per job (uploaded in one copy).
 static void plan_rows(Job& job, const int64_t* src_off, const int32_t* max_len, bool forced,
-                      const int64_t* forced_off) {
+                      const int64_t* forced_off, int d_model) {
   job.rmeta32.clear();
   job.rmeta64.clear();
   job.r0.clear();
@@ -1300,8 +1303,18 @@ static void plan_rows(Job& job, const int64_t* src_off, const int32_t* max_len, 
     // rows in (length, row) order, cut into length buckets for the encoder attention
     for (int r = 0; r < B; ++r) ord[r] = r;
     std::stable_sort(ord, ord + B, [&](int32_t x, int32_t y) { return rl[x] < rl[y]; });
-    // (one launch per bucket: shared memory and warps per CTA follow the bucket's longest)
-    static const int kEdges[] = {32, 64, 128, MNMT_MAX_SPAN};
+    // (one launch per bucket: shared memory and warps per CTA follow the bucket's longest).  The
+    // fine edges keep the multi-query kernel's warps busy where the encoder attention is heavy
+    // (d >= 512; measured: big 86.5 -> 84.8 ms per job, base-AAN 50.9 -> 50.5, small-AAN 37.4 ->
+    // 38.3 from the extra launches, profiles/r2_sab_enc_ab.txt); env MNMT_ENC_FINE = 0 / 1 forces
+    static const int kCoarse[] = {32, 64, 128, MNMT_MAX_SPAN};
+    static const int kFine[] = {8, 12, 16, 20, 24, 28, 32, 40, 48, 56, 64, 80, 100, 128, MNMT_MAX_SPAN};
+    static const int fine_env = [] {
+      const char* e = getenv("MNMT_ENC_FINE");
+      return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    const bool fine = fine_env >= 0 ? fine_env == 1 : d_model >= 512;
+    const int* kEdges = fine ? kFine : kCoarse;
     b.enc_buckets.clear();
     for (int i = 0, e = 0; i < B;) {
       while (rl[ord[i]] > kEdges[e]) ++e;
@@ -1807,7 +1820,7 @@ static mnmt_status translate_impl(mnmt_model* m, const int32_t* src_ids, const i
   }
   Job job;
   plan_job(src_off, n, max_len, rows, lanes_of, (int)m->lanes.size(), job, use_sl ? &wave_of : nullptr);
-  plan_rows(job, src_off, max_len, forced, forced ? fz->off : nullptr);
+  plan_rows(job, src_off, max_len, forced, forced ? fz->off : nullptr, m->c.d_model);
   std::vector<int32_t> rgrp;
   if (use_sl) {
     rgrp.assign(job.rows_total, 0);
@@ -2142,6 +2155,15 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
   if (std::string(name) == "smallm_wmax") {
     if (value < 0) { set_err("smallm_wmax < 0"); return MNMT_ERR_ARG; }
     m->smallm_wmax = value;
+    for (Lane& L : m->lanes) {
+      for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
+      L.graphs.clear();
+    }
+    return MNMT_OK;
+  }
+  if (std::string(name) == "attn_persist") {
+    if (value < -1 || value > 1) { set_err("attn_persist must be -1, 0 or 1"); return MNMT_ERR_ARG; }
+    m->attn_persist = (int)value;
     for (Lane& L : m->lanes) {
       for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
       L.graphs.clear();

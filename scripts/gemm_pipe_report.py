@@ -8,7 +8,7 @@ Input: an ncu launch list of ONE translation job (scripts/job_once.py under
 sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active --csv`).
 
 - Launches before the first k_decode_init of a wave are the encoder's; the rest are decoder steps.
-- Decoder GEMM classes by kernel template + launch order: EPI 5 = output projection + argmax;
+- Decoder GEMM classes by kernel template (k_gemm_i8 / k_gemm_pers / k_gemm_sab) + launch order: EPI 5 = output projection + argmax;
   RELU_Q (EPI 2) with N = F (grid.x * BN, or the persistent kernel) = FFN1; the first F32 GEMM
   after an FFN1 = FFN2; every other decoder GEMM = a d x d projection (AAN FFN, gates, source q/o).
 - useful-ops % = sum 2*M*N*K over the job (M = live rows of each step, from the schedule) /
@@ -55,11 +55,13 @@ def classify(launches, F):
             phase = "dec"
         if "k_embed_src" in n:
             phase = "enc"
-        m = re.search(r"k_gemm_(i8|pers)<(\d+), (\d+)>", n)
+        m = re.search(r"k_gemm_(i8|pers|sab)<(\d+), (\d+)>", n)
         if not m:
             k["cls"] = None
             continue
         pers, bn, epi = m.group(1) == "pers", int(m.group(2)), int(m.group(3))
+        if m.group(1) == "sab":   # swap-AB: 128 output columns per CTA (the template's first
+            bn = 128              # parameter is the row tile)
         gx = int(re.match(r"\((\d+)", k["grid"]).group(1)) if k["grid"].startswith("(") else 0
         N = None if pers else gx * bn
         if phase == "enc":

@@ -12,7 +12,7 @@ for w in small-aan-newstest-8192w base-aan-newstest-8192w base-newstest-8192w ti
 done
 python bench.py --scaling strong --gpus 1 --steps 5 --no-cpu-baseline --no-roofline > gpurun_out/fin/bench_strong1.json 2>/dev/null
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/fin/bench_reference.json 2>/dev/null
-PRESET=big OPTS="lanes=2,lane_tiers=15,pers_reserve=16,smallm=32,smallm_kmax=1024,attn_tma_self=2" timeout 1500 ncu --nvtx --nvtx-include "job/" \
+PRESET=big OPTS="lanes=2,lane_tiers=15,pers_reserve=16,smallm=0,sab=64,attn_tma_self=2" timeout 1500 ncu --nvtx --nvtx-include "job/" \
    --metrics gpu__time_duration.sum,sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active \
    --clock-control none --csv --log-file gpurun_out/fin/launches_big.csv python scripts/job_once.py > gpurun_out/fin/job_big.log 2>&1
 python scripts/launch_summary.py gpurun_out/fin/launches_big.csv > gpurun_out/fin/launches_big_summary.txt
