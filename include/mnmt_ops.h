@@ -121,17 +121,6 @@ mnmt_status mnmt_op_src_attention(const float* q_dev, int64_t ldq, const float* 
                                   int32_t max_span, int32_t n, int32_t d, int32_t H, float clip,
                                   int8_t* out_q_dev, float* out_f_dev, void* stream);
 
-/* As mnmt_op_src_attention with the one-warp TMA kernel chosen explicitly: persist = 1 runs the
- * persistent ping-pong variant (each warp walks (row, head) tasks with two tile buffers, the next
- * task's first K chunk in flight during the current task's context), 0 the one-launch-per-task
- * kernel.  Identical outputs either way. */
-mnmt_status mnmt_op_src_attention_persist(const float* q_dev, int64_t ldq, const float* kv_dev,
-                                          int64_t kv_rows, int64_t ldkv, int32_t k_off, int32_t v_off,
-                                          const int32_t* kv_start_dev, const int32_t* kv_len_dev,
-                                          int32_t max_span, int32_t n, int32_t d, int32_t H,
-                                          float clip, int8_t* out_q_dev, float* out_f_dev,
-                                          int32_t persist, void* stream);
-
 /* As mnmt_op_attention with bf16 keys / values: kv16 holds bfloat16 bit
  * patterns (uint16) in the same layout (strides and offsets in elements, multiples of 4). */
 mnmt_status mnmt_op_attention_bf16(const float* q_dev, int64_t ldq, const uint16_t* kv16_dev,

@@ -311,158 +311,6 @@ inline size_t attn_tma_smem(int dh, int span, bool share) {
                                     (size_t)dh * 4);
 }
 
-// Persistent variant of k_attn_tma (SHARE layout per task): each warp walks (row, head) tasks
-// gw, gw + G, ... (G = grid warps) with two tile buffers used in turn, so the next task's first K
-// chunk is in flight while the current task forms its normaliser and context -- no warp waits for
-// the first tile of a task, and no CTA launch / barrier set-up happens per task.  Per task the
-// chunk order, the V-reuses-the-K-buffer rule and every arithmetic step are k_attn_tma's, so the
-// outputs are identical to it.  Grid: the CTAs resident at once (occupancy x SMs), capped by the
-// tasks of the static row bound; the live row count is read after the PDL wait.
-template <int DH>
-__global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma_p(const __grid_constant__ CUtensorMap tm,
-                                                              AttnArgs a) {
-  constexpr int HB = DH / 32;
-  constexpr int TB = HB * AT_TILE;            // one tile buffer (K chunks, then V chunks)
-  extern __shared__ uint8_t at_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(at_raw) + 1023) & ~uintptr_t(1023));
-  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* buf0 = base + wi * 2 * TB;
-  double* sc = reinterpret_cast<double*>(base + AT_WARPS * 2 * TB) + (size_t)wi * a.span;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(base + AT_WARPS * 2 * TB + (size_t)AT_WARPS * a.span * 8) +
-                  (2 + DH / 2) * wi;
-  float4* qv = reinterpret_cast<float4*>(bar + 2);
-  if (lane == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_barrier_init();
-    tma_prefetch_desc(&tm);
-  }
-  __syncwarp();
-  pdl_wait();
-  pdl_trigger_early();
-  const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
-  const int64_t ntask = (int64_t)n_live * a.H, G = (int64_t)gridDim.x * AT_WARPS;
-  int64_t gw = (int64_t)blockIdx.x * AT_WARPS + wi;
-  if (gw >= ntask) return;
-  // task gw -> (row, head, span); self mode appends the row's k, v at position t first and
-  // orders those generic-proxy stores before the tensor copies that read them
-  auto task = [&](int64_t g, int& r, int& h, int& start, int& len) {
-    r = (int)(g / a.H);
-    h = (int)(g - (int64_t)r * a.H);
-    if (a.mode == ATTN_ENC) {
-      start = a.kv_start[r];
-      len = a.kv_len[r];
-    } else if (a.mode == ATTN_SELF) {
-      start = a.live[r] * a.t_cap;
-      len = a.ctrl[1];
-      const float* qk = a.q + (int64_t)r * a.ldq + h * DH;
-      float* dst = a.kv_w + (int64_t)(start + len - 1) * a.ldkv + h * DH;
-      for (int c = lane; c < DH; c += 32) {
-        dst[a.k_off + c] = qk[a.d + c];
-        dst[a.v_off + c] = qk[2 * a.d + c];
-      }
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      __syncwarp();
-    } else if (a.live_start) {
-      start = a.live_start[r];
-      len = a.live_len[r];
-    } else {
-      const int orig = a.live[r];
-      start = a.kv_start[orig];
-      len = a.kv_len[orig];
-    }
-  };
-  auto load = [&](uint64_t* b, uint8_t* dst, int row0, int len, int col, int c0) {
-    const int nb = min(4, (len - c0 + 7) >> 3);
-    mbar_arrive_expect_tx(b, HB * nb * AT_BOX);
-    for (int hb = 0; hb < HB; ++hb)
-      for (int x = 0; x < nb; ++x)
-        tma_load_2d(dst + hb * AT_TILE + x * AT_BOX, &tm, b, col + 32 * hb, row0 + c0 + 8 * x);
-  };
-  const double inv_sqrt = 1.0 / sqrt((double)DH);
-  uint32_t ph[2] = {0, 0};
-  int r, h, start, len;
-  task(gw, r, h, start, len);
-  if (lane == 0 && len > 0) load(&bar[0], buf0, (int)(a.kv_row0 + start), len, a.k_off + h * DH, 0);
-  for (int it = 0; gw < ntask; gw += G, ++it) {
-    const int X = it & 1;
-    uint8_t* kt = buf0 + X * TB;
-    const int row0 = (int)(a.kv_row0 + start);
-    const int kc = a.k_off + h * DH, vc = a.v_off + h * DH;
-    if (lane < DH / 4) qv[lane] = *reinterpret_cast<const float4*>(a.q + (int64_t)r * a.ldq + h * DH + 4 * lane);
-    __syncwarp();
-    double mx = -INFINITY;
-    for (int c0 = 0; c0 < len; c0 += 32) {
-      mbar_wait(&bar[X], ph[X]);
-      ph[X] ^= 1;
-      const int j = c0 + lane;
-      if (j < len) {
-        double dot = 0.0;
-#pragma unroll
-        for (int c = 0; c < DH; c += 4) {
-          const float4 k4 = *reinterpret_cast<const float4*>(kt + (c >> 5) * AT_TILE + at_swz(lane, c & 31));
-          const float4 q4 = qv[c >> 2];
-          dot = __fma_rn((double)q4.x, (double)k4.x, dot);
-          dot = __fma_rn((double)q4.y, (double)k4.y, dot);
-          dot = __fma_rn((double)q4.z, (double)k4.z, dot);
-          dot = __fma_rn((double)q4.w, (double)k4.w, dot);
-        }
-        const double s = __dmul_rn(dot, inv_sqrt);
-        sc[j] = s;
-        mx = fmax(mx, s);
-      }
-      __syncwarp();
-      if (lane == 0 && c0 + 32 < len) load(&bar[X], kt, row0, len, kc, c0 + 32);
-    }
-    // this task's first V chunk into its (consumed) K buffer; the next task's first K chunk into
-    // the other buffer (its previous contents, the last task's V, were consumed last iteration)
-    if (lane == 0 && len > 0) load(&bar[X], kt, row0, len, vc, 0);
-    const int64_t gn = gw + G;
-    int rn = 0, hn = 0, sn = 0, ln = 0;
-    if (gn < ntask) {
-      task(gn, rn, hn, sn, ln);
-      if (lane == 0 && ln > 0) load(&bar[X ^ 1], buf0 + (X ^ 1) * TB, (int)(a.kv_row0 + sn), ln, a.k_off + hn * DH, 0);
-    }
-    mx = warp_max_f64(mx);
-    double z = 0.0;
-    for (int jj = lane; jj < len; jj += 32) {
-      const double p = exp(__dsub_rn(sc[jj], mx));
-      sc[jj] = p;
-      z = __dadd_rn(z, p);
-    }
-    z = warp_sum_f64(z);
-    __syncwarp();
-    double acc[HB];
-#pragma unroll
-    for (int i = 0; i < HB; ++i) acc[i] = 0.0;
-    for (int c0 = 0; c0 < len; c0 += 32) {
-      mbar_wait(&bar[X], ph[X]);
-      ph[X] ^= 1;
-      const int je = min(32, len - c0);
-      for (int jj = 0; jj < je; ++jj) {
-        const double p = sc[c0 + jj];
-#pragma unroll
-        for (int i = 0; i < HB; ++i)
-          acc[i] = __fma_rn(p, (double)*reinterpret_cast<const float*>(kt + i * AT_TILE + at_swz(jj, lane)), acc[i]);
-      }
-      __syncwarp();
-      if (lane == 0 && c0 + 32 < len) load(&bar[X], kt, row0, len, vc, c0 + 32);
-    }
-    int8_t* out = a.out_q + (int64_t)r * a.d + h * DH;
-#pragma unroll
-    for (int i = 0; i < HB; ++i) {
-      const int c = lane + 32 * i;
-      const float ctx = len > 0 ? (float)__ddiv_rn(acc[i], z) : 0.0f;
-      out[c] = (int8_t)q8(ctx, a.clip, a.sigma);
-      if (a.out_f) a.out_f[(int64_t)r * a.d + h * DH + c] = ctx;
-    }
-    r = rn; h = hn; start = sn; len = ln;
-    __syncwarp();   // sc / qv reused by the next task
-  }
-}
-
-inline size_t attn_tma_p_smem(int dh, int span) { return attn_tma_smem(dh, span, false); }
-
 // Long spans at small row counts, split over NS warps per (row, head) with TMA tiles (A7 and the
 // greedy A6' self-attention; fp32 K/V, d_h = 32 / 64): one (row, head) per CTA of NS warps; warp
 // w takes the 32-position chunks w, w + NS, ... and requests each chunk's K tile by bulk tensor
@@ -1187,12 +1035,6 @@ cudaError_t attn_init() {   // once per device
     e = cudaFuncSetAttribute(k_attn_tma<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)attn_tma_smem(64, MNMT_MAX_KV, true));
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_attn_tma_p<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)attn_tma_p_smem(64, MNMT_MAX_KV));
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_attn_tma_p<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)attn_tma_p_smem(32, MNMT_MAX_KV));
-  if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn_tma<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)attn_tma_smem(32, MNMT_MAX_KV, true));
   if (e == cudaSuccess)
@@ -1305,24 +1147,6 @@ cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
       const char* e = getenv("MNMT_ATTN_SHARE");
       return !(e && e[0] == '0');
     }();
-    // persistent ping-pong variant (env MNMT_ATTN_PERSIST: 0 off, 1 on; A/B)
-    static const int persist_env = [] {
-      const char* e = getenv("MNMT_ATTN_PERSIST");
-      return e ? atoi(e) : 0;
-    }();
-    if (b.tma_persist > 0 || (b.tma_persist < 0 && persist_env)) {
-      const size_t smem = attn_tma_p_smem(b.dh, b.span);
-      const void* fn = b.dh == 64 ? (const void*)k_attn_tma_p<64> : (const void*)k_attn_tma_p<32>;
-      int occ = 0, dev = 0, sms = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, AT_WARPS * 32, smem) != cudaSuccess || occ < 1)
-        occ = 1;
-      const int64_t need = (warps + AT_WARPS - 1) / AT_WARPS;
-      const dim3 grid((unsigned)std::min<int64_t>(need, (int64_t)occ * sms)), block(AT_WARPS * 32);
-      return b.dh == 64 ? launch_pdl(k_attn_tma_p<64>, grid, block, smem, st, *b.tmap, b)
-                        : launch_pdl(k_attn_tma_p<32>, grid, block, smem, st, *b.tmap, b);
-    }
     const dim3 grid((unsigned)((warps + AT_WARPS - 1) / AT_WARPS)), block(AT_WARPS * 32);
     const size_t smem = attn_tma_smem(b.dh, b.span, share);
     if (share)

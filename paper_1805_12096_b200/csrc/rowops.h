@@ -85,8 +85,6 @@ struct AttnArgs {
   int64_t kv_row0;
   int tma_self;             // self mode: 0 generic kernels, 1 TMA split kernel for long decodes at
                             // <= 128 rows, 2 also the one-warp TMA kernel (measured per workload)
-  int tma_persist;          // one-warp TMA kernel as the persistent ping-pong variant: -1 the
-                            // library default (env MNMT_ATTN_PERSIST), 0 off, 1 on
 };
 
 // Encoder self-attention over Q|K|V rows [M x 3d] (A3), one CTA per (sentence, head).

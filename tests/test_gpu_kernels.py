@@ -427,34 +427,6 @@ def test_src_attention_tma(d, H):
     assert not boundary_explained(ref, O.quantize(ref), oq.cpu().numpy()).any()
 
 
-@pytest.mark.parametrize("d,H,n", [(1024, 16, 630), (256, 8, 50), (512, 8, 3), (1024, 16, 2000)])
-def test_src_attention_tma_persistent(d, H, n):
-    """The persistent ping-pong TMA attention (warps walk (row, head) tasks with two tile buffers;
-    more tasks than resident warps at n = 630 / 2000, multi-chunk spans, empty spans) writes
-    exactly the one-launch-per-task kernel's fp32 context and codes."""
-    rng = np.random.default_rng(d + n)
-    lens = rng.integers(0, 101, size=n).astype(np.int32)
-    lens[0], lens[-1] = 100, 0
-    starts = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int32)
-    S = int(lens.sum())
-    kv = rng.normal(0, 1, size=(S, 2 * d)).astype(np.float32)
-    q = rng.normal(0, 1, size=(n, d)).astype(np.float32)
-    kd, qd, sd, ld = to_dev(kv), to_dev(q), to_dev(starts), to_dev(lens)
-    outs = []
-    for persist in (0, 1):
-        oq, of = zeros((n, d), torch.int8), zeros((n, d), torch.float32)
-        M.op_src_attention_persist(ptr(qd), d, ptr(kd), S, 2 * d, 0, d, ptr(sd), ptr(ld), int(lens.max()), n, d,
-                                   H, CLIP, ptr(oq), ptr(of), persist)
-        sync()
-        outs.append((oq.cpu().numpy(), of.cpu().numpy()))
-    assert np.array_equal(outs[0][0], outs[1][0])
-    assert np.array_equal(outs[0][1], outs[1][1])
-    for r in (0, n // 2, n - 2):
-        if lens[r] > 0:
-            blk = kv[starts[r]:starts[r] + lens[r]]
-            np.testing.assert_allclose(outs[1][1][r], O.attention(q[r], blk[:, :d], blk[:, d:], H), rtol=1e-6, atol=1e-7)
-
-
 # ------------------------------------------------------------------ A11 across GPUs (unshard)
 def test_gather_rows():
     """mnmt_op_gather_rows puts the all-gathered rows of a strong-scaling job back in input order:
