@@ -48,8 +48,9 @@ mnmt_status mnmt_op_quantize(const float* x_dev, int64_t n, float clip, int8_t* 
  * epilogue arithmetic; M <= 32, EPI_F32 .. EPI_SIGMOID, A and W 16-byte aligned);
  * -2 = the swap-AB tcgen05 kernel (D^T = W . A^T: W's 128-row tiles as the MMA's M operand, the
  * M <= 128 rows of A as its N = 16 / 32 / 64 / 128 operand; same s32 sums and epilogue
- * arithmetic; every epilogue but EPI_TOPK; A 16-byte aligned).  Argument errors (not a silent
- * fallback) when the chosen kernel cannot take the call. */
+ * arithmetic; every epilogue but EPI_TOPK; A 16-byte aligned); -3 = the CTA-pair persistent
+ * kernel (256 x 256 tiles on a 2-CTA cluster, tcgen05 cta_group::2; any M; every epilogue but
+ * EPI_TOPK).  Argument errors (not a silent fallback) when the chosen kernel cannot take the call. */
 mnmt_status mnmt_op_gemm_i8(const int8_t* A_dev, const int8_t* W_dev, int32_t M, int32_t N,
                             int32_t K, const float* bias_dev, float clip, int32_t epilogue,
                             void* out_dev, void* out2_dev, int32_t n_tile, void* stream);

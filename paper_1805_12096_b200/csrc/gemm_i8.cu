@@ -784,6 +784,170 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
 }
 
+// ------------------------------------------------------------------ CTA-pair persistent variant
+// For the many-row GEMMs (encoder, K|V, the output layer at hundreds of rows) the one-CTA
+// persistent kernel is bound by L2 -> SM traffic: a 128 x 256 tile streams 48 KB per K block for
+// 4.2 M MACs (ncu: ~50 % of the int8 pipe).  k_gemm_pers2 runs a 256 x 256 tile on a CTA pair
+// (thread-block cluster of 2, tcgen05 cta_group::2): each CTA loads its 128 rows of A and its
+// 128 rows of B (32 KB per K block, both completing on the leader's barrier), the leader issues
+// M = 256 MMAs that read both CTAs' shared memory, and each CTA's TMEM receives its 128 rows of
+// the accumulator (two 256-column buffers).  Commits are multicast to both CTAs; each CTA's
+// epilogue warps release an accumulator buffer on the leader's barrier.  Numerics and epilogues
+// are k_gemm_pers's (exact s32 sums; outputs identical).
+constexpr int P2_BN = 256;
+struct Pers2Cfg {
+  static constexpr int A_BYTES = BM * BK;              // this CTA's 128 rows of A
+  static constexpr int B_BYTES = (P2_BN / 2) * BK;     // this CTA's 128 rows of B
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = 5;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + EPI_STAGE_BYTES;
+  static constexpr int TMEM_COLS = 2 * P2_BN;          // two accumulator buffers
+};
+
+template <int EPI>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    k_gemm_pers2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const GemmArgs args) {
+  using Cfg = Pers2Cfg;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[STAGES];    // leader: both CTAs' bytes
+  __shared__ __align__(8) uint64_t empty_bar[STAGES];   // both: the leader's commit (multicast)
+  __shared__ __align__(8) uint64_t tfull_bar[2];        // both: accumulator buffer complete
+  __shared__ __align__(8) uint64_t tempty_bar[2];       // leader: both CTAs' epilogue warps
+  __shared__ uint32_t tmem_slot;
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tempty_bar[i], 2 * EPI_WARPS);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair<Cfg::TMEM_COLS>(&tmem_slot);
+  __syncwarp();
+  tc_fence_before();
+  cluster_sync();   // both CTAs' barriers initialised and TMEM allocated before any remote use
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_slot;
+  pdl_wait();
+  const int M_live = args.M_dyn ? min(args.M, *args.M_dyn) : args.M;
+  const int m_tiles = (M_live + 2 * BM - 1) / (2 * BM);
+  const int n_tiles = (args.N + P2_BN - 1) / P2_BN;
+  const int T = m_tiles * n_tiles;
+  const int num_kb = (args.K + BK - 1) / BK;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs): this CTA's A and B halves, counted on the
+      // leader's full barrier
+      uint32_t ps = 0, pph = 0;
+      for (int t = pair; t < T; t += npairs) {
+        const int m0 = (t / n_tiles) * 2 * BM + (int)rank * BM, n0 = (t % n_tiles) * P2_BN + (int)rank * (P2_BN / 2);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[ps], pph ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[ps], 2 * Cfg::STAGE_BYTES);
+          const uint32_t fb = mapa_shared(smem_u32(&full_bar[ps]), 0);
+          uint8_t* sa = smem + ps * Cfg::STAGE_BYTES;
+          uint8_t* sb = sa + Cfg::A_BYTES;
+          tma_load_2d_pair(sa, &tmA, fb, kb * BK, m0);
+          tma_load_2d_pair(sa + 64 * BK, &tmA, fb, kb * BK, m0 + 64);
+          tma_load_2d_pair(sb, &tmB, fb, kb * BK, n0);
+          tma_load_2d_pair(sb + 64 * BK, &tmB, fb, kb * BK, n0 + 64);
+          if (++ps == STAGES) { ps = 0; pph ^= 1; }
+        }
+      }
+      // drain: every stage's last use released (the commits that arrive here have landed)
+      for (int i = 0; i < STAGES; ++i) {
+        mbar_wait(&empty_bar[ps], pph ^ 1);
+        if (++ps == STAGES) { ps = 0; pph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (leader): 256 x 256 x 32 per instruction for the pair
+      constexpr uint32_t idesc = idesc_i8<2 * BM, P2_BN>();
+      uint32_t cs = 0, cph = 0, ab = 0, aph = 0;
+      for (int t = pair; t < T; t += npairs) {
+        mbar_wait_cluster(&tempty_bar[ab], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + ab * P2_BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait_cluster(&full_bar[cs], cph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + cs * Cfg::STAGE_BYTES);
+          const uint64_t adesc = umma_desc_sw128(sa);
+          const uint64_t bdesc = umma_desc_sw128(sa + Cfg::A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 32; ++k)
+            mma_i8_pair(d_tmem, adesc + (uint64_t)(2 * k), bdesc + (uint64_t)(2 * k), idesc, (kb | k) != 0);
+          mma_commit_pair(&empty_bar[cs], 0x3);
+          if (++cs == STAGES) { cs = 0; cph ^= 1; }
+        }
+        mma_commit_pair(&tfull_bar[ab], 0x3);
+        ab ^= 1;
+        if (ab == 0) aph ^= 1;
+      }
+    }
+  } else {
+    // ---------------- epilogue (both CTAs): this CTA's 128 rows x 256 columns
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    constexpr int HALF = P2_BN / 2;
+    const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty_bar[0]), 0);
+    uint32_t ab = 0, aph = 0;
+    bool first = true;
+    for (int t = pair; t < T; t += npairs) {
+      const int m0 = (t / n_tiles) * 2 * BM + (int)rank * BM, n0 = (t % n_tiles) * P2_BN;
+      const int row = m0 + q * 32 + lane;
+      const bool row_ok = row < M_live;
+      uint32_t slw[HALF / 32];
+      if constexpr (EPI == EPI_ARGMAX) sl_words<HALF>(args, row, row_ok, n0 + half * HALF, slw);
+      mbar_wait_cluster(&tfull_bar[ab], aph);
+      tc_fence_after();
+      if (first && warp == 2 && lane == 0) pdl_launch_dependents();
+      first = false;
+      const uint32_t t_row = tmem_base + ab * P2_BN + ((uint32_t)(q * 32) << 16) + half * HALF;
+      float* stage = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES) + (warp - 2) * EPI_STAGE_FLOATS;
+      float best_v = -INFINITY;
+      int best_j = -1;
+#pragma unroll 1
+      for (int c = 0; c < HALF; c += 32) {
+        int32_t acc[32];
+        tmem_ld16(t_row + c, *reinterpret_cast<int32_t(*)[16]>(acc));
+        tmem_ld16(t_row + c + 16, *reinterpret_cast<int32_t(*)[16]>(acc + 16));
+        tmem_ld_wait();
+        const int n = n0 + half * HALF + c;
+        if (n >= args.N) break;
+        epi_store_chunk<EPI>(args, args.bias, row, row_ok, n, acc, best_v, best_j, stage,
+                             EPI == EPI_ARGMAX ? slw[c / 32] : 0u);
+      }
+      if constexpr (EPI == EPI_ARGMAX) {
+        if (row_ok && best_j >= 0) atomicMax(args.keys + row, argmax_key(best_v, (uint32_t)best_j));
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader + ab * 8);
+      ab ^= 1;
+      if (ab == 0) aph ^= 1;
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  cluster_sync();   // both CTAs done: every MMA has completed and been read
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc_pair<Cfg::TMEM_COLS>(tmem_base);
+}
+
 // ------------------------------------------------------------------ swap-AB variant
 // For a handful of live rows (a decoder step of the critical lane, <= 64 rows) the 128-row A
 // tile of k_gemm_i8 is mostly padding, yet every CTA streams it from L2 after the PDL wait (the
@@ -1159,6 +1323,62 @@ static cudaError_t launch_pers_t(const CUtensorMap& tmA, const CUtensorMap& tmB,
   return cudaLaunchKernelEx(&cfg, k_gemm_pers<BN, EPI>, tmA, tmB, a);
 }
 
+// CTA-pair persistent launch: one cluster of 2 per pair of SMs, 256 x 256 tiles.  Taken for the
+// BN = 256 persistent launches with deep K (>= 2048: the operand stream, not the epilogue's
+// stores, bounds the tile; measured encoder FFN2 of the big student, 33k rows, K 4096: 70.6 ->
+// 81.8 % of the int8 peak, while the K = 1024 GEMMs with fp32 outputs lose 3-10 %,
+// profiles/r2_pair_micro.txt).  env MNMT_PERS2 = 0 / 1 forces it off / on (A/B).
+static int pers2_mode() {
+  static const int v = [] {
+    const char* e = getenv("MNMT_PERS2");
+    return e ? atoi(e) : -1;
+  }();
+  return v;
+}
+static bool pers2_take(const GemmArgs& a) {
+  if (a.pers2 != 0) return a.pers2 > 0;
+  const int mode = pers2_mode();
+  return mode >= 0 ? mode == 1 : a.K >= 2048;
+}
+
+template <int EPI>
+static cudaError_t launch_pers2_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
+                                  cudaStream_t st) {
+  const int tiles = ((a.M + 2 * BM - 1) / (2 * BM)) * ((a.N + P2_BN - 1) / P2_BN);
+  int cap = num_sms();
+  if (a.pers_grid > 0 && a.pers_grid < cap) cap = a.pers_grid;
+  const int pairs = std::max(1, std::min(tiles, cap / 2));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = Pers2Cfg::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 2;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, k_gemm_pers2<EPI>, tmA, tmB, a);
+}
+
+static cudaError_t launch_pers2(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, int epi,
+                                cudaStream_t st) {
+  switch (epi) {
+    case EPI_F32: return launch_pers2_t<EPI_F32>(tmA, tmB, a, st);
+    case EPI_F32_Q: return launch_pers2_t<EPI_F32_Q>(tmA, tmB, a, st);
+    case EPI_RELU_Q: return launch_pers2_t<EPI_RELU_Q>(tmA, tmB, a, st);
+    case EPI_RELU_F32_Q: return launch_pers2_t<EPI_RELU_F32_Q>(tmA, tmB, a, st);
+    case EPI_SIGMOID: return launch_pers2_t<EPI_SIGMOID>(tmA, tmB, a, st);
+    case EPI_ARGMAX: return launch_pers2_t<EPI_ARGMAX>(tmA, tmB, a, st);
+    case EPI_ACC: return launch_pers2_t<EPI_ACC>(tmA, tmB, a, st);
+  }
+  return cudaErrorNotSupported;
+}
+
 // Split-K factor of a non-persistent launch (GemmArgs::split_k: 0 none, > 1 forced, -1 the rule
 // below): deep K and a grid that leaves most SMs idle (FFN2 of the base / big students at small
 // row counts, where each CTA would stream its whole K = F range alone).  Powers of two while the split grid fits the launch's SM budget, every
@@ -1207,7 +1427,11 @@ template <int BN, int EPI>
 static cudaError_t launch_t(const CUtensorMap& tmA_in, const CUtensorMap& tmB_in, const GemmArgs& a,
                             cudaStream_t st) {
   if constexpr (BN >= 64)   // BN = 32 (16-column epilogue chunks) is never persistent
-    if (gemm_persistent(a.M, a.N, BN, a.pers_grid)) return launch_pers_t<BN, EPI>(tmA_in, tmB_in, a, st);
+    if (gemm_persistent(a.M, a.N, BN, a.pers_grid)) {
+      if (BN == 256 && pers2_take(a))
+        return launch_pers2_t<EPI>(tmA_in, tmB_in, a, st);
+      return launch_pers_t<BN, EPI>(tmA_in, tmB_in, a, st);
+    }
   using Cfg = GemmCfg<BN>;
   const int ks = gemm_split_k(a, BN, EPI);
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, ks);
@@ -1306,6 +1530,12 @@ static cudaError_t gemm_init_all() {
   if ((e = set_attr_bn32()) != cudaSuccess) return e;
   if ((e = set_attr_bn<64>()) != cudaSuccess) return e;
   if ((e = set_attr_bn<128>()) != cudaSuccess) return e;
+  for (const void* f : {(const void*)k_gemm_pers2<EPI_F32>, (const void*)k_gemm_pers2<EPI_F32_Q>,
+                        (const void*)k_gemm_pers2<EPI_RELU_Q>, (const void*)k_gemm_pers2<EPI_RELU_F32_Q>,
+                        (const void*)k_gemm_pers2<EPI_SIGMOID>, (const void*)k_gemm_pers2<EPI_ARGMAX>,
+                        (const void*)k_gemm_pers2<EPI_ACC>})
+    if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, Pers2Cfg::SMEM)) != cudaSuccess)
+      return e;
   if ((e = set_attr_sab<16>()) != cudaSuccess) return e;
   if ((e = set_attr_sab<32>()) != cudaSuccess) return e;
   if ((e = set_attr_sab<64>()) != cudaSuccess) return e;
@@ -1627,6 +1857,7 @@ cudaError_t launch_gemm_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const
     if (epi == EPI_TOPK4) return launch_np<TOPK_BN, EPI_TOPK4>(tmA, tmB, a, st);
     return launch_np<TOPK_BN, EPI_TOPK>(tmA, tmB, a, st);
   }
+  if (bn == -3) return launch_pers2(tmA, tmB, a, epi, st);   // op level: the CTA-pair kernel
   if (bn == 0) bn = gemm_pick_bn(a.M, a.N, a.pers_grid);
   // 32-wide tiles halve each epilogue warp's columns where the 64-wide grid is small
   // (env MNMT_BN32=0 disables; A/B)

@@ -76,6 +76,8 @@ struct GemmArgs {
   int sab_kmin;                // shallowest K the swap-AB path takes (model path; 0 = any)
   int sab_force;               // op level: take the swap-AB path for any M <= 128 (error otherwise)
   int sab_kb;                  // K blocks per CTA before K is split over a cluster (0 = default 8)
+  int pers2;                   // BN = 256 persistent launches on CTA pairs (k_gemm_pers2): 1 on,
+                               // -1 off, 0 the library default (env MNMT_PERS2)
   int a_box;                   // (launch-internal) k_gemm_i8: A loaded as one a_box-row box (0: 2 x 64)
   int b_box32;                 // (launch-internal) k_gemm_i8<32>: B loaded as one 32-row box
   int ring_cap;                // (launch-internal) TMA ring depth cap of a split-K launch
@@ -93,7 +95,7 @@ bool make_tmap_i8(CUtensorMap* map, const void* base, int64_t rows, int64_t K);
 bool make_tmap_kv(CUtensorMap* map, const void* base, int64_t rows, int64_t cols);
 
 // A is [>= M x K] activation codes, B is [N x K] weight codes (both via make_tmap_i8).
-// bn = 0 picks the N tile.
+// bn = 0 picks the N tile; -3 forces the CTA-pair persistent kernel (256 x 256 tiles).
 cudaError_t launch_gemm_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                            int epi, int bn, cudaStream_t st);
 

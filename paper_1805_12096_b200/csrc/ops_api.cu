@@ -72,10 +72,14 @@ static mnmt_status gemm_op(const int8_t* A, const int8_t* W, int32_t M, int32_t 
   if (small && (M > 32 || epi > MNMT_EPI_SIGMOID || (uintptr_t)A % 16 || (uintptr_t)W % 16))
     return arg_error("mnmt_op_gemm_i8: n_tile -1 needs M <= 32, an fp32 / code epilogue and 16-byte aligned A, W");
   const bool sab = n_tile == -2;     // the swap-AB tcgen05 kernel (k_gemm_sab)
+  const bool pair = n_tile == -3;    // the CTA-pair persistent kernel (k_gemm_pers2)
+  if (pair && (epi == MNMT_EPI_TOPK || split_k > 1))
+    return arg_error("mnmt_op_gemm_i8: n_tile -3 takes no TOPK epilogue and no split-K");
   if (sab && (M > 128 || epi == MNMT_EPI_TOPK || (uintptr_t)A % 16))
     return arg_error("mnmt_op_gemm_i8: n_tile -2 needs M <= 128, a non-TOPK epilogue and 16-byte aligned A");
-  if (epi != MNMT_EPI_TOPK && n_tile != 0 && n_tile != 64 && n_tile != 128 && n_tile != 256 && !small && !sab)
-    return arg_error("mnmt_op_gemm_i8: n_tile must be -2, -1, 0, 64, 128 or 256");
+  if (epi != MNMT_EPI_TOPK && n_tile != 0 && n_tile != 64 && n_tile != 128 && n_tile != 256 && !small && !sab &&
+      !pair)
+    return arg_error("mnmt_op_gemm_i8: n_tile must be -3, -2, -1, 0, 64, 128 or 256");
   int n_tile_topk = 0;
   if (cudaError_t e = gemm_init(); e != cudaSuccess) return cuda_status(e, "gemm init");
   CUtensorMap ta, tb;

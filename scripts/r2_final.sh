@@ -25,6 +25,10 @@ run() {
   ncu -i gpurun_out/fin/ncu/$n.ncu-rep --page raw --csv > gpurun_out/fin/ncu/$n.csv 2>/dev/null
   ncu -i gpurun_out/fin/ncu/$n.ncu-rep --page details --print-details all > gpurun_out/fin/ncu/$n.details.txt 2>/dev/null
 }
+run sab_ffn2 'k_gemm' KERNEL=ffn2 D=1024 F=4096 M=32 NTILE=-2
+run sab_dxd 'k_gemm' KERNEL=dxd D=1024 M=16 NTILE=-2
+run enc_mq 'k_attn_enc' KERNEL=enc D=1024 H=16 M=2371 S=28 ENCV=2
+run pair_ffn2 'k_gemm' KERNEL=ffn2 D=1024 F=4096 M=33000 NTILE=-3
 run attn 'k_attn' KERNEL=attn D=1024 H=16 M=630 S=21
 run ln 'k_ln' KERNEL=ln D=1024 M=630
 run dxd 'k_gemm' KERNEL=dxd D=1024 M=630
@@ -34,5 +38,9 @@ python scripts/ncu_full_summary.py \
   "ln@big-newstest-8192w|rows=630 d=1024 (k_ln_split<4>)|gpurun_out/fin/ncu/ln.csv" \
   "dxd@big-newstest-8192w|M=630 N=1024 K=1024 (k_gemm_i8<64,EPI_F32>)|gpurun_out/fin/ncu/dxd.csv" \
   "out@big-newstest-8192w|M=630 N=36000 K=1024 (k_gemm_pers<256,EPI_ARGMAX>)|gpurun_out/fin/ncu/out.csv" \
+  "sab_ffn2@big-newstest-8192w|M=32 N=1024 K=4096 (k_gemm_sab<32,EPI_F32>, 4-CTA K split)|gpurun_out/fin/ncu/sab_ffn2.csv" \
+  "sab_dxd@big-newstest-8192w|M=16 N=1024 K=1024 (k_gemm_sab<16,EPI_F32>)|gpurun_out/fin/ncu/sab_dxd.csv" \
+  "enc_mq@big-newstest-8192w|2371 sentences of 10..28 tokens, d=1024 H=16 (k_attn_enc_mq<4>)|gpurun_out/fin/ncu/enc_mq.csv" \
+  "pair_ffn2@big-newstest-8192w|M=33000 N=1024 K=4096 (k_gemm_pers2<EPI_F32>, CTA pairs)|gpurun_out/fin/ncu/pair_ffn2.csv" \
   > gpurun_out/fin/ncu_full_kernels.json
 rm -f gpurun_out/fin/ncu/*.ncu-rep

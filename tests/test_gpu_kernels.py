@@ -242,6 +242,76 @@ def test_gemm_swap_ab_argmax_bitexact_with_ties(Mr, N, K):
     assert np.array_equal(ids.cpu().numpy(), ref)
 
 
+# CTA-pair persistent kernel (n_tile -3: 256 x 256 tiles on a 2-CTA cluster, tcgen05 cta_group::2)
+PAIR_SHAPES = [(256, 256, 128), (257, 304, 256), (1000, 1024, 1024), (5000, 3072, 1024), (130, 36000, 256),
+               (4097, 2048, 1040), (1, 256, 64)]
+
+
+@pytest.mark.parametrize("Mr,N,K", PAIR_SHAPES)
+def test_gemm_pair_acc_bitexact(Mr, N, K):
+    a = rand_codes((Mr, K), Mr + K + 5)
+    w = rand_codes((N, K), N + 13)
+    out = empty((Mr, N), torch.int32)
+    M.op_gemm_i8(ptr(to_dev(a)), ptr(to_dev(w)), Mr, N, K, None, CLIP, M.EPI_ACC, ptr(out), None, -3)
+    sync()
+    assert np.array_equal(out.cpu().numpy(), O.gemm_acc(a, w))
+
+
+@pytest.mark.parametrize("epi", [M.EPI_F32, M.EPI_F32_Q, M.EPI_RELU_Q, M.EPI_RELU_F32_Q, M.EPI_SIGMOID])
+@pytest.mark.parametrize("Mr,N,K", [(600, 1024, 1024), (3001, 4096, 256), (77, 160, 512)])
+def test_gemm_pair_epilogues_bitexact(epi, Mr, N, K):
+    rng = np.random.default_rng(epi * 31 + Mr)
+    x = rng.normal(0, 1.0, size=(Mr, K)).astype(np.float32)
+    W = rng.uniform(-0.08, 0.08, size=(N, K)).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, size=N).astype(np.float32)
+    qa, qw = O.quantize(x), O.quantize(W)
+    v = O.linear(qa, qw, b, CLIP)
+    A, Wd, bd = to_dev(qa), to_dev(qw), to_dev(b)
+    of = empty((Mr, N), torch.float32)
+    oq = empty((Mr, N), torch.int8)
+    if epi == M.EPI_RELU_Q:
+        M.op_gemm_i8(ptr(A), ptr(Wd), Mr, N, K, ptr(bd), CLIP, epi, ptr(oq), None, -3)
+    else:
+        M.op_gemm_i8(ptr(A), ptr(Wd), Mr, N, K, ptr(bd), CLIP, epi, ptr(of), ptr(oq), -3)
+    sync()
+    r = np.maximum(v, np.float32(0))
+    if epi in (M.EPI_F32, M.EPI_F32_Q):
+        assert np.array_equal(of.cpu().numpy(), v)
+    if epi == M.EPI_F32_Q:
+        assert np.array_equal(oq.cpu().numpy(), O.quantize(v))
+    if epi == M.EPI_RELU_Q:
+        assert np.array_equal(oq.cpu().numpy(), O.quantize(r))
+    if epi == M.EPI_RELU_F32_Q:
+        assert np.array_equal(of.cpu().numpy(), r)
+        assert np.array_equal(oq.cpu().numpy(), O.quantize(r))
+    if epi == M.EPI_SIGMOID:
+        assert np.array_equal(of.cpu().numpy(), O.sigmoid_array(v))
+
+
+@pytest.mark.parametrize("Mr,K", [(630, 1024), (3000, 256)])
+def test_gemm_pair_argmax_bitexact_with_ties(Mr, K):
+    N = 36000
+    rng = np.random.default_rng(Mr + K + 7)
+    x = rng.normal(0, 1.0, size=(Mr, K)).astype(np.float32)
+    E = rng.uniform(-0.5, 0.5, size=(N, K)).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, size=N).astype(np.float32)
+    qa, qE = O.quantize(x), O.quantize(E)
+    best = np.argmax(O.linear(qa, qE, b, CLIP), axis=1)
+    for i in range(0, Mr, 5):
+        j = int(best[i])
+        for j2 in ((j * 7 + 11) % N, (j + N // 2) % N):
+            if j2 != j:
+                qE[j2] = qE[j]
+                b[j2] = b[j]
+    ref = np.argmax(O.linear(qa, qE, b, CLIP), axis=1)
+    keys = zeros((Mr,), torch.int64)
+    M.op_gemm_i8(ptr(to_dev(qa)), ptr(to_dev(qE)), Mr, N, K, ptr(to_dev(b)), CLIP, M.EPI_ARGMAX, ptr(keys), None, -3)
+    ids = empty((Mr,), torch.int32)
+    M.op_argmax_ids(ptr(keys), Mr, ptr(ids))
+    sync()
+    assert np.array_equal(ids.cpu().numpy(), ref)
+
+
 def test_gemm_swap_ab_rejects():
     """n_tile -2 is an argument error (never a silent fallback) beyond 128 rows."""
     a = to_dev(rand_codes((129, 64), 1))
