@@ -122,6 +122,17 @@ mnmt_status mnmt_op_src_attention(const float* q_dev, int64_t ldq, const float* 
                                   int32_t max_span, int32_t n, int32_t d, int32_t H, float clip,
                                   int8_t* out_q_dev, float* out_f_dev, void* stream);
 
+/* As mnmt_op_src_attention with the one-warp TMA kernel in fp32 arithmetic (the model option
+ * "attn_f32"): fp32 dot products in order, expf, fp32 normaliser and context sums.  It departs
+ * from R20 (fp64 sums): ctx agrees with the oracle to ~1e-6 relative and codes differ only at
+ * rounding boundaries; long spans at <= 128 rows still take the fp64 split kernel.  d / H = 32
+ * or 64 (argument error otherwise). */
+mnmt_status mnmt_op_src_attention_f32(const float* q_dev, int64_t ldq, const float* kv_dev,
+                                      int64_t kv_rows, int64_t ldkv, int32_t k_off, int32_t v_off,
+                                      const int32_t* kv_start_dev, const int32_t* kv_len_dev,
+                                      int32_t max_span, int32_t n, int32_t d, int32_t H, float clip,
+                                      int8_t* out_q_dev, float* out_f_dev, void* stream);
+
 /* As mnmt_op_attention with bf16 keys / values: kv16 holds bfloat16 bit
  * patterns (uint16) in the same layout (strides and offsets in elements, multiples of 4). */
 mnmt_status mnmt_op_attention_bf16(const float* q_dev, int64_t ldq, const uint16_t* kv16_dev,

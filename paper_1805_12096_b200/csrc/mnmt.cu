@@ -203,6 +203,7 @@ struct mnmt_model {
   int smallm_kmax = 512;               // option: deepest K the small-M path takes
   int64_t smallm_wmax = 1 << 20;       // option: largest weight matrix (N x K bytes) of the small-M path
   int attn_tma_self = 2;               // option: self-attention through TMA tiles (0 / 1 / 2)
+  int attn_f32 = 0;                    // option: decoder attention in fp32 (departs from R20; off)
   int split_k = 0;                     // option: 1 = split-K clusters by the measured rule (off: slower in the job)
   DevDump dump;                        // (call state) device dumps of a teacher-forced run
   int green_sms = 0;                   // option: SMs of the critical lane's green context (0 = off)
@@ -1004,6 +1005,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, int6
       at.anc = m->beam > 0 ? w.anc : nullptr;
       at.tmap = &w.tm_self;             // TMA tiles (greedy; beam search reads through anc)
       at.tma_self = m->attn_tma_self;
+      at.f32 = m->attn_f32;
       at.kv_row0 = (int64_t)l * w.B_cap * w.T_cap;
       at.clip = c.clip;
       at.sigma = sigma_of(m);
@@ -1034,6 +1036,7 @@ static cudaError_t launch_step(mnmt_model* m, Lane& Ln, int n, bool forced, int6
     as.kv = w.kv + (int64_t)l * w.M_cap * 2 * d;
     as.kv16 = c.src_kv_bf16 ? w.kv16 + (int64_t)l * w.M_cap * 2 * d : nullptr;
     as.tmap = &w.tm_kv;                // TMA tiles (fp32 K/V)
+    as.f32 = m->attn_f32;
     as.kv_row0 = (int64_t)l * w.M_cap;
     as.ldkv = 2 * d;
     as.k_off = 0;
@@ -2152,6 +2155,15 @@ extern "C" mnmt_status mnmt_model_set_option(mnmt_model* m, const char* name, in
   if (std::string(name) == "smallm_wmax") {
     if (value < 0) { set_err("smallm_wmax < 0"); return MNMT_ERR_ARG; }
     m->smallm_wmax = value;
+    for (Lane& L : m->lanes) {
+      for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
+      L.graphs.clear();
+    }
+    return MNMT_OK;
+  }
+  if (std::string(name) == "attn_f32") {
+    if (value != 0 && value != 1) { set_err("attn_f32 must be 0 or 1"); return MNMT_ERR_ARG; }
+    m->attn_f32 = (int)value;
     for (Lane& L : m->lanes) {
       for (auto& kv : L.graphs) cudaGraphExecDestroy(kv.second);
       L.graphs.clear();

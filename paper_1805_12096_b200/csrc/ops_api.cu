@@ -256,11 +256,37 @@ mnmt_status mnmt_op_attention_enc(const float* qkv, const int32_t* sent_start, c
   return cuda_status(e, "encoder attention");
 }
 
+static mnmt_status src_attention_op(const float* q, int64_t ldq, const float* kv, int64_t kv_rows,
+                                    int64_t ldkv, int32_t k_off, int32_t v_off,
+                                    const int32_t* kv_start, const int32_t* kv_len, int32_t max_span,
+                                    int32_t n, int32_t d, int32_t H, float clip, int8_t* out_q,
+                                    float* out_f, int f32, void* stream);
+
 mnmt_status mnmt_op_src_attention(const float* q, int64_t ldq, const float* kv, int64_t kv_rows,
                                   int64_t ldkv, int32_t k_off, int32_t v_off,
                                   const int32_t* kv_start, const int32_t* kv_len, int32_t max_span,
                                   int32_t n, int32_t d, int32_t H, float clip, int8_t* out_q,
                                   float* out_f, void* stream) {
+  return src_attention_op(q, ldq, kv, kv_rows, ldkv, k_off, v_off, kv_start, kv_len, max_span, n, d,
+                          H, clip, out_q, out_f, 0, stream);
+}
+
+mnmt_status mnmt_op_src_attention_f32(const float* q, int64_t ldq, const float* kv, int64_t kv_rows,
+                                      int64_t ldkv, int32_t k_off, int32_t v_off,
+                                      const int32_t* kv_start, const int32_t* kv_len, int32_t max_span,
+                                      int32_t n, int32_t d, int32_t H, float clip, int8_t* out_q,
+                                      float* out_f, void* stream) {
+  if (d % H || (d / H != 32 && d / H != 64))
+    return arg_error("mnmt_op_src_attention_f32: d / H must be 32 or 64 (the TMA kernel)");
+  return src_attention_op(q, ldq, kv, kv_rows, ldkv, k_off, v_off, kv_start, kv_len, max_span, n, d,
+                          H, clip, out_q, out_f, 1, stream);
+}
+
+static mnmt_status src_attention_op(const float* q, int64_t ldq, const float* kv, int64_t kv_rows,
+                                    int64_t ldkv, int32_t k_off, int32_t v_off,
+                                    const int32_t* kv_start, const int32_t* kv_len, int32_t max_span,
+                                    int32_t n, int32_t d, int32_t H, float clip, int8_t* out_q,
+                                    float* out_f, int f32, void* stream) {
   if (n < 0 || H < 1 || d % H || (d / H) % 4 || d / H > 64 || !q || !kv || kv_rows < 1 ||
       max_span < 0 || max_span > MNMT_MAX_KV ||
       !kv_start || !kv_len || !out_q || ldq % 4 || ldkv % 4 || k_off % 4 || v_off % 4 ||
@@ -290,6 +316,7 @@ mnmt_status mnmt_op_src_attention(const float* q, int64_t ldq, const float* kv, 
   a.out_f = out_f;
   a.tmap = &tm;
   a.kv_row0 = 0;
+  a.f32 = f32;
   return cuda_status(launch_attn(a, (cudaStream_t)stream), "source attention");
 }
 

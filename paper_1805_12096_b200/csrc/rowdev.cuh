@@ -154,19 +154,22 @@ __device__ __forceinline__ void ln_row(const LnArgs a, int r, const float* vsm =
 // partial sums (its elements in order), warp tree, then the W warp partials combined in warp
 // order through shared memory (red: [rows per block][W] doubles).  Same arithmetic as ln_row
 // (R20: fp64 sums in another order, one rounding to fp32).
-template <int W>
+template <int W, int NV = 2>
 __device__ __forceinline__ void ln_row_split(const LnArgs a, int r, double* red, bool store) {
+  // NV float4 columns per thread: d = 128 W NV (NV = 2: 8 elements per thread; NV = 1: 4)
   const int tid = threadIdx.x % (32 * W), wr = tid >> 5, lane = threadIdx.x & 31;
   const int d = a.d;
   const int64_t off = (int64_t)r * d;
   const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
   const int orig = a.aan.C ? a.live[r] : 0;
   const float tf = a.aan.C ? (float)a.ctrl[1] : 1.0f;
-  const int c0 = 4 * tid, c1 = 4 * (tid + 32 * W);   // the thread's two float4 columns
-  float4 v[2];
+  // the division by d is exact as a multiplication when d is a power of two
+  const bool pow2 = (d & (d - 1)) == 0;
+  const double rd = 1.0 / (double)d;
+  float4 v[NV];
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int c = i ? c1 : c0;
+  for (int i = 0; i < NV; ++i) {
+    const int c = 4 * (tid + 32 * W * i);
     const float4 x = ld4(a.x + off + c);
     float4 z;
     if (a.gi) {
@@ -181,17 +184,19 @@ __device__ __forceinline__ void ln_row_split(const LnArgs a, int r, double* red,
     v[i] = add4(x, z);
   }
   double s = __dadd_rn(__dadd_rn(__dadd_rn((double)v[0].x, (double)v[0].y), (double)v[0].z), (double)v[0].w);
-  s = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(s, (double)v[1].x), (double)v[1].y), (double)v[1].z), (double)v[1].w);
+#pragma unroll
+  for (int i = 1; i < NV; ++i)
+    s = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(s, (double)v[i].x), (double)v[i].y), (double)v[i].z), (double)v[i].w);
   s = warp_sum_f64(s);
   if (lane == 0) red[wr] = s;
   __syncthreads();
   double tot = red[0];
 #pragma unroll
   for (int k = 1; k < W; ++k) tot = __dadd_rn(tot, red[k]);
-  const double mu = __ddiv_rn(tot, (double)d);
+  const double mu = pow2 ? __dmul_rn(tot, rd) : __ddiv_rn(tot, (double)d);
   double q = 0.0;
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < NV; ++i) {
     const double t0 = __dsub_rn((double)v[i].x, mu), t1 = __dsub_rn((double)v[i].y, mu);
     const double t2 = __dsub_rn((double)v[i].z, mu), t3 = __dsub_rn((double)v[i].w, mu);
     q = __dadd_rn(q, __dmul_rn(t0, t0));
@@ -206,12 +211,12 @@ __device__ __forceinline__ void ln_row_split(const LnArgs a, int r, double* red,
   double qt = red[0];
 #pragma unroll
   for (int k = 1; k < W; ++k) qt = __dadd_rn(qt, red[k]);
-  const double var = __ddiv_rn(qt, (double)d);
+  const double var = pow2 ? __dmul_rn(qt, rd) : __ddiv_rn(qt, (double)d);
   const double inv = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(var, (double)a.eps)));
   if (!store || r >= n_live) return;   // after the last barrier
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int c = i ? c1 : c0;
+  for (int i = 0; i < NV; ++i) {
+    const int c = 4 * (tid + 32 * W * i);
     const float4 g = ld4(a.gamma + c), b = ld4(a.beta + c);
     float4 o;
     o.x = (float)__dadd_rn(__dmul_rn(__dmul_rn(__dsub_rn((double)v[i].x, mu), inv), (double)g.x), (double)b.x);

@@ -12,6 +12,7 @@
 //   k_attn_enc     encoder self-attention, warp per query row (other shapes)          (A3)
 //   k_finish       argmax decode + EOS/max_len + stable live-row compaction (A9, A10)
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <utility>
@@ -112,7 +113,7 @@ __global__ void k_ln(LnArgs a) {
 }
 
 // Wide rows (d = 256 W, W >= 2): W warps per row, 256-thread blocks (256 / (32 W) rows each).
-template <int W>
+template <int W, int NV = 2>
 __global__ void __launch_bounds__(256) k_ln_split(LnArgs a) {
   __shared__ double red[256 / 32];
   pdl_wait();
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(256) k_ln_split(LnArgs a) {
   const int r = blockIdx.x * RPB + rb;
   // rows past the static bound compute a clamped row (every thread reaches every barrier)
   // and store nothing
-  ln_row_split<W>(a, min(r, a.n - 1), red + rb * W, r < a.n);
+  ln_row_split<W, NV>(a, min(r, a.n - 1), red + rb * W, r < a.n);
 }
 
 constexpr int ATTN_WARPS = 8;
@@ -167,7 +168,27 @@ __device__ __forceinline__ int at_swz(int j, int cc) {   // byte offset of (row 
 // chunk's scores are formed, overlapping the normaliser): half the shared memory per warp, twice
 // the resident warps (six CTAs of 4 warps per SM instead of three), one more round trip per warp.
 // Measured: 630 rows d = 1024 33.8 -> 23.9 us (warm), big job 106.9 -> 102.0 ms.
-template <int DH, bool SHARE>
+// F32 (model option attn_f32, off by default -- it departs from R20's fp64 sums): the same kernel
+// with fp32 dot products (FMA chains in order), expf, normaliser and context sums; measured 7-18 %
+// faster per launch and 5.6 % on the big job (profiles/r2_attn_f32_measure.txt).
+__device__ __forceinline__ float at_fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double at_fma(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float at_exp(float x) { return expf(x); }
+__device__ __forceinline__ double at_exp(double x) { return exp(x); }
+__device__ __forceinline__ float at_wmax(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double at_wmax(double v) { return warp_max_f64(v); }
+__device__ __forceinline__ float at_wsum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double at_wsum(double v) { return warp_sum_f64(v); }
+
+template <int DH, bool SHARE, bool F32 = false>
 __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constant__ CUtensorMap tm,
                                                             AttnArgs a) {
   constexpr int HB = DH / 32;                 // 32-column boxes per head slice
@@ -242,27 +263,28 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
   float4* qv = reinterpret_cast<float4*>(bar + 2);
   if (lane < DH / 4) qv[lane] = *reinterpret_cast<const float4*>(q + 4 * lane);
   __syncwarp();
-  const double inv_sqrt = 1.0 / sqrt((double)DH);
-  double mx = -INFINITY;
+  using T = typename std::conditional<F32, float, double>::type;
+  const T inv_sqrt = (T)(1.0 / sqrt((double)DH));
+  T mx = -INFINITY;
   uint32_t kph = 0, vph = 0;
   for (int c0 = 0; c0 < len; c0 += 32) {
     mbar_wait(&bar[0], kph);
     kph ^= 1;
     const int j = c0 + lane;
     if (j < len) {
-      double dot = 0.0;
+      T dot = 0;
 #pragma unroll
       for (int c = 0; c < DH; c += 4) {
         const float4 k4 = *reinterpret_cast<const float4*>(kt + (c >> 5) * AT_TILE + at_swz(lane, c & 31));
         const float4 q4 = qv[c >> 2];
-        dot = __fma_rn((double)q4.x, (double)k4.x, dot);
-        dot = __fma_rn((double)q4.y, (double)k4.y, dot);
-        dot = __fma_rn((double)q4.z, (double)k4.z, dot);
-        dot = __fma_rn((double)q4.w, (double)k4.w, dot);
+        dot = at_fma((T)q4.x, (T)k4.x, dot);
+        dot = at_fma((T)q4.y, (T)k4.y, dot);
+        dot = at_fma((T)q4.z, (T)k4.z, dot);
+        dot = at_fma((T)q4.w, (T)k4.w, dot);
       }
-      const double s = __dmul_rn(dot, inv_sqrt);
+      const T s = dot * inv_sqrt;
       sc[j] = s;
-      mx = fmax(mx, s);
+      mx = mx > s ? mx : s;
     }
     __syncwarp();
     if (lane == 0 && c0 + 32 < len) load(&bar[0], kt, kc, c0 + 32);
@@ -271,27 +293,27 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
   // it while the normaliser is formed
   if constexpr (SHARE)
     if (lane == 0 && len > 0) load(&bar[1], vt, vc, 0);
-  mx = warp_max_f64(mx);
-  double z = 0.0;
+  mx = at_wmax(mx);
+  T z = 0;
   for (int j = lane; j < len; j += 32) {
-    const double p = exp(__dsub_rn(sc[j], mx));
+    const T p = at_exp((T)sc[j] - mx);
     sc[j] = p;
-    z = __dadd_rn(z, p);
+    z = z + p;
   }
-  z = warp_sum_f64(z);
+  z = at_wsum(z);
   __syncwarp();
-  double acc[HB];
+  T acc[HB];
 #pragma unroll
-  for (int i = 0; i < HB; ++i) acc[i] = 0.0;
+  for (int i = 0; i < HB; ++i) acc[i] = 0;
   for (int c0 = 0; c0 < len; c0 += 32) {
     mbar_wait(&bar[1], vph);
     vph ^= 1;
     const int je = min(32, len - c0);
     for (int jj = 0; jj < je; ++jj) {
-      const double p = sc[c0 + jj];
+      const T p = (T)sc[c0 + jj];
 #pragma unroll
       for (int i = 0; i < HB; ++i)
-        acc[i] = __fma_rn(p, (double)*reinterpret_cast<const float*>(vt + i * AT_TILE + at_swz(jj, lane)), acc[i]);
+        acc[i] = at_fma(p, (T)*reinterpret_cast<const float*>(vt + i * AT_TILE + at_swz(jj, lane)), acc[i]);
     }
     __syncwarp();
     if (lane == 0 && c0 + 32 < len) load(&bar[1], vt, vc, c0 + 32);
@@ -300,7 +322,7 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
 #pragma unroll
   for (int i = 0; i < HB; ++i) {
     const int c = lane + 32 * i;
-    const float ctx = len > 0 ? (float)__ddiv_rn(acc[i], z) : 0.0f;
+    const float ctx = len > 0 ? (float)(acc[i] / z) : 0.0f;
     out[c] = (int8_t)q8(ctx, a.clip, a.sigma);
     if (a.out_f) a.out_f[(int64_t)r * a.d + h * DH + c] = ctx;
   }
@@ -968,6 +990,19 @@ cudaError_t launch_ln(const LnArgs& a, cudaStream_t st) {
     const char* e = getenv("MNMT_LN_SPLIT");
     return !(e && e[0] == '0');
   }();
+  // one float4 per thread (W = d / 128 warps per row): measured 300.7 -> 283.3 us per big decoder
+  // step at 1 row, 413 -> 391 at 64 rows, base-AAN job 50.0 -> 48.7 ms (profiles/r2_ln_nv1.txt);
+  // env MNMT_LN_NV1=0: two float4 per thread (W = d / 256; A/B)
+  static const bool nv1 = [] {
+    const char* e = getenv("MNMT_LN_NV1");
+    return !(e && e[0] == '0');
+  }();
+  if (split && nv1 && (a.d == 512 || a.d == 1024)) {
+    const int W = a.d / 128, rpb = 256 / (32 * W);
+    dim3 grid((a.n + rpb - 1) / rpb), block(256);
+    return W == 4 ? launch_pdl(k_ln_split<4, 1>, grid, block, 0, st, a)
+                  : launch_pdl(k_ln_split<8, 1>, grid, block, 0, st, a);
+  }
   if (split && (a.d == 512 || a.d == 1024)) {
     const int W = a.d / 256, rpb = 256 / (32 * W);
     dim3 grid((a.n + rpb - 1) / rpb), block(256);
@@ -1034,6 +1069,12 @@ cudaError_t attn_init() {   // once per device
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn_tma<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)attn_tma_smem(64, MNMT_MAX_KV, true));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn_tma<64, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)attn_tma_smem(64, MNMT_MAX_KV, true));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_attn_tma<32, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)attn_tma_smem(32, MNMT_MAX_KV, true));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn_tma<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)attn_tma_smem(32, MNMT_MAX_KV, true));
@@ -1149,6 +1190,13 @@ cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
     }();
     const dim3 grid((unsigned)((warps + AT_WARPS - 1) / AT_WARPS)), block(AT_WARPS * 32);
     const size_t smem = attn_tma_smem(b.dh, b.span, share);
+    static const bool f32 = [] {   // env MNMT_ATTN_F32=1: the fp32 variant everywhere (A/B)
+      const char* e = getenv("MNMT_ATTN_F32");
+      return e && e[0] == '1';
+    }();
+    if (share && (f32 || b.f32))
+      return b.dh == 64 ? launch_pdl(k_attn_tma<64, true, true>, grid, block, smem, st, *b.tmap, b)
+                        : launch_pdl(k_attn_tma<32, true, true>, grid, block, smem, st, *b.tmap, b);
     if (share)
       return b.dh == 64 ? launch_pdl(k_attn_tma<64, true>, grid, block, smem, st, *b.tmap, b)
                         : launch_pdl(k_attn_tma<32, true>, grid, block, smem, st, *b.tmap, b);

@@ -85,6 +85,8 @@ struct AttnArgs {
   int64_t kv_row0;
   int tma_self;             // self mode: 0 generic kernels, 1 TMA split kernel for long decodes at
                             // <= 128 rows, 2 also the one-warp TMA kernel (measured per workload)
+  int f32;                  // one-warp TMA kernel in fp32 arithmetic (model option attn_f32; departs
+                            // from R20: ids exact or near-tie-explained, intermediates not within 1e-4)
 };
 
 // Encoder self-attention over Q|K|V rows [M x 3d] (A3), one CTA per (sentence, head).

@@ -56,7 +56,7 @@ EXPORTS = [
     "mnmt_get_stats", "mnmt_last_error", "mnmt_model_destroy", "mnmt_model_set_option",
     "mnmt_op_quantize", "mnmt_op_gemm_i8", "mnmt_op_argmax_ids", "mnmt_op_layernorm",
     "mnmt_op_aan_step", "mnmt_op_embed", "mnmt_op_attention", "mnmt_op_attention_enc", "mnmt_op_attention_bf16",
-    "mnmt_op_gather_rows", "mnmt_op_src_attention", "mnmt_op_gemm_i8_split",
+    "mnmt_op_gather_rows", "mnmt_op_src_attention", "mnmt_op_src_attention_f32", "mnmt_op_gemm_i8_split",
 ]
 
 _lib = None
@@ -102,6 +102,7 @@ def lib():
     L.mnmt_op_gather_rows.argtypes = [P, P, P, P, P, I32, P, P, P]
     L.mnmt_op_gemm_i8_split.argtypes = [P, P, I32, I32, I32, P, F, I32, P, P, I32, I32, P]
     L.mnmt_op_src_attention.argtypes = [P, I64, P, I64, I64, I32, I32, P, P, I32, I32, I32, I32, F, P, P, P]
+    L.mnmt_op_src_attention_f32.argtypes = [P, I64, P, I64, I64, I32, I32, P, P, I32, I32, I32, I32, F, P, P, P]
     for name in EXPORTS:
         fn = getattr(L, name)
         if name not in ("mnmt_config_default", "mnmt_last_error", "mnmt_model_destroy"):
@@ -370,6 +371,14 @@ def op_attention(q_ptr, ldq, kv_ptr, ldkv, k_off, v_off, start_ptr, len_ptr, n, 
                  out_q_ptr, out_f_ptr=None, stream=None) -> None:
     _check(lib().mnmt_op_attention(q_ptr, ldq, kv_ptr, ldkv, k_off, v_off, start_ptr, len_ptr, n,
                                    d, H, clip, out_q_ptr, out_f_ptr, _stream_ptr(stream)))
+
+
+def op_src_attention_f32(q_ptr, ldq, kv_ptr, kv_rows, ldkv, k_off, v_off, start_ptr, len_ptr,
+                         max_span, n, d, H, clip, out_q_ptr, out_f_ptr=None, stream=None) -> None:
+    """A7 through the one-warp TMA kernel in fp32 arithmetic (option attn_f32; departs from R20)."""
+    _check(lib().mnmt_op_src_attention_f32(q_ptr, ldq, kv_ptr, kv_rows, ldkv, k_off, v_off, start_ptr,
+                                           len_ptr, max_span, n, d, H, clip, out_q_ptr, out_f_ptr,
+                                           _stream_ptr(stream)))
 
 
 def op_src_attention(q_ptr, ldq, kv_ptr, kv_rows, ldkv, k_off, v_off, start_ptr, len_ptr,

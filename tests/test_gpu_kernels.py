@@ -497,6 +497,33 @@ def test_src_attention_tma(d, H):
     assert not boundary_explained(ref, O.quantize(ref), oq.cpu().numpy()).any()
 
 
+@pytest.mark.parametrize("d,H,n", [(1024, 16, 630), (512, 8, 300), (256, 4, 200)])
+def test_src_attention_f32_option(d, H, n):
+    """The fp32 variant of the one-warp TMA attention (option attn_f32): context within 4e-6 of the
+    fp64 oracle relative to the row's scale, every code equal to the oracle's or a boundary-explained
+    flip (x * sigma within 1e-4 relative of a rounding midpoint), and the flips rare."""
+    rng = np.random.default_rng(d + n + 3)
+    lens = rng.integers(1, 60, size=n).astype(np.int32)
+    starts = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int32)
+    S = int(lens.sum())
+    kv = rng.normal(0, 1, size=(S, 2 * d)).astype(np.float32)
+    q = rng.normal(0, 1, size=(n, d)).astype(np.float32)
+    oq, of = zeros((n, d), torch.int8), zeros((n, d), torch.float32)
+    M.op_src_attention_f32(ptr(to_dev(q)), d, ptr(to_dev(kv)), S, 2 * d, 0, d, ptr(to_dev(starts)), ptr(to_dev(lens)),
+                           int(lens.max()), n, d, H, CLIP, ptr(oq), ptr(of))
+    sync()
+    ref = np.zeros((n, d), np.float32)
+    for r in range(n):
+        blk = kv[starts[r]:starts[r] + lens[r]]
+        ref[r] = O.attention(q[r], blk[:, :d], blk[:, d:], H)
+    got = of.cpu().numpy()
+    scale = np.maximum(np.abs(ref), np.sqrt(np.mean(ref.astype(np.float64) ** 2, axis=1, keepdims=True)))
+    assert np.max(np.abs(got - ref) / scale) < 4e-6
+    rq, gq = O.quantize(ref), oq.cpu().numpy()
+    assert not boundary_explained(ref, rq, gq, rel=1e-4).any()
+    assert np.mean(gq != rq) < 1e-3
+
+
 # ------------------------------------------------------------------ A11 across GPUs (unshard)
 def test_gather_rows():
     """mnmt_op_gather_rows puts the all-gathered rows of a strong-scaling job back in input order:
