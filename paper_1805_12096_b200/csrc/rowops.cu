@@ -997,10 +997,16 @@ cudaError_t launch_ln(const LnArgs& a, cudaStream_t st) {
     const char* e = getenv("MNMT_LN_NV1");
     return !(e && e[0] == '0');
   }();
-  if (split && nv1 && (a.d == 512 || a.d == 1024)) {
+  // d = 256 (small students) over 2 warps per row: env MNMT_LN_SPLIT256=1 (A/B)
+  static const bool s256 = [] {
+    const char* e = getenv("MNMT_LN_SPLIT256");
+    return e && e[0] == '1';
+  }();
+  if (split && nv1 && (a.d == 512 || a.d == 1024 || (a.d == 256 && s256))) {
     const int W = a.d / 128, rpb = 256 / (32 * W);
     dim3 grid((a.n + rpb - 1) / rpb), block(256);
-    return W == 4 ? launch_pdl(k_ln_split<4, 1>, grid, block, 0, st, a)
+    return W == 2 ? launch_pdl(k_ln_split<2, 1>, grid, block, 0, st, a)
+         : W == 4 ? launch_pdl(k_ln_split<4, 1>, grid, block, 0, st, a)
                   : launch_pdl(k_ln_split<8, 1>, grid, block, 0, st, a);
   }
   if (split && (a.d == 512 || a.d == 1024)) {
