@@ -25,6 +25,7 @@
 
 namespace mnmt {
 __constant__ int c_pdl_early = 1;
+__constant__ int c_attn_kv2 = 1;   // k_attn_tma: K and V of spans <= 16 in flight together
 // Let the next kernel of the chain launch (and run its prologue) right away; its
 // griddepcontrol.wait still waits for this grid to complete (env MNMT_PDL_EARLY=0 disables).
 __device__ __forceinline__ void pdl_trigger_early() {
@@ -188,6 +189,9 @@ __device__ __forceinline__ float at_wsum(float v) {
 }
 __device__ __forceinline__ double at_wsum(double v) { return warp_sum_f64(v); }
 
+// K and V of spans <= 16 in flight together (env MNMT_ATTN_KV2=0 disables; A/B)
+__device__ __forceinline__ bool kv_pair_on() { return c_attn_kv2 != 0; }
+
 template <int DH, bool SHARE, bool F32 = false>
 __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constant__ CUtensorMap tm,
                                                             AttnArgs a) {
@@ -246,16 +250,22 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
   const int row0 = (int)(a.kv_row0 + start);
   const int kc = a.k_off + h * DH, vc = a.v_off + h * DH;
   // chunk c0 (positions c0 .. c0 + 31 of the span): only the 8-row boxes holding positions < len
-  auto load = [&](uint64_t* b, uint8_t* dst, int col, int c0) {
+  // box0: first 8-row box of the destination tile (spans <= 16 put V in boxes 2-3 of K's tile)
+  auto load = [&](uint64_t* b, uint8_t* dst, int col, int c0, int box0 = 0) {
     const int nb = min(4, (len - c0 + 7) >> 3);
     mbar_arrive_expect_tx(b, HB * nb * AT_BOX);
     for (int hb = 0; hb < HB; ++hb)
       for (int x = 0; x < nb; ++x)
-        tma_load_2d(dst + hb * AT_TILE + x * AT_BOX, &tm, b, col + 32 * hb, row0 + c0 + 8 * x);
+        tma_load_2d(dst + hb * AT_TILE + (box0 + x) * AT_BOX, &tm, b, col + 32 * hb, row0 + c0 + 8 * x);
   };
+  // SHARE with a span of <= 16 positions: K fills boxes 0-1 and V boxes 2-3 of the one tile
+  // buffer, so both are in flight at once (no second round trip after the scores)
+  const bool kv2 = SHARE && len <= 16 && kv_pair_on();
+  const int voff = kv2 ? 16 : 0;   // V row offset inside the tile
   if (lane == 0 && len > 0) {
     load(&bar[0], kt, kc, 0);
     if constexpr (!SHARE) load(&bar[1], vt, vc, 0);
+    if (kv2) load(&bar[1], kt, vc, 0, 2);
   }
   const float* q = a.q + (int64_t)r * a.ldq + h * DH;
   // the query staged in shared memory while the tiles are in flight (the dot loop then reads
@@ -292,7 +302,7 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
   // SHARE: every lane has read the K buffer (the __syncwarp above); the first V chunk goes into
   // it while the normaliser is formed
   if constexpr (SHARE)
-    if (lane == 0 && len > 0) load(&bar[1], vt, vc, 0);
+    if (lane == 0 && len > 0 && !kv2) load(&bar[1], vt, vc, 0);
   mx = at_wmax(mx);
   T z = 0;
   for (int j = lane; j < len; j += 32) {
@@ -313,7 +323,7 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
       const T p = (T)sc[c0 + jj];
 #pragma unroll
       for (int i = 0; i < HB; ++i)
-        acc[i] = at_fma(p, (T)*reinterpret_cast<const float*>(vt + i * AT_TILE + at_swz(jj, lane)), acc[i]);
+        acc[i] = at_fma(p, (T)*reinterpret_cast<const float*>(vt + i * AT_TILE + at_swz(jj + voff, lane)), acc[i]);
     }
     __syncwarp();
     if (lane == 0 && c0 + 32 < len) load(&bar[1], vt, vc, c0 + 32);
@@ -997,10 +1007,11 @@ cudaError_t launch_ln(const LnArgs& a, cudaStream_t st) {
     const char* e = getenv("MNMT_LN_NV1");
     return !(e && e[0] == '0');
   }();
-  // d = 256 (small students) over 2 warps per row: env MNMT_LN_SPLIT256=1 (A/B)
+  // d = 256 (small students) over 2 warps per row: small-AAN decoder step 205 -> 180 us at 1 row,
+  // job 37.3-37.6 -> 36.4 ms (profiles/r2_ln_split256.txt); env MNMT_LN_SPLIT256=0 disables (A/B)
   static const bool s256 = [] {
     const char* e = getenv("MNMT_LN_SPLIT256");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   if (split && nv1 && (a.d == 512 || a.d == 1024 || (a.d == 256 && s256))) {
     const int W = a.d / 128, rpb = 256 / (32 * W);
@@ -1114,6 +1125,11 @@ cudaError_t attn_init() {   // once per device
     const char* pe = getenv("MNMT_PDL_EARLY");
     const int v = (pe && pe[0] == '0') ? 0 : 1;
     e = cudaMemcpyToSymbol(c_pdl_early, &v, sizeof v);
+  }
+  if (e == cudaSuccess) {
+    const char* pe = getenv("MNMT_ATTN_KV2");
+    const int v = (pe && pe[0] == '0') ? 0 : 1;
+    e = cudaMemcpyToSymbol(c_attn_kv2, &v, sizeof v);
   }
   if (e == cudaSuccess && dev >= 0 && dev < 64) done[dev] = true;
   return e;
