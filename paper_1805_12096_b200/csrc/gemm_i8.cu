@@ -417,11 +417,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   int32_t* red = reinterpret_cast<int32_t*>(smem + ring * Cfg::STAGE_BYTES + EPI_STAGE_BYTES);
   if (ks > 1) cluster_arrive_relaxed();   // phase 1: this CTA is running (DSMEM valid)
 
-  // a_box > 0: tmA covers only the launch's a.M <= 64 rows with one a_box-row box (the rest of
-  // the A tile stays stale: those accumulator rows are never stored); b_box32: tmB has 32-row
+  // a_box > 0: tmA holds one a_box-row box per K block (a_box < 128: the launch's a.M <= 64 rows;
+  // the rest of the A tile stays stale, those accumulator rows are never stored); b_box > 0: tmB
+  // holds one b_box-row box (BN = 32: 32 rows; else the whole B tile).  Otherwise 64-row boxes.
   // boxes (BN = 32 loads only its own weight rows)
   const int a_bytes = args.a_box > 0 ? args.a_box * BK : Cfg::A_BYTES;
-  const int b_bytes = (BN == 32 && args.b_box32) ? 32 * BK : Cfg::B_BYTES;
+  const int b_bytes = args.b_box > 0 ? args.b_box * BK : Cfg::B_BYTES;
   const int tx_bytes = a_bytes + b_bytes;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -437,7 +438,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int s = 0; s < stages; ++s) {
       mbar_arrive_expect_tx(&full_bar[s], tx_bytes);
       uint8_t* sb = smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES;
-      if (BN == 32 && args.b_box32) {
+      if (args.b_box > 0) {
         tma_load_2d(sb, &tmB, &full_bar[s], (kb0 + s) * BK, n0);
       } else {
 #pragma unroll
@@ -493,7 +494,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         uint8_t* sb = sa + Cfg::A_BYTES;
         mbar_wait(&empty_bar[s], ((kb / stages) - 1) & 1);
         mbar_arrive_expect_tx(&full_bar[s], tx_bytes);
-        if (BN == 32 && args.b_box32) {
+        if (args.b_box > 0) {
           tma_load_2d(sb, &tmB, &full_bar[s], (kb0 + kb) * BK, n0);
         } else {
 #pragma unroll
@@ -1423,6 +1424,15 @@ static bool abox_on() {
   return on;
 }
 
+// One TMA box per operand per K block at any row count (env MNMT_BIGBOX = 1; A/B)
+static bool bigbox_on() {
+  static const bool on = [] {
+    const char* e = getenv("MNMT_BIGBOX");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 template <int BN, int EPI>
 static cudaError_t launch_t(const CUtensorMap& tmA_in, const CUtensorMap& tmB_in, const GemmArgs& a,
                             cudaStream_t st) {
@@ -1439,14 +1449,19 @@ static cudaError_t launch_t(const CUtensorMap& tmA_in, const CUtensorMap& tmB_in
   GemmArgs b = a;
   CUtensorMap tmA = tmA_in, tmB = tmB_in;
   b.a_box = 0;
-  b.b_box32 = 0;
+  b.b_box = 0;
   if (abox_on() && a.a_ptr && a.M <= 64 && a.K % 16 == 0 && a.lda % 16 == 0) {
     const int box = a.M <= 16 ? 16 : a.M <= 32 ? 32 : 64;
     if (make_tmap_rows(&tmA, a.a_ptr, a.M, a.K, a.lda, box)) b.a_box = box;
     else tmA = tmA_in;
+  } else if (bigbox_on() && a.a_ptr && a.K % 16 == 0 && a.lda % 16 == 0) {
+    // one 128-row box per K block (fewer TMA operations per stage)
+    if (make_tmap_rows(&tmA, a.a_ptr, a.M, a.K, a.lda, BM)) b.a_box = BM;
+    else tmA = tmA_in;
   }
-  if (BN == 32 && abox_on() && a.b_ptr) {
-    if (make_tmap_rows(&tmB, a.b_ptr, a.N, a.K, a.K, 32)) b.b_box32 = 1;
+  if (abox_on() && a.b_ptr && (BN == 32 || bigbox_on())) {
+    const int rows = BN == 32 ? 32 : GemmCfg<BN>::B_ROWS;
+    if (make_tmap_rows(&tmB, a.b_ptr, a.N, a.K, a.K, rows)) b.b_box = rows;
     else tmB = tmB_in;
   }
   int ring = kb_per < Cfg::STAGES ? kb_per : Cfg::STAGES;

@@ -25,7 +25,6 @@
 
 namespace mnmt {
 __constant__ int c_pdl_early = 1;
-__constant__ int c_attn_kv2 = 1;   // k_attn_tma: K and V of spans <= 16 in flight together
 // Let the next kernel of the chain launch (and run its prologue) right away; its
 // griddepcontrol.wait still waits for this grid to complete (env MNMT_PDL_EARLY=0 disables).
 __device__ __forceinline__ void pdl_trigger_early() {
@@ -189,9 +188,6 @@ __device__ __forceinline__ float at_wsum(float v) {
 }
 __device__ __forceinline__ double at_wsum(double v) { return warp_sum_f64(v); }
 
-// K and V of spans <= 16 in flight together (env MNMT_ATTN_KV2=0 disables; A/B)
-__device__ __forceinline__ bool kv_pair_on() { return c_attn_kv2 != 0; }
-
 template <int DH, bool SHARE, bool F32 = false>
 __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constant__ CUtensorMap tm,
                                                             AttnArgs a) {
@@ -250,22 +246,16 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
   const int row0 = (int)(a.kv_row0 + start);
   const int kc = a.k_off + h * DH, vc = a.v_off + h * DH;
   // chunk c0 (positions c0 .. c0 + 31 of the span): only the 8-row boxes holding positions < len
-  // box0: first 8-row box of the destination tile (spans <= 16 put V in boxes 2-3 of K's tile)
-  auto load = [&](uint64_t* b, uint8_t* dst, int col, int c0, int box0 = 0) {
+  auto load = [&](uint64_t* b, uint8_t* dst, int col, int c0) {
     const int nb = min(4, (len - c0 + 7) >> 3);
     mbar_arrive_expect_tx(b, HB * nb * AT_BOX);
     for (int hb = 0; hb < HB; ++hb)
       for (int x = 0; x < nb; ++x)
-        tma_load_2d(dst + hb * AT_TILE + (box0 + x) * AT_BOX, &tm, b, col + 32 * hb, row0 + c0 + 8 * x);
+        tma_load_2d(dst + hb * AT_TILE + x * AT_BOX, &tm, b, col + 32 * hb, row0 + c0 + 8 * x);
   };
-  // SHARE with a span of <= 16 positions: K fills boxes 0-1 and V boxes 2-3 of the one tile
-  // buffer, so both are in flight at once (no second round trip after the scores)
-  const bool kv2 = SHARE && len <= 16 && kv_pair_on();
-  const int voff = kv2 ? 16 : 0;   // V row offset inside the tile
   if (lane == 0 && len > 0) {
     load(&bar[0], kt, kc, 0);
     if constexpr (!SHARE) load(&bar[1], vt, vc, 0);
-    if (kv2) load(&bar[1], kt, vc, 0, 2);
   }
   const float* q = a.q + (int64_t)r * a.ldq + h * DH;
   // the query staged in shared memory while the tiles are in flight (the dot loop then reads
@@ -302,7 +292,7 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
   // SHARE: every lane has read the K buffer (the __syncwarp above); the first V chunk goes into
   // it while the normaliser is formed
   if constexpr (SHARE)
-    if (lane == 0 && len > 0 && !kv2) load(&bar[1], vt, vc, 0);
+    if (lane == 0 && len > 0) load(&bar[1], vt, vc, 0);
   mx = at_wmax(mx);
   T z = 0;
   for (int j = lane; j < len; j += 32) {
@@ -323,7 +313,7 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
       const T p = (T)sc[c0 + jj];
 #pragma unroll
       for (int i = 0; i < HB; ++i)
-        acc[i] = at_fma(p, (T)*reinterpret_cast<const float*>(vt + i * AT_TILE + at_swz(jj + voff, lane)), acc[i]);
+        acc[i] = at_fma(p, (T)*reinterpret_cast<const float*>(vt + i * AT_TILE + at_swz(jj, lane)), acc[i]);
     }
     __syncwarp();
     if (lane == 0 && c0 + 32 < len) load(&bar[1], vt, vc, c0 + 32);
@@ -1125,11 +1115,6 @@ cudaError_t attn_init() {   // once per device
     const char* pe = getenv("MNMT_PDL_EARLY");
     const int v = (pe && pe[0] == '0') ? 0 : 1;
     e = cudaMemcpyToSymbol(c_pdl_early, &v, sizeof v);
-  }
-  if (e == cudaSuccess) {
-    const char* pe = getenv("MNMT_ATTN_KV2");
-    const int v = (pe && pe[0] == '0') ? 0 : 1;
-    e = cudaMemcpyToSymbol(c_attn_kv2, &v, sizeof v);
   }
   if (e == cudaSuccess && dev >= 0 && dev < 64) done[dev] = true;
   return e;
