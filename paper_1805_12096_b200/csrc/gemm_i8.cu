@@ -1424,15 +1424,6 @@ static bool abox_on() {
   return on;
 }
 
-// One TMA box per operand per K block at any row count (env MNMT_BIGBOX = 1; A/B)
-static bool bigbox_on() {
-  static const bool on = [] {
-    const char* e = getenv("MNMT_BIGBOX");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
 template <int BN, int EPI>
 static cudaError_t launch_t(const CUtensorMap& tmA_in, const CUtensorMap& tmB_in, const GemmArgs& a,
                             cudaStream_t st) {
@@ -1454,14 +1445,9 @@ static cudaError_t launch_t(const CUtensorMap& tmA_in, const CUtensorMap& tmB_in
     const int box = a.M <= 16 ? 16 : a.M <= 32 ? 32 : 64;
     if (make_tmap_rows(&tmA, a.a_ptr, a.M, a.K, a.lda, box)) b.a_box = box;
     else tmA = tmA_in;
-  } else if (bigbox_on() && a.a_ptr && a.K % 16 == 0 && a.lda % 16 == 0) {
-    // one 128-row box per K block (fewer TMA operations per stage)
-    if (make_tmap_rows(&tmA, a.a_ptr, a.M, a.K, a.lda, BM)) b.a_box = BM;
-    else tmA = tmA_in;
   }
-  if (abox_on() && a.b_ptr && (BN == 32 || bigbox_on())) {
-    const int rows = BN == 32 ? 32 : GemmCfg<BN>::B_ROWS;
-    if (make_tmap_rows(&tmB, a.b_ptr, a.N, a.K, a.K, rows)) b.b_box = rows;
+  if (abox_on() && a.b_ptr && BN == 32) {
+    if (make_tmap_rows(&tmB, a.b_ptr, a.N, a.K, a.K, 32)) b.b_box = 32;
     else tmB = tmB_in;
   }
   int ring = kb_per < Cfg::STAGES ? kb_per : Cfg::STAGES;
