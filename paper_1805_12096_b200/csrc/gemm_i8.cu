@@ -512,18 +512,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       cluster_wait();
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer (single thread)
-      constexpr uint32_t idesc = idesc_i8<BM, BN>();
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % stages;
-        mbar_wait(&full_bar[s], (kb / stages) & 1);
-        if (kb == 0) GEMM_TRACE(2);
-        tc_fence_after();
-        const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
-        const uint32_t sb = sa + Cfg::A_BYTES;
-        const uint64_t adesc = umma_desc_sw128(sa);
-        const uint64_t bdesc = umma_desc_sw128(sb);
+    // ---------------- MMA issuer: the whole warp walks the K blocks (warp-uniform, so the
+    // descriptors live in uniform registers), one elected lane issues the MMAs and their commits
+    // (measured: 100-107 -> 72-82 cycles per tcgen05.mma with the per-K-block bookkeeping,
+    // profiles/r2_mma_issue_bench.txt; small-N MMAs are issue-bound)
+    constexpr uint32_t idesc = idesc_i8<BM, BN>();
+    for (int kb = 0; kb < num_kb; ++kb) {
+      const int s = kb % stages;
+      mbar_wait(&full_bar[s], (kb / stages) & 1);
+      if (kb == 0 && lane == 0) GEMM_TRACE(2);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
+      const uint32_t sb = sa + Cfg::A_BYTES;
+      const uint64_t adesc = umma_desc_sw128(sa);
+      const uint64_t bdesc = umma_desc_sw128(sb);
+      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < BK / 32; ++k) {
           // advance the start address by k * 32 bytes (encoded >> 4) inside the swizzle atom
@@ -532,8 +535,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         mma_commit(&empty_bar[s]);  // smem stage free once these MMAs have read it
       }
-      mma_commit(&tmem_full_bar);   // accumulator complete
+      __syncwarp();
     }
+    if (elect_one()) mma_commit(&tmem_full_bar);   // accumulator complete
     __syncwarp();
     if (ks > 1) {
       cluster_wait();
@@ -714,29 +718,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_i8<BM, BN>();
-      uint32_t cs = 0, cph = 0, ab = 0, aph = 0;
-      for (int t = blockIdx.x; t < T; t += gridDim.x) {
-        mbar_wait(&tempty_bar[ab], aph ^ 1);
+    // MMA issuer: warp-uniform loop, one elected lane issues (as in k_gemm_i8)
+    constexpr uint32_t idesc = idesc_i8<BM, BN>();
+    uint32_t cs = 0, cph = 0, ab = 0, aph = 0;
+    for (int t = blockIdx.x; t < T; t += gridDim.x) {
+      mbar_wait(&tempty_bar[ab], aph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + ab * BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full_bar[cs], cph);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + ab * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&full_bar[cs], cph);
-          tc_fence_after();
-          const uint32_t sa = smem_u32(smem + cs * Cfg::STAGE_BYTES);
-          const uint64_t adesc = umma_desc_sw128(sa);
-          const uint64_t bdesc = umma_desc_sw128(sa + Cfg::A_BYTES);
+        const uint32_t sa = smem_u32(smem + cs * Cfg::STAGE_BYTES);
+        const uint64_t adesc = umma_desc_sw128(sa);
+        const uint64_t bdesc = umma_desc_sw128(sa + Cfg::A_BYTES);
+        if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < BK / 32; ++k)
             mma_i8(d_tmem, adesc + (uint64_t)(2 * k), bdesc + (uint64_t)(2 * k), idesc, (kb | k) != 0);
           mma_commit(&empty_bar[cs]);
-          if (++cs == STAGES) { cs = 0; cph ^= 1; }
         }
-        mma_commit(&tfull_bar[ab]);
-        ab ^= 1;
-        if (ab == 0) aph ^= 1;
+        __syncwarp();
+        if (++cs == STAGES) { cs = 0; cph ^= 1; }
       }
+      if (elect_one()) mma_commit(&tfull_bar[ab]);
+      __syncwarp();
+      ab ^= 1;
+      if (ab == 0) aph ^= 1;
     }
   } else {
     const int q = warp & 3, half = (warp - 2) >> 2;
@@ -875,8 +882,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
-      // ---------------- MMA issuer (leader): 256 x 256 x 32 per instruction for the pair
+    if (rank == 0) {
+      // ---------------- MMA issuer (leader's warp 1, warp-uniform; one elected lane issues):
+      // 256 x 256 x 32 per instruction for the pair
       constexpr uint32_t idesc = idesc_i8<2 * BM, P2_BN>();
       uint32_t cs = 0, cph = 0, ab = 0, aph = 0;
       for (int t = pair; t < T; t += npairs) {
@@ -889,13 +897,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const uint32_t sa = smem_u32(smem + cs * Cfg::STAGE_BYTES);
           const uint64_t adesc = umma_desc_sw128(sa);
           const uint64_t bdesc = umma_desc_sw128(sa + Cfg::A_BYTES);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 32; ++k)
-            mma_i8_pair(d_tmem, adesc + (uint64_t)(2 * k), bdesc + (uint64_t)(2 * k), idesc, (kb | k) != 0);
-          mma_commit_pair(&empty_bar[cs], 0x3);
+            for (int k = 0; k < BK / 32; ++k)
+              mma_i8_pair(d_tmem, adesc + (uint64_t)(2 * k), bdesc + (uint64_t)(2 * k), idesc, (kb | k) != 0);
+            mma_commit_pair(&empty_bar[cs], 0x3);
+          }
+          __syncwarp();
           if (++cs == STAGES) { cs = 0; cph ^= 1; }
         }
-        mma_commit_pair(&tfull_bar[ab], 0x3);
+        if (elect_one()) mma_commit_pair(&tfull_bar[ab], 0x3);
+        __syncwarp();
         ab ^= 1;
         if (ab == 0) aph ^= 1;
       }
@@ -1066,24 +1078,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       cluster_wait();
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer: D^T[128 x MP] (+)= W[128 x 32] . A[MP x 32]^T per step
-      constexpr uint32_t idesc = idesc_i8<BM, MP>();
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % stages;
-        mbar_wait(&full_bar[s], (kb / stages) & 1);
-        if (kb == 0) GEMM_TRACE(2);
-        tc_fence_after();
-        const uint32_t sw = smem_u32(smem + s * Cfg::STAGE_BYTES);
-        const uint64_t wdesc = umma_desc_sw128(sw);
-        const uint64_t adesc = umma_desc_sw128(sw + Cfg::W_BYTES);
+    // ---------------- MMA issuer (warp-uniform, one elected lane issues):
+    // D^T[128 x MP] (+)= W[128 x 32] . A[MP x 32]^T per step
+    constexpr uint32_t idesc = idesc_i8<BM, MP>();
+    for (int kb = 0; kb < num_kb; ++kb) {
+      const int s = kb % stages;
+      mbar_wait(&full_bar[s], (kb / stages) & 1);
+      if (kb == 0 && lane == 0) GEMM_TRACE(2);
+      tc_fence_after();
+      const uint32_t sw = smem_u32(smem + s * Cfg::STAGE_BYTES);
+      const uint64_t wdesc = umma_desc_sw128(sw);
+      const uint64_t adesc = umma_desc_sw128(sw + Cfg::W_BYTES);
+      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < BK / 32; ++k)
           mma_i8(tmem_base, wdesc + (uint64_t)(2 * k), adesc + (uint64_t)(2 * k), idesc, (kb | k) != 0);
         mma_commit(&empty_bar[s]);
       }
-      mma_commit(&tmem_full_bar);
+      __syncwarp();
     }
+    if (elect_one()) mma_commit(&tmem_full_bar);
     __syncwarp();
     if (ks > 1) {
       cluster_wait();
