@@ -1310,7 +1310,10 @@ bool gemm_persistent(int M, int N, int bn, int sms) {
   }();
   if (force >= 0) return force == 1;
   const long tiles = (long)((M + BM - 1) / BM) * ((N + bn - 1) / bn);
-  return tiles > 2L * (sms > 0 ? sms : num_sms());
+  // also every launch with more than 64 rows: the persistent kernel is 0.3-4 us faster per launch
+  // at 128-630 rows even with one tile per CTA (d x d 4.84 -> 4.03 us at 128 rows, FFN1 11.2 ->
+  // 7.1 at 630, FFN2 9.8 -> 7.4 at 128; big job 83.4 -> 81.3 ms, profiles/r2_gemm_persistent_ab.txt)
+  return tiles > 2L * (sms > 0 ? sms : num_sms()) || M > 64;
 }
 
 int gemm_pick_bn(int M, int N, int sms) {
@@ -1464,7 +1467,7 @@ template <int BN, int EPI>
 static cudaError_t launch_t(const CUtensorMap& tmA_in, const CUtensorMap& tmB_in, const GemmArgs& a,
                             cudaStream_t st) {
   if constexpr (BN >= 64)   // BN = 32 (16-column epilogue chunks) is never persistent
-    if (gemm_persistent(a.M, a.N, BN, a.pers_grid)) {
+    if (gemm_persistent(a.M, a.N, BN, a.pers_grid) && gemm_split_k(a, BN, EPI) == 1) {
       if (BN == 256 && pers2_take(a))
         return launch_pers2_t<EPI>(tmA_in, tmB_in, a, st);
       return launch_pers_t<BN, EPI>(tmA_in, tmB_in, a, st);
