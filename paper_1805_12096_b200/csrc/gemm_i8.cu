@@ -457,6 +457,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (args.bias && warp >= 2)
     for (int i = (int)threadIdx.x - 64; i < BN; i += 32 * EPI_WARPS)
       bias_s[i] = n0 + i < args.N ? __ldg(args.bias + n0 + i) : 0.0f;
+  if (args.npsync) {   // the CTA barrier before the PDL wait (as the persistent kernel; A/B)
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
   pdl_wait();   // everything below may read the previous kernel's outputs
   if (threadIdx.x == 0) GEMM_TRACE(1);
   // The A tiles of the first ring stages are requested right away, in parallel with the
@@ -492,10 +498,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     return;
   }
 
-  __syncwarp();   // (compute-sanitizer synccheck: divergent warp 0 at the barrier otherwise)
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
+  if (!args.npsync) {
+    __syncwarp();   // (compute-sanitizer synccheck: divergent warp 0 at the barrier otherwise)
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
   const uint32_t tmem_base = tmem_slot;
 
   if (warp == 0) {
@@ -1058,18 +1066,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       bias_s[i] = n0 + i < args.N ? __ldg(args.bias + n0 + i) : 0.0f;
   if constexpr (EPI == EPI_ARGMAX)
     if (warp >= 2 && (int)threadIdx.x - 64 < MP) amax_s[threadIdx.x - 64] = 0ull;
+  // the CTA barrier before the PDL wait (measured faster than after it, as in k_gemm_i8)
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_slot;
   pdl_wait();
   if (threadIdx.x == 0) GEMM_TRACE(1);
   if (warp == 0 && lane == 0)
     for (int s = 0; s < stages; ++s)
       tma_load_2d(smem + s * Cfg::STAGE_BYTES + Cfg::W_BYTES, &tmA, &full_bar[s], (kb0 + s) * BK, 0);
   const int M_live = args.M_dyn ? min(args.M, *args.M_dyn) : args.M;
-
-  __syncwarp();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1454,6 +1462,17 @@ static bool abox_on() {
   return on;
 }
 
+// The one-shot kernel's CTA barrier before the PDL wait instead of after it (the persistent
+// kernel's order): d x d 4.21 -> 3.90 us at 8 rows, 4.84 -> 4.37 at 128, FFN2 (K 4096) 9.0 -> 8.8
+// (profiles/r2_gemm_npsync_ab.txt).  env MNMT_NPSYNC = 0 restores the old order (A/B).
+static int gemm_npsync() {
+  static const int v = [] {
+    const char* e = getenv("MNMT_NPSYNC");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 // Weight stages requested before the PDL wait (env MNMT_BPRE: -1 all, n the first n; A/B)
 static int gemm_bpre() {
   static const int v = [] {
@@ -1478,6 +1497,7 @@ static cudaError_t launch_t(const CUtensorMap& tmA_in, const CUtensorMap& tmB_in
   const int num_kb = (a.K + BK - 1) / BK, kb_per = (num_kb + ks - 1) / ks;
   GemmArgs b = a;
   b.bpre = gemm_bpre();
+  b.npsync = gemm_npsync();
   CUtensorMap tmA = tmA_in, tmB = tmB_in;
   b.a_box = 0;
   b.b_box = 0;
@@ -1622,6 +1642,7 @@ static cudaError_t launch_np(const CUtensorMap& tmA, const CUtensorMap& tmB, con
   cfg.numAttrs = 1;
   GemmArgs b = a;
   b.bpre = gemm_bpre();
+  b.npsync = gemm_npsync();
   return cudaLaunchKernelEx(&cfg, k_gemm_i8<BN, EPI>, tmA, tmB, b);
 }
 
@@ -1657,8 +1678,8 @@ __global__ void __launch_bounds__(256) k_gemm_smallm(const GemmArgs args) {
     const int n = nbase + cw * CPW + c;
     b[c] = (args.bias && seg == 0 && n < args.N) ? __ldg(args.bias + n) : 0.0f;
   }
+  __syncthreads();   // weights staged (the barrier before the PDL wait, as in k_gemm_i8)
   pdl_wait();
-  __syncthreads();   // weights staged
   const int n_live = args.M_dyn ? min(args.M, *args.M_dyn) : args.M;
   const bool row_ok = lane < n_live;
   int32_t acc[CPW];
