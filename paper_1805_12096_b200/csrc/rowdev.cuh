@@ -154,8 +154,11 @@ __device__ __forceinline__ void ln_row(const LnArgs a, int r, const float* vsm =
 // partial sums (its elements in order), warp tree, then the W warp partials combined in warp
 // order through shared memory (red: [rows per block][W] doubles).  Same arithmetic as ln_row
 // (R20: fp64 sums in another order, one rounding to fp32).
+// gamma / beta of the thread's NV float4 columns, loaded by the caller before the PDL wait
+// (model constants), or null (loaded at the output stage)
 template <int W, int NV = 2>
-__device__ __forceinline__ void ln_row_split(const LnArgs a, int r, double* red, bool store) {
+__device__ __forceinline__ void ln_row_split(const LnArgs a, int r, double* red, bool store,
+                                             const float4* gpre = nullptr, const float4* bpre = nullptr) {
   // NV float4 columns per thread: d = 128 W NV (NV = 2: 8 elements per thread; NV = 1: 4)
   const int tid = threadIdx.x % (32 * W), wr = tid >> 5, lane = threadIdx.x & 31;
   const int d = a.d;
@@ -217,7 +220,7 @@ __device__ __forceinline__ void ln_row_split(const LnArgs a, int r, double* red,
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int c = 4 * (tid + 32 * W * i);
-    const float4 g = ld4(a.gamma + c), b = ld4(a.beta + c);
+    const float4 g = gpre ? gpre[i] : ld4(a.gamma + c), b = bpre ? bpre[i] : ld4(a.beta + c);
     float4 o;
     o.x = (float)__dadd_rn(__dmul_rn(__dmul_rn(__dsub_rn((double)v[i].x, mu), inv), (double)g.x), (double)b.x);
     o.y = (float)__dadd_rn(__dmul_rn(__dmul_rn(__dsub_rn((double)v[i].y, mu), inv), (double)g.y), (double)b.y);

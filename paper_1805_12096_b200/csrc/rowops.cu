@@ -116,6 +116,15 @@ __global__ void k_ln(LnArgs a) {
 template <int W, int NV = 2>
 __global__ void __launch_bounds__(256) k_ln_split(LnArgs a) {
   __shared__ double red[256 / 32];
+  // gamma / beta are model constants: loaded before the PDL wait (off the dependent chain)
+  const int tid = threadIdx.x % (32 * W);
+  float4 g[NV], b[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = 4 * (tid + 32 * W * i);
+    g[i] = ld4(a.gamma + c);
+    b[i] = ld4(a.beta + c);
+  }
   pdl_wait();
   pdl_trigger_early();
   constexpr int RPB = 256 / (32 * W);
@@ -123,7 +132,7 @@ __global__ void __launch_bounds__(256) k_ln_split(LnArgs a) {
   const int r = blockIdx.x * RPB + rb;
   // rows past the static bound compute a clamped row (every thread reaches every barrier)
   // and store nothing
-  ln_row_split<W, NV>(a, min(r, a.n - 1), red + rb * W, r < a.n);
+  ln_row_split<W, NV>(a, min(r, a.n - 1), red + rb * W, r < a.n, g, b);
 }
 
 constexpr int ATTN_WARPS = 8;
