@@ -165,7 +165,8 @@ __global__ void __launch_bounds__(ATTN_WARPS * 32) k_attn(AttnArgs a) {
 // ncu, long-scoreboard stalls at 45 % occupancy).  The swizzle makes both access patterns
 // conflict-free: lane = position reading 16-byte column groups of its row (scores), lane =
 // column reading one row (context).  Arithmetic and order are warp_attend's (identical outputs).
-constexpr int AT_WARPS = 4;
+constexpr int AT_WARPS = 4;       // warps per CTA of the one-warp TMA kernels (default)
+constexpr int AT_WARPS_MAX = 8;
 constexpr int AT_TILE = 32 * 128;   // one 32-position chunk of 32 floats (four 8-row boxes)
 constexpr int AT_BOX = 8 * 128;     // one TMA box: 8 rows x 32 floats = one 128B-swizzle atom
 
@@ -198,7 +199,7 @@ __device__ __forceinline__ float at_wsum(float v) {
 __device__ __forceinline__ double at_wsum(double v) { return warp_sum_f64(v); }
 
 template <int DH, bool SHARE, bool F32 = false>
-__global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constant__ CUtensorMap tm,
+__global__ void __launch_bounds__(AT_WARPS_MAX * 32) k_attn_tma(const __grid_constant__ CUtensorMap tm,
                                                             AttnArgs a) {
   constexpr int HB = DH / 32;                 // 32-column boxes per head slice
   constexpr int WB = (SHARE ? 1 : 2) * HB * AT_TILE;   // this warp's K (and V) tiles
@@ -207,9 +208,10 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* kt = base + wi * WB;
   uint8_t* vt = SHARE ? kt : kt + HB * AT_TILE;
-  double* sc = reinterpret_cast<double*>(base + AT_WARPS * WB) + (size_t)wi * a.span;
+  const int nw = blockDim.x >> 5;   // warps per CTA (AT_WARPS, or the launch's choice)
+  double* sc = reinterpret_cast<double*>(base + nw * WB) + (size_t)wi * a.span;
   // per warp: two mbarriers, then its query (DH floats)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(base + AT_WARPS * WB + (size_t)AT_WARPS * a.span * 8) +
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + nw * WB + (size_t)nw * a.span * 8) +
                   (2 + DH / 2) * wi;
   if (lane == 0) {
     mbar_init(&bar[0], 1);
@@ -220,7 +222,7 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
   __syncwarp();
   pdl_wait();
   pdl_trigger_early();
-  const int64_t gw = (int64_t)blockIdx.x * AT_WARPS + wi;
+  const int64_t gw = (int64_t)blockIdx.x * nw + wi;
   const int r = (int)(gw / a.H), h = (int)(gw - (int64_t)r * a.H);
   if (r >= a.n) return;
   const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
@@ -337,9 +339,9 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attn_tma(const __grid_constan
   }
 }
 
-inline size_t attn_tma_smem(int dh, int span, bool share) {
-  return 1024 + (size_t)AT_WARPS * ((share ? 1 : 2) * (dh / 32) * AT_TILE + (size_t)span * 8 + 16 +
-                                    (size_t)dh * 4);
+inline size_t attn_tma_smem(int dh, int span, bool share, int nw = AT_WARPS) {
+  return 1024 + (size_t)nw * ((share ? 1 : 2) * (dh / 32) * AT_TILE + (size_t)span * 8 + 16 +
+                              (size_t)dh * 4);
 }
 
 // Long spans at small row counts, split over NS warps per (row, head) with TMA tiles (A7 and the
@@ -1078,22 +1080,22 @@ cudaError_t attn_init() {   // once per device
                              ATTN_WARPS * (MNMT_MAX_KV + 64) * (int)sizeof(double));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn_tma<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)attn_tma_smem(64, MNMT_MAX_KV, false));
+                             (int)attn_tma_smem(64, MNMT_MAX_KV, false, AT_WARPS_MAX));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn_tma<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)attn_tma_smem(32, MNMT_MAX_KV, false));
+                             (int)attn_tma_smem(32, MNMT_MAX_KV, false, AT_WARPS_MAX));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn_tma<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)attn_tma_smem(64, MNMT_MAX_KV, true));
+                             (int)attn_tma_smem(64, MNMT_MAX_KV, true, AT_WARPS_MAX));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn_tma<64, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)attn_tma_smem(64, MNMT_MAX_KV, true));
+                             (int)attn_tma_smem(64, MNMT_MAX_KV, true, AT_WARPS_MAX));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn_tma<32, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)attn_tma_smem(32, MNMT_MAX_KV, true));
+                             (int)attn_tma_smem(32, MNMT_MAX_KV, true, AT_WARPS_MAX));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn_tma<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)attn_tma_smem(32, MNMT_MAX_KV, true));
+                             (int)attn_tma_smem(32, MNMT_MAX_KV, true, AT_WARPS_MAX));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_attn_split_tma<4, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)attn_split_tma_smem(4, 64, MNMT_MAX_KV));
@@ -1204,8 +1206,13 @@ cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
       const char* e = getenv("MNMT_ATTN_SHARE");
       return !(e && e[0] == '0');
     }();
-    const dim3 grid((unsigned)((warps + AT_WARPS - 1) / AT_WARPS)), block(AT_WARPS * 32);
-    const size_t smem = attn_tma_smem(b.dh, b.span, share);
+    static const int atw = [] {   // warps per CTA (env MNMT_AT_WARPS = 2 / 4 / 8; A/B)
+      const char* e = getenv("MNMT_AT_WARPS");
+      const int v = e ? atoi(e) : AT_WARPS;
+      return (v == 2 || v == 8) ? v : AT_WARPS;
+    }();
+    const dim3 grid((unsigned)((warps + atw - 1) / atw)), block(atw * 32);
+    const size_t smem = attn_tma_smem(b.dh, b.span, share, atw);
     static const bool f32 = [] {   // env MNMT_ATTN_F32=1: the fp32 variant everywhere (A/B)
       const char* e = getenv("MNMT_ATTN_F32");
       return e && e[0] == '1';

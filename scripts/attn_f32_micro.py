@@ -18,7 +18,7 @@ def t(fn, iters=40):
     a.record(); g.replay(); b.record(); b.synchronize(); return 1000 * a.elapsed_time(b) / iters
 
 
-for rows, S in ((630, 21), (2048, 15), (632, 48), (128, 60), (630, 12), (2048, 8), (256, 16)):
+for rows, S in ((630, 21), (2048, 15), (632, 48), (128, 60), (630, 12), (2048, 8), (256, 16), (32, 80)):
     L = np.full(rows, S, np.int32); st = (np.arange(rows) * S).astype(np.int32)
     copies = max(1, min(8, int(np.ceil(160e6 / (rows * S * 8 * d)))))
     kvs = [torch.randn(rows * S, 2 * d, device=dev) for _ in range(copies)]
@@ -28,4 +28,4 @@ for rows, S in ((630, 21), (2048, 15), (632, 48), (128, 60), (630, 12), (2048, 8
     us = t(lambda s_, i: M.op_src_attention(q.data_ptr(), d, kvs[i % copies].data_ptr(), rows * S, 2 * d, 0, d,
                                             Sd.data_ptr(), Ld.data_ptr(), S, rows, d, H, 2.0, oq.data_ptr(), None, s_))
     gbs = rows * S * 2 * d * 4 / (us * 1e-6) / 1e9
-    print(f"{'fp32' if os.environ.get('MNMT_ATTN_F32') == '1' else 'fp64'} kv2={os.environ.get('MNMT_ATTN_KV2', '1')} rows {rows:5d} S {S:3d}: {us:7.2f} us ({gbs:6.0f} GB/s)", flush=True)
+    print(f"{'fp32' if os.environ.get('MNMT_ATTN_F32') == '1' else 'fp64'} warps={os.environ.get('MNMT_AT_WARPS', '4')} rows {rows:5d} S {S:3d}: {us:7.2f} us ({gbs:6.0f} GB/s)", flush=True)
