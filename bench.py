@@ -56,19 +56,21 @@ DEFAULT_WORKLOAD = "big-newstest-8192w"   # BASELINE.json configs[3]: the metric
 # 91.5 -> 90.8 ms per job in round 2 (profiles/r2_sweep_big_options.txt)).
 # sab: row bound of the swap-AB tcgen05 GEMM (weights as the 128-row MMA operand, live rows as
 # N = 16 / 32 / 64; profiles/r2_sab_enc_ab.txt): big 88.9-89.5 -> 86.3-87.4 ms per job with sab 64
-# and the IDP4A path off; the smaller students neutral (off).
+# and the IDP4A path off.  Every workload now runs its small-row decoder GEMMs on the tensor cores
+# (sab, smallm 0): on the final build the IDP4A path is within 0.2-0.4 % of it for the AAN students
+# (profiles/r2_tensor_core_small_rows.txt), and these products are dense contractions.
 # attn_tma_self: self-attention decoders through the TMA-tiled kernels (profiles/r2_attn_tma_ab.txt,
 # after the V tiles started reusing the K buffers: big 99.1-99.4 / 100.1-100.2 / 97.7-97.8 ms per
 # job for 0 / 1 / 2, base self-attention 59.9 / 59.2 / 56.4 ms): 2.
 WORKLOAD_OPTS = {
-    "small-aan-newstest-8192w": {"lanes": 3, "green_sms": 48, "lane_tiers": 40, "smallm": 32, "smallm_kmax": 2048,
-                                 "attn_tma_self": 2},
+    "small-aan-newstest-8192w": {"lanes": 3, "green_sms": 48, "lane_tiers": 40, "smallm": 0, "smallm_kmax": 2048,
+                                 "attn_tma_self": 2, "sab": 32},
     "tiny192-aan-newstest-8192w": {"lanes": 3, "green_sms": 56, "lane_tiers": 40, "smallm": 0, "smallm_kmax": 512,
-                                   "attn_tma_self": 2},
+                                   "attn_tma_self": 2, "sab": 32},
     "base-newstest-8192w": {"lanes": 3, "green_sms": 24, "lane_tiers": 40, "smallm": 0, "smallm_kmax": 512,
-                            "attn_tma_self": 2},
-    "base-aan-newstest-8192w": {"lanes": 3, "green_sms": 40, "lane_tiers": 35, "smallm": 32, "smallm_kmax": 512,
-                                "attn_tma_self": 2},
+                            "attn_tma_self": 2, "sab": 32},
+    "base-aan-newstest-8192w": {"lanes": 3, "green_sms": 40, "lane_tiers": 35, "smallm": 0, "smallm_kmax": 512,
+                                "attn_tma_self": 2, "sab": 32},
     "big-newstest-8192w": {"lanes": 2, "green_sms": 0, "lane_tiers": 15, "smallm": 0, "smallm_kmax": 1024,
                            "attn_tma_self": 2, "sab": 64},
 }

@@ -424,8 +424,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int a_bytes = args.a_box > 0 ? args.a_box * BK : Cfg::A_BYTES;
   const int b_bytes = args.b_box > 0 ? args.b_box * BK : Cfg::B_BYTES;
   const int tx_bytes = a_bytes + b_bytes;
-  // stages whose weight tile is requested before the PDL wait (GemmArgs::bpre: -1 all)
-  const int bpre = args.bpre < 0 ? stages : min(args.bpre, stages);
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -435,9 +433,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     mbar_init(&tmem_full_bar, 1);
     fence_barrier_init();
-    // Weights are constant for the life of the model: fetch the first bpre stages' B tiles
+    // Weights are constant for the life of the model: fetch the first stages' B tiles
     // before waiting on the previous kernel (programmatic dependent launch).
-    for (int s = 0; s < bpre; ++s) {
+    for (int s = 0; s < stages; ++s) {
       mbar_arrive_expect_tx(&full_bar[s], tx_bytes);
       uint8_t* sb = smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES;
       if (args.b_box > 0) {
@@ -470,17 +468,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
       uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
-      if (s >= bpre) {   // this stage's B after the wait, in stage order with its A
-        mbar_arrive_expect_tx(&full_bar[s], tx_bytes);
-        uint8_t* sb = sa + Cfg::A_BYTES;
-        if (args.b_box > 0) {
-          tma_load_2d(sb, &tmB, &full_bar[s], (kb0 + s) * BK, n0);
-        } else {
-#pragma unroll
-          for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
-            tma_load_2d(sb + j * 64 * BK, &tmB, &full_bar[s], (kb0 + s) * BK, n0 + j * 64);
-        }
-      }
       tma_load_2d(sa, &tmA, &full_bar[s], (kb0 + s) * BK, m0);
       if (args.a_box == 0) tma_load_2d(sa + 64 * BK, &tmA, &full_bar[s], (kb0 + s) * BK, m0 + 64);
     }
@@ -1473,15 +1460,6 @@ static int gemm_npsync() {
   return v;
 }
 
-// Weight stages requested before the PDL wait (env MNMT_BPRE: -1 all, n the first n; A/B)
-static int gemm_bpre() {
-  static const int v = [] {
-    const char* e = getenv("MNMT_BPRE");
-    return e ? atoi(e) : -1;
-  }();
-  return v;
-}
-
 template <int BN, int EPI>
 static cudaError_t launch_t(const CUtensorMap& tmA_in, const CUtensorMap& tmB_in, const GemmArgs& a,
                             cudaStream_t st) {
@@ -1496,7 +1474,6 @@ static cudaError_t launch_t(const CUtensorMap& tmA_in, const CUtensorMap& tmB_in
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, ks);
   const int num_kb = (a.K + BK - 1) / BK, kb_per = (num_kb + ks - 1) / ks;
   GemmArgs b = a;
-  b.bpre = gemm_bpre();
   b.npsync = gemm_npsync();
   CUtensorMap tmA = tmA_in, tmB = tmB_in;
   b.a_box = 0;
@@ -1641,7 +1618,6 @@ static cudaError_t launch_np(const CUtensorMap& tmA, const CUtensorMap& tmB, con
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   GemmArgs b = a;
-  b.bpre = gemm_bpre();
   b.npsync = gemm_npsync();
   return cudaLaunchKernelEx(&cfg, k_gemm_i8<BN, EPI>, tmA, tmB, b);
 }

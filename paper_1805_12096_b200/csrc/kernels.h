@@ -80,7 +80,6 @@ struct GemmArgs {
                                // -1 off, 0 the library default (env MNMT_PERS2)
   int a_box;                   // (launch-internal) k_gemm_i8: A loaded as one a_box-row box (0: 2 x 64)
   int b_box;                   // (launch-internal) k_gemm_i8: B loaded as one b_box-row box (0: 64-row boxes)
-  int bpre;                    // (launch-internal) k_gemm_i8: weight stages requested before the PDL wait
   int npsync;                  // (launch-internal) k_gemm_i8: CTA barrier before the PDL wait
   int ring_cap;                // (launch-internal) TMA ring depth cap of a split-K launch
   int split_k;                 // 0 / 1: no split-K; -1: the K / row-bound rule; 2, 4, 8: forced
