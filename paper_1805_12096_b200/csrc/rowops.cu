@@ -220,29 +220,55 @@ __global__ void __launch_bounds__(AT_WARPS_MAX * 32) k_attn_tma(const __grid_con
     tma_prefetch_desc(&tm);
   }
   __syncwarp();
-  pdl_wait();
-  pdl_trigger_early();
+  // Source attention (and the op-level ENC mode) reads only data written before the previous
+  // kernel started: the source K / V cache (encoder), the live-row metadata and count (k_finish of
+  // the previous step).  Its metadata loads and the first K tile's copy are issued BEFORE the PDL
+  // wait, overlapping the previous kernel (the query projection); only the query needs the wait.
+  // Self-attention appends this step's k, v (from the previous kernel) first, so it waits.
+  const bool pre = a.mode != ATTN_SELF;
   const int64_t gw = (int64_t)blockIdx.x * nw + wi;
   const int r = (int)(gw / a.H), h = (int)(gw - (int64_t)r * a.H);
-  if (r >= a.n) return;
-  const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
-  int start, len;
-  if (a.mode == ATTN_ENC) {   // op level: row r's own span
-    start = a.kv_start[r];
-    len = a.kv_len[r];
-  } else if (a.mode == ATTN_SELF) {   // cache rows of positions 1..t of this row's slot
-    start = a.live[r] * a.t_cap;
-    len = a.ctrl[1];
-  } else if (a.live_start) {
-    start = a.live_start[r];
-    len = a.live_len[r];
-  } else {
-    const int orig = a.live[r];
-    start = a.kv_start[orig];
-    len = a.kv_len[orig];
+  int n_live = 0, start = 0, len = 0;
+  auto meta = [&]() {
+    n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
+    if (a.mode == ATTN_ENC) {   // op level: row r's own span
+      start = a.kv_start[r];
+      len = a.kv_len[r];
+    } else if (a.mode == ATTN_SELF) {   // cache rows of positions 1..t of this row's slot
+      start = a.live[r] * a.t_cap;
+      len = a.ctrl[1];
+    } else if (a.live_start) {
+      start = a.live_start[r];
+      len = a.live_len[r];
+    } else {
+      const int orig = a.live[r];
+      start = a.kv_start[orig];
+      len = a.kv_len[orig];
+    }
+  };
+  const int kc = a.k_off + h * DH, vc = a.v_off + h * DH;
+  // chunk c0 (positions c0 .. c0 + 31 of the span): only the 8-row boxes holding positions < len
+  auto load = [&](uint64_t* b, uint8_t* dst, int col, int c0) {
+    const int row0 = (int)(a.kv_row0 + start);
+    const int nb = min(4, (len - c0 + 7) >> 3);
+    mbar_arrive_expect_tx(b, HB * nb * AT_BOX);
+    for (int hb = 0; hb < HB; ++hb)
+      for (int x = 0; x < nb; ++x)
+        tma_load_2d(dst + hb * AT_TILE + x * AT_BOX, &tm, b, col + 32 * hb, row0 + c0 + 8 * x);
+  };
+  if (pre && r < a.n) {
+    meta();
+    if (lane == 0 && r < n_live && len > 0) {
+      load(&bar[0], kt, kc, 0);
+      if constexpr (!SHARE) load(&bar[1], vt, vc, 0);
+    }
   }
+  pdl_wait();
+  pdl_trigger_early();
+  if (r >= a.n) return;
+  if (!pre) meta();
   if (r >= n_live) return;
-  if (a.mode == ATTN_SELF) {
+  if (!pre) {
     // append this step's k, v (head slice, qkv columns [d, 2d) / [2d, 3d)) at position t, then
     // order the generic-proxy stores before the tensor copies that read them
     const float* qk = a.q + (int64_t)r * a.ldq + h * DH;
@@ -253,20 +279,10 @@ __global__ void __launch_bounds__(AT_WARPS_MAX * 32) k_attn_tma(const __grid_con
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");
     __syncwarp();
-  }
-  const int row0 = (int)(a.kv_row0 + start);
-  const int kc = a.k_off + h * DH, vc = a.v_off + h * DH;
-  // chunk c0 (positions c0 .. c0 + 31 of the span): only the 8-row boxes holding positions < len
-  auto load = [&](uint64_t* b, uint8_t* dst, int col, int c0) {
-    const int nb = min(4, (len - c0 + 7) >> 3);
-    mbar_arrive_expect_tx(b, HB * nb * AT_BOX);
-    for (int hb = 0; hb < HB; ++hb)
-      for (int x = 0; x < nb; ++x)
-        tma_load_2d(dst + hb * AT_TILE + x * AT_BOX, &tm, b, col + 32 * hb, row0 + c0 + 8 * x);
-  };
-  if (lane == 0 && len > 0) {
-    load(&bar[0], kt, kc, 0);
-    if constexpr (!SHARE) load(&bar[1], vt, vc, 0);
+    if (lane == 0 && len > 0) {
+      load(&bar[0], kt, kc, 0);
+      if constexpr (!SHARE) load(&bar[1], vt, vc, 0);
+    }
   }
   const float* q = a.q + (int64_t)r * a.ldq + h * DH;
   // the query staged in shared memory while the tiles are in flight (the dot loop then reads
@@ -372,25 +388,45 @@ __global__ void __launch_bounds__(NS * 32) k_attn_split_tma(const __grid_constan
     tma_prefetch_desc(&tm);
   }
   __syncwarp();
+  // source mode: metadata and the warp's first K tile before the PDL wait (written before the
+  // previous kernel started, as in k_attn_tma); self mode appends k, v after the wait first
+  const bool pre = a.mode != ATTN_SELF;
+  const int r = (int)(blockIdx.x / a.H), h = (int)(blockIdx.x - (int64_t)r * a.H);
+  int n_live = 0, start = 0, len = 0;
+  auto meta = [&]() {
+    n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
+    if (a.mode == ATTN_SELF) {
+      start = a.live[r] * a.t_cap;
+      len = a.ctrl[1];
+    } else if (a.live_start) {
+      start = a.live_start[r];
+      len = a.live_len[r];
+    } else {
+      const int orig = a.live[r];
+      start = a.kv_start[orig];
+      len = a.kv_len[orig];
+    }
+  };
+  const int kc = a.k_off + h * DH, vc = a.v_off + h * DH;
+  // chunk c0 (positions c0 .. c0 + 31 of the span): only the 8-row boxes holding positions < len
+  auto load = [&](uint64_t* b, uint8_t* dst, int col, int c0) {
+    const int row0 = (int)(a.kv_row0 + start);
+    const int nb = min(4, (len - c0 + 7) >> 3);
+    mbar_arrive_expect_tx(b, HB * nb * AT_BOX);
+    for (int hb = 0; hb < HB; ++hb)
+      for (int x = 0; x < nb; ++x)
+        tma_load_2d(dst + hb * AT_TILE + x * AT_BOX, &tm, b, col + 32 * hb, row0 + c0 + 8 * x);
+  };
+  if (pre) {
+    meta();
+    if (lane == 0 && r < n_live && w * 32 < len) load(&bar[0], kt, kc, w * 32);
+  }
   pdl_wait();
   pdl_trigger_early();
-  const int r = (int)(blockIdx.x / a.H), h = (int)(blockIdx.x - (int64_t)r * a.H);
-  const int n_live = a.n_dyn ? min(a.n, *a.n_dyn) : a.n;
+  if (!pre) meta();
   if (r >= n_live) return;   // uniform over the CTA
-  int start, len;
-  if (a.mode == ATTN_SELF) {
-    start = a.live[r] * a.t_cap;
-    len = a.ctrl[1];
-  } else if (a.live_start) {
-    start = a.live_start[r];
-    len = a.live_len[r];
-  } else {
-    const int orig = a.live[r];
-    start = a.kv_start[orig];
-    len = a.kv_len[orig];
-  }
   const float* q = a.q + (int64_t)r * a.ldq + h * DH;
-  if (a.mode == ATTN_SELF) {
+  if (!pre) {
     if (w == 0) {
       float* dst = a.kv_w + (int64_t)(start + len - 1) * a.ldkv + h * DH;
       for (int c = lane; c < DH; c += 32) {
@@ -400,18 +436,8 @@ __global__ void __launch_bounds__(NS * 32) k_attn_split_tma(const __grid_constan
       asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     __syncthreads();
+    if (lane == 0 && w * 32 < len) load(&bar[0], kt, kc, w * 32);
   }
-  const int row0 = (int)(a.kv_row0 + start);
-  const int kc = a.k_off + h * DH, vc = a.v_off + h * DH;
-  // chunk c0 (positions c0 .. c0 + 31 of the span): only the 8-row boxes holding positions < len
-  auto load = [&](uint64_t* b, uint8_t* dst, int col, int c0) {
-    const int nb = min(4, (len - c0 + 7) >> 3);
-    mbar_arrive_expect_tx(b, HB * nb * AT_BOX);
-    for (int hb = 0; hb < HB; ++hb)
-      for (int x = 0; x < nb; ++x)
-        tma_load_2d(dst + hb * AT_TILE + x * AT_BOX, &tm, b, col + 32 * hb, row0 + c0 + 8 * x);
-  };
-  if (lane == 0 && w * 32 < len) load(&bar[0], kt, kc, w * 32);
   // the query staged in shared memory while the tiles are in flight (broadcast reads)
   float4* qv = reinterpret_cast<float4*>(bar + 2);
   if (lane < DH / 4) qv[lane] = *reinterpret_cast<const float4*>(q + 4 * lane);
