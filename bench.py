@@ -51,7 +51,7 @@ DEFAULT_WORKLOAD = "big-newstest-8192w"   # BASELINE.json configs[3]: the metric
 # lane's SM partition pays off for the smaller students and costs the big one (its bulk lanes
 # need every SM).
 # smallm / smallm_kmax: the small-M (IDP4A, <= 32 live rows) GEMM path's row bound and deepest K
-# per workload, from the A/B in profiles/r1_ab_smallm.txt (small-aan: +2 % with FFN2's K = 2048
+# per workload, from the A/B in profiles/r1_ab_smallm_*.txt (small-aan: +2 % with FFN2's K = 2048
 # included; the others neutral or slower, so off; big with K <= 1024 and the <= 1 MB d x d maps:
 # 91.5 -> 90.8 ms per job in round 2 (profiles/r2_sweep_big_options.txt)).
 # sab: row bound of the swap-AB tcgen05 GEMM (weights as the 128-row MMA operand, live rows as
