@@ -247,36 +247,26 @@ __global__ void __launch_bounds__(AT_WARPS_MAX * 32) k_attn_tma(const __grid_con
     }
   };
   const int kc = a.k_off + h * DH, vc = a.v_off + h * DH;
-  // chunk c0 (positions c0 .. c0 + 31 of the span): only the 8-row boxes holding positions < n
-  // (n = len by default)
-  auto load = [&](uint64_t* b, uint8_t* dst, int col, int c0, int n = -1) {
+  // chunk c0 (positions c0 .. c0 + 31 of the span): only the 8-row boxes holding positions < len
+  auto load = [&](uint64_t* b, uint8_t* dst, int col, int c0) {
     const int row0 = (int)(a.kv_row0 + start);
-    const int nb = min(4, ((n < 0 ? len : n) - c0 + 7) >> 3);
+    const int nb = min(4, (len - c0 + 7) >> 3);
     mbar_arrive_expect_tx(b, HB * nb * AT_BOX);
     for (int hb = 0; hb < HB; ++hb)
       for (int x = 0; x < nb; ++x)
         tma_load_2d(dst + hb * AT_TILE + x * AT_BOX, &tm, b, col + 32 * hb, row0 + c0 + 8 * x);
   };
-  // Self-attention (SHARE): positions 0 .. t-2 were written by earlier steps, only position t-1
-  // is appended by this kernel after the wait -- chunk 0's earlier positions are requested before
-  // the wait too, and the new position's key is read from the query projection's output.
-  const bool self_pre = SHARE && !pre && a.self_pre;
-  int old0 = 0;   // positions of chunk 0 in the pre-wait copy (self_pre)
   if (pre && r < a.n) {
     meta();
     if (lane == 0 && r < n_live && len > 0) {
       load(&bar[0], kt, kc, 0);
       if constexpr (!SHARE) load(&bar[1], vt, vc, 0);
     }
-  } else if (self_pre && r < a.n) {
-    meta();
-    old0 = min(len - 1, 32);
-    if (lane == 0 && r < n_live && old0 > 0) load(&bar[0], kt, kc, 0, old0);
   }
   pdl_wait();
   pdl_trigger_early();
   if (r >= a.n) return;
-  if (!pre && !self_pre) meta();
+  if (!pre) meta();
   if (r >= n_live) return;
   if (!pre) {
     // append this step's k, v (head slice, qkv columns [d, 2d) / [2d, 3d)) at position t, then
@@ -289,13 +279,9 @@ __global__ void __launch_bounds__(AT_WARPS_MAX * 32) k_attn_tma(const __grid_con
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");
     __syncwarp();
-    if (!self_pre) {
-      if (lane == 0 && len > 0) {
-        load(&bar[0], kt, kc, 0);
-        if constexpr (!SHARE) load(&bar[1], vt, vc, 0);
-      }
-    } else if (lane == 0 && old0 == 0 && len > 0) {
-      mbar_arrive_expect_tx(&bar[0], 0);   // chunk 0 holds only the new position: no copy
+    if (lane == 0 && len > 0) {
+      load(&bar[0], kt, kc, 0);
+      if constexpr (!SHARE) load(&bar[1], vt, vc, 0);
     }
   }
   const float* q = a.q + (int64_t)r * a.ldq + h * DH;
@@ -314,13 +300,9 @@ __global__ void __launch_bounds__(AT_WARPS_MAX * 32) k_attn_tma(const __grid_con
     const int j = c0 + lane;
     if (j < len) {
       T dot = 0;
-      // the new position of a pre-wait chunk 0 (self_pre): its key from the qkv row itself
-      const float* knew = (self_pre && c0 == 0 && j == len - 1)
-                              ? a.q + (int64_t)r * a.ldq + a.d + h * DH : nullptr;
 #pragma unroll
       for (int c = 0; c < DH; c += 4) {
-        const float4 k4 = knew ? *reinterpret_cast<const float4*>(knew + c)
-                               : *reinterpret_cast<const float4*>(kt + (c >> 5) * AT_TILE + at_swz(lane, c & 31));
+        const float4 k4 = *reinterpret_cast<const float4*>(kt + (c >> 5) * AT_TILE + at_swz(lane, c & 31));
         const float4 q4 = qv[c >> 2];
         dot = at_fma((T)q4.x, (T)k4.x, dot);
         dot = at_fma((T)q4.y, (T)k4.y, dot);
@@ -1255,11 +1237,6 @@ cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
       const int v = e ? atoi(e) : AT_WARPS;
       return (v == 2 || v == 8) ? v : AT_WARPS;
     }();
-    static const int self_pre = [] {   // env MNMT_ATTN_SELF_PRE=0: self-attention waits first (A/B)
-      const char* e = getenv("MNMT_ATTN_SELF_PRE");
-      return e ? atoi(e) : 1;
-    }();
-    b.self_pre = self_pre;
     const dim3 grid((unsigned)((warps + atw - 1) / atw)), block(atw * 32);
     const size_t smem = attn_tma_smem(b.dh, b.span, share, atw);
     static const bool f32 = [] {   // env MNMT_ATTN_F32=1: the fp32 variant everywhere (A/B)

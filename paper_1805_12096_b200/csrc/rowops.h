@@ -85,7 +85,6 @@ struct AttnArgs {
   int64_t kv_row0;
   int tma_self;             // self mode: 0 generic kernels, 1 TMA split kernel for long decodes at
                             // <= 128 rows, 2 also the one-warp TMA kernel (measured per workload)
-  int self_pre;             // (launch-internal) self mode: chunk 0's earlier positions before the PDL wait
   int f32;                  // one-warp TMA kernel in fp32 arithmetic (model option attn_f32; departs
                             // from R20: ids exact or near-tie-explained, intermediates not within 1e-4)
 };
