@@ -1316,6 +1316,10 @@ int gemm_pick_bn(int M, int N, int sms) {
   const int mt = (M + BM - 1) / BM;
   if ((long)mt * ((N + 255) / 256) > 2L * S) return 256;   // persistent, widest tile
   if (((N + 255) / 256) * mt >= S) return 256;
+  // few rows, very wide N (the output layer at <= 128 rows): 128-wide tiles would need two waves,
+  // 256-wide ones fit one (output GEMM + argmax at 1-64 rows, d 1024: 11.1 -> 8.2 us; d 256:
+  // 7.2 -> 5.3 us; profiles/r2_out_gemm_tiles.txt)
+  if (M <= 128 && (long)((N + 127) / 128) * mt > S) return 256;
   if (((N + 127) / 128) * mt >= S / 2) return 128;
   return 64;
 }
